@@ -1,0 +1,715 @@
+/* oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Built with: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -lm
+ * so that every expression is evaluated exactly as written (no FMA
+ * contraction, no reassociation).  fma() is used only where DESIGN.md §3
+ * writes "fma".
+ *
+ * Section map (DESIGN.md §3 = the written definitions):
+ *   §3.1 correctly rounded sums ........ or_fsum / or_dot / or_sumabs
+ *   §3.2 7-point operator ................ or_spmv
+ *   §3.3 momentum row .................... or_assemble_mom     (Eq. 2)
+ *   §3.4 pressure-correction row ......... or_assemble_pp      (Eq. 1)
+ *   §3.5 scalar row ...................... or_assemble_scalar
+ *   §3.6 BiCGSTAB ........................ or_bicgstab
+ *   §3.7 correction ...................... or_correct
+ *   §3.8 SIMPLE outer iteration .......... or_simple_iter
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ §3.1 */
+/* Exact summation with Shewchuk's non-overlapping partials (the algorithm of
+ * Python's math.fsum): the returned value is the exact sum rounded once to
+ * nearest-even.  Inputs must be finite and the partial sums must not
+ * overflow (always true for the fields of this problem). */
+typedef struct { double p[256]; int n; } xsum;
+
+static void xs_init(xsum *s) { s->n = 0; }
+
+static void xs_add(xsum *s, double x)
+{
+    int i = 0;
+    for (int j = 0; j < s->n; j++) {
+        double y = s->p[j];
+        if (fabs(x) < fabs(y)) { double t = x; x = y; y = t; }
+        double hi = x + y;
+        double lo = y - (hi - x);
+        if (lo != 0.0) s->p[i++] = lo;
+        x = hi;
+    }
+    s->n = i;
+    s->p[s->n++] = x;
+}
+
+static double xs_round(const xsum *s)
+{
+    int n = s->n;
+    double hi = 0.0, lo = 0.0;
+    if (n > 0) {
+        hi = s->p[--n];
+        while (n > 0) {
+            double x = hi, y = s->p[--n];
+            hi = x + y;
+            double yr = hi - x;
+            lo = y - yr;
+            if (lo != 0.0) break;
+        }
+        /* round-half-even correction when the remainder is exactly half an ulp */
+        if (n > 0 && ((lo < 0.0 && s->p[n - 1] < 0.0) || (lo > 0.0 && s->p[n - 1] > 0.0))) {
+            double y = lo * 2.0;
+            double x = hi + y;
+            double yr = x - hi;
+            if (y == yr) hi = x;
+        }
+    }
+    return hi + 0.0; /* an exact zero is +0 */
+}
+
+double or_fsum(long n, const double *x)
+{
+    xsum s; xs_init(&s);
+    for (long i = 0; i < n; i++) xs_add(&s, x[i]);
+    return xs_round(&s);
+}
+
+/* <a,b> = exact sum of the products a_i b_i, rounded once.  Each product is
+ * split exactly as hi + lo with hi = fl(a b), lo = fma(a, b, -hi). */
+double or_dot(long n, const double *a, const double *b)
+{
+    xsum s; xs_init(&s);
+    for (long i = 0; i < n; i++) {
+        double hi = a[i] * b[i];
+        double lo = fma(a[i], b[i], -hi);
+        xs_add(&s, hi);
+        xs_add(&s, lo);
+    }
+    return xs_round(&s);
+}
+
+double or_sumabs(long n, const double *x)
+{
+    xsum s; xs_init(&s);
+    for (long i = 0; i < n; i++) xs_add(&s, fabs(x[i]));
+    return xs_round(&s);
+}
+
+/* ------------------------------------------------------------ helpers */
+static long idx(const og_grid *g, int i, int j, int k)
+{
+    return (long)i + (long)g->nx * ((long)j + (long)g->ny * (long)k);
+}
+static int ext(const og_grid *g, int a) { return a == 0 ? g->nx : (a == 1 ? g->ny : g->nz); }
+static double spacing(const og_grid *g, int a) { return a == 0 ? g->dx : (a == 1 ? g->dy : g->dz); }
+static double area(const og_grid *g, int a)
+{
+    return a == 0 ? g->dy * g->dz : (a == 1 ? g->dx * g->dz : g->dx * g->dy);
+}
+static double volume(const og_grid *g) { return (g->dx * g->dy) * g->dz; }
+static int inside(const og_grid *g, const int q[3])
+{
+    return q[0] >= 0 && q[0] < g->nx && q[1] >= 0 && q[1] < g->ny && q[2] >= 0 && q[2] < g->nz;
+}
+static long at(const og_grid *g, const int q[3]) { return idx(g, q[0], q[1], q[2]); }
+static double maxp(double f) { return f > 0.0 ? f : 0.0; }
+static long ncell(const og_grid *g) { return (long)g->nx * g->ny * g->nz; }
+
+static int grid_ok(const og_grid *g)
+{
+    if (g->nx < 2 || g->ny < 2 || g->nz < 2) return 0;
+    if (!(g->dx > 0 && g->dy > 0 && g->dz > 0)) return 0;
+    if (g->bc_zlo != OG_WALL && g->bc_zlo != OG_INLET) return 0;
+    if (g->bc_zhi != OG_WALL && g->bc_zhi != OG_OUTLET && g->bc_zhi != OG_DIRICHLET_TEST) return 0;
+    return 1;
+}
+
+/* ------------------------------------------------------------------ §3.2 */
+/* y = A x, row by row: y = aP x_P, then y = fma(-a_nb, x_nb, y) for nb in
+ * W, E, S, N, B, T.  Out-of-domain neighbours contribute a_nb = 0, x_nb = 0.
+ * Symmetric (p') storage: a_W(n) = c_x[n - 1], a_E(n) = c_x[n], etc. */
+void or_spmv(const og_grid *g, const og_eqsys *A, const double *x, double *y)
+{
+    const int sym = (A->aW == NULL);
+    const long sx = 1, sy = g->nx, sz = (long)g->nx * g->ny;
+    for (int k = 0; k < g->nz; k++)
+        for (int j = 0; j < g->ny; j++)
+            for (int i = 0; i < g->nx; i++) {
+                long n = idx(g, i, j, k);
+                double aW, aE, aS, aN, aB, aT;
+                if (sym) {
+                    aW = i > 0 ? A->aE[n - sx] : 0.0;
+                    aE = A->aE[n];
+                    aS = j > 0 ? A->aN[n - sy] : 0.0;
+                    aN = A->aN[n];
+                    aB = k > 0 ? A->aT[n - sz] : 0.0;
+                    aT = A->aT[n];
+                } else {
+                    aW = A->aW[n]; aE = A->aE[n]; aS = A->aS[n];
+                    aN = A->aN[n]; aB = A->aB[n]; aT = A->aT[n];
+                }
+                double xW = i > 0 ? x[n - sx] : 0.0;
+                double xE = i < g->nx - 1 ? x[n + sx] : 0.0;
+                double xS = j > 0 ? x[n - sy] : 0.0;
+                double xN = j < g->ny - 1 ? x[n + sy] : 0.0;
+                double xB = k > 0 ? x[n - sz] : 0.0;
+                double xT = k < g->nz - 1 ? x[n + sz] : 0.0;
+                double r = A->aP[n] * x[n];
+                r = fma(-aW, xW, r);
+                r = fma(-aE, xE, r);
+                r = fma(-aS, xS, r);
+                r = fma(-aN, xN, r);
+                r = fma(-aB, xB, r);
+                r = fma(-aT, xT, r);
+                y[n] = r;
+            }
+}
+
+/* ------------------------------------------------------------------ §3.3 */
+/* Momentum row for staggered component c (0=u,1=v,2=w) at cell P: the face
+ * between P and E = P + e_c.  Convection first-order upwind in
+ * non-conservative form, diffusion mu*eps (Q12), implicit
+ * drag beta V plus explicit S V (Q11), pressure -eps grad p (Eq. 2 gauge),
+ * gravity eps rho g, implicit under-relaxation.
+ * Boundary rules B1 (known value at distance h), B2 (known value at h/2,
+ * mirror ghost), B3 (zero gradient, dropped) as in DESIGN.md §3.3. */
+
+enum { ROW_INTERIOR = 0, ROW_IDENTITY = 1, ROW_OUTLET = 2 };
+
+static int mom_row_type(const og_grid *g, int c, const int P[3])
+{
+    if (P[c] < ext(g, c) - 1) return ROW_INTERIOR;
+    if (c == 2 && g->bc_zhi == OG_OUTLET) return ROW_OUTLET;
+    return ROW_IDENTITY;
+}
+
+static const double *comp_field(const og_state *st, int a)
+{
+    return a == 0 ? st->u : (a == 1 ? st->v : st->w);
+}
+
+/* velocity of component c on the face Q + e_c/2 (Q may be one step outside) */
+static double vel_c(const og_grid *g, const og_state *st, int c, const int Q[3])
+{
+    if (Q[c] == -1) return (c == 2 && g->bc_zlo == OG_INLET) ? g->w_in : 0.0;
+    if (Q[c] == ext(g, c) - 1 && mom_row_type(g, c, Q) == ROW_IDENTITY) return 0.0;
+    return comp_field(st, c)[at(g, Q)];
+}
+
+/* mass flux through the +t face of cell X, the face being interior */
+static double mflux_t(const og_grid *g, const og_params *pr, const og_state *st, int t, const int X[3])
+{
+    int Xt[3] = {X[0], X[1], X[2]};
+    Xt[t] += 1;
+    double ef = 0.5 * (st->eps[at(g, X)] + st->eps[at(g, Xt)]);
+    return ((pr->rho * ef) * area(g, t)) * comp_field(st, t)[at(g, X)];
+}
+
+int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state *st,
+                    og_eqsys *out, double resid2[2])
+{
+    if (!grid_ok(g) || c < 0 || c > 2) return OG_ERR_ARG;
+    if (g->bc_zhi == OG_DIRICHLET_TEST) return OG_ERR_ARG;
+    const double V = volume(g);
+    const double rVdt = (pr->rho * V) / pr->dt;
+    const double *um = comp_field(st, c);
+    const double *uold = c == 0 ? st->u_old : (c == 1 ? st->v_old : st->w_old);
+    const double *S = c == 0 ? st->sbeta_u : (c == 1 ? st->sbeta_v : st->sbeta_w);
+    double Dc[3];
+    for (int a = 0; a < 3; a++) Dc[a] = (pr->mu * area(g, a)) / spacing(g, a);
+    const long N = ncell(g);
+    double *rnum = malloc(sizeof(double) * N), *rden = malloc(sizeof(double) * N);
+    long nres = 0;
+    int status = OG_OK;
+
+    for (int k = 0; k < g->nz; k++)
+        for (int j = 0; j < g->ny; j++)
+            for (int i = 0; i < g->nx; i++) {
+                const int P[3] = {i, j, k};
+                const long n = at(g, P);
+                const int type = mom_row_type(g, c, P);
+                if (type == ROW_IDENTITY) {
+                    out->aP[n] = 1.0;
+                    out->aW[n] = out->aE[n] = out->aS[n] = out->aN[n] = out->aB[n] = out->aT[n] = 0.0;
+                    out->b[n] = 0.0;
+                    out->d[n] = 0.0;
+                    continue;
+                }
+                /* E: the other cell of the face, clamped onto P at the outlet row */
+                int E[3] = {i, j, k};
+                if (type == ROW_INTERIOR) E[c] += 1;
+                const long nE = at(g, E);
+
+                /* six sides in geometric order x-,x+,y-,y+,z-,z+ */
+                double a_side[6], phi_b[6];
+                int kept[6], inP[6];
+                for (int s6 = 0; s6 < 6; s6++) { a_side[s6] = 0.0; phi_b[s6] = 0.0; kept[s6] = 0; inP[s6] = 0; }
+
+                for (int t = 0; t < 3; t++) {
+                    if (t == c) {
+                        /* main axis, minus side: face at the centre of P */
+                        int Qm[3] = {i, j, k}; Qm[c] -= 1;
+                        double Fm = ((pr->rho * st->eps[n]) * area(g, c)) *
+                                    (0.5 * (vel_c(g, st, c, Qm) + vel_c(g, st, c, P)));
+                        double Dm = Dc[c] * st->eps[n];
+                        a_side[2 * c] = Dm + maxp(Fm);
+                        inP[2 * c] = 1;
+                        if (P[c] >= 1) kept[2 * c] = 1;
+                        else phi_b[2 * c] = vel_c(g, st, c, Qm); /* B1 */
+                        /* plus side: face at the centre of E */
+                        if (type == ROW_OUTLET) {
+                            a_side[2 * c + 1] = 0.0; /* B3 */
+                        } else {
+                            double Fp = ((pr->rho * st->eps[nE]) * area(g, c)) *
+                                        (0.5 * (vel_c(g, st, c, P) + vel_c(g, st, c, E)));
+                            double Dp = Dc[c] * st->eps[nE];
+                            a_side[2 * c + 1] = Dp + maxp(-Fp);
+                            inP[2 * c + 1] = 1;
+                            if (mom_row_type(g, c, E) == ROW_IDENTITY) phi_b[2 * c + 1] = 0.0; /* B1 */
+                            else kept[2 * c + 1] = 1;
+                        }
+                        continue;
+                    }
+                    for (int s = -1; s <= 1; s += 2) {
+                        const int side = 2 * t + (s > 0);
+                        int Pt[3] = {i, j, k}; Pt[t] += s;
+                        int Et[3] = {E[0], E[1], E[2]}; Et[t] += s;
+                        if (inside(g, Pt)) {
+                            const int *Q = s > 0 ? P : Pt;
+                            const int *R = s > 0 ? E : Et;
+                            double F = 0.5 * (mflux_t(g, pr, st, t, Q) + mflux_t(g, pr, st, t, R));
+                            double e4 = 0.25 * (((st->eps[n] + st->eps[nE]) + st->eps[at(g, Pt)]) +
+                                                st->eps[at(g, Et)]);
+                            double D = Dc[t] * e4;
+                            a_side[side] = D + maxp(s > 0 ? -F : F);
+                            inP[side] = 1;
+                            kept[side] = 1;
+                        } else {
+                            int bc = OG_WALL;
+                            if (t == 2) bc = s < 0 ? g->bc_zlo : g->bc_zhi;
+                            if (bc == OG_OUTLET) { a_side[side] = 0.0; continue; } /* B3 */
+                            double F = 0.0;
+                            if (bc == OG_INLET)
+                                F = 0.5 * (((pr->rho * st->eps[n]) * area(g, 2)) * g->w_in +
+                                           ((pr->rho * st->eps[nE]) * area(g, 2)) * g->w_in);
+                            double e2 = 0.5 * (st->eps[n] + st->eps[nE]);
+                            double D = Dc[t] * e2;
+                            a_side[side] = 2.0 * D + maxp(s > 0 ? -F : F); /* B2, phi_b = 0 */
+                            inP[side] = 1;
+                            phi_b[side] = 0.0;
+                        }
+                    }
+                }
+
+                double sum = ((((a_side[0] + a_side[1]) + a_side[2]) + a_side[3]) + a_side[4]) + a_side[5];
+                double bcb = 0.0;
+                for (int s6 = 0; s6 < 6; s6++)
+                    if (inP[s6] && !kept[s6]) bcb = bcb + a_side[s6] * phi_b[s6];
+                const double ef = 0.5 * (st->eps[n] + st->eps[nE]);
+                const double e0f = 0.5 * (st->eps_old[n] + st->eps_old[nE]);
+                const double bf = 0.5 * (st->beta[n] + st->beta[nE]);
+                const double Sf = 0.5 * (S[n] + S[nE]);
+                const double pE = type == ROW_OUTLET ? 0.0 : st->p[nE];
+                const double a0 = rVdt * e0f;
+                const double aP = (sum + a0) + bf * V;
+                const double b = ((((a0 * uold[n]) + (ef * area(g, c)) * (st->p[n] - pE)) +
+                                   ((pr->rho * ef) * pr->g[c]) * V) + Sf * V) + bcb;
+                const double aPr = aP / pr->urf_mom;
+                const double bR = b + (aPr - aP) * um[n];
+                const double d = (ef * area(g, c)) / aPr;
+
+                double st6[6];
+                for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? a_side[s6] : 0.0;
+                out->aW[n] = st6[0]; out->aE[n] = st6[1];
+                out->aS[n] = st6[2]; out->aN[n] = st6[3];
+                out->aB[n] = st6[4]; out->aT[n] = st6[5];
+                out->aP[n] = aPr;
+                out->b[n] = bR;
+                out->d[n] = d;
+                if (!isfinite(aPr) || !isfinite(bR) || !isfinite(d)) status = OG_ERR_NONFINITE;
+                else if (aPr == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+
+                /* snapshot residual, un-relaxed row */
+                double res = b - aP * um[n];
+                for (int s6 = 0; s6 < 6; s6++) {
+                    int Q[3] = {i, j, k};
+                    Q[s6 / 2] += (s6 & 1) ? 1 : -1;
+                    double unb = inside(g, Q) ? um[at(g, Q)] : 0.0;
+                    res = res + st6[s6] * unb;
+                }
+                rnum[nres] = fabs(res);
+                rden[nres] = fabs(aP * um[n]);
+                nres++;
+            }
+    if (resid2) {
+        resid2[0] = or_sumabs(nres, rnum);
+        resid2[1] = or_sumabs(nres, rden);
+    }
+    free(rnum); free(rden);
+    return status;
+}
+
+/* ------------------------------------------------------------------ §3.4 */
+/* p' row (SIMPLE): face coefficient c_f = rho eps_f A_f d_f,
+ * one stored value per face (A symmetric), a_P = sum of the six faces; the
+ * outlet face stays in a_P with ghost p' = 0 (Q13).  b = mass imbalance of
+ * the starred field minus the transient term (Eq. 1 discretised). */
+
+static double face_eps(const og_grid *g, const og_state *st, int a, const int X[3])
+{
+    int Y[3] = {X[0], X[1], X[2]}; Y[a] += 1;
+    return 0.5 * (st->eps[at(g, X)] + st->eps[at(g, Y)]);
+}
+
+/* coefficient-like quantity rho eps_f A_f q on the +a face of X */
+static double plus_face(const og_grid *g, const og_params *pr, const og_state *st, int a,
+                        const int X[3], const double *q)
+{
+    if (X[a] <= ext(g, a) - 2)
+        return ((pr->rho * face_eps(g, st, a, X)) * area(g, a)) * q[at(g, X)];
+    if (a == 2 && g->bc_zhi == OG_OUTLET)
+        return ((pr->rho * st->eps[at(g, X)]) * area(g, 2)) * q[at(g, X)];
+    return 0.0;
+}
+
+int or_assemble_pp(const og_grid *g, const og_params *pr, const og_state *st,
+                   const double *us, const double *vs, const double *ws,
+                   const double *dxv, const double *dyv, const double *dzv,
+                   og_eqsys *out, double *cont)
+{
+    if (!grid_ok(g) || g->bc_zhi == OG_DIRICHLET_TEST) return OG_ERR_ARG;
+    const double V = volume(g);
+    const double rVdt = (pr->rho * V) / pr->dt;
+    const double *vel[3] = {us, vs, ws};
+    const double *dd[3] = {dxv, dyv, dzv};
+    double *cf[3] = {out->aE, out->aN, out->aT};
+    int status = OG_OK;
+    for (int k = 0; k < g->nz; k++)
+        for (int j = 0; j < g->ny; j++)
+            for (int i = 0; i < g->nx; i++) {
+                const int P[3] = {i, j, k};
+                const long n = at(g, P);
+                double cm[3], cpl[3], mm[3], mp[3];
+                for (int a = 0; a < 3; a++) {
+                    cpl[a] = plus_face(g, pr, st, a, P, dd[a]);
+                    mp[a] = plus_face(g, pr, st, a, P, vel[a]);
+                    if (P[a] >= 1) {
+                        int Q[3] = {i, j, k}; Q[a] -= 1;
+                        cm[a] = plus_face(g, pr, st, a, Q, dd[a]);
+                        mm[a] = plus_face(g, pr, st, a, Q, vel[a]);
+                    } else {
+                        cm[a] = 0.0;
+                        mm[a] = (a == 2 && g->bc_zlo == OG_INLET)
+                                    ? ((pr->rho * st->eps[n]) * area(g, 2)) * g->w_in : 0.0;
+                    }
+                }
+                double aP = ((((cm[0] + cpl[0]) + cm[1]) + cpl[1]) + cm[2]) + cpl[2];
+                double b = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) -
+                           rVdt * (st->eps[n] - st->eps_old[n]);
+                out->aP[n] = aP;
+                for (int a = 0; a < 3; a++) cf[a][n] = cpl[a];
+                out->b[n] = b;
+                if (!isfinite(aP) || !isfinite(b)) status = OG_ERR_NONFINITE;
+                else if (aP == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+            }
+    if (cont) *cont = or_sumabs(ncell(g), out->b);
+    return status;
+}
+
+/* ------------------------------------------------------------------ §3.5 */
+/* Cell-centred scalar (energy / species): FOUP convection-
+ * diffusion with transient; Dirichlet inlet (B2), zero-gradient outlet (B3),
+ * zero-flux walls; test-only Dirichlet top (B2 with phi_out). */
+int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_state *st,
+                       og_eqsys *out, double resid2[2])
+{
+    if (!grid_ok(g) || sid < 0 || sid > 3) return OG_ERR_ARG;
+    const double V = volume(g);
+    const double rVdt = (pr->rho * V) / pr->dt;
+    const double gam = pr->gamma_phi[sid];
+    const double *phim = st->phi[sid], *phi0 = st->phi_old[sid];
+    const double *vel[3] = {st->u, st->v, st->w};
+    double Dc[3];
+    for (int a = 0; a < 3; a++) Dc[a] = (gam * area(g, a)) / spacing(g, a);
+    const long N = ncell(g);
+    double *rnum = malloc(sizeof(double) * N), *rden = malloc(sizeof(double) * N);
+    int status = OG_OK;
+    for (int k = 0; k < g->nz; k++)
+        for (int j = 0; j < g->ny; j++)
+            for (int i = 0; i < g->nx; i++) {
+                const int P[3] = {i, j, k};
+                const long n = at(g, P);
+                double a_side[6], phib[6];
+                int kept[6], inP[6];
+                for (int a = 0; a < 3; a++) {
+                    /* minus side */
+                    int sm = 2 * a, sp = 2 * a + 1;
+                    a_side[sm] = a_side[sp] = 0.0; phib[sm] = phib[sp] = 0.0;
+                    kept[sm] = kept[sp] = 0; inP[sm] = inP[sp] = 0;
+                    if (P[a] >= 1) {
+                        int Q[3] = {i, j, k}; Q[a] -= 1;
+                        double e = 0.5 * (st->eps[at(g, Q)] + st->eps[n]);
+                        double F = ((pr->rho * e) * area(g, a)) * vel[a][at(g, Q)];
+                        a_side[sm] = Dc[a] * e + maxp(F);
+                        kept[sm] = inP[sm] = 1;
+                    } else if (a == 2 && g->bc_zlo == OG_INLET) {
+                        double F = ((pr->rho * st->eps[n]) * area(g, 2)) * g->w_in;
+                        a_side[sm] = 2.0 * (Dc[2] * st->eps[n]) + maxp(F);
+                        inP[sm] = 1;
+                        phib[sm] = g->phi_in;
+                    }
+                    /* plus side */
+                    if (P[a] <= ext(g, a) - 2) {
+                        double e = 0.5 * (st->eps[n] + st->eps[at(g, (int[3]){i + (a == 0), j + (a == 1), k + (a == 2)})]);
+                        double F = ((pr->rho * e) * area(g, a)) * vel[a][n];
+                        a_side[sp] = Dc[a] * e + maxp(-F);
+                        kept[sp] = inP[sp] = 1;
+                    } else if (a == 2 && g->bc_zhi == OG_DIRICHLET_TEST) {
+                        double F = ((pr->rho * st->eps[n]) * area(g, 2)) * vel[2][n];
+                        a_side[sp] = 2.0 * (Dc[2] * st->eps[n]) + maxp(-F);
+                        inP[sp] = 1;
+                        phib[sp] = g->phi_out;
+                    }
+                }
+                double sum = ((((a_side[0] + a_side[1]) + a_side[2]) + a_side[3]) + a_side[4]) + a_side[5];
+                double bcb = 0.0;
+                for (int s6 = 0; s6 < 6; s6++)
+                    if (inP[s6] && !kept[s6]) bcb = bcb + a_side[s6] * phib[s6];
+                const double a0 = rVdt * st->eps_old[n];
+                const double aP = sum + a0;
+                const double b = (a0 * phi0[n]) + bcb;
+                const double aPr = aP / pr->urf_phi;
+                const double bR = b + (aPr - aP) * phim[n];
+                double st6[6];
+                for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? a_side[s6] : 0.0;
+                out->aW[n] = st6[0]; out->aE[n] = st6[1];
+                out->aS[n] = st6[2]; out->aN[n] = st6[3];
+                out->aB[n] = st6[4]; out->aT[n] = st6[5];
+                out->aP[n] = aPr;
+                out->b[n] = bR;
+                if (out->d) out->d[n] = 0.0;
+                if (!isfinite(aPr) || !isfinite(bR)) status = OG_ERR_NONFINITE;
+                else if (aPr == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+                double res = b - aP * phim[n];
+                for (int s6 = 0; s6 < 6; s6++) {
+                    int Q[3] = {i, j, k};
+                    Q[s6 / 2] += (s6 & 1) ? 1 : -1;
+                    double unb = inside(g, Q) ? phim[at(g, Q)] : 0.0;
+                    res = res + st6[s6] * unb;
+                }
+                rnum[n] = fabs(res);
+                rden[n] = fabs(aP * phim[n]);
+            }
+    if (resid2) {
+        resid2[0] = or_sumabs(N, rnum);
+        resid2[1] = or_sumabs(N, rden);
+    }
+    free(rnum); free(rden);
+    return status;
+}
+
+/* ------------------------------------------------------------------ §3.6 */
+/* Unpreconditioned BiCGSTAB (van der Vorst), "No preconditioners";
+ * SPEC.md:370-378; readings Q1-Q5, Q17. */
+int or_bicgstab(const og_grid *g, const og_eqsys *A, double *x, double tol, int maxit,
+                og_solve_info *info, double *trace)
+{
+    const long N = ncell(g);
+    double *r = calloc(N, sizeof(double)), *rh = calloc(N, sizeof(double));
+    double *p = calloc(N, sizeof(double)), *v = calloc(N, sizeof(double));
+    double *s = calloc(N, sizeof(double)), *t = calloc(N, sizeof(double));
+    double *y = calloc(N, sizeof(double));
+    int status = OG_NOT_CONVERGED, iters = 0, restarts = 0;
+    double rel = 0.0;
+
+    or_spmv(g, A, x, y);
+    for (long n = 0; n < N; n++) r[n] = A->b[n] - y[n];
+    const double bn = sqrt(or_dot(N, A->b, A->b));
+    double rr = or_dot(N, r, r);
+    double rn = sqrt(rr);
+    if (bn == 0.0) {
+        for (long n = 0; n < N; n++) x[n] = 0.0;
+        status = OG_OK; iters = 0; rel = 0.0;
+        goto done;
+    }
+    if (rn <= tol * bn) { status = OG_OK; iters = 0; rel = rn / bn; goto done; }
+
+    for (long n = 0; n < N; n++) rh[n] = r[n];
+    double rhn = rn;
+    double rho = or_dot(N, rh, r);
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    int restarted = 0;
+
+    for (int it = 1; it <= maxit; it++) {
+        double *tr = trace ? trace + 8 * (long)(it - 1) : NULL;
+        if (fabs(rho) <= (1e-14 * rhn) * rn) {
+            if (restarted) { status = OG_ERR_BREAKDOWN; iters = it - 1; goto done_rel; }
+            for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
+            rhn = rn; rho = or_dot(N, rh, r);
+            rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
+        }
+        const double beta = (rho / rho_prev) * (alpha / omega);
+        for (long n = 0; n < N; n++) p[n] = fma(beta, fma(-omega, v[n], p[n]), r[n]);
+        or_spmv(g, A, p, v);
+        const double sigma = or_dot(N, rh, v);
+        if (tr) { tr[0] = rho; tr[1] = sigma; }
+        if (sigma == 0.0) {
+            if (restarted) { status = OG_ERR_BREAKDOWN; iters = it; goto done_rel; }
+            for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
+            rhn = rn; rho = or_dot(N, rh, r);
+            rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
+            continue;
+        }
+        alpha = rho / sigma;
+        for (long n = 0; n < N; n++) s[n] = fma(-alpha, v[n], r[n]);
+        const double ss = or_dot(N, s, s);
+        if (tr) { tr[2] = alpha; tr[3] = ss; }
+        if (sqrt(ss) <= tol * bn) {
+            for (long n = 0; n < N; n++) { x[n] = fma(alpha, p[n], x[n]); r[n] = s[n]; }
+            rn = sqrt(ss);
+            status = OG_OK; iters = it; goto done_rel;
+        }
+        or_spmv(g, A, s, t);
+        const double ts = or_dot(N, t, s);
+        const double tt = or_dot(N, t, t);
+        const double om = tt == 0.0 ? 0.0 : ts / tt;
+        if (tr) { tr[4] = ts; tr[5] = tt; tr[6] = om; }
+        if (tt == 0.0 || om == 0.0) {
+            if (restarted) { status = OG_ERR_BREAKDOWN; iters = it; goto done_rel; }
+            for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
+            rhn = rn; rho = or_dot(N, rh, r);
+            rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
+            continue;
+        }
+        omega = om;
+        for (long n = 0; n < N; n++) {
+            x[n] = fma(omega, s[n], fma(alpha, p[n], x[n]));
+            r[n] = fma(-omega, t[n], s[n]);
+        }
+        rho_prev = rho;
+        rho = or_dot(N, rh, r);
+        rr = or_dot(N, r, r);
+        rn = sqrt(rr);
+        if (tr) tr[7] = rr;
+        if (rn <= tol * bn) { status = OG_OK; iters = it; goto done_rel; }
+    }
+    iters = maxit;
+    status = OG_NOT_CONVERGED;
+done_rel:
+    rel = rn / bn;
+done:
+    if (info) { info->iters = iters; info->status = status; info->restarts = restarts; info->rel_resid = rel; }
+    free(r); free(rh); free(p); free(v); free(s); free(t); free(y);
+    return status;
+}
+
+/* ------------------------------------------------------------------ §3.7 */
+/* u_e = u*_e + d_e (p'_P - p'_E) on interior and outlet faces (outlet ghost
+ * p' = 0, Q13/Q27); identity (wall) faces are copied; p = p + urf_p p'. */
+void or_correct(const og_grid *g, const og_params *pr,
+                const double *us, const double *vs, const double *ws,
+                const double *dxv, const double *dyv, const double *dzv,
+                const double *pp, const double *p,
+                double *u, double *v, double *w, double *pnew)
+{
+    const double *vin[3] = {us, vs, ws};
+    const double *dd[3] = {dxv, dyv, dzv};
+    double *vout[3] = {u, v, w};
+    for (int k = 0; k < g->nz; k++)
+        for (int j = 0; j < g->ny; j++)
+            for (int i = 0; i < g->nx; i++) {
+                const int P[3] = {i, j, k};
+                const long n = at(g, P);
+                for (int a = 0; a < 3; a++) {
+                    if (P[a] <= ext(g, a) - 2) {
+                        int E[3] = {i, j, k}; E[a] += 1;
+                        vout[a][n] = vin[a][n] + dd[a][n] * (pp[n] - pp[at(g, E)]);
+                    } else if (a == 2 && g->bc_zhi == OG_OUTLET) {
+                        vout[a][n] = vin[a][n] + dd[a][n] * (pp[n] - 0.0);
+                    } else {
+                        vout[a][n] = vin[a][n];
+                    }
+                }
+                pnew[n] = p[n] + pr->urf_p * pp[n];
+            }
+}
+
+/* ------------------------------------------------------------------ §3.8 */
+static og_eqsys alloc_sys(long N, int sym)
+{
+    og_eqsys e;
+    e.aP = calloc(N, sizeof(double)); e.aE = calloc(N, sizeof(double));
+    e.aN = calloc(N, sizeof(double)); e.aT = calloc(N, sizeof(double));
+    e.b = calloc(N, sizeof(double)); e.d = calloc(N, sizeof(double));
+    if (sym) { e.aW = e.aS = e.aB = NULL; }
+    else { e.aW = calloc(N, sizeof(double)); e.aS = calloc(N, sizeof(double)); e.aB = calloc(N, sizeof(double)); }
+    return e;
+}
+static void free_sys(og_eqsys *e)
+{
+    free(e->aP); free(e->aE); free(e->aN); free(e->aT); free(e->b); free(e->d);
+    free(e->aW); free(e->aS); free(e->aB);
+}
+
+int or_simple_iter(const og_grid *g, const og_params *pr, int n_scalars, og_state *st,
+                   double resid[4], int iters[8], int status[8])
+{
+    if (!grid_ok(g) || n_scalars < 0 || n_scalars > 4) return OG_ERR_ARG;
+    const long N = ncell(g);
+    double *star[3], *dv[3];
+    double R[3];
+    int worst = OG_OK;
+    for (int q = 0; q < 8; q++) { iters[q] = 0; status[q] = OG_OK; }
+    /* momentum predictors from the snapshot (u, v, w solved independently) */
+    for (int c = 0; c < 3; c++) {
+        og_eqsys e = alloc_sys(N, 0);
+        double r2[2];
+        int rc = or_assemble_mom(g, pr, c, st, &e, r2);
+        if (rc < 0) { free_sys(&e); return rc; }
+        R[c] = r2[0] / (r2[1] > 1e-30 ? r2[1] : 1e-30);
+        star[c] = malloc(sizeof(double) * N);
+        memcpy(star[c], c == 0 ? st->u : (c == 1 ? st->v : st->w), sizeof(double) * N);
+        og_solve_info inf;
+        or_bicgstab(g, &e, star[c], pr->lin_tol_mom, pr->lin_maxit_mom, &inf, NULL);
+        iters[c] = inf.iters; status[c] = inf.status;
+        if (inf.status < 0) worst = inf.status;
+        dv[c] = e.d; e.d = NULL;
+        free_sys(&e);
+    }
+    /* scalars from the same snapshot (Q22) */
+    double *phinew[4] = {NULL, NULL, NULL, NULL};
+    for (int s = 0; s < n_scalars; s++) {
+        og_eqsys e = alloc_sys(N, 0);
+        double r2[2];
+        int rc = or_assemble_scalar(g, pr, s, st, &e, r2);
+        if (rc < 0) { free_sys(&e); return rc; }
+        phinew[s] = malloc(sizeof(double) * N);
+        memcpy(phinew[s], st->phi[s], sizeof(double) * N);
+        og_solve_info inf;
+        or_bicgstab(g, &e, phinew[s], pr->lin_tol_phi, pr->lin_maxit_phi, &inf, NULL);
+        iters[4 + s] = inf.iters; status[4 + s] = inf.status;
+        if (inf.status < 0) worst = inf.status;
+        free_sys(&e);
+    }
+    /* pressure correction */
+    og_eqsys e = alloc_sys(N, 1);
+    double cont;
+    int rc = or_assemble_pp(g, pr, st, star[0], star[1], star[2], dv[0], dv[1], dv[2], &e, &cont);
+    if (rc < 0) { free_sys(&e); return rc; }
+    double *pp = calloc(N, sizeof(double));
+    og_solve_info inf;
+    or_bicgstab(g, &e, pp, pr->lin_tol_pp, pr->lin_maxit_pp, &inf, NULL);
+    iters[3] = inf.iters; status[3] = inf.status;
+    if (inf.status < 0) worst = inf.status;
+    free_sys(&e);
+    double *pn = malloc(sizeof(double) * N);
+    or_correct(g, pr, star[0], star[1], star[2], dv[0], dv[1], dv[2], pp, st->p, st->u, st->v, st->w, pn);
+    memcpy(st->p, pn, sizeof(double) * N);
+    for (int s = 0; s < n_scalars; s++) { memcpy(st->phi[s], phinew[s], sizeof(double) * N); free(phinew[s]); }
+    resid[0] = R[0]; resid[1] = R[1]; resid[2] = R[2]; resid[3] = cont;
+    for (int c = 0; c < 3; c++) { free(star[c]); free(dv[c]); }
+    free(pp); free(pn);
+    return worst;
+}

@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""bench.py -- BiCGSTAB iters/s (and SIMPLE iters/s) of the equation-decomposed
+SIMPLE hot path on B200, BASELINE.json metric, configuration 2 grid.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mfx|reference]
+
+A step is one SIMPLE outer iteration (all SURVEY §8(a) rows: u, v, w momentum
+assembly + BiCGSTAB, p' assembly + BiCGSTAB, correction, state exchange) on the
+128x128x512 fluidized-bed grid (8.4M cells, fp64).  `value` = BiCGSTAB
+iterations completed by all equations on all ranks / device time (CUDA events,
+max over ranks); `e2e` = the same metric through the C ABI with the snapshot
+copied from pinned host memory and u, v, w, p read back inside the timed region.
+
+--impl reference times the CPU oracle (oracle/, single thread) on a bounded
+sample of the same workload: it is the "reference arm" of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BiCGSTAB iters/s and SIMPLE iters/s per grid; achieved HBM GB/s vs 8 TB/s"
+UNIT = "iters/s"
+CONFIG_ID = 2
+
+# algorithmic bytes per cell per launch (SURVEY §8(d) byte model)
+BYTES_PER_CELL = {
+    "K1_mom": 4 * 8 + 2 * 8 + 7 * 8,     # r, p_old, v_old, r^ read; p, v write; 7 coefficients
+    "K2_mom": 2 * 8 + 1 * 8 + 7 * 8,     # r, v read; t write; 7 coefficients
+    "K1_pp": 4 * 8 + 2 * 8 + 4 * 8,      # symmetric p' storage: aP, c_x, c_y, c_z
+    "K2_pp": 2 * 8 + 1 * 8 + 4 * 8,
+    "K3": 6 * 8 + 2 * 8,                 # x, p, r, v, t, r^ read; x, r write
+    "spmv_setup": None, "assemble": None, "correct": None,
+}
+
+
+def assignment_for(n):
+    return {1: "111[1]", 2: "222[1]", 3: "234[1]", 4: "234[1]"}.get(n, "234[1]" + "".join(str(5 + s) for s in range(min(n - 4, 4))))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- reference arm (oracle)
+def oracle_sample(seconds_hint=False):
+    """Bounded sample: BiCGSTAB on the oracle-assembled c2 p' system, x0 = 0,
+    maxit = 2 (includes the setup r = b - A x0).  Returns (iters/s, seconds)."""
+    import numpy as np
+    import oracle
+    import synth
+    g, pr, st = synth.config_case(CONFIG_ID)
+    rng = np.random.default_rng(0)
+    dv = [rng.uniform(1e-4, 1e-3, g.n) for _ in range(3)]
+    sysd, _, _ = oracle.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+
+    def step():
+        t0 = time.perf_counter()
+        res = oracle.bicgstab(g, sysd, np.zeros(g.n), pr.lin_tol_pp, 2)
+        dt = time.perf_counter() - t0
+        return res["iters"], dt
+    return step
+
+
+SAMPLE_DESC = ("oracle BiCGSTAB (oracle/oracle.c, correctly rounded dots) on the oracle-assembled "
+               "128x128x512 p' system, x0=0, maxit=2 per sample including setup; 1 thread")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    step = oracle_sample()
+    for _ in range(args.warmup):
+        step()
+    tot_it, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        it, dt = step()
+        tot_it += it
+        tot_t += dt
+    v = tot_it / tot_t
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "c2 p' BiCGSTAB sample (oracle)", "grid": [128, 128, 512]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": SAMPLE_DESC},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- product arm
+def run_mfx(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import synth
+    import paper_2211_15605_b200 as mfx
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    g, pr, st = synth.config_case(CONFIG_ID, n_scalars=4)
+    asg = assignment_for(world)
+    n_scal = mfx.parse_assignment(asg, world)["n_scalars"]
+    if n_scal:
+        rng = np.random.default_rng(77)
+        for s in range(n_scal):
+            st[f"phi_old{s}"] = rng.uniform(0, 1, g.n)
+            st[f"phi{s}"] = st[f"phi_old{s}"].copy()
+    keep = list(synth.FIELD_NAMES) + [f"phi{s}" for s in range(n_scal)] + [f"phi_old{s}" for s in range(n_scal)]
+    host = {k: torch.from_numpy(st[k]).pin_memory() for k in keep}
+    sd = {k: v.cuda(non_blocking=True) for k, v in host.items()}
+    uid = None
+    if world > 1:
+        obj = [mfx.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = mfx.SimpleContext(asg, g, pr, rank=rank, nranks=world, uid=uid)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier(device_ids=[local_rank])
+
+    def my_iters(out):
+        owner = ctx.assignment["owner"]
+        return sum(out["iters"][q] for q in range(8) if owner[q] >= 0)
+
+    # ---- warm-up (untimed)
+    for _ in range(args.warmup):
+        ctx.step(sd)
+    # ---- device-timed region: K consecutive SIMPLE outer iterations
+    for k in ("u", "v", "w", "p"):
+        sd[k].copy_(host[k], non_blocking=True)
+    clocks = ClockSampler(local_rank)
+    mfx.prof_reset()
+    mfx.prof_enable(True)
+    barrier()
+    clocks.start()
+    l0 = mfx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters_total, outs = 0, []
+    for _ in range(args.steps):
+        out = ctx.step(sd)
+        outs.append(out)
+        iters_total += sum(out["iters"][q] for q in range(8) if ctx.assignment["owner"][q] >= 0)
+    ev1.record(stream)
+    barrier()
+    launches = mfx.launch_count() - l0
+    clk = clocks.stop()
+    mfx.prof_enable(False)
+    prof = mfx.prof_read()
+    t_ms = ev0.elapsed_time(ev1)
+    phase = ctx.phase_times()
+    if dist is not None:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    # iterations: every equation counted once (owners are disjoint; identical records on all ranks)
+    it_all = sum(outs[i]["iters"][q] for i in range(len(outs)) for q in range(8)
+                 if ctx.assignment["owner"][q] >= 0)
+    value = it_all / (t_ms / 1e3)
+    simple_per_s = args.steps / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event times, this stream)
+    n = g.n
+    peak, peak_kind = load_peaks()
+    best = max((k for k in prof if prof[k]["launches"]), key=lambda k: prof[k]["ms"])
+    kern = best
+    roof = None
+    if BYTES_PER_CELL.get(kern) is not None:
+        per_launch_ms = prof[kern]["ms"] / prof[kern]["launches"]
+        alg = BYTES_PER_CELL[kern] * n
+        achieved = alg / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_kind,
+                "alg_bytes_per_launch": alg, "avg_launch_us": per_launch_ms * 1e3,
+                "traffic": None, "share_of_step": prof[kern]["ms"] / t_ms}
+    # per-iteration p' rate: K1_pp + K2_pp + K3 (p' launches dominate K3 in this workload)
+    kern_ms = {k: (prof[k]["ms"] / prof[k]["launches"] if prof[k]["launches"] else None) for k in prof}
+
+    # ---- e2e through the C ABI with host buffers
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d = sum(v.numel() * 8 for v in host.values())
+    outbuf = {k: torch.empty_like(host[k]).pin_memory() for k in ("u", "v", "w", "p")}
+    d2h = sum(v.numel() * 8 for v in outbuf.values())
+    e2e_steps = max(1, min(args.steps, 3))
+    e0.record(stream)
+    e2e_iters = 0
+    for _ in range(e2e_steps):
+        for k, v in host.items():
+            sd[k].copy_(v, non_blocking=True)
+        out = ctx.step(sd)
+        e2e_iters += sum(out["iters"][q] for q in range(8) if ctx.assignment["owner"][q] >= 0)
+        for k in outbuf:
+            outbuf[k].copy_(sd[k], non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        tt = torch.tensor([e_ms, float(e2e_iters)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt[0].item())
+    e2e_value = e2e_iters / (e_ms / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        step = oracle_sample()
+        it, dt = step()
+        cpu = {"value": it / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": SAMPLE_DESC,
+               "seconds": dt}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak" if world > 4 else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded fluidized-bed fields, synth/)",
+                "config": {"workload": "c2: one SIMPLE outer iteration per step on 128x128x512 "
+                                       f"(assignment {asg}): u,v,w momentum assembly+BiCGSTAB "
+                                       "(tol 1e-4, maxit 20), p' assembly+BiCGSTAB (tol 1e-6, maxit 500), "
+                                       "correction, state exchange",
+                           "grid": [g.nx, g.ny, g.nz], "assignment": asg, "equations": 4 + n_scal,
+                           "l2": "inputs larger than L2 (13 fields x 64 MiB snapshot + systems >> 126 MB)"},
+                "simple_iters_per_s": simple_per_s,
+                "bicgstab_iters_per_step": it_all / args.steps,
+                "iters_last_step": outs[-1]["iters"],
+                "phase_ms_last_step": phase,
+                "kernel_avg_us": {k: (v * 1e3 if v else None) for k, v in kern_ms.items()},
+                "roofline": roof,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "steps": e2e_steps},
+                "gpu_launches": launches,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mfx", choices=["mfx", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_mfx(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/* mfx.h -- C ABI of libmfx.so: the B200-native hot path of arXiv 2211.15605
+ * ("equation decomposition" of the MP-PIC gas phase, §2.2.2).
+ *
+ * One SIMPLE outer iteration = assemble the
+ * 7-point finite-volume stencil of u, v, w momentum (Eq. 2) and of the
+ * pressure correction p' (Eq. 1), plus optional transported scalars
+ * (P:85), solve each with unpreconditioned BiCGSTAB, correct, and
+ * exchange the state between equation-owning GPUs once.
+ * The discrete definitions are written out in DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *  - Fields are caller-owned, contiguous IEEE binary64 DEVICE buffers of
+ *    N = nx*ny*nz elements on the calling thread's current device, linear
+ *    index n = i + nx*(j + ny*k) (x fastest).  Staggered velocities: u[n] sits
+ *    on the +x face of cell n, v on +y, w on +z.
+ *  - All calls are stream-ordered on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and never allocate device memory,
+ *    except mfx_ctx_create.  Nothing throws; every call returns mfx_status.
+ *  - Argument errors (NULL pointer, bad sizes, odd nx, unsupported boundary
+ *    combination, workspace too small) return MFX_ERR_ARG before any launch;
+ *    mfx_last_error() (thread-local) describes the first error.
+ *  - Device-side problems (non-finite coefficient, zero diagonal) are latched
+ *    in the workspace and reported by mfx_ws_check() (synchronises `stream`)
+ *    with the first offending linear cell index in mfx_last_error().
+ *  - Requirements: nx even (TMA/row-stride 16-byte rule), nx, ny, nz >= 2,
+ *    x/y sides are no-slip walls, z- INLET or WALL, z+ OUTLET or WALL
+ *    (DIRICHLET_TEST: scalar equations only).
+ */
+#ifndef MFX_H
+#define MFX_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MFX_OK = 0,
+    MFX_NOT_CONVERGED = 1,     /* status, not an error: last iterate returned (Q5) */
+    MFX_ERR_ARG = -1,
+    MFX_ERR_NONFINITE = -2,
+    MFX_ERR_ZERO_DIAG = -3,
+    MFX_ERR_BREAKDOWN = -4,    /* SPEC.md:374, after one restart */
+    MFX_ERR_CUDA = -5,
+    MFX_ERR_NCCL = -6
+} mfx_status;
+
+typedef enum { MFX_EQ_U = 0, MFX_EQ_V = 1, MFX_EQ_W = 2, MFX_EQ_PP = 3, MFX_EQ_SCALAR = 4 } mfx_eq_kind;
+
+typedef enum { MFX_BC_WALL = 0, MFX_BC_INLET = 1, MFX_BC_OUTLET = 2, MFX_BC_DIRICHLET_TEST = 3 } mfx_bc;
+
+typedef struct {
+    int nx, ny, nz;
+    double dx, dy, dz;          /* uniform spacing (m) */
+    int bc_zlo, bc_zhi;         /* mfx_bc; x/y sides are walls */
+    double w_in;                /* inlet normal velocity (m/s) */
+    double phi_in, phi_out;     /* scalar Dirichlet values (inlet; test-only top) */
+} mfx_grid;
+
+typedef struct {
+    double rho, mu;             /* gas density, viscosity */
+    double gamma_phi[4];        /* scalar diffusivities (Q21) */
+    double g[3];                /* gravity (m/s^2); paper: -z */
+    double dt;                  /* time step (s) */
+    double urf_mom, urf_p, urf_phi;  /* under-relaxation */
+    double tol;                 /* SIMPLE residual tolerance */
+    double lin_tol_mom, lin_tol_pp, lin_tol_phi;
+    int lin_maxit_mom, lin_maxit_pp, lin_maxit_phi;
+} mfx_params;
+
+/* Snapshot state (device pointers, N each).  Read-only to assembly; u, v, w,
+ * p, phi[] are overwritten by mfx_simple_iter. */
+typedef struct {
+    double *eps, *eps_old;                /* gas volume fraction now / old time */
+    double *u, *v, *w;                    /* staggered velocities, snapshot m */
+    double *u_old, *v_old, *w_old;        /* old-time velocities */
+    double *p;                            /* gauge pressure */
+    double *beta;                         /* implicit drag coefficient per cell (Q11) */
+    double *sbeta_u, *sbeta_v, *sbeta_w;  /* explicit drag source beta*u_s per cell */
+    double *phi[4], *phi_old[4];          /* optional scalars (NULL if unused) */
+} mfx_state;
+
+/* Equation system (device pointers, N each).  Momentum/scalar: all seven
+ * coefficient arrays, row a_P x_P - sum a_nb x_nb = b.  p': symmetric
+ * storage, aE/aN/aT hold the face coefficients c_x/c_y/c_z and aW/aS/aB must
+ * be NULL.  d (momentum only) = eps_f A_f / a_P,relaxed (Q16, Q27). */
+typedef struct { double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d; } mfx_eqsys;
+
+typedef struct {
+    int iters;                 /* BiCGSTAB iterations (half-step exit counts 1, Q3) */
+    int status;                /* mfx_status */
+    int restarts;              /* breakdown restarts taken (0 or 1) */
+    double rel_resid;          /* recursive ||r|| / ||b|| at exit */
+} mfx_solve_info;
+
+typedef struct {
+    double R_u, R_v, R_w, R_cont;   /* SIMPLE residuals (Norm_g = 1 P:157) */
+    double R_phi[4];
+    int iters[8];                   /* u, v, w, pp, phi0..3 */
+    int status[8];
+    int converged;                  /* max(R_u,R_v,R_w,R_cont) < tol */
+} mfx_resid;
+
+const char *mfx_last_error(void);
+const char *mfx_version(void);
+
+/* Initialise a freshly allocated workspace (clears reduction tickets and the
+ * error latch).  Must be called once before first use. */
+mfx_status mfx_ws_init(void *ws, size_t ws_bytes, void *stream);
+
+/* Bytes of device workspace needed to assemble and solve one equation of
+ * `kind` on `grid` (solver vectors r, r^, p x2, v x2, t + reduction scratch). */
+size_t mfx_workspace_bytes(const mfx_grid *grid, int kind);
+
+/* Reads and clears the device-side error latch of `ws` (synchronises stream). */
+mfx_status mfx_ws_check(void *ws, size_t ws_bytes, void *stream);
+
+/* a-1/a-2/a-3: assemble one equation's coefficients.
+ *  kind MFX_EQ_U/V/W: momentum; needs state->eps..sbeta_*; out->d required.
+ *  kind MFX_EQ_PP: star = {u*, v*, w*, d_x, d_y, d_z} (device); out aW/aS/aB NULL.
+ *  kind MFX_EQ_SCALAR: scalar_id 0..3, uses phi[scalar_id], phi_old[scalar_id].
+ *  resid2 (device, may be NULL): momentum/scalar {sum|res|, sum|aP u|};
+ *  p': {sum|b|, 0}.  Sums are correctly rounded. */
+mfx_status mfx_assemble_eq(int kind, int scalar_id, const mfx_grid *grid, const mfx_params *params,
+                           const mfx_state *state, const double *const star[6], mfx_eqsys *out,
+                           double *resid2, void *ws, size_t ws_bytes, void *stream);
+
+/* a-4: y = A x with the canonical term order of DESIGN.md §3.2. */
+mfx_status mfx_spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y,
+                    void *stream);
+
+/* a-5/a-6: unpreconditioned BiCGSTAB on A x = A->b.
+ * x: in x0, out solution (last iterate if not converged).  info (host) may be
+ * NULL: then the call is fully asynchronous and runs the device loop to
+ * convergence without host round trips; otherwise it synchronises `stream`
+ * once at exit.  Returns the solve status (MFX_OK / MFX_NOT_CONVERGED /
+ * MFX_ERR_BREAKDOWN) when info != NULL, else MFX_OK after launching. */
+mfx_status mfx_bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x,
+                              double tol, int maxit, void *ws, size_t ws_bytes,
+                              mfx_solve_info *info, void *stream);
+
+/* a-7: SIMPLE correction: u = u* + d (p'_P - p'_E), p = p + urf_p p'.
+ * star = {u*, v*, w*, d_x, d_y, d_z}; outputs may alias nothing in star. */
+mfx_status mfx_correct(const mfx_grid *grid, const mfx_params *params, const double *const star[6],
+                       const double *pp, const double *p, double *u, double *v, double *w,
+                       double *p_new, void *stream);
+
+/* ---------------------------------------------------------------- equation decomposition */
+/* Assignment string: three 1-based GPU ids for U, V, W,
+ * a bracketed P list, then optional scalar owners, e.g. "111[1]", "234[1]",
+ * "234[1]5678".  v1 accepts a single-entry P list (multi-GPU p' is NEXT-1). */
+typedef struct {
+    int owner[8];       /* 0-based rank owning u, v, w, pp, phi0..phi3; -1 = absent */
+    int n_scalars;
+    int n_ranks_used;   /* max id */
+} mfx_assignment;
+
+mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *out);
+
+/* Exchange schedule for `rank` (host logic, no device work).  phase 0 =
+ * GATHER (momentum owners -> p' owner: u*, d per component, plus a 16-double
+ * residual record), phase 1 = BCAST (p' owner -> all: u, v, w, p, residual
+ * record; scalar owners -> all: phi).  Ops are returned in the order they are
+ * issued inside one NCCL group. */
+enum { MFX_OP_SEND = 0, MFX_OP_RECV = 1, MFX_OP_BCAST = 2 };
+enum { MFX_BUF_U = 0, MFX_BUF_V, MFX_BUF_W, MFX_BUF_DX, MFX_BUF_DY, MFX_BUF_DZ,
+       MFX_BUF_P, MFX_BUF_PHI0, MFX_BUF_PHI1, MFX_BUF_PHI2, MFX_BUF_PHI3,
+       MFX_BUF_META, MFX_NBUF };
+/* buf MFX_BUF_META moves nslots 16-double residual records starting at slot;
+ * every other buffer moves N doubles (slot = nslots = 0).  peer = root for BCAST. */
+typedef struct { int op, peer, buf, slot, nslots; } mfx_xfer;
+mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops,
+                             int *n_ops);
+
+/* NCCL bootstrap: rank 0 calls mfx_nccl_unique_id and ships the 128 bytes to
+ * the other ranks (e.g. torch.distributed.broadcast_object_list). */
+mfx_status mfx_nccl_unique_id(unsigned char out[128]);
+
+typedef struct mfx_ctx mfx_ctx;
+
+/* Creates the per-rank context: parses the assignment, allocates the solver
+ * workspaces and exchange buffers for the equations this rank owns, and (for
+ * nranks > 1) an NCCL communicator from `uid`.  uid may be NULL when nranks == 1. */
+mfx_status mfx_ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid,
+                          const mfx_grid *grid, const mfx_params *params, mfx_ctx **out);
+void mfx_ctx_destroy(mfx_ctx *ctx);
+
+/* a-8: execute `phase` of the exchange plan on the context's buffers
+ * (fields = MFX_NBUF device pointers indexed by MFX_BUF_*; unused may be NULL). */
+mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_NBUF], void *stream);
+
+/* a-9: one SIMPLE outer iteration on this rank's share of the equations.
+ * state: in snapshot m, out m+1 (u, v, w, p and owned/broadcast phi on every
+ * rank).  out (host) receives the residual record (identical on all ranks).
+ * Synchronises `stream` once at the end (residual record to host). */
+mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void *stream);
+
+/* Per-phase device times of the last mfx_simple_iter on this rank (ms):
+ * [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction,
+ * [4] BCAST, [5] total. */
+mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
+
+/* ---------------------------------------------------------------- instrumentation */
+/* Kernel timing with CUDA events recorded on the launching stream around
+ * every hot kernel launch (off by default).  ids: 0 spmv/setup, 1 K1 (momentum/
+ * scalar), 2 K2 (momentum/scalar), 3 K3, 4 assemble, 5 correct, 6 K1 (p'), 7 K2 (p').  mfx_prof_read synchronises the device and
+ * returns, per id, launches and total milliseconds since mfx_prof_reset. */
+void mfx_prof_enable(int on);
+void mfx_prof_reset(void);
+mfx_status mfx_prof_read(int counts[8], double ms[8]);
+/* Number of libmfx kernel launches issued since process start. */
+long long mfx_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFX_H */

@@ -1,0 +1,332 @@
+"""Python binding of libmfx.so (include/mfx.h) -- argument marshalling only.
+
+Every step of the hot path (assembly, 7-point apply, BiCGSTAB, correction,
+SIMPLE orchestration, NCCL exchange) runs inside libmfx.so's sm_100a kernels.
+torch supplies device memory, streams and the process group used to ship the
+NCCL unique id.  There is no CPU fallback: if the library is missing this
+module raises ImportError, and every call raises MfxError on a non-OK status.
+
+Names follow include/mfx.h (§2.2.2 notation: U/V/W/P devices,
+assignment strings such as "111[1]" and "234[1]5678").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libmfx.so")
+if not os.path.exists(_SO):
+    raise ImportError(f"{_SO} is not built: run `python -m paper_2211_15605_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(_SO, mode=C.RTLD_GLOBAL)
+
+EQ_U, EQ_V, EQ_W, EQ_PP, EQ_SCALAR = 0, 1, 2, 3, 4
+BC_WALL, BC_INLET, BC_OUTLET, BC_DIRICHLET_TEST = 0, 1, 2, 3
+OK, NOT_CONVERGED, ERR_ARG, ERR_NONFINITE, ERR_ZERO_DIAG, ERR_BREAKDOWN, ERR_CUDA, ERR_NCCL = 0, 1, -1, -2, -3, -4, -5, -6
+OP_SEND, OP_RECV, OP_BCAST = 0, 1, 2
+BUF_NAMES = ("u", "v", "w", "dx", "dy", "dz", "p", "phi0", "phi1", "phi2", "phi3", "meta")
+NBUF = len(BUF_NAMES)
+
+
+class MfxError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        super().__init__(f"{where}: status {status}: {_lib.mfx_last_error().decode()}")
+
+
+class Grid(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+                ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double),
+                ("bc_zlo", C.c_int), ("bc_zhi", C.c_int),
+                ("w_in", C.c_double), ("phi_in", C.c_double), ("phi_out", C.c_double)]
+
+
+class Params(C.Structure):
+    _fields_ = [("rho", C.c_double), ("mu", C.c_double), ("gamma_phi", C.c_double * 4),
+                ("g", C.c_double * 3), ("dt", C.c_double), ("urf_mom", C.c_double),
+                ("urf_p", C.c_double), ("urf_phi", C.c_double), ("tol", C.c_double),
+                ("lin_tol_mom", C.c_double), ("lin_tol_pp", C.c_double), ("lin_tol_phi", C.c_double),
+                ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int)]
+
+
+_DP = C.POINTER(C.c_double)
+STATE_KEYS = ("eps", "eps_old", "u", "v", "w", "u_old", "v_old", "w_old", "p", "beta",
+              "sbeta_u", "sbeta_v", "sbeta_w")
+SYS_KEYS = ("aP", "aE", "aW", "aN", "aS", "aT", "aB", "b", "d")
+
+
+class State(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in STATE_KEYS] + [("phi", C.c_void_p * 4), ("phi_old", C.c_void_p * 4)]
+
+
+class Eqsys(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in SYS_KEYS]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("iters", C.c_int), ("status", C.c_int), ("restarts", C.c_int), ("rel_resid", C.c_double)]
+
+
+class Resid(C.Structure):
+    _fields_ = [("R_u", C.c_double), ("R_v", C.c_double), ("R_w", C.c_double), ("R_cont", C.c_double),
+                ("R_phi", C.c_double * 4), ("iters", C.c_int * 8), ("status", C.c_int * 8),
+                ("converged", C.c_int)]
+
+
+class Assignment(C.Structure):
+    _fields_ = [("owner", C.c_int * 8), ("n_scalars", C.c_int), ("n_ranks_used", C.c_int)]
+
+
+class Xfer(C.Structure):
+    _fields_ = [("op", C.c_int), ("peer", C.c_int), ("buf", C.c_int), ("slot", C.c_int), ("nslots", C.c_int)]
+
+
+_V = C.c_void_p
+_sigs = {
+    "mfx_last_error": (C.c_char_p, []),
+    "mfx_version": (C.c_char_p, []),
+    "mfx_workspace_bytes": (C.c_size_t, [C.POINTER(Grid), C.c_int]),
+    "mfx_ws_init": (C.c_int, [_V, C.c_size_t, _V]),
+    "mfx_ws_check": (C.c_int, [_V, C.c_size_t, _V]),
+    "mfx_assemble_eq": (C.c_int, [C.c_int, C.c_int, C.POINTER(Grid), C.POINTER(Params), C.POINTER(State),
+                                  C.POINTER(_V), C.POINTER(Eqsys), _V, _V, C.c_size_t, _V]),
+    "mfx_spmv": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, _V, _V]),
+    "mfx_bicgstab_solve": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
+                                     _V, C.c_size_t, C.POINTER(SolveInfo), _V]),
+    "mfx_correct": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(_V), _V, _V, _V, _V, _V, _V, _V]),
+    "mfx_parse_assignment": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(Assignment)]),
+    "mfx_exchange_plan": (C.c_int, [C.POINTER(Assignment), C.c_int, C.c_int, C.POINTER(Xfer), C.c_int,
+                                    C.POINTER(C.c_int)]),
+    "mfx_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "mfx_ctx_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(Grid), C.POINTER(Params),
+                                 C.POINTER(_V)]),
+    "mfx_ctx_destroy": (None, [_V]),
+    "mfx_exchange_state": (C.c_int, [_V, C.c_int, C.POINTER(_V), _V]),
+    "mfx_simple_iter": (C.c_int, [_V, C.POINTER(State), C.POINTER(Resid), _V]),
+    "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
+    "mfx_prof_enable": (None, [C.c_int]),
+    "mfx_prof_reset": (None, []),
+    "mfx_prof_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "mfx_launch_count": (C.c_longlong, []),
+}
+for _name, (_res, _args) in _sigs.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+EXPORTED = tuple(_sigs)
+
+
+def lib():
+    return _lib
+
+
+def _check(st, where, ok=(OK,)):
+    if st not in ok:
+        raise MfxError(st, where)
+    return st
+
+
+def version() -> str:
+    return _lib.mfx_version().decode()
+
+
+def last_error() -> str:
+    return _lib.mfx_last_error().decode()
+
+
+# ---------------------------------------------------------------- marshalling helpers
+def c_grid(g) -> Grid:
+    return Grid(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, g.bc_zlo, g.bc_zhi, g.w_in,
+                getattr(g, "phi_in", 1.0), getattr(g, "phi_out", 0.0))
+
+
+def c_params(p) -> Params:
+    return Params(p.rho, p.mu, (C.c_double * 4)(*p.gamma_phi), (C.c_double * 3)(*p.g), p.dt, p.urf_mom,
+                  p.urf_p, p.urf_phi, p.tol, p.lin_tol_mom, p.lin_tol_pp, p.lin_tol_phi,
+                  p.lin_maxit_mom, p.lin_maxit_pp, p.lin_maxit_phi)
+
+
+def _ptr(t, n=None):
+    if t is None:
+        return None
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def c_state(state: dict, n: int) -> State:
+    st = State(*[_ptr(state.get(k), n) for k in STATE_KEYS])
+    for s in range(4):
+        st.phi[s] = _ptr(state.get(f"phi{s}"), n)
+        st.phi_old[s] = _ptr(state.get(f"phi_old{s}"), n)
+    return st
+
+
+def c_sys(sysd: dict, n: int) -> Eqsys:
+    return Eqsys(*[_ptr(sysd.get(k), n) for k in SYS_KEYS])
+
+
+def new_system(kind: int, n: int, device="cuda"):
+    import torch
+    keys = ("aP", "aE", "aN", "aT", "b") if kind == EQ_PP else SYS_KEYS
+    return {k: torch.empty(n, dtype=torch.float64, device=device) for k in keys}
+
+
+class Workspace:
+    """Device workspace for one equation (reduction scratch + 7 solver vectors)."""
+
+    def __init__(self, grid, kind: int = 0, device="cuda", stream=None):
+        import torch
+        self.nbytes = int(_lib.mfx_workspace_bytes(C.byref(c_grid(grid)), kind))
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8, device=device)
+        off = (-self.buf.data_ptr()) % 256
+        self.ptr = self.buf.data_ptr() + off
+        _check(_lib.mfx_ws_init(self.ptr, self.nbytes, _stream(stream)), "mfx_ws_init")
+
+    def check(self, stream=None):
+        return _check(_lib.mfx_ws_check(self.ptr, self.nbytes, _stream(stream)), "mfx_ws_check")
+
+
+# ---------------------------------------------------------------- hot-path entry points
+def assemble_eq(kind, grid, params, state: dict, ws: Workspace, star=None, out=None, resid2=None,
+                scalar_id: int = 0, stream=None):
+    """a-1/a-2/a-3. Returns (system dict, resid2 device tensor[2])."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    dev = state["eps"].device
+    out = out if out is not None else new_system(kind, n, dev)
+    resid2 = resid2 if resid2 is not None else torch.zeros(2, dtype=torch.float64, device=dev)
+    cs = c_state(state, n)
+    sarr = None
+    if star is not None:
+        sarr = (C.c_void_p * 6)(*[_ptr(t, n) for t in star])
+    _check(_lib.mfx_assemble_eq(kind, scalar_id, C.byref(c_grid(grid)), C.byref(c_params(params)), C.byref(cs),
+                                sarr, C.byref(c_sys(out, n)), _ptr(resid2), C.c_void_p(ws.ptr), ws.nbytes,
+                                _stream(stream)), "mfx_assemble_eq")
+    return out, resid2
+
+
+def spmv(kind, grid, sysd: dict, x, y=None, stream=None):
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    y = y if y is not None else torch.empty_like(x)
+    _check(_lib.mfx_spmv(kind, C.byref(c_grid(grid)), C.byref(c_sys(sysd, n)), _ptr(x, n), _ptr(y, n),
+                         _stream(stream)), "mfx_spmv")
+    return y
+
+
+def bicgstab_solve(kind, grid, sysd: dict, x, tol: float, maxit: int, ws: Workspace, sync: bool = True,
+                   stream=None):
+    """a-5/a-6; x is updated in place. Returns the info dict (sync) or None."""
+    n = grid.nx * grid.ny * grid.nz
+    info = SolveInfo()
+    st = _lib.mfx_bicgstab_solve(kind, C.byref(c_grid(grid)), C.byref(c_sys(sysd, n)), _ptr(x, n), tol, maxit,
+                                 C.c_void_p(ws.ptr), ws.nbytes, C.byref(info) if sync else None, _stream(stream))
+    _check(st, "mfx_bicgstab_solve", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
+    if not sync:
+        return None
+    return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid)
+
+
+def correct(grid, params, star, pp, p, out=None, stream=None):
+    """a-7. star = (u*, v*, w*, d_x, d_y, d_z). Returns (u, v, w, p_new)."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    out = out if out is not None else [torch.empty_like(pp) for _ in range(4)]
+    sarr = (C.c_void_p * 6)(*[_ptr(t, n) for t in star])
+    _check(_lib.mfx_correct(C.byref(c_grid(grid)), C.byref(c_params(params)), sarr, _ptr(pp, n), _ptr(p, n),
+                            *[_ptr(t, n) for t in out], _stream(stream)), "mfx_correct")
+    return out
+
+
+# ---------------------------------------------------------------- equation decomposition
+def parse_assignment(text: str, nranks: int) -> dict:
+    a = Assignment()
+    _check(_lib.mfx_parse_assignment(text.encode(), nranks, C.byref(a)), "mfx_parse_assignment")
+    return dict(owner=list(a.owner), n_scalars=a.n_scalars, n_ranks_used=a.n_ranks_used)
+
+
+def exchange_plan(text: str, nranks: int, rank: int, phase: int):
+    a = Assignment()
+    _check(_lib.mfx_parse_assignment(text.encode(), nranks, C.byref(a)), "mfx_parse_assignment")
+    ops = (Xfer * 64)()
+    n = C.c_int()
+    _check(_lib.mfx_exchange_plan(C.byref(a), rank, phase, ops, 64, C.byref(n)), "mfx_exchange_plan")
+    return [dict(op=o.op, peer=o.peer, buf=BUF_NAMES[o.buf], slot=o.slot, nslots=o.nslots) for o in ops[:n.value]]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.mfx_nccl_unique_id(buf), "mfx_nccl_unique_id")
+    return buf.raw
+
+
+class SimpleContext:
+    """Per-rank equation-decomposition context (mfx_ctx)."""
+
+    def __init__(self, assignment: str, grid, params, rank: int = 0, nranks: int = 1, uid: bytes | None = None):
+        self.grid, self.params = grid, params
+        self._g, self._p = c_grid(grid), c_params(params)
+        self.ptr = C.c_void_p()
+        _check(_lib.mfx_ctx_create(assignment.encode(), rank, nranks, uid, C.byref(self._g), C.byref(self._p),
+                                   C.byref(self.ptr)), "mfx_ctx_create")
+        self.assignment = parse_assignment(assignment, nranks)
+
+    def step(self, state: dict, stream=None) -> dict:
+        """a-9: one SIMPLE outer iteration; state tensors updated in place."""
+        n = self.grid.nx * self.grid.ny * self.grid.nz
+        cs = c_state(state, n)
+        r = Resid()
+        st = _lib.mfx_simple_iter(self.ptr, C.byref(cs), C.byref(r), _stream(stream))
+        _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
+        return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
+                    status=list(r.status), converged=bool(r.converged))
+
+    def phase_times(self):
+        ms = (C.c_double * 6)()
+        _check(_lib.mfx_ctx_phase_times(self.ptr, ms), "mfx_ctx_phase_times")
+        return dict(zip(("momentum", "gather", "pp", "correct", "bcast", "total"), list(ms)))
+
+    def close(self):
+        if self.ptr:
+            _lib.mfx_ctx_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- instrumentation
+PROF_IDS = ("spmv_setup", "K1_mom", "K2_mom", "K3", "assemble", "correct", "K1_pp", "K2_pp")
+
+
+def prof_enable(on: bool = True):
+    _lib.mfx_prof_enable(1 if on else 0)
+
+
+def prof_reset():
+    _lib.mfx_prof_reset()
+
+
+def prof_read():
+    counts = (C.c_int * 8)()
+    ms = (C.c_double * 8)()
+    _check(_lib.mfx_prof_read(counts, ms), "mfx_prof_read")
+    return {PROF_IDS[i]: dict(launches=counts[i], ms=ms[i]) for i in range(len(PROF_IDS))}
+
+
+def launch_count() -> int:
+    return int(_lib.mfx_launch_count())

@@ -1,0 +1,236 @@
+// api.cu -- the extern "C" boundary of libmfx.so (include/mfx.h): argument
+// marshalling, workspace layout, error reporting and launch instrumentation.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mfx {
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// ------------------------------------------------------------------ workspace
+static size_t r256(size_t b) { return (b + 255) & ~(size_t)255; }
+size_t ws_header_bytes() { return r256(sizeof(WsHeader)); }
+static size_t ws_part_bytes() { return r256(sizeof(dd) * kMaxBlocks * kMaxDots); }
+size_t ws_total_bytes(long long N) { return ws_header_bytes() + ws_part_bytes() + 7 * r256(sizeof(double) * N); }
+
+bool ws_view(void *ws, size_t bytes, long long N, bool need_vectors, WsView &W)
+{
+    if (!ws) { set_error("workspace is NULL"); return false; }
+    if (((uintptr_t)ws) & 255) { set_error("workspace must be 256-byte aligned"); return false; }
+    const size_t need = need_vectors ? ws_total_bytes(N) : ws_header_bytes() + ws_part_bytes();
+    if (bytes < need) { set_error("workspace too small: %zu < %zu bytes", bytes, need); return false; }
+    char *b = (char *)ws;
+    W.hdr = (WsHeader *)b;
+    W.part = (dd *)(b + ws_header_bytes());
+    char *v = b + ws_header_bytes() + ws_part_bytes();
+    const size_t vb = r256(sizeof(double) * N);
+    double *vec[7];
+    for (int q = 0; q < 7; q++) vec[q] = need_vectors ? (double *)(v + vb * q) : nullptr;
+    W.r = vec[0]; W.rh = vec[1]; W.p[0] = vec[2]; W.p[1] = vec[3]; W.v[0] = vec[4]; W.v[1] = vec[5]; W.t = vec[6];
+    return true;
+}
+
+int reduce_grid(long long N)
+{
+    // fixed, device-independent grid -> fixed reduction order
+    long long b = (N + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+// ------------------------------------------------------------------ instrumentation
+static std::atomic<long long> g_launches{0};
+static std::atomic<int> g_prof{0};
+struct ProfRec { int id; cudaEvent_t a, b; };
+static std::mutex g_mu;
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_pool;
+static thread_local cudaEvent_t g_pending = nullptr;
+
+static cudaEvent_t get_event()
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void count_launch(int id, cudaStream_t s, bool start)
+{
+    if (!start) g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!g_prof.load(std::memory_order_relaxed) || id >= 8) return;
+    if (start) {
+        g_pending = get_event();
+        cudaEventRecord(g_pending, s);
+    } else if (g_pending) {
+        cudaEvent_t e = get_event();
+        cudaEventRecord(e, s);
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_recs.push_back({id, g_pending, e});
+        g_pending = nullptr;
+    }
+}
+
+// forward declarations (other translation units)
+bool grid_valid(const mfx_grid *g, bool scalar);
+mfx_status assemble_eq(int, int, const mfx_grid *, const mfx_params *, const mfx_state *, const double *const[6],
+                       mfx_eqsys *, double *, void *, size_t, cudaStream_t);
+mfx_status spmv(int, const mfx_grid *, const mfx_eqsys *, const double *, double *, cudaStream_t);
+mfx_status bicgstab_solve(int, const mfx_grid *, const mfx_eqsys *, double *, double, int, void *, size_t,
+                          mfx_solve_info *, cudaStream_t);
+mfx_status correct(const mfx_grid *, const mfx_params *, const double *const[6], const double *, const double *,
+                   double *, double *, double *, double *, cudaStream_t);
+mfx_status parse_assignment(const char *, int, mfx_assignment *);
+mfx_status exchange_plan(const mfx_assignment *, int, int, mfx_xfer *, int, int *);
+mfx_status nccl_unique_id(unsigned char out[128]);
+mfx_status ctx_create(const char *, int, int, const unsigned char *, const mfx_grid *, const mfx_params *,
+                      mfx_ctx **);
+mfx_status exchange_state(mfx_ctx *, int, double *const[MFX_NBUF], cudaStream_t);
+mfx_status simple_iter(mfx_ctx *, mfx_state *, mfx_resid *, cudaStream_t);
+
+}  // namespace mfx
+
+using namespace mfx;
+
+#define API extern "C" __attribute__((visibility("default")))
+
+API const char *mfx_last_error(void) { return g_err; }
+API const char *mfx_version(void) { return "mfx 0.1 (sm_100a, fp64, v1 kernels)"; }
+
+API size_t mfx_workspace_bytes(const mfx_grid *grid, int kind)
+{
+    (void)kind;
+    if (!grid) return 0;
+    return ws_total_bytes((long long)grid->nx * grid->ny * grid->nz);
+}
+
+API mfx_status mfx_ws_init(void *ws, size_t ws_bytes, void *stream)
+{
+    MFX_ARG_CHECK(ws && ws_bytes >= ws_header_bytes(), "bad workspace");
+    cudaStream_t s = (cudaStream_t)stream;
+    MFX_CUDA_TRY(cudaMemsetAsync(ws, 0, ws_header_bytes(), s));
+    WsHeader *h = (WsHeader *)ws;
+    MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_nonfinite, 0xff, 16, s));
+    return MFX_OK;
+}
+
+API mfx_status mfx_ws_check(void *ws, size_t ws_bytes, void *stream)
+{
+    MFX_ARG_CHECK(ws && ws_bytes >= ws_header_bytes(), "bad workspace");
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long bad[2];
+    WsHeader *h = (WsHeader *)ws;
+    MFX_CUDA_TRY(cudaMemcpyAsync(bad, &h->bad_nonfinite, 16, cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_nonfinite, 0xff, 16, s));
+    if (bad[0] != ~0ull) {
+        set_error("non-finite coefficient at cell %llu", bad[0]);
+        return MFX_ERR_NONFINITE;
+    }
+    if (bad[1] != ~0ull) {
+        set_error("zero diagonal at cell %llu", bad[1]);
+        return MFX_ERR_ZERO_DIAG;
+    }
+    return MFX_OK;
+}
+
+API mfx_status mfx_assemble_eq(int kind, int scalar_id, const mfx_grid *grid, const mfx_params *params,
+                               const mfx_state *state, const double *const star[6], mfx_eqsys *out, double *resid2,
+                               void *ws, size_t ws_bytes, void *stream)
+{
+    return assemble_eq(kind, scalar_id, grid, params, state, star, out, resid2, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, void *stream)
+{
+    return spmv(kind, grid, A, x, y, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol,
+                                  int maxit, void *ws, size_t ws_bytes, mfx_solve_info *info, void *stream)
+{
+    return bicgstab_solve(kind, grid, A, x, tol, maxit, ws, ws_bytes, info, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_correct(const mfx_grid *grid, const mfx_params *params, const double *const star[6],
+                           const double *pp, const double *p, double *u, double *v, double *w, double *p_new,
+                           void *stream)
+{
+    return correct(grid, params, star, pp, p, u, v, w, p_new, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *out)
+{
+    return parse_assignment(text, nranks, out);
+}
+
+API mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops)
+{
+    return exchange_plan(a, rank, phase, ops, max_ops, n_ops);
+}
+
+API mfx_status mfx_nccl_unique_id(unsigned char out[128]) { return nccl_unique_id(out); }
+
+API mfx_status mfx_ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid,
+                              const mfx_grid *grid, const mfx_params *params, mfx_ctx **out)
+{
+    return ctx_create(assignment, rank, nranks, uid, grid, params, out);
+}
+
+API mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_NBUF], void *stream)
+{
+    return exchange_state(ctx, phase, fields, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void *stream)
+{
+    return simple_iter(ctx, state, out, (cudaStream_t)stream);
+}
+
+API void mfx_prof_enable(int on) { g_prof.store(on ? 1 : 0); }
+
+API void mfx_prof_reset(void)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+    g_recs.clear();
+}
+
+API mfx_status mfx_prof_read(int counts[8], double ms[8])
+{
+    MFX_ARG_CHECK(counts && ms, "NULL out");
+    MFX_CUDA_TRY(cudaDeviceSynchronize());
+    for (int q = 0; q < 8; q++) { counts[q] = 0; ms[q] = 0.0; }
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &r : g_recs) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+            counts[r.id] += 1;
+            ms[r.id] += t;
+        }
+    }
+    return MFX_OK;
+}
+
+API long long mfx_launch_count(void) { return g_launches.load(); }

@@ -1,0 +1,557 @@
+// assemble.cu -- a-1 momentum, a-2 pressure-correction and a-3 scalar
+// coefficient assembly (Eq. 1, Eq. 2 P:53,
+// P:85) and a-7 the SIMPLE correction.
+//
+// One thread per row, grid-stride over cells with a fixed grid, so the
+// residual sums reduce in a fixed order (correctly rounded).
+// Assembly runs once per outer iteration; the BiCGSTAB kernels dominate.
+#include <climits>
+
+#include "common.cuh"
+
+namespace mfx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double maxp(double f) { return f > 0.0 ? f : 0.0; }
+
+struct Cell {
+    int q[3];
+};
+
+__device__ __forceinline__ long long lin(const Geo &G, const int q[3])
+{
+    return (long long)q[0] + (long long)G.nx * ((long long)q[1] + (long long)G.ny * q[2]);
+}
+__device__ __forceinline__ int extent(const Geo &G, int a) { return a == 0 ? G.nx : (a == 1 ? G.ny : G.nz); }
+__device__ __forceinline__ bool in_dom(const Geo &G, const int q[3])
+{
+    return q[0] >= 0 && q[0] < G.nx && q[1] >= 0 && q[1] < G.ny && q[2] >= 0 && q[2] < G.nz;
+}
+__device__ __forceinline__ void decode(const Geo &G, long long n, int q[3])
+{
+    long long pl = n / G.sz;
+    long long rem = n - pl * G.sz;
+    q[2] = (int)pl;
+    q[1] = (int)(rem / G.nx);
+    q[0] = (int)(rem - (long long)q[1] * G.nx);
+}
+
+__device__ __forceinline__ void latch(WsHeader *h, bool nonfinite, bool zerodiag, long long n)
+{
+    if (nonfinite) atomicMin(&h->bad_nonfinite, (unsigned long long)n);
+    else if (zerodiag) atomicMin(&h->bad_zerodiag, (unsigned long long)n);
+}
+
+// ------------------------------------------------------------------ momentum
+struct MomArgs {
+    Geo G;
+    double rho, urf, gc, rVdt;
+    double Dc[3];
+    const double *eps, *eps0, *vel0, *vel1, *vel2, *uold, *p, *beta, *S;
+    double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d;
+    double *resid2;
+    WsHeader *hdr;
+    dd *part;
+};
+
+enum { kInterior = 0, kIdentity = 1, kOutlet = 2 };
+
+template <int C>
+__device__ __forceinline__ int row_type(const Geo &G, const int q[3])
+{
+    if (q[C] < extent(G, C) - 1) return kInterior;
+    if (C == 2 && G.bc_zhi == MFX_BC_OUTLET) return kOutlet;
+    return kIdentity;
+}
+
+template <int C>
+__device__ __forceinline__ const double *vfield(const MomArgs &a, int t)
+{
+    return t == 0 ? a.vel0 : (t == 1 ? a.vel1 : a.vel2);
+}
+
+// component-C velocity on the face Q + e_C/2 (DESIGN.md §3.3 vel_c)
+template <int C>
+__device__ __forceinline__ double vel_c(const MomArgs &a, const int Q[3])
+{
+    const Geo &G = a.G;
+    if (Q[C] == -1) return (C == 2 && G.bc_zlo == MFX_BC_INLET) ? G.w_in : 0.0;
+    if (Q[C] == extent(G, C) - 1 && row_type<C>(G, Q) == kIdentity) return 0.0;
+    return __ldg(vfield<C>(a, C) + lin(G, Q));
+}
+
+// +t face mass flux of cell X (interior face)
+template <int C>
+__device__ __forceinline__ double mflux_t(const MomArgs &a, int t, const int X[3])
+{
+    const Geo &G = a.G;
+    int Xt[3] = {X[0], X[1], X[2]};
+    Xt[t] += 1;
+    double ef = 0.5 * (__ldg(a.eps + lin(G, X)) + __ldg(a.eps + lin(G, Xt)));
+    return ((a.rho * ef) * G.A[t]) * __ldg(vfield<C>(a, t) + lin(G, X));
+}
+
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
+{
+    const Geo &G = a.G;
+    Acc num, den;
+    num.zero();
+    den.zero();
+    const double *um = vfield<C>(a, C);
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
+         n += (long long)gridDim.x * blockDim.x) {
+        int P[3];
+        decode(G, n, P);
+        const int type = row_type<C>(G, P);
+        if (type == kIdentity) {
+            a.aP[n] = 1.0;
+            a.aE[n] = 0.0; a.aW[n] = 0.0; a.aN[n] = 0.0; a.aS[n] = 0.0; a.aT[n] = 0.0; a.aB[n] = 0.0;
+            a.b[n] = 0.0;
+            a.d[n] = 0.0;
+            continue;
+        }
+        int E[3] = {P[0], P[1], P[2]};
+        if (type == kInterior) E[C] += 1;
+        const long long nE = lin(G, E);
+        const double epsP = __ldg(a.eps + n), epsE = __ldg(a.eps + nE);
+
+        double as[6], phib[6];
+        bool kept[6], inP[6];
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) { as[s6] = 0.0; phib[s6] = 0.0; kept[s6] = false; inP[s6] = false; }
+
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            if (t == C) {
+                int Qm[3] = {P[0], P[1], P[2]};
+                Qm[C] -= 1;
+                const double vP = vel_c<C>(a, P);
+                const double vm = vel_c<C>(a, Qm);
+                const double Fm = ((a.rho * epsP) * G.A[C]) * (0.5 * (vm + vP));
+                const double Dm = a.Dc[C] * epsP;
+                as[2 * C] = Dm + maxp(Fm);
+                inP[2 * C] = true;
+                if (P[C] >= 1) kept[2 * C] = true;
+                else phib[2 * C] = vm;                                   // B1
+                if (type == kOutlet) {
+                    as[2 * C + 1] = 0.0;                                 // B3
+                } else {
+                    const double Fp = ((a.rho * epsE) * G.A[C]) * (0.5 * (vP + vel_c<C>(a, E)));
+                    const double Dp = a.Dc[C] * epsE;
+                    as[2 * C + 1] = Dp + maxp(-Fp);
+                    inP[2 * C + 1] = true;
+                    if (row_type<C>(G, E) == kIdentity) phib[2 * C + 1] = 0.0;   // B1
+                    else kept[2 * C + 1] = true;
+                }
+                continue;
+            }
+#pragma unroll
+            for (int sgn = 0; sgn < 2; sgn++) {
+                const int s = sgn ? 1 : -1;
+                const int side = 2 * t + sgn;
+                int Pt[3] = {P[0], P[1], P[2]};
+                Pt[t] += s;
+                int Et[3] = {E[0], E[1], E[2]};
+                Et[t] += s;
+                if (in_dom(G, Pt)) {
+                    const int *Q = s > 0 ? P : Pt;
+                    const int *R = s > 0 ? E : Et;
+                    const double F = 0.5 * (mflux_t<C>(a, t, Q) + mflux_t<C>(a, t, R));
+                    const double e4 = 0.25 * (((epsP + epsE) + __ldg(a.eps + lin(G, Pt))) +
+                                              __ldg(a.eps + lin(G, Et)));
+                    const double D = a.Dc[t] * e4;
+                    as[side] = D + maxp(s > 0 ? -F : F);
+                    inP[side] = true;
+                    kept[side] = true;
+                } else {
+                    int bc = MFX_BC_WALL;
+                    if (t == 2) bc = s < 0 ? G.bc_zlo : G.bc_zhi;
+                    if (bc == MFX_BC_OUTLET) { as[side] = 0.0; continue; }   // B3
+                    double F = 0.0;
+                    if (bc == MFX_BC_INLET)
+                        F = 0.5 * (((a.rho * epsP) * G.A[2]) * G.w_in + ((a.rho * epsE) * G.A[2]) * G.w_in);
+                    const double e2 = 0.5 * (epsP + epsE);
+                    const double D = a.Dc[t] * e2;
+                    as[side] = 2.0 * D + maxp(s > 0 ? -F : F);            // B2, phi_b = 0
+                    inP[side] = true;
+                    phib[side] = 0.0;
+                }
+            }
+        }
+        const double sum = ((((as[0] + as[1]) + as[2]) + as[3]) + as[4]) + as[5];
+        double bcb = 0.0;
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++)
+            if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
+        const double ef = 0.5 * (epsP + epsE);
+        const double e0f = 0.5 * (__ldg(a.eps0 + n) + __ldg(a.eps0 + nE));
+        const double bf = 0.5 * (__ldg(a.beta + n) + __ldg(a.beta + nE));
+        const double Sf = 0.5 * (__ldg(a.S + n) + __ldg(a.S + nE));
+        const double pE = type == kOutlet ? 0.0 : __ldg(a.p + nE);
+        const double a0 = a.rVdt * e0f;
+        const double aP = (sum + a0) + bf * G.V;
+        const double bb = ((((a0 * __ldg(a.uold + n)) + (ef * G.A[C]) * (__ldg(a.p + n) - pE)) +
+                            ((a.rho * ef) * a.gc) * G.V) + Sf * G.V) + bcb;
+        const double umP = __ldg(um + n);
+        const double aPr = aP / a.urf;
+        const double bR = bb + (aPr - aP) * umP;
+        const double dd_ = (ef * G.A[C]) / aPr;
+        double st6[6];
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? as[s6] : 0.0;
+        a.aW[n] = st6[0]; a.aE[n] = st6[1];
+        a.aS[n] = st6[2]; a.aN[n] = st6[3];
+        a.aB[n] = st6[4]; a.aT[n] = st6[5];
+        a.aP[n] = aPr;
+        a.b[n] = bR;
+        a.d[n] = dd_;
+        const bool nonfin = !isfinite(aPr) || !isfinite(bR) || !isfinite(dd_);
+        if (nonfin || aPr == 0.0) latch(a.hdr, nonfin, aPr == 0.0, n);
+
+        double res = bb - aP * umP;
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) {
+            int Q[3] = {P[0], P[1], P[2]};
+            Q[s6 / 2] += (s6 & 1) ? 1 : -1;
+            const double unb = in_dom(G, Q) ? __ldg(um + lin(G, Q)) : 0.0;
+            res = res + st6[s6] * unb;
+        }
+        num.add(fabs(res));
+        den.add(fabs(aP * umP));
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd v[2] = {num.get(), den.get()}, out[2];
+    if (grid_reduce_dd<2>(v, a.part, &a.hdr->ticket[0], sh, out) && threadIdx.x == 0 && a.resid2) {
+        a.resid2[0] = dd_round(out[0]);
+        a.resid2[1] = dd_round(out[1]);
+    }
+}
+
+// ------------------------------------------------------------------ p'
+struct PPArgs {
+    Geo G;
+    double rho, rVdt;
+    const double *eps, *eps0, *us[3], *dv[3];
+    double *aP, *cx, *cy, *cz, *b;
+    double *resid2;
+    WsHeader *hdr;
+    dd *part;
+};
+
+// rho eps_f A q on the +a face of X
+__device__ __forceinline__ double plus_face(const PPArgs &a, int ax, const int X[3], const double *q)
+{
+    const Geo &G = a.G;
+    const long long nX = lin(G, X);
+    if (X[ax] <= extent(G, ax) - 2) {
+        int Y[3] = {X[0], X[1], X[2]};
+        Y[ax] += 1;
+        const double ef = 0.5 * (__ldg(a.eps + nX) + __ldg(a.eps + lin(G, Y)));
+        return ((a.rho * ef) * G.A[ax]) * __ldg(q + nX);
+    }
+    if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET) return ((a.rho * __ldg(a.eps + nX)) * G.A[2]) * __ldg(q + nX);
+    return 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
+{
+    const Geo &G = a.G;
+    Acc cont;
+    cont.zero();
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
+         n += (long long)gridDim.x * blockDim.x) {
+        int P[3];
+        decode(G, n, P);
+        double cm[3], cpl[3], mm[3], mp[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            cpl[ax] = plus_face(a, ax, P, a.dv[ax]);
+            mp[ax] = plus_face(a, ax, P, a.us[ax]);
+            if (P[ax] >= 1) {
+                int Q[3] = {P[0], P[1], P[2]};
+                Q[ax] -= 1;
+                cm[ax] = plus_face(a, ax, Q, a.dv[ax]);
+                mm[ax] = plus_face(a, ax, Q, a.us[ax]);
+            } else {
+                cm[ax] = 0.0;
+                mm[ax] = (ax == 2 && G.bc_zlo == MFX_BC_INLET) ? ((a.rho * __ldg(a.eps + n)) * G.A[2]) * G.w_in
+                                                               : 0.0;
+            }
+        }
+        const double aP = ((((cm[0] + cpl[0]) + cm[1]) + cpl[1]) + cm[2]) + cpl[2];
+        const double bb = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) -
+                          a.rVdt * (__ldg(a.eps + n) - __ldg(a.eps0 + n));
+        a.aP[n] = aP;
+        a.cx[n] = cpl[0];
+        a.cy[n] = cpl[1];
+        a.cz[n] = cpl[2];
+        a.b[n] = bb;
+        const bool nonfin = !isfinite(aP) || !isfinite(bb);
+        if (nonfin || aP == 0.0) latch(a.hdr, nonfin, aP == 0.0, n);
+        cont.add(fabs(bb));
+    }
+    __shared__ dd sh[(kThreads / 32) * 1];
+    dd v[1] = {cont.get()}, out[1];
+    if (grid_reduce_dd<1>(v, a.part, &a.hdr->ticket[0], sh, out) && threadIdx.x == 0 && a.resid2) {
+        a.resid2[0] = dd_round(out[0]);
+        a.resid2[1] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------ scalar
+struct ScalArgs {
+    Geo G;
+    double rho, urf, rVdt;
+    double Dc[3];
+    const double *eps, *eps0, *vel[3], *phim, *phi0;
+    double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d;
+    double *resid2;
+    WsHeader *hdr;
+    dd *part;
+};
+
+__global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
+{
+    const Geo &G = a.G;
+    Acc num, den;
+    num.zero();
+    den.zero();
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
+         n += (long long)gridDim.x * blockDim.x) {
+        int P[3];
+        decode(G, n, P);
+        const double epsP = __ldg(a.eps + n);
+        double as[6], phib[6];
+        bool kept[6], inP[6];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            const int sm = 2 * ax, sp = 2 * ax + 1;
+            as[sm] = 0.0; as[sp] = 0.0; phib[sm] = 0.0; phib[sp] = 0.0;
+            kept[sm] = false; kept[sp] = false; inP[sm] = false; inP[sp] = false;
+            if (P[ax] >= 1) {
+                int Q[3] = {P[0], P[1], P[2]};
+                Q[ax] -= 1;
+                const long long nQ = lin(G, Q);
+                const double e = 0.5 * (__ldg(a.eps + nQ) + epsP);
+                const double F = ((a.rho * e) * G.A[ax]) * __ldg(a.vel[ax] + nQ);
+                as[sm] = a.Dc[ax] * e + maxp(F);
+                kept[sm] = true; inP[sm] = true;
+            } else if (ax == 2 && G.bc_zlo == MFX_BC_INLET) {
+                const double F = ((a.rho * epsP) * G.A[2]) * G.w_in;
+                as[sm] = 2.0 * (a.Dc[2] * epsP) + maxp(F);
+                inP[sm] = true;
+                phib[sm] = G.phi_in;
+            }
+            if (P[ax] <= extent(G, ax) - 2) {
+                int Q[3] = {P[0], P[1], P[2]};
+                Q[ax] += 1;
+                const double e = 0.5 * (epsP + __ldg(a.eps + lin(G, Q)));
+                const double F = ((a.rho * e) * G.A[ax]) * __ldg(a.vel[ax] + n);
+                as[sp] = a.Dc[ax] * e + maxp(-F);
+                kept[sp] = true; inP[sp] = true;
+            } else if (ax == 2 && G.bc_zhi == MFX_BC_DIRICHLET_TEST) {
+                const double F = ((a.rho * epsP) * G.A[2]) * __ldg(a.vel[2] + n);
+                as[sp] = 2.0 * (a.Dc[2] * epsP) + maxp(-F);
+                inP[sp] = true;
+                phib[sp] = G.phi_out;
+            }
+        }
+        const double sum = ((((as[0] + as[1]) + as[2]) + as[3]) + as[4]) + as[5];
+        double bcb = 0.0;
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++)
+            if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
+        const double a0 = a.rVdt * __ldg(a.eps0 + n);
+        const double aP = sum + a0;
+        const double bb = (a0 * __ldg(a.phi0 + n)) + bcb;
+        const double phP = __ldg(a.phim + n);
+        const double aPr = aP / a.urf;
+        const double bR = bb + (aPr - aP) * phP;
+        double st6[6];
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? as[s6] : 0.0;
+        a.aW[n] = st6[0]; a.aE[n] = st6[1];
+        a.aS[n] = st6[2]; a.aN[n] = st6[3];
+        a.aB[n] = st6[4]; a.aT[n] = st6[5];
+        a.aP[n] = aPr;
+        a.b[n] = bR;
+        if (a.d) a.d[n] = 0.0;
+        const bool nonfin = !isfinite(aPr) || !isfinite(bR);
+        if (nonfin || aPr == 0.0) latch(a.hdr, nonfin, aPr == 0.0, n);
+        double res = bb - aP * phP;
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) {
+            int Q[3] = {P[0], P[1], P[2]};
+            Q[s6 / 2] += (s6 & 1) ? 1 : -1;
+            const double unb = in_dom(G, Q) ? __ldg(a.phim + lin(G, Q)) : 0.0;
+            res = res + st6[s6] * unb;
+        }
+        num.add(fabs(res));
+        den.add(fabs(aP * phP));
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd v[2] = {num.get(), den.get()}, out[2];
+    if (grid_reduce_dd<2>(v, a.part, &a.hdr->ticket[0], sh, out) && threadIdx.x == 0 && a.resid2) {
+        a.resid2[0] = dd_round(out[0]);
+        a.resid2[1] = dd_round(out[1]);
+    }
+}
+
+// ------------------------------------------------------------------ correction
+struct CorrArgs {
+    Geo G;
+    double urf_p;
+    const double *us[3], *dv[3], *pp, *p;
+    double *u[3], *pnew;
+};
+
+__global__ void __launch_bounds__(kThreads) k_correct(CorrArgs a)
+{
+    const Geo &G = a.G;
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
+         n += (long long)gridDim.x * blockDim.x) {
+        int P[3];
+        decode(G, n, P);
+        const double ppP = __ldg(a.pp + n);
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            const double vs = __ldg(a.us[ax] + n);
+            double out;
+            if (P[ax] <= extent(G, ax) - 2) {
+                int E[3] = {P[0], P[1], P[2]};
+                E[ax] += 1;
+                out = vs + __ldg(a.dv[ax] + n) * (ppP - __ldg(a.pp + lin(G, E)));
+            } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET) {
+                out = vs + __ldg(a.dv[ax] + n) * (ppP - 0.0);
+            } else {
+                out = vs;
+            }
+            a.u[ax][n] = out;
+        }
+        a.pnew[n] = __ldg(a.p + n) + a.urf_p * ppP;
+    }
+}
+
+bool grid_ok(const mfx_grid *g, bool scalar)
+{
+    if (!g) { set_error("grid is NULL"); return false; }
+    if (g->nx < 2 || g->ny < 2 || g->nz < 2) { set_error("grid extents must be >= 2 (got %d %d %d)", g->nx, g->ny, g->nz); return false; }
+    if (g->nx % 2) { set_error("nx must be even (16-byte row stride), got %d", g->nx); return false; }
+    if (!(g->dx > 0 && g->dy > 0 && g->dz > 0)) { set_error("spacing must be positive"); return false; }
+    if (g->bc_zlo != MFX_BC_WALL && g->bc_zlo != MFX_BC_INLET) { set_error("bc_zlo must be WALL or INLET"); return false; }
+    const bool hi_ok = g->bc_zhi == MFX_BC_WALL || g->bc_zhi == MFX_BC_OUTLET ||
+                       (scalar && g->bc_zhi == MFX_BC_DIRICHLET_TEST);
+    if (!hi_ok) { set_error("bc_zhi %d not allowed for this equation", g->bc_zhi); return false; }
+    return true;
+}
+
+}  // namespace
+
+bool grid_valid(const mfx_grid *g, bool scalar) { return grid_ok(g, scalar); }
+
+mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params *pr, const mfx_state *st,
+                       const double *const star[6], mfx_eqsys *out, double *resid2, void *ws, size_t wsb,
+                       cudaStream_t s)
+{
+    const bool scalar = kind == MFX_EQ_SCALAR;
+    if (!grid_ok(grid, scalar)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(pr && st && out, "NULL params/state/out");
+    MFX_ARG_CHECK(kind >= MFX_EQ_U && kind <= MFX_EQ_SCALAR, "bad kind %d", kind);
+    const Geo G = make_geo(*grid);
+    WsView W;
+    if (!ws_view(ws, wsb, G.N, false, W)) return MFX_ERR_ARG;
+    const int nb = reduce_grid(G.N);
+    const double V = G.V;
+    const double rVdt = (pr->rho * V) / pr->dt;
+    if (kind <= MFX_EQ_W) {
+        MFX_ARG_CHECK(st->eps && st->eps_old && st->u && st->v && st->w && st->u_old && st->v_old && st->w_old &&
+                      st->p && st->beta && st->sbeta_u && st->sbeta_v && st->sbeta_w, "NULL state field");
+        MFX_ARG_CHECK(out->aP && out->aE && out->aW && out->aN && out->aS && out->aT && out->aB && out->b && out->d,
+                      "NULL eqsys array");
+        MomArgs a;
+        a.G = G;
+        a.rho = pr->rho;
+        a.urf = pr->urf_mom;
+        a.gc = pr->g[kind];
+        a.rVdt = rVdt;
+        for (int t = 0; t < 3; t++) a.Dc[t] = (pr->mu * G.A[t]) / G.h[t];
+        a.eps = st->eps; a.eps0 = st->eps_old;
+        a.vel0 = st->u; a.vel1 = st->v; a.vel2 = st->w;
+        a.uold = kind == 0 ? st->u_old : (kind == 1 ? st->v_old : st->w_old);
+        a.S = kind == 0 ? st->sbeta_u : (kind == 1 ? st->sbeta_v : st->sbeta_w);
+        a.p = st->p; a.beta = st->beta;
+        a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
+        a.aB = out->aB; a.b = out->b; a.d = out->d;
+        a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
+        count_launch(4, s, true);
+        if (kind == 0) k_assemble_mom<0><<<nb, kThreads, 0, s>>>(a);
+        else if (kind == 1) k_assemble_mom<1><<<nb, kThreads, 0, s>>>(a);
+        else k_assemble_mom<2><<<nb, kThreads, 0, s>>>(a);
+        count_launch(4, s, false);
+    } else if (kind == MFX_EQ_PP) {
+        MFX_ARG_CHECK(star && star[0] && star[1] && star[2] && star[3] && star[4] && star[5], "p' needs star[6]");
+        MFX_ARG_CHECK(st->eps && st->eps_old, "NULL eps");
+        MFX_ARG_CHECK(out->aP && out->aE && out->aN && out->aT && out->b && !out->aW && !out->aS && !out->aB,
+                      "p' eqsys: aP,aE,aN,aT,b required and aW,aS,aB must be NULL");
+        PPArgs a;
+        a.G = G;
+        a.rho = pr->rho;
+        a.rVdt = rVdt;
+        a.eps = st->eps; a.eps0 = st->eps_old;
+        for (int t = 0; t < 3; t++) { a.us[t] = star[t]; a.dv[t] = star[3 + t]; }
+        a.aP = out->aP; a.cx = out->aE; a.cy = out->aN; a.cz = out->aT; a.b = out->b;
+        a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
+        count_launch(4, s, true);
+        k_assemble_pp<<<nb, kThreads, 0, s>>>(a);
+        count_launch(4, s, false);
+    } else {
+        MFX_ARG_CHECK(sid >= 0 && sid < 4, "scalar id %d", sid);
+        MFX_ARG_CHECK(st->eps && st->eps_old && st->u && st->v && st->w && st->phi[sid] && st->phi_old[sid],
+                      "NULL scalar state field");
+        MFX_ARG_CHECK(out->aP && out->aE && out->aW && out->aN && out->aS && out->aT && out->aB && out->b,
+                      "NULL eqsys array");
+        ScalArgs a;
+        a.G = G;
+        a.rho = pr->rho;
+        a.urf = pr->urf_phi;
+        a.rVdt = rVdt;
+        for (int t = 0; t < 3; t++) a.Dc[t] = (pr->gamma_phi[sid] * G.A[t]) / G.h[t];
+        a.eps = st->eps; a.eps0 = st->eps_old;
+        a.vel[0] = st->u; a.vel[1] = st->v; a.vel[2] = st->w;
+        a.phim = st->phi[sid]; a.phi0 = st->phi_old[sid];
+        a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
+        a.aB = out->aB; a.b = out->b; a.d = out->d;
+        a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
+        count_launch(4, s, true);
+        k_assemble_scalar<<<nb, kThreads, 0, s>>>(a);
+        count_launch(4, s, false);
+    }
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+mfx_status correct(const mfx_grid *grid, const mfx_params *pr, const double *const star[6], const double *pp,
+                   const double *p, double *u, double *v, double *w, double *pnew, cudaStream_t s)
+{
+    if (!grid_ok(grid, false)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(pr && star && pp && p && u && v && w && pnew, "NULL argument");
+    for (int q = 0; q < 6; q++) MFX_ARG_CHECK(star[q], "star[%d] NULL", q);
+    CorrArgs a;
+    a.G = make_geo(*grid);
+    a.urf_p = pr->urf_p;
+    for (int t = 0; t < 3; t++) { a.us[t] = star[t]; a.dv[t] = star[3 + t]; }
+    a.pp = pp; a.p = p;
+    a.u[0] = u; a.u[1] = v; a.u[2] = w; a.pnew = pnew;
+    const int nb = reduce_grid(a.G.N);
+    count_launch(5, s, true);
+    k_correct<<<nb, kThreads, 0, s>>>(a);
+    count_launch(5, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+}  // namespace mfx

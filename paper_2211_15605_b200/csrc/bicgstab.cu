@@ -1,0 +1,415 @@
+// bicgstab.cu -- a-4 matrix-free 7-point apply and a-5/a-6 BiCGSTAB
+// ("No preconditioners").
+//
+// Per iteration three fused kernels, each ending in a deterministic,
+// correctly rounded grid reduction whose last block runs the scalar part of
+// the algorithm on the device (no host round trip):
+//   K1: p = fma(beta, fma(-omega, v, p), r) (recomputed at the halo from the
+//       OLD p, v -> p and v are ping-pong buffers), v = A p, sigma = <r^, v>
+//   K2: s = fma(-alpha, v, r) (recomputed at the halo), t = A s,
+//       <t,s>, <t,t>, <s,s>
+//   K3: x = fma(omega, s, fma(alpha, p, x)), r = fma(-omega, t, s),
+//       rho = <r^, r>, rr = <r, r>
+// 17 vector passes + 2 coefficient passes per iteration.
+#include <climits>
+
+#include "common.cuh"
+
+namespace mfx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Coef {
+    const double *aP, *aE, *aW, *aN, *aS, *aT, *aB;
+};
+
+// y = aP x_P, then fma(-a_nb, x_nb, y) for W,E,S,N,B,T
+template <bool SYM, class XV>
+__device__ __forceinline__ double stencil(const Geo &G, const Coef &c, long long n, int i, int j, int k,
+                                          XV xv)
+{
+    double aW, aE, aS, aN, aB, aT;
+    if (SYM) {
+        aW = i > 0 ? __ldg(c.aE + n - 1) : 0.0;
+        aE = __ldg(c.aE + n);
+        aS = j > 0 ? __ldg(c.aN + n - G.sy) : 0.0;
+        aN = __ldg(c.aN + n);
+        aB = k > 0 ? __ldg(c.aT + n - G.sz) : 0.0;
+        aT = __ldg(c.aT + n);
+    } else {
+        aW = __ldg(c.aW + n); aE = __ldg(c.aE + n); aS = __ldg(c.aS + n);
+        aN = __ldg(c.aN + n); aB = __ldg(c.aB + n); aT = __ldg(c.aT + n);
+    }
+    const double xW = i > 0 ? xv(n - 1) : 0.0;
+    const double xE = i < G.nx - 1 ? xv(n + 1) : 0.0;
+    const double xS = j > 0 ? xv(n - G.sy) : 0.0;
+    const double xN = j < G.ny - 1 ? xv(n + G.sy) : 0.0;
+    const double xB = k > 0 ? xv(n - G.sz) : 0.0;
+    const double xT = k < G.nz - 1 ? xv(n + G.sz) : 0.0;
+    double y = __ldg(c.aP + n) * xv(n);
+    y = fma(-aW, xW, y);
+    y = fma(-aE, xE, y);
+    y = fma(-aS, xS, y);
+    y = fma(-aN, xN, y);
+    y = fma(-aB, xB, y);
+    y = fma(-aT, xT, y);
+    return y;
+}
+
+__device__ __forceinline__ void decode(const Geo &G, long long n, int &i, int &j, int &k)
+{
+    long long pl = n / G.sz;
+    long long rem = n - pl * G.sz;
+    k = (int)pl;
+    j = (int)(rem / G.nx);
+    i = (int)(rem - (long long)j * G.nx);
+}
+
+#define GRID_STRIDE(n) \
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N; n += (long long)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------------ plain apply
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k_spmv(Geo G, Coef c, const double *__restrict__ x, double *y)
+{
+    GRID_STRIDE(n)
+    {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        y[n] = stencil<SYM>(G, c, n, i, j, k, [&](long long m) { return __ldg(x + m); });
+    }
+}
+
+// ------------------------------------------------------------------ setup
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k_setup(Geo G, Coef c, const double *__restrict__ b,
+                                                   const double *__restrict__ x, double *r, WsHeader *h, dd *part,
+                                                   double tol, int maxit)
+{
+    Acc bb, rr;
+    bb.zero();
+    rr.zero();
+    GRID_STRIDE(n)
+    {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        const double y = stencil<SYM>(G, c, n, i, j, k, [&](long long m) { return __ldg(x + m); });
+        const double bv = __ldg(b + n);
+        const double rv = bv - y;
+        r[n] = rv;
+        bb.prod(bv, bv);
+        rr.prod(rv, rv);
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd v[2] = {bb.get(), rr.get()}, out[2];
+    if (grid_reduce_dd<2>(v, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        SolverScalars &s = h->sc;
+        const double bn = sqrt(dd_round(out[0]));
+        const double rrv = dd_round(out[1]);
+        s.tol = tol;
+        s.maxit = maxit;
+        s.bn = bn;
+        s.rr = rrv;
+        s.rn = sqrt(rrv);
+        s.it = 0;
+        s.status = MFX_NOT_CONVERGED;
+        s.done = 0;
+        s.restarted = 0;
+        s.restarts = 0;
+        s.restart_mode = 1;   // r^ = r, p = v = 0, rho = <r^,r> = rr (DESIGN.md §3.6 init)
+        s.skip = 0;
+        s.half = 0;
+        s.zero_x = 0;
+        s.rho = rrv;
+        s.rhn = s.rn;
+        s.rho_prev = 1.0;
+        s.alpha = 1.0;
+        s.omega = 1.0;
+        if (bn == 0.0) {
+            s.zero_x = 1;
+            s.done = 1;
+            s.status = MFX_OK;
+            s.rn = 0.0;
+        } else if (s.rn <= tol * bn) {
+            s.done = 1;
+            s.status = MFX_OK;
+        } else if (maxit <= 0) {
+            s.done = 1;
+        }
+    }
+}
+
+__global__ void k_zero_if(const WsHeader *h, double *x, long long N)
+{
+    if (!h->sc.zero_x) return;
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += (long long)gridDim.x * blockDim.x)
+        x[n] = 0.0;
+}
+
+// ------------------------------------------------------------------ K1
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k1(Geo G, Coef c, const double *__restrict__ r, double *rh,
+                                              const double *__restrict__ p_old, const double *__restrict__ v_old,
+                                              double *p_new, double *v_new, WsHeader *h, dd *part)
+{
+    SolverScalars &S = h->sc;
+    if (S.done) return;
+    double rho = S.rho, rhn = S.rhn, rho_prev = S.rho_prev, alpha = S.alpha, omega = S.omega;
+    const double rn = S.rn, rr = S.rr;
+    const int restarted = S.restarted;
+    bool rst = S.restart_mode != 0;
+    bool newly = false;
+    if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
+    if (fabs(rho) <= (1e-14 * rhn) * rn) {
+        if (restarted) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) { S.status = MFX_ERR_BREAKDOWN; S.done = 1; }
+            return;
+        }
+        rst = true;
+        newly = true;
+        rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
+    }
+    const double beta = (rho / rho_prev) * (alpha / omega);
+    Acc sg;
+    sg.zero();
+    GRID_STRIDE(n)
+    {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        auto pv = [&](long long m) {
+            if (rst) return fma(beta, fma(-omega, 0.0, 0.0), __ldg(r + m));
+            return fma(beta, fma(-omega, __ldg(v_old + m), __ldg(p_old + m)), __ldg(r + m));
+        };
+        const double v = stencil<SYM>(G, c, n, i, j, k, pv);
+        p_new[n] = pv(n);
+        v_new[n] = v;
+        double rhv;
+        if (rst) {
+            rhv = __ldg(r + n);
+            rh[n] = rhv;
+        } else {
+            rhv = rh[n];
+        }
+        sg.prod(rhv, v);
+    }
+    __shared__ dd sh[(kThreads / 32) * 1];
+    dd vv[1] = {sg.get()}, out[1];
+    if (grid_reduce_dd<1>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        if (rst) {
+            S.rho = rho; S.rhn = rhn; S.rho_prev = 1.0; S.alpha = 1.0; S.omega = 1.0;
+        }
+        if (newly) { S.restarted = 1; S.restarts += 1; }
+        S.restart_mode = 0;
+        S.skip = 0;
+        const double sigma = dd_round(out[0]);
+        S.sigma = sigma;
+        if (sigma == 0.0) {
+            if (S.restarted) {
+                S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
+            } else {
+                S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
+                if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+            }
+        } else {
+            S.alpha = rho / sigma;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__restrict__ r,
+                                              const double *__restrict__ v, double *t, WsHeader *h, dd *part)
+{
+    SolverScalars &S = h->sc;
+    if (S.done || S.skip) return;
+    const double alpha = S.alpha;
+    Acc ts, tt, ss;
+    ts.zero(); tt.zero(); ss.zero();
+    GRID_STRIDE(n)
+    {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        auto sv = [&](long long m) { return fma(-alpha, __ldg(v + m), __ldg(r + m)); };
+        const double tv = stencil<SYM>(G, c, n, i, j, k, sv);
+        const double s = sv(n);
+        t[n] = tv;
+        ts.prod(tv, s);
+        tt.prod(tv, tv);
+        ss.prod(s, s);
+    }
+    __shared__ dd sh[(kThreads / 32) * 3];
+    dd vv[3] = {ts.get(), tt.get(), ss.get()}, out[3];
+    if (grid_reduce_dd<3>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
+        S.ts = tsv; S.tt = ttv; S.ss = ssv;
+        if (sqrt(ssv) <= S.tol * S.bn) {
+            S.half = 1;
+        } else {
+            const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
+            if (ttv == 0.0 || om == 0.0) {
+                if (S.restarted) {
+                    S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
+                } else {
+                    S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
+                    if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+                }
+            } else {
+                S.omega = om;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K3
+__global__ void __launch_bounds__(kThreads) k3(Geo G, double *x, double *r, const double *__restrict__ rh,
+                                              const double *__restrict__ p, const double *__restrict__ v,
+                                              const double *__restrict__ t, WsHeader *h, dd *part)
+{
+    SolverScalars &S = h->sc;
+    if (S.done || S.skip) return;
+    const double alpha = S.alpha, omega = S.omega;
+    const bool half = S.half != 0;
+    Acc rhr, rr;
+    rhr.zero(); rr.zero();
+    GRID_STRIDE(n)
+    {
+        const double s = fma(-alpha, __ldg(v + n), r[n]);
+        double xn, rn;
+        if (half) {
+            xn = fma(alpha, __ldg(p + n), x[n]);
+            rn = s;
+        } else {
+            xn = fma(omega, s, fma(alpha, __ldg(p + n), x[n]));
+            rn = fma(-omega, __ldg(t + n), s);
+        }
+        x[n] = xn;
+        r[n] = rn;
+        rhr.prod(__ldg(rh + n), rn);
+        rr.prod(rn, rn);
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd vv[2] = {rhr.get(), rr.get()}, out[2];
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        S.it += 1;
+        if (half) {
+            S.rn = sqrt(S.ss);
+            S.status = MFX_OK;
+            S.done = 1;
+        } else {
+            S.rho_prev = S.rho;
+            S.rho = dd_round(out[0]);
+            S.rr = dd_round(out[1]);
+            S.rn = sqrt(S.rr);
+            if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
+            else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+        }
+    }
+}
+
+Coef coef_of(const mfx_eqsys *A)
+{
+    Coef c;
+    c.aP = A->aP; c.aE = A->aE; c.aW = A->aW; c.aN = A->aN; c.aS = A->aS; c.aT = A->aT; c.aB = A->aB;
+    return c;
+}
+
+bool sys_ok(int kind, const mfx_eqsys *A)
+{
+    if (!A || !A->aP || !A->aE || !A->aN || !A->aT) return false;
+    if (kind == MFX_EQ_PP) return !A->aW && !A->aS && !A->aB;
+    return A->aW && A->aS && A->aB;
+}
+
+template <bool SYM>
+void launch_iteration(const Geo &G, const Coef &c, const WsView &W, double *x, int parity, int nb, cudaStream_t s)
+{
+    double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
+    double *v_old = W.v[parity], *v_new = W.v[parity ^ 1];
+    count_launch(SYM ? 6 : 1, s, true);
+    k1<SYM><<<nb, kThreads, 0, s>>>(G, c, W.r, W.rh, p_old, v_old, p_new, v_new, W.hdr, W.part);
+    count_launch(SYM ? 6 : 1, s, false);
+    count_launch(SYM ? 7 : 2, s, true);
+    k2<SYM><<<nb, kThreads, 0, s>>>(G, c, W.r, v_new, W.t, W.hdr, W.part);
+    count_launch(SYM ? 7 : 2, s, false);
+    count_launch(3, s, true);
+    k3<<<nb, kThreads, 0, s>>>(G, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part);
+    count_launch(3, s, false);
+}
+
+struct HostScratch {
+    SolverScalars *pinned = nullptr;
+    ~HostScratch() {}
+};
+thread_local HostScratch g_host;
+
+}  // namespace
+
+bool grid_valid(const mfx_grid *g, bool scalar);
+
+mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, cudaStream_t s)
+{
+    if (!grid_valid(grid, kind == MFX_EQ_SCALAR)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(sys_ok(kind, A), "bad eqsys for kind %d", kind);
+    MFX_ARG_CHECK(x && y, "NULL x/y");
+    const Geo G = make_geo(*grid);
+    const int nb = reduce_grid(G.N);
+    count_launch(0, s, true);
+    if (kind == MFX_EQ_PP) k_spmv<true><<<nb, kThreads, 0, s>>>(G, coef_of(A), x, y);
+    else k_spmv<false><<<nb, kThreads, 0, s>>>(G, coef_of(A), x, y);
+    count_launch(0, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol, int maxit,
+                          void *ws, size_t wsb, mfx_solve_info *info, cudaStream_t s)
+{
+    if (!grid_valid(grid, kind == MFX_EQ_SCALAR)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(sys_ok(kind, A) && A->b, "bad eqsys for kind %d", kind);
+    MFX_ARG_CHECK(x, "NULL x");
+    MFX_ARG_CHECK(tol >= 0.0 && maxit >= 0, "bad tol/maxit");
+    const Geo G = make_geo(*grid);
+    WsView W;
+    if (!ws_view(ws, wsb, G.N, true, W)) return MFX_ERR_ARG;
+    const bool sym = kind == MFX_EQ_PP;
+    const Coef c = coef_of(A);
+    const int nb = reduce_grid(G.N);
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
+    count_launch(0, s, true);
+    if (sym) k_setup<true><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
+    else k_setup<false><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
+    count_launch(0, s, false);
+    k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
+    count_launch(8, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
+    int launched = 0, chunk = 4;
+    while (launched < maxit) {
+        const int cnt = maxit - launched < chunk ? maxit - launched : chunk;
+        for (int q = 0; q < cnt; q++, launched++) {
+            if (sym) launch_iteration<true>(G, c, W, x, launched & 1, nb, s);
+            else launch_iteration<false>(G, c, W, x, launched & 1, nb, s);
+        }
+        MFX_CUDA_TRY(cudaGetLastError());
+        if (!info) continue;
+        MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+        MFX_CUDA_TRY(cudaStreamSynchronize(s));
+        if (g_host.pinned->done) break;
+        chunk = chunk * 2 > 64 ? 64 : chunk * 2;
+    }
+    if (!info) return MFX_OK;
+    MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    const SolverScalars &S = *g_host.pinned;
+    info->iters = S.it;
+    info->status = S.status;
+    info->restarts = S.restarts;
+    info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
+    return (mfx_status)S.status;
+}
+
+}  // namespace mfx

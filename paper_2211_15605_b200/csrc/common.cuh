@@ -1,0 +1,234 @@
+// common.cuh -- shared device helpers of libmfx (CUDA path only; the oracle
+// never includes this).  Compiled with --fmad=false: no FMA contraction,
+// fma() appears only where DESIGN.md §3 writes it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mfx.h"
+
+namespace mfx {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+#define MFX_CUDA_TRY(expr)                                                               \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            ::mfx::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+            return MFX_ERR_CUDA;                                                         \
+        }                                                                                \
+    } while (0)
+#define MFX_ARG_CHECK(cond, ...)                \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            ::mfx::set_error(__VA_ARGS__);                                               \
+            return MFX_ERR_ARG;                                                          \
+        }                                                                                \
+    } while (0)
+
+// ------------------------------------------------------------------ geometry
+struct Geo {
+    int nx, ny, nz;
+    long long N;
+    long long sy, sz;            // strides (elements)
+    double dx, dy, dz;
+    double A[3], h[3], V;        // A_x = dy*dz, A_y = dx*dz, A_z = dx*dy, V = (dx*dy)*dz
+    int bc_zlo, bc_zhi;
+    double w_in, phi_in, phi_out;
+};
+
+inline Geo make_geo(const mfx_grid &g)
+{
+    Geo G;
+    G.nx = g.nx; G.ny = g.ny; G.nz = g.nz;
+    G.N = (long long)g.nx * g.ny * g.nz;
+    G.sy = g.nx; G.sz = (long long)g.nx * g.ny;
+    G.dx = g.dx; G.dy = g.dy; G.dz = g.dz;
+    G.A[0] = g.dy * g.dz; G.A[1] = g.dx * g.dz; G.A[2] = g.dx * g.dy;
+    G.h[0] = g.dx; G.h[1] = g.dy; G.h[2] = g.dz;
+    G.V = (g.dx * g.dy) * g.dz;
+    G.bc_zlo = g.bc_zlo; G.bc_zhi = g.bc_zhi;
+    G.w_in = g.w_in; G.phi_in = g.phi_in; G.phi_out = g.phi_out;
+    return G;
+}
+
+// ------------------------------------------------------------------ double-double
+// Correctly rounded reductions: per-thread compensated
+// accumulation of exact products, then an accurate double-double tree.
+struct dd { double hi, lo; };
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e)
+{
+    s = a + b;
+    double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ void fast_two_sum(double a, double b, double &s, double &e)
+{
+    s = a + b;
+    e = b - (s - a);
+}
+// AccurateDWPlusDW (Joldes, Muller, Popescu 2017, Alg. 6): rel. error <= 3u^2.
+__device__ __forceinline__ dd dd_add(dd x, dd y)
+{
+    double sh, sl, th, tl, vh, vl, zh, zl;
+    two_sum(x.hi, y.hi, sh, sl);
+    two_sum(x.lo, y.lo, th, tl);
+    double c = sl + th;
+    fast_two_sum(sh, c, vh, vl);
+    double w = tl + vl;
+    fast_two_sum(vh, w, zh, zl);
+    return dd{zh, zl};
+}
+
+// Per-thread accumulator: s + c with s the running TwoSum head.
+struct Acc {
+    double s, c;
+    __device__ __forceinline__ void zero() { s = 0.0; c = 0.0; }
+    __device__ __forceinline__ void prod(double a, double b)
+    {
+        double ph = a * b;
+        double pl = fma(a, b, -ph);
+        double t, e;
+        two_sum(s, ph, t, e);
+        s = t;
+        c = c + (e + pl);
+    }
+    __device__ __forceinline__ void add(double x)
+    {
+        double t, e;
+        two_sum(s, x, t, e);
+        s = t;
+        c = c + e;
+    }
+    __device__ __forceinline__ dd get() const
+    {
+        dd r;
+        two_sum(s, c, r.hi, r.lo);
+        return r;
+    }
+};
+
+__device__ __forceinline__ dd shfl_dd(dd v, int off)
+{
+    dd r;
+    r.hi = __shfl_xor_sync(0xffffffffu, v.hi, off);
+    r.lo = __shfl_xor_sync(0xffffffffu, v.lo, off);
+    return r;
+}
+
+// Block reduction of K double-doubles in a fixed order; result valid in
+// thread 0.  `sh` needs (blockDim/32) * K dd slots.  All threads must call.
+template <int K>
+__device__ __forceinline__ void block_reduce_dd(dd (&v)[K], dd *sh)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+        dd x = v[q];
+        // fixed butterfly: lane 0 ends with ((0+16)+(8..))... deterministic
+        for (int off = 16; off > 0; off >>= 1) {
+            dd y = shfl_dd(x, off);
+            x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
+        }
+        v[q] = x;
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) sh[wid * K + q] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            dd x = sh[q];
+            for (int w = 1; w < nw; w++) x = dd_add(x, sh[w * K + q]);
+            v[q] = x;
+        }
+    }
+    __syncthreads();
+}
+
+// Deterministic grid reduction: each block writes K partials to part[blk*K+q];
+// the last block to finish (ticket) folds them in block order with all its
+// threads (strided sequential fold, then a fixed block tree) and returns true
+// in every thread of that block, with out[q] valid in thread 0.
+template <int K>
+__device__ __forceinline__ bool grid_reduce_dd(dd (&v)[K], dd *part, unsigned int *ticket, dd *sh,
+                                               dd (&out)[K])
+{
+    block_reduce_dd<K>(v, sh);
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) part[(size_t)blockIdx.x * K + q] = v[q];
+        __threadfence();
+        unsigned int t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    dd acc[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) acc[q] = dd{0.0, 0.0};
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            dd x;
+            x.hi = __ldcg(&part[(size_t)b * K + q].hi);
+            x.lo = __ldcg(&part[(size_t)b * K + q].lo);
+            acc[q] = dd_add(acc[q], x);
+        }
+    }
+    block_reduce_dd<K>(acc, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) out[q] = acc[q];
+        *ticket = 0u;   // reset for the next launch (stream-ordered)
+    }
+    return true;
+}
+
+__device__ __forceinline__ double dd_round(dd x) { return (x.hi + x.lo) + 0.0; }
+
+// ------------------------------------------------------------------ workspace
+struct SolverScalars {
+    double rho, rho_prev, alpha, omega;
+    double sigma, ss, ts, tt, rr;
+    double bn, rn, rhn, tol;
+    int it, maxit, status, done;
+    int restarted, restarts, restart_mode, skip;
+    int half, zero_x, pad0, pad1;
+};
+
+struct WsHeader {
+    SolverScalars sc;
+    unsigned long long bad_nonfinite;   // first offending cell (ULLONG_MAX = none)
+    unsigned long long bad_zerodiag;
+    unsigned int ticket[4];
+    double resid[4];
+    double pad[6];
+};
+
+constexpr int kMaxBlocks = 2048;
+constexpr int kMaxDots = 4;
+
+struct WsView {
+    WsHeader *hdr;
+    dd *part;                 // kMaxBlocks * kMaxDots
+    double *r, *rh, *p[2], *v[2], *t;
+};
+
+size_t ws_header_bytes();
+size_t ws_total_bytes(long long N);
+bool ws_view(void *ws, size_t bytes, long long N, bool need_vectors, WsView &out);
+
+// launch accounting / profiling
+void count_launch(int id, cudaStream_t s, bool start);
+int reduce_grid(long long N);
+
+}  // namespace mfx

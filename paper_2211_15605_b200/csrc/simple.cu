@@ -1,0 +1,462 @@
+// simple.cu -- a-8 state exchange and a-9 the equation-decomposed SIMPLE
+// outer iteration (§2.2.2: Udev/Vdev/Wdev/Pdev, P:85, P:95;
+// "infrequent movement of entire field variables").
+//
+// Each equation is owned by one rank (assignment string); its assembly,
+// every BiCGSTAB dot product and its convergence test stay on that GPU.  The
+// only inter-GPU traffic per outer iteration is one NCCL group of
+// point-to-point sends into the p' owner (GATHER: u*, d per component) and one
+// group of broadcasts out of it (BCAST: corrected u, v, w, p; scalar owners
+// broadcast phi).  Payloads are copied, never reduced, so any assignment gives
+// bitwise the same state as "111[1]".
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mfx {
+
+bool grid_valid(const mfx_grid *g, bool scalar);
+mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params *pr, const mfx_state *st,
+                       const double *const star[6], mfx_eqsys *out, double *resid2, void *ws, size_t wsb,
+                       cudaStream_t s);
+mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol, int maxit,
+                          void *ws, size_t wsb, mfx_solve_info *info, cudaStream_t s);
+mfx_status correct(const mfx_grid *grid, const mfx_params *pr, const double *const star[6], const double *pp,
+                   const double *p, double *u, double *v, double *w, double *pnew, cudaStream_t s);
+
+// ------------------------------------------------------------------ assignment
+mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
+{
+    MFX_ARG_CHECK(text && out, "NULL assignment/out");
+    MFX_ARG_CHECK(nranks >= 1 && nranks <= 64, "nranks %d out of range", nranks);
+    mfx_assignment a;
+    for (int q = 0; q < 8; q++) a.owner[q] = -1;
+    a.n_scalars = 0;
+    a.n_ranks_used = 0;
+    const char *c = text;
+    auto digit = [&](int &id) -> bool {
+        if (*c < '1' || *c > '9') return false;
+        id = *c - '0';
+        c++;
+        return true;
+    };
+    int id;
+    for (int q = 0; q < 3; q++) {
+        MFX_ARG_CHECK(digit(id), "assignment '%s': expected a digit 1-9 for %c", text, "UVW"[q]);
+        a.owner[q] = id - 1;
+    }
+    MFX_ARG_CHECK(*c == '[', "assignment '%s': expected '['", text);
+    c++;
+    int np = 0;
+    while (*c && *c != ']') {
+        MFX_ARG_CHECK(digit(id), "assignment '%s': bad P list", text);
+        if (np == 0) a.owner[3] = id - 1;
+        np++;
+    }
+    MFX_ARG_CHECK(*c == ']' && np >= 1, "assignment '%s': expected non-empty [P] list", text);
+    MFX_ARG_CHECK(np == 1, "assignment '%s': multi-GPU pressure solve [P..] (paper's [1234]) is NEXT-1, "
+                  "not implemented", text);
+    c++;
+    while (*c) {
+        MFX_ARG_CHECK(a.n_scalars < 4, "assignment '%s': at most 4 scalar equations", text);
+        MFX_ARG_CHECK(digit(id), "assignment '%s': bad scalar owner", text);
+        a.owner[4 + a.n_scalars++] = id - 1;
+    }
+    for (int q = 0; q < 8; q++) {
+        if (a.owner[q] < 0) continue;
+        MFX_ARG_CHECK(a.owner[q] < nranks, "assignment '%s': device id %d exceeds %d ranks (S:448)", text,
+                      a.owner[q] + 1, nranks);
+        if (a.owner[q] + 1 > a.n_ranks_used) a.n_ranks_used = a.owner[q] + 1;
+    }
+    *out = a;
+    return MFX_OK;
+}
+
+// ------------------------------------------------------------------ exchange plan
+// GATHER: momentum owners -> p' owner (u*, d, meta slot); BCAST: p' owner ->
+// all (u, v, w, p, meta slots 0-3), scalar owner -> all (phi, its meta slot).
+mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops)
+{
+    MFX_ARG_CHECK(a && n_ops && (ops || max_ops == 0), "NULL argument");
+    MFX_ARG_CHECK(phase == 0 || phase == 1, "phase must be 0 (GATHER) or 1 (BCAST)");
+    std::vector<mfx_xfer> v;
+    const int P = a->owner[3];
+    if (phase == 0) {
+        for (int c = 0; c < 3; c++) {
+            const int o = a->owner[c];
+            if (o == P) continue;
+            if (rank == o) {
+                v.push_back({MFX_OP_SEND, P, MFX_BUF_U + c, 0, 0});
+                v.push_back({MFX_OP_SEND, P, MFX_BUF_DX + c, 0, 0});
+                v.push_back({MFX_OP_SEND, P, MFX_BUF_META, c, 1});
+            } else if (rank == P) {
+                v.push_back({MFX_OP_RECV, o, MFX_BUF_U + c, 0, 0});
+                v.push_back({MFX_OP_RECV, o, MFX_BUF_DX + c, 0, 0});
+                v.push_back({MFX_OP_RECV, o, MFX_BUF_META, c, 1});
+            }
+        }
+    } else {
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_U, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_V, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_W, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_P, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_META, 0, 4});
+        for (int s = 0; s < a->n_scalars; s++) {
+            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_PHI0 + s, 0, 0});
+            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_META, 4 + s, 1});
+        }
+    }
+    *n_ops = (int)v.size();
+    MFX_ARG_CHECK((int)v.size() <= max_ops || !ops, "plan needs %d ops, buffer holds %d", (int)v.size(), max_ops);
+    if (ops)
+        for (size_t q = 0; q < v.size(); q++) ops[q] = v[q];
+    return MFX_OK;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool load()
+    {
+        if (h) return true;
+        const char *env = getenv("MFX_NCCL_PATH");
+        if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // torch's, if already loaded
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { set_error("cannot dlopen libnccl.so.2: %s", dlerror()); return false; }
+#define SYM(name) name = (decltype(name))dlsym(h, "nccl" #name); if (!name) { set_error("nccl%s missing", #name); return false; }
+        SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(GroupStart) SYM(GroupEnd) SYM(Send) SYM(Recv)
+        SYM(Broadcast) SYM(GetErrorString)
+#undef SYM
+        return true;
+    }
+};
+Nccl g_nccl;
+
+#define MFX_NCCL_TRY(expr)                                                                     \
+    do {                                                                                       \
+        ncclResult_t r_ = (expr);                                                              \
+        if (r_ != ncclSuccess) {                                                               \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, g_nccl.GetErrorString(r_));    \
+            return MFX_ERR_NCCL;                                                               \
+        }                                                                                      \
+    } while (0)
+
+size_t round256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+__global__ void k_meta(const WsHeader *h, const double *resid2, double *slot, int solved)
+{
+    if (threadIdx.x != 0) return;
+    const SolverScalars &S = h->sc;
+    slot[0] = resid2 ? resid2[0] : 0.0;
+    slot[1] = resid2 ? resid2[1] : 0.0;
+    slot[2] = solved ? (double)S.it : 0.0;
+    slot[3] = solved ? (double)S.status : 0.0;
+    slot[4] = solved ? (double)S.restarts : 0.0;
+    slot[5] = solved && S.bn != 0.0 ? S.rn / S.bn : 0.0;
+    slot[6] = 1.0;   // present
+}
+}  // namespace
+
+mfx_status nccl_unique_id(unsigned char out[128])
+{
+    MFX_ARG_CHECK(out, "NULL out");
+    if (!g_nccl.load()) return MFX_ERR_NCCL;
+    ncclUniqueId id;
+    MFX_NCCL_TRY(g_nccl.GetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return MFX_OK;
+}
+
+}  // namespace mfx
+
+// ------------------------------------------------------------------ context
+struct mfx_ctx {
+    int rank, nranks;
+    mfx_assignment asg;
+    mfx_grid grid;
+    mfx_params params;
+    long long N;
+    std::vector<void *> allocs;
+    mfx_eqsys sys[8];        // per equation (owned ones allocated)
+    void *ws[8];
+    size_t ws_bytes;
+    double *resid2;          // device [8][2]
+    double *star[3], *dv[3]; // u*, v*, w*, d_x, d_y, d_z (owned or received)
+    double *pp;              // p' solution
+    double *phinew[4];
+    double *meta;            // device [8][16]
+    double *meta_host;       // pinned [8][16]
+    ncclComm_t comm;
+    cudaEvent_t ev[6];
+    double phase_ms[6];
+};
+
+namespace mfx {
+
+static mfx_status ctx_alloc(mfx_ctx *c, void **p, size_t bytes)
+{
+    MFX_CUDA_TRY(cudaMalloc(p, bytes));
+    c->allocs.push_back(*p);
+    return MFX_OK;
+}
+
+mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid, const mfx_grid *grid,
+                      const mfx_params *params, mfx_ctx **out)
+{
+    MFX_ARG_CHECK(out && params, "NULL out/params");
+    *out = nullptr;
+    if (!grid_valid(grid, false)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(rank >= 0 && rank < nranks, "rank %d of %d", rank, nranks);
+    mfx_assignment a;
+    mfx_status st = parse_assignment(assignment, nranks, &a);
+    if (st != MFX_OK) return st;
+    MFX_ARG_CHECK(nranks == 1 || uid, "uid required for nranks > 1");
+    mfx_ctx *c = new mfx_ctx();
+    c->rank = rank; c->nranks = nranks; c->asg = a; c->grid = *grid; c->params = *params;
+    c->N = (long long)grid->nx * grid->ny * grid->nz;
+    c->comm = nullptr;
+    const size_t vb = round256(sizeof(double) * c->N);
+    c->ws_bytes = ws_total_bytes(c->N);
+    auto fail = [&](mfx_status s) { mfx_ctx_destroy(c); return s; };
+    for (int q = 0; q < 8; q++) { memset(&c->sys[q], 0, sizeof(mfx_eqsys)); c->ws[q] = nullptr; }
+    const int P = a.owner[3];
+    for (int q = 0; q < 8; q++) {
+        if (a.owner[q] != rank) continue;
+        const int narr = q == 3 ? 5 : 9;
+        void *blk;
+        if ((st = ctx_alloc(c, &blk, vb * narr)) != MFX_OK) return fail(st);
+        double *b0 = (double *)blk;
+        auto arr = [&](int k) { return (double *)((char *)b0 + vb * k); };
+        mfx_eqsys &e = c->sys[q];
+        e.aP = arr(0); e.aE = arr(1); e.aN = arr(2); e.aT = arr(3); e.b = arr(4);
+        if (q != 3) { e.aW = arr(5); e.aS = arr(6); e.aB = arr(7); e.d = arr(8); }
+        if ((st = ctx_alloc(c, &c->ws[q], c->ws_bytes)) != MFX_OK) return fail(st);
+        if (cudaMemset(c->ws[q], 0, ws_header_bytes()) != cudaSuccess) return fail(MFX_ERR_CUDA);
+        WsView W;
+        ws_view(c->ws[q], c->ws_bytes, c->N, false, W);
+        const unsigned long long none = ~0ull;
+        cudaMemcpy(&W.hdr->bad_nonfinite, &none, 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(&W.hdr->bad_zerodiag, &none, 8, cudaMemcpyHostToDevice);
+    }
+    // starred velocities and d: on the owner of each component and on the p' owner
+    for (int q = 0; q < 3; q++) {
+        c->star[q] = c->dv[q] = nullptr;
+        if (a.owner[q] == rank || P == rank) {
+            void *blk;
+            if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
+            c->star[q] = (double *)blk;
+            if (a.owner[q] == rank) c->dv[q] = c->sys[q].d;
+            else {
+                if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
+                c->dv[q] = (double *)blk;
+            }
+        }
+    }
+    c->pp = nullptr;
+    if (P == rank) {
+        void *blk;
+        if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
+        c->pp = (double *)blk;
+    }
+    for (int s = 0; s < 4; s++) {
+        c->phinew[s] = nullptr;
+        if (s < a.n_scalars && a.owner[4 + s] == rank) {
+            void *blk;
+            if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
+            c->phinew[s] = (double *)blk;
+        }
+    }
+    {
+        void *blk;
+        if ((st = ctx_alloc(c, &blk, 256 + 8 * 16 * sizeof(double))) != MFX_OK) return fail(st);
+        c->resid2 = (double *)blk;
+        c->meta = (double *)((char *)blk + 256);
+        if (cudaMemset(blk, 0, 256 + 8 * 16 * sizeof(double)) != cudaSuccess) return fail(MFX_ERR_CUDA);
+    }
+    if (cudaMallocHost(&c->meta_host, 8 * 16 * sizeof(double)) != cudaSuccess) {
+        c->meta_host = nullptr;
+        return fail(MFX_ERR_CUDA);
+    }
+    for (int q = 0; q < 6; q++) {
+        if (cudaEventCreate(&c->ev[q]) != cudaSuccess) return fail(MFX_ERR_CUDA);
+        c->phase_ms[q] = 0.0;
+    }
+    if (nranks > 1) {
+        if (!g_nccl.load()) return fail(MFX_ERR_NCCL);
+        ncclUniqueId id;
+        memcpy(&id, uid, 128);
+        ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            set_error("ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+            c->comm = nullptr;
+            return fail(MFX_ERR_NCCL);
+        }
+    }
+    *out = c;
+    return MFX_OK;
+}
+
+mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF], cudaStream_t s)
+{
+    MFX_ARG_CHECK(c && fields, "NULL ctx/fields");
+    if (c->nranks == 1) return MFX_OK;
+    mfx_xfer ops[64];
+    int n = 0;
+    mfx_status st = exchange_plan(&c->asg, c->rank, phase, ops, 64, &n);
+    if (st != MFX_OK) return st;
+    MFX_NCCL_TRY(g_nccl.GroupStart());
+    for (int q = 0; q < n; q++) {
+        const mfx_xfer &o = ops[q];
+        double *buf = fields[o.buf];
+        size_t count = (size_t)c->N;
+        if (o.buf == MFX_BUF_META) {
+            buf = buf + 16 * o.slot;
+            count = 16 * (size_t)o.nslots;
+        }
+        if (!buf) {
+            g_nccl.GroupEnd();
+            set_error("exchange: buffer %d is NULL on rank %d", o.buf, c->rank);
+            return MFX_ERR_ARG;
+        }
+        if (o.op == MFX_OP_SEND) MFX_NCCL_TRY(g_nccl.Send(buf, count, ncclDouble, o.peer, c->comm, s));
+        else if (o.op == MFX_OP_RECV) MFX_NCCL_TRY(g_nccl.Recv(buf, count, ncclDouble, o.peer, c->comm, s));
+        else MFX_NCCL_TRY(g_nccl.Broadcast(buf, buf, count, ncclDouble, o.peer, c->comm, s));
+    }
+    MFX_NCCL_TRY(g_nccl.GroupEnd());
+    return MFX_OK;
+}
+
+mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s)
+{
+    MFX_ARG_CHECK(c && st && out, "NULL argument");
+    const mfx_assignment &a = c->asg;
+    const mfx_params &pr = c->params;
+    const int r = c->rank, P = a.owner[3];
+    const size_t vbytes = sizeof(double) * (size_t)c->N;
+    mfx_status rc;
+    MFX_CUDA_TRY(cudaMemsetAsync(c->meta, 0, 8 * 16 * sizeof(double), s));
+    MFX_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    // momentum predictors (snapshot) on their owners
+    for (int q = 0; q < 3; q++) {
+        if (a.owner[q] != r) continue;
+        if ((rc = assemble_eq(q, 0, &c->grid, &pr, st, nullptr, &c->sys[q], c->resid2 + 2 * q, c->ws[q],
+                              c->ws_bytes, s)) != MFX_OK) return rc;
+        const double *snap = q == 0 ? st->u : (q == 1 ? st->v : st->w);
+        MFX_CUDA_TRY(cudaMemcpyAsync(c->star[q], snap, vbytes, cudaMemcpyDeviceToDevice, s));
+        mfx_solve_info info;
+        rc = bicgstab_solve(q, &c->grid, &c->sys[q], c->star[q], pr.lin_tol_mom, pr.lin_maxit_mom, c->ws[q],
+                            c->ws_bytes, &info, s);
+        if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
+        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
+    }
+    // scalars (same snapshot, Q22)
+    for (int sc = 0; sc < a.n_scalars; sc++) {
+        const int q = 4 + sc;
+        if (a.owner[q] != r) continue;
+        if ((rc = assemble_eq(MFX_EQ_SCALAR, sc, &c->grid, &pr, st, nullptr, &c->sys[q], c->resid2 + 2 * q,
+                              c->ws[q], c->ws_bytes, s)) != MFX_OK) return rc;
+        MFX_CUDA_TRY(cudaMemcpyAsync(c->phinew[sc], st->phi[sc], vbytes, cudaMemcpyDeviceToDevice, s));
+        mfx_solve_info info;
+        rc = bicgstab_solve(MFX_EQ_SCALAR, &c->grid, &c->sys[q], c->phinew[sc], pr.lin_tol_phi, pr.lin_maxit_phi,
+                            c->ws[q], c->ws_bytes, &info, s);
+        if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
+        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
+    }
+    MFX_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    double *F[MFX_NBUF] = {0};
+    F[MFX_BUF_U] = c->star[0]; F[MFX_BUF_V] = c->star[1]; F[MFX_BUF_W] = c->star[2];
+    F[MFX_BUF_DX] = c->dv[0]; F[MFX_BUF_DY] = c->dv[1]; F[MFX_BUF_DZ] = c->dv[2];
+    F[MFX_BUF_META] = c->meta;
+    if ((rc = exchange_state(c, 0, F, s)) != MFX_OK) return rc;
+    MFX_CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    if (r == P) {
+        const double *star6[6] = {c->star[0], c->star[1], c->star[2], c->dv[0], c->dv[1], c->dv[2]};
+        if ((rc = assemble_eq(MFX_EQ_PP, 0, &c->grid, &pr, st, star6, &c->sys[3], c->resid2 + 6, c->ws[3],
+                              c->ws_bytes, s)) != MFX_OK) return rc;
+        MFX_CUDA_TRY(cudaMemsetAsync(c->pp, 0, vbytes, s));
+        mfx_solve_info info;
+        rc = bicgstab_solve(MFX_EQ_PP, &c->grid, &c->sys[3], c->pp, pr.lin_tol_pp, pr.lin_maxit_pp, c->ws[3],
+                            c->ws_bytes, &info, s);
+        if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
+        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[3], c->resid2 + 6, c->meta + 48, 1);
+        MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
+        if ((rc = correct(&c->grid, &pr, star6, c->pp, st->p, st->u, st->v, st->w, st->p, s)) != MFX_OK) return rc;
+    } else {
+        MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
+    }
+    for (int sc = 0; sc < a.n_scalars; sc++)
+        if (a.owner[4 + sc] == r)
+            MFX_CUDA_TRY(cudaMemcpyAsync(st->phi[sc], c->phinew[sc], vbytes, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    double *B[MFX_NBUF] = {0};
+    B[MFX_BUF_U] = st->u; B[MFX_BUF_V] = st->v; B[MFX_BUF_W] = st->w; B[MFX_BUF_P] = st->p;
+    for (int sc = 0; sc < a.n_scalars; sc++) B[MFX_BUF_PHI0 + sc] = st->phi[sc];
+    B[MFX_BUF_META] = c->meta;
+    if ((rc = exchange_state(c, 1, B, s)) != MFX_OK) return rc;
+    MFX_CUDA_TRY(cudaEventRecord(c->ev[5], s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(c->meta_host, c->meta, 8 * 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    float ms;
+    // [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction, [4] BCAST, [5] total
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); c->phase_ms[0] = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); c->phase_ms[1] = ms;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); c->phase_ms[2] = ms;
+    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); c->phase_ms[3] = ms;
+    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]); c->phase_ms[4] = ms;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]); c->phase_ms[5] = ms;
+    const double *m = c->meta_host;
+    auto R = [&](int q) { const double den = m[16 * q + 1]; return m[16 * q] / (den > 1e-30 ? den : 1e-30); };
+    memset(out, 0, sizeof(*out));
+    out->R_u = R(0); out->R_v = R(1); out->R_w = R(2); out->R_cont = m[16 * 3];
+    for (int sc = 0; sc < 4; sc++) out->R_phi[sc] = sc < a.n_scalars ? R(4 + sc) : 0.0;
+    int worst = MFX_OK;
+    for (int q = 0; q < 8; q++) {
+        out->iters[q] = (int)m[16 * q + 2];
+        out->status[q] = (int)m[16 * q + 3];
+        if (out->status[q] < 0) worst = out->status[q];
+    }
+    double mx = out->R_u;
+    if (out->R_v > mx) mx = out->R_v;
+    if (out->R_w > mx) mx = out->R_w;
+    if (out->R_cont > mx) mx = out->R_cont;
+    out->converged = mx < pr.tol;
+    return (mfx_status)worst;
+}
+
+}  // namespace mfx
+
+void mfx_ctx_destroy(mfx_ctx *c)
+{
+    if (!c) return;
+    if (c->comm && mfx::g_nccl.CommDestroy) mfx::g_nccl.CommDestroy(c->comm);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->meta_host) cudaFreeHost(c->meta_host);
+    for (int q = 0; q < 6; q++)
+        if (c->ev[q]) cudaEventDestroy(c->ev[q]);
+    delete c;
+}
+
+mfx_status mfx_ctx_phase_times(const mfx_ctx *c, double ms[6])
+{
+    if (!c || !ms) return MFX_ERR_ARG;
+    for (int q = 0; q < 6; q++) ms[q] = c->phase_ms[q];
+    return MFX_OK;
+}

@@ -1,0 +1,126 @@
+"""CPU-only checks of the C-ABI boundary: libmfx.so loads without a GPU, exports
+every function include/mfx.h declares, and its host logic (assignment parsing,
+exchange plan, workspace sizing, argument validation) behaves as specified
+(PAPER.md:95 assignment notation)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mfx.h")
+
+
+@pytest.fixture(scope="module")
+def mfx():
+    from paper_2211_15605_b200 import build
+    build.build()
+    import paper_2211_15605_b200 as m
+    return m
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mfx_[a-z_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(mfx):
+    so = os.path.join(ROOT, "paper_2211_15605_b200", "libmfx.so")
+    out = subprocess.check_output(["nm", "-D", "--defined-only", so], text=True)
+    exported = set(re.findall(r" T (mfx_[a-z_]+)$", out, flags=re.M))
+    decl = declared_functions()
+    assert len(decl) >= 20
+    missing = [f for f in decl if f not in exported]
+    assert not missing, missing
+    lib = mfx.lib()
+    for f in decl:
+        assert getattr(lib, f) is not None
+    assert set(mfx.EXPORTED) == set(decl)
+
+
+def test_no_driver_link_dependency():
+    so = os.path.join(ROOT, "paper_2211_15605_b200", "libmfx.so")
+    out = subprocess.check_output(["ldd", so], text=True)
+    assert "libcuda.so" not in out and "libnccl" not in out and "libtorch" not in out
+
+
+def test_version(mfx):
+    assert "sm_100a" in mfx.version()
+
+
+@pytest.mark.parametrize("text,n,owner", [
+    ("111[1]", 1, [0, 0, 0, 0, -1, -1, -1, -1]),          # PAPER.md:95 single GPU
+    ("234[1]", 4, [1, 2, 3, 0, -1, -1, -1, -1]),          # Fig. 2b with single-GPU P
+    ("222[1]", 2, [1, 1, 1, 0, -1, -1, -1, -1]),
+    ("234[1]5678", 8, [1, 2, 3, 0, 4, 5, 6, 7]),          # extra scalar equations
+    ("111[1]1111", 1, [0, 0, 0, 0, 0, 0, 0, 0]),
+])
+def test_parse_assignment(mfx, text, n, owner):
+    a = mfx.parse_assignment(text, n)
+    assert a["owner"] == owner
+    assert a["n_scalars"] == sum(o >= 0 for o in owner[4:])
+
+
+@pytest.mark.parametrize("text,n", [
+    ("123[45]", 4),        # SPEC.md:448 id 5 out of range
+    ("12[1]", 4),          # malformed
+    ("111", 1),
+    ("111[]", 1),
+    ("111[1]x", 1),
+    ("234[1234]", 4),      # multi-GPU pressure (NEXT-1) rejected in v1
+    ("111[1]11111", 1),    # > 4 scalars
+])
+def test_parse_assignment_errors(mfx, text, n):
+    with pytest.raises(mfx.MfxError) as e:
+        mfx.parse_assignment(text, n)
+    assert e.value.status == mfx.ERR_ARG
+    assert mfx.last_error()
+
+
+def _plan_all(mfx, text, n):
+    return {r: (mfx.exchange_plan(text, n, r, 0), mfx.exchange_plan(text, n, r, 1)) for r in range(n)}
+
+
+@pytest.mark.parametrize("text,n", [("234[1]", 4), ("222[1]", 2), ("234[1]5678", 8), ("211[2]3", 3),
+                                    ("111[1]", 1), ("111[1]", 3)])
+def test_exchange_plan_consistency(mfx, text, n):
+    plans = _plan_all(mfx, text, n)
+    a = mfx.parse_assignment(text, n)
+    P = a["owner"][3]
+    # GATHER: every send has exactly one matching recv on the peer, same buffer
+    sends = [(r, o["peer"], o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_SEND]
+    recvs = [(o["peer"], r, o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_RECV]
+    assert sorted(sends) == sorted(recvs)
+    for (src, dst, buf, slot) in sends:
+        assert dst == P and src != P
+    # each momentum component not owned by P is gathered (u*, d, meta)
+    need = {c for c in range(3) if a["owner"][c] != P}
+    got = {"uvw".index(b) for (_, _, b, _) in sends if b in ("u", "v", "w")}
+    assert got == need
+    # BCAST: identical op list on every rank (collective order must match)
+    b0 = plans[0][1]
+    for r in range(n):
+        assert plans[r][1] == b0
+    roots = {o["buf"]: o["peer"] for o in b0 if o["buf"] != "meta"}
+    assert roots["u"] == roots["v"] == roots["w"] == roots["p"] == P
+    for s in range(a["n_scalars"]):
+        assert roots[f"phi{s}"] == a["owner"][4 + s]
+
+
+def test_exchange_plan_counts(mfx):
+    g = mfx.exchange_plan("234[1]", 4, 0, 0)
+    assert len(g) == 9                      # recv u*,d,meta from 3 owners
+    assert len(mfx.exchange_plan("234[1]", 4, 2, 0)) == 3
+    assert len(mfx.exchange_plan("111[1]", 1, 0, 0)) == 0
+
+
+def test_workspace_bytes_scale(mfx):
+    import synth
+    g1 = synth.make_grid(16, 16, 32)
+    g2 = synth.make_grid(32, 16, 32)
+    b1 = mfx.lib().mfx_workspace_bytes(C.byref(mfx.c_grid(g1)), 0)
+    b2 = mfx.lib().mfx_workspace_bytes(C.byref(mfx.c_grid(g2)), 0)
+    assert b2 - b1 == 7 * 8 * 16 * 16 * 32

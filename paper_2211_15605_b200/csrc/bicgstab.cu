@@ -12,10 +12,15 @@
 //       rho = <r^, r>, rr = <r, r>
 // 17 vector passes + 2 coefficient passes per iteration.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace mfx {
+
+mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
+                          const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
+                          double tol, int maxit, cudaStream_t s);
 
 namespace {
 
@@ -324,6 +329,29 @@ bool sys_ok(int kind, const mfx_eqsys *A)
 }
 
 template <bool SYM>
+mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &W, double *x, int parity, int nb,
+                                cudaStream_t s)
+{
+    double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
+    double *v_old = W.v[parity], *v_new = W.v[parity ^ 1];
+    mfx_status st;
+    count_launch(SYM ? 6 : 1, s, true);
+    const double *h1[3] = {W.r, p_old, v_old};
+    st = stencil_launch(2, SYM, G, h1, A, W.rh, p_new, v_new, W.rh, W.hdr, W.part, 0.0, 0, s);
+    count_launch(SYM ? 6 : 1, s, false);
+    if (st != MFX_OK) return st;
+    count_launch(SYM ? 7 : 2, s, true);
+    const double *h2[3] = {W.r, v_new, nullptr};
+    st = stencil_launch(3, SYM, G, h2, A, nullptr, W.t, nullptr, nullptr, W.hdr, W.part, 0.0, 0, s);
+    count_launch(SYM ? 7 : 2, s, false);
+    if (st != MFX_OK) return st;
+    count_launch(3, s, true);
+    k3<<<nb, kThreads, 0, s>>>(G, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part);
+    count_launch(3, s, false);
+    return MFX_OK;
+}
+
+template <bool SYM>
 void launch_iteration(const Geo &G, const Coef &c, const WsView &W, double *x, int parity, int nb, cudaStream_t s)
 {
     double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
@@ -349,6 +377,18 @@ thread_local HostScratch g_host;
 
 bool grid_valid(const mfx_grid *g, bool scalar);
 
+// MFX_KERNELS=v1 selects the simple grid-stride kernels (kept as an A/B
+// reference for tests and profiling); default is the TMA z-marching path.
+static bool use_tma()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MFX_KERNELS");
+        v = (e && e[0] == 'v' && e[1] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, cudaStream_t s)
 {
     if (!grid_valid(grid, kind == MFX_EQ_SCALAR)) return MFX_ERR_ARG;
@@ -357,6 +397,13 @@ mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double
     const Geo G = make_geo(*grid);
     const int nb = reduce_grid(G.N);
     count_launch(0, s, true);
+    if (use_tma()) {
+        const double *halo[3] = {x, nullptr, nullptr};
+        mfx_status st = stencil_launch(0, kind == MFX_EQ_PP, G, halo, A, nullptr, y, nullptr, nullptr, nullptr,
+                                       nullptr, 0.0, 0, s);
+        count_launch(0, s, false);
+        return st;
+    }
     if (kind == MFX_EQ_PP) k_spmv<true><<<nb, kThreads, 0, s>>>(G, coef_of(A), x, y);
     else k_spmv<false><<<nb, kThreads, 0, s>>>(G, coef_of(A), x, y);
     count_launch(0, s, false);
@@ -380,8 +427,15 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
     count_launch(0, s, true);
-    if (sym) k_setup<true><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
-    else k_setup<false><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
+    if (use_tma()) {
+        const double *h0[3] = {x, nullptr, nullptr};
+        mfx_status st = stencil_launch(1, sym, G, h0, A, A->b, W.r, nullptr, nullptr, W.hdr, W.part, tol, maxit, s);
+        if (st != MFX_OK) return st;
+    } else if (sym) {
+        k_setup<true><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
+    } else {
+        k_setup<false><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);
+    }
     count_launch(0, s, false);
     k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
     count_launch(8, s, false);
@@ -391,8 +445,15 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     while (launched < maxit) {
         const int cnt = maxit - launched < chunk ? maxit - launched : chunk;
         for (int q = 0; q < cnt; q++, launched++) {
-            if (sym) launch_iteration<true>(G, c, W, x, launched & 1, nb, s);
-            else launch_iteration<false>(G, c, W, x, launched & 1, nb, s);
+            if (use_tma()) {
+                mfx_status st = sym ? launch_iteration_tma<true>(G, A, W, x, launched & 1, nb, s)
+                                    : launch_iteration_tma<false>(G, A, W, x, launched & 1, nb, s);
+                if (st != MFX_OK) return st;
+            } else if (sym) {
+                launch_iteration<true>(G, c, W, x, launched & 1, nb, s);
+            } else {
+                launch_iteration<false>(G, c, W, x, launched & 1, nb, s);
+            }
         }
         MFX_CUDA_TRY(cudaGetLastError());
         if (!info) continue;

@@ -1,0 +1,549 @@
+// stencil_tma.cu -- the bandwidth-critical 7-point kernels of BiCGSTAB
+// (setup r = b - A x0, K1, K2, plain apply) as persistent TMA z-marching
+// kernels for sm_100a.
+//
+// Layout: fields are nx*ny*nz fp64, x fastest, described to the TMA unit as
+// 3-D tensors (16-byte row stride: nx even).  A CTA owns an x-y tile of
+// TX x TY cells and marches along z; every plane of every input array is
+// fetched by ONE cp.async.bulk.tensor per array into a ring of S shared-
+// memory stages (mbarrier complete_tx), S-2 planes ahead of the compute.
+// Arrays read with a stencil halo are fetched as (TX+4) x (TY+2) boxes whose
+// out-of-domain part the TMA zero-fills, which is exactly the boundary rule
+// of DESIGN.md §3.2 (x_nb = 0 outside the domain).
+//
+// Per plane:  step 1  value on the halo'd plane (x for the apply,
+//                     p = fma(beta, fma(-omega, v, p), r) for K1,
+//                     s = fma(-alpha, v, r) for K2) -> P ring (4 planes:
+//                     one barrier per plane suffices)
+//             sync; thread 0 refills the stage freed two planes ago
+//             step 2  y = A P at the plane below, canonical order
+//                     W,E,S,N,B,T, fused epilogue + correctly rounded dots.
+// Work is split into equal runs of (tile, plane) units over a persistent grid
+// (148 x CTAs/SM), so every SM streams the same number of planes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "common.cuh"
+
+namespace mfx {
+
+enum StencilMode { SM_SPMV = 0, SM_SETUP = 1, SM_K1 = 2, SM_K2 = 3 };
+
+struct TmaMaps {
+    CUtensorMap halo[3];   // halo box arrays (x | r,p_old,v_old | r,v)
+    CUtensorMap coef[7];   // SYM: aP, cz (cell), cx (x-halo box), cy (y-halo box); else aP,aW,aE,aS,aN,aB,aT
+    CUtensorMap extra;     // SETUP: b ; K1: r^
+};
+
+struct StencilArgs {
+    int nx, ny, nz;
+    int tiles_x, tiles_y;
+    long long units;                       // tiles * nz output planes
+    double *out0, *out1, *out2;            // SPMV: y | SETUP: r | K1: p_new, v_new, r^ | K2: t
+    WsHeader *h;
+    dd *part;
+    double tol;
+    int maxit;
+};
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+constexpr int r128(int b) { return (b + 127) & ~127; }
+
+template <int MODE, bool SYM, int TX, int TY>
+struct Cfg {
+    static constexpr int NT = 256;
+    static constexpr int HX = TX + 4, HY = TY + 2;        // halo box: x in [x0-2, x0+TX+2), y in [y0-1, y0+TY+1)
+    static constexpr int CPT = (TX * TY + NT - 1) / NT;    // owned cells per thread
+    static constexpr int NH = MODE == SM_K1 ? 3 : (MODE == SM_K2 ? 2 : 1);
+    static constexpr int NCELLC = SYM ? 2 : 7;             // coefficient arrays with the cell box
+    static constexpr int NE = (MODE == SM_SETUP || MODE == SM_K1) ? 1 : 0;
+    static constexpr int HALO_TX = HX * HY * 8, CELL_TX = TX * TY * 8;
+    static constexpr int XW_TX = HX * TY * 8, YS_TX = TX * (TY + 1) * 8;
+    static constexpr int HALO_B = r128(HALO_TX), CELL_B = r128(CELL_TX), XW_B = r128(XW_TX), YS_B = r128(YS_TX);
+    static constexpr int STAGE_TX = NH * HALO_TX + NCELLC * CELL_TX + (SYM ? XW_TX + YS_TX : 0) + NE * CELL_TX;
+    static constexpr int STAGE_B = NH * HALO_B + NCELLC * CELL_B + (SYM ? XW_B + YS_B : 0) + NE * CELL_B;
+    static constexpr int PBUF_B = r128(HX * HY * 8);
+    // stage offsets
+    static constexpr int OFF_HALO = 0;
+    static constexpr int OFF_CELL = NH * HALO_B;
+    static constexpr int OFF_XW = OFF_CELL + NCELLC * CELL_B;
+    static constexpr int OFF_YS = OFF_XW + (SYM ? XW_B : 0);
+    static constexpr int OFF_EXTRA = OFF_YS + (SYM ? YS_B : 0);
+    static constexpr int NDOT = MODE == SM_SPMV ? 0 : (MODE == SM_SETUP ? 2 : (MODE == SM_K1 ? 1 : 3));
+};
+
+template <class C>
+__host__ __device__ constexpr size_t smem_bytes(int S)
+{
+    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 128;
+}
+
+// plane-stream cursor over this CTA's units [u0, u1): segments of consecutive
+// planes of one tile; stream planes k0-1 .. k1 (virtual outside [0, nz)).
+struct Cursor {
+    long long unext, uend;
+    int tile, k, k0, k1;
+    bool valid;
+    __device__ void start(long long u, int nz)
+    {
+        if (u >= uend) { valid = false; return; }
+        tile = (int)(u / nz);
+        k0 = (int)(u - (long long)tile * nz);
+        long long left = uend - u;
+        k1 = (int)((long long)k0 + left < nz ? (long long)k0 + left : nz);
+        unext = u + (k1 - k0);
+        k = k0 - 1;
+        valid = true;
+    }
+    __device__ void init(long long u0, long long u1, int nz)
+    {
+        uend = u1;
+        start(u0, nz);
+    }
+    __device__ void advance(int nz)
+    {
+        k++;
+        if (k > k1) start(unext, nz);
+    }
+    __device__ bool is_virtual(int nz) const { return k < 0 || k >= nz; }
+    __device__ bool produces() const { return k >= k0 + 1; }
+};
+
+template <int MODE, bool SYM, int TX, int TY, int S>
+__device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, int tiles_x, uint8_t *stages,
+                                      uint64_t *full, long long q)
+{
+    using C = Cfg<MODE, SYM, TX, TY>;
+    const int s = (int)(q % S);
+    uint64_t *bar = &full[s];
+    if (c.is_virtual(nz)) {
+        mbar_arrive(bar);
+        return;
+    }
+    uint8_t *st = stages + (size_t)s * C::STAGE_B;
+    const int x0 = (c.tile % tiles_x) * TX, y0 = (c.tile / tiles_x) * TY, k = c.k;
+    mbar_arrive_expect_tx(bar, C::STAGE_TX);
+#pragma unroll
+    for (int a = 0; a < C::NH; a++) tma_load_3d(st + C::OFF_HALO + a * C::HALO_B, &M.halo[a], x0 - 2, y0 - 1, k, bar);
+#pragma unroll
+    for (int a = 0; a < C::NCELLC; a++) tma_load_3d(st + C::OFF_CELL + a * C::CELL_B, &M.coef[a], x0, y0, k, bar);
+    if (SYM) {
+        tma_load_3d(st + C::OFF_XW, &M.coef[2], x0 - 2, y0, k, bar);
+        tma_load_3d(st + C::OFF_YS, &M.coef[3], x0, y0 - 1, k, bar);
+    }
+    if (C::NE) tma_load_3d(st + C::OFF_EXTRA, &M.extra, x0, y0, k, bar);
+}
+
+template <int MODE, bool SYM, int TX, int TY, int S>
+__global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps M, StencilArgs a)
+{
+    using C = Cfg<MODE, SYM, TX, TY>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *stages = smem;
+    double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
+    uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + 4 * C::PBUF_B);
+    const int tid = threadIdx.x;
+
+    // ---- scalar prologue (uniform across the grid)
+    double beta = 0.0, omega = 0.0, alpha = 0.0, rho = 0.0, rhn = 0.0;
+    bool rst = false, newly = false;
+    if (MODE == SM_K1 || MODE == SM_K2) {
+        SolverScalars &Sc = a.h->sc;
+        if (Sc.done) return;
+        if (MODE == SM_K2 && Sc.skip) return;
+        if (MODE == SM_K1) {
+            rho = Sc.rho; rhn = Sc.rhn;
+            double rho_prev = Sc.rho_prev;
+            alpha = Sc.alpha; omega = Sc.omega;
+            const double rn = Sc.rn, rr = Sc.rr;
+            rst = Sc.restart_mode != 0;
+            if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
+            if (fabs(rho) <= (1e-14 * rhn) * rn) {
+                if (Sc.restarted) {
+                    if (blockIdx.x == 0 && tid == 0) { Sc.status = MFX_ERR_BREAKDOWN; Sc.done = 1; }
+                    return;
+                }
+                rst = true; newly = true;
+                rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
+            }
+            beta = (rho / rho_prev) * (alpha / omega);
+        } else {
+            alpha = Sc.alpha;
+        }
+    }
+
+    // ---- partition: equal runs of (tile, plane) units
+    const long long G = gridDim.x;
+    const long long u0 = a.units * blockIdx.x / G, u1 = a.units * (blockIdx.x + 1) / G;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
+    }
+    __syncthreads();
+
+    Cursor prod, cons;
+    long long qp = 0;
+    if (tid == 0) {
+        prod.init(u0, u1, a.nz);
+        for (; qp < S - 2 && prod.valid; qp++) {
+            issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, a.tiles_x, stages, full, qp);
+            prod.advance(a.nz);
+        }
+    }
+    cons.init(u0, u1, a.nz);
+
+    Acc acc[C::NDOT > 0 ? C::NDOT : 1];
+#pragma unroll
+    for (int d = 0; d < (C::NDOT > 0 ? C::NDOT : 1); d++) acc[d].zero();
+    double czq1[C::CPT], czq0[C::CPT];   // cz at planes q-1 (aT of output) and q-2 (aB of output)
+#pragma unroll
+    for (int m = 0; m < C::CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
+
+    for (long long q = 0; cons.valid; q++) {
+        const int s = (int)(q % S);
+        const bool virt = cons.is_virtual(a.nz);
+        const bool produce = cons.produces();
+        const int tile = cons.tile, kout = cons.k - 1;
+        const int x0 = (tile % a.tiles_x) * TX, y0 = (tile / a.tiles_x) * TY;
+        mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+        const uint8_t *st = stages + (size_t)s * C::STAGE_B;
+        double *P = pbuf + (size_t)(q % 4) * (C::PBUF_B / 8);
+
+        // step 1: value on the halo'd plane
+        for (int idx = tid; idx < C::HX * C::HY; idx += C::NT) {
+            double val = 0.0;
+            if (!virt) {
+                const double *h0 = (const double *)(st + C::OFF_HALO);
+                if (MODE == SM_SPMV || MODE == SM_SETUP) {
+                    val = h0[idx];
+                } else if (MODE == SM_K1) {
+                    const double rv = h0[idx];
+                    const double pv = ((const double *)(st + C::OFF_HALO + C::HALO_B))[idx];
+                    const double vv = ((const double *)(st + C::OFF_HALO + 2 * C::HALO_B))[idx];
+                    val = rst ? fma(beta, fma(-omega, 0.0, 0.0), rv) : fma(beta, fma(-omega, vv, pv), rv);
+                } else {
+                    const double rv = h0[idx];
+                    const double vv = ((const double *)(st + C::OFF_HALO + C::HALO_B))[idx];
+                    val = fma(-alpha, vv, rv);
+                }
+            }
+            P[idx] = val;
+        }
+        // cz queue (SYM): aT of output plane q-1 is cz(q-1); aB is cz(q-2)
+        double czcur[C::CPT];
+        if (SYM) {
+#pragma unroll
+            for (int m = 0; m < C::CPT; m++) {
+                const int idx = tid + m * C::NT;
+                czcur[m] = (!virt && idx < TX * TY) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[idx] : 0.0;
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && prod.valid) {
+            issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, a.tiles_x, stages, full, qp);
+            prod.advance(a.nz);
+            qp++;
+        }
+        // step 2: output plane kout = k(q) - 1
+        if (produce) {
+            const uint8_t *so = stages + (size_t)((q + S - 1) % S) * C::STAGE_B;   // stage of plane q-1
+            const double *Pc = pbuf + (size_t)((q + 3) % 4) * (C::PBUF_B / 8);      // plane q-1
+            const double *Pb = pbuf + (size_t)((q + 2) % 4) * (C::PBUF_B / 8);      // plane q-2
+            const double *Pt = P;                                                   // plane q
+#pragma unroll
+            for (int m = 0; m < C::CPT; m++) {
+                const int idx = tid + m * C::NT;
+                if (idx >= TX * TY) break;
+                const int cx = idx % TX, cy = idx / TX;
+                const int gx = x0 + cx, gy = y0 + cy;
+                const bool active = gx < a.nx && gy < a.ny;
+                const int hc = (cy + 1) * C::HX + (cx + 2);
+                double aP, aW, aE, aS, aN, aB, aT;
+                const double *cell = (const double *)(so + C::OFF_CELL);
+                if (SYM) {
+                    aP = cell[idx];
+                    const double *xw = (const double *)(so + C::OFF_XW);
+                    const double *ys = (const double *)(so + C::OFF_YS);
+                    aW = xw[cy * C::HX + cx + 1];
+                    aE = xw[cy * C::HX + cx + 2];
+                    aS = ys[cy * TX + cx];
+                    aN = ys[(cy + 1) * TX + cx];
+                    aB = czq0[m];
+                    aT = czq1[m];
+                } else {
+                    aP = cell[idx];
+                    aW = cell[1 * (C::CELL_B / 8) + idx];
+                    aE = cell[2 * (C::CELL_B / 8) + idx];
+                    aS = cell[3 * (C::CELL_B / 8) + idx];
+                    aN = cell[4 * (C::CELL_B / 8) + idx];
+                    aB = cell[5 * (C::CELL_B / 8) + idx];
+                    aT = cell[6 * (C::CELL_B / 8) + idx];
+                }
+                const double xc = Pc[hc];
+                double y = aP * xc;
+                y = fma(-aW, Pc[hc - 1], y);
+                y = fma(-aE, Pc[hc + 1], y);
+                y = fma(-aS, Pc[hc - C::HX], y);
+                y = fma(-aN, Pc[hc + C::HX], y);
+                y = fma(-aB, Pb[hc], y);
+                y = fma(-aT, Pt[hc], y);
+                if (active) {
+                    const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
+                    if (MODE == SM_SPMV) {
+                        a.out0[n] = y;
+                    } else if (MODE == SM_SETUP) {
+                        const double bv = ((const double *)(so + C::OFF_EXTRA))[idx];
+                        const double rv = bv - y;
+                        a.out0[n] = rv;
+                        acc[0].prod(bv, bv);
+                        acc[1].prod(rv, rv);
+                    } else if (MODE == SM_K1) {
+                        a.out0[n] = xc;   // p_new
+                        a.out1[n] = y;    // v_new
+                        double rhv;
+                        if (rst) {
+                            rhv = ((const double *)(so + C::OFF_HALO))[hc];   // r at the cell
+                            a.out2[n] = rhv;
+                        } else {
+                            rhv = ((const double *)(so + C::OFF_EXTRA))[idx];
+                        }
+                        acc[0].prod(rhv, y);
+                    } else {
+                        a.out0[n] = y;    // t
+                        acc[0].prod(y, xc);
+                        acc[1].prod(y, y);
+                        acc[2].prod(xc, xc);
+                    }
+                }
+            }
+        }
+        if (SYM) {
+#pragma unroll
+            for (int m = 0; m < C::CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
+        }
+        cons.advance(a.nz);
+    }
+
+    if (C::NDOT == 0) return;
+    __syncthreads();
+    constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
+    __shared__ dd sh[8 * ND];
+    dd v[ND], out[ND];
+#pragma unroll
+    for (int d = 0; d < ND; d++) v[d] = acc[d].get();
+    if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+    SolverScalars &Sc = a.h->sc;
+    if (MODE == SM_SETUP) {
+        const double bn = sqrt(dd_round(out[0]));
+        const double rrv = dd_round(out[1]);
+        Sc.tol = a.tol; Sc.maxit = a.maxit; Sc.bn = bn; Sc.rr = rrv; Sc.rn = sqrt(rrv);
+        Sc.it = 0; Sc.status = MFX_NOT_CONVERGED; Sc.done = 0; Sc.restarted = 0; Sc.restarts = 0;
+        Sc.restart_mode = 1; Sc.skip = 0; Sc.half = 0; Sc.zero_x = 0;
+        Sc.rho = rrv; Sc.rhn = Sc.rn; Sc.rho_prev = 1.0; Sc.alpha = 1.0; Sc.omega = 1.0;
+        if (bn == 0.0) { Sc.zero_x = 1; Sc.done = 1; Sc.status = MFX_OK; Sc.rn = 0.0; }
+        else if (Sc.rn <= a.tol * bn) { Sc.done = 1; Sc.status = MFX_OK; }
+        else if (a.maxit <= 0) { Sc.done = 1; }
+    } else if (MODE == SM_K1) {
+        if (rst) { Sc.rho = rho; Sc.rhn = rhn; Sc.rho_prev = 1.0; Sc.alpha = 1.0; Sc.omega = 1.0; }
+        if (newly) { Sc.restarted = 1; Sc.restarts += 1; }
+        Sc.restart_mode = 0;
+        Sc.skip = 0;
+        const double sigma = dd_round(out[0]);
+        Sc.sigma = sigma;
+        if (sigma == 0.0) {
+            if (Sc.restarted) { Sc.status = MFX_ERR_BREAKDOWN; Sc.it += 1; Sc.done = 1; }
+            else {
+                Sc.restarted = 1; Sc.restarts += 1; Sc.restart_mode = 1; Sc.skip = 1; Sc.it += 1;
+                if (Sc.it >= Sc.maxit) { Sc.status = MFX_NOT_CONVERGED; Sc.done = 1; }
+            }
+        } else {
+            Sc.alpha = rho / sigma;
+        }
+    } else if (MODE == SM_K2) {
+        const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
+        Sc.ts = tsv; Sc.tt = ttv; Sc.ss = ssv;
+        if (sqrt(ssv) <= Sc.tol * Sc.bn) {
+            Sc.half = 1;
+        } else {
+            const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
+            if (ttv == 0.0 || om == 0.0) {
+                if (Sc.restarted) { Sc.status = MFX_ERR_BREAKDOWN; Sc.it += 1; Sc.done = 1; }
+                else {
+                    Sc.restarted = 1; Sc.restarts += 1; Sc.restart_mode = 1; Sc.skip = 1; Sc.it += 1;
+                    if (Sc.it >= Sc.maxit) { Sc.status = MFX_NOT_CONVERGED; Sc.done = 1; }
+                }
+            } else {
+                Sc.omega = om;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool get_encode()
+{
+    if (g_encode) return true;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return true;
+}
+
+bool make_map(CUtensorMap *m, const double *ptr, int nx, int ny, int nz, int bx, int by)
+{
+    if (!ptr) { memset(m, 0, sizeof(*m)); return true; }
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)ptr, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d) for box %dx%d", (int)r, bx, by);
+        return false;
+    }
+    return true;
+}
+
+template <int MODE, bool SYM, int TX, int TY, int S>
+struct Launcher {
+    using C = Cfg<MODE, SYM, TX, TY>;
+    static int grid_size()
+    {
+        static int g = 0;
+        if (g) return g;
+        const size_t sm = smem_bytes<C>(S);
+        cudaFuncSetAttribute(k_stencil<MODE, SYM, TX, TY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, S>, 256, sm);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g = sms * (occ > 0 ? occ : 1);
+        if (g > kMaxBlocks) g = kMaxBlocks;
+        return g;
+    }
+    static mfx_status run(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
+                          const StencilArgs &args0, cudaStream_t s)
+    {
+        if (!get_encode()) return MFX_ERR_CUDA;
+        TmaMaps M;
+        memset(&M, 0, sizeof(M));
+        for (int q = 0; q < C::NH; q++)
+            if (!make_map(&M.halo[q], halo[q], G.nx, G.ny, G.nz, C::HX, C::HY)) return MFX_ERR_CUDA;
+        for (int q = 0; q < C::NCELLC; q++)
+            if (!make_map(&M.coef[q], coef[q], G.nx, G.ny, G.nz, TX, TY)) return MFX_ERR_CUDA;
+        if (SYM) {
+            if (!make_map(&M.coef[2], coef[2], G.nx, G.ny, G.nz, C::HX, TY)) return MFX_ERR_CUDA;
+            if (!make_map(&M.coef[3], coef[3], G.nx, G.ny, G.nz, TX, TY + 1)) return MFX_ERR_CUDA;
+        }
+        if (C::NE && !make_map(&M.extra, extra, G.nx, G.ny, G.nz, TX, TY)) return MFX_ERR_CUDA;
+        StencilArgs a = args0;
+        a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
+        a.tiles_x = (G.nx + TX - 1) / TX;
+        a.tiles_y = (G.ny + TY - 1) / TY;
+        a.units = (long long)a.tiles_x * a.tiles_y * G.nz;
+        int grid = grid_size();
+        if (grid > a.units) grid = (int)a.units;
+        k_stencil<MODE, SYM, TX, TY, S><<<grid, 256, smem_bytes<C>(S), s>>>(M, a);
+        MFX_CUDA_TRY(cudaGetLastError());
+        return MFX_OK;
+    }
+};
+
+template <int MODE, bool SYM>
+mfx_status run_mode(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
+                    const StencilArgs &a, cudaStream_t s)
+{
+    constexpr int S = (MODE == SM_K1 && !SYM) ? 3 : 4;
+    if (G.nx <= 32) return Launcher<MODE, SYM, 32, 8, S>::run(G, halo, coef, extra, a, s);
+    return Launcher<MODE, SYM, 64, 4, S>::run(G, halo, coef, extra, a, s);
+}
+
+}  // namespace
+
+// coefficient order for the maps: SYM -> {aP, cz, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
+mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],
+                          const mfx_eqsys *A, const double *extra, double *o0, double *o1, double *o2,
+                          WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s)
+{
+    const double *coef[7];
+    if (sym) {
+        coef[0] = A->aP; coef[1] = A->aT; coef[2] = A->aE; coef[3] = A->aN;
+        coef[4] = coef[5] = coef[6] = nullptr;
+    } else {
+        coef[0] = A->aP; coef[1] = A->aW; coef[2] = A->aE; coef[3] = A->aS;
+        coef[4] = A->aN; coef[5] = A->aB; coef[6] = A->aT;
+    }
+    StencilArgs a;
+    memset(&a, 0, sizeof(a));
+    a.out0 = o0; a.out1 = o1; a.out2 = o2; a.h = h; a.part = part; a.tol = tol; a.maxit = maxit;
+    switch (mode * 2 + (sym ? 1 : 0)) {
+    case SM_SPMV * 2 + 0: return run_mode<SM_SPMV, false>(G, halo, coef, extra, a, s);
+    case SM_SPMV * 2 + 1: return run_mode<SM_SPMV, true>(G, halo, coef, extra, a, s);
+    case SM_SETUP * 2 + 0: return run_mode<SM_SETUP, false>(G, halo, coef, extra, a, s);
+    case SM_SETUP * 2 + 1: return run_mode<SM_SETUP, true>(G, halo, coef, extra, a, s);
+    case SM_K1 * 2 + 0: return run_mode<SM_K1, false>(G, halo, coef, extra, a, s);
+    case SM_K1 * 2 + 1: return run_mode<SM_K1, true>(G, halo, coef, extra, a, s);
+    case SM_K2 * 2 + 0: return run_mode<SM_K2, false>(G, halo, coef, extra, a, s);
+    case SM_K2 * 2 + 1: return run_mode<SM_K2, true>(G, halo, coef, extra, a, s);
+    }
+    set_error("bad stencil mode");
+    return MFX_ERR_ARG;
+}
+
+}  // namespace mfx

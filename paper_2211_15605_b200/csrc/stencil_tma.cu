@@ -18,11 +18,13 @@
 //             sync; thread 0 refills the stage freed two planes ago
 //             step 2  y = A P at the plane below, canonical order
 //                     W,E,S,N,B,T, fused epilogue + correctly rounded dots.
-// Work is split into equal runs of (tile, plane) units over a persistent grid
-// (148 x CTAs/SM), so every SM streams the same number of planes.
+// Work is split into (z-chunk, tile) units dealt round-robin over a persistent
+// grid (148 x CTAs/SM) so neighbouring tiles march in lockstep (L2 reuse of
+// the halo rows) and every SM streams about the same number of planes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -40,7 +42,8 @@ struct TmaMaps {
 struct StencilArgs {
     int nx, ny, nz;
     int tiles_x, tiles_y;
-    long long units;                       // tiles * nz output planes
+    int Lz;                                // z-chunk length
+    long long units;                       // tiles * ceil(nz / Lz) work units
     double *out0, *out1, *out2;            // SPMV: y | SETUP: r | K1: p_new, v_new, r^ | K2: t
     WsHeader *h;
     dd *part;
@@ -121,32 +124,36 @@ __host__ __device__ constexpr size_t smem_bytes(int S)
     return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 128;
 }
 
-// plane-stream cursor over this CTA's units [u0, u1): segments of consecutive
-// planes of one tile; stream planes k0-1 .. k1 (virtual outside [0, nz)).
+// plane-stream cursor.  Units are (z-chunk, tile) pairs in chunk-major order,
+// dealt round-robin to the persistent CTAs (unit u -> CTA u % G), so at any
+// time all CTAs work on the same slab of ~G/ntiles chunks: a tile's y/x halo
+// rows and its chunk-boundary planes are fetched by the neighbouring CTAs at
+// the same moment and hit in L2.  A unit streams planes k0-1 .. k1
+// (virtual, i.e. zero, outside [0, nz)) and outputs planes k0 .. k1-1.
 struct Cursor {
-    long long unext, uend;
+    long long u, units;
+    int G, ntiles, Lz;
     int tile, k, k0, k1;
     bool valid;
-    __device__ void start(long long u, int nz)
+    __device__ void start(int nz)
     {
-        if (u >= uend) { valid = false; return; }
-        tile = (int)(u / nz);
-        k0 = (int)(u - (long long)tile * nz);
-        long long left = uend - u;
-        k1 = (int)((long long)k0 + left < nz ? (long long)k0 + left : nz);
-        unext = u + (k1 - k0);
+        if (u >= units) { valid = false; return; }
+        const int chunk = (int)(u / ntiles);
+        tile = (int)(u - (long long)chunk * ntiles);
+        k0 = chunk * Lz;
+        k1 = k0 + Lz < nz ? k0 + Lz : nz;
         k = k0 - 1;
         valid = true;
     }
-    __device__ void init(long long u0, long long u1, int nz)
+    __device__ void init(long long u0, long long nunits, int g, int nt, int lz, int nz)
     {
-        uend = u1;
-        start(u0, nz);
+        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz;
+        start(nz);
     }
     __device__ void advance(int nz)
     {
         k++;
-        if (k > k1) start(unext, nz);
+        if (k > k1) { u += G; start(nz); }
     }
     __device__ bool is_virtual(int nz) const { return k < 0 || k >= nz; }
     __device__ bool produces() const { return k >= k0 + 1; }
@@ -215,9 +222,7 @@ __global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps
         }
     }
 
-    // ---- partition: equal runs of (tile, plane) units
-    const long long G = gridDim.x;
-    const long long u0 = a.units * blockIdx.x / G, u1 = a.units * (blockIdx.x + 1) / G;
+    const int ntiles = a.tiles_x * a.tiles_y;
 
     if (tid == 0) {
         for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
@@ -230,13 +235,13 @@ __global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps
     Cursor prod, cons;
     long long qp = 0;
     if (tid == 0) {
-        prod.init(u0, u1, a.nz);
+        prod.init(blockIdx.x, a.units, gridDim.x, ntiles, a.Lz, a.nz);
         for (; qp < S - 2 && prod.valid; qp++) {
             issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, a.tiles_x, stages, full, qp);
             prod.advance(a.nz);
         }
     }
-    cons.init(u0, u1, a.nz);
+    cons.init(blockIdx.x, a.units, gridDim.x, ntiles, a.Lz, a.nz);
 
     Acc acc[C::NDOT > 0 ? C::NDOT : 1];
 #pragma unroll
@@ -459,6 +464,28 @@ bool make_map(CUtensorMap *m, const double *ptr, int nx, int ny, int nz, int bx,
     return true;
 }
 
+// z-chunk length: minimise rounds * (Lz + 2) (the +2 boundary planes of a
+// chunk are L2 hits, counted as full planes to stay conservative);
+// MFX_LZ overrides for tuning.
+int choose_lz(long long ntiles, int nz, int grid)
+{
+    static int env = -2;
+    if (env == -2) {
+        const char *e = getenv("MFX_LZ");
+        env = e ? atoi(e) : -1;
+    }
+    if (env > 0) return env < nz ? env : nz;
+    int best = nz;
+    double best_cost = 1e300;
+    for (int lz = 4; lz <= nz; lz++) {
+        const long long units = ntiles * ((nz + lz - 1) / lz);
+        const long long rounds = (units + grid - 1) / grid;
+        const double cost = (double)rounds * (lz + 2);
+        if (cost < best_cost - 1e-9) { best_cost = cost; best = lz; }
+    }
+    return best;
+}
+
 template <int MODE, bool SYM, int TX, int TY, int S>
 struct Launcher {
     using C = Cfg<MODE, SYM, TX, TY>;
@@ -496,8 +523,10 @@ struct Launcher {
         a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
         a.tiles_x = (G.nx + TX - 1) / TX;
         a.tiles_y = (G.ny + TY - 1) / TY;
-        a.units = (long long)a.tiles_x * a.tiles_y * G.nz;
         int grid = grid_size();
+        const long long ntiles = (long long)a.tiles_x * a.tiles_y;
+        a.Lz = choose_lz(ntiles, G.nz, grid);
+        a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
         if (grid > a.units) grid = (int)a.units;
         k_stencil<MODE, SYM, TX, TY, S><<<grid, 256, smem_bytes<C>(S), s>>>(M, a);
         MFX_CUDA_TRY(cudaGetLastError());

@@ -30,7 +30,12 @@ else:
     sysd, _ = mfx.assemble_eq(mfx.EQ_W, g, pr, sd, ws)
     kind = mfx.EQ_W
 torch.cuda.synchronize()
+N = g.n
+BPC = {"K1_pp": 80, "K2_pp": 56, "K3": 64, "K1_mom": 104, "K2_mom": 80, "spmv_setup": None}
 for r in range(args.repeat):
+    if r == args.repeat - 1:
+        mfx.prof_reset()
+        mfx.prof_enable(True)
     x = torch.zeros(g.n, dtype=torch.float64, device="cuda")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -38,4 +43,13 @@ for r in range(args.repeat):
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    print(f"{args.kind} iters={info['iters']} ms={ms:.3f} us/iter={1e3 * ms / max(info['iters'], 1):.1f}")
+    print(f"{args.kind} iters={info['iters']} ms={ms:.3f} us/iter={1e3 * ms / max(info['iters'], 1):.1f}", flush=True)
+mfx.prof_enable(False)
+pr_ = mfx.prof_read()
+line = []
+for k, v in pr_.items():
+    if v["launches"]:
+        us = 1e3 * v["ms"] / v["launches"]
+        bw = f" {BPC[k] * N / (us * 1e-6) / 1e9:.0f}GB/s" if BPC.get(k) else ""
+        line.append(f"{k}:{us:.1f}us{bw}")
+print("   kernels: " + "  ".join(line), flush=True)

@@ -121,7 +121,7 @@ struct Cfg {
 template <class C>
 __host__ __device__ constexpr size_t smem_bytes(int S)
 {
-    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 128;
+    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 16 * (size_t)S;
 }
 
 // plane-stream cursor.  Units are (z-chunk, tile) pairs in chunk-major order,
@@ -131,23 +131,26 @@ __host__ __device__ constexpr size_t smem_bytes(int S)
 // the same moment and hit in L2.  A unit streams planes k0-1 .. k1
 // (virtual, i.e. zero, outside [0, nz)) and outputs planes k0 .. k1-1.
 struct Cursor {
-    long long u, units;
-    int G, ntiles, Lz;
-    int tile, k, k0, k1;
+    int u, units;
+    int G, ntiles, Lz, tiles_x, TX, TY;
+    int x0, y0, k, k0, k1;
     bool valid;
     __device__ void start(int nz)
     {
         if (u >= units) { valid = false; return; }
-        const int chunk = (int)(u / ntiles);
-        tile = (int)(u - (long long)chunk * ntiles);
+        const int chunk = u / ntiles;
+        const int tile = u - chunk * ntiles;
+        const int ty = tile / tiles_x;
+        x0 = (tile - ty * tiles_x) * TX;
+        y0 = ty * TY;
         k0 = chunk * Lz;
         k1 = k0 + Lz < nz ? k0 + Lz : nz;
         k = k0 - 1;
         valid = true;
     }
-    __device__ void init(long long u0, long long nunits, int g, int nt, int lz, int nz)
+    __device__ void init(int u0, int nunits, int g, int nt, int lz, int tx, int tX, int tY, int nz)
     {
-        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz;
+        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz; tiles_x = tx; TX = tX; TY = tY;
         start(nz);
     }
     __device__ void advance(int nz)
@@ -160,18 +163,18 @@ struct Cursor {
 };
 
 template <int MODE, bool SYM, int TX, int TY, int S>
-__device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, int tiles_x, uint8_t *stages,
-                                      uint64_t *full, long long q)
+__device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, uint8_t *stages, uint64_t *full,
+                                      int q)
 {
     using C = Cfg<MODE, SYM, TX, TY>;
-    const int s = (int)(q % S);
+    const int s = q % S;
     uint64_t *bar = &full[s];
     if (c.is_virtual(nz)) {
         mbar_arrive(bar);
         return;
     }
     uint8_t *st = stages + (size_t)s * C::STAGE_B;
-    const int x0 = (c.tile % tiles_x) * TX, y0 = (c.tile / tiles_x) * TY, k = c.k;
+    const int x0 = c.x0, y0 = c.y0, k = c.k;
     mbar_arrive_expect_tx(bar, C::STAGE_TX);
 #pragma unroll
     for (int a = 0; a < C::NH; a++) tma_load_3d(st + C::OFF_HALO + a * C::HALO_B, &M.halo[a], x0 - 2, y0 - 1, k, bar);
@@ -185,14 +188,17 @@ __device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz,
 }
 
 template <int MODE, bool SYM, int TX, int TY, int S>
-__global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps M, StencilArgs a)
+__global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps M, StencilArgs a)
 {
+    // warps 0-7: consumers (one owned cell per thread); warp 8: TMA producer
     using C = Cfg<MODE, SYM, TX, TY>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *stages = smem;
     double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
     uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + 4 * C::PBUF_B);
+    uint64_t *empty = full + S;
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
 
     // ---- scalar prologue (uniform across the grid)
     double beta = 0.0, omega = 0.0, alpha = 0.0, rho = 0.0, rhn = 0.0;
@@ -223,112 +229,108 @@ __global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps
     }
 
     const int ntiles = a.tiles_x * a.tiles_y;
-
     if (tid == 0) {
-        for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 8);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
     }
     __syncthreads();
 
-    Cursor prod, cons;
-    long long qp = 0;
-    if (tid == 0) {
-        prod.init(blockIdx.x, a.units, gridDim.x, ntiles, a.Lz, a.nz);
-        for (; qp < S - 2 && prod.valid; qp++) {
-            issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, a.tiles_x, stages, full, qp);
-            prod.advance(a.nz);
+    constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
+    Acc acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; d++) acc[d].zero();
+
+    if (warp == 8) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
+            Cursor prod;
+            prod.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz);
+            for (int q = 0; prod.valid; q++) {
+                if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
+                issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, stages, full, q);
+                prod.advance(a.nz);
+            }
         }
-    }
-    cons.init(blockIdx.x, a.units, gridDim.x, ntiles, a.Lz, a.nz);
+    } else {
+        // ------------------------------------------------ consumer warps
+        Cursor cons;
+        cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz);
+        double czq1 = 0.0, czq0 = 0.0;   // cz at planes q-1 (aT of output) and q-2 (aB of output)
+        const int cx = tid % TX, cy = tid / TX;
+        const int hc = (cy + 1) * C::HX + (cx + 2);
+        for (int q = 0; cons.valid; q++) {
+            const int s = q % S;
+            const bool virt = cons.is_virtual(a.nz);
+            const bool produce = cons.produces();
+            const int kout = cons.k - 1;
+            const int x0 = cons.x0, y0 = cons.y0;
+            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+            const uint8_t *st = stages + (size_t)s * C::STAGE_B;
+            double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
-    Acc acc[C::NDOT > 0 ? C::NDOT : 1];
-#pragma unroll
-    for (int d = 0; d < (C::NDOT > 0 ? C::NDOT : 1); d++) acc[d].zero();
-    double czq1[C::CPT], czq0[C::CPT];   // cz at planes q-1 (aT of output) and q-2 (aB of output)
-#pragma unroll
-    for (int m = 0; m < C::CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
-
-    for (long long q = 0; cons.valid; q++) {
-        const int s = (int)(q % S);
-        const bool virt = cons.is_virtual(a.nz);
-        const bool produce = cons.produces();
-        const int tile = cons.tile, kout = cons.k - 1;
-        const int x0 = (tile % a.tiles_x) * TX, y0 = (tile / a.tiles_x) * TY;
-        mbar_wait(&full[s], (uint32_t)((q / S) & 1));
-        const uint8_t *st = stages + (size_t)s * C::STAGE_B;
-        double *P = pbuf + (size_t)(q % 4) * (C::PBUF_B / 8);
-
-        // step 1: value on the halo'd plane
-        for (int idx = tid; idx < C::HX * C::HY; idx += C::NT) {
-            double val = 0.0;
-            if (!virt) {
-                const double *h0 = (const double *)(st + C::OFF_HALO);
-                if (MODE == SM_SPMV || MODE == SM_SETUP) {
-                    val = h0[idx];
-                } else if (MODE == SM_K1) {
-                    const double rv = h0[idx];
-                    const double pv = ((const double *)(st + C::OFF_HALO + C::HALO_B))[idx];
-                    const double vv = ((const double *)(st + C::OFF_HALO + 2 * C::HALO_B))[idx];
-                    val = rst ? fma(beta, fma(-omega, 0.0, 0.0), rv) : fma(beta, fma(-omega, vv, pv), rv);
-                } else {
-                    const double rv = h0[idx];
-                    const double vv = ((const double *)(st + C::OFF_HALO + C::HALO_B))[idx];
-                    val = fma(-alpha, vv, rv);
+            // step 1: value on the halo'd plane, two x-adjacent cells per thread
+            for (int pi = tid; pi < C::HX * C::HY / 2; pi += 256) {
+                double2 val = make_double2(0.0, 0.0);
+                if (!virt) {
+                    const double2 *h0 = (const double2 *)(st + C::OFF_HALO);
+                    if (MODE == SM_SPMV || MODE == SM_SETUP) {
+                        val = h0[pi];
+                    } else if (MODE == SM_K1) {
+                        const double2 rv = h0[pi];
+                        const double2 pv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
+                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + 2 * C::HALO_B))[pi];
+                        if (rst) {
+                            val.x = fma(beta, fma(-omega, 0.0, 0.0), rv.x);
+                            val.y = fma(beta, fma(-omega, 0.0, 0.0), rv.y);
+                        } else {
+                            val.x = fma(beta, fma(-omega, vv.x, pv.x), rv.x);
+                            val.y = fma(beta, fma(-omega, vv.y, pv.y), rv.y);
+                        }
+                    } else {
+                        const double2 rv = h0[pi];
+                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
+                        val.x = fma(-alpha, vv.x, rv.x);
+                        val.y = fma(-alpha, vv.y, rv.y);
+                    }
                 }
+                ((double2 *)P)[pi] = val;
             }
-            P[idx] = val;
-        }
-        // cz queue (SYM): aT of output plane q-1 is cz(q-1); aB is cz(q-2)
-        double czcur[C::CPT];
-        if (SYM) {
-#pragma unroll
-            for (int m = 0; m < C::CPT; m++) {
-                const int idx = tid + m * C::NT;
-                czcur[m] = (!virt && idx < TX * TY) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[idx] : 0.0;
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && prod.valid) {
-            issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, a.tiles_x, stages, full, qp);
-            prod.advance(a.nz);
-            qp++;
-        }
-        // step 2: output plane kout = k(q) - 1
-        if (produce) {
-            const uint8_t *so = stages + (size_t)((q + S - 1) % S) * C::STAGE_B;   // stage of plane q-1
-            const double *Pc = pbuf + (size_t)((q + 3) % 4) * (C::PBUF_B / 8);      // plane q-1
-            const double *Pb = pbuf + (size_t)((q + 2) % 4) * (C::PBUF_B / 8);      // plane q-2
-            const double *Pt = P;                                                   // plane q
-#pragma unroll
-            for (int m = 0; m < C::CPT; m++) {
-                const int idx = tid + m * C::NT;
-                if (idx >= TX * TY) break;
-                const int cx = idx % TX, cy = idx / TX;
+            double czcur = 0.0;
+            if (SYM && !virt) czcur = ((const double *)(st + C::OFF_CELL + C::CELL_B))[tid];
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+
+            // step 2: output plane kout = k(q) - 1 (stage of plane q-1)
+            if (produce) {
+                const uint8_t *so = stages + (size_t)((q + S - 1) % S) * C::STAGE_B;
+                const double *Pc = pbuf + (size_t)((q + 3) & 3) * (C::PBUF_B / 8);   // plane q-1
+                const double *Pb = pbuf + (size_t)((q + 2) & 3) * (C::PBUF_B / 8);   // plane q-2
+                const double *Pt = P;                                                // plane q
                 const int gx = x0 + cx, gy = y0 + cy;
                 const bool active = gx < a.nx && gy < a.ny;
-                const int hc = (cy + 1) * C::HX + (cx + 2);
                 double aP, aW, aE, aS, aN, aB, aT;
                 const double *cell = (const double *)(so + C::OFF_CELL);
+                aP = cell[tid];
                 if (SYM) {
-                    aP = cell[idx];
                     const double *xw = (const double *)(so + C::OFF_XW);
                     const double *ys = (const double *)(so + C::OFF_YS);
                     aW = xw[cy * C::HX + cx + 1];
                     aE = xw[cy * C::HX + cx + 2];
                     aS = ys[cy * TX + cx];
                     aN = ys[(cy + 1) * TX + cx];
-                    aB = czq0[m];
-                    aT = czq1[m];
+                    aB = czq0;
+                    aT = czq1;
                 } else {
-                    aP = cell[idx];
-                    aW = cell[1 * (C::CELL_B / 8) + idx];
-                    aE = cell[2 * (C::CELL_B / 8) + idx];
-                    aS = cell[3 * (C::CELL_B / 8) + idx];
-                    aN = cell[4 * (C::CELL_B / 8) + idx];
-                    aB = cell[5 * (C::CELL_B / 8) + idx];
-                    aT = cell[6 * (C::CELL_B / 8) + idx];
+                    aW = cell[1 * (C::CELL_B / 8) + tid];
+                    aE = cell[2 * (C::CELL_B / 8) + tid];
+                    aS = cell[3 * (C::CELL_B / 8) + tid];
+                    aN = cell[4 * (C::CELL_B / 8) + tid];
+                    aB = cell[5 * (C::CELL_B / 8) + tid];
+                    aT = cell[6 * (C::CELL_B / 8) + tid];
                 }
                 const double xc = Pc[hc];
                 double y = aP * xc;
@@ -343,11 +345,11 @@ __global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps
                     if (MODE == SM_SPMV) {
                         a.out0[n] = y;
                     } else if (MODE == SM_SETUP) {
-                        const double bv = ((const double *)(so + C::OFF_EXTRA))[idx];
+                        const double bv = ((const double *)(so + C::OFF_EXTRA))[tid];
                         const double rv = bv - y;
                         a.out0[n] = rv;
                         acc[0].prod(bv, bv);
-                        acc[1].prod(rv, rv);
+                        acc[ND > 1 ? 1 : 0].prod(rv, rv);
                     } else if (MODE == SM_K1) {
                         a.out0[n] = xc;   // p_new
                         a.out1[n] = y;    // v_new
@@ -356,29 +358,27 @@ __global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ TmaMaps
                             rhv = ((const double *)(so + C::OFF_HALO))[hc];   // r at the cell
                             a.out2[n] = rhv;
                         } else {
-                            rhv = ((const double *)(so + C::OFF_EXTRA))[idx];
+                            rhv = ((const double *)(so + C::OFF_EXTRA))[tid];
                         }
                         acc[0].prod(rhv, y);
                     } else {
                         a.out0[n] = y;    // t
                         acc[0].prod(y, xc);
-                        acc[1].prod(y, y);
-                        acc[2].prod(xc, xc);
+                        acc[ND > 1 ? 1 : 0].prod(y, y);
+                        acc[ND > 2 ? 2 : 0].prod(xc, xc);
                     }
                 }
             }
+            // stage of plane q-1 is no longer read: release it to the producer
+            __syncwarp();
+            if (q >= 1 && lane == 0) mbar_arrive(&empty[(q + S - 1) % S]);
+            if (SYM) { czq0 = czq1; czq1 = czcur; }
+            cons.advance(a.nz);
         }
-        if (SYM) {
-#pragma unroll
-            for (int m = 0; m < C::CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
-        }
-        cons.advance(a.nz);
     }
 
     if (C::NDOT == 0) return;
-    __syncthreads();
-    constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
-    __shared__ dd sh[8 * ND];
+    __shared__ dd sh[9 * ND];
     dd v[ND], out[ND];
 #pragma unroll
     for (int d = 0; d < ND; d++) v[d] = acc[d].get();
@@ -496,7 +496,7 @@ struct Launcher {
         const size_t sm = smem_bytes<C>(S);
         cudaFuncSetAttribute(k_stencil<MODE, SYM, TX, TY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, S>, 256, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, S>, 288, sm);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -528,19 +528,38 @@ struct Launcher {
         a.Lz = choose_lz(ntiles, G.nz, grid);
         a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
         if (grid > a.units) grid = (int)a.units;
-        k_stencil<MODE, SYM, TX, TY, S><<<grid, 256, smem_bytes<C>(S), s>>>(M, a);
+        k_stencil<MODE, SYM, TX, TY, S><<<grid, 288, smem_bytes<C>(S), s>>>(M, a);
         MFX_CUDA_TRY(cudaGetLastError());
         return MFX_OK;
     }
 };
 
+// MFX_TILE=32x8 / 64x4 and MFX_STAGES=3/4/6 override the defaults (tuning).
+int env_int(const char *name, int dflt)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <int MODE, bool SYM, int TX, int TY>
+mfx_status run_tile(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
+                    const StencilArgs &a, cudaStream_t s)
+{
+    static const int st = env_int("MFX_STAGES", 0);
+    const int S = st ? st : ((MODE == SM_K1 && !SYM) ? 3 : 4);
+    if (S == 3) return Launcher<MODE, SYM, TX, TY, 3>::run(G, halo, coef, extra, a, s);
+    if (S == 6) return Launcher<MODE, SYM, TX, TY, 6>::run(G, halo, coef, extra, a, s);
+    return Launcher<MODE, SYM, TX, TY, 4>::run(G, halo, coef, extra, a, s);
+}
+
 template <int MODE, bool SYM>
 mfx_status run_mode(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
                     const StencilArgs &a, cudaStream_t s)
 {
-    constexpr int S = (MODE == SM_K1 && !SYM) ? 3 : 4;
-    if (G.nx <= 32) return Launcher<MODE, SYM, 32, 8, S>::run(G, halo, coef, extra, a, s);
-    return Launcher<MODE, SYM, 64, 4, S>::run(G, halo, coef, extra, a, s);
+    static const int tile = env_int("MFX_TILE", 0);   // 32 -> 32x8, 64 -> 64x4
+    const bool narrow = tile ? tile == 32 : G.nx <= 32;
+    if (narrow) return run_tile<MODE, SYM, 32, 8>(G, halo, coef, extra, a, s);
+    return run_tile<MODE, SYM, 64, 4>(G, halo, coef, extra, a, s);
 }
 
 }  // namespace

@@ -314,6 +314,108 @@ __global__ void __launch_bounds__(kThreads) k3(Geo G, double *x, double *r, cons
     }
 }
 
+// K3, streaming form used with the TMA path: x fastest and nx even, so every
+// field is a sequence of 16-byte pairs; a persistent grid walks the pairs two
+// at a time with all twelve 16-byte loads issued before any arithmetic.
+__device__ __forceinline__ double2 ldg2(const double *p) { return __ldg((const double2 *)p); }
+
+struct K3Pair {
+    double2 x, r, rh, p, v, t;
+};
+
+__device__ __forceinline__ void k3_load(K3Pair &d, long long e, const double *x, const double *r, const double *rh,
+                                        const double *p, const double *v, const double *t, bool half)
+{
+    d.v = ldg2(v + e);
+    d.r = *(const double2 *)(r + e);
+    d.p = ldg2(p + e);
+    d.x = *(const double2 *)(x + e);
+    d.rh = ldg2(rh + e);
+    if (!half) d.t = ldg2(t + e);
+}
+
+__device__ __forceinline__ void k3_cell(double xv, double rv, double rhv, double pv, double vv, double tv, double alpha,
+                                        double omega, bool half, double &xo, double &ro, Acc &rhr, Acc &rr)
+{
+    const double s = fma(-alpha, vv, rv);
+    if (half) {
+        xo = fma(alpha, pv, xv);
+        ro = s;
+    } else {
+        xo = fma(omega, s, fma(alpha, pv, xv));
+        ro = fma(-omega, tv, s);
+    }
+    rhr.prod(rhv, ro);
+    rr.prod(ro, ro);
+}
+
+__device__ __forceinline__ void k3_store(const K3Pair &d, long long e, double *x, double *r, double alpha,
+                                         double omega, bool half, Acc &rhr, Acc &rr)
+{
+    double2 xo, ro;
+    k3_cell(d.x.x, d.r.x, d.rh.x, d.p.x, d.v.x, d.t.x, alpha, omega, half, xo.x, ro.x, rhr, rr);
+    k3_cell(d.x.y, d.r.y, d.rh.y, d.p.y, d.v.y, d.t.y, alpha, omega, half, xo.y, ro.y, rhr, rr);
+    *(double2 *)(x + e) = xo;
+    *(double2 *)(r + e) = ro;
+}
+
+__global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *r, const double *__restrict__ rh,
+                                               const double *__restrict__ p, const double *__restrict__ v,
+                                               const double *__restrict__ t, WsHeader *h, dd *part)
+{
+    SolverScalars &S = h->sc;
+    if (S.done || S.skip) return;
+    const double alpha = S.alpha, omega = S.omega;
+    const bool half = S.half != 0;
+    Acc rhr, rr;
+    rhr.zero(); rr.zero();
+    const long long npairs = N / 2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    K3Pair A, B;
+    A.t = B.t = make_double2(0.0, 0.0);
+    for (; i + stride < npairs; i += 2 * stride) {
+        k3_load(A, 2 * i, x, r, rh, p, v, t, half);
+        k3_load(B, 2 * (i + stride), x, r, rh, p, v, t, half);
+        k3_store(A, 2 * i, x, r, alpha, omega, half, rhr, rr);
+        k3_store(B, 2 * (i + stride), x, r, alpha, omega, half, rhr, rr);
+    }
+    if (i < npairs) {
+        k3_load(A, 2 * i, x, r, rh, p, v, t, half);
+        k3_store(A, 2 * i, x, r, alpha, omega, half, rhr, rr);
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd vv[2] = {rhr.get(), rr.get()}, out[2];
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        S.it += 1;
+        if (half) {
+            S.rn = sqrt(S.ss);
+            S.status = MFX_OK;
+            S.done = 1;
+        } else {
+            S.rho_prev = S.rho;
+            S.rho = dd_round(out[0]);
+            S.rr = dd_round(out[1]);
+            S.rn = sqrt(S.rr);
+            if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
+            else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+        }
+    }
+}
+
+int k3v_grid()
+{
+    static int g = 0;
+    if (g) return g;
+    int occ = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3v, kThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = sms * (occ > 0 ? occ : 1);
+    if (g > kMaxBlocks) g = kMaxBlocks;
+    return g;
+}
+
 Coef coef_of(const mfx_eqsys *A)
 {
     Coef c;
@@ -346,8 +448,14 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
     count_launch(SYM ? 7 : 2, s, false);
     if (st != MFX_OK) return st;
     count_launch(3, s, true);
-    k3<<<nb, kThreads, 0, s>>>(G, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part);
+    {
+        long long np = G.N / 2;
+        int g3 = k3v_grid();
+        if ((long long)g3 * kThreads > np) g3 = (int)((np + kThreads - 1) / kThreads);
+        k3v<<<g3, kThreads, 0, s>>>(G.N, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part);
+    }
     count_launch(3, s, false);
+    (void)nb;
     return MFX_OK;
 }
 

@@ -95,11 +95,19 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap *map)
 
 constexpr int r128(int b) { return (b + 127) & ~127; }
 
+template <int CPT>
+__device__ __forceinline__ void store_cells(double *dst, const double (&v)[CPT])
+{
+    if (CPT == 2) *(double2 *)dst = make_double2(v[0], v[CPT - 1]);
+    else dst[0] = v[0];
+}
+
 template <int MODE, bool SYM, int TX, int TY>
 struct Cfg {
     static constexpr int NT = 256;
     static constexpr int HX = TX + 4, HY = TY + 2;        // halo box: x in [x0-2, x0+TX+2), y in [y0-1, y0+TY+1)
-    static constexpr int CPT = (TX * TY + NT - 1) / NT;    // owned cells per thread
+    static constexpr int CPT = TX * TY / NT;                // owned cells per consumer thread (1 or 2)
+    static_assert(TX * TY == NT || TX * TY == 2 * NT, "tile must hold 256 or 512 cells");
     static constexpr int NH = MODE == SM_K1 ? 3 : (MODE == SM_K2 ? 2 : 1);
     static constexpr int NCELLC = SYM ? 2 : 7;             // coefficient arrays with the cell box
     static constexpr int NE = (MODE == SM_SETUP || MODE == SM_K1) ? 1 : 0;
@@ -258,11 +266,18 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
         }
     } else {
         // ------------------------------------------------ consumer warps
+        // CPT = 1: thread owns cell (tid % TX, tid / TX); CPT = 2: the x-adjacent
+        // pair (2 (tid % (TX/2)), tid / (TX/2)), read and written as double2.
+        constexpr int CPT = C::CPT;
+        constexpr int RW = TX / CPT;                 // threads per tile row
         Cursor cons;
         cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz);
-        double czq1 = 0.0, czq0 = 0.0;   // cz at planes q-1 (aT of output) and q-2 (aB of output)
-        const int cx = tid % TX, cy = tid / TX;
-        const int hc = (cy + 1) * C::HX + (cx + 2);
+        double czq1[CPT], czq0[CPT];                 // cz at planes q-1 (aT of output) and q-2 (aB)
+#pragma unroll
+        for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
+        const int cx0 = (tid % RW) * CPT, cy = tid / RW;
+        const int ci = cy * TX + cx0;                // cell-box index of the first owned cell
+        const int hc = (cy + 1) * C::HX + (cx0 + 2); // halo-box index of the first owned cell
         for (int q = 0; cons.valid; q++) {
             const int s = q % S;
             const bool virt = cons.is_virtual(a.nz);
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
             const uint8_t *st = stages + (size_t)s * C::STAGE_B;
             double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
-            // step 1: value on the halo'd plane, two x-adjacent cells per thread
+            // step 1: value on the halo'd plane, two x-adjacent cells per item
             for (int pi = tid; pi < C::HX * C::HY / 2; pi += 256) {
                 double2 val = make_double2(0.0, 0.0);
                 if (!virt) {
@@ -300,8 +315,10 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                 }
                 ((double2 *)P)[pi] = val;
             }
-            double czcur = 0.0;
-            if (SYM && !virt) czcur = ((const double *)(st + C::OFF_CELL + C::CELL_B))[tid];
+            double czcur[CPT];
+#pragma unroll
+            for (int m = 0; m < CPT; m++)
+                czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
             asm volatile("bar.sync 1, 256;" ::: "memory");
 
             // step 2: output plane kout = k(q) - 1 (stage of plane q-1)
@@ -310,69 +327,102 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                 const double *Pc = pbuf + (size_t)((q + 3) & 3) * (C::PBUF_B / 8);   // plane q-1
                 const double *Pb = pbuf + (size_t)((q + 2) & 3) * (C::PBUF_B / 8);   // plane q-2
                 const double *Pt = P;                                                // plane q
-                const int gx = x0 + cx, gy = y0 + cy;
-                const bool active = gx < a.nx && gy < a.ny;
-                double aP, aW, aE, aS, aN, aB, aT;
+                const int gx = x0 + cx0, gy = y0 + cy;
+                const bool active = gx < a.nx && gy < a.ny;   // nx even: a pair is all in or all out
                 const double *cell = (const double *)(so + C::OFF_CELL);
-                aP = cell[tid];
-                if (SYM) {
-                    const double *xw = (const double *)(so + C::OFF_XW);
-                    const double *ys = (const double *)(so + C::OFF_YS);
-                    aW = xw[cy * C::HX + cx + 1];
-                    aE = xw[cy * C::HX + cx + 2];
-                    aS = ys[cy * TX + cx];
-                    aN = ys[(cy + 1) * TX + cx];
-                    aB = czq0;
-                    aT = czq1;
+                double aP[CPT], aW[CPT], aE[CPT], aS[CPT], aN[CPT], aB[CPT], aT[CPT];
+                double xc[CPT], xW[CPT], xE[CPT], xS[CPT], xN[CPT], xB[CPT], xT[CPT];
+                if (CPT == 2) {
+                    const double2 c2 = *(const double2 *)&Pc[hc];
+                    const double2 s2 = *(const double2 *)&Pc[hc - C::HX];
+                    const double2 n2 = *(const double2 *)&Pc[hc + C::HX];
+                    const double2 b2 = *(const double2 *)&Pb[hc];
+                    const double2 t2 = *(const double2 *)&Pt[hc];
+                    xc[0] = c2.x; xc[CPT - 1] = c2.y;
+                    xW[0] = Pc[hc - 1]; xW[CPT - 1] = c2.x;
+                    xE[0] = c2.y; xE[CPT - 1] = Pc[hc + 2];
+                    xS[0] = s2.x; xS[CPT - 1] = s2.y;
+                    xN[0] = n2.x; xN[CPT - 1] = n2.y;
+                    xB[0] = b2.x; xB[CPT - 1] = b2.y;
+                    xT[0] = t2.x; xT[CPT - 1] = t2.y;
                 } else {
-                    aW = cell[1 * (C::CELL_B / 8) + tid];
-                    aE = cell[2 * (C::CELL_B / 8) + tid];
-                    aS = cell[3 * (C::CELL_B / 8) + tid];
-                    aN = cell[4 * (C::CELL_B / 8) + tid];
-                    aB = cell[5 * (C::CELL_B / 8) + tid];
-                    aT = cell[6 * (C::CELL_B / 8) + tid];
+                    xc[0] = Pc[hc]; xW[0] = Pc[hc - 1]; xE[0] = Pc[hc + 1];
+                    xS[0] = Pc[hc - C::HX]; xN[0] = Pc[hc + C::HX]; xB[0] = Pb[hc]; xT[0] = Pt[hc];
                 }
-                const double xc = Pc[hc];
-                double y = aP * xc;
-                y = fma(-aW, Pc[hc - 1], y);
-                y = fma(-aE, Pc[hc + 1], y);
-                y = fma(-aS, Pc[hc - C::HX], y);
-                y = fma(-aN, Pc[hc + C::HX], y);
-                y = fma(-aB, Pb[hc], y);
-                y = fma(-aT, Pt[hc], y);
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    aP[m] = cell[ci + m];
+                    if (SYM) {
+                        const double *xw = (const double *)(so + C::OFF_XW);
+                        const double *ys = (const double *)(so + C::OFF_YS);
+                        aW[m] = xw[cy * C::HX + cx0 + m + 1];
+                        aE[m] = xw[cy * C::HX + cx0 + m + 2];
+                        aS[m] = ys[cy * TX + cx0 + m];
+                        aN[m] = ys[(cy + 1) * TX + cx0 + m];
+                        aB[m] = czq0[m];
+                        aT[m] = czq1[m];
+                    } else {
+                        aW[m] = cell[1 * (C::CELL_B / 8) + ci + m];
+                        aE[m] = cell[2 * (C::CELL_B / 8) + ci + m];
+                        aS[m] = cell[3 * (C::CELL_B / 8) + ci + m];
+                        aN[m] = cell[4 * (C::CELL_B / 8) + ci + m];
+                        aB[m] = cell[5 * (C::CELL_B / 8) + ci + m];
+                        aT[m] = cell[6 * (C::CELL_B / 8) + ci + m];
+                    }
+                }
+                double y[CPT];
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    double t = aP[m] * xc[m];
+                    t = fma(-aW[m], xW[m], t);
+                    t = fma(-aE[m], xE[m], t);
+                    t = fma(-aS[m], xS[m], t);
+                    t = fma(-aN[m], xN[m], t);
+                    t = fma(-aB[m], xB[m], t);
+                    t = fma(-aT[m], xT[m], t);
+                    y[m] = t;
+                }
                 if (active) {
                     const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
                     if (MODE == SM_SPMV) {
-                        a.out0[n] = y;
+                        store_cells<CPT>(a.out0 + n, y);
                     } else if (MODE == SM_SETUP) {
-                        const double bv = ((const double *)(so + C::OFF_EXTRA))[tid];
-                        const double rv = bv - y;
-                        a.out0[n] = rv;
-                        acc[0].prod(bv, bv);
-                        acc[ND > 1 ? 1 : 0].prod(rv, rv);
-                    } else if (MODE == SM_K1) {
-                        a.out0[n] = xc;   // p_new
-                        a.out1[n] = y;    // v_new
-                        double rhv;
-                        if (rst) {
-                            rhv = ((const double *)(so + C::OFF_HALO))[hc];   // r at the cell
-                            a.out2[n] = rhv;
-                        } else {
-                            rhv = ((const double *)(so + C::OFF_EXTRA))[tid];
+                        const double *bb = (const double *)(so + C::OFF_EXTRA) + ci;
+                        double rv[CPT];
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            rv[m] = bb[m] - y[m];
+                            acc[0].prod(bb[m], bb[m]);
+                            acc[ND > 1 ? 1 : 0].prod(rv[m], rv[m]);
                         }
-                        acc[0].prod(rhv, y);
+                        store_cells<CPT>(a.out0 + n, rv);
+                    } else if (MODE == SM_K1) {
+                        store_cells<CPT>(a.out0 + n, xc);   // p_new
+                        store_cells<CPT>(a.out1 + n, y);    // v_new
+                        double rhv[CPT];
+#pragma unroll
+                        for (int m = 0; m < CPT; m++)
+                            rhv[m] = rst ? ((const double *)(so + C::OFF_HALO))[hc + m]     // r at the cell
+                                         : ((const double *)(so + C::OFF_EXTRA))[ci + m];
+                        if (rst) store_cells<CPT>(a.out2 + n, rhv);
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) acc[0].prod(rhv[m], y[m]);
                     } else {
-                        a.out0[n] = y;    // t
-                        acc[0].prod(y, xc);
-                        acc[ND > 1 ? 1 : 0].prod(y, y);
-                        acc[ND > 2 ? 2 : 0].prod(xc, xc);
+                        store_cells<CPT>(a.out0 + n, y);    // t
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            acc[0].prod(y[m], xc[m]);
+                            acc[ND > 1 ? 1 : 0].prod(y[m], y[m]);
+                            acc[ND > 2 ? 2 : 0].prod(xc[m], xc[m]);
+                        }
                     }
                 }
             }
             // stage of plane q-1 is no longer read: release it to the producer
             __syncwarp();
             if (q >= 1 && lane == 0) mbar_arrive(&empty[(q + S - 1) % S]);
-            if (SYM) { czq0 = czq1; czq1 = czcur; }
+#pragma unroll
+            for (int m = 0; m < CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
             cons.advance(a.nz);
         }
     }
@@ -546,7 +596,7 @@ mfx_status run_tile(const Geo &G, const double *const halo[3], const double *con
                     const StencilArgs &a, cudaStream_t s)
 {
     static const int st = env_int("MFX_STAGES", 0);
-    const int S = st ? st : ((MODE == SM_K1 && !SYM) ? 3 : 4);
+    const int S = st ? st : ((TX * TY == 512 || (MODE == SM_K1 && !SYM)) ? 3 : 4);
     if (S == 3) return Launcher<MODE, SYM, TX, TY, 3>::run(G, halo, coef, extra, a, s);
     if (S == 6) return Launcher<MODE, SYM, TX, TY, 6>::run(G, halo, coef, extra, a, s);
     return Launcher<MODE, SYM, TX, TY, 4>::run(G, halo, coef, extra, a, s);
@@ -556,9 +606,13 @@ template <int MODE, bool SYM>
 mfx_status run_mode(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
                     const StencilArgs &a, cudaStream_t s)
 {
-    static const int tile = env_int("MFX_TILE", 0);   // 32 -> 32x8, 64 -> 64x4
-    const bool narrow = tile ? tile == 32 : G.nx <= 32;
-    if (narrow) return run_tile<MODE, SYM, 32, 8>(G, halo, coef, extra, a, s);
+    // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
+    static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8, 3: 32x16, 4: 32x8
+    int t = tile;
+    if (!t) t = G.nx <= 32 ? 3 : ((MODE == SM_K1) ? 1 : 2);
+    if (t == 2) return run_tile<MODE, SYM, 64, 8>(G, halo, coef, extra, a, s);
+    if (t == 3) return run_tile<MODE, SYM, 32, 16>(G, halo, coef, extra, a, s);
+    if (t == 4) return run_tile<MODE, SYM, 32, 8>(G, halo, coef, extra, a, s);
     return run_tile<MODE, SYM, 64, 4>(G, halo, coef, extra, a, s);
 }
 

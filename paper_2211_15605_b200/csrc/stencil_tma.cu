@@ -247,9 +247,11 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
     __syncthreads();
 
     constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
-    Acc acc[ND];
+    Acc acc[ND][C::CPT];   // one accumulator per dot and owned cell: independent TwoSum chains
 #pragma unroll
-    for (int d = 0; d < ND; d++) acc[d].zero();
+    for (int d = 0; d < ND; d++)
+#pragma unroll
+        for (int m = 0; m < C::CPT; m++) acc[d][m].zero();
 
     if (warp == 8) {
         // ------------------------------------------------ producer warp
@@ -316,9 +318,14 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                 ((double2 *)P)[pi] = val;
             }
             double czcur[CPT];
+            if (CPT == 2 && SYM && !virt) {
+                const double2 z2 = *(const double2 *)((const double *)(st + C::OFF_CELL + C::CELL_B) + ci);
+                czcur[0] = z2.x; czcur[CPT - 1] = z2.y;
+            } else {
 #pragma unroll
-            for (int m = 0; m < CPT; m++)
-                czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
+                for (int m = 0; m < CPT; m++)
+                    czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
+            }
             asm volatile("bar.sync 1, 256;" ::: "memory");
 
             // step 2: output plane kout = k(q) - 1 (stage of plane q-1)
@@ -349,6 +356,31 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                     xc[0] = Pc[hc]; xW[0] = Pc[hc - 1]; xE[0] = Pc[hc + 1];
                     xS[0] = Pc[hc - C::HX]; xN[0] = Pc[hc + C::HX]; xB[0] = Pb[hc]; xT[0] = Pt[hc];
                 }
+                if (CPT == 2) {
+                    const double2 p2 = *(const double2 *)&cell[ci];
+                    aP[0] = p2.x; aP[CPT - 1] = p2.y;
+                    if (SYM) {
+                        const double *xw = (const double *)(so + C::OFF_XW);
+                        const double *ys = (const double *)(so + C::OFF_YS);
+                        const double2 e2 = *(const double2 *)&xw[cy * C::HX + cx0 + 2];
+                        aW[0] = xw[cy * C::HX + cx0 + 1]; aE[0] = e2.x;
+                        aW[CPT - 1] = e2.x; aE[CPT - 1] = e2.y;
+                        const double2 s2 = *(const double2 *)&ys[cy * TX + cx0];
+                        const double2 n2 = *(const double2 *)&ys[(cy + 1) * TX + cx0];
+                        aS[0] = s2.x; aS[CPT - 1] = s2.y;
+                        aN[0] = n2.x; aN[CPT - 1] = n2.y;
+                        aB[0] = czq0[0]; aB[CPT - 1] = czq0[CPT - 1];
+                        aT[0] = czq1[0]; aT[CPT - 1] = czq1[CPT - 1];
+                    } else {
+                        double2 t2;
+                        t2 = *(const double2 *)&cell[1 * (C::CELL_B / 8) + ci]; aW[0] = t2.x; aW[CPT - 1] = t2.y;
+                        t2 = *(const double2 *)&cell[2 * (C::CELL_B / 8) + ci]; aE[0] = t2.x; aE[CPT - 1] = t2.y;
+                        t2 = *(const double2 *)&cell[3 * (C::CELL_B / 8) + ci]; aS[0] = t2.x; aS[CPT - 1] = t2.y;
+                        t2 = *(const double2 *)&cell[4 * (C::CELL_B / 8) + ci]; aN[0] = t2.x; aN[CPT - 1] = t2.y;
+                        t2 = *(const double2 *)&cell[5 * (C::CELL_B / 8) + ci]; aB[0] = t2.x; aB[CPT - 1] = t2.y;
+                        t2 = *(const double2 *)&cell[6 * (C::CELL_B / 8) + ci]; aT[0] = t2.x; aT[CPT - 1] = t2.y;
+                    }
+                } else
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
                     aP[m] = cell[ci + m];
@@ -392,8 +424,8 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
 #pragma unroll
                         for (int m = 0; m < CPT; m++) {
                             rv[m] = bb[m] - y[m];
-                            acc[0].prod(bb[m], bb[m]);
-                            acc[ND > 1 ? 1 : 0].prod(rv[m], rv[m]);
+                            acc[0][m].prod(bb[m], bb[m]);
+                            acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
                         }
                         store_cells<CPT>(a.out0 + n, rv);
                     } else if (MODE == SM_K1) {
@@ -406,14 +438,14 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                                          : ((const double *)(so + C::OFF_EXTRA))[ci + m];
                         if (rst) store_cells<CPT>(a.out2 + n, rhv);
 #pragma unroll
-                        for (int m = 0; m < CPT; m++) acc[0].prod(rhv[m], y[m]);
+                        for (int m = 0; m < CPT; m++) acc[0][m].prod(rhv[m], y[m]);
                     } else {
                         store_cells<CPT>(a.out0 + n, y);    // t
 #pragma unroll
                         for (int m = 0; m < CPT; m++) {
-                            acc[0].prod(y[m], xc[m]);
-                            acc[ND > 1 ? 1 : 0].prod(y[m], y[m]);
-                            acc[ND > 2 ? 2 : 0].prod(xc[m], xc[m]);
+                            acc[0][m].prod(y[m], xc[m]);
+                            acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
+                            acc[ND > 2 ? 2 : 0][m].prod(xc[m], xc[m]);
                         }
                     }
                 }
@@ -431,7 +463,11 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
     __shared__ dd sh[9 * ND];
     dd v[ND], out[ND];
 #pragma unroll
-    for (int d = 0; d < ND; d++) v[d] = acc[d].get();
+    for (int d = 0; d < ND; d++) {
+        v[d] = acc[d][0].get();
+#pragma unroll
+        for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+    }
     if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
     SolverScalars &Sc = a.h->sc;
     if (MODE == SM_SETUP) {
@@ -609,7 +645,7 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
     // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
     static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8, 3: 32x16, 4: 32x8
     int t = tile;
-    if (!t) t = G.nx <= 32 ? 3 : ((MODE == SM_K1) ? 1 : 2);
+    if (!t) t = G.nx <= 32 ? (SYM ? 3 : 4) : ((MODE == SM_K1 || !SYM) ? 1 : 2);
     if (t == 2) return run_tile<MODE, SYM, 64, 8>(G, halo, coef, extra, a, s);
     if (t == 3) return run_tile<MODE, SYM, 32, 16>(G, halo, coef, extra, a, s);
     if (t == 4) return run_tile<MODE, SYM, 32, 8>(G, halo, coef, extra, a, s);

@@ -20,7 +20,24 @@ namespace mfx {
 
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
                           const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
-                          double tol, int maxit, cudaStream_t s);
+                          double tol, int maxit, cudaStream_t s, int reverse = 0);
+
+// L2 ping-pong: consecutive sweeps alternate direction so each kernel starts
+// on the cells the previous one touched last (126 MB L2).  MFX_REVERSE=0
+// disables it.  Results are unchanged (elementwise updates, correctly
+// rounded dots).
+static int sweep_dir(bool flip)
+{
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char *e = getenv("MFX_REVERSE");
+        enabled = e ? atoi(e) : 1;
+    }
+    static thread_local int dir = 0;
+    if (!enabled) return 0;
+    if (flip) dir ^= 1;
+    return dir;
+}
 
 namespace {
 
@@ -361,7 +378,7 @@ __device__ __forceinline__ void k3_store(const K3Pair &d, long long e, double *x
 
 __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *r, const double *__restrict__ rh,
                                                const double *__restrict__ p, const double *__restrict__ v,
-                                               const double *__restrict__ t, WsHeader *h, dd *part)
+                                               const double *__restrict__ t, WsHeader *h, dd *part, int rev)
 {
     SolverScalars &S = h->sc;
     if (S.done || S.skip) return;
@@ -375,14 +392,16 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
     K3Pair A, B;
     A.t = B.t = make_double2(0.0, 0.0);
     for (; i + stride < npairs; i += 2 * stride) {
-        k3_load(A, 2 * i, x, r, rh, p, v, t, half);
-        k3_load(B, 2 * (i + stride), x, r, rh, p, v, t, half);
-        k3_store(A, 2 * i, x, r, alpha, omega, half, rhr, rr);
-        k3_store(B, 2 * (i + stride), x, r, alpha, omega, half, rhr, rr);
+        const long long ea = 2 * (rev ? npairs - 1 - i : i), eb = 2 * (rev ? npairs - 1 - (i + stride) : i + stride);
+        k3_load(A, ea, x, r, rh, p, v, t, half);
+        k3_load(B, eb, x, r, rh, p, v, t, half);
+        k3_store(A, ea, x, r, alpha, omega, half, rhr, rr);
+        k3_store(B, eb, x, r, alpha, omega, half, rhr, rr);
     }
     if (i < npairs) {
-        k3_load(A, 2 * i, x, r, rh, p, v, t, half);
-        k3_store(A, 2 * i, x, r, alpha, omega, half, rhr, rr);
+        const long long ea = 2 * (rev ? npairs - 1 - i : i);
+        k3_load(A, ea, x, r, rh, p, v, t, half);
+        k3_store(A, ea, x, r, alpha, omega, half, rhr, rr);
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
@@ -439,12 +458,12 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
     mfx_status st;
     count_launch(SYM ? 6 : 1, s, true);
     const double *h1[3] = {W.r, p_old, v_old};
-    st = stencil_launch(2, SYM, G, h1, A, W.rh, p_new, v_new, W.rh, W.hdr, W.part, 0.0, 0, s);
+    st = stencil_launch(2, SYM, G, h1, A, W.rh, p_new, v_new, W.rh, W.hdr, W.part, 0.0, 0, s, sweep_dir(true));
     count_launch(SYM ? 6 : 1, s, false);
     if (st != MFX_OK) return st;
     count_launch(SYM ? 7 : 2, s, true);
     const double *h2[3] = {W.r, v_new, nullptr};
-    st = stencil_launch(3, SYM, G, h2, A, nullptr, W.t, nullptr, nullptr, W.hdr, W.part, 0.0, 0, s);
+    st = stencil_launch(3, SYM, G, h2, A, nullptr, W.t, nullptr, nullptr, W.hdr, W.part, 0.0, 0, s, sweep_dir(true));
     count_launch(SYM ? 7 : 2, s, false);
     if (st != MFX_OK) return st;
     count_launch(3, s, true);
@@ -452,7 +471,7 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
         long long np = G.N / 2;
         int g3 = k3v_grid();
         if ((long long)g3 * kThreads > np) g3 = (int)((np + kThreads - 1) / kThreads);
-        k3v<<<g3, kThreads, 0, s>>>(G.N, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part);
+        k3v<<<g3, kThreads, 0, s>>>(G.N, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part, sweep_dir(true));
     }
     count_launch(3, s, false);
     (void)nb;
@@ -537,7 +556,8 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     count_launch(0, s, true);
     if (use_tma()) {
         const double *h0[3] = {x, nullptr, nullptr};
-        mfx_status st = stencil_launch(1, sym, G, h0, A, A->b, W.r, nullptr, nullptr, W.hdr, W.part, tol, maxit, s);
+        mfx_status st = stencil_launch(1, sym, G, h0, A, A->b, W.r, nullptr, nullptr, W.hdr, W.part, tol, maxit, s,
+                                       sweep_dir(true));
         if (st != MFX_OK) return st;
     } else if (sym) {
         k_setup<true><<<nb, kThreads, 0, s>>>(G, c, A->b, x, W.r, W.hdr, W.part, tol, maxit);

@@ -43,6 +43,7 @@ struct StencilArgs {
     int nx, ny, nz;
     int tiles_x, tiles_y;
     int Lz;                                // z-chunk length
+    int reverse;                           // walk the units last-to-first (L2 ping-pong)
     long long units;                       // tiles * ceil(nz / Lz) work units
     double *out0, *out1, *out2;            // SPMV: y | SETUP: r | K1: p_new, v_new, r^ | K2: t
     WsHeader *h;
@@ -140,14 +141,15 @@ __host__ __device__ constexpr size_t smem_bytes(int S)
 // (virtual, i.e. zero, outside [0, nz)) and outputs planes k0 .. k1-1.
 struct Cursor {
     int u, units;
-    int G, ntiles, Lz, tiles_x, TX, TY;
+    int G, ntiles, Lz, tiles_x, TX, TY, rev;
     int x0, y0, k, k0, k1;
     bool valid;
     __device__ void start(int nz)
     {
         if (u >= units) { valid = false; return; }
-        const int chunk = u / ntiles;
-        const int tile = u - chunk * ntiles;
+        const int uu = rev ? units - 1 - u : u;
+        const int chunk = uu / ntiles;
+        const int tile = uu - chunk * ntiles;
         const int ty = tile / tiles_x;
         x0 = (tile - ty * tiles_x) * TX;
         y0 = ty * TY;
@@ -156,9 +158,9 @@ struct Cursor {
         k = k0 - 1;
         valid = true;
     }
-    __device__ void init(int u0, int nunits, int g, int nt, int lz, int tx, int tX, int tY, int nz)
+    __device__ void init(int u0, int nunits, int g, int nt, int lz, int tx, int tX, int tY, int nz, int rv)
     {
-        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz; tiles_x = tx; TX = tX; TY = tY;
+        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz; tiles_x = tx; TX = tX; TY = tY; rev = rv;
         start(nz);
     }
     __device__ void advance(int nz)
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
 #pragma unroll
             for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
             Cursor prod;
-            prod.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz);
+            prod.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
             for (int q = 0; prod.valid; q++) {
                 if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
                 issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, stages, full, q);
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
         constexpr int CPT = C::CPT;
         constexpr int RW = TX / CPT;                 // threads per tile row
         Cursor cons;
-        cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz);
+        cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
         double czq1[CPT], czq0[CPT];                 // cz at planes q-1 (aT of output) and q-2 (aB)
 #pragma unroll
         for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
@@ -657,7 +659,7 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
 // coefficient order for the maps: SYM -> {aP, cz, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],
                           const mfx_eqsys *A, const double *extra, double *o0, double *o1, double *o2,
-                          WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s)
+                          WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s, int reverse)
 {
     const double *coef[7];
     if (sym) {
@@ -670,6 +672,7 @@ mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const 
     StencilArgs a;
     memset(&a, 0, sizeof(a));
     a.out0 = o0; a.out1 = o1; a.out2 = o2; a.h = h; a.part = part; a.tol = tol; a.maxit = maxit;
+    a.reverse = reverse;
     switch (mode * 2 + (sym ? 1 : 0)) {
     case SM_SPMV * 2 + 0: return run_mode<SM_SPMV, false>(G, halo, coef, extra, a, s);
     case SM_SPMV * 2 + 1: return run_mode<SM_SPMV, true>(G, halo, coef, extra, a, s);

@@ -192,24 +192,18 @@ def run_mfx(args, rank, world, local_rank):
     for k in ("u", "v", "w", "p"):
         sd[k].copy_(host[k], non_blocking=True)
     clocks = ClockSampler(local_rank)
-    mfx.prof_reset()
-    mfx.prof_enable(True)
     barrier()
     clocks.start()
     l0 = mfx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    iters_total, outs = 0, []
+    outs = []
     for _ in range(args.steps):
-        out = ctx.step(sd)
-        outs.append(out)
-        iters_total += sum(out["iters"][q] for q in range(8) if ctx.assignment["owner"][q] >= 0)
+        outs.append(ctx.step(sd))
     ev1.record(stream)
     barrier()
     launches = mfx.launch_count() - l0
     clk = clocks.stop()
-    mfx.prof_enable(False)
-    prof = mfx.prof_read()
     t_ms = ev0.elapsed_time(ev1)
     phase = ctx.phase_times()
     if dist is not None:
@@ -222,7 +216,25 @@ def run_mfx(args, rank, world, local_rank):
     value = it_all / (t_ms / 1e3)
     simple_per_s = args.steps / (t_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (live CUDA-event times, this stream)
+    # ---- instrumented replay of the same K steps: CUDA events recorded by libmfx
+    # on the launching stream around every hot kernel (graphs off while
+    # instrumented, so this pass is slightly slower than the timed one)
+    for k in ("u", "v", "w", "p"):
+        sd[k].copy_(host[k], non_blocking=True)
+    barrier()
+    mfx.prof_reset()
+    mfx.prof_enable(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        ctx.step(sd)
+    p1.record(stream)
+    barrier()
+    mfx.prof_enable(False)
+    prof = mfx.prof_read()
+    t_prof_ms = p0.elapsed_time(p1)
+
+    # ---- roofline of the dominant kernel
     n = g.n
     peak, peak_kind = load_peaks()
     best = max((k for k in prof if prof[k]["launches"]), key=lambda k: prof[k]["ms"])
@@ -235,9 +247,11 @@ def run_mfx(args, rank, world, local_rank):
         roof = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_kind,
                 "alg_bytes_per_launch": alg, "avg_launch_us": per_launch_ms * 1e3,
-                "traffic": None, "share_of_step": prof[kern]["ms"] / t_ms}
-    # per-iteration p' rate: K1_pp + K2_pp + K3 (p' launches dominate K3 in this workload)
+                "traffic": None, "share_of_step": prof[kern]["ms"] / t_prof_ms,
+                "timing": "CUDA events around each launch on its stream, instrumented replay of the timed steps"}
     kern_ms = {k: (prof[k]["ms"] / prof[k]["launches"] if prof[k]["launches"] else None) for k in prof}
+    # whole-iteration algorithmic bandwidth of the p' solve (K1 + K2 + K3 per iteration)
+    pp_iter_bytes = (BYTES_PER_CELL["K1_pp"] + BYTES_PER_CELL["K2_pp"] + BYTES_PER_CELL["K3"]) * n
 
     # ---- e2e through the C ABI with host buffers
     barrier()
@@ -287,6 +301,10 @@ def run_mfx(args, rank, world, local_rank):
                 "iters_last_step": outs[-1]["iters"],
                 "phase_ms_last_step": phase,
                 "kernel_avg_us": {k: (v * 1e3 if v else None) for k, v in kern_ms.items()},
+                "pp_iteration": {"alg_bytes": pp_iter_bytes,
+                                 "us": 1e3 * phase["pp"] / max(outs[-1]["iters"][3], 1),
+                                 "alg_GBps": pp_iter_bytes / (1e-3 * phase["pp"] / max(outs[-1]["iters"][3], 1)) / 1e9},
+                "instrumented_ms_per_step": t_prof_ms / args.steps,
                 "roofline": roof,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

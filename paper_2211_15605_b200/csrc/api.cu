@@ -92,6 +92,11 @@ void count_launch(int id, cudaStream_t s, bool start)
     }
 }
 
+bool prof_enabled() { return g_prof.load(std::memory_order_relaxed) != 0; }
+long long launch_count_get() { return g_launches.load(); }
+void launch_count_set(long long v) { g_launches.store(v); }
+void launch_count_add(long long v) { g_launches.fetch_add(v); }
+
 // forward declarations (other translation units)
 bool grid_valid(const mfx_grid *g, bool scalar);
 mfx_status assemble_eq(int, int, const mfx_grid *, const mfx_params *, const mfx_state *, const double *const[6],

@@ -13,6 +13,8 @@
 // 17 vector passes + 2 coefficient passes per iteration.
 #include <climits>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -494,6 +496,71 @@ void launch_iteration(const Geo &G, const Coef &c, const WsView &W, double *x, i
     count_launch(3, s, false);
 }
 
+// ------------------------------------------------------------------ CUDA graphs
+// GC BiCGSTAB iterations (3*GC kernels) captured once per (system, x,
+// workspace) and replayed: removes per-kernel launch latency from the loop.
+constexpr int GC = 16;
+struct GraphKey {
+    const void *p[10];
+    long long N;
+    int sym;
+    bool operator<(const GraphKey &o) const
+    {
+        if (N != o.N) return N < o.N;
+        if (sym != o.sym) return sym < o.sym;
+        for (int q = 0; q < 10; q++)
+            if (p[q] != o.p[q]) return p[q] < o.p[q];
+        return false;
+    }
+};
+std::mutex g_graph_mu;
+std::map<GraphKey, cudaGraphExec_t> g_graphs;
+
+bool use_graphs()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MFX_GRAPH");
+        v = e ? atoi(e) : 1;
+    }
+    return v == 1 && !prof_enabled();
+}
+
+template <bool SYM>
+mfx_status get_graph(const Geo &G, const mfx_eqsys *A, const WsView &W, double *x, int nb, cudaGraphExec_t &out)
+{
+    GraphKey k;
+    const void *ptrs[10] = {A->aP, A->aE, A->aW, A->aN, A->aS, A->aT, A->aB, A->b, x, W.hdr};
+    for (int q = 0; q < 10; q++) k.p[q] = ptrs[q];
+    k.N = G.N;
+    k.sym = SYM;
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        auto it = g_graphs.find(k);
+        if (it != g_graphs.end()) { out = it->second; return MFX_OK; }
+    }
+    cudaStream_t cs;
+    MFX_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const long long l0 = launch_count_get();
+    MFX_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    mfx_status st = MFX_OK;
+    for (int q = 0; q < GC && st == MFX_OK; q++) st = launch_iteration_tma<SYM>(G, A, W, x, q & 1, nb, cs);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    launch_count_set(l0);
+    cudaStreamDestroy(cs);
+    if (st != MFX_OK) return st;
+    if (e != cudaSuccess) { set_error("graph capture: %s", cudaGetErrorString(e)); return MFX_ERR_CUDA; }
+    cudaGraphExec_t ex;
+    e = cudaGraphInstantiate(&ex, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { set_error("graph instantiate: %s", cudaGetErrorString(e)); return MFX_ERR_CUDA; }
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graphs[k] = ex;
+    out = ex;
+    return MFX_OK;
+}
+
 struct HostScratch {
     SolverScalars *pinned = nullptr;
     ~HostScratch() {}
@@ -571,7 +638,16 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
     int launched = 0, chunk = 4;
     while (launched < maxit) {
-        const int cnt = maxit - launched < chunk ? maxit - launched : chunk;
+        int cnt = maxit - launched < chunk ? maxit - launched : chunk;
+        if (use_tma() && use_graphs() && cnt >= GC && (launched & 1) == 0) {
+            cudaGraphExec_t ex;
+            mfx_status st = sym ? get_graph<true>(G, A, W, x, nb, ex) : get_graph<false>(G, A, W, x, nb, ex);
+            if (st != MFX_OK) return st;
+            for (; cnt >= GC; cnt -= GC, launched += GC) {
+                MFX_CUDA_TRY(cudaGraphLaunch(ex, s));
+                launch_count_add(3 * GC);
+            }
+        }
         for (int q = 0; q < cnt; q++, launched++) {
             if (use_tma()) {
                 mfx_status st = sym ? launch_iteration_tma<true>(G, A, W, x, launched & 1, nb, s)

@@ -229,6 +229,10 @@ bool ws_view(void *ws, size_t bytes, long long N, bool need_vectors, WsView &out
 
 // launch accounting / profiling
 void count_launch(int id, cudaStream_t s, bool start);
+bool prof_enabled();
+long long launch_count_get();
+void launch_count_set(long long v);
+void launch_count_add(long long v);
 int reduce_grid(long long N);
 
 }  // namespace mfx

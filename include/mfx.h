@@ -209,6 +209,14 @@ mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
 void mfx_prof_enable(int on);
 void mfx_prof_reset(void);
 mfx_status mfx_prof_read(int counts[8], double ms[8]);
+/* Runtime options (process-wide).  "solver_path": 0 = auto (cluster kernel
+ * when the system fits one cluster's shared memory, else TMA z-marching),
+ * 1 = TMA z-marching kernels, 2 = single-cluster persistent kernel,
+ * 3 = v1 grid-stride reference kernels.  "graphs": 1/0 enables CUDA-graph
+ * replay of the iteration loop.  Returns MFX_ERR_ARG for an unknown key. */
+mfx_status mfx_set_option(const char *key, int value);
+int mfx_get_option(const char *key);
+
 /* Number of libmfx kernel launches issued since process start. */
 long long mfx_launch_count(void);
 

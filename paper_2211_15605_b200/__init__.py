@@ -109,6 +109,8 @@ _sigs = {
     "mfx_prof_reset": (None, []),
     "mfx_prof_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "mfx_launch_count": (C.c_longlong, []),
+    "mfx_set_option": (C.c_int, [C.c_char_p, C.c_int]),
+    "mfx_get_option": (C.c_int, [C.c_char_p]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -326,6 +328,18 @@ def prof_read():
     ms = (C.c_double * 8)()
     _check(_lib.mfx_prof_read(counts, ms), "mfx_prof_read")
     return {PROF_IDS[i]: dict(launches=counts[i], ms=ms[i]) for i in range(len(PROF_IDS))}
+
+
+PATH_AUTO, PATH_TMA, PATH_CLUSTER, PATH_V1 = 0, 1, 2, 3
+
+
+def set_option(key: str, value: int):
+    """Process-wide options: "solver_path" (PATH_*), "graphs" (0/1)."""
+    _check(_lib.mfx_set_option(key.encode(), int(value)), "mfx_set_option")
+
+
+def get_option(key: str) -> int:
+    return int(_lib.mfx_get_option(key.encode()))
 
 
 def launch_count() -> int:

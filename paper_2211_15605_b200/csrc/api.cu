@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -93,6 +94,34 @@ void count_launch(int id, cudaStream_t s, bool start)
 }
 
 bool prof_enabled() { return g_prof.load(std::memory_order_relaxed) != 0; }
+
+// ------------------------------------------------------------------ options
+static int env_default(const char *name, int dflt)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+static std::atomic<int> g_opt_path{-1};
+static std::atomic<int> g_opt_graphs{-1};
+int opt_solver_path()
+{
+    int v = g_opt_path.load();
+    if (v < 0) {
+        const char *e = getenv("MFX_KERNELS");
+        v = (e && e[0] == 'v' && e[1] == '1') ? 3 : env_default("MFX_SOLVER_PATH", 0);
+        g_opt_path.store(v);
+    }
+    return v;
+}
+int opt_graphs()
+{
+    int v = g_opt_graphs.load();
+    if (v < 0) {
+        v = env_default("MFX_GRAPH", 1);
+        g_opt_graphs.store(v);
+    }
+    return v;
+}
 long long launch_count_get() { return g_launches.load(); }
 void launch_count_set(long long v) { g_launches.store(v); }
 void launch_count_add(long long v) { g_launches.fetch_add(v); }
@@ -239,3 +268,27 @@ API mfx_status mfx_prof_read(int counts[8], double ms[8])
 }
 
 API long long mfx_launch_count(void) { return g_launches.load(); }
+
+API mfx_status mfx_set_option(const char *key, int value)
+{
+    MFX_ARG_CHECK(key, "NULL key");
+    if (!strcmp(key, "solver_path")) {
+        MFX_ARG_CHECK(value >= 0 && value <= 3, "solver_path must be 0..3");
+        g_opt_path.store(value);
+        return MFX_OK;
+    }
+    if (!strcmp(key, "graphs")) {
+        g_opt_graphs.store(value ? 1 : 0);
+        return MFX_OK;
+    }
+    set_error("unknown option '%s'", key);
+    return MFX_ERR_ARG;
+}
+
+API int mfx_get_option(const char *key)
+{
+    if (!key) return -1;
+    if (!strcmp(key, "solver_path")) return opt_solver_path();
+    if (!strcmp(key, "graphs")) return opt_graphs();
+    return -1;
+}

@@ -1,0 +1,324 @@
+// bicg_cluster.cu -- a-6 for small systems (BASELINE.json configuration 1,
+// 16x16x32): the whole unpreconditioned BiCGSTAB solve in
+// ONE launch of one thread-block cluster of 8 CTAs (8 SMs).
+//
+// The grid is split into 8 z-slabs; CTA `rank` keeps its slab of every
+// coefficient and vector in shared memory for the whole solve, reads the z
+// halo planes of its neighbours through distributed shared memory
+// (map_shared_rank), and replaces the grid-wide reductions of the large-N
+// kernels by cluster barriers: each CTA publishes its double-double partial,
+// barrier.cluster, and every CTA folds the 8 partials in rank order, so all
+// CTAs take identical scalar decisions (correctly rounded dots, §3.1).
+// Five cluster barriers per iteration; no kernel launches inside the loop.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mfx {
+
+namespace {
+
+constexpr int CL = 8;     // CTAs per cluster (portable maximum)
+constexpr int CT = 256;   // threads per CTA
+
+struct ClArgs {
+    int nx, ny, nz;
+    const double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b;
+    double *x;
+    double tol;
+    int maxit;
+    int M;                 // smem stride: max cells owned by one CTA
+    WsHeader *h;
+};
+
+template <int K>
+struct ClusterReducer {
+    dd *sh;                // block scratch (8 * K)
+    dd (*red)[4];          // [2][4] own publication slots
+    dd *bc;                // [4] CTA broadcast
+    int buf;
+    __device__ void run(cg::cluster_group &cl, dd (&v)[K], double (&out)[K])
+    {
+        block_reduce_dd<K>(v, sh);
+        if (threadIdx.x == 0)
+            for (int q = 0; q < K; q++) red[buf][q] = v[q];
+        cl.sync();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < K; q++) {
+                dd acc = dd{0.0, 0.0};
+                for (int r = 0; r < CL; r++) {
+                    const dd *rem = cl.map_shared_rank(&red[buf][q], r);
+                    acc = dd_add(acc, *rem);
+                }
+                bc[q] = acc;
+            }
+        }
+        __syncthreads();
+        for (int q = 0; q < K; q++) out[q] = dd_round(bc[q]);
+        buf ^= 1;
+    }
+};
+
+template <bool SYM>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int tid = threadIdx.x;
+    constexpr int NA = SYM ? 4 : 7;
+    extern __shared__ __align__(16) double smd[];
+    const int M = a.M;
+    double *C = smd;                     // NA arrays: SYM {aP, cx, cy, cz}; else {aP, aW, aE, aS, aN, aB, aT}
+    double *b = C + NA * M;
+    double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
+    __shared__ int k0s[CL + 1];
+    __shared__ dd sh[8 * 3];
+    __shared__ dd red[2][4];
+    __shared__ dd bc[4];
+    const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
+    if (tid <= CL) k0s[tid] = (int)((long long)nz * tid / CL);
+    __syncthreads();
+    const int k0 = k0s[rank], k1 = k0s[rank + 1];
+    const int npl = k1 - k0, nc = npl * plane;
+    const long long g0 = (long long)k0 * plane;
+    // owners of the halo planes k0-1 and k1 (ranks with at least one plane)
+    int rb = -1, ra = -1;
+    if (k0 >= 1 && npl > 0)
+        for (int q = 0; q < CL; q++)
+            if (k0s[q] <= k0 - 1 && k0 - 1 < k0s[q + 1]) rb = q;
+    if (k1 < nz && npl > 0)
+        for (int q = 0; q < CL; q++)
+            if (k0s[q] <= k1 && k1 < k0s[q + 1]) ra = q;
+    const int lb = rb >= 0 ? (k0 - 1 - k0s[rb]) * plane : 0;   // offset of plane k0-1 in rb's slab
+    const int la = ra >= 0 ? (k1 - k0s[ra]) * plane : 0;       // offset of plane k1 in ra's slab
+
+    for (int i = tid; i < nc; i += CT) {
+        if (SYM) {
+            C[0 * M + i] = a.aP[g0 + i];
+            C[1 * M + i] = a.aE[g0 + i];
+            C[2 * M + i] = a.aN[g0 + i];
+            C[3 * M + i] = a.aT[g0 + i];
+        } else {
+            C[0 * M + i] = a.aP[g0 + i];
+            C[1 * M + i] = a.aW[g0 + i];
+            C[2 * M + i] = a.aE[g0 + i];
+            C[3 * M + i] = a.aS[g0 + i];
+            C[4 * M + i] = a.aN[g0 + i];
+            C[5 * M + i] = a.aB[g0 + i];
+            C[6 * M + i] = a.aT[g0 + i];
+        }
+        b[i] = a.b[g0 + i];
+        x[i] = a.x[g0 + i];
+    }
+    ClusterReducer<1> R1{sh, red, bc, 0};
+    ClusterReducer<2> R2{sh, red, bc, 0};
+    ClusterReducer<3> R3{sh, red, bc, 0};
+    int buf = 0;   // parity of the publication slots, shared by all reductions
+
+    // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X read with its z halo
+    auto apply = [&](const double *X, int i) -> double {
+        const int kl = i / plane, o = i - kl * plane;
+        const int iy = o / nx, ix = o - iy * nx;
+        const int k = k0 + kl;
+        const double xc = X[i];
+        const double xW = ix > 0 ? X[i - 1] : 0.0;
+        const double xE = ix < nx - 1 ? X[i + 1] : 0.0;
+        const double xS = iy > 0 ? X[i - nx] : 0.0;
+        const double xN = iy < ny - 1 ? X[i + nx] : 0.0;
+        double xB = 0.0, xT = 0.0;
+        if (k > 0) xB = kl > 0 ? X[i - plane] : cl.map_shared_rank(X, rb)[lb + o];
+        if (k < nz - 1) xT = kl < npl - 1 ? X[i + plane] : cl.map_shared_rank(X, ra)[la + o];
+        double aP, aW, aE, aS, aN, aB, aT;
+        aP = C[i];
+        if (SYM) {
+            const double *cx = C + M, *cy = C + 2 * M, *cz = C + 3 * M;
+            aW = ix > 0 ? cx[i - 1] : 0.0;
+            aE = cx[i];
+            aS = iy > 0 ? cy[i - nx] : 0.0;
+            aN = cy[i];
+            aB = 0.0;
+            if (k > 0) aB = kl > 0 ? cz[i - plane] : cl.map_shared_rank(cz, rb)[lb + o];
+            aT = cz[i];
+        } else {
+            aW = C[1 * M + i]; aE = C[2 * M + i]; aS = C[3 * M + i];
+            aN = C[4 * M + i]; aB = C[5 * M + i]; aT = C[6 * M + i];
+        }
+        double y = aP * xc;
+        y = fma(-aW, xW, y);
+        y = fma(-aE, xE, y);
+        y = fma(-aS, xS, y);
+        y = fma(-aN, xN, y);
+        y = fma(-aB, xB, y);
+        y = fma(-aT, xT, y);
+        return y;
+    };
+    auto reduce1 = [&](Acc &a0, double &o0) {
+        dd vv[1] = {a0.get()};
+        double out[1];
+        R1.buf = buf;
+        R1.run(cl, vv, out);
+        buf ^= 1;
+        o0 = out[0];
+    };
+    auto reduce2 = [&](Acc &a0, Acc &a1, double &o0, double &o1) {
+        dd vv[2] = {a0.get(), a1.get()};
+        double out[2];
+        R2.buf = buf;
+        R2.run(cl, vv, out);
+        buf ^= 1;
+        o0 = out[0]; o1 = out[1];
+    };
+
+    const double tol = a.tol;
+    const int maxit = a.maxit;
+    int status = MFX_NOT_CONVERGED, iters = 0, restarts = 0;
+    double bn, rr, rn;
+
+    // ---- setup: r = b - A x0
+    cl.sync();   // x0 of every slab loaded
+    {
+        Acc bb, ra_;
+        bb.zero(); ra_.zero();
+        for (int i = tid; i < nc; i += CT) {
+            const double y = apply(x, i);
+            const double rv = b[i] - y;
+            r[i] = rv;
+            bb.prod(b[i], b[i]);
+            ra_.prod(rv, rv);
+        }
+        double bbv;
+        reduce2(bb, ra_, bbv, rr);
+        bn = sqrt(bbv);
+        rn = sqrt(rr);
+    }
+    if (bn == 0.0) {
+        for (int i = tid; i < nc; i += CT) x[i] = 0.0;
+        status = MFX_OK; rn = 0.0;
+    } else if (rn <= tol * bn) {
+        status = MFX_OK;
+    } else {
+        for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
+        double rhn = rn, rho = rr, rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+        bool restarted = false;
+        int it;
+        for (it = 1; it <= maxit; it++) {
+            if (fabs(rho) <= (1e-14 * rhn) * rn) {
+                if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it - 1; break; }
+                for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
+                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+            }
+            const double beta = (rho / rho_prev) * (alpha / omega);
+            for (int i = tid; i < nc; i += CT) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
+            cl.sync();   // p of every slab visible
+            Acc sg;
+            sg.zero();
+            for (int i = tid; i < nc; i += CT) {
+                const double vv = apply(p, i);
+                v[i] = vv;
+                sg.prod(rh[i], vv);
+            }
+            double sigma;
+            reduce1(sg, sigma);
+            if (sigma == 0.0) {
+                if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it; break; }
+                for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
+                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+                continue;
+            }
+            alpha = rho / sigma;
+            for (int i = tid; i < nc; i += CT) s[i] = fma(-alpha, v[i], r[i]);
+            cl.sync();   // s of every slab visible
+            Acc ts, tt, ss;
+            ts.zero(); tt.zero(); ss.zero();
+            for (int i = tid; i < nc; i += CT) {
+                const double tv = apply(s, i);
+                t[i] = tv;
+                ts.prod(tv, s[i]);
+                tt.prod(tv, tv);
+                ss.prod(s[i], s[i]);
+            }
+            double tsv, ttv, ssv;
+            {
+                dd vv[3] = {ts.get(), tt.get(), ss.get()};
+                double out[3];
+                R3.buf = buf;
+                R3.run(cl, vv, out);
+                buf ^= 1;
+                tsv = out[0]; ttv = out[1]; ssv = out[2];
+            }
+            if (sqrt(ssv) <= tol * bn) {
+                for (int i = tid; i < nc; i += CT) { x[i] = fma(alpha, p[i], x[i]); r[i] = s[i]; }
+                rn = sqrt(ssv);
+                status = MFX_OK; iters = it;
+                break;
+            }
+            const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
+            if (ttv == 0.0 || om == 0.0) {
+                if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it; break; }
+                for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
+                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+                continue;
+            }
+            omega = om;
+            Acc rhr, rra;
+            rhr.zero(); rra.zero();
+            for (int i = tid; i < nc; i += CT) {
+                const double xn = fma(omega, s[i], fma(alpha, p[i], x[i]));
+                const double rv = fma(-omega, t[i], s[i]);
+                x[i] = xn;
+                r[i] = rv;
+                rhr.prod(rh[i], rv);
+                rra.prod(rv, rv);
+            }
+            rho_prev = rho;
+            reduce2(rhr, rra, rho, rr);
+            rn = sqrt(rr);
+            if (rn <= tol * bn) { status = MFX_OK; iters = it; break; }
+        }
+        if (it > maxit) { status = MFX_NOT_CONVERGED; iters = maxit; }
+    }
+    for (int i = tid; i < nc; i += CT) a.x[g0 + i] = x[i];
+    if (rank == 0 && tid == 0) {
+        SolverScalars &S = a.h->sc;
+        S.it = iters; S.status = status; S.restarts = restarts; S.rn = rn; S.bn = bn; S.done = 1;
+        S.tol = tol; S.maxit = maxit;
+    }
+    cl.sync();   // keep every CTA's shared memory alive until all remote reads are done
+}
+
+}  // namespace
+
+int cluster_max_cells(bool sym)
+{
+    return (int)((227 * 1024 - 1024) / ((sym ? 12 : 15) * 8));
+}
+
+bool cluster_fits(const Geo &G, bool sym)
+{
+    const long long M = (long long)G.nx * G.ny * ((G.nz + CL - 1) / CL);
+    return M <= cluster_max_cells(sym);
+}
+
+mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
+                         WsHeader *h, cudaStream_t s)
+{
+    ClArgs a;
+    a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
+    a.aP = A->aP; a.aE = A->aE; a.aW = A->aW; a.aN = A->aN; a.aS = A->aS; a.aT = A->aT; a.aB = A->aB; a.b = A->b;
+    a.x = x; a.tol = tol; a.maxit = maxit; a.h = h;
+    a.M = G.nx * G.ny * ((G.nz + CL - 1) / CL);
+    const size_t smem = (size_t)(sym ? 12 : 15) * a.M * sizeof(double);
+    if (sym) {
+        MFX_CUDA_TRY(cudaFuncSetAttribute(k_bicg_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_bicg_cluster<true><<<CL, CT, smem, s>>>(a);
+    } else {
+        MFX_CUDA_TRY(cudaFuncSetAttribute(k_bicg_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_bicg_cluster<false><<<CL, CT, smem, s>>>(a);
+    }
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+}  // namespace mfx

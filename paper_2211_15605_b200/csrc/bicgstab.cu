@@ -516,15 +516,7 @@ struct GraphKey {
 std::mutex g_graph_mu;
 std::map<GraphKey, cudaGraphExec_t> g_graphs;
 
-bool use_graphs()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MFX_GRAPH");
-        v = e ? atoi(e) : 1;
-    }
-    return v == 1 && !prof_enabled();
-}
+bool use_graphs() { return opt_graphs() == 1 && !prof_enabled(); }
 
 template <bool SYM>
 mfx_status get_graph(const Geo &G, const mfx_eqsys *A, const WsView &W, double *x, int nb, cudaGraphExec_t &out)
@@ -573,15 +565,7 @@ bool grid_valid(const mfx_grid *g, bool scalar);
 
 // MFX_KERNELS=v1 selects the simple grid-stride kernels (kept as an A/B
 // reference for tests and profiling); default is the TMA z-marching path.
-static bool use_tma()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MFX_KERNELS");
-        v = (e && e[0] == 'v' && e[1] == '1') ? 0 : 1;
-    }
-    return v == 1;
-}
+static bool use_tma() { return opt_solver_path() != 3; }
 
 mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, cudaStream_t s)
 {
@@ -620,6 +604,24 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     const int nb = reduce_grid(G.N);
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
+    if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
+    const int path = opt_solver_path();
+    if (path == 2 || (path == 0 && cluster_fits(G, sym))) {
+        MFX_ARG_CHECK(cluster_fits(G, sym), "system too large for the single-cluster solver");
+        count_launch(0, s, true);
+        mfx_status st = cluster_solve(sym, G, A, x, tol, maxit, W.hdr, s);
+        count_launch(0, s, false);
+        if (st != MFX_OK) return st;
+        if (!info) return MFX_OK;
+        MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+        MFX_CUDA_TRY(cudaStreamSynchronize(s));
+        const SolverScalars &S = *g_host.pinned;
+        info->iters = S.it;
+        info->status = S.status;
+        info->restarts = S.restarts;
+        info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
+        return (mfx_status)S.status;
+    }
     count_launch(0, s, true);
     if (use_tma()) {
         const double *h0[3] = {x, nullptr, nullptr};
@@ -635,7 +637,6 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
     count_launch(8, s, false);
     MFX_CUDA_TRY(cudaGetLastError());
-    if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
     int launched = 0, chunk = 4;
     while (launched < maxit) {
         int cnt = maxit - launched < chunk ? maxit - launched : chunk;

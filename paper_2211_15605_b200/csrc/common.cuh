@@ -230,6 +230,11 @@ bool ws_view(void *ws, size_t bytes, long long N, bool need_vectors, WsView &out
 // launch accounting / profiling
 void count_launch(int id, cudaStream_t s, bool start);
 bool prof_enabled();
+int opt_solver_path();   // 0 auto, 1 TMA, 2 cluster, 3 v1
+int opt_graphs();
+bool cluster_fits(const Geo &G, bool sym);
+mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
+                         WsHeader *h, cudaStream_t s);
 long long launch_count_get();
 void launch_count_set(long long v);
 void launch_count_add(long long v);

@@ -1,5 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for cfg in "" "MFX_GRAPH=0"; do
-  echo "== pp $cfg"; env $cfg python scripts/prof_solve.py --kind pp --iters 200 --repeat 3 | tail -2
-done
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for path in 1 2 3; do echo "== c1 pp path $path"; python scripts/prof_solve.py --config 1 --kind pp --iters 500 --repeat 4 --path $path | tail -2; done
+for path in 1 2; do echo "== c1 w path $path"; python scripts/prof_solve.py --config 1 --kind w --iters 200 --repeat 4 --path $path | tail -2; done
+echo "== c3 pp"; python scripts/prof_solve.py --config 3 --kind pp --iters 200 --repeat 3 | tail -2

@@ -16,8 +16,11 @@ ap.add_argument("--kind", default="pp", choices=["pp", "w"])
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--path", type=int, default=0, help="solver_path option: 0 auto, 1 tma, 2 cluster, 3 v1")
+ap.add_argument("--tol", type=float, default=0.0)
 args = ap.parse_args()
 
+mfx.set_option("solver_path", args.path)
 g, pr, st = synth.config_case(args.config)
 sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
 ws = mfx.Workspace(g)
@@ -39,7 +42,7 @@ for r in range(args.repeat):
     x = torch.zeros(g.n, dtype=torch.float64, device="cuda")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    info = mfx.bicgstab_solve(kind, g, sysd, x, 0.0, args.iters, ws)
+    info = mfx.bicgstab_solve(kind, g, sysd, x, args.tol, args.iters, ws)
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)

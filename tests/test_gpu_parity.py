@@ -24,6 +24,24 @@ def mfx():
     return m
 
 
+@pytest.fixture(params=["tma", "cluster", "v1"])
+def solver_path(request, mfx):
+    v = {"tma": mfx.PATH_TMA, "cluster": mfx.PATH_CLUSTER, "v1": mfx.PATH_V1}[request.param]
+    mfx.set_option("solver_path", v)
+    yield request.param
+    mfx.set_option("solver_path", mfx.PATH_AUTO)
+
+
+def cluster_fits(g, sym):
+    m = g.nx * g.ny * -(-g.nz // 8)
+    return m <= (227 * 1024 - 1024) // ((12 if sym else 15) * 8)
+
+
+def need_path(solver_path, g, sym):
+    if solver_path == "cluster" and not cluster_fits(g, sym):
+        pytest.skip("system does not fit the single-cluster solver")
+
+
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
 
@@ -148,15 +166,16 @@ def assert_solve_parity(ref, info, x):
 
 @pytest.mark.parametrize("name", list(GRIDS))
 @pytest.mark.parametrize("comp", [0, 2])
-def test_bicgstab_momentum_parity(mfx, orc, name, comp):
+def test_bicgstab_momentum_parity(mfx, orc, name, comp, solver_path):
     g, pr, st = case(name)
+    need_path(solver_path, g, False)
     sysd, _, _ = orc.assemble_mom(g, pr, comp, st)
     x0 = [st["u"], st["v"], st["w"]][comp]
     ref, info, x = solve_both(mfx, orc, g, comp, sysd, x0, 1e-10, 200)
     assert_solve_parity(ref, info, x)
 
 
-def test_bicgstab_pp_c1_parity(mfx, orc):
+def test_bicgstab_pp_c1_parity(mfx, orc, solver_path):
     """Configuration 1 (BASELINE.json): p' BiCGSTAB on 16x16x32 with bed contrast,
     tol 1e-6, maxit 5000 (SURVEY §8d c1 procedure)."""
     g, pr, st = synth.config_case(1)
@@ -173,8 +192,9 @@ def test_bicgstab_pp_c1_parity(mfx, orc):
 
 
 @pytest.mark.parametrize("name", ["rag1", "rag2", "tall"])
-def test_bicgstab_pp_ragged_parity(mfx, orc, name):
+def test_bicgstab_pp_ragged_parity(mfx, orc, name, solver_path):
     g, pr, st = case(name)
+    need_path(solver_path, g, True)
     dv = [np.random.default_rng(9 + a).uniform(1e-4, 1e-3, g.n) for a in range(3)]
     sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
     ref, info, x = solve_both(mfx, orc, g, mfx.EQ_PP, sysd, np.zeros(g.n), 1e-8, 3000)
@@ -182,8 +202,9 @@ def test_bicgstab_pp_ragged_parity(mfx, orc, name):
 
 
 @pytest.mark.parametrize("maxit", [0, 1, 2, 7])
-def test_bicgstab_not_converged_last_iterate(mfx, orc, maxit):
+def test_bicgstab_not_converged_last_iterate(mfx, orc, maxit, solver_path):
     g, pr, st = case("rag2")
+    need_path(solver_path, g, True)
     dv = [np.full(g.n, 5e-4)] * 3
     sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
     ref, info, x = solve_both(mfx, orc, g, mfx.EQ_PP, sysd, np.zeros(g.n), 1e-14, maxit)
@@ -191,7 +212,7 @@ def test_bicgstab_not_converged_last_iterate(mfx, orc, maxit):
     assert np.array_equal(x, ref["x"])
 
 
-def test_bicgstab_edge_cases(mfx, orc):
+def test_bicgstab_edge_cases(mfx, orc, solver_path):
     g = Grid(4, 2, 2, 1.0, 1.0, 1.0)
     n = g.n
     z = {k: np.zeros(n) for k in ("aE", "aW", "aN", "aS", "aT", "aB", "d")}
@@ -215,8 +236,9 @@ def test_bicgstab_edge_cases(mfx, orc):
     assert info["iters"] == 0 and np.array_equal(x, np.ones(n))
 
 
-def test_bicgstab_deterministic(mfx, orc):
+def test_bicgstab_deterministic(mfx, orc, solver_path):
     g, pr, st = case("rag2")
+    need_path(solver_path, g, True)
     dv = [np.full(g.n, 5e-4)] * 3
     sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
     d = {k: dev(v) for k, v in sysd.items()}
@@ -245,8 +267,9 @@ def test_correct_bitwise(mfx, orc, name):
 
 # ---------------------------------------------------------------- a-9 SIMPLE
 @pytest.mark.parametrize("name,n_scalars", [("c1", 0), ("rag2", 1), ("tall", 2)])
-def test_simple_iter_111_parity(mfx, orc, name, n_scalars):
+def test_simple_iter_111_parity(mfx, orc, name, n_scalars, solver_path):
     g, pr, st = case(name, n_scalars=n_scalars)
+    need_path(solver_path, g, False)
     pr.lin_maxit_pp = 2000
     asg = "111[1]" + "1" * n_scalars
     ctx = mfx.SimpleContext(asg, g, pr)

@@ -33,29 +33,46 @@ struct ClArgs {
     WsHeader *h;
 };
 
-template <int K>
-struct ClusterReducer {
-    dd *sh;                // block scratch (8 * K)
-    dd (*red)[4];          // [2][4] own publication slots
-    dd *bc;                // [4] CTA broadcast
-    int buf;
-    __device__ void run(cg::cluster_group &cl, dd (&v)[K], double (&out)[K])
+// Cluster-wide correctly rounded reduction of K double-doubles: each warp
+// publishes its butterfly partial; after barrier.cluster the 64 partials
+// (8 CTAs x 8 warps) of each value are gathered in parallel into local
+// shared memory and folded by one warp in a fixed order, so every CTA gets
+// the identical result.  Publication slots alternate between two buffers
+// (the barrier of reduction j+1 orders all remote reads of reduction j
+// before any CTA overwrites its slots in reduction j+2).
+struct ClusterRed {
+    dd (*pub)[3][8];       // [2][3][8] this CTA's per-warp partials
+    dd (*tmp)[64];         // [3][64] gathered partials
+    dd *bc;                // [3] folded results
+    template <int K>
+    __device__ void run(cg::cluster_group &cl, int &buf, dd (&v)[K], double (&out)[K])
     {
-        block_reduce_dd<K>(v, sh);
-        if (threadIdx.x == 0)
-            for (int q = 0; q < K; q++) red[buf][q] = v[q];
-        cl.sync();
-        if (threadIdx.x == 0) {
-            for (int q = 0; q < K; q++) {
-                dd acc = dd{0.0, 0.0};
-                for (int r = 0; r < CL; r++) {
-                    const dd *rem = cl.map_shared_rank(&red[buf][q], r);
-                    acc = dd_add(acc, *rem);
-                }
-                bc[q] = acc;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            dd x = v[q];
+            for (int off = 16; off > 0; off >>= 1) {
+                dd y = shfl_dd(x, off);
+                x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
             }
+            if (lane == 0) pub[buf][q][wid] = x;
+        }
+        cl.sync();
+        if (threadIdx.x < 64 * K) {
+            const int q = threadIdx.x >> 6, idx = threadIdx.x & 63;
+            tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx & 7], idx >> 3);
         }
         __syncthreads();
+        if (wid < K) {
+            dd x = dd_add(tmp[wid][lane], tmp[wid][lane + 32]);
+            for (int off = 16; off > 0; off >>= 1) {
+                dd y = shfl_dd(x, off);
+                x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
+            }
+            if (lane == 0) bc[wid] = x;
+        }
+        __syncthreads();
+#pragma unroll
         for (int q = 0; q < K; q++) out[q] = dd_round(bc[q]);
         buf ^= 1;
     }
@@ -74,9 +91,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     double *b = C + NA * M;
     double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
     __shared__ int k0s[CL + 1];
-    __shared__ dd sh[8 * 3];
-    __shared__ dd red[2][4];
-    __shared__ dd bc[4];
+    __shared__ dd pub[2][3][8];
+    __shared__ dd tmp[3][64];
+    __shared__ dd bc[3];
     const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
     if (tid <= CL) k0s[tid] = (int)((long long)nz * tid / CL);
     __syncthreads();
@@ -112,10 +129,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         b[i] = a.b[g0 + i];
         x[i] = a.x[g0 + i];
     }
-    ClusterReducer<1> R1{sh, red, bc, 0};
-    ClusterReducer<2> R2{sh, red, bc, 0};
-    ClusterReducer<3> R3{sh, red, bc, 0};
+    ClusterRed R{pub, tmp, bc};
     int buf = 0;   // parity of the publication slots, shared by all reductions
+    double *hb = t + M, *ha = hb + plane;                 // local copies of the z-halo planes
+    double *czb = ha + plane;                             // cz of plane k0-1 (SYM)
 
     // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X read with its z halo
     auto apply = [&](const double *X, int i) -> double {
@@ -128,8 +145,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         const double xS = iy > 0 ? X[i - nx] : 0.0;
         const double xN = iy < ny - 1 ? X[i + nx] : 0.0;
         double xB = 0.0, xT = 0.0;
-        if (k > 0) xB = kl > 0 ? X[i - plane] : cl.map_shared_rank(X, rb)[lb + o];
-        if (k < nz - 1) xT = kl < npl - 1 ? X[i + plane] : cl.map_shared_rank(X, ra)[la + o];
+        if (k > 0) xB = kl > 0 ? X[i - plane] : hb[o];
+        if (k < nz - 1) xT = kl < npl - 1 ? X[i + plane] : ha[o];
         double aP, aW, aE, aS, aN, aB, aT;
         aP = C[i];
         if (SYM) {
@@ -139,7 +156,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             aS = iy > 0 ? cy[i - nx] : 0.0;
             aN = cy[i];
             aB = 0.0;
-            if (k > 0) aB = kl > 0 ? cz[i - plane] : cl.map_shared_rank(cz, rb)[lb + o];
+            if (k > 0) aB = kl > 0 ? cz[i - plane] : czb[o];
             aT = cz[i];
         } else {
             aW = C[1 * M + i]; aE = C[2 * M + i]; aS = C[3 * M + i];
@@ -157,18 +174,22 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     auto reduce1 = [&](Acc &a0, double &o0) {
         dd vv[1] = {a0.get()};
         double out[1];
-        R1.buf = buf;
-        R1.run(cl, vv, out);
-        buf ^= 1;
+        R.run<1>(cl, buf, vv, out);
         o0 = out[0];
     };
     auto reduce2 = [&](Acc &a0, Acc &a1, double &o0, double &o1) {
         dd vv[2] = {a0.get(), a1.get()};
         double out[2];
-        R2.buf = buf;
-        R2.run(cl, vv, out);
-        buf ^= 1;
+        R.run<2>(cl, buf, vv, out);
         o0 = out[0]; o1 = out[1];
+    };
+    // after a cluster barrier: copy the neighbours' boundary planes of X locally
+    auto fetch_halo = [&](const double *X) {
+        for (int o = tid; o < plane; o += CT) {
+            if (rb >= 0) hb[o] = cl.map_shared_rank(X, rb)[lb + o];
+            if (ra >= 0) ha[o] = cl.map_shared_rank(X, ra)[la + o];
+        }
+        __syncthreads();
     };
 
     const double tol = a.tol;
@@ -177,7 +198,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     double bn, rr, rn;
 
     // ---- setup: r = b - A x0
-    cl.sync();   // x0 of every slab loaded
+    cl.sync();   // x0 and coefficients of every slab loaded
+    if (SYM)
+        for (int o = tid; o < plane; o += CT) czb[o] = rb >= 0 ? cl.map_shared_rank(C + 3 * M, rb)[lb + o] : 0.0;
+    fetch_halo(x);
     {
         Acc bb, ra_;
         bb.zero(); ra_.zero();
@@ -212,6 +236,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             const double beta = (rho / rho_prev) * (alpha / omega);
             for (int i = tid; i < nc; i += CT) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
             cl.sync();   // p of every slab visible
+            fetch_halo(p);
             Acc sg;
             sg.zero();
             for (int i = tid; i < nc; i += CT) {
@@ -230,6 +255,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             alpha = rho / sigma;
             for (int i = tid; i < nc; i += CT) s[i] = fma(-alpha, v[i], r[i]);
             cl.sync();   // s of every slab visible
+            fetch_halo(s);
             Acc ts, tt, ss;
             ts.zero(); tt.zero(); ss.zero();
             for (int i = tid; i < nc; i += CT) {
@@ -243,9 +269,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             {
                 dd vv[3] = {ts.get(), tt.get(), ss.get()};
                 double out[3];
-                R3.buf = buf;
-                R3.run(cl, vv, out);
-                buf ^= 1;
+                R.run<3>(cl, buf, vv, out);
                 tsv = out[0]; ttv = out[1]; ssv = out[2];
             }
             if (sqrt(ssv) <= tol * bn) {
@@ -290,16 +314,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
 
 }  // namespace
 
-int cluster_max_cells(bool sym)
+// dynamic smem: (NA + 8) arrays of M cells + 3 planes (two halo copies, cz below)
+size_t cluster_smem(const Geo &G, bool sym)
 {
-    return (int)((227 * 1024 - 1024) / ((sym ? 12 : 15) * 8));
+    const long long plane = (long long)G.nx * G.ny;
+    const long long M = plane * ((G.nz + CL - 1) / CL);
+    return (size_t)(((sym ? 12 : 15) * M + 3 * plane) * sizeof(double));
 }
 
-bool cluster_fits(const Geo &G, bool sym)
-{
-    const long long M = (long long)G.nx * G.ny * ((G.nz + CL - 1) / CL);
-    return M <= cluster_max_cells(sym);
-}
+bool cluster_fits(const Geo &G, bool sym) { return cluster_smem(G, sym) <= 200 * 1024; }
 
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s)
@@ -309,7 +332,7 @@ mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, 
     a.aP = A->aP; a.aE = A->aE; a.aW = A->aW; a.aN = A->aN; a.aS = A->aS; a.aT = A->aT; a.aB = A->aB; a.b = A->b;
     a.x = x; a.tol = tol; a.maxit = maxit; a.h = h;
     a.M = G.nx * G.ny * ((G.nz + CL - 1) / CL);
-    const size_t smem = (size_t)(sym ? 12 : 15) * a.M * sizeof(double);
+    const size_t smem = cluster_smem(G, sym);
     if (sym) {
         MFX_CUDA_TRY(cudaFuncSetAttribute(k_bicg_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_bicg_cluster<true><<<CL, CT, smem, s>>>(a);

@@ -33,8 +33,9 @@ def solver_path(request, mfx):
 
 
 def cluster_fits(g, sym):
-    m = g.nx * g.ny * -(-g.nz // 8)
-    return m <= (227 * 1024 - 1024) // ((12 if sym else 15) * 8)
+    plane = g.nx * g.ny
+    m = plane * -(-g.nz // 8)
+    return ((12 if sym else 15) * m + 3 * plane) * 8 <= 200 * 1024
 
 
 def need_path(solver_path, g, sym):

@@ -23,6 +23,17 @@ namespace {
 constexpr int CL = 8;     // CTAs per cluster (portable maximum)
 constexpr int CT = 256;   // threads per CTA
 
+// Cluster barrier for shared-memory exchange.  cg::cluster_group::sync()
+// (barrier.cluster.arrive.release) compiles to MEMBAR.ALL.GPU on sm_100a;
+// everything exchanged here lives in shared memory, so a CTA barrier (which
+// drains this CTA's pending shared stores) followed by a relaxed cluster
+// arrive / wait orders the writes before any remote DSMEM read.
+__device__ __forceinline__ void cluster_barrier()
+{
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 struct ClArgs {
     int nx, ny, nz;
     const double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b;
@@ -57,7 +68,7 @@ struct ClusterRed {
             }
             if (lane == 0) pub[buf][q][wid] = x;
         }
-        cl.sync();
+        cluster_barrier();
         if (threadIdx.x < 64 * K) {
             const int q = threadIdx.x >> 6, idx = threadIdx.x & 63;
             tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx & 7], idx >> 3);
@@ -198,7 +209,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     double bn, rr, rn;
 
     // ---- setup: r = b - A x0
-    cl.sync();   // x0 and coefficients of every slab loaded
+    cluster_barrier();   // x0 and coefficients of every slab loaded
     if (SYM)
         for (int o = tid; o < plane; o += CT) czb[o] = rb >= 0 ? cl.map_shared_rank(C + 3 * M, rb)[lb + o] : 0.0;
     fetch_halo(x);
@@ -235,7 +246,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             }
             const double beta = (rho / rho_prev) * (alpha / omega);
             for (int i = tid; i < nc; i += CT) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
-            cl.sync();   // p of every slab visible
+            cluster_barrier();   // p of every slab visible
             fetch_halo(p);
             Acc sg;
             sg.zero();
@@ -254,7 +265,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             }
             alpha = rho / sigma;
             for (int i = tid; i < nc; i += CT) s[i] = fma(-alpha, v[i], r[i]);
-            cl.sync();   // s of every slab visible
+            cluster_barrier();   // s of every slab visible
             fetch_halo(s);
             Acc ts, tt, ss;
             ts.zero(); tt.zero(); ss.zero();
@@ -309,7 +320,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         S.it = iters; S.status = status; S.restarts = restarts; S.rn = rn; S.bn = bn; S.done = 1;
         S.tol = tol; S.maxit = maxit;
     }
-    cl.sync();   // keep every CTA's shared memory alive until all remote reads are done
+    cluster_barrier();   // keep every CTA's shared memory alive until all remote reads are done
 }
 
 }  // namespace

@@ -196,6 +196,11 @@ mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_
  * Synchronises `stream` once at the end (residual record to host). */
 mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void *stream);
 
+/* Device pointers to the context's internal buffers from the last
+ * mfx_simple_iter (NULL where this rank does not hold them): which =
+ * 0..2 u*, v*, w* (momentum predictors), 3..5 d_x, d_y, d_z, 6 p' solution. */
+double *mfx_ctx_buffer(mfx_ctx *ctx, int which);
+
 /* Per-phase device times of the last mfx_simple_iter on this rank (ms):
  * [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction,
  * [4] BCAST, [5] total. */

@@ -105,6 +105,7 @@ _sigs = {
     "mfx_exchange_state": (C.c_int, [_V, C.c_int, C.POINTER(_V), _V]),
     "mfx_simple_iter": (C.c_int, [_V, C.POINTER(State), C.POINTER(Resid), _V]),
     "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
+    "mfx_ctx_buffer": (C.c_void_p, [_V, C.c_int]),
     "mfx_prof_enable": (None, [C.c_int]),
     "mfx_prof_reset": (None, []),
     "mfx_prof_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
@@ -294,6 +295,15 @@ class SimpleContext:
         return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
                     status=list(r.status), converged=bool(r.converged))
 
+    def buffer(self, which: str):
+        """Copy of an internal buffer of the last step: 'u*','v*','w*','dx','dy','dz','pp'."""
+        idx = ("u*", "v*", "w*", "dx", "dy", "dz", "pp").index(which)
+        ptr = _lib.mfx_ctx_buffer(self.ptr, idx)
+        if not ptr:
+            return None
+        n = self.grid.nx * self.grid.ny * self.grid.nz
+        return device_view(ptr, n).clone()
+
     def phase_times(self):
         ms = (C.c_double * 6)()
         _check(_lib.mfx_ctx_phase_times(self.ptr, ms), "mfx_ctx_phase_times")
@@ -309,6 +319,19 @@ class SimpleContext:
             self.close()
         except Exception:
             pass
+
+
+class _DevPtr:
+    """Minimal __cuda_array_interface__ holder for a raw fp64 device pointer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
+def device_view(ptr: int, n: int):
+    """torch view (no copy) of n doubles at a libmfx-owned device pointer."""
+    import torch
+    return torch.as_tensor(_DevPtr(ptr, n), device="cuda")
 
 
 # ---------------------------------------------------------------- instrumentation

@@ -454,6 +454,14 @@ void mfx_ctx_destroy(mfx_ctx *c)
     delete c;
 }
 
+double *mfx_ctx_buffer(mfx_ctx *c, int which)
+{
+    if (!c || which < 0 || which > 6) return nullptr;
+    if (which < 3) return c->star[which];
+    if (which < 6) return c->dv[which - 3];
+    return c->pp;
+}
+
 mfx_status mfx_ctx_phase_times(const mfx_ctx *c, double ms[6])
 {
     if (!c || !ms) return MFX_ERR_ARG;

@@ -83,3 +83,42 @@ def test_c2_simple_iteration_properties(mfx, orc, c2):
     assert 1 <= out["iters"][3] <= 50
     assert all(0 <= it <= pr.lin_maxit_mom for it in out["iters"][:3])
     ctx.close()
+
+
+def test_c2_simple_iteration_in_bench_configuration(mfx, orc, c2):
+    """The bench's exact launch configuration (SimpleContext '111[1]', CUDA
+    graphs, TMA kernels) at full size: the w-momentum predictor w* equals the
+    oracle's bitwise; the p' system assembled from the GPU's u*, d equals the
+    oracle's bitwise; the correction satisfies the continuity identity
+    b(u_corr) = b(u*) - A p'."""
+    g, pr, st = c2
+    pr = synth.Params()
+    assert mfx.get_option("graphs") == 1
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    sd = {k: dev(v) for k, v in st.items()}
+    out = ctx.step(sd)
+    # w predictor vs oracle (assembly + BiCGSTAB to 1e-4, maxit 20)
+    sw, _, _ = orc.assemble_mom(g, pr, 2, st)
+    ow = orc.bicgstab(g, sw, st["w"], pr.lin_tol_mom, pr.lin_maxit_mom)
+    assert out["iters"][2] == ow["iters"]
+    assert np.array_equal(host(ctx.buffer("w*")), ow["x"])
+    assert np.array_equal(host(ctx.buffer("dz")), sw["d"])
+    # p' system from the GPU's own predictors
+    star = [host(ctx.buffer(k)) for k in ("u*", "v*", "w*")]
+    dv = [host(ctx.buffer(k)) for k in ("dx", "dy", "dz")]
+    ref, cont, _ = orc.assemble_pp(g, pr, st, star, dv)
+    assert out["R"][3] == cont
+    ws = mfx.Workspace(g)
+    gsys, _ = mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws, star=[dev(a) for a in star + dv])
+    # (sd now holds the corrected state; eps/eps_old are unchanged inputs)
+    for k in ("aP", "aE", "aN", "aT", "b"):
+        assert np.array_equal(host(gsys[k]), ref[k]), k
+    pp = ctx.buffer("pp")
+    Ap = host(mfx.spmv(mfx.EQ_PP, g, gsys, pp))
+    ccorr, _ = mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws, star=[sd["u"], sd["v"], sd["w"]] + [dev(a) for a in dv])
+    lhs = host(ccorr["b"])
+    scale = pr.rho * g.dx * g.dy * 1.0
+    assert np.max(np.abs(lhs - (ref["b"] - Ap))) <= 1e-10 * scale
+    # the p' solve either met its tolerance or ran to maxit (last iterate returned)
+    assert out["iters"][3] == pr.lin_maxit_pp or out["status"][3] == 0
+    ctx.close()

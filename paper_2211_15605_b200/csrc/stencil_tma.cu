@@ -103,12 +103,14 @@ __device__ __forceinline__ void store_cells(double *dst, const double (&v)[CPT])
     else dst[0] = v[0];
 }
 
-template <int MODE, bool SYM, int TX, int TY>
+template <int MODE, bool SYM, int TX, int TY, int CPT_>
 struct Cfg {
-    static constexpr int NT = 256;
+    static constexpr int NT = TX * TY / CPT_;               // consumer threads (one per owned cell or pair)
     static constexpr int HX = TX + 4, HY = TY + 2;        // halo box: x in [x0-2, x0+TX+2), y in [y0-1, y0+TY+1)
-    static constexpr int CPT = TX * TY / NT;                // owned cells per consumer thread (1 or 2)
-    static_assert(TX * TY == NT || TX * TY == 2 * NT, "tile must hold 256 or 512 cells");
+    static constexpr int CPT = CPT_;                        // owned cells per consumer thread (1 or 2)
+    static constexpr int NW = NT / 32;                      // consumer warps; the producer is warp NW
+    static_assert(CPT == 1 || CPT == 2, "1 or 2 cells per thread");
+    static_assert(NT % 32 == 0 && NT <= 512, "consumer threads");
     static constexpr int NH = MODE == SM_K1 ? 3 : (MODE == SM_K2 ? 2 : 1);
     static constexpr int NCELLC = SYM ? 2 : 7;             // coefficient arrays with the cell box
     static constexpr int NE = (MODE == SM_SETUP || MODE == SM_K1) ? 1 : 0;
@@ -172,11 +174,11 @@ struct Cursor {
     __device__ bool produces() const { return k >= k0 + 1; }
 };
 
-template <int MODE, bool SYM, int TX, int TY, int S>
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S>
 __device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, uint8_t *stages, uint64_t *full,
                                       int q)
 {
-    using C = Cfg<MODE, SYM, TX, TY>;
+    using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     const int s = q % S;
     uint64_t *bar = &full[s];
     if (c.is_virtual(nz)) {
@@ -197,11 +199,11 @@ __device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz,
     if (C::NE) tma_load_3d(st + C::OFF_EXTRA, &M.extra, x0, y0, k, bar);
 }
 
-template <int MODE, bool SYM, int TX, int TY, int S>
-__global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps M, StencilArgs a)
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S>
+__global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stencil(const __grid_constant__ TmaMaps M, StencilArgs a)
 {
     // warps 0-7: consumers (one owned cell per thread); warp 8: TMA producer
-    using C = Cfg<MODE, SYM, TX, TY>;
+    using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *stages = smem;
     double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
     if (tid == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 8);
+            mbar_init(&empty[s], C::NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
 #pragma unroll
         for (int m = 0; m < C::CPT; m++) acc[d][m].zero();
 
-    if (warp == 8) {
+    if (warp == C::NW) {
         // ------------------------------------------------ producer warp
         if (lane == 0) {
 #pragma unroll
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
             prod.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
             for (int q = 0; prod.valid; q++) {
                 if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
-                issue<MODE, SYM, TX, TY, S>(M, prod, a.nz, stages, full, q);
+                issue<MODE, SYM, TX, TY, CPT_, S>(M, prod, a.nz, stages, full, q);
                 prod.advance(a.nz);
             }
         }
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
             double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
             // step 1: value on the halo'd plane, two x-adjacent cells per item
-            for (int pi = tid; pi < C::HX * C::HY / 2; pi += 256) {
+            for (int pi = tid; pi < C::HX * C::HY / 2; pi += C::NT) {
                 double2 val = make_double2(0.0, 0.0);
                 if (!virt) {
                     const double2 *h0 = (const double2 *)(st + C::OFF_HALO);
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
                 for (int m = 0; m < CPT; m++)
                     czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(C::NT) : "memory");
 
             // step 2: output plane kout = k(q) - 1 (stage of plane q-1)
             if (produce) {
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(288) k_stencil(const __grid_constant__ TmaMaps
     }
 
     if (C::NDOT == 0) return;
-    __shared__ dd sh[9 * ND];
+    __shared__ dd sh[(C::NW + 1) * ND];
     dd v[ND], out[ND];
 #pragma unroll
     for (int d = 0; d < ND; d++) {
@@ -574,17 +576,17 @@ int choose_lz(long long ntiles, int nz, int grid)
     return best;
 }
 
-template <int MODE, bool SYM, int TX, int TY, int S>
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S>
 struct Launcher {
-    using C = Cfg<MODE, SYM, TX, TY>;
+    using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     static int grid_size()
     {
         static int g = 0;
         if (g) return g;
         const size_t sm = smem_bytes<C>(S);
-        cudaFuncSetAttribute(k_stencil<MODE, SYM, TX, TY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_stencil<MODE, SYM, TX, TY, CPT_, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, S>, 288, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, CPT_, S>, C::NT + 32, sm);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -616,7 +618,7 @@ struct Launcher {
         a.Lz = choose_lz(ntiles, G.nz, grid);
         a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
         if (grid > a.units) grid = (int)a.units;
-        k_stencil<MODE, SYM, TX, TY, S><<<grid, 288, smem_bytes<C>(S), s>>>(M, a);
+        k_stencil<MODE, SYM, TX, TY, CPT_, S><<<grid, C::NT + 32, smem_bytes<C>(S), s>>>(M, a);
         MFX_CUDA_TRY(cudaGetLastError());
         return MFX_OK;
     }
@@ -629,15 +631,15 @@ int env_int(const char *name, int dflt)
     return e ? atoi(e) : dflt;
 }
 
-template <int MODE, bool SYM, int TX, int TY>
+template <int MODE, bool SYM, int TX, int TY, int CPT_>
 mfx_status run_tile(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
                     const StencilArgs &a, cudaStream_t s)
 {
     static const int st = env_int("MFX_STAGES", 0);
     const int S = st ? st : ((TX * TY == 512 || (MODE == SM_K1 && !SYM)) ? 3 : 4);
-    if (S == 3) return Launcher<MODE, SYM, TX, TY, 3>::run(G, halo, coef, extra, a, s);
-    if (S == 6) return Launcher<MODE, SYM, TX, TY, 6>::run(G, halo, coef, extra, a, s);
-    return Launcher<MODE, SYM, TX, TY, 4>::run(G, halo, coef, extra, a, s);
+    if (S == 3) return Launcher<MODE, SYM, TX, TY, CPT_, 3>::run(G, halo, coef, extra, a, s);
+    if (S == 6) return Launcher<MODE, SYM, TX, TY, CPT_, 6>::run(G, halo, coef, extra, a, s);
+    return Launcher<MODE, SYM, TX, TY, CPT_, 4>::run(G, halo, coef, extra, a, s);
 }
 
 template <int MODE, bool SYM>
@@ -645,13 +647,14 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
                     const StencilArgs &a, cudaStream_t s)
 {
     // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
-    static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8, 3: 32x16, 4: 32x8
+    static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8 pairs, 3: 32x16 pairs, 4: 32x8, 5: 64x8
     int t = tile;
     if (!t) t = G.nx <= 32 ? (SYM ? 3 : 4) : ((MODE == SM_K1 || !SYM) ? 1 : 2);
-    if (t == 2) return run_tile<MODE, SYM, 64, 8>(G, halo, coef, extra, a, s);
-    if (t == 3) return run_tile<MODE, SYM, 32, 16>(G, halo, coef, extra, a, s);
-    if (t == 4) return run_tile<MODE, SYM, 32, 8>(G, halo, coef, extra, a, s);
-    return run_tile<MODE, SYM, 64, 4>(G, halo, coef, extra, a, s);
+    if (t == 2) return run_tile<MODE, SYM, 64, 8, 2>(G, halo, coef, extra, a, s);
+    if (t == 3) return run_tile<MODE, SYM, 32, 16, 2>(G, halo, coef, extra, a, s);
+    if (t == 4) return run_tile<MODE, SYM, 32, 8, 1>(G, halo, coef, extra, a, s);
+    if (t == 5) return run_tile<MODE, SYM, 64, 8, 1>(G, halo, coef, extra, a, s);
+    return run_tile<MODE, SYM, 64, 4, 1>(G, halo, coef, extra, a, s);
 }
 
 }  // namespace

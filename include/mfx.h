@@ -218,7 +218,8 @@ mfx_status mfx_prof_read(int counts[8], double ms[8]);
  * when the system fits one cluster's shared memory, else TMA z-marching),
  * 1 = TMA z-marching kernels, 2 = single-cluster persistent kernel,
  * 3 = v1 grid-stride reference kernels.  "graphs": 1/0 enables CUDA-graph
- * replay of the iteration loop.  Returns MFX_ERR_ARG for an unknown key. */
+ * replay of the iteration loop.  "pdl": 1/0 enables programmatic dependent
+ * launch between the BiCGSTAB kernels.  Returns MFX_ERR_ARG for an unknown key. */
 mfx_status mfx_set_option(const char *key, int value);
 int mfx_get_option(const char *key);
 

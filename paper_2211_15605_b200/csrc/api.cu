@@ -103,6 +103,16 @@ static int env_default(const char *name, int dflt)
 }
 static std::atomic<int> g_opt_path{-1};
 static std::atomic<int> g_opt_graphs{-1};
+static std::atomic<int> g_opt_pdl{-1};
+int opt_pdl()
+{
+    int v = g_opt_pdl.load();
+    if (v < 0) {
+        v = env_default("MFX_PDL", 1);
+        g_opt_pdl.store(v);
+    }
+    return v;
+}
 int opt_solver_path()
 {
     int v = g_opt_path.load();
@@ -281,6 +291,10 @@ API mfx_status mfx_set_option(const char *key, int value)
         g_opt_graphs.store(value ? 1 : 0);
         return MFX_OK;
     }
+    if (!strcmp(key, "pdl")) {
+        g_opt_pdl.store(value ? 1 : 0);
+        return MFX_OK;
+    }
     set_error("unknown option '%s'", key);
     return MFX_ERR_ARG;
 }
@@ -290,5 +304,6 @@ API int mfx_get_option(const char *key)
     if (!key) return -1;
     if (!strcmp(key, "solver_path")) return opt_solver_path();
     if (!strcmp(key, "graphs")) return opt_graphs();
+    if (!strcmp(key, "pdl")) return opt_pdl();
     return -1;
 }

@@ -382,6 +382,8 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
                                                const double *__restrict__ p, const double *__restrict__ v,
                                                const double *__restrict__ t, WsHeader *h, dd *part, int rev)
 {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     SolverScalars &S = h->sc;
     if (S.done || S.skip) return;
     const double alpha = S.alpha, omega = S.omega;
@@ -473,7 +475,18 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
         long long np = G.N / 2;
         int g3 = k3v_grid();
         if ((long long)g3 * kThreads > np) g3 = (int)((np + kThreads - 1) / kThreads);
-        k3v<<<g3, kThreads, 0, s>>>(G.N, x, W.r, W.rh, p_new, v_new, W.t, W.hdr, W.part, sweep_dir(true));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g3);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = opt_pdl() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k3v, G.N, x, W.r, (const double *)W.rh, (const double *)p_new,
+                                        (const double *)v_new, (const double *)W.t, W.hdr, W.part,
+                                        sweep_dir(true)));
     }
     count_launch(3, s, false);
     (void)nb;

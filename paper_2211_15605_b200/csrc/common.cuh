@@ -232,6 +232,7 @@ void count_launch(int id, cudaStream_t s, bool start);
 bool prof_enabled();
 int opt_solver_path();   // 0 auto, 1 TMA, 2 cluster, 3 v1
 int opt_graphs();
+int opt_pdl();
 bool cluster_fits(const Geo &G, bool sym);
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s);

@@ -89,6 +89,8 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap *map)
 {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -212,6 +214,22 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
+    // Programmatic dependent launch: let the next kernel in the stream start its
+    // launch and prologue while this grid drains; everything below the wait
+    // reads data the previous kernel produced.
+    pdl_trigger();
+    const int ntiles = a.tiles_x * a.tiles_y;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    pdl_wait();
+
     // ---- scalar prologue (uniform across the grid)
     double beta = 0.0, omega = 0.0, alpha = 0.0, rho = 0.0, rhn = 0.0;
     bool rst = false, newly = false;
@@ -239,16 +257,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             alpha = Sc.alpha;
         }
     }
-
-    const int ntiles = a.tiles_x * a.tiles_y;
-    if (tid == 0) {
-        for (int s = 0; s < S; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], C::NW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
 
     constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
     Acc acc[ND][C::CPT];   // one accumulator per dot and owned cell: independent TwoSum chains
@@ -618,8 +626,17 @@ struct Launcher {
         a.Lz = choose_lz(ntiles, G.nz, grid);
         a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
         if (grid > a.units) grid = (int)a.units;
-        k_stencil<MODE, SYM, TX, TY, CPT_, S><<<grid, C::NT + 32, smem_bytes<C>(S), s>>>(M, a);
-        MFX_CUDA_TRY(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C::NT + 32);
+        cfg.dynamicSmemBytes = smem_bytes<C>(S);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = opt_pdl() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil<MODE, SYM, TX, TY, CPT_, S>, M, a));
         return MFX_OK;
     }
 };

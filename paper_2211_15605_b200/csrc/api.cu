@@ -108,7 +108,7 @@ int opt_pdl()
 {
     int v = g_opt_pdl.load();
     if (v < 0) {
-        v = env_default("MFX_PDL", 1);
+        v = env_default("MFX_PDL", 0);   // off: measured slower (early dependent CTAs unbalance the persistent grids)
         g_opt_pdl.store(v);
     }
     return v;

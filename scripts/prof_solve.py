@@ -46,7 +46,9 @@ for r in range(args.repeat):
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    print(f"{args.kind} iters={info['iters']} ms={ms:.3f} us/iter={1e3 * ms / max(info['iters'], 1):.1f}", flush=True)
+    tag = "instrumented(no graphs)" if r == args.repeat - 1 else ("first(capture)" if r == 0 else "timed")
+    print(f"{args.kind} [{tag}] iters={info['iters']} ms={ms:.3f} us/iter={1e3 * ms / max(info['iters'], 1):.1f}",
+          flush=True)
 mfx.prof_enable(False)
 pr_ = mfx.prof_read()
 line = []

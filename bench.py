@@ -146,6 +146,69 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- other BASELINE grids
+def measure_other_configs(mfx, torch):
+    """Side measurements on the other BASELINE.json grids (same kernels, N=1):
+    config 1: the p' BiCGSTAB solve (tol 1e-6, maxit 5000) on 16x16x32 (single-
+    cluster solver); configs 3 and 4: SIMPLE outer iterations '111[1]' on
+    64x64x256 and 256x256x512 (4 equations on one GPU)."""
+    import numpy as np
+    import synth
+    out = {}
+    # config 1: p' system from the GPU's own momentum predictors
+    g, pr, st = synth.config_case(1)
+    pr.lin_maxit_pp = 5000
+    sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    ctx.step({k: v.clone() for k, v in sd.items()})
+    star = [ctx.buffer(k) for k in ("u*", "v*", "w*", "dx", "dy", "dz")]
+    ws = mfx.Workspace(g)
+    sysd, _ = mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws, star=star)
+    ctx.close()
+    times, iters = [], 0
+    for rep in range(12):
+        x = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        info = mfx.bicgstab_solve(mfx.EQ_PP, g, sysd, x, pr.lin_tol_pp, pr.lin_maxit_pp, ws)
+        e1.record()
+        torch.cuda.synchronize()
+        if rep >= 2:
+            times.append(e0.elapsed_time(e1))
+        iters = info["iters"]
+    ms = float(np.median(times))
+    out["c1"] = {"workload": "p' BiCGSTAB solve 16x16x32, tol 1e-6 (single-cluster solver)",
+                 "iters": iters, "ms_per_solve": ms, "us_per_iter": 1e3 * ms / iters,
+                 "bicgstab_iters_per_s": iters / (ms / 1e3)}
+    for cid, steps in ((3, 5), (4, 3)):
+        g, pr, st = synth.config_case(cid)
+        sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+        ctx = mfx.SimpleContext("111[1]", g, pr)
+        ctx.step(sd)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        its = 0
+        for _ in range(steps):
+            o = ctx.step(sd)
+            its += sum(o["iters"][:4])
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        ph = ctx.phase_times()
+        pp_it = max(o["iters"][3], 1)
+        out[f"c{cid}"] = {"workload": f"SIMPLE outer iteration 111[1] on {g.nx}x{g.ny}x{g.nz}",
+                          "simple_iters_per_s": steps / (ms / 1e3),
+                          "bicgstab_iters_per_s": its / (ms / 1e3),
+                          "pp_us_per_iter": 1e3 * ph["pp"] / pp_it,
+                          "pp_alg_GBps": 200 * g.n / (1e-3 * ph["pp"] / pp_it) / 1e9,
+                          "iters_last": o["iters"][:4]}
+        ctx.close()
+        del sd
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- product arm
 def run_mfx(args, rank, world, local_rank):
     import numpy as np
@@ -278,6 +341,10 @@ def run_mfx(args, rank, world, local_rank):
         e_ms = float(tt[0].item())
     e2e_value = e2e_iters / (e_ms / 1e3)
 
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = measure_other_configs(mfx, torch)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         step = oracle_sample()
@@ -310,7 +377,8 @@ def run_mfx(args, rank, world, local_rank):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "steps": e2e_steps},
                 "gpu_launches": launches,
-                "clocks": clk}
+                "clocks": clk,
+                "other_configs": extras}
         print(json.dumps(line), flush=True)
     ctx.close()
 
@@ -322,6 +390,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mfx", choices=["mfx", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config 1/3/4 side measurements")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

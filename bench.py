@@ -307,10 +307,17 @@ def run_mfx(args, rank, world, local_rank):
         per_launch_ms = prof[kern]["ms"] / prof[kern]["launches"]
         alg = BYTES_PER_CELL[kern] * n
         achieved = alg / (per_launch_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f)["dram_bytes_per_launch"].get(kern)
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_kind,
                 "alg_bytes_per_launch": alg, "avg_launch_us": per_launch_ms * 1e3,
-                "traffic": None, "share_of_step": prof[kern]["ms"] / t_prof_ms,
+                "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
+                "share_of_step": prof[kern]["ms"] / t_prof_ms,
                 "timing": "CUDA events around each launch on its stream, instrumented replay of the timed steps"}
     kern_ms = {k: (prof[k]["ms"] / prof[k]["launches"] if prof[k]["launches"] else None) for k in prof}
     # whole-iteration algorithmic bandwidth of the p' solve (K1 + K2 + K3 per iteration)

@@ -39,7 +39,10 @@ BYTES_PER_CELL = {
     "K1_pp": 4 * 8 + 2 * 8 + 4 * 8,      # symmetric p' storage: aP, c_x, c_y, c_z
     "K2_pp": 2 * 8 + 1 * 8 + 4 * 8,
     "K3": 6 * 8 + 2 * 8,                 # x, p, r, v, t, r^ read; x, r write
-    "spmv_setup": None, "assemble": None, "correct": None,
+    "assemble_mom": 9 * 8 + 9 * 8,       # eps, eps0, u, v, w, c_old, p, beta, S read; 7 coef + b + d write
+    "assemble_pp": 8 * 8 + 5 * 8,        # eps, eps0, u*, v*, w*, d_x, d_y, d_z read; aP, c_x, c_y, c_z, b write
+    "correct": 8 * 8 + 4 * 8,            # u*, v*, w*, d_x, d_y, d_z, p', p read; u, v, w, p write
+    "spmv_setup": None, "assemble_scalar": None,
 }
 
 
@@ -320,6 +323,15 @@ def run_mfx(args, rank, world, local_rank):
                 "share_of_step": prof[kern]["ms"] / t_prof_ms,
                 "timing": "CUDA events around each launch on its stream, instrumented replay of the timed steps"}
     kern_ms = {k: (prof[k]["ms"] / prof[k]["launches"] if prof[k]["launches"] else None) for k in prof}
+    # every kernel class with a byte model: achieved algorithmic GB/s and fraction of the measured peak
+    kernels_roof = {}
+    for k, v in prof.items():
+        if v["launches"] and BYTES_PER_CELL.get(k):
+            us = 1e3 * v["ms"] / v["launches"]
+            gbs = BYTES_PER_CELL[k] * n / (us * 1e-6) / 1e9 if (n := g.n) else 0.0
+            kernels_roof[k] = {"launches": v["launches"], "avg_us": us, "alg_bytes": BYTES_PER_CELL[k] * g.n,
+                               "achieved_GBps": gbs, "frac": gbs / load_peaks()[0],
+                               "share_of_step": v["ms"] / t_prof_ms}
     # whole-iteration algorithmic bandwidth of the p' solve (K1 + K2 + K3 per iteration)
     pp_iter_bytes = (BYTES_PER_CELL["K1_pp"] + BYTES_PER_CELL["K2_pp"] + BYTES_PER_CELL["K3"]) * n
 
@@ -380,6 +392,7 @@ def run_mfx(args, rank, world, local_rank):
                                  "alg_GBps": pp_iter_bytes / (1e-3 * phase["pp"] / max(outs[-1]["iters"][3], 1)) / 1e9},
                 "instrumented_ms_per_step": t_prof_ms / args.steps,
                 "roofline": roof,
+                "kernels": kernels_roof,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "steps": e2e_steps},

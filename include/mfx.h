@@ -178,6 +178,7 @@ mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_x
 mfx_status mfx_nccl_unique_id(unsigned char out[128]);
 
 typedef struct mfx_ctx mfx_ctx;
+typedef struct mfx_local_group mfx_local_group;
 
 /* Creates the per-rank context: parses the assignment, allocates the solver
  * workspaces and exchange buffers for the equations this rank owns, and (for
@@ -185,6 +186,16 @@ typedef struct mfx_ctx mfx_ctx;
 mfx_status mfx_ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid,
                           const mfx_grid *grid, const mfx_params *params, mfx_ctx **out);
 void mfx_ctx_destroy(mfx_ctx *ctx);
+
+/* In-process transport (no NCCL): the ranks of a group are host threads of
+ * one process, each calling mfx_simple_iter on its own stream (same or
+ * different GPUs).  The exchange plan runs as device-to-device pull copies
+ * ordered by CUDA events and host barriers.  Used to exercise the multi-rank
+ * path on one GPU and for single-node runs without NCCL. */
+mfx_status mfx_local_group_create(int nranks, mfx_local_group **out);
+void mfx_local_group_destroy(mfx_local_group *group);
+mfx_status mfx_ctx_create_local(const char *assignment, int rank, int nranks, mfx_local_group *group,
+                                const mfx_grid *grid, const mfx_params *params, mfx_ctx **out);
 
 /* a-8: execute `phase` of the exchange plan on the context's buffers
  * (fields = MFX_NBUF device pointers indexed by MFX_BUF_*; unused may be NULL). */
@@ -209,11 +220,12 @@ mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
 /* ---------------------------------------------------------------- instrumentation */
 /* Kernel timing with CUDA events recorded on the launching stream around
  * every hot kernel launch (off by default).  ids: 0 spmv/setup, 1 K1 (momentum/
- * scalar), 2 K2 (momentum/scalar), 3 K3, 4 assemble, 5 correct, 6 K1 (p'), 7 K2 (p').  mfx_prof_read synchronises the device and
+ * scalar), 2 K2 (momentum/scalar), 3 K3, 4 momentum assembly, 5 correct, 6 K1 (p'), 7 K2 (p'),
+ * 8 p' assembly, 9 scalar assembly (the single-cluster solve is timed under id 0).  mfx_prof_read synchronises the device and
  * returns, per id, launches and total milliseconds since mfx_prof_reset. */
 void mfx_prof_enable(int on);
 void mfx_prof_reset(void);
-mfx_status mfx_prof_read(int counts[8], double ms[8]);
+mfx_status mfx_prof_read(int counts[16], double ms[16]);
 /* Runtime options (process-wide).  "solver_path": 0 = auto (cluster kernel
  * when the system fits one cluster's shared memory, else TMA z-marching),
  * 1 = TMA z-marching kernels, 2 = single-cluster persistent kernel,

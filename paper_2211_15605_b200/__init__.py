@@ -102,6 +102,10 @@ _sigs = {
     "mfx_ctx_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(Grid), C.POINTER(Params),
                                  C.POINTER(_V)]),
     "mfx_ctx_destroy": (None, [_V]),
+    "mfx_local_group_create": (C.c_int, [C.c_int, C.POINTER(_V)]),
+    "mfx_local_group_destroy": (None, [_V]),
+    "mfx_ctx_create_local": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _V, C.POINTER(Grid), C.POINTER(Params),
+                                       C.POINTER(_V)]),
     "mfx_exchange_state": (C.c_int, [_V, C.c_int, C.POINTER(_V), _V]),
     "mfx_simple_iter": (C.c_int, [_V, C.POINTER(State), C.POINTER(Resid), _V]),
     "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
@@ -274,15 +278,36 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-class SimpleContext:
-    """Per-rank equation-decomposition context (mfx_ctx)."""
+class LocalGroup:
+    """In-process transport for `nranks` thread-ranks (mfx_local_group)."""
 
-    def __init__(self, assignment: str, grid, params, rank: int = 0, nranks: int = 1, uid: bytes | None = None):
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.ptr = C.c_void_p()
+        _check(_lib.mfx_local_group_create(nranks, C.byref(self.ptr)), "mfx_local_group_create")
+
+    def close(self):
+        if self.ptr:
+            _lib.mfx_local_group_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+class SimpleContext:
+    """Per-rank equation-decomposition context (mfx_ctx).  Transport: NCCL when
+    `uid` is given (one process per GPU), the in-process LocalGroup when
+    `group` is given (thread-ranks), none for nranks == 1."""
+
+    def __init__(self, assignment: str, grid, params, rank: int = 0, nranks: int = 1, uid: bytes | None = None,
+                 group: LocalGroup | None = None):
         self.grid, self.params = grid, params
         self._g, self._p = c_grid(grid), c_params(params)
         self.ptr = C.c_void_p()
-        _check(_lib.mfx_ctx_create(assignment.encode(), rank, nranks, uid, C.byref(self._g), C.byref(self._p),
-                                   C.byref(self.ptr)), "mfx_ctx_create")
+        if group is not None:
+            _check(_lib.mfx_ctx_create_local(assignment.encode(), rank, nranks, group.ptr, C.byref(self._g),
+                                             C.byref(self._p), C.byref(self.ptr)), "mfx_ctx_create_local")
+        else:
+            _check(_lib.mfx_ctx_create(assignment.encode(), rank, nranks, uid, C.byref(self._g), C.byref(self._p),
+                                       C.byref(self.ptr)), "mfx_ctx_create")
         self.assignment = parse_assignment(assignment, nranks)
 
     def step(self, state: dict, stream=None) -> dict:
@@ -335,7 +360,8 @@ def device_view(ptr: int, n: int):
 
 
 # ---------------------------------------------------------------- instrumentation
-PROF_IDS = ("spmv_setup", "K1_mom", "K2_mom", "K3", "assemble", "correct", "K1_pp", "K2_pp")
+PROF_IDS = ("spmv_setup", "K1_mom", "K2_mom", "K3", "assemble_mom", "correct", "K1_pp", "K2_pp",
+            "assemble_pp", "assemble_scalar")
 
 
 def prof_enable(on: bool = True):
@@ -347,8 +373,8 @@ def prof_reset():
 
 
 def prof_read():
-    counts = (C.c_int * 8)()
-    ms = (C.c_double * 8)()
+    counts = (C.c_int * 16)()
+    ms = (C.c_double * 16)()
     _check(_lib.mfx_prof_read(counts, ms), "mfx_prof_read")
     return {PROF_IDS[i]: dict(launches=counts[i], ms=ms[i]) for i in range(len(PROF_IDS))}
 

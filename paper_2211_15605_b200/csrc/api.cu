@@ -80,7 +80,7 @@ static cudaEvent_t get_event()
 void count_launch(int id, cudaStream_t s, bool start)
 {
     if (!start) g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (!g_prof.load(std::memory_order_relaxed) || id >= 8) return;
+    if (!g_prof.load(std::memory_order_relaxed) || id >= 12) return;
     if (start) {
         g_pending = get_event();
         cudaEventRecord(g_pending, s);
@@ -149,7 +149,7 @@ mfx_status parse_assignment(const char *, int, mfx_assignment *);
 mfx_status exchange_plan(const mfx_assignment *, int, int, mfx_xfer *, int, int *);
 mfx_status nccl_unique_id(unsigned char out[128]);
 mfx_status ctx_create(const char *, int, int, const unsigned char *, const mfx_grid *, const mfx_params *,
-                      mfx_ctx **);
+                      mfx_ctx **, mfx_local_group *);
 mfx_status exchange_state(mfx_ctx *, int, double *const[MFX_NBUF], cudaStream_t);
 mfx_status simple_iter(mfx_ctx *, mfx_state *, mfx_resid *, cudaStream_t);
 
@@ -239,7 +239,7 @@ API mfx_status mfx_nccl_unique_id(unsigned char out[128]) { return nccl_unique_i
 API mfx_status mfx_ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid,
                               const mfx_grid *grid, const mfx_params *params, mfx_ctx **out)
 {
-    return ctx_create(assignment, rank, nranks, uid, grid, params, out);
+    return ctx_create(assignment, rank, nranks, uid, grid, params, out, nullptr);
 }
 
 API mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_NBUF], void *stream)
@@ -261,11 +261,11 @@ API void mfx_prof_reset(void)
     g_recs.clear();
 }
 
-API mfx_status mfx_prof_read(int counts[8], double ms[8])
+API mfx_status mfx_prof_read(int counts[16], double ms[16])
 {
     MFX_ARG_CHECK(counts && ms, "NULL out");
     MFX_CUDA_TRY(cudaDeviceSynchronize());
-    for (int q = 0; q < 8; q++) { counts[q] = 0; ms[q] = 0.0; }
+    for (int q = 0; q < 16; q++) { counts[q] = 0; ms[q] = 0.0; }
     std::lock_guard<std::mutex> lk(g_mu);
     for (auto &r : g_recs) {
         float t = 0.f;

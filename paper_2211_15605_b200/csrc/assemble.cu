@@ -505,9 +505,9 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         for (int t = 0; t < 3; t++) { a.us[t] = star[t]; a.dv[t] = star[3 + t]; }
         a.aP = out->aP; a.cx = out->aE; a.cy = out->aN; a.cz = out->aT; a.b = out->b;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
-        count_launch(4, s, true);
+        count_launch(8, s, true);
         k_assemble_pp<<<nb, kThreads, 0, s>>>(a);
-        count_launch(4, s, false);
+        count_launch(8, s, false);
     } else {
         MFX_ARG_CHECK(sid >= 0 && sid < 4, "scalar id %d", sid);
         MFX_ARG_CHECK(st->eps && st->eps_old && st->u && st->v && st->w && st->phi[sid] && st->phi_old[sid],
@@ -526,9 +526,9 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
-        count_launch(4, s, true);
+        count_launch(9, s, true);
         k_assemble_scalar<<<nb, kThreads, 0, s>>>(a);
-        count_launch(4, s, false);
+        count_launch(9, s, false);
     }
     MFX_CUDA_TRY(cudaGetLastError());
     return MFX_OK;

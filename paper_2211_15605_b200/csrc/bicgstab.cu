@@ -648,7 +648,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     }
     count_launch(0, s, false);
     k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
-    count_launch(8, s, false);
+    count_launch(15, s, false);
     MFX_CUDA_TRY(cudaGetLastError());
     int launched = 0, chunk = 4;
     while (launched < maxit) {

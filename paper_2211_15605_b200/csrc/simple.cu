@@ -12,9 +12,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -187,6 +189,36 @@ mfx_status nccl_unique_id(unsigned char out[128])
 
 }  // namespace mfx
 
+// ------------------------------------------------------------------ local transport
+// In-process transport: ranks are host threads of one process (same or
+// different GPUs), each with its own stream.  The exchange plan is executed as
+// pull copies: every rank publishes its buffer pointers and records a "ready"
+// event, a host barrier orders publication before use, receivers/non-roots
+// wait on the producer's event and copy peer-to-peer, and a second barrier +
+// "done" events keep producers from overwriting a buffer still being read.
+struct mfx_local_group {
+    int nranks;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long gen = 0;
+    double *fields[64][MFX_NBUF];
+    cudaEvent_t ready[64];
+    cudaEvent_t done[64];
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const unsigned long g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            gen++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
 // ------------------------------------------------------------------ context
 struct mfx_ctx {
     int rank, nranks;
@@ -205,6 +237,7 @@ struct mfx_ctx {
     double *meta;            // device [8][16]
     double *meta_host;       // pinned [8][16]
     ncclComm_t comm;
+    mfx_local_group *group;  // non-NULL: in-process transport instead of NCCL
     cudaEvent_t ev[6];
     double phase_ms[6];
 };
@@ -219,7 +252,7 @@ static mfx_status ctx_alloc(mfx_ctx *c, void **p, size_t bytes)
 }
 
 mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsigned char *uid, const mfx_grid *grid,
-                      const mfx_params *params, mfx_ctx **out)
+                      const mfx_params *params, mfx_ctx **out, mfx_local_group *group = nullptr)
 {
     MFX_ARG_CHECK(out && params, "NULL out/params");
     *out = nullptr;
@@ -228,11 +261,14 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     mfx_assignment a;
     mfx_status st = parse_assignment(assignment, nranks, &a);
     if (st != MFX_OK) return st;
-    MFX_ARG_CHECK(nranks == 1 || uid, "uid required for nranks > 1");
+    MFX_ARG_CHECK(nranks == 1 || uid || group, "uid (NCCL) or a local group required for nranks > 1");
+    MFX_ARG_CHECK(!group || group->nranks == nranks, "local group has %d ranks, expected %d",
+                  group ? group->nranks : 0, nranks);
     mfx_ctx *c = new mfx_ctx();
     c->rank = rank; c->nranks = nranks; c->asg = a; c->grid = *grid; c->params = *params;
     c->N = (long long)grid->nx * grid->ny * grid->nz;
     c->comm = nullptr;
+    c->group = group;
     const size_t vb = round256(sizeof(double) * c->N);
     c->ws_bytes = ws_total_bytes(c->N);
     auto fail = [&](mfx_status s) { mfx_ctx_destroy(c); return s; };
@@ -299,7 +335,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
         if (cudaEventCreate(&c->ev[q]) != cudaSuccess) return fail(MFX_ERR_CUDA);
         c->phase_ms[q] = 0.0;
     }
-    if (nranks > 1) {
+    if (nranks > 1 && !group) {
         if (!g_nccl.load()) return fail(MFX_ERR_NCCL);
         ncclUniqueId id;
         memcpy(&id, uid, 128);
@@ -322,6 +358,36 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     int n = 0;
     mfx_status st = exchange_plan(&c->asg, c->rank, phase, ops, 64, &n);
     if (st != MFX_OK) return st;
+    if (c->group) {
+        mfx_local_group &g = *c->group;
+        for (int b = 0; b < MFX_NBUF; b++) g.fields[c->rank][b] = fields[b];
+        MFX_CUDA_TRY(cudaEventRecord(g.ready[c->rank], s));
+        g.barrier();
+        for (int q = 0; q < n; q++) {
+            const mfx_xfer &o = ops[q];
+            if (o.op == MFX_OP_SEND || (o.op == MFX_OP_BCAST && o.peer == c->rank)) continue;
+            double *dst = fields[o.buf];
+            const double *src = g.fields[o.peer][o.buf];
+            size_t count = (size_t)c->N;
+            if (o.buf == MFX_BUF_META) {
+                dst += 16 * o.slot;
+                src += 16 * o.slot;
+                count = 16 * (size_t)o.nslots;
+            }
+            if (!dst || !src) {
+                set_error("local exchange: buffer %d missing (rank %d <- %d)", o.buf, c->rank, o.peer);
+                return MFX_ERR_ARG;
+            }
+            MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[o.peer], 0));
+            MFX_CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDefault, s));
+        }
+        MFX_CUDA_TRY(cudaEventRecord(g.done[c->rank], s));
+        g.barrier();
+        for (int q = 0; q < g.nranks; q++)
+            if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.done[q], 0));
+        g.barrier();   // every rank has enqueued its waits before any event is re-recorded
+        return MFX_OK;
+    }
     MFX_NCCL_TRY(g_nccl.GroupStart());
     for (int q = 0; q < n; q++) {
         const mfx_xfer &o = ops[q];
@@ -442,6 +508,41 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
 }
 
 }  // namespace mfx
+
+mfx_status mfx_local_group_create(int nranks, mfx_local_group **out)
+{
+    MFX_ARG_CHECK(out && nranks >= 1 && nranks <= 64, "bad arguments");
+    mfx_local_group *g = new mfx_local_group();
+    g->nranks = nranks;
+    for (int q = 0; q < nranks; q++) {
+        for (int b = 0; b < MFX_NBUF; b++) g->fields[q][b] = nullptr;
+        if (cudaEventCreateWithFlags(&g->ready[q], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g->done[q], cudaEventDisableTiming) != cudaSuccess) {
+            mfx::set_error("cudaEventCreate failed");
+            delete g;
+            return MFX_ERR_CUDA;
+        }
+    }
+    *out = g;
+    return MFX_OK;
+}
+
+void mfx_local_group_destroy(mfx_local_group *g)
+{
+    if (!g) return;
+    for (int q = 0; q < g->nranks; q++) {
+        cudaEventDestroy(g->ready[q]);
+        cudaEventDestroy(g->done[q]);
+    }
+    delete g;
+}
+
+mfx_status mfx_ctx_create_local(const char *assignment, int rank, int nranks, mfx_local_group *group,
+                                const mfx_grid *grid, const mfx_params *params, mfx_ctx **out)
+{
+    MFX_ARG_CHECK(group, "NULL group");
+    return mfx::ctx_create(assignment, rank, nranks, nullptr, grid, params, out, group);
+}
 
 void mfx_ctx_destroy(mfx_ctx *c)
 {

@@ -1,1 +1,1 @@
-timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['pp_iteration'], json.dumps(d['other_configs'], indent=1))"
+timeout 1200 python -m pytest tests/test_gpu_multirank.py -x -q 2>&1 | tail -15

@@ -1,0 +1,91 @@
+"""Multi-rank equation decomposition on the GPU:
+thread-ranks sharing the one B200 through libmfx's in-process transport run
+mfx_simple_iter concurrently, each on its own stream, with the assignment
+strings of the paper.  Every rank must end with exactly the state of the
+single-rank "111[1]" iteration and of the CPU oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mfx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2211_15605_b200 as m
+    return m
+
+
+def make_case(n_scalars):
+    g = synth.make_grid(24, 14, 30)
+    pr = synth.Params(lin_maxit_pp=1500)
+    st = synth.make_state(g, 2468, pr, n_scalars=n_scalars)
+    rng = np.random.default_rng(5)
+    for s in range(n_scalars):
+        st[f"phi_old{s}"] = rng.uniform(0, 1, g.n)
+        st[f"phi{s}"] = st[f"phi_old{s}"].copy()
+    return g, pr, st
+
+
+def run_ranks(mfx, assignment, nranks, g, pr, st, outer=2):
+    group = mfx.LocalGroup(nranks)
+    results, errors = {}, []
+    barrier = threading.Barrier(nranks)
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+                ctx = mfx.SimpleContext(assignment, g, pr, rank=rank, nranks=nranks, group=group)
+                barrier.wait()
+                outs = [ctx.step(sd, stream=stream) for _ in range(outer)]
+                stream.synchronize()
+                results[rank] = ({k: v.cpu().numpy() for k, v in sd.items()}, outs)
+                ctx.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((rank, repr(e)))
+            barrier.abort()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    group.close()
+    assert not errors, errors
+    return results
+
+
+@pytest.mark.parametrize("assignment,nranks,n_scalars", [
+    ("222[1]", 2, 0),
+    ("234[1]", 4, 0),
+    ("121[2]", 2, 0),
+    ("234[1]5678", 8, 4),
+    ("111[1]2", 2, 1),
+])
+def test_multirank_equals_single_rank(mfx, orc, assignment, nranks, n_scalars):
+    g, pr, st = make_case(n_scalars)
+    single = run_ranks(mfx, "111[1]" + "1" * n_scalars, 1, g, pr, st)
+    multi = run_ranks(mfx, assignment, nranks, g, pr, st)
+    keys = ("u", "v", "w", "p") + tuple(f"phi{s}" for s in range(n_scalars))
+    ref_state, ref_outs = single[0]
+    for rank in range(nranks):
+        state, outs = multi[rank]
+        for k in keys:
+            assert np.array_equal(state[k], ref_state[k]), (rank, k)
+        for o, r in zip(outs, ref_outs):
+            assert o["R"] == r["R"] and o["iters"] == r["iters"], (rank, o, r)
+    # and the single-rank GPU iteration equals the oracle's two outer iterations
+    s = st
+    for _ in range(2):
+        s, R, iters, status, rc = orc.simple_iter(g, pr, s, n_scalars=n_scalars)
+    for k in keys:
+        assert np.array_equal(ref_state[k], s[k]), k

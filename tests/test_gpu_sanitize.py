@@ -1,0 +1,28 @@
+"""compute-sanitizer memcheck/racecheck/synccheck over one SIMPLE iteration
+(assembly, TMA z-marching kernels with mbarrier rings, K3, single-cluster
+solver with DSMEM, correction) on a ragged grid (SURVEY §4 tests/sanitize)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("path", [1, 2])
+def test_sanitizer_clean(tool, path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not found")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "scripts", "sanitize_case.py"), str(path)],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert ("0 errors" in r.stdout) or ("0 hazards" in r.stdout)

@@ -94,18 +94,42 @@ __device__ __forceinline__ double mflux_t(const MomArgs &a, int t, const int X[3
     return ((a.rho * ef) * G.A[t]) * __ldg(vfield<C>(a, t) + lin(G, X));
 }
 
+// Clamped neighbour index (always a valid cell; values read at clamped
+// positions are only used where DESIGN.md §3.3 says the neighbour exists).
+__device__ __forceinline__ long long lin_cl(const Geo &G, int i, int j, int k)
+{
+    i = i < 0 ? 0 : (i >= G.nx ? G.nx - 1 : i);
+    j = j < 0 ? 0 : (j >= G.ny ? G.ny - 1 : j);
+    k = k < 0 ? 0 : (k >= G.nz ? G.nz - 1 : k);
+    return (long long)i + (long long)G.nx * ((long long)j + (long long)G.ny * k);
+}
+
+__device__ __forceinline__ void decode32(const Geo &G, long long n, int q[3])
+{
+    const unsigned int un = (unsigned int)n, sz = (unsigned int)G.sz, nx = (unsigned int)G.nx;
+    const unsigned int k = un / sz, rem = un - k * sz, j = rem / nx;
+    q[0] = (int)(rem - j * nx);
+    q[1] = (int)j;
+    q[2] = (int)k;
+}
+
+// Momentum row.  Every neighbour value the row can need is
+// loaded first, unconditionally, from clamped indices (34 independent loads in
+// flight per thread); the boundary rules then only select among them.
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
 {
     const Geo &G = a.G;
+    constexpr int T1 = C == 0 ? 1 : 0, T2 = C == 2 ? 1 : 2;   // transverse axes
     Acc num, den;
     num.zero();
     den.zero();
     const double *um = vfield<C>(a, C);
+    const double *vt[2] = {vfield<C>(a, T1), vfield<C>(a, T2)};
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
          n += (long long)gridDim.x * blockDim.x) {
         int P[3];
-        decode(G, n, P);
+        decode32(G, n, P);
         const int type = row_type<C>(G, P);
         if (type == kIdentity) {
             a.aP[n] = 1.0;
@@ -117,52 +141,89 @@ __global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
         int E[3] = {P[0], P[1], P[2]};
         if (type == kInterior) E[C] += 1;
         const long long nE = lin(G, E);
+        // ---- gather
         const double epsP = __ldg(a.eps + n), epsE = __ldg(a.eps + nE);
+        double epsPt[2][2], epsEt[2][2], vP[2][2], vE[2][2];   // [transverse t][side: 0 = -, 1 = +]
+#pragma unroll
+        for (int ti = 0; ti < 2; ti++) {
+            const int t = ti == 0 ? T1 : T2;
+#pragma unroll
+            for (int sg = 0; sg < 2; sg++) {
+                const int s = sg ? 1 : -1;
+                int Pt[3] = {P[0], P[1], P[2]}, Et[3] = {E[0], E[1], E[2]};
+                Pt[t] += s;
+                Et[t] += s;
+                const long long iP = lin_cl(G, Pt[0], Pt[1], Pt[2]), iE = lin_cl(G, Et[0], Et[1], Et[2]);
+                epsPt[ti][sg] = __ldg(a.eps + iP);
+                epsEt[ti][sg] = __ldg(a.eps + iE);
+                // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
+                vP[ti][sg] = __ldg(vt[ti] + (s > 0 ? n : iP));
+                vE[ti][sg] = __ldg(vt[ti] + (s > 0 ? nE : iE));
+            }
+        }
+        int Pm[3] = {P[0], P[1], P[2]};
+        Pm[C] -= 1;
+        const double umP = __ldg(um + n);
+        const double umE = __ldg(um + nE);
+        const double umM = __ldg(um + lin_cl(G, Pm[0], Pm[1], Pm[2]));
+        double unb[6];                                            // residual neighbours W,E,S,N,B,T
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) {
+            int Q[3] = {P[0], P[1], P[2]};
+            Q[s6 / 2] += (s6 & 1) ? 1 : -1;
+            unb[s6] = in_dom(G, Q) ? __ldg(um + lin_cl(G, Q[0], Q[1], Q[2])) : 0.0;
+        }
+        const double e0P = __ldg(a.eps0 + n), e0E = __ldg(a.eps0 + nE);
+        const double bP = __ldg(a.beta + n), bE = __ldg(a.beta + nE);
+        const double SP = __ldg(a.S + n), SE = __ldg(a.S + nE);
+        const double pP = __ldg(a.p + n), pEv = __ldg(a.p + nE);
+        const double uoP = __ldg(a.uold + n);
 
+        // ---- row (same expressions as DESIGN.md §3.3)
         double as[6], phib[6];
         bool kept[6], inP[6];
 #pragma unroll
         for (int s6 = 0; s6 < 6; s6++) { as[s6] = 0.0; phib[s6] = 0.0; kept[s6] = false; inP[s6] = false; }
-
-#pragma unroll
-        for (int t = 0; t < 3; t++) {
-            if (t == C) {
-                int Qm[3] = {P[0], P[1], P[2]};
-                Qm[C] -= 1;
-                const double vP = vel_c<C>(a, P);
-                const double vm = vel_c<C>(a, Qm);
-                const double Fm = ((a.rho * epsP) * G.A[C]) * (0.5 * (vm + vP));
-                const double Dm = a.Dc[C] * epsP;
-                as[2 * C] = Dm + maxp(Fm);
-                inP[2 * C] = true;
-                if (P[C] >= 1) kept[2 * C] = true;
-                else phib[2 * C] = vm;                                   // B1
-                if (type == kOutlet) {
-                    as[2 * C + 1] = 0.0;                                 // B3
-                } else {
-                    const double Fp = ((a.rho * epsE) * G.A[C]) * (0.5 * (vP + vel_c<C>(a, E)));
-                    const double Dp = a.Dc[C] * epsE;
-                    as[2 * C + 1] = Dp + maxp(-Fp);
-                    inP[2 * C + 1] = true;
-                    if (row_type<C>(G, E) == kIdentity) phib[2 * C + 1] = 0.0;   // B1
-                    else kept[2 * C + 1] = true;
-                }
-                continue;
+        {
+            // main axis
+            double vm;
+            if (P[C] == 0) vm = (C == 2 && G.bc_zlo == MFX_BC_INLET) ? G.w_in : 0.0;
+            else vm = umM;
+            const double Fm = ((a.rho * epsP) * G.A[C]) * (0.5 * (vm + umP));
+            const double Dm = a.Dc[C] * epsP;
+            as[2 * C] = Dm + maxp(Fm);
+            inP[2 * C] = true;
+            if (P[C] >= 1) kept[2 * C] = true;
+            else phib[2 * C] = vm;                                            // B1
+            if (type == kOutlet) {
+                as[2 * C + 1] = 0.0;                                          // B3
+            } else {
+                const bool e_ident = row_type<C>(G, E) == kIdentity;
+                const double vE_ = e_ident ? 0.0 : umE;
+                const double Fp = ((a.rho * epsE) * G.A[C]) * (0.5 * (umP + vE_));
+                const double Dp = a.Dc[C] * epsE;
+                as[2 * C + 1] = Dp + maxp(-Fp);
+                inP[2 * C + 1] = true;
+                if (e_ident) phib[2 * C + 1] = 0.0;                           // B1
+                else kept[2 * C + 1] = true;
             }
+        }
 #pragma unroll
-            for (int sgn = 0; sgn < 2; sgn++) {
-                const int s = sgn ? 1 : -1;
-                const int side = 2 * t + sgn;
-                int Pt[3] = {P[0], P[1], P[2]};
-                Pt[t] += s;
-                int Et[3] = {E[0], E[1], E[2]};
-                Et[t] += s;
-                if (in_dom(G, Pt)) {
-                    const int *Q = s > 0 ? P : Pt;
-                    const int *R = s > 0 ? E : Et;
-                    const double F = 0.5 * (mflux_t<C>(a, t, Q) + mflux_t<C>(a, t, R));
-                    const double e4 = 0.25 * (((epsP + epsE) + __ldg(a.eps + lin(G, Pt))) +
-                                              __ldg(a.eps + lin(G, Et)));
+        for (int ti = 0; ti < 2; ti++) {
+            const int t = ti == 0 ? T1 : T2;
+#pragma unroll
+            for (int sg = 0; sg < 2; sg++) {
+                const int s = sg ? 1 : -1;
+                const int side = 2 * t + sg;
+                const int pt = P[t] + s;
+                if (pt >= 0 && pt < extent(G, t)) {
+                    // +t face mass fluxes of Q and R: eps at X and X + e_t
+                    const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
+                    const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
+                    const double mQ = ((a.rho * (0.5 * (eQ0 + eQ1))) * G.A[t]) * vP[ti][sg];
+                    const double mR = ((a.rho * (0.5 * (eR0 + eR1))) * G.A[t]) * vE[ti][sg];
+                    const double F = 0.5 * (mQ + mR);
+                    const double e4 = 0.25 * (((epsP + epsE) + epsPt[ti][sg]) + epsEt[ti][sg]);
                     const double D = a.Dc[t] * e4;
                     as[side] = D + maxp(s > 0 ? -F : F);
                     inP[side] = true;
@@ -170,13 +231,13 @@ __global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
                 } else {
                     int bc = MFX_BC_WALL;
                     if (t == 2) bc = s < 0 ? G.bc_zlo : G.bc_zhi;
-                    if (bc == MFX_BC_OUTLET) { as[side] = 0.0; continue; }   // B3
+                    if (bc == MFX_BC_OUTLET) continue;                        // B3
                     double F = 0.0;
                     if (bc == MFX_BC_INLET)
                         F = 0.5 * (((a.rho * epsP) * G.A[2]) * G.w_in + ((a.rho * epsE) * G.A[2]) * G.w_in);
                     const double e2 = 0.5 * (epsP + epsE);
                     const double D = a.Dc[t] * e2;
-                    as[side] = 2.0 * D + maxp(s > 0 ? -F : F);            // B2, phi_b = 0
+                    as[side] = 2.0 * D + maxp(s > 0 ? -F : F);                // B2, phi_b = 0
                     inP[side] = true;
                     phib[side] = 0.0;
                 }
@@ -188,15 +249,13 @@ __global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
         for (int s6 = 0; s6 < 6; s6++)
             if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
         const double ef = 0.5 * (epsP + epsE);
-        const double e0f = 0.5 * (__ldg(a.eps0 + n) + __ldg(a.eps0 + nE));
-        const double bf = 0.5 * (__ldg(a.beta + n) + __ldg(a.beta + nE));
-        const double Sf = 0.5 * (__ldg(a.S + n) + __ldg(a.S + nE));
-        const double pE = type == kOutlet ? 0.0 : __ldg(a.p + nE);
+        const double e0f = 0.5 * (e0P + e0E);
+        const double bf = 0.5 * (bP + bE);
+        const double Sf = 0.5 * (SP + SE);
+        const double pE = type == kOutlet ? 0.0 : pEv;
         const double a0 = a.rVdt * e0f;
         const double aP = (sum + a0) + bf * G.V;
-        const double bb = ((((a0 * __ldg(a.uold + n)) + (ef * G.A[C]) * (__ldg(a.p + n) - pE)) +
-                            ((a.rho * ef) * a.gc) * G.V) + Sf * G.V) + bcb;
-        const double umP = __ldg(um + n);
+        const double bb = ((((a0 * uoP) + (ef * G.A[C]) * (pP - pE)) + ((a.rho * ef) * a.gc) * G.V) + Sf * G.V) + bcb;
         const double aPr = aP / a.urf;
         const double bR = bb + (aPr - aP) * umP;
         const double dd_ = (ef * G.A[C]) / aPr;
@@ -214,12 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble_mom(MomArgs a)
 
         double res = bb - aP * umP;
 #pragma unroll
-        for (int s6 = 0; s6 < 6; s6++) {
-            int Q[3] = {P[0], P[1], P[2]};
-            Q[s6 / 2] += (s6 & 1) ? 1 : -1;
-            const double unb = in_dom(G, Q) ? __ldg(um + lin(G, Q)) : 0.0;
-            res = res + st6[s6] * unb;
-        }
+        for (int s6 = 0; s6 < 6; s6++) res = res + st6[s6] * unb[s6];
         num.add(fabs(res));
         den.add(fabs(aP * umP));
     }
@@ -242,49 +296,59 @@ struct PPArgs {
     dd *part;
 };
 
-// rho eps_f A q on the +a face of X
-__device__ __forceinline__ double plus_face(const PPArgs &a, int ax, const int X[3], const double *q)
-{
-    const Geo &G = a.G;
-    const long long nX = lin(G, X);
-    if (X[ax] <= extent(G, ax) - 2) {
-        int Y[3] = {X[0], X[1], X[2]};
-        Y[ax] += 1;
-        const double ef = 0.5 * (__ldg(a.eps + nX) + __ldg(a.eps + lin(G, Y)));
-        return ((a.rho * ef) * G.A[ax]) * __ldg(q + nX);
-    }
-    if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET) return ((a.rho * __ldg(a.eps + nX)) * G.A[2]) * __ldg(q + nX);
-    return 0.0;
-}
-
 __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
 {
+    // DESIGN.md §3.4; all 20 neighbour values loaded up front from clamped indices
     const Geo &G = a.G;
     Acc cont;
     cont.zero();
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
          n += (long long)gridDim.x * blockDim.x) {
         int P[3];
-        decode(G, n, P);
+        decode32(G, n, P);
+        const double epsP = __ldg(a.eps + n), eps0P = __ldg(a.eps0 + n);
+        double eM[3], eP[3], dP[3], dM[3], uP[3], uM[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            int Qm[3] = {P[0], P[1], P[2]}, Qp[3] = {P[0], P[1], P[2]};
+            Qm[ax] -= 1;
+            Qp[ax] += 1;
+            const long long im = lin_cl(G, Qm[0], Qm[1], Qm[2]), ip = lin_cl(G, Qp[0], Qp[1], Qp[2]);
+            eM[ax] = __ldg(a.eps + im);
+            eP[ax] = __ldg(a.eps + ip);
+            dP[ax] = __ldg(a.dv[ax] + n);
+            dM[ax] = __ldg(a.dv[ax] + im);
+            uP[ax] = __ldg(a.us[ax] + n);
+            uM[ax] = __ldg(a.us[ax] + im);
+        }
         double cm[3], cpl[3], mm[3], mp[3];
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
-            cpl[ax] = plus_face(a, ax, P, a.dv[ax]);
-            mp[ax] = plus_face(a, ax, P, a.us[ax]);
+            const int ext = extent(G, ax);
+            // +a face of P
+            if (P[ax] <= ext - 2) {
+                const double ef = 0.5 * (epsP + eP[ax]);
+                cpl[ax] = ((a.rho * ef) * G.A[ax]) * dP[ax];
+                mp[ax] = ((a.rho * ef) * G.A[ax]) * uP[ax];
+            } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET) {
+                cpl[ax] = ((a.rho * epsP) * G.A[2]) * dP[ax];
+                mp[ax] = ((a.rho * epsP) * G.A[2]) * uP[ax];
+            } else {
+                cpl[ax] = 0.0;
+                mp[ax] = 0.0;
+            }
+            // -a face of P = +a face of P - e_a (interior by construction)
             if (P[ax] >= 1) {
-                int Q[3] = {P[0], P[1], P[2]};
-                Q[ax] -= 1;
-                cm[ax] = plus_face(a, ax, Q, a.dv[ax]);
-                mm[ax] = plus_face(a, ax, Q, a.us[ax]);
+                const double ef = 0.5 * (eM[ax] + epsP);
+                cm[ax] = ((a.rho * ef) * G.A[ax]) * dM[ax];
+                mm[ax] = ((a.rho * ef) * G.A[ax]) * uM[ax];
             } else {
                 cm[ax] = 0.0;
-                mm[ax] = (ax == 2 && G.bc_zlo == MFX_BC_INLET) ? ((a.rho * __ldg(a.eps + n)) * G.A[2]) * G.w_in
-                                                               : 0.0;
+                mm[ax] = (ax == 2 && G.bc_zlo == MFX_BC_INLET) ? ((a.rho * epsP) * G.A[2]) * G.w_in : 0.0;
             }
         }
         const double aP = ((((cm[0] + cpl[0]) + cm[1]) + cpl[1]) + cm[2]) + cpl[2];
-        const double bb = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) -
-                          a.rVdt * (__ldg(a.eps + n) - __ldg(a.eps0 + n));
+        const double bb = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) - a.rVdt * (epsP - eps0P);
         a.aP[n] = aP;
         a.cx[n] = cpl[0];
         a.cy[n] = cpl[1];

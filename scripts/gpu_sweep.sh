@@ -1,6 +1,3 @@
-for tool in memcheck racecheck synccheck; do
-  for path in 1 2; do
-    echo "== $tool path $path"
-    timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py $path 2>&1 | grep -E "ERROR SUMMARY|path|Error|error" | head -8
-  done
-done
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q 2>&1 | tail -2
+timeout 900 python bench.py --steps 5 --warmup 3 --no-extras > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "
+import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['pp_iteration']['us']); print(json.dumps(d['kernels'], indent=0))"

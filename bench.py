@@ -323,15 +323,25 @@ def run_mfx(args, rank, world, local_rank):
                 "share_of_step": prof[kern]["ms"] / t_prof_ms,
                 "timing": "CUDA events around each launch on its stream, instrumented replay of the timed steps"}
     kern_ms = {k: (prof[k]["ms"] / prof[k]["launches"] if prof[k]["launches"] else None) for k in prof}
-    # every kernel class with a byte model: achieved algorithmic GB/s and fraction of the measured peak
+    # every kernel class with a byte model: achieved algorithmic GB/s and fraction of the measured peak.
+    # Solves that converge inside a launch chunk leave no-op launches behind (they exit at once), so the
+    # per-call time divides the total by the iterations actually executed (identical in both passes:
+    # the instrumented replay restarts from the same state and the solver is deterministic).
+    owner = ctx.assignment["owner"]
+    it_pp = sum(o["iters"][3] for o in outs if owner[3] >= 0)
+    it_mom = sum(o["iters"][q] for o in outs for q in range(3) if owner[q] >= 0)
+    it_sc = sum(o["iters"][q] for o in outs for q in range(4, 8) if owner[q] >= 0)
+    eff = {"K1_pp": it_pp, "K2_pp": it_pp, "K1_mom": it_mom + it_sc, "K2_mom": it_mom + it_sc,
+           "K3": it_pp + it_mom + it_sc}
     kernels_roof = {}
     for k, v in prof.items():
         if v["launches"] and BYTES_PER_CELL.get(k):
-            us = 1e3 * v["ms"] / v["launches"]
-            gbs = BYTES_PER_CELL[k] * n / (us * 1e-6) / 1e9 if (n := g.n) else 0.0
-            kernels_roof[k] = {"launches": v["launches"], "avg_us": us, "alg_bytes": BYTES_PER_CELL[k] * g.n,
-                               "achieved_GBps": gbs, "frac": gbs / load_peaks()[0],
-                               "share_of_step": v["ms"] / t_prof_ms}
+            calls = eff.get(k) or v["launches"]
+            us = 1e3 * v["ms"] / calls
+            gbs = BYTES_PER_CELL[k] * g.n / (us * 1e-6) / 1e9
+            kernels_roof[k] = {"launches": v["launches"], "executed": calls, "avg_us": us,
+                               "alg_bytes": BYTES_PER_CELL[k] * g.n, "achieved_GBps": gbs,
+                               "frac": gbs / load_peaks()[0], "share_of_step": v["ms"] / t_prof_ms}
     # whole-iteration algorithmic bandwidth of the p' solve (K1 + K2 + K3 per iteration)
     pp_iter_bytes = (BYTES_PER_CELL["K1_pp"] + BYTES_PER_CELL["K2_pp"] + BYTES_PER_CELL["K3"]) * n
 

@@ -12,6 +12,9 @@
 // Five cluster barriers per iteration; no kernel launches inside the loop.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -42,6 +45,7 @@ struct ClArgs {
     int maxit;
     int M;                 // smem stride: max cells owned by one CTA
     WsHeader *h;
+    long long *trace;      // optional: clock64 stamps of CTA 0 per phase (MFX_CLUSTER_TRACE)
 };
 
 // Cluster-wide correctly rounded reduction of K double-doubles: each warp
@@ -205,6 +209,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
 
     const double tol = a.tol;
     const int maxit = a.maxit;
+    int tix = 0;
+    auto stamp = [&]() {
+        if (a.trace && rank == 0 && tid == 0 && tix < 512) a.trace[tix++] = clock64();
+    };
     int status = MFX_NOT_CONVERGED, iters = 0, restarts = 0;
     double bn, rr, rn;
 
@@ -244,10 +252,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
                 for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
                 rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
             }
+            stamp();
             const double beta = (rho / rho_prev) * (alpha / omega);
             for (int i = tid; i < nc; i += CT) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
+            stamp();
             cluster_barrier();   // p of every slab visible
+            stamp();
             fetch_halo(p);
+            stamp();
             Acc sg;
             sg.zero();
             for (int i = tid; i < nc; i += CT) {
@@ -256,7 +268,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
                 sg.prod(rh[i], vv);
             }
             double sigma;
+            stamp();
             reduce1(sg, sigma);
+            stamp();
             if (sigma == 0.0) {
                 if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it; break; }
                 for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
@@ -267,6 +281,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             for (int i = tid; i < nc; i += CT) s[i] = fma(-alpha, v[i], r[i]);
             cluster_barrier();   // s of every slab visible
             fetch_halo(s);
+            stamp();
             Acc ts, tt, ss;
             ts.zero(); tt.zero(); ss.zero();
             for (int i = tid; i < nc; i += CT) {
@@ -277,6 +292,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
                 ss.prod(s[i], s[i]);
             }
             double tsv, ttv, ssv;
+            stamp();
             {
                 dd vv[3] = {ts.get(), tt.get(), ss.get()};
                 double out[3];
@@ -308,7 +324,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
                 rra.prod(rv, rv);
             }
             rho_prev = rho;
+            stamp();
             reduce2(rhr, rra, rho, rr);
+            stamp();
             rn = sqrt(rr);
             if (rn <= tol * bn) { status = MFX_OK; iters = it; break; }
         }
@@ -324,6 +342,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
 }
 
 }  // namespace
+
+long long *&cluster_trace_ptr()
+{
+    static long long *p = nullptr;
+    return p;
+}
 
 // dynamic smem: (NA + 8) arrays of M cells + 3 planes (two halo copies, cz below)
 size_t cluster_smem(const Geo &G, bool sym)
@@ -342,6 +366,14 @@ mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, 
     a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
     a.aP = A->aP; a.aE = A->aE; a.aW = A->aW; a.aN = A->aN; a.aS = A->aS; a.aT = A->aT; a.aB = A->aB; a.b = A->b;
     a.x = x; a.tol = tol; a.maxit = maxit; a.h = h;
+    a.trace = nullptr;
+    if (getenv("MFX_CLUSTER_TRACE")) {
+        static long long *tr = nullptr;
+        if (!tr) cudaMalloc(&tr, 512 * sizeof(long long));
+        cudaMemsetAsync(tr, 0, 512 * sizeof(long long), s);
+        a.trace = tr;
+        cluster_trace_ptr() = tr;
+    }
     a.M = G.nx * G.ny * ((G.nz + CL - 1) / CL);
     const size_t smem = cluster_smem(G, sym);
     if (sym) {
@@ -352,6 +384,18 @@ mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, 
         k_bicg_cluster<false><<<CL, CT, smem, s>>>(a);
     }
     MFX_CUDA_TRY(cudaGetLastError());
+    if (a.trace) {   // debug: per-phase cycle deltas of CTA 0 for the first iterations
+        long long h[512];
+        cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "cluster trace (cycles): p-update bar halo apply1 red1 s+bar+halo+apply2 red3 k3 red2\n");
+        for (int it = 0; it < 8 && h[it * 10 + 9] != 0; it++) {
+            fprintf(stderr, "  it %d:", it + 1);
+            for (int q = 1; q < 10; q++) fprintf(stderr, " %lld", h[it * 10 + q] - h[it * 10 + q - 1]);
+            if (h[(it + 1) * 10] != 0) fprintf(stderr, " | total %lld", h[(it + 1) * 10] - h[it * 10]);
+            fprintf(stderr, "\n");
+        }
+    }
     return MFX_OK;
 }
 

@@ -1,3 +1,1 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q 2>&1 | tail -2
-timeout 900 python bench.py --steps 5 --warmup 3 --no-extras > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "
-import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['pp_iteration']['us']); print(json.dumps(d['kernels'], indent=0))"
+MFX_CLUSTER_TRACE=1 python scripts/prof_solve.py --config 1 --kind pp --iters 30 --repeat 2 --path 2 2>&1 | tail -14

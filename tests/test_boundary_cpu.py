@@ -124,3 +124,13 @@ def test_workspace_bytes_scale(mfx):
     b1 = mfx.lib().mfx_workspace_bytes(C.byref(mfx.c_grid(g1)), 0)
     b2 = mfx.lib().mfx_workspace_bytes(C.byref(mfx.c_grid(g2)), 0)
     assert b2 - b1 == 7 * 8 * 16 * 16 * 32
+
+
+def test_no_unresolved_library_symbols():
+    """Every symbol libmfx.so needs at load time comes from libc/libstdc++/libm
+    (a missing definition would only surface at dlopen on the GPU box)."""
+    so = os.path.join(ROOT, "paper_2211_15605_b200", "libmfx.so")
+    out = subprocess.check_output(["nm", "-D", "--undefined-only", so], text=True)
+    bad = [l for l in out.splitlines() if l.strip() and not re.search(r"@(GLIBC|GLIBCXX|CXXABI|GCC)", l)
+           and "__gmon_start__" not in l and "_ITM_" not in l and "__cxa_finalize" not in l]
+    assert not bad, bad

@@ -63,28 +63,41 @@ struct ClusterRed {
     __device__ void run(cg::cluster_group &cl, int &buf, dd (&v)[K], double (&out)[K])
     {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        dd x[K];
 #pragma unroll
-        for (int q = 0; q < K; q++) {
-            dd x = v[q];
-            for (int off = 16; off > 0; off >>= 1) {
-                dd y = shfl_dd(x, off);
-                x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
-            }
-            if (lane == 0) pub[buf][q][wid] = x;
+        for (int q = 0; q < K; q++) x[q] = v[q];
+        // the K butterflies advance level by level (independent chains interleave)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            dd y[K];
+#pragma unroll
+            for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+            for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add(y[q], x[q]) : dd_add(x[q], y[q]);
         }
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < K; q++) pub[buf][q][wid] = x[q];
         cluster_barrier();
         if (threadIdx.x < 64 * K) {
             const int q = threadIdx.x >> 6, idx = threadIdx.x & 63;
             tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx & 7], idx >> 3);
         }
         __syncthreads();
-        if (wid < K) {
-            dd x = dd_add(tmp[wid][lane], tmp[wid][lane + 32]);
+        if (wid == 0) {
+#pragma unroll
+            for (int q = 0; q < K; q++) x[q] = dd_add(tmp[q][lane], tmp[q][lane + 32]);
+#pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
-                dd y = shfl_dd(x, off);
-                x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
+                dd y[K];
+#pragma unroll
+                for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+                for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add(y[q], x[q]) : dd_add(x[q], y[q]);
             }
-            if (lane == 0) bc[wid] = x;
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < K; q++) bc[q] = x[q];
         }
         __syncthreads();
 #pragma unroll
@@ -148,30 +161,44 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     int buf = 0;   // parity of the publication slots, shared by all reductions
     double *hb = t + M, *ha = hb + plane;                 // local copies of the z-halo planes
     double *czb = ha + plane;                             // cz of plane k0-1 (SYM)
-
-    // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X read with its z halo
-    auto apply = [&](const double *X, int i) -> double {
+    int *cf = (int *)(czb + plane);                       // per-cell neighbour flags | in-plane offset << 8
+    for (int i = tid; i < nc; i += CT) {
         const int kl = i / plane, o = i - kl * plane;
         const int iy = o / nx, ix = o - iy * nx;
         const int k = k0 + kl;
+        int f = 0;
+        if (ix > 0) f |= 1;
+        if (ix < nx - 1) f |= 2;
+        if (iy > 0) f |= 4;
+        if (iy < ny - 1) f |= 8;
+        if (k > 0) f |= 16;
+        if (k < nz - 1) f |= 32;
+        if (kl > 0) f |= 64;
+        if (kl < npl - 1) f |= 128;
+        cf[i] = f | (o << 8);
+    }
+
+    // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X read with its z halo
+    auto apply = [&](const double *X, int i) -> double {
+        const int f = cf[i], o = f >> 8;
         const double xc = X[i];
-        const double xW = ix > 0 ? X[i - 1] : 0.0;
-        const double xE = ix < nx - 1 ? X[i + 1] : 0.0;
-        const double xS = iy > 0 ? X[i - nx] : 0.0;
-        const double xN = iy < ny - 1 ? X[i + nx] : 0.0;
+        const double xW = (f & 1) ? X[i - 1] : 0.0;
+        const double xE = (f & 2) ? X[i + 1] : 0.0;
+        const double xS = (f & 4) ? X[i - nx] : 0.0;
+        const double xN = (f & 8) ? X[i + nx] : 0.0;
         double xB = 0.0, xT = 0.0;
-        if (k > 0) xB = kl > 0 ? X[i - plane] : hb[o];
-        if (k < nz - 1) xT = kl < npl - 1 ? X[i + plane] : ha[o];
+        if (f & 16) xB = (f & 64) ? X[i - plane] : hb[o];
+        if (f & 32) xT = (f & 128) ? X[i + plane] : ha[o];
         double aP, aW, aE, aS, aN, aB, aT;
         aP = C[i];
         if (SYM) {
             const double *cx = C + M, *cy = C + 2 * M, *cz = C + 3 * M;
-            aW = ix > 0 ? cx[i - 1] : 0.0;
+            aW = (f & 1) ? cx[i - 1] : 0.0;
             aE = cx[i];
-            aS = iy > 0 ? cy[i - nx] : 0.0;
+            aS = (f & 4) ? cy[i - nx] : 0.0;
             aN = cy[i];
             aB = 0.0;
-            if (k > 0) aB = kl > 0 ? cz[i - plane] : czb[o];
+            if (f & 16) aB = (f & 64) ? cz[i - plane] : czb[o];
             aT = cz[i];
         } else {
             aW = C[1 * M + i]; aE = C[2 * M + i]; aS = C[3 * M + i];
@@ -354,7 +381,7 @@ size_t cluster_smem(const Geo &G, bool sym)
 {
     const long long plane = (long long)G.nx * G.ny;
     const long long M = plane * ((G.nz + CL - 1) / CL);
-    return (size_t)(((sym ? 12 : 15) * M + 3 * plane) * sizeof(double));
+    return (size_t)(((sym ? 12 : 15) * M + 3 * plane) * sizeof(double) + M * sizeof(int));
 }
 
 bool cluster_fits(const Geo &G, bool sym) { return cluster_smem(G, sym) <= 200 * 1024; }

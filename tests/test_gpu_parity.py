@@ -35,7 +35,7 @@ def solver_path(request, mfx):
 def cluster_fits(g, sym):
     plane = g.nx * g.ny
     m = plane * -(-g.nz // 8)
-    return ((12 if sym else 15) * m + 3 * plane) * 8 <= 200 * 1024
+    return ((12 if sym else 15) * m + 3 * plane) * 8 + 4 * m <= 200 * 1024
 
 
 def need_path(solver_path, g, sym):

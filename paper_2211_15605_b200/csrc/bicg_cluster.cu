@@ -73,7 +73,7 @@ struct ClusterRed {
 #pragma unroll
             for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
 #pragma unroll
-            for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add(y[q], x[q]) : dd_add(x[q], y[q]);
+            for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
         }
         if (lane == 0)
 #pragma unroll
@@ -86,14 +86,14 @@ struct ClusterRed {
         __syncthreads();
         if (wid == 0) {
 #pragma unroll
-            for (int q = 0; q < K; q++) x[q] = dd_add(tmp[q][lane], tmp[q][lane + 32]);
+            for (int q = 0; q < K; q++) x[q] = dd_add_fast(tmp[q][lane], tmp[q][lane + 32]);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 dd y[K];
 #pragma unroll
                 for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
 #pragma unroll
-                for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add(y[q], x[q]) : dd_add(x[q], y[q]);
+                for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
             }
             if (lane == 0)
 #pragma unroll

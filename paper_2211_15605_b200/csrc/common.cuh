@@ -83,6 +83,20 @@ __device__ __forceinline__ dd dd_add(dd x, dd y)
     return dd{zh, zl};
 }
 
+// Dekker's double-double add ("sloppy"): TwoSum of the heads, tails added
+// plainly.  Error <= ~u^2 (|x| + |y|) per add -- the same O(u^2 * sum|partials|)
+// class as the per-thread accumulation -- at half the dependent-add depth of
+// dd_add.  Used where a reduction tree sits on a latency-critical path.
+__device__ __forceinline__ dd dd_add_fast(dd x, dd y)
+{
+    double s, e;
+    two_sum(x.hi, y.hi, s, e);
+    const double c = (x.lo + y.lo) + e;
+    dd r;
+    fast_two_sum(s, c, r.hi, r.lo);
+    return r;
+}
+
 // Per-thread accumulator: s + c with s the running TwoSum head.
 struct Acc {
     double s, c;

@@ -24,8 +24,7 @@ namespace mfx {
 namespace {
 
 constexpr int CL = 8;     // CTAs per cluster (portable maximum)
-constexpr int CT = 512;   // threads per CTA
-constexpr int NWC = CT / 32;   // warps per CTA
+constexpr int CT = 256;   // threads per CTA
 
 // Cluster barrier for shared-memory exchange.  cg::cluster_group::sync()
 // (barrier.cluster.arrive.release) compiles to MEMBAR.ALL.GPU on sm_100a;
@@ -57,8 +56,9 @@ struct ClArgs {
 // (the barrier of reduction j+1 orders all remote reads of reduction j
 // before any CTA overwrites its slots in reduction j+2).
 struct ClusterRed {
-    dd (*pub)[3][NWC];     // [2][3][NWC] this CTA's per-warp partials
-    dd (*tmp)[CL * NWC];   // [3][CL*NWC] gathered partials
+    dd (*pub)[3][8];       // [2][3][8] this CTA's per-warp partials
+    dd (*tmp)[64];         // [3][64] gathered partials
+    dd *bc;                // [3] folded results
     template <int K>
     __device__ void run(cg::cluster_group &cl, int &buf, dd (&v)[K], double (&out)[K])
     {
@@ -79,28 +79,29 @@ struct ClusterRed {
 #pragma unroll
             for (int q = 0; q < K; q++) pub[buf][q][wid] = x[q];
         cluster_barrier();
-        if (threadIdx.x < CL * NWC * K) {
-            const int q = threadIdx.x / (CL * NWC), idx = threadIdx.x % (CL * NWC);
-            tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx % NWC], idx / NWC);
+        if (threadIdx.x < 64 * K) {
+            const int q = threadIdx.x >> 6, idx = threadIdx.x & 63;
+            tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx & 7], idx >> 3);
         }
         __syncthreads();
-        // every warp folds the CL*NWC partials in the same fixed order (no broadcast barrier)
+        if (wid == 0) {
 #pragma unroll
-        for (int q = 0; q < K; q++) {
-            x[q] = tmp[q][lane];
+            for (int q = 0; q < K; q++) x[q] = dd_add_fast(tmp[q][lane], tmp[q][lane + 32]);
 #pragma unroll
-            for (int j = 1; j < CL * NWC / 32; j++) x[q] = dd_add_fast(x[q], tmp[q][lane + 32 * j]);
+            for (int off = 16; off > 0; off >>= 1) {
+                dd y[K];
+#pragma unroll
+                for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+                for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
+            }
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < K; q++) bc[q] = x[q];
         }
+        __syncthreads();
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            dd y[K];
-#pragma unroll
-            for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
-#pragma unroll
-            for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < K; q++) out[q] = dd_round(x[q]);
+        for (int q = 0; q < K; q++) out[q] = dd_round(bc[q]);
         buf ^= 1;
     }
 };
@@ -118,8 +119,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     double *b = C + NA * M;
     double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
     __shared__ int k0s[CL + 1];
-    __shared__ dd pub[2][3][NWC];
-    __shared__ dd tmp[3][CL * NWC];
+    __shared__ dd pub[2][3][8];
+    __shared__ dd tmp[3][64];
+    __shared__ dd bc[3];
     const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
     if (tid <= CL) k0s[tid] = (int)((long long)nz * tid / CL);
     __syncthreads();
@@ -155,7 +157,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         b[i] = a.b[g0 + i];
         x[i] = a.x[g0 + i];
     }
-    ClusterRed R{pub, tmp};
+    ClusterRed R{pub, tmp, bc};
     int buf = 0;   // parity of the publication slots, shared by all reductions
     double *hb = t + M, *ha = hb + plane;                 // local copies of the z-halo planes
     double *czb = ha + plane;                             // cz of plane k0-1 (SYM)

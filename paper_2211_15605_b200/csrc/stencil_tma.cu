@@ -129,15 +129,12 @@ struct Cfg {
     static constexpr int OFF_YS = OFF_XW + (SYM ? XW_B : 0);
     static constexpr int OFF_EXTRA = OFF_YS + (SYM ? YS_B : 0);
     static constexpr int NDOT = MODE == SM_SPMV ? 0 : (MODE == SM_SETUP ? 2 : (MODE == SM_K1 ? 1 : 3));
-    // barrier-free consumers for every mode whose halo value is cheap to recompute
-    static constexpr bool NOBAR = MODE != SM_K1;
-    static constexpr int NPBUF = NOBAR ? 0 : 4;
 };
 
 template <class C>
 __host__ __device__ constexpr size_t smem_bytes(int S)
 {
-    return (size_t)S * C::STAGE_B + C::NPBUF * (size_t)C::PBUF_B + 16 * (size_t)S;
+    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 16 * (size_t)S;
 }
 
 // plane-stream cursor.  Units are (z-chunk, tile) pairs in chunk-major order,
@@ -212,7 +209,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *stages = smem;
     double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
-    uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + C::NPBUF * C::PBUF_B);
+    uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + 4 * C::PBUF_B);
     uint64_t *empty = full + S;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -280,120 +277,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                 issue<MODE, SYM, TX, TY, CPT_, S>(M, prod, a.nz, stages, full, q);
                 prod.advance(a.nz);
             }
-        }
-    } else if constexpr (C::NOBAR) {
-        // ------------------------------------------------ consumer warps, barrier-free variant
-        // (setup / apply / K2): the stencil value at any point is x (apply) or
-        // s = fma(-alpha, v, r) (K2), computed directly from the staged halo
-        // boxes of planes q-2, q-1, q -- no shared P plane, no CTA barrier.
-        // A stage is released once the plane two below the current is consumed.
-        constexpr int CPT = C::CPT;
-        constexpr int RW = TX / CPT;
-        Cursor cons;
-        cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
-        double czq1[CPT], czq0[CPT];
-#pragma unroll
-        for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
-        const int cx0 = (tid % RW) * CPT, cy = tid / RW;
-        const int ci = cy * TX + cx0;
-        const int hc = (cy + 1) * C::HX + (cx0 + 2);
-        bool v1 = true, v2 = true;   // planes q-1, q-2 virtual (zero)
-        auto val = [&](const uint8_t *stg, bool isv, int idx) -> double {
-            if (isv) return 0.0;
-            const double *h0 = (const double *)(stg + C::OFF_HALO);
-            if (MODE == SM_K2) {
-                const double *h1 = (const double *)(stg + C::OFF_HALO + C::HALO_B);
-                return fma(-alpha, h1[idx], h0[idx]);
-            }
-            return h0[idx];
-        };
-        for (int q = 0; cons.valid; q++) {
-            const int s = q % S;
-            const bool virt = cons.is_virtual(a.nz);
-            const bool produce = cons.produces();
-            const int kout = cons.k - 1;
-            const int x0 = cons.x0, y0 = cons.y0;
-            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
-            const uint8_t *st = stages + (size_t)s * C::STAGE_B;
-            double czcur[CPT];
-#pragma unroll
-            for (int m = 0; m < CPT; m++)
-                czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
-            if (produce) {
-                const uint8_t *so = stages + (size_t)((q + S - 1) % S) * C::STAGE_B;   // plane q-1
-                const uint8_t *sb = stages + (size_t)((q + S - 2) % S) * C::STAGE_B;   // plane q-2
-                const int gx = x0 + cx0, gy = y0 + cy;
-                const bool active = gx < a.nx && gy < a.ny;
-                const double *cell = (const double *)(so + C::OFF_CELL);
-                double y[CPT], xcv[CPT];
-#pragma unroll
-                for (int m = 0; m < CPT; m++) {
-                    const int h = hc + m, c = ci + m;
-                    const double xc = val(so, v1, h);
-                    const double xW = val(so, v1, h - 1), xE = val(so, v1, h + 1);
-                    const double xS = val(so, v1, h - C::HX), xN = val(so, v1, h + C::HX);
-                    const double xB = val(sb, v2, h), xT = val(st, virt, h);
-                    double aP, aW, aE, aS, aN, aB, aT;
-                    aP = cell[c];
-                    if (SYM) {
-                        const double *xw = (const double *)(so + C::OFF_XW);
-                        const double *ys = (const double *)(so + C::OFF_YS);
-                        aW = xw[cy * C::HX + cx0 + m + 1];
-                        aE = xw[cy * C::HX + cx0 + m + 2];
-                        aS = ys[cy * TX + cx0 + m];
-                        aN = ys[(cy + 1) * TX + cx0 + m];
-                        aB = czq0[m];
-                        aT = czq1[m];
-                    } else {
-                        aW = cell[1 * (C::CELL_B / 8) + c];
-                        aE = cell[2 * (C::CELL_B / 8) + c];
-                        aS = cell[3 * (C::CELL_B / 8) + c];
-                        aN = cell[4 * (C::CELL_B / 8) + c];
-                        aB = cell[5 * (C::CELL_B / 8) + c];
-                        aT = cell[6 * (C::CELL_B / 8) + c];
-                    }
-                    double t = aP * xc;
-                    t = fma(-aW, xW, t);
-                    t = fma(-aE, xE, t);
-                    t = fma(-aS, xS, t);
-                    t = fma(-aN, xN, t);
-                    t = fma(-aB, xB, t);
-                    t = fma(-aT, xT, t);
-                    y[m] = t;
-                    xcv[m] = xc;
-                }
-                if (active) {
-                    const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
-                    if (MODE == SM_SPMV) {
-                        store_cells<CPT>(a.out0 + n, y);
-                    } else if (MODE == SM_SETUP) {
-                        const double *bb = (const double *)(so + C::OFF_EXTRA) + ci;
-                        double rv[CPT];
-#pragma unroll
-                        for (int m = 0; m < CPT; m++) {
-                            rv[m] = bb[m] - y[m];
-                            acc[0][m].prod(bb[m], bb[m]);
-                            acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
-                        }
-                        store_cells<CPT>(a.out0 + n, rv);
-                    } else {
-                        store_cells<CPT>(a.out0 + n, y);    // t
-#pragma unroll
-                        for (int m = 0; m < CPT; m++) {
-                            acc[0][m].prod(y[m], xcv[m]);
-                            acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
-                            acc[ND > 2 ? 2 : 0][m].prod(xcv[m], xcv[m]);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            if (q >= 2 && lane == 0) mbar_arrive(&empty[(q + S - 2) % S]);
-#pragma unroll
-            for (int m = 0; m < CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
-            v2 = v1;
-            v1 = virt;
-            cons.advance(a.nz);
         }
     } else {
         // ------------------------------------------------ consumer warps
@@ -770,7 +653,7 @@ mfx_status run_tile(const Geo &G, const double *const halo[3], const double *con
                     const StencilArgs &a, cudaStream_t s)
 {
     static const int st = env_int("MFX_STAGES", 0);
-    const int S = st ? st : (MODE != SM_K1 ? 6 : ((TX * TY == 512 || !SYM) ? 3 : 4));
+    const int S = st ? st : ((TX * TY == 512 || (MODE == SM_K1 && !SYM)) ? 3 : 4);
     if (S == 3) return Launcher<MODE, SYM, TX, TY, CPT_, 3>::run(G, halo, coef, extra, a, s);
     if (S == 6) return Launcher<MODE, SYM, TX, TY, CPT_, 6>::run(G, halo, coef, extra, a, s);
     return Launcher<MODE, SYM, TX, TY, CPT_, 4>::run(G, halo, coef, extra, a, s);
@@ -783,7 +666,7 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
     // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
     static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8 pairs, 3: 32x16 pairs, 4: 32x8, 5: 64x8
     int t = tile;
-    if (!t) t = G.nx <= 32 ? 4 : 1;
+    if (!t) t = G.nx <= 32 ? (SYM ? 3 : 4) : ((MODE == SM_K1 || !SYM) ? 1 : 2);
     if (t == 2) return run_tile<MODE, SYM, 64, 8, 2>(G, halo, coef, extra, a, s);
     if (t == 3) return run_tile<MODE, SYM, 32, 16, 2>(G, halo, coef, extra, a, s);
     if (t == 4) return run_tile<MODE, SYM, 32, 8, 1>(G, halo, coef, extra, a, s);

@@ -1,3 +1,3 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q 2>&1 | tail -2
-for cfg in "" "MFX_STAGES=4" "MFX_TILE=2"; do echo "== pp $cfg"; env $cfg python scripts/prof_solve.py --kind pp --iters 200 --repeat 3 2>&1 | tail -2; done
-echo "== w"; python scripts/prof_solve.py --kind w --iters 200 --repeat 3 2>&1 | tail -2
+timeout 1500 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "cluster" 2>&1 | tail -2
+MFX_CLUSTER_TRACE=1 python scripts/prof_solve.py --config 1 --kind pp --iters 30 --repeat 2 --path 2 2>&1 | tail -6
+python scripts/prof_solve.py --config 1 --kind pp --iters 500 --repeat 3 --path 2 2>&1 | tail -3

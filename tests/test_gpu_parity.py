@@ -311,3 +311,45 @@ def test_nonfinite_latched(mfx):
         ws.check()
     assert e.value.status == mfx.ERR_NONFINITE
     ws.check()  # latch cleared
+
+
+@pytest.mark.parametrize("bc_zhi,w_in", [(BC_OUTLET, 0.15), (BC_WALL, 0.0)])
+def test_simple_outer_loop_parity(mfx, orc, bc_zhi, w_in):
+    """Ten consecutive SIMPLE outer iterations (state m -> m+10) on GPU and oracle:
+    bitwise identical states, residual records and iteration counts at every
+    iteration; with an outlet, the residuals fall (the loop converges)."""
+    g = synth.make_grid(12, 10, 16, bc_zhi=bc_zhi, w_in=w_in)
+    pr = Params(lin_maxit_pp=3000, lin_tol_pp=1e-8)
+    st = synth.make_state(g, 777, pr)
+    if bc_zhi == BC_WALL:
+        st["w"] = np.zeros(g.n)   # closed box: at rest, only the bed's momentum sources act
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    sd = state_dev(st)
+    ref = st
+    Rs = []
+    for it in range(10):
+        ref, R, iters, status, rc = orc.simple_iter(g, pr, ref)
+        out = ctx.step(sd)
+        assert out["iters"][:4] == iters[:4], (it, out["iters"], iters)
+        assert np.array_equal(np.array(out["R"]), R), it
+        for k in ("u", "v", "w", "p"):
+            assert np.array_equal(host(sd[k]), ref[k]), (it, k)
+        Rs.append(max(R))
+    if bc_zhi == BC_OUTLET:
+        assert Rs[-1] < Rs[0]
+    ctx.close()
+
+
+def test_simple_thin_grid(mfx, orc):
+    """Degenerate extents: 2 x 2 x 2 cells (every row touches a boundary)."""
+    g = synth.make_grid(2, 2, 2)
+    pr = Params()
+    st = synth.make_state(g, 31, pr)
+    ref, R, iters, status, rc = orc.simple_iter(g, pr, st)
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    sd = state_dev(st)
+    out = ctx.step(sd)
+    assert out["iters"][:4] == iters[:4]
+    for k in ("u", "v", "w", "p"):
+        assert np.array_equal(host(sd[k]), ref[k]), k
+    ctx.close()

@@ -316,7 +316,7 @@ class SimpleContext:
         cs = c_state(state, n)
         r = Resid()
         st = _lib.mfx_simple_iter(self.ptr, C.byref(cs), C.byref(r), _stream(stream))
-        _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
+        _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))   # NONFINITE/ZERO_DIAG raise
         return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
                     status=list(r.status), converged=bool(r.converged))
 

@@ -499,6 +499,21 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         out->status[q] = (int)m[16 * q + 3];
         if (out->status[q] < 0) worst = out->status[q];
     }
+    // non-finite / zero-diagonal rows latched by any assembly of this rank
+    for (int q = 0; q < 8; q++) {
+        if (!c->ws[q]) continue;
+        unsigned long long bad[2];
+        const WsHeader *h = (const WsHeader *)c->ws[q];
+        MFX_CUDA_TRY(cudaMemcpy(bad, &h->bad_nonfinite, 16, cudaMemcpyDeviceToHost));
+        if (bad[0] != ~0ull || bad[1] != ~0ull) {
+            const unsigned long long none = ~0ull;
+            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_nonfinite, &none, 8, cudaMemcpyHostToDevice));
+            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_zerodiag, &none, 8, cudaMemcpyHostToDevice));
+            set_error("equation %d: %s at cell %llu", q, bad[0] != ~0ull ? "non-finite coefficient" : "zero diagonal",
+                      bad[0] != ~0ull ? bad[0] : bad[1]);
+            worst = bad[0] != ~0ull ? MFX_ERR_NONFINITE : MFX_ERR_ZERO_DIAG;
+        }
+    }
     double mx = out->R_u;
     if (out->R_v > mx) mx = out->R_v;
     if (out->R_w > mx) mx = out->R_w;

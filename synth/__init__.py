@@ -91,6 +91,8 @@ def syamlal_obrien_beta(eps, slip, d_p=200e-6, rho_g=1.0, mu_g=1.8e-5):
 
 
 def make_grid(nx, ny, nz, bc_zlo=BC_INLET, bc_zhi=BC_OUTLET, w_in=0.15) -> Grid:
+    if bc_zlo == BC_WALL:
+        w_in = 0.0
     h = 0.12 / nx
     return Grid(nx, ny, nz, h, h, h, bc_zlo=bc_zlo, bc_zhi=bc_zhi, w_in=w_in)
 

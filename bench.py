@@ -47,7 +47,12 @@ BYTES_PER_CELL = {
 
 
 def assignment_for(n):
-    return {1: "111[1]", 2: "222[1]", 3: "234[1]", 4: "234[1]"}.get(n, "234[1]" + "".join(str(5 + s) for s in range(min(n - 4, 4))))
+    """Equation decomposition per GPU count (PAPER.md:95 notation; p' on GPU 1,
+    momentum on the others, then energy + species scalars on GPUs 5..8)."""
+    fixed = {1: "111[1]", 2: "222[1]", 3: "233[1]", 4: "234[1]"}
+    if n in fixed:
+        return fixed[n]
+    return "234[1]" + "".join(str(5 + s) for s in range(min(n - 4, 4)))
 
 
 def load_peaks():

@@ -201,6 +201,20 @@ mfx_status mfx_ctx_create_local(const char *assignment, int rank, int nranks, mf
  * (fields = MFX_NBUF device pointers indexed by MFX_BUF_*; unused may be NULL). */
 mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_NBUF], void *stream);
 
+/* Domain-decomposed (z-slab) BiCGSTAB over all ranks of `ctx`: the
+ * "domain-decomposed allreduce-dot baseline" of configuration 5 (the MPI
+ * strategy of P:87, Fig. 2a) and the basis of a multi-GPU pressure solve
+ * (P:85).  Rank r owns global planes [k0, k1) of mfx_dist_slab(); its
+ * A_slab / x_slab arrays hold only those planes (nx*ny*(k1-k0) each, same
+ * storage conventions as a global system).  Per iteration one halo plane is
+ * exchanged per stencil apply and the double-double dot partials of all ranks
+ * are all-gathered and folded in rank order, so every rank takes identical
+ * decisions and the iterates equal the single-GPU mfx_bicgstab_solve bitwise.
+ * Requires nz >= number of ranks.  Synchronises `stream` once per chunk. */
+mfx_status mfx_dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eqsys *A_slab, double *x_slab,
+                          double tol, int maxit, mfx_solve_info *info, void *stream);
+void mfx_dist_slab(int nz, int rank, int nranks, int *k0, int *k1);
+
 /* a-9: one SIMPLE outer iteration on this rank's share of the equations.
  * state: in snapshot m, out m+1 (u, v, w, p and owned/broadcast phi on every
  * rank).  out (host) receives the residual record (identical on all ranks).

@@ -110,6 +110,9 @@ _sigs = {
     "mfx_simple_iter": (C.c_int, [_V, C.POINTER(State), C.POINTER(Resid), _V]),
     "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
     "mfx_ctx_buffer": (C.c_void_p, [_V, C.c_int]),
+    "mfx_dist_solve": (C.c_int, [_V, C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
+                                 C.POINTER(SolveInfo), _V]),
+    "mfx_dist_slab": (None, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "mfx_prof_enable": (None, [C.c_int]),
     "mfx_prof_reset": (None, []),
     "mfx_prof_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
@@ -272,6 +275,13 @@ def exchange_plan(text: str, nranks: int, rank: int, phase: int):
     return [dict(op=o.op, peer=o.peer, buf=BUF_NAMES[o.buf], slot=o.slot, nslots=o.nslots) for o in ops[:n.value]]
 
 
+def dist_slab(nz: int, rank: int, nranks: int):
+    """Global z-planes [k0, k1) owned by `rank` in the domain-decomposed solver."""
+    k0, k1 = C.c_int(), C.c_int()
+    _lib.mfx_dist_slab(nz, rank, nranks, C.byref(k0), C.byref(k1))
+    return k0.value, k1.value
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.mfx_nccl_unique_id(buf), "mfx_nccl_unique_id")
@@ -300,6 +310,7 @@ class SimpleContext:
     def __init__(self, assignment: str, grid, params, rank: int = 0, nranks: int = 1, uid: bytes | None = None,
                  group: LocalGroup | None = None):
         self.grid, self.params = grid, params
+        self.rank, self.nranks = rank, nranks
         self._g, self._p = c_grid(grid), c_params(params)
         self.ptr = C.c_void_p()
         if group is not None:
@@ -328,6 +339,16 @@ class SimpleContext:
             return None
         n = self.grid.nx * self.grid.ny * self.grid.nz
         return device_view(ptr, n).clone()
+
+    def dist_solve(self, kind: int, sysd_slab: dict, x_slab, tol: float, maxit: int, stream=None) -> dict:
+        """Domain-decomposed BiCGSTAB over the context's ranks (this rank's slab)."""
+        k0, k1 = dist_slab(self.grid.nz, self.rank, self.nranks)
+        n = self.grid.nx * self.grid.ny * (k1 - k0)
+        info = SolveInfo()
+        st = _lib.mfx_dist_solve(self.ptr, kind, C.byref(self._g), C.byref(c_sys(sysd_slab, n)), _ptr(x_slab, n),
+                                 tol, maxit, C.byref(info), _stream(stream))
+        _check(st, "mfx_dist_solve", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
+        return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid)
 
     def phase_times(self):
         ms = (C.c_double * 6)()

@@ -133,6 +133,7 @@ struct Nccl {
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
     bool load()
     {
@@ -144,7 +145,7 @@ struct Nccl {
         if (!h) { set_error("cannot dlopen libnccl.so.2: %s", dlerror()); return false; }
 #define SYM(name) name = (decltype(name))dlsym(h, "nccl" #name); if (!name) { set_error("nccl%s missing", #name); return false; }
         SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(GroupStart) SYM(GroupEnd) SYM(Send) SYM(Recv)
-        SYM(Broadcast) SYM(GetErrorString)
+        SYM(Broadcast) SYM(AllGather) SYM(GetErrorString)
 #undef SYM
         return true;
     }
@@ -203,6 +204,8 @@ struct mfx_local_group {
     int arrived = 0;
     unsigned long gen = 0;
     double *fields[64][MFX_NBUF];
+    const void *dptr[64];     // distributed solver: published slab / partials pointer
+    long long dlen[64];       // ... and its length (planes or values)
     cudaEvent_t ready[64];
     cudaEvent_t done[64];
     void barrier()
@@ -238,6 +241,8 @@ struct mfx_ctx {
     double *meta_host;       // pinned [8][16]
     ncclComm_t comm;
     mfx_local_group *group;  // non-NULL: in-process transport instead of NCCL
+    void *dist_scratch;      // distributed-solver workspace (allocated on first use)
+    size_t dist_bytes;
     cudaEvent_t ev[6];
     double phase_ms[6];
 };
@@ -269,6 +274,8 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     c->N = (long long)grid->nx * grid->ny * grid->nz;
     c->comm = nullptr;
     c->group = group;
+    c->dist_scratch = nullptr;
+    c->dist_bytes = 0;
     const size_t vb = round256(sizeof(double) * c->N);
     c->ws_bytes = ws_total_bytes(c->N);
     auto fail = [&](mfx_status s) { mfx_ctx_destroy(c); return s; };
@@ -407,6 +414,100 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
         else MFX_NCCL_TRY(g_nccl.Broadcast(buf, buf, count, ncclDouble, o.peer, c->comm, s));
     }
     MFX_NCCL_TRY(g_nccl.GroupEnd());
+    return MFX_OK;
+}
+
+// ------------------------------------------------------------------ distributed-solver transport
+int ctx_rank(const mfx_ctx *c) { return c->rank; }
+int ctx_nranks(const mfx_ctx *c) { return c->nranks; }
+
+void *ctx_dist_scratch(mfx_ctx *c, size_t bytes)
+{
+    if (c->dist_bytes < bytes) {
+        if (c->dist_scratch) cudaFree(c->dist_scratch);
+        c->dist_scratch = nullptr;
+        c->dist_bytes = 0;
+        if (cudaMalloc(&c->dist_scratch, bytes) != cudaSuccess) {
+            set_error("cudaMalloc(%zu) for the distributed solver failed", bytes);
+            return nullptr;
+        }
+        c->dist_bytes = bytes;
+    }
+    return c->dist_scratch;
+}
+
+// local transport: publish (ptr, len), barrier, pull, done-events, barrier
+template <class Pull>
+static mfx_status local_phase(mfx_ctx *c, const void *ptr, long long len, cudaStream_t s, Pull pull)
+{
+    mfx_local_group &g = *c->group;
+    g.dptr[c->rank] = ptr;
+    g.dlen[c->rank] = len;
+    MFX_CUDA_TRY(cudaEventRecord(g.ready[c->rank], s));
+    g.barrier();
+    mfx_status st = pull(g);
+    if (st != MFX_OK) return st;
+    MFX_CUDA_TRY(cudaEventRecord(g.done[c->rank], s));
+    g.barrier();
+    for (int q = 0; q < g.nranks; q++)
+        if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.done[q], 0));
+    g.barrier();
+    return MFX_OK;
+}
+
+// hb <- last plane of rank-1's slab, ha <- first plane of rank+1's slab
+mfx_status ctx_halo_exchange(mfx_ctx *c, const double *slab, int npl, long long plane, double *hb, double *ha,
+                             cudaStream_t s)
+{
+    const int r = c->rank, R = c->nranks;
+    if (R == 1) return MFX_OK;
+    const size_t pb = sizeof(double) * (size_t)plane;
+    if (c->group) {
+        return local_phase(c, slab, npl, s, [&](mfx_local_group &g) -> mfx_status {
+            if (r > 0) {
+                MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[r - 1], 0));
+                const double *src = (const double *)g.dptr[r - 1] + (g.dlen[r - 1] - 1) * plane;
+                MFX_CUDA_TRY(cudaMemcpyAsync(hb, src, pb, cudaMemcpyDefault, s));
+            }
+            if (r < R - 1) {
+                MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[r + 1], 0));
+                MFX_CUDA_TRY(cudaMemcpyAsync(ha, g.dptr[r + 1], pb, cudaMemcpyDefault, s));
+            }
+            return MFX_OK;
+        });
+    }
+    MFX_NCCL_TRY(g_nccl.GroupStart());
+    if (r > 0) {
+        MFX_NCCL_TRY(g_nccl.Send(slab, (size_t)plane, ncclDouble, r - 1, c->comm, s));
+        MFX_NCCL_TRY(g_nccl.Recv(hb, (size_t)plane, ncclDouble, r - 1, c->comm, s));
+    }
+    if (r < R - 1) {
+        MFX_NCCL_TRY(g_nccl.Send(slab + (size_t)(npl - 1) * plane, (size_t)plane, ncclDouble, r + 1, c->comm, s));
+        MFX_NCCL_TRY(g_nccl.Recv(ha, (size_t)plane, ncclDouble, r + 1, c->comm, s));
+    }
+    MFX_NCCL_TRY(g_nccl.GroupEnd());
+    return MFX_OK;
+}
+
+// all[q*K .. q*K+K) <- rank q's K double-double partials, for every rank q
+mfx_status ctx_allgather_dd(mfx_ctx *c, const dd *mine, int K, dd *all, cudaStream_t s)
+{
+    const int R = c->nranks;
+    const size_t kb = sizeof(dd) * (size_t)K;
+    if (R == 1) {
+        MFX_CUDA_TRY(cudaMemcpyAsync(all, mine, kb, cudaMemcpyDeviceToDevice, s));
+        return MFX_OK;
+    }
+    if (c->group) {
+        return local_phase(c, mine, K, s, [&](mfx_local_group &g) -> mfx_status {
+            for (int q = 0; q < R; q++) {
+                if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[q], 0));
+                MFX_CUDA_TRY(cudaMemcpyAsync(all + (size_t)q * K, g.dptr[q], kb, cudaMemcpyDefault, s));
+            }
+            return MFX_OK;
+        });
+    }
+    MFX_NCCL_TRY(g_nccl.AllGather(mine, all, 2 * (size_t)K, ncclDouble, c->comm, s));
     return MFX_OK;
 }
 
@@ -564,11 +665,26 @@ void mfx_ctx_destroy(mfx_ctx *c)
     if (!c) return;
     if (c->comm && mfx::g_nccl.CommDestroy) mfx::g_nccl.CommDestroy(c->comm);
     for (void *p : c->allocs) cudaFree(p);
+    if (c->dist_scratch) cudaFree(c->dist_scratch);
     if (c->meta_host) cudaFreeHost(c->meta_host);
     for (int q = 0; q < 6; q++)
         if (c->ev[q]) cudaEventDestroy(c->ev[q]);
     delete c;
 }
+
+namespace mfx {
+mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol,
+                      int maxit, mfx_solve_info *info, cudaStream_t s);
+void dist_slab(int nz, int rank, int nranks, int *k0, int *k1);
+}
+
+mfx_status mfx_dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eqsys *A_slab, double *x_slab,
+                          double tol, int maxit, mfx_solve_info *info, void *stream)
+{
+    return mfx::dist_solve(ctx, kind, grid, A_slab, x_slab, tol, maxit, info, (cudaStream_t)stream);
+}
+
+void mfx_dist_slab(int nz, int rank, int nranks, int *k0, int *k1) { mfx::dist_slab(nz, rank, nranks, k0, k1); }
 
 double *mfx_ctx_buffer(mfx_ctx *c, int which)
 {

@@ -1,1 +1,1 @@
-timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
+timeout 1500 python -m pytest tests/test_gpu_dist_solver.py -x -q 2>&1 | tail -15

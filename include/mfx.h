@@ -149,29 +149,36 @@ mfx_status mfx_correct(const mfx_grid *grid, const mfx_params *params, const dou
 /* ---------------------------------------------------------------- equation decomposition */
 /* Assignment string: three 1-based GPU ids for U, V, W,
  * a bracketed P list, then optional scalar owners, e.g. "111[1]", "234[1]",
- * "234[1]5678".  v1 accepts a single-entry P list (multi-GPU p' is NEXT-1). */
+ * "234[1]5678", "234[1234]".  A multi-entry P list must name every rank in
+ * order ([12..R]): the pressure correction is then solved by the domain-
+ * decomposed solver over all ranks (the paper's multi-GPU pressure solver,
+ * P:85); owner[3] is its first entry (P0, which corrects and
+ * broadcasts). */
 typedef struct {
     int owner[8];       /* 0-based rank owning u, v, w, pp, phi0..phi3; -1 = absent */
     int n_scalars;
     int n_ranks_used;   /* max id */
+    int n_p;            /* entries of the P list (1, or every rank) */
 } mfx_assignment;
 
 mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *out);
 
 /* Exchange schedule for `rank` (host logic, no device work).  phase 0 =
- * GATHER (momentum owners -> p' owner: u*, d per component, plus a 16-double
- * residual record), phase 1 = BCAST (p' owner -> all: u, v, w, p, residual
- * record; scalar owners -> all: phi).  Ops are returned in the order they are
- * issued inside one NCCL group. */
+ * GATHER (momentum owners -> p' owner(s): u*, d per component, plus a
+ * 16-double residual record), phase 1 = BCAST (p' owner -> all: u, v, w, p,
+ * residual record; scalar owners -> all: phi), phase 2 = PSLAB (multi-GPU p':
+ * every rank's slab of p' -> P0; k0/k1 give the plane range).  Ops are
+ * returned in the order they are issued inside one NCCL group. */
 enum { MFX_OP_SEND = 0, MFX_OP_RECV = 1, MFX_OP_BCAST = 2 };
 enum { MFX_BUF_U = 0, MFX_BUF_V, MFX_BUF_W, MFX_BUF_DX, MFX_BUF_DY, MFX_BUF_DZ,
        MFX_BUF_P, MFX_BUF_PHI0, MFX_BUF_PHI1, MFX_BUF_PHI2, MFX_BUF_PHI3,
-       MFX_BUF_META, MFX_NBUF };
+       MFX_BUF_META, MFX_BUF_PP, MFX_NBUF };
 /* buf MFX_BUF_META moves nslots 16-double residual records starting at slot;
- * every other buffer moves N doubles (slot = nslots = 0).  peer = root for BCAST. */
-typedef struct { int op, peer, buf, slot, nslots; } mfx_xfer;
+ * other buffers move planes [k0, k1) (k1 = 0: the whole field of N doubles).
+ * peer = root for BCAST. */
+typedef struct { int op, peer, buf, slot, nslots, k0, k1; } mfx_xfer;
 mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops,
-                             int *n_ops);
+                             int *n_ops, int nz /* grid extent, used by PSLAB */);
 
 /* NCCL bootstrap: rank 0 calls mfx_nccl_unique_id and ships the 128 bytes to
  * the other ranks (e.g. torch.distributed.broadcast_object_list). */
@@ -198,7 +205,8 @@ mfx_status mfx_ctx_create_local(const char *assignment, int rank, int nranks, mf
                                 const mfx_grid *grid, const mfx_params *params, mfx_ctx **out);
 
 /* a-8: execute `phase` of the exchange plan on the context's buffers
- * (fields = MFX_NBUF device pointers indexed by MFX_BUF_*; unused may be NULL). */
+ * (fields = MFX_NBUF device pointers indexed by MFX_BUF_*; unused may be NULL;
+ * MFX_BUF_PP is the p' solution). */
 mfx_status mfx_exchange_state(mfx_ctx *ctx, int phase, double *const fields[MFX_NBUF], void *stream);
 
 /* Domain-decomposed (z-slab) BiCGSTAB over all ranks of `ctx`: the

@@ -25,7 +25,7 @@ EQ_U, EQ_V, EQ_W, EQ_PP, EQ_SCALAR = 0, 1, 2, 3, 4
 BC_WALL, BC_INLET, BC_OUTLET, BC_DIRICHLET_TEST = 0, 1, 2, 3
 OK, NOT_CONVERGED, ERR_ARG, ERR_NONFINITE, ERR_ZERO_DIAG, ERR_BREAKDOWN, ERR_CUDA, ERR_NCCL = 0, 1, -1, -2, -3, -4, -5, -6
 OP_SEND, OP_RECV, OP_BCAST = 0, 1, 2
-BUF_NAMES = ("u", "v", "w", "dx", "dy", "dz", "p", "phi0", "phi1", "phi2", "phi3", "meta")
+BUF_NAMES = ("u", "v", "w", "dx", "dy", "dz", "p", "phi0", "phi1", "phi2", "phi3", "meta", "pp")
 NBUF = len(BUF_NAMES)
 
 
@@ -75,11 +75,12 @@ class Resid(C.Structure):
 
 
 class Assignment(C.Structure):
-    _fields_ = [("owner", C.c_int * 8), ("n_scalars", C.c_int), ("n_ranks_used", C.c_int)]
+    _fields_ = [("owner", C.c_int * 8), ("n_scalars", C.c_int), ("n_ranks_used", C.c_int), ("n_p", C.c_int)]
 
 
 class Xfer(C.Structure):
-    _fields_ = [("op", C.c_int), ("peer", C.c_int), ("buf", C.c_int), ("slot", C.c_int), ("nslots", C.c_int)]
+    _fields_ = [("op", C.c_int), ("peer", C.c_int), ("buf", C.c_int), ("slot", C.c_int), ("nslots", C.c_int),
+                ("k0", C.c_int), ("k1", C.c_int)]
 
 
 _V = C.c_void_p
@@ -97,7 +98,7 @@ _sigs = {
     "mfx_correct": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(_V), _V, _V, _V, _V, _V, _V, _V]),
     "mfx_parse_assignment": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(Assignment)]),
     "mfx_exchange_plan": (C.c_int, [C.POINTER(Assignment), C.c_int, C.c_int, C.POINTER(Xfer), C.c_int,
-                                    C.POINTER(C.c_int)]),
+                                    C.POINTER(C.c_int), C.c_int]),
     "mfx_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mfx_ctx_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(Grid), C.POINTER(Params),
                                  C.POINTER(_V)]),
@@ -263,16 +264,17 @@ def correct(grid, params, star, pp, p, out=None, stream=None):
 def parse_assignment(text: str, nranks: int) -> dict:
     a = Assignment()
     _check(_lib.mfx_parse_assignment(text.encode(), nranks, C.byref(a)), "mfx_parse_assignment")
-    return dict(owner=list(a.owner), n_scalars=a.n_scalars, n_ranks_used=a.n_ranks_used)
+    return dict(owner=list(a.owner), n_scalars=a.n_scalars, n_ranks_used=a.n_ranks_used, n_p=a.n_p)
 
 
-def exchange_plan(text: str, nranks: int, rank: int, phase: int):
+def exchange_plan(text: str, nranks: int, rank: int, phase: int, nz: int = 0):
     a = Assignment()
     _check(_lib.mfx_parse_assignment(text.encode(), nranks, C.byref(a)), "mfx_parse_assignment")
     ops = (Xfer * 64)()
     n = C.c_int()
-    _check(_lib.mfx_exchange_plan(C.byref(a), rank, phase, ops, 64, C.byref(n)), "mfx_exchange_plan")
-    return [dict(op=o.op, peer=o.peer, buf=BUF_NAMES[o.buf], slot=o.slot, nslots=o.nslots) for o in ops[:n.value]]
+    _check(_lib.mfx_exchange_plan(C.byref(a), rank, phase, ops, 64, C.byref(n), nz), "mfx_exchange_plan")
+    return [dict(op=o.op, peer=o.peer, buf=BUF_NAMES[o.buf], slot=o.slot, nslots=o.nslots, k0=o.k0, k1=o.k1)
+            for o in ops[:n.value]]
 
 
 def dist_slab(nz: int, rank: int, nranks: int):

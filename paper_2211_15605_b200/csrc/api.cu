@@ -146,7 +146,7 @@ mfx_status bicgstab_solve(int, const mfx_grid *, const mfx_eqsys *, double *, do
 mfx_status correct(const mfx_grid *, const mfx_params *, const double *const[6], const double *, const double *,
                    double *, double *, double *, double *, cudaStream_t);
 mfx_status parse_assignment(const char *, int, mfx_assignment *);
-mfx_status exchange_plan(const mfx_assignment *, int, int, mfx_xfer *, int, int *);
+mfx_status exchange_plan(const mfx_assignment *, int, int, mfx_xfer *, int, int *, int);
 mfx_status nccl_unique_id(unsigned char out[128]);
 mfx_status ctx_create(const char *, int, int, const unsigned char *, const mfx_grid *, const mfx_params *,
                       mfx_ctx **, mfx_local_group *);
@@ -229,9 +229,10 @@ API mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment
     return parse_assignment(text, nranks, out);
 }
 
-API mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops)
+API mfx_status mfx_exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops,
+                                 int nz)
 {
-    return exchange_plan(a, rank, phase, ops, max_ops, n_ops);
+    return exchange_plan(a, rank, phase, ops, max_ops, n_ops, nz);
 }
 
 API mfx_status mfx_nccl_unique_id(unsigned char out[128]) { return nccl_unique_id(out); }

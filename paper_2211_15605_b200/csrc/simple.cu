@@ -41,6 +41,7 @@ mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
     for (int q = 0; q < 8; q++) a.owner[q] = -1;
     a.n_scalars = 0;
     a.n_ranks_used = 0;
+    a.n_p = 1;
     const char *c = text;
     auto digit = [&](int &id) -> bool {
         if (*c < '1' || *c > '9') return false;
@@ -56,14 +57,18 @@ mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
     MFX_ARG_CHECK(*c == '[', "assignment '%s': expected '['", text);
     c++;
     int np = 0;
+    bool in_order = true;
     while (*c && *c != ']') {
         MFX_ARG_CHECK(digit(id), "assignment '%s': bad P list", text);
         if (np == 0) a.owner[3] = id - 1;
+        if (id != np + 1) in_order = false;
         np++;
     }
     MFX_ARG_CHECK(*c == ']' && np >= 1, "assignment '%s': expected non-empty [P] list", text);
-    MFX_ARG_CHECK(np == 1, "assignment '%s': multi-GPU pressure solve [P..] (paper's [1234]) is NEXT-1, "
-                  "not implemented", text);
+    MFX_ARG_CHECK(np == 1 || (in_order && np == nranks),
+                  "assignment '%s': a multi-GPU pressure list must name every rank in order ([12..%d])", text,
+                  nranks);
+    a.n_p = np;
     c++;
     while (*c) {
         MFX_ARG_CHECK(a.n_scalars < 4, "assignment '%s': at most 4 scalar equations", text);
@@ -83,35 +88,54 @@ mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
 // ------------------------------------------------------------------ exchange plan
 // GATHER: momentum owners -> p' owner (u*, d, meta slot); BCAST: p' owner ->
 // all (u, v, w, p, meta slots 0-3), scalar owner -> all (phi, its meta slot).
-mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops)
+void dist_slab(int nz, int rank, int nranks, int *k0, int *k1);
+mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol,
+                      int maxit, mfx_solve_info *info, cudaStream_t s);
+
+mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer *ops, int max_ops, int *n_ops,
+                         int nz)
 {
     MFX_ARG_CHECK(a && n_ops && (ops || max_ops == 0), "NULL argument");
-    MFX_ARG_CHECK(phase == 0 || phase == 1, "phase must be 0 (GATHER) or 1 (BCAST)");
+    MFX_ARG_CHECK(phase != 2 || a->n_p == 1 || nz >= a->n_p, "PSLAB plan needs nz >= number of p' ranks");
+    MFX_ARG_CHECK(phase >= 0 && phase <= 2, "phase must be 0 (GATHER), 1 (BCAST) or 2 (PSLAB)");
     std::vector<mfx_xfer> v;
     const int P = a->owner[3];
+    const bool multi_p = a->n_p > 1;   // every rank is a p' rank
     if (phase == 0) {
         for (int c = 0; c < 3; c++) {
             const int o = a->owner[c];
-            if (o == P) continue;
-            if (rank == o) {
-                v.push_back({MFX_OP_SEND, P, MFX_BUF_U + c, 0, 0});
-                v.push_back({MFX_OP_SEND, P, MFX_BUF_DX + c, 0, 0});
-                v.push_back({MFX_OP_SEND, P, MFX_BUF_META, c, 1});
-            } else if (rank == P) {
-                v.push_back({MFX_OP_RECV, o, MFX_BUF_U + c, 0, 0});
-                v.push_back({MFX_OP_RECV, o, MFX_BUF_DX + c, 0, 0});
-                v.push_back({MFX_OP_RECV, o, MFX_BUF_META, c, 1});
+            for (int dst = 0; dst < (multi_p ? a->n_p : 1); dst++) {
+                const int pr = multi_p ? dst : P;
+                if (pr == o) continue;
+                if (rank == o) {
+                    v.push_back({MFX_OP_SEND, pr, MFX_BUF_U + c, 0, 0, 0, 0});
+                    v.push_back({MFX_OP_SEND, pr, MFX_BUF_DX + c, 0, 0, 0, 0});
+                    v.push_back({MFX_OP_SEND, pr, MFX_BUF_META, c, 1, 0, 0});
+                } else if (rank == pr) {
+                    v.push_back({MFX_OP_RECV, o, MFX_BUF_U + c, 0, 0, 0, 0});
+                    v.push_back({MFX_OP_RECV, o, MFX_BUF_DX + c, 0, 0, 0, 0});
+                    v.push_back({MFX_OP_RECV, o, MFX_BUF_META, c, 1, 0, 0});
+                }
             }
         }
-    } else {
-        v.push_back({MFX_OP_BCAST, P, MFX_BUF_U, 0, 0});
-        v.push_back({MFX_OP_BCAST, P, MFX_BUF_V, 0, 0});
-        v.push_back({MFX_OP_BCAST, P, MFX_BUF_W, 0, 0});
-        v.push_back({MFX_OP_BCAST, P, MFX_BUF_P, 0, 0});
-        v.push_back({MFX_OP_BCAST, P, MFX_BUF_META, 0, 4});
+    } else if (phase == 1) {
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_U, 0, 0, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_V, 0, 0, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_W, 0, 0, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_P, 0, 0, 0, 0});
+        v.push_back({MFX_OP_BCAST, P, MFX_BUF_META, 0, 4, 0, 0});
         for (int s = 0; s < a->n_scalars; s++) {
-            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_PHI0 + s, 0, 0});
-            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_META, 4 + s, 1});
+            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_PHI0 + s, 0, 0, 0, 0});
+            v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_META, 4 + s, 1, 0, 0});
+        }
+    } else if (multi_p) {
+        // PSLAB: the slabs of the domain-decomposed p' solution -> P0 (= rank 0)
+        for (int q = 0; q < a->n_p; q++) {
+            if (q == P) continue;
+            int k0, k1;
+            dist_slab(nz, q, a->n_p, &k0, &k1);
+            if (rank == q) v.push_back({MFX_OP_SEND, P, MFX_BUF_PP, 0, 0, k0, k1});
+            else if (rank == P) v.push_back({MFX_OP_RECV, q, MFX_BUF_PP, 0, 0, k0, k1});
         }
     }
     *n_ops = (int)v.size();
@@ -162,6 +186,18 @@ Nccl g_nccl;
     } while (0)
 
 size_t round256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+__global__ void k_meta_vals(const double *resid2, double *slot, int iters, int status, int restarts, double rel)
+{
+    if (threadIdx.x != 0) return;
+    slot[0] = resid2[0];
+    slot[1] = resid2[1];
+    slot[2] = (double)iters;
+    slot[3] = (double)status;
+    slot[4] = (double)restarts;
+    slot[5] = rel;
+    slot[6] = 1.0;
+}
 
 __global__ void k_meta(const WsHeader *h, const double *resid2, double *slot, int solved)
 {
@@ -281,8 +317,11 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     auto fail = [&](mfx_status s) { mfx_ctx_destroy(c); return s; };
     for (int q = 0; q < 8; q++) { memset(&c->sys[q], 0, sizeof(mfx_eqsys)); c->ws[q] = nullptr; }
     const int P = a.owner[3];
+    const bool multi_p = a.n_p > 1;                 // every rank solves a slab of p'
+    MFX_ARG_CHECK(!multi_p || grid->nz >= nranks, "multi-GPU p' needs nz >= ranks");
+    auto holds = [&](int q) { return a.owner[q] == rank || (q == 3 && multi_p); };
     for (int q = 0; q < 8; q++) {
-        if (a.owner[q] != rank) continue;
+        if (!holds(q)) continue;
         const int narr = q == 3 ? 5 : 9;
         void *blk;
         if ((st = ctx_alloc(c, &blk, vb * narr)) != MFX_OK) return fail(st);
@@ -302,7 +341,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     // starred velocities and d: on the owner of each component and on the p' owner
     for (int q = 0; q < 3; q++) {
         c->star[q] = c->dv[q] = nullptr;
-        if (a.owner[q] == rank || P == rank) {
+        if (a.owner[q] == rank || P == rank || multi_p) {
             void *blk;
             if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
             c->star[q] = (double *)blk;
@@ -314,7 +353,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
         }
     }
     c->pp = nullptr;
-    if (P == rank) {
+    if (P == rank || multi_p) {
         void *blk;
         if ((st = ctx_alloc(c, &blk, vb)) != MFX_OK) return fail(st);
         c->pp = (double *)blk;
@@ -363,8 +402,15 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     if (c->nranks == 1) return MFX_OK;
     mfx_xfer ops[64];
     int n = 0;
-    mfx_status st = exchange_plan(&c->asg, c->rank, phase, ops, 64, &n);
+    mfx_status st = exchange_plan(&c->asg, c->rank, phase, ops, 64, &n, c->grid.nz);
     if (st != MFX_OK) return st;
+    const long long plane = (long long)c->grid.nx * c->grid.ny;
+    // element offset and count of op o in its buffer
+    auto span = [&](const mfx_xfer &o, size_t &off, size_t &count) {
+        if (o.buf == MFX_BUF_META) { off = 16 * (size_t)o.slot; count = 16 * (size_t)o.nslots; }
+        else if (o.k1 > o.k0) { off = (size_t)(o.k0 * plane); count = (size_t)((o.k1 - o.k0) * plane); }
+        else { off = 0; count = (size_t)c->N; }
+    };
     if (c->group) {
         mfx_local_group &g = *c->group;
         for (int b = 0; b < MFX_NBUF; b++) g.fields[c->rank][b] = fields[b];
@@ -375,12 +421,10 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
             if (o.op == MFX_OP_SEND || (o.op == MFX_OP_BCAST && o.peer == c->rank)) continue;
             double *dst = fields[o.buf];
             const double *src = g.fields[o.peer][o.buf];
-            size_t count = (size_t)c->N;
-            if (o.buf == MFX_BUF_META) {
-                dst += 16 * o.slot;
-                src += 16 * o.slot;
-                count = 16 * (size_t)o.nslots;
-            }
+            size_t off, count;
+            span(o, off, count);
+            if (dst) dst += off;
+            if (src) src += off;
             if (!dst || !src) {
                 set_error("local exchange: buffer %d missing (rank %d <- %d)", o.buf, c->rank, o.peer);
                 return MFX_ERR_ARG;
@@ -399,11 +443,9 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     for (int q = 0; q < n; q++) {
         const mfx_xfer &o = ops[q];
         double *buf = fields[o.buf];
-        size_t count = (size_t)c->N;
-        if (o.buf == MFX_BUF_META) {
-            buf = buf + 16 * o.slot;
-            count = 16 * (size_t)o.nslots;
-        }
+        size_t off, count;
+        span(o, off, count);
+        if (buf) buf += off;
         if (!buf) {
             g_nccl.GroupEnd();
             set_error("exchange: buffer %d is NULL on rank %d", o.buf, c->rank);
@@ -554,7 +596,33 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     F[MFX_BUF_META] = c->meta;
     if ((rc = exchange_state(c, 0, F, s)) != MFX_OK) return rc;
     MFX_CUDA_TRY(cudaEventRecord(c->ev[2], s));
-    if (r == P) {
+    if (a.n_p > 1) {
+        // multi-GPU pressure correction: every rank assembles p'
+        // (cheap, from the gathered u*, d), solves its z-slab with the
+        // domain-decomposed BiCGSTAB, and the slabs are gathered to P0.
+        const double *star6[6] = {c->star[0], c->star[1], c->star[2], c->dv[0], c->dv[1], c->dv[2]};
+        if ((rc = assemble_eq(MFX_EQ_PP, 0, &c->grid, &pr, st, star6, &c->sys[3], c->resid2 + 6, c->ws[3],
+                              c->ws_bytes, s)) != MFX_OK) return rc;
+        MFX_CUDA_TRY(cudaMemsetAsync(c->pp, 0, vbytes, s));
+        int k0, k1;
+        dist_slab(c->grid.nz, r, c->nranks, &k0, &k1);
+        const size_t off = (size_t)k0 * c->grid.nx * c->grid.ny;
+        mfx_eqsys sl;
+        memset(&sl, 0, sizeof(sl));
+        sl.aP = c->sys[3].aP + off; sl.aE = c->sys[3].aE + off; sl.aN = c->sys[3].aN + off;
+        sl.aT = c->sys[3].aT + off; sl.b = c->sys[3].b + off;
+        mfx_solve_info info;
+        rc = dist_solve(c, MFX_EQ_PP, &c->grid, &sl, c->pp + off, pr.lin_tol_pp, pr.lin_maxit_pp, &info, s);
+        if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
+        k_meta_vals<<<1, 32, 0, s>>>(c->resid2 + 6, c->meta + 48, info.iters, info.status, info.restarts,
+                                     info.rel_resid);
+        double *Fp[MFX_NBUF] = {0};
+        Fp[MFX_BUF_PP] = c->pp;
+        if ((rc = exchange_state(c, 2, Fp, s)) != MFX_OK) return rc;
+        MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
+        if (r == P && (rc = correct(&c->grid, &pr, star6, c->pp, st->p, st->u, st->v, st->w, st->p, s)) != MFX_OK)
+            return rc;
+    } else if (r == P) {
         const double *star6[6] = {c->star[0], c->star[1], c->star[2], c->dv[0], c->dv[1], c->dv[2]};
         if ((rc = assemble_eq(MFX_EQ_PP, 0, &c->grid, &pr, st, star6, &c->sys[3], c->resid2 + 6, c->ws[3],
                               c->ws_bytes, s)) != MFX_OK) return rc;

@@ -1,1 +1,1 @@
-timeout 1500 python -m pytest tests/test_gpu_dist_solver.py -x -q 2>&1 | tail -15
+timeout 1500 python -m pytest tests/test_gpu_multirank.py tests/test_gpu_dist_solver.py -x -q 2>&1 | tail -15

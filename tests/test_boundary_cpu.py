@@ -57,6 +57,8 @@ def test_version(mfx):
     ("222[1]", 2, [1, 1, 1, 0, -1, -1, -1, -1]),
     ("234[1]5678", 8, [1, 2, 3, 0, 4, 5, 6, 7]),          # extra scalar equations
     ("111[1]1111", 1, [0, 0, 0, 0, 0, 0, 0, 0]),
+    ("234[1234]", 4, [1, 2, 3, 0, -1, -1, -1, -1]),       # Fig. 2b: multi-GPU pressure
+    ("222[12]1", 2, [1, 1, 1, 0, 0, -1, -1, -1]),
 ])
 def test_parse_assignment(mfx, text, n, owner):
     a = mfx.parse_assignment(text, n)
@@ -70,7 +72,8 @@ def test_parse_assignment(mfx, text, n, owner):
     ("111", 1),
     ("111[]", 1),
     ("111[1]x", 1),
-    ("234[1234]", 4),      # multi-GPU pressure (NEXT-1) rejected in v1
+    ("234[124]", 4),       # a multi-GPU pressure list must name every rank ...
+    ("234[2134]", 4),      # ... in order
     ("111[1]11111", 1),    # > 4 scalars
 ])
 def test_parse_assignment_errors(mfx, text, n):
@@ -80,26 +83,35 @@ def test_parse_assignment_errors(mfx, text, n):
     assert mfx.last_error()
 
 
-def _plan_all(mfx, text, n):
-    return {r: (mfx.exchange_plan(text, n, r, 0), mfx.exchange_plan(text, n, r, 1)) for r in range(n)}
+def _plan_all(mfx, text, n, nz=16):
+    return {r: (mfx.exchange_plan(text, n, r, 0, nz), mfx.exchange_plan(text, n, r, 1, nz)) for r in range(n)}
 
 
 @pytest.mark.parametrize("text,n", [("234[1]", 4), ("222[1]", 2), ("234[1]5678", 8), ("211[2]3", 3),
-                                    ("111[1]", 1), ("111[1]", 3)])
+                                    ("111[1]", 1), ("111[1]", 3), ("234[1234]", 4), ("222[12]1", 2)])
 def test_exchange_plan_consistency(mfx, text, n):
     plans = _plan_all(mfx, text, n)
     a = mfx.parse_assignment(text, n)
     P = a["owner"][3]
+    prs = list(range(n)) if a["n_p"] > 1 else [P]
     # GATHER: every send has exactly one matching recv on the peer, same buffer
     sends = [(r, o["peer"], o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_SEND]
     recvs = [(o["peer"], r, o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_RECV]
     assert sorted(sends) == sorted(recvs)
     for (src, dst, buf, slot) in sends:
-        assert dst == P and src != P
-    # each momentum component not owned by P is gathered (u*, d, meta)
-    need = {c for c in range(3) if a["owner"][c] != P}
-    got = {"uvw".index(b) for (_, _, b, _) in sends if b in ("u", "v", "w")}
-    assert got == need
+        assert dst in prs and src != dst
+    # every p' rank ends up with every momentum component (u*, d, meta)
+    for pr in prs:
+        got = {"uvw".index(b) for (_, d, b, _) in sends if b in ("u", "v", "w") and d == pr}
+        assert got == {c for c in range(3) if a["owner"][c] != pr}
+    # PSLAB (multi-GPU p'): slabs tile [0, nz) and all go to P0
+    if a["n_p"] > 1:
+        slabs = sorted((o["k0"], o["k1"]) for r in range(n) for o in mfx.exchange_plan(text, n, r, 2, 16)
+                       if o["op"] == mfx.OP_RECV)
+        own = mfx.dist_slab(16, P, n)
+        cover = sorted(slabs + [own])
+        assert cover[0][0] == 0 and cover[-1][1] == 16
+        assert all(cover[i][1] == cover[i + 1][0] for i in range(len(cover) - 1))
     # BCAST: identical op list on every rank (collective order must match)
     b0 = plans[0][1]
     for r in range(n):

@@ -70,6 +70,9 @@ def run_ranks(mfx, assignment, nranks, g, pr, st, outer=2):
     ("121[2]", 2, 0),
     ("234[1]5678", 8, 4),
     ("111[1]2", 2, 1),
+    ("234[1234]", 4, 0),          # Fig. 2b: multi-GPU pressure solve
+    ("212[12]1", 2, 1),
+    ("234[12345678]5678", 8, 4),  # p' over all 8 ranks + 4 scalars
 ])
 def test_multirank_equals_single_rank(mfx, orc, assignment, nranks, n_scalars):
     g, pr, st = make_case(n_scalars)

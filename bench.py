@@ -55,6 +55,13 @@ def assignment_for(n):
     return "234[1]" + "".join(str(5 + s) for s in range(min(n - 4, 4)))
 
 
+def assignment_multi_p(n):
+    """Same equation owners, pressure correction split over every GPU ([12..n])."""
+    base = assignment_for(n)
+    head, tail = base.split("]")
+    return head.split("[")[0] + "[" + "".join(str(i + 1) for i in range(n)) + "]" + tail
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -378,6 +385,54 @@ def run_mfx(args, rank, world, local_rank):
     extras = None
     if world == 1 and not args.no_extras:
         extras = measure_other_configs(mfx, torch)
+    elif world > 1 and not args.no_extras:
+        extras = {}
+        try:   # (a) the paper's multi-GPU pressure solve: same owners, p' over [12..N]
+            obj = [mfx.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            asg2 = assignment_multi_p(world)
+            ctx2 = mfx.SimpleContext(asg2, g, pr, rank=rank, nranks=world, uid=obj[0])
+            for k, v in host.items():
+                sd[k].copy_(v, non_blocking=True)
+            ctx2.step(sd)
+            barrier()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            its2 = 0
+            for _ in range(args.steps):
+                o2 = ctx2.step(sd)
+                its2 += sum(o2["iters"][q] for q in range(8) if ctx2.assignment["owner"][q] >= 0)
+            m1.record(stream)
+            barrier()
+            tt = torch.tensor([m0.elapsed_time(m1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms2 = float(tt.item())
+            extras["multi_gpu_pressure"] = {"assignment": asg2, "simple_iters_per_s": args.steps / (ms2 / 1e3),
+                                            "bicgstab_iters_per_s": its2 / (ms2 / 1e3),
+                                            "pp_phase_ms_last": ctx2.phase_times()["pp"]}
+            # (b) domain-decomposed comparator: the p' solve of this step over all N ranks
+            #     (halo planes + all-gathered dots every iteration, P:87 / Fig. 2a)
+            k0, k1 = mfx.dist_slab(g.nz, rank, world)
+            plane = g.nx * g.ny
+            ws2 = mfx.Workspace(g)
+            star = [ctx2.buffer(k) for k in ("u*", "v*", "w*", "dx", "dy", "dz")]   # every rank holds them
+            sysd, _ = mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws2, star=star)
+            sl = {k: v[k0 * plane:k1 * plane] for k, v in sysd.items()}
+            xs = torch.zeros((k1 - k0) * plane, dtype=torch.float64, device="cuda")
+            barrier()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            info = ctx2.dist_solve(mfx.EQ_PP, sl, xs, 0.0, 100)
+            d1.record(stream)
+            barrier()
+            tt = torch.tensor([d0.elapsed_time(d1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            extras["dd_comparator_pp"] = {"ranks": world, "iters": info["iters"],
+                                          "us_per_iter": 1e3 * float(tt.item()) / max(info["iters"], 1),
+                                          "single_rank_us_per_iter": 1e3 * phase["pp"] / max(outs[-1]["iters"][3], 1)}
+            ctx2.close()
+        except Exception as e:  # keep the main line
+            extras["error"] = repr(e)[:300]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -39,3 +39,12 @@ def test_peaks_file_used():
         assert kind == "measured" and peak == json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     else:
         assert "fallback" in kind
+
+
+@pytest.mark.parametrize("n", range(1, 9))
+def test_assignment_multi_p_every_gpu_count(n):
+    import paper_2211_15605_b200 as mfx
+    b = load_bench()
+    a = mfx.parse_assignment(b.assignment_multi_p(n), n)
+    assert a["n_p"] == n and a["owner"][3] == 0
+    assert a["owner"][:3] == mfx.parse_assignment(b.assignment_for(n), n)["owner"][:3]

@@ -1,1 +1,3 @@
-timeout 1500 python -m pytest tests/test_gpu_multirank.py tests/test_gpu_dist_solver.py -x -q 2>&1 | tail -15
+timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "
+import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['pp_iteration'], d['e2e']['value'], d['roofline']['frac'])"

@@ -36,14 +36,15 @@ CONFIG_ID = 2
 BYTES_PER_CELL = {
     "K1_mom": 4 * 8 + 2 * 8 + 7 * 8,     # r, p_old, v_old, r^ read; p, v write; 7 coefficients
     "K2_mom": 2 * 8 + 1 * 8 + 7 * 8,     # r, v read; t write; 7 coefficients
-    "K1_pp": 4 * 8 + 2 * 8 + 4 * 8,      # symmetric p' storage: aP, c_x, c_y, c_z
-    "K2_pp": 2 * 8 + 1 * 8 + 4 * 8,
+    "K1_pp": 4 * 8 + 2 * 8 + 3 * 8,      # symmetric p' storage c_x, c_y, c_z; aP = row sum, not read
+    "K2_pp": 2 * 8 + 1 * 8 + 3 * 8,
     "K3": 6 * 8 + 2 * 8,                 # x, p, r, v, t, r^ read; x, r write
     "assemble_mom": 9 * 8 + 9 * 8,       # eps, eps0, u, v, w, c_old, p, beta, S read; 7 coef + b + d write
     "assemble_pp": 8 * 8 + 5 * 8,        # eps, eps0, u*, v*, w*, d_x, d_y, d_z read; aP, c_x, c_y, c_z, b write
     "correct": 8 * 8 + 4 * 8,            # u*, v*, w*, d_x, d_y, d_z, p', p read; u, v, w, p write
     "spmv_setup": None, "assemble_scalar": None,
 }
+PP_ITER_BPC = BYTES_PER_CELL["K1_pp"] + BYTES_PER_CELL["K2_pp"] + BYTES_PER_CELL["K3"]   # 184
 
 
 def assignment_for(n):
@@ -216,7 +217,7 @@ def measure_other_configs(mfx, torch):
                           "simple_iters_per_s": steps / (ms / 1e3),
                           "bicgstab_iters_per_s": its / (ms / 1e3),
                           "pp_us_per_iter": 1e3 * ph["pp"] / pp_it,
-                          "pp_alg_GBps": 200 * g.n / (1e-3 * ph["pp"] / pp_it) / 1e9,
+                          "pp_alg_GBps": PP_ITER_BPC * g.n / (1e-3 * ph["pp"] / pp_it) / 1e9,
                           "iters_last": o["iters"][:4]}
         ctx.close()
         del sd

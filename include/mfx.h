@@ -84,7 +84,11 @@ typedef struct {
 /* Equation system (device pointers, N each).  Momentum/scalar: all seven
  * coefficient arrays, row a_P x_P - sum a_nb x_nb = b.  p': symmetric
  * storage, aE/aN/aT hold the face coefficients c_x/c_y/c_z and aW/aS/aB must
- * be NULL.  d (momentum only) = eps_f A_f / a_P,relaxed (Q16, Q27). */
+ * be NULL; its diagonal is by definition the ordered row sum
+ * a_P = ((((c_W + c_E) + c_S) + c_N) + c_B) + c_T, which
+ * mfx_spmv / the solvers rebuild on the fly: they never read aP (may be NULL;
+ * mfx_assemble_eq still writes it).  d (momentum only) = eps_f A_f /
+ * a_P,relaxed (Q16, Q27). */
 typedef struct { double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d; } mfx_eqsys;
 
 typedef struct {

@@ -112,10 +112,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     const int tid = threadIdx.x;
-    constexpr int NA = SYM ? 4 : 7;
+    constexpr int NA = SYM ? 3 : 7;
     extern __shared__ __align__(16) double smd[];
     const int M = a.M;
-    double *C = smd;                     // NA arrays: SYM {aP, cx, cy, cz}; else {aP, aW, aE, aS, aN, aB, aT}
+    double *C = smd;                     // NA arrays: SYM {cx, cy, cz} (aP derived); else {aP, aW, aE, aS, aN, aB, aT}
     double *b = C + NA * M;
     double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
     __shared__ int k0s[CL + 1];
@@ -141,10 +141,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
 
     for (int i = tid; i < nc; i += CT) {
         if (SYM) {
-            C[0 * M + i] = a.aP[g0 + i];
-            C[1 * M + i] = a.aE[g0 + i];
-            C[2 * M + i] = a.aN[g0 + i];
-            C[3 * M + i] = a.aT[g0 + i];
+            C[0 * M + i] = a.aE[g0 + i];
+            C[1 * M + i] = a.aN[g0 + i];
+            C[2 * M + i] = a.aT[g0 + i];
         } else {
             C[0 * M + i] = a.aP[g0 + i];
             C[1 * M + i] = a.aW[g0 + i];
@@ -190,9 +189,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         if (f & 16) xB = (f & 64) ? X[i - plane] : hb[o];
         if (f & 32) xT = (f & 128) ? X[i + plane] : ha[o];
         double aP, aW, aE, aS, aN, aB, aT;
-        aP = C[i];
         if (SYM) {
-            const double *cx = C + M, *cy = C + 2 * M, *cz = C + 3 * M;
+            const double *cx = C, *cy = C + M, *cz = C + 2 * M;
             aW = (f & 1) ? cx[i - 1] : 0.0;
             aE = cx[i];
             aS = (f & 4) ? cy[i - nx] : 0.0;
@@ -200,7 +198,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             aB = 0.0;
             if (f & 16) aB = (f & 64) ? cz[i - plane] : czb[o];
             aT = cz[i];
+            aP = ((((aW + aE) + aS) + aN) + aB) + aT;   // p' diagonal = row sum
         } else {
+            aP = C[i];
             aW = C[1 * M + i]; aE = C[2 * M + i]; aS = C[3 * M + i];
             aN = C[4 * M + i]; aB = C[5 * M + i]; aT = C[6 * M + i];
         }
@@ -246,7 +246,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     // ---- setup: r = b - A x0
     cluster_barrier();   // x0 and coefficients of every slab loaded
     if (SYM)
-        for (int o = tid; o < plane; o += CT) czb[o] = rb >= 0 ? cl.map_shared_rank(C + 3 * M, rb)[lb + o] : 0.0;
+        for (int o = tid; o < plane; o += CT) czb[o] = rb >= 0 ? cl.map_shared_rank(C + 2 * M, rb)[lb + o] : 0.0;
     fetch_halo(x);
     {
         Acc bb, ra_;
@@ -381,7 +381,7 @@ size_t cluster_smem(const Geo &G, bool sym)
 {
     const long long plane = (long long)G.nx * G.ny;
     const long long M = plane * ((G.nz + CL - 1) / CL);
-    return (size_t)(((sym ? 12 : 15) * M + 3 * plane) * sizeof(double) + M * sizeof(int));
+    return (size_t)(((sym ? 11 : 15) * M + 3 * plane) * sizeof(double) + M * sizeof(int));
 }
 
 bool cluster_fits(const Geo &G, bool sym) { return cluster_smem(G, sym) <= 200 * 1024; }

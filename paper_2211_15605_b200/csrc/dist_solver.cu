@@ -52,7 +52,7 @@ __device__ __forceinline__ double apply_slab(const DSlab &D, const DCoef &c, con
     double xB = 0.0, xT = 0.0;
     if (k > 0) xB = kl > 0 ? X[n - D.plane] : hb[o];
     if (k < D.nz - 1) xT = kl < D.npl - 1 ? X[n + D.plane] : ha[o];
-    double aP = c.aP[n], aW, aE, aS, aN, aB, aT;
+    double aP, aW, aE, aS, aN, aB, aT;
     if (SYM) {
         aW = ix > 0 ? c.aE[n - 1] : 0.0;
         aE = c.aE[n];
@@ -61,7 +61,9 @@ __device__ __forceinline__ double apply_slab(const DSlab &D, const DCoef &c, con
         aB = 0.0;
         if (k > 0) aB = kl > 0 ? c.aT[n - D.plane] : czb[o];
         aT = c.aT[n];
+        aP = ((((aW + aE) + aS) + aN) + aB) + aT;   // p' diagonal = row sum
     } else {
+        aP = c.aP[n];
         aW = c.aW[n]; aE = c.aE[n]; aS = c.aS[n]; aN = c.aN[n]; aB = c.aB[n]; aT = c.aT[n];
     }
     double y = aP * xc;
@@ -349,8 +351,8 @@ mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eq
 {
     MFX_ARG_CHECK(ctx && grid && A && x, "NULL argument");
     const bool sym = kind == MFX_EQ_PP;
-    MFX_ARG_CHECK(A->aP && A->aE && A->aN && A->aT && A->b && (sym ? (!A->aW && !A->aS && !A->aB)
-                                                                   : (A->aW && A->aS && A->aB)),
+    MFX_ARG_CHECK(A->aE && A->aN && A->aT && A->b && (sym ? (!A->aW && !A->aS && !A->aB)
+                                                          : (A->aP && A->aW && A->aS && A->aB)),
                   "bad slab eqsys for kind %d", kind);
     const int R = ctx_nranks(ctx), rank = ctx_rank(ctx);
     MFX_ARG_CHECK(grid->nz >= R, "dist solve: nz (%d) must be >= number of ranks (%d)", grid->nz, R);

@@ -35,7 +35,7 @@ enum StencilMode { SM_SPMV = 0, SM_SETUP = 1, SM_K1 = 2, SM_K2 = 3 };
 
 struct TmaMaps {
     CUtensorMap halo[3];   // halo box arrays (x | r,p_old,v_old | r,v)
-    CUtensorMap coef[7];   // SYM: aP, cz (cell), cx (x-halo box), cy (y-halo box); else aP,aW,aE,aS,aN,aB,aT
+    CUtensorMap coef[7];   // SYM: cz (cell), -, cx (x-halo box), cy (y-halo box); else aP,aW,aE,aS,aN,aB,aT
     CUtensorMap extra;     // SETUP: b ; K1: r^
 };
 
@@ -114,7 +114,7 @@ struct Cfg {
     static_assert(CPT == 1 || CPT == 2, "1 or 2 cells per thread");
     static_assert(NT % 32 == 0 && NT <= 512, "consumer threads");
     static constexpr int NH = MODE == SM_K1 ? 3 : (MODE == SM_K2 ? 2 : 1);
-    static constexpr int NCELLC = SYM ? 2 : 7;             // coefficient arrays with the cell box
+    static constexpr int NCELLC = SYM ? 1 : 7;             // coefficient arrays with the cell box (SYM: cz; aP derived)
     static constexpr int NE = (MODE == SM_SETUP || MODE == SM_K1) ? 1 : 0;
     static constexpr int HALO_TX = HX * HY * 8, CELL_TX = TX * TY * 8;
     static constexpr int XW_TX = HX * TY * 8, YS_TX = TX * (TY + 1) * 8;
@@ -331,12 +331,12 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             }
             double czcur[CPT];
             if (CPT == 2 && SYM && !virt) {
-                const double2 z2 = *(const double2 *)((const double *)(st + C::OFF_CELL + C::CELL_B) + ci);
+                const double2 z2 = *(const double2 *)((const double *)(st + C::OFF_CELL) + ci);
                 czcur[0] = z2.x; czcur[CPT - 1] = z2.y;
             } else {
 #pragma unroll
                 for (int m = 0; m < CPT; m++)
-                    czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL + C::CELL_B))[ci + m] : 0.0;
+                    czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL))[ci + m] : 0.0;
             }
             asm volatile("bar.sync 1, %0;" ::"n"(C::NT) : "memory");
 
@@ -369,8 +369,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                     xS[0] = Pc[hc - C::HX]; xN[0] = Pc[hc + C::HX]; xB[0] = Pb[hc]; xT[0] = Pt[hc];
                 }
                 if (CPT == 2) {
-                    const double2 p2 = *(const double2 *)&cell[ci];
-                    aP[0] = p2.x; aP[CPT - 1] = p2.y;
                     if (SYM) {
                         const double *xw = (const double *)(so + C::OFF_XW);
                         const double *ys = (const double *)(so + C::OFF_YS);
@@ -385,6 +383,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         aT[0] = czq1[0]; aT[CPT - 1] = czq1[CPT - 1];
                     } else {
                         double2 t2;
+                        t2 = *(const double2 *)&cell[ci]; aP[0] = t2.x; aP[CPT - 1] = t2.y;
                         t2 = *(const double2 *)&cell[1 * (C::CELL_B / 8) + ci]; aW[0] = t2.x; aW[CPT - 1] = t2.y;
                         t2 = *(const double2 *)&cell[2 * (C::CELL_B / 8) + ci]; aE[0] = t2.x; aE[CPT - 1] = t2.y;
                         t2 = *(const double2 *)&cell[3 * (C::CELL_B / 8) + ci]; aS[0] = t2.x; aS[CPT - 1] = t2.y;
@@ -395,7 +394,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                 } else
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
-                    aP[m] = cell[ci + m];
                     if (SYM) {
                         const double *xw = (const double *)(so + C::OFF_XW);
                         const double *ys = (const double *)(so + C::OFF_YS);
@@ -406,6 +404,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         aB[m] = czq0[m];
                         aT[m] = czq1[m];
                     } else {
+                        aP[m] = cell[ci + m];
                         aW[m] = cell[1 * (C::CELL_B / 8) + ci + m];
                         aE[m] = cell[2 * (C::CELL_B / 8) + ci + m];
                         aS[m] = cell[3 * (C::CELL_B / 8) + ci + m];
@@ -414,6 +413,11 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         aT[m] = cell[6 * (C::CELL_B / 8) + ci + m];
                     }
                 }
+                // p': the diagonal is the row sum of the face coefficients (DESIGN.md
+                // §3.4), rebuilt in the assembly's order instead of streamed (8 B/cell)
+                if (SYM)
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) aP[m] = ((((aW[m] + aE[m]) + aS[m]) + aN[m]) + aB[m]) + aT[m];
                 double y[CPT];
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
@@ -676,14 +680,14 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
 
 }  // namespace
 
-// coefficient order for the maps: SYM -> {aP, cz, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
+// coefficient order for the maps: SYM -> {cz, -, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],
                           const mfx_eqsys *A, const double *extra, double *o0, double *o1, double *o2,
                           WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s, int reverse)
 {
     const double *coef[7];
     if (sym) {
-        coef[0] = A->aP; coef[1] = A->aT; coef[2] = A->aE; coef[3] = A->aN;
+        coef[0] = A->aT; coef[1] = nullptr; coef[2] = A->aE; coef[3] = A->aN;
         coef[4] = coef[5] = coef[6] = nullptr;
     } else {
         coef[0] = A->aP; coef[1] = A->aW; coef[2] = A->aE; coef[3] = A->aS;

@@ -1,3 +1,2 @@
-timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "
-import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['pp_iteration'], d['e2e']['value'], d['roofline']['frac'])"
+ncu --set full --clock-control none --import-source on -k regex:"k_stencil|k3v" -s 4 -c 3 -o gpurun_out/r01b_prof_pp python scripts/prof_solve.py --kind pp --iters 4 > gpurun_out/ncu_pp.log 2>&1; tail -1 gpurun_out/ncu_pp.log
+ls -la gpurun_out/

@@ -34,7 +34,7 @@ else:
     kind = mfx.EQ_W
 torch.cuda.synchronize()
 N = g.n
-BPC = {"K1_pp": 80, "K2_pp": 56, "K3": 64, "K1_mom": 104, "K2_mom": 80, "spmv_setup": None}
+BPC = {"K1_pp": 72, "K2_pp": 48, "K3": 64, "K1_mom": 104, "K2_mom": 80, "spmv_setup": None}
 for r in range(args.repeat):
     if r == args.repeat - 1:
         mfx.prof_reset()

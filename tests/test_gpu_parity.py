@@ -202,6 +202,29 @@ def test_bicgstab_pp_ragged_parity(mfx, orc, name, solver_path):
     assert_solve_parity(ref, info, x)
 
 
+def test_pp_diagonal_derived_not_read(mfx, orc, solver_path):
+    """p' kind: every path rebuilds a_P as the ordered row sum
+    and never reads A->aP -- a NaN-poisoned or absent aP changes no bit."""
+    g, pr, st = case("rag2")
+    need_path(solver_path, g, True)
+    dv = [np.random.default_rng(21 + a).uniform(1e-4, 1e-3, g.n) for a in range(3)]
+    sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+    ref = orc.bicgstab(g, sysd, np.zeros(g.n), 1e-9, 400)
+    x = np.random.default_rng(5).normal(size=g.n)
+    yref = orc.spmv(g, sysd, x)
+    for variant in ("nan", "absent"):
+        d = {k: dev(v) for k, v in sysd.items()}
+        if variant == "nan":
+            d["aP"] = torch.full_like(d["aP"], float("nan"))
+        else:
+            del d["aP"]
+        assert np.array_equal(host(mfx.spmv(mfx.EQ_PP, g, d, dev(x))), yref), variant
+        ws = mfx.Workspace(g)
+        xs = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+        info = mfx.bicgstab_solve(mfx.EQ_PP, g, d, xs, 1e-9, 400, ws)
+        assert info["iters"] == ref["iters"] and np.array_equal(host(xs), ref["x"]), variant
+
+
 @pytest.mark.parametrize("maxit", [0, 1, 2, 7])
 def test_bicgstab_not_converged_last_iterate(mfx, orc, maxit, solver_path):
     g, pr, st = case("rag2")

@@ -51,6 +51,34 @@ def test_pp_symmetric_and_diagonal_sum(orc):
     assert cont == pytest.approx(np.abs(s["b"]).sum(), rel=1e-14)
 
 
+@pytest.mark.parametrize("shape,bc", [((16, 16, 32), (BC_INLET, BC_OUTLET)), ((6, 5, 7), (BC_WALL, BC_OUTLET)),
+                                      ((4, 9, 3), (BC_INLET, BC_WALL))])
+def test_pp_diagonal_is_ordered_row_sum(orc, shape, bc):
+    """a_P = ((((c_W + c_E) + c_S) + c_N) + c_B) + c_T with the
+    minus-face coefficients taken from the neighbours' stored c_x, c_y, c_z
+    (0 at the minus boundary).  Bitwise: the GPU solver rebuilds a_P this way
+    instead of streaming it, so the stored a_P must be exactly this sum."""
+    g = synth.make_grid(*shape, bc_zlo=bc[0], bc_zhi=bc[1])
+    pr = Params()
+    st = synth.make_state(g, 77, pr)
+    rng = np.random.default_rng(1)
+    dv = [rng.uniform(1e-4, 1e-3, g.n) for _ in range(3)]
+    s, _, rc = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+    assert rc == 0
+    sh = (g.nz, g.ny, g.nx)
+    cx, cy, cz = (s[k].reshape(sh) for k in ("aE", "aN", "aT"))
+    cW = np.zeros(sh); cW[:, :, 1:] = cx[:, :, :-1]
+    cS = np.zeros(sh); cS[:, 1:, :] = cy[:, :-1, :]
+    cB = np.zeros(sh); cB[1:, :, :] = cz[:-1, :, :]
+    rowsum = ((((cW + cx) + cS) + cy) + cB) + cz
+    assert np.array_equal(s["aP"].reshape(sh), rowsum)
+    assert np.all(cx[:, :, -1] == 0) and np.all(cy[:, -1, :] == 0)      # wall faces
+    if bc[1] == BC_WALL:
+        assert np.all(cz[-1] == 0)
+    else:
+        assert np.all(cz[-1] > 0)                                        # outlet face stays in a_P
+
+
 def test_pp_laplacian_closed_form(orc):
     """eps = 1, uniform d: interior coefficient c = rho A d and A q for a
     quadratic q equals -sum_a 2 c_a h_a^2 exactly (7-point Laplacian of x^2+y^2+z^2)."""

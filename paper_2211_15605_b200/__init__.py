@@ -17,7 +17,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libmfx.so")
 if not os.path.exists(_SO):
-    raise ImportError(f"{_SO} is not built: run `python -m paper_2211_15605_b200.build` "
+    raise ImportError(f"{_SO} is not built: run `python paper_2211_15605_b200/build.py` "
                       "(there is no CPU fallback)")
 _lib = C.CDLL(_SO, mode=C.RTLD_GLOBAL)
 

@@ -1,6 +1,6 @@
 """Build libmfx.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2211_15605_b200.build [--force] [--verbose]
+    python paper_2211_15605_b200/build.py [--force] [--verbose]
 
 --fmad=false: no FMA contraction (DESIGN.md §3 arithmetic contract; fma() is
 explicit).  -cudart static keeps the library independent of torch's cudart.

@@ -18,3 +18,19 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def build_mfx():
+    """Compile libmfx.so if it is missing or stale.  build.py is loaded by
+    path: importing the package itself raises until the library exists."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_mfx_build", os.path.join(ROOT, "paper_2211_15605_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()
+
+
+@pytest.fixture(scope="session")
+def mfx_built():
+    return build_mfx()

@@ -14,9 +14,7 @@ HEADER = os.path.join(ROOT, "include", "mfx.h")
 
 
 @pytest.fixture(scope="module")
-def mfx():
-    from paper_2211_15605_b200 import build
-    build.build()
+def mfx(mfx_built):
     import paper_2211_15605_b200 as m
     return m
 

@@ -140,9 +140,7 @@ def worker(rank, world, port, assignment, n_scalars, q):
 
 @pytest.mark.parametrize("assignment,n_scalars", [("222[1]", 0), ("121[2]", 0), ("211[1]2", 1), ("112[2]12", 2),
                                                    ("212[12]", 0), ("122[12]2", 1)])
-def test_two_rank_decomposition_bitwise(orc, assignment, n_scalars):
-    from paper_2211_15605_b200 import build
-    build.build()
+def test_two_rank_decomposition_bitwise(orc, mfx_built, assignment, n_scalars):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -117,6 +117,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def bench_config(asg, grid, n_scal):
+    return {"workload": "c2: one SIMPLE outer iteration per step on 128x128x512 "
+                        f"(assignment {asg}): u,v,w momentum assembly+BiCGSTAB "
+                        "(tol 1e-4, maxit 20), p' assembly+BiCGSTAB (tol 1e-6, maxit 500), "
+                        "correction, state exchange",
+            "grid": list(grid), "assignment": asg, "equations": 4 + n_scal,
+            "l2": "inputs larger than L2 (13 fields x 64 MiB snapshot + systems >> 126 MB)"}
+
+
 # ---------------------------------------------------------------- reference arm (oracle)
 def oracle_sample(seconds_hint=False):
     """Bounded sample: BiCGSTAB on the oracle-assembled c2 p' system, x0 = 0,
@@ -156,7 +165,8 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "c2 p' BiCGSTAB sample (oracle)", "grid": [128, 128, 512]},
+            "data": "synthetic (seeded fluidized-bed fields, synth/)",
+            "config": bench_config("111[1]", (128, 128, 512), 0),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": SAMPLE_DESC},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -196,6 +206,7 @@ def measure_other_configs(mfx, torch):
     out["c1"] = {"workload": "p' BiCGSTAB solve 16x16x32, tol 1e-6 (single-cluster solver)",
                  "iters": iters, "ms_per_solve": ms, "us_per_iter": 1e3 * ms / iters,
                  "bicgstab_iters_per_s": iters / (ms / 1e3)}
+    out["c2_momentum"] = measure_momentum_c2(mfx, torch)
     for cid, steps in ((3, 5), (4, 3)):
         g, pr, st = synth.config_case(cid)
         sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
@@ -222,7 +233,95 @@ def measure_other_configs(mfx, torch):
         ctx.close()
         del sd
         torch.cuda.empty_cache()
+    out["c5_one_gpu"] = measure_scalars_one_gpu(mfx, torch)
     return out
+
+
+def _ev_ms(torch, fn, reps):
+    """Median device time (CUDA events on the current stream) of fn() over reps."""
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts), r
+
+
+def measure_momentum_c2(mfx, torch):
+    """BASELINE.json configs[1] exactly: one momentum equation (w: convection-
+    diffusion + implicit drag) assembled and solved on 128x128x512, 1 GPU.
+    Per-iteration time by the SURVEY §8(d) procedure: tol = 0 with maxit 2 and
+    10, (T10 - T2) / 8, which excludes the setup."""
+    import synth
+    g, pr, st = synth.config_case(CONFIG_ID)
+    sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+    ws = mfx.Workspace(g)
+    sysd = mfx.new_system(mfx.EQ_W, g.n)
+    asm_ms, _ = _ev_ms(torch, lambda: mfx.assemble_eq(mfx.EQ_W, g, pr, sd, ws, out=sysd), 7)
+    x = sd["w"].clone()
+
+    def solve(tol, maxit):
+        x.copy_(sd["w"])
+        return mfx.bicgstab_solve(mfx.EQ_W, g, sysd, x, tol, maxit, ws)
+    solve_ms, info = _ev_ms(torch, lambda: solve(pr.lin_tol_mom, pr.lin_maxit_mom), 7)
+    t2, _ = _ev_ms(torch, lambda: solve(0.0, 2), 7)
+    t10, _ = _ev_ms(torch, lambda: solve(0.0, 10), 7)
+    it_us = 1e3 * (t10 - t2) / 8
+    bpc = BYTES_PER_CELL["K1_mom"] + BYTES_PER_CELL["K2_mom"] + BYTES_PER_CELL["K3"]
+    res = {"workload": "configs[1]: w-momentum assembly + BiCGSTAB (tol 1e-4, maxit 20, x0 = snapshot) "
+                       "on 128x128x512",
+           "assemble_us": 1e3 * asm_ms,
+           "assemble_alg_GBps": BYTES_PER_CELL["assemble_mom"] * g.n / (asm_ms * 1e-3) / 1e9,
+           "solve_iters": info["iters"], "solve_us": 1e3 * solve_ms,
+           "assemble_plus_solve_per_s": 1e3 / (asm_ms + solve_ms),
+           "bicgstab_iters_per_s": info["iters"] / ((asm_ms + solve_ms) * 1e-3),
+           "us_per_iter": it_us, "iter_alg_GBps": bpc * g.n / (it_us * 1e-6) / 1e9}
+    del sd, sysd, ws, x
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_scalars_one_gpu(mfx, torch):
+    """Configuration 5, strong reading (ii) at N = 1: the fixed 8-equation set
+    {u, v, w, p', E, Y1, Y2, Y3} ('111[1]1111') against the 4-equation '111[1]',
+    one SIMPLE outer iteration each, on the c3 and c2 grids."""
+    import numpy as np
+    import synth
+    res = {}
+    for cid in (3, 2):
+        g, pr, st = synth.config_case(cid, n_scalars=4)
+        rng = np.random.default_rng(77)
+        for s in range(4):
+            st[f"phi_old{s}"] = rng.uniform(0, 1, g.n)
+            st[f"phi{s}"] = st[f"phi_old{s}"].copy()
+        base = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+        row = {}
+        for asg in ("111[1]", "111[1]1111"):
+            ctx = mfx.SimpleContext(asg, g, pr)
+            sd = {k: v.clone() for k, v in base.items()}
+            ctx.step(sd)
+            ms_l, its = [], 0
+            for _ in range(3):
+                sd = {k: v.clone() for k, v in base.items()}
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                o = ctx.step(sd)
+                e1.record()
+                torch.cuda.synchronize()
+                ms_l.append(e0.elapsed_time(e1))
+                its = sum(o["iters"])
+            ms = statistics.median(ms_l)
+            row[asg] = {"ms_per_simple_iter": ms, "bicgstab_iters": its, "iters": o["iters"],
+                        "equation_solves_per_s": (4 if asg == "111[1]" else 8) / (ms * 1e-3)}
+            ctx.close()
+        res[f"c{cid}"] = row
+        del base
+        torch.cuda.empty_cache()
+    return res
 
 
 # ---------------------------------------------------------------- product arm
@@ -447,12 +546,7 @@ def run_mfx(args, rank, world, local_rank):
                 "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak" if world > 4 else "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded fluidized-bed fields, synth/)",
-                "config": {"workload": "c2: one SIMPLE outer iteration per step on 128x128x512 "
-                                       f"(assignment {asg}): u,v,w momentum assembly+BiCGSTAB "
-                                       "(tol 1e-4, maxit 20), p' assembly+BiCGSTAB (tol 1e-6, maxit 500), "
-                                       "correction, state exchange",
-                           "grid": [g.nx, g.ny, g.nz], "assignment": asg, "equations": 4 + n_scal,
-                           "l2": "inputs larger than L2 (13 fields x 64 MiB snapshot + systems >> 126 MB)"},
+                "config": bench_config(asg, (g.nx, g.ny, g.nz), n_scal),
                 "simple_iters_per_s": simple_per_s,
                 "bicgstab_iters_per_step": it_all / args.steps,
                 "iters_last_step": outs[-1]["iters"],

@@ -21,6 +21,10 @@ Parity status per function:
                                    dominance); the general 3-D row with every term
                                    active is "parity unpinned" beyond these cases.
   or_correct ..................... pinned (continuity identity b(u_corr) = b(u*) - A p')
+  or_pic_deposit_eps / or_pic_drag  pinned (partition of unity, node coincidence, symmetry,
+                                   trilinear exactness on linear fields, Dalla Valle
+                                   single-sphere limit eps_g = 1 -> V_r = 1, Stokes limit,
+                                   SPEC.md:290 V_r = A at Re = 0, momentum bookkeeping)
 """
 from __future__ import annotations
 
@@ -80,6 +84,14 @@ class OgSolveInfo(C.Structure):
                 ("rel_resid", C.c_double)]
 
 
+class OgParcels(C.Structure):
+    _fields_ = [(k, _DP) for k in ("x", "y", "z", "u", "v", "w", "omega")] + [("n", C.c_long)]
+
+
+class OgPicParams(C.Structure):
+    _fields_ = [("d_p", C.c_double), ("eps_min", C.c_double)]
+
+
 _lib = None
 
 
@@ -105,6 +117,12 @@ def lib():
         L.or_correct.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams)] + [_DP] * 12
         L.or_simple_iter.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.c_int,
                                      C.POINTER(OgState), _DP, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.or_pic_deposit_eps.argtypes = [C.POINTER(OgGrid), C.POINTER(OgPicParams), C.POINTER(OgParcels), _DP]
+        L.or_pic_drag_coef.restype = C.c_double
+        L.or_pic_drag_coef.argtypes = [C.POINTER(OgParams), C.POINTER(OgPicParams), C.c_double, C.c_double,
+                                       C.c_double]
+        L.or_pic_drag.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.POINTER(OgPicParams),
+                                  C.POINTER(OgParcels)] + [_DP] * 10
         _lib = L
     return _lib
 
@@ -245,6 +263,53 @@ def simple_iter(grid, params, state: dict, n_scalars: int = 0):
     cg, cp = c_grid(grid), c_params(params)
     rc = lib().or_simple_iter(C.byref(cg), C.byref(cp), n_scalars, C.byref(S.c), _p(resid), iters, status)
     return S.arrays, resid, list(iters), list(status), rc
+
+
+PARCEL_KEYS = ("x", "y", "z", "u", "v", "w", "omega")
+
+
+class _Parcels:
+    def __init__(self, parcels: dict):
+        self.arrays = {k: _f64(parcels[k]) for k in PARCEL_KEYS}
+        n = self.arrays["x"].size
+        assert all(a.size == n for a in self.arrays.values())
+        self.c = OgParcels(*[_p(self.arrays[k]) for k in PARCEL_KEYS], n)
+
+
+def pic_deposit_eps(grid, pic, parcels: dict):
+    """§3.9 D1: gas volume fraction from parcel solid volume.
+    pic = object with d_p, eps_min.  Returns (eps_g[N], rc)."""
+    P = _Parcels(parcels)
+    eps = np.zeros(grid.n)
+    cg, cpp = c_grid(grid), OgPicParams(pic.d_p, pic.eps_min)
+    rc = lib().or_pic_deposit_eps(C.byref(cg), C.byref(cpp), C.byref(P.c), _p(eps))
+    return eps, rc
+
+
+def pic_drag_coef(params, pic, eg: float, slip: float, omega: float = 1.0) -> float:
+    cp, cpp = c_params(params), OgPicParams(pic.d_p, pic.eps_min)
+    return lib().or_pic_drag_coef(C.byref(cp), C.byref(cpp), eg, slip, omega)
+
+
+def pic_drag(grid, params, pic, parcels: dict, eps_g, u, v, w, diag: bool = False):
+    """§3.9 D2: per-parcel Syamlal-O'Brien drag deposited to cell-centred beta and
+    beta*u_s.  Returns dict(beta, sbeta_u,
+    sbeta_v, sbeta_w, sabs[3,N], diag[M,5] = eps_g@p, u_g@p, v_g@p, w_g@p, K; rc)."""
+    P = _Parcels(parcels)
+    n, m = grid.n, P.c.n
+    out = {k: np.zeros(n) for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")}
+    sabs = np.zeros((3, n))
+    dg = np.zeros((m, 5)) if diag else None
+    fields = [_f64(a) for a in (eps_g, u, v, w)]
+    cg, cp, cpp = c_grid(grid), c_params(params), OgPicParams(pic.d_p, pic.eps_min)
+    rc = lib().or_pic_drag(C.byref(cg), C.byref(cp), C.byref(cpp), C.byref(P.c), *[_p(a) for a in fields],
+                           _p(out["beta"]), _p(out["sbeta_u"]), _p(out["sbeta_v"]), _p(out["sbeta_w"]),
+                           _p(dg) if diag else None, _p(sabs))
+    out["sabs"] = sabs
+    out["rc"] = rc
+    if diag:
+        out["diag"] = dg
+    return out
 
 
 # ---------------------------------------------------------------- helpers for pins

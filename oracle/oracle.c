@@ -713,3 +713,179 @@ int or_simple_iter(const og_grid *g, const og_params *pr, int n_scalars, og_stat
     free(pp); free(pn);
     return worst;
 }
+
+/* ------------------------------------------------------------------ §3.9 */
+/* Particle -> grid coupling on the PIC device (NEXT-2; "F is the
+ * interpolated force from the parcel location to the corresponding fluid
+ * cell", PAPER.md:97 explicit vs implicit refresh, "bilinear
+ * numerical interpolation" of eps_p; SPEC.md:200-208 deposit
+ * Syamlal-O'Brien drag).  Plain definition: parcels in ascending index order,
+ * the 8 nodes of each parcel in (kk, jj, ii) order, every expression exactly
+ * as DESIGN.md §3.9 writes it.
+ *
+ * Weights along one axis:
+ *   cell-centred lattice: xi = x/h - 0.5, node positions (i + 0.5) h;
+ *   face lattice of the velocity component along its own axis: xi = x/h - 1.0,
+ *   node positions (i + 1) h, node -1 = the unstored boundary face.
+ *   i0 = floor(xi), f = xi - i0; nodes i0 (weight 1 - f) and i0 + 1 (weight f).
+ *   Cell nodes are clamped into [0, n-1] (a parcel within half a cell of a
+ *   wall folds both weights onto the boundary cell: partition of unity kept);
+ *   face nodes are clamped into [-1, n-1]. */
+static double pic_vs(double dp) { return (((OG_PI / 6.0) * dp) * dp) * dp; }
+
+static void pic_axis(double x, double h, int n, int face, int node[2], double w[2])
+{
+    const double xi = face ? x / h - 1.0 : x / h - 0.5;
+    const double fl = floor(xi);
+    const double f = xi - fl;
+    int i0 = (int)fl, i1 = i0 + 1;
+    const int lo = face ? -1 : 0;
+    i0 = i0 < lo ? lo : (i0 > n - 1 ? n - 1 : i0);
+    i1 = i1 < lo ? lo : (i1 > n - 1 ? n - 1 : i1);
+    node[0] = i0; node[1] = i1;
+    w[0] = 1.0 - f; w[1] = f;
+}
+
+/* 8 nodes and weights of parcel position X for the lattice whose face axis is
+ * `fa` (-1: cell-centred on every axis). */
+static void pic_stencil(const og_grid *g, const double X[3], int fa, int nd[3][2], double w[3][2])
+{
+    for (int a = 0; a < 3; a++) pic_axis(X[a], spacing(g, a), ext(g, a), a == fa, nd[a], w[a]);
+}
+
+/* value of velocity component c at face node (i, j, k); index -1 along c is
+ * the unstored boundary face: w_in for the z INLET, else 0 (wall). */
+static double pic_face_value(const og_grid *g, const double *f, int c, const int q[3])
+{
+    if (q[c] == -1) return (c == 2 && g->bc_zlo == OG_INLET) ? g->w_in : 0.0;
+    return f[at(g, q)];
+}
+
+static double pic_interp(const og_grid *g, const double *f, int fa, const double X[3])
+{
+    int nd[3][2];
+    double w[3][2];
+    pic_stencil(g, X, fa, nd, w);
+    double val = 0.0;
+    for (int kk = 0; kk < 2; kk++)
+        for (int jj = 0; jj < 2; jj++)
+            for (int ii = 0; ii < 2; ii++) {
+                const int q[3] = {nd[0][ii], nd[1][jj], nd[2][kk]};
+                const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+                const double v = fa < 0 ? f[at(g, q)] : pic_face_value(g, f, fa, q);
+                val = val + W * v;
+            }
+    return val;
+}
+
+static int pic_ok(const og_grid *g, const og_parcels *pc, const og_pic_params *pp)
+{
+    if (!grid_ok(g) || !pc || !pp || pc->n < 0) return 0;
+    if (!(pp->d_p > 0.0)) return 0;
+    const double L[3] = {g->nx * g->dx, g->ny * g->dy, g->nz * g->dz};
+    for (long p = 0; p < pc->n; p++) {
+        const double X[3] = {pc->x[p], pc->y[p], pc->z[p]};
+        for (int a = 0; a < 3; a++)
+            if (!(X[a] >= 0.0 && X[a] <= L[a])) return 0;
+        if (!(pc->omega[p] >= 0.0)) return 0;
+    }
+    return 1;
+}
+
+/* D1: eps_g[c] = max(1 - (sum_p W_pc (omega_p Vs)) / V, eps_min) */
+int or_pic_deposit_eps(const og_grid *g, const og_pic_params *pp, const og_parcels *pc, double *eps_g)
+{
+    if (!pic_ok(g, pc, pp)) return OG_ERR_ARG;
+    const long N = ncell(g);
+    const double Vs = pic_vs(pp->d_p), V = volume(g);
+    for (long n = 0; n < N; n++) eps_g[n] = 0.0;
+    for (long p = 0; p < pc->n; p++) {
+        const double X[3] = {pc->x[p], pc->y[p], pc->z[p]};
+        const double vol = pc->omega[p] * Vs;
+        int nd[3][2];
+        double w[3][2];
+        pic_stencil(g, X, -1, nd, w);
+        for (int kk = 0; kk < 2; kk++)
+            for (int jj = 0; jj < 2; jj++)
+                for (int ii = 0; ii < 2; ii++) {
+                    const int q[3] = {nd[0][ii], nd[1][jj], nd[2][kk]};
+                    const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+                    eps_g[at(g, q)] += W * vol;
+                }
+    }
+    for (long n = 0; n < N; n++) {
+        const double e = 1.0 - eps_g[n] / V;
+        eps_g[n] = e < pp->eps_min ? pp->eps_min : e;
+    }
+    return OG_OK;
+}
+
+/* Syamlal-O'Brien per-parcel drag coefficient K (N s / m): the force on the
+ * gas is -K (u_g - u_p); K = beta_d (omega Vs) / eps_s with beta_d of
+ * SPEC.md:285-289, written without the eps_s that cancels. */
+double or_pic_drag_coef(const og_params *pr, const og_pic_params *pp, double eg, double slip, double omega)
+{
+    double Re = ((pr->rho * pp->d_p) * slip) / pr->mu;
+    Re = Re < 1e-12 ? 1e-12 : Re;
+    const double A = pow(eg, 4.14);
+    const double B = eg <= 0.85 ? 0.8 * pow(eg, 1.28) : pow(eg, 2.65);
+    const double q = 0.06 * Re;
+    const double Vr = 0.5 * ((A - q) + sqrt((q * q + (0.12 * Re) * (2.0 * B - A)) + A * A));
+    double Cd = 0.63 + 4.8 / sqrt(Re / Vr);
+    Cd = Cd * Cd;
+    return (omega * pic_vs(pp->d_p)) * ((((0.75 * Cd) * eg) * pr->rho) * slip) / ((Vr * Vr) * pp->d_p);
+}
+
+/* D2: per parcel interpolate eps_g (cell lattice) and u_g (staggered
+ * lattices), slip, K; deposit beta = sum W K / V and sbeta_c = sum W (K u_p,c) / V.
+ * diag (optional, may be NULL): per parcel {eps_g@p, u_g@p, v_g@p, w_g@p, K}.
+ * sabs (optional, may be NULL): 3 x N, sum W |K u_p,c| / V (error scale of sbeta). */
+int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, const og_parcels *pc,
+                const double *eps_g, const double *u, const double *v, const double *w,
+                double *beta, double *sbu, double *sbv, double *sbw, double *diag, double *sabs)
+{
+    if (!pic_ok(g, pc, pp)) return OG_ERR_ARG;
+    const long N = ncell(g);
+    const double V = volume(g);
+    const double *vel[3] = {u, v, w};
+    double *sb[3] = {sbu, sbv, sbw};
+    for (long n = 0; n < N; n++) {
+        beta[n] = 0.0; sbu[n] = 0.0; sbv[n] = 0.0; sbw[n] = 0.0;
+        if (sabs) { sabs[n] = 0.0; sabs[N + n] = 0.0; sabs[2 * N + n] = 0.0; }
+    }
+    for (long p = 0; p < pc->n; p++) {
+        const double X[3] = {pc->x[p], pc->y[p], pc->z[p]};
+        const double up[3] = {pc->u[p], pc->v[p], pc->w[p]};
+        const double eg = pic_interp(g, eps_g, -1, X);
+        double ug[3];
+        for (int c = 0; c < 3; c++) ug[c] = pic_interp(g, vel[c], c, X);
+        const double sx = ug[0] - up[0], sy = ug[1] - up[1], sz = ug[2] - up[2];
+        const double slip = sqrt((sx * sx + sy * sy) + sz * sz);
+        const double K = or_pic_drag_coef(pr, pp, eg, slip, pc->omega[p]);
+        if (diag) {
+            diag[5 * p + 0] = eg; diag[5 * p + 1] = ug[0]; diag[5 * p + 2] = ug[1]; diag[5 * p + 3] = ug[2];
+            diag[5 * p + 4] = K;
+        }
+        int nd[3][2];
+        double wt[3][2];
+        pic_stencil(g, X, -1, nd, wt);
+        for (int kk = 0; kk < 2; kk++)
+            for (int jj = 0; jj < 2; jj++)
+                for (int ii = 0; ii < 2; ii++) {
+                    const int q[3] = {nd[0][ii], nd[1][jj], nd[2][kk]};
+                    const double W = (wt[0][ii] * wt[1][jj]) * wt[2][kk];
+                    const long n = at(g, q);
+                    beta[n] += W * K;
+                    for (int c = 0; c < 3; c++) {
+                        sb[c][n] += W * (K * up[c]);
+                        if (sabs) sabs[c * N + n] += W * fabs(K * up[c]);
+                    }
+                }
+    }
+    for (long n = 0; n < N; n++) {
+        beta[n] = beta[n] / V;
+        for (int c = 0; c < 3; c++) sb[c][n] = sb[c][n] / V;
+        if (sabs) for (int c = 0; c < 3; c++) sabs[c * N + n] = sabs[c * N + n] / V;
+    }
+    return OG_OK;
+}

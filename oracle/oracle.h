@@ -82,6 +82,18 @@ void or_correct(const og_grid *g, const og_params *pr,
 int or_simple_iter(const og_grid *g, const og_params *pr, int n_scalars, og_state *st,
                    double resid[4], int iters[8], int status[8]);
 
+/* §3.9 particle -> grid coupling (NEXT-2).  Parcels: SoA, positions in
+ * [0, L] per axis, velocities, statistical weight omega >= 0. */
+#define OG_PI 3.14159265358979323846
+typedef struct { const double *x, *y, *z, *u, *v, *w, *omega; long n; } og_parcels;
+typedef struct { double d_p, eps_min; } og_pic_params;
+
+int or_pic_deposit_eps(const og_grid *g, const og_pic_params *pp, const og_parcels *pc, double *eps_g);
+double or_pic_drag_coef(const og_params *pr, const og_pic_params *pp, double eg, double slip, double omega);
+int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, const og_parcels *pc,
+                const double *eps_g, const double *u, const double *v, const double *w,
+                double *beta, double *sbu, double *sbv, double *sbw, double *diag, double *sabs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -183,3 +183,49 @@ def config_case(config_id: int, n_scalars: int = 0):
 
 def random_vector(n: int, seed: int, scale: float = 1.0):
     return np.random.default_rng(seed).uniform(-scale, scale, n)
+
+
+@dataclasses.dataclass
+class PicParams:
+    """Parcel properties (d_p = 200 um, rho_p = 2000 kg/m3) and the
+    gas-fraction floor of the deposit."""
+    d_p: float = 200e-6
+    rho_p: float = 2000.0
+    eps_min: float = 0.35
+
+
+# parcels in the paper's bed (PAPER.md:155 "total number of parcels present in
+# the domain was 2,983,447"); used for the configuration 2 grid
+PAPER_PARCELS = 2_983_447
+
+PARCEL_KEYS = ("x", "y", "z", "u", "v", "w", "omega")
+
+
+def make_parcels(grid: Grid, seed: int, n_parcels: int, eps=None, pic: PicParams | None = None):
+    """Seeded parcels (SoA dict of float64 arrays, DESIGN.md §6 recipe): cells
+    drawn with probability proportional to the snapshot's solid fraction
+    (1 - eps), positions uniform inside the cell, velocities N(0, 0.05) m/s, one
+    statistical weight omega for all parcels such that the parcels carry the
+    snapshot's total solid volume.  Sorted by nothing: parcel order is random."""
+    pic = pic or PicParams()
+    rng = np.random.default_rng(seed)
+    n = grid.n
+    if eps is None:
+        eps = make_state(grid, seed)["eps"]
+    solid = np.clip(1.0 - np.asarray(eps, dtype=np.float64), 0.0, None)
+    if solid.sum() <= 0.0:
+        solid = np.ones(n)
+    prob = solid / solid.sum()
+    cell = rng.choice(n, size=n_parcels, p=prob)
+    i = cell % grid.nx
+    j = (cell // grid.nx) % grid.ny
+    k = cell // (grid.nx * grid.ny)
+    x = (i + rng.uniform(0.0, 1.0, n_parcels)) * grid.dx
+    y = (j + rng.uniform(0.0, 1.0, n_parcels)) * grid.dy
+    z = (k + rng.uniform(0.0, 1.0, n_parcels)) * grid.dz
+    vs = np.pi / 6.0 * pic.d_p ** 3
+    total_solid = solid.sum() * grid.dx * grid.dy * grid.dz
+    omega = np.full(n_parcels, total_solid / (n_parcels * vs))
+    vel = rng.normal(0.0, 0.05, (3, n_parcels))
+    out = dict(x=x, y=y, z=z, u=vel[0], v=vel[1], w=vel[2], omega=omega)
+    return {k: np.ascontiguousarray(out[k], dtype=np.float64) for k in PARCEL_KEYS}

@@ -234,7 +234,44 @@ def measure_other_configs(mfx, torch):
         del sd
         torch.cuda.empty_cache()
     out["c5_one_gpu"] = measure_scalars_one_gpu(mfx, torch)
+    out["pic_coupling"] = measure_pic(mfx, torch)
     return out
+
+
+def measure_pic(mfx, torch):
+    """NEXT-2: the PIC device's coupling deposits on the
+    configuration 2 grid with the paper's parcel count, parcels
+    in random order and sorted by cell.  Per launch pair: the eps deposit
+    (zero fill + k_pic_eps + finalize) and the drag deposit (4 zero fills +
+    k_pic_drag).  Unique HBM bytes: parcels 32 / 56 B, fields 16N (eps: zero +
+    finalize read/write ~ 24N) / 4 x 8N written + 4 x 8N gathered."""
+    import numpy as np
+    import synth
+    g, pr, st = synth.config_case(CONFIG_ID)
+    pic = synth.PicParams()
+    pc = synth.make_parcels(g, 15605 + 77, synth.PAPER_PARCELS, st["eps"], pic)
+    cell = (np.minimum((pc["x"] / g.dx).astype(np.int64), g.nx - 1) + g.nx *
+            (np.minimum((pc["y"] / g.dy).astype(np.int64), g.ny - 1) + g.ny *
+             np.minimum((pc["z"] / g.dz).astype(np.int64), g.nz - 1)))
+    order = np.argsort(cell, kind="stable")
+    ws = mfx.Workspace(g)
+    u, v, w = (torch.from_numpy(st[k]).cuda() for k in ("u", "v", "w"))
+    eps = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    outs = {k: torch.empty(g.n, dtype=torch.float64, device="cuda") for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")}
+    res = {"workload": f"{synth.PAPER_PARCELS} parcels (PAPER.md:155) on 128x128x512", "parcels": synth.PAPER_PARCELS}
+    m = synth.PAPER_PARCELS
+    for name, idx in (("random_order", None), ("cell_sorted", order)):
+        d = {k: torch.from_numpy(np.ascontiguousarray(a if idx is None else a[idx])).cuda() for k, a in pc.items()}
+        t_eps, _ = _ev_ms(torch, lambda: mfx.pic_deposit_eps(g, pic, d, ws, eps=eps), 7)
+        t_drag, _ = _ev_ms(torch, lambda: mfx.pic_drag(g, pr, pic, d, eps, u, v, w, ws, out=outs), 7)
+        ws.check()
+        res[name] = {"eps_deposit_us": 1e3 * t_eps, "drag_deposit_us": 1e3 * t_drag,
+                     "parcels_per_s_drag": m / (t_drag * 1e-3),
+                     "atomic_updates_per_s_drag": 32 * m / (t_drag * 1e-3),
+                     "drag_unique_GBps": (56 * m + 8 * 8 * g.n) / (t_drag * 1e-3) / 1e9}
+        del d
+    torch.cuda.empty_cache()
+    return res
 
 
 def _ev_ms(torch, fn, reps):

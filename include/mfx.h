@@ -150,6 +150,42 @@ mfx_status mfx_correct(const mfx_grid *grid, const mfx_params *params, const dou
                        const double *pp, const double *p, double *u, double *v, double *w,
                        double *p_new, void *stream);
 
+/* ---------------------------------------------------------------- particle -> grid coupling (NEXT-2) */
+/* The PIC device's coupling terms: "F is the
+ * interpolated force from the parcel location to the corresponding fluid
+ * cell"; PAPER.md:97 explicit (once per time step) or implicit (head of every
+ * SIMPLE iteration) refresh; PAPER.md:131 interpolation of eps_p; closure of
+ * SPEC.md:285-289 (Syamlal-O'Brien).
+ * Parcels: caller-owned DEVICE arrays of n doubles each (structure of arrays):
+ * position x, y, z (m, inside [0, nx dx] x [0, ny dy] x [0, nz dz]), velocity
+ * u, v, w (m/s), statistical weight omega (real particles per parcel, >= 0).
+ * A parcel outside the domain, or with a negative/NaN weight, is skipped and
+ * latched in `ws` (mfx_ws_check then returns MFX_ERR_ARG with its index). */
+typedef struct { const double *x, *y, *z, *u, *v, *w, *omega; long long n; } mfx_parcels;
+typedef struct {
+    double d_p;        /* particle diameter (m) */
+    double eps_min;    /* floor of the deposited gas fraction */
+} mfx_pic_params;
+
+/* eps_g[c] = max(1 - sum_p W_pc (omega_p Vs) / V, eps_min), Vs = pi d_p^3 / 6,
+ * W_pc = trilinear weight of cell centre c (nodes clamped into the grid).
+ * eps_g (device, N) is overwritten.  Sums in arrival order (fp64 atomics):
+ * equal to the parcel-ordered definition within (m - 1) u sum|terms| per cell. */
+mfx_status mfx_pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pic, const mfx_parcels *parcels,
+                               double *eps_g, void *ws, size_t ws_bytes, void *stream);
+
+/* Per parcel p: eps_g and the staggered u, v, w interpolated to the parcel
+ * (trilinear; the unstored boundary face carries 0 at walls and w_in at the
+ * inlet), slip = |u_g - u_p|, K_p = Syamlal-O'Brien beta_d omega_p Vs / eps_s
+ * (N s/m); then beta[c] = sum_p W_pc (K_p / V) and
+ * sbeta_a[c] = sum_p W_pc ((K_p u_p,a) / V): the cell-centred implicit drag
+ * coefficient and explicit source of mfx_state (reading Q11).  Outputs
+ * (device, N each) are overwritten; K (device, n, may be NULL) receives K_p. */
+mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,
+                        const mfx_parcels *parcels, const double *eps_g, const double *u, const double *v,
+                        const double *w, double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w,
+                        double *K, void *ws, size_t ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------- equation decomposition */
 /* Assignment string: three 1-based GPU ids for U, V, W,
  * a bracketed P list, then optional scalar owners, e.g. "111[1]", "234[1]",
@@ -247,7 +283,8 @@ mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
 /* Kernel timing with CUDA events recorded on the launching stream around
  * every hot kernel launch (off by default).  ids: 0 spmv/setup, 1 K1 (momentum/
  * scalar), 2 K2 (momentum/scalar), 3 K3, 4 momentum assembly, 5 correct, 6 K1 (p'), 7 K2 (p'),
- * 8 p' assembly, 9 scalar assembly (the single-cluster solve is timed under id 0).  mfx_prof_read synchronises the device and
+ * 8 p' assembly, 9 scalar assembly, 10 PIC eps deposit, 11 PIC drag deposit (the single-cluster
+ * solve is timed under id 0).  mfx_prof_read synchronises the device and
  * returns, per id, launches and total milliseconds since mfx_prof_reset. */
 void mfx_prof_enable(int on);
 void mfx_prof_reset(void);

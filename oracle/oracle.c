@@ -837,9 +837,11 @@ double or_pic_drag_coef(const og_params *pr, const og_pic_params *pp, double eg,
 }
 
 /* D2: per parcel interpolate eps_g (cell lattice) and u_g (staggered
- * lattices), slip, K; deposit beta = sum W K / V and sbeta_c = sum W (K u_p,c) / V.
+ * lattices), slip, K; deposit beta = sum_p W (K / V) and
+ * sbeta_c = sum_p W ((K u_p,c) / V) (the division is per parcel, so the sums
+ * are the fields: no pass over the grid after the deposit).
  * diag (optional, may be NULL): per parcel {eps_g@p, u_g@p, v_g@p, w_g@p, K}.
- * sabs (optional, may be NULL): 3 x N, sum W |K u_p,c| / V (error scale of sbeta). */
+ * sabs (optional, may be NULL): 3 x N, sum W |(K u_p,c) / V| (error scale of sbeta). */
 int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, const og_parcels *pc,
                 const double *eps_g, const double *u, const double *v, const double *w,
                 double *beta, double *sbu, double *sbv, double *sbw, double *diag, double *sabs)
@@ -866,6 +868,9 @@ int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, 
             diag[5 * p + 0] = eg; diag[5 * p + 1] = ug[0]; diag[5 * p + 2] = ug[1]; diag[5 * p + 3] = ug[2];
             diag[5 * p + 4] = K;
         }
+        const double KV = K / V;
+        double KuV[3];
+        for (int c = 0; c < 3; c++) KuV[c] = (K * up[c]) / V;
         int nd[3][2];
         double wt[3][2];
         pic_stencil(g, X, -1, nd, wt);
@@ -875,17 +880,12 @@ int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, 
                     const int q[3] = {nd[0][ii], nd[1][jj], nd[2][kk]};
                     const double W = (wt[0][ii] * wt[1][jj]) * wt[2][kk];
                     const long n = at(g, q);
-                    beta[n] += W * K;
+                    beta[n] += W * KV;
                     for (int c = 0; c < 3; c++) {
-                        sb[c][n] += W * (K * up[c]);
-                        if (sabs) sabs[c * N + n] += W * fabs(K * up[c]);
+                        sb[c][n] += W * KuV[c];
+                        if (sabs) sabs[c * N + n] += W * fabs(KuV[c]);
                     }
                 }
-    }
-    for (long n = 0; n < N; n++) {
-        beta[n] = beta[n] / V;
-        for (int c = 0; c < 3; c++) sb[c][n] = sb[c][n] / V;
-        if (sabs) for (int c = 0; c < 3; c++) sabs[c * N + n] = sabs[c * N + n] / V;
     }
     return OG_OK;
 }

@@ -83,6 +83,16 @@ class Xfer(C.Structure):
                 ("k0", C.c_int), ("k1", C.c_int)]
 
 
+class Parcels(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("x", "y", "z", "u", "v", "w", "omega")] + [("n", C.c_longlong)]
+
+
+class PicParams(C.Structure):
+    _fields_ = [("d_p", C.c_double), ("eps_min", C.c_double)]
+
+
+PARCEL_KEYS = ("x", "y", "z", "u", "v", "w", "omega")
+
 _V = C.c_void_p
 _sigs = {
     "mfx_last_error": (C.c_char_p, []),
@@ -92,6 +102,10 @@ _sigs = {
     "mfx_ws_check": (C.c_int, [_V, C.c_size_t, _V]),
     "mfx_assemble_eq": (C.c_int, [C.c_int, C.c_int, C.POINTER(Grid), C.POINTER(Params), C.POINTER(State),
                                   C.POINTER(_V), C.POINTER(Eqsys), _V, _V, C.c_size_t, _V]),
+    "mfx_pic_deposit_eps": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), _V, _V,
+                                      C.c_size_t, _V]),
+    "mfx_pic_drag": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(PicParams), C.POINTER(Parcels)] +
+                     [_V] * 9 + [_V, C.c_size_t, _V]),
     "mfx_spmv": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, _V, _V]),
     "mfx_bicgstab_solve": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
                                      _V, C.c_size_t, C.POINTER(SolveInfo), _V]),
@@ -247,6 +261,45 @@ def bicgstab_solve(kind, grid, sysd: dict, x, tol: float, maxit: int, ws: Worksp
     if not sync:
         return None
     return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid)
+
+
+def c_parcels(parcels: dict) -> Parcels:
+    n = parcels["x"].numel()
+    for k in PARCEL_KEYS:
+        t = parcels[k]
+        assert t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous() and t.numel() == n, k
+    return Parcels(*[_ptr(parcels[k], n) for k in PARCEL_KEYS], n)
+
+
+def pic_deposit_eps(grid, pic, parcels: dict, ws: Workspace, eps=None, stream=None):
+    """NEXT-2: gas volume fraction from the parcels' solid volume.
+    pic: object with d_p, eps_min.  Returns eps_g (device, N)."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    eps = eps if eps is not None else torch.empty(n, dtype=torch.float64, device=parcels["x"].device)
+    _check(_lib.mfx_pic_deposit_eps(C.byref(c_grid(grid)), C.byref(PicParams(pic.d_p, pic.eps_min)),
+                                    C.byref(c_parcels(parcels)), _ptr(eps, n), C.c_void_p(ws.ptr), ws.nbytes,
+                                    _stream(stream)), "mfx_pic_deposit_eps")
+    return eps
+
+
+def pic_drag(grid, params, pic, parcels: dict, eps, u, v, w, ws: Workspace, out=None, K=None, stream=None):
+    """NEXT-2: Syamlal-O'Brien drag of every parcel deposited to the
+    cell-centred beta and beta*u_s (the mfx_state drag inputs).  Returns dict
+    beta, sbeta_u, sbeta_v, sbeta_w (device, N); K (per parcel) if given."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    dev = eps.device
+    out = out if out is not None else {k: torch.empty(n, dtype=torch.float64, device=dev)
+                                       for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")}
+    m = parcels["x"].numel()
+    _check(_lib.mfx_pic_drag(C.byref(c_grid(grid)), C.byref(c_params(params)),
+                             C.byref(PicParams(pic.d_p, pic.eps_min)), C.byref(c_parcels(parcels)),
+                             _ptr(eps, n), _ptr(u, n), _ptr(v, n), _ptr(w, n),
+                             *[_ptr(out[k], n) for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")],
+                             _ptr(K, m) if K is not None else None, C.c_void_p(ws.ptr), ws.nbytes,
+                             _stream(stream)), "mfx_pic_drag")
+    return out
 
 
 def correct(grid, params, star, pp, p, out=None, stream=None):

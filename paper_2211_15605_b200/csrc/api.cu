@@ -160,7 +160,7 @@ using namespace mfx;
 #define API extern "C" __attribute__((visibility("default")))
 
 API const char *mfx_last_error(void) { return g_err; }
-API const char *mfx_version(void) { return "mfx 0.1 (sm_100a, fp64, v1 kernels)"; }
+API const char *mfx_version(void) { return "mfx 0.2 (sm_100a, fp64; TMA z-marching BiCGSTAB, cluster solver, PIC coupling)"; }
 
 API size_t mfx_workspace_bytes(const mfx_grid *grid, int kind)
 {
@@ -176,6 +176,7 @@ API mfx_status mfx_ws_init(void *ws, size_t ws_bytes, void *stream)
     MFX_CUDA_TRY(cudaMemsetAsync(ws, 0, ws_header_bytes(), s));
     WsHeader *h = (WsHeader *)ws;
     MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_nonfinite, 0xff, 16, s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_parcel, 0xff, 8, s));
     return MFX_OK;
 }
 
@@ -183,11 +184,17 @@ API mfx_status mfx_ws_check(void *ws, size_t ws_bytes, void *stream)
 {
     MFX_ARG_CHECK(ws && ws_bytes >= ws_header_bytes(), "bad workspace");
     cudaStream_t s = (cudaStream_t)stream;
-    unsigned long long bad[2];
+    unsigned long long bad[2], badp;
     WsHeader *h = (WsHeader *)ws;
     MFX_CUDA_TRY(cudaMemcpyAsync(bad, &h->bad_nonfinite, 16, cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(&badp, &h->bad_parcel, 8, cudaMemcpyDeviceToHost, s));
     MFX_CUDA_TRY(cudaStreamSynchronize(s));
     MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_nonfinite, 0xff, 16, s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&h->bad_parcel, 0xff, 8, s));
+    if (badp != ~0ull) {
+        set_error("parcel %llu outside the domain (or negative / NaN weight)", badp);
+        return MFX_ERR_ARG;
+    }
     if (bad[0] != ~0ull) {
         set_error("non-finite coefficient at cell %llu", bad[0]);
         return MFX_ERR_NONFINITE;
@@ -204,6 +211,21 @@ API mfx_status mfx_assemble_eq(int kind, int scalar_id, const mfx_grid *grid, co
                                void *ws, size_t ws_bytes, void *stream)
 {
     return assemble_eq(kind, scalar_id, grid, params, state, star, out, resid2, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pic, const mfx_parcels *parcels,
+                                   double *eps_g, void *ws, size_t ws_bytes, void *stream)
+{
+    return pic_deposit_eps(grid, pic, parcels, eps_g, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,
+                            const mfx_parcels *parcels, const double *eps_g, const double *u, const double *v,
+                            const double *w, double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w,
+                            double *K, void *ws, size_t ws_bytes, void *stream)
+{
+    return pic_drag(grid, params, pic, parcels, eps_g, u, v, w, beta, sbeta_u, sbeta_v, sbeta_w, K, ws, ws_bytes,
+                    (cudaStream_t)stream);
 }
 
 API mfx_status mfx_spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, void *stream)

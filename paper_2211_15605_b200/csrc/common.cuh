@@ -225,7 +225,8 @@ struct WsHeader {
     unsigned long long bad_zerodiag;
     unsigned int ticket[4];
     double resid[4];
-    double pad[6];
+    unsigned long long bad_parcel;      // first parcel outside the domain (ULLONG_MAX = none)
+    double pad[5];
 };
 
 constexpr int kMaxBlocks = 2048;
@@ -251,6 +252,11 @@ bool cluster_fits(const Geo &G, bool sym);
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s);
 long long launch_count_get();
+mfx_status pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *pc, double *eps,
+                           void *ws, size_t wsb, cudaStream_t s);
+mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp, const mfx_parcels *pc,
+                    const double *eps, const double *u, const double *v, const double *w, double *beta,
+                    double *sbu, double *sbv, double *sbw, double *Kout, void *ws, size_t wsb, cudaStream_t s);
 void launch_count_set(long long v);
 void launch_count_add(long long v);
 int reduce_grid(long long N);

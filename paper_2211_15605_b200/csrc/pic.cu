@@ -1,0 +1,313 @@
+// pic.cu -- particle -> grid coupling on the PIC device (NEXT-2; DESIGN.md
+// §3.9; "F is the interpolated force from the parcel location to
+// the corresponding fluid cell", PAPER.md:97 explicit vs implicit refresh at
+// the head of every SIMPLE iteration, PAPER.md:131 interpolation of eps_p).
+//
+// Two deposits produce the hot path's inputs:
+//   k_pic_eps   parcel solid volume -> cell accumulators (trilinear weights),
+//               then k_pic_eps_final: eps_g = max(1 - acc / V, eps_min);
+//   k_pic_drag  per parcel: trilinear eps_g and staggered-lattice u_g at the
+//               parcel, slip, Syamlal-O'Brien K; deposit W (K / V) into beta
+//               and W ((K u_p) / V) into beta*u_s (no pass over the grid after).
+//
+// One thread per parcel, grid-stride over a fixed grid; the 8 node updates go
+// to global memory as fp64 reductions (RED.ADD.F64, resolved in L2).  The
+// fields the parcels touch (the bed) sit in L2 after the first parcels, so
+// the gathers and the reductions are L2 traffic; HBM sees the parcel stream
+// (56 B / parcel), the output fields and the zero fill.  Summation order
+// inside a cell is the order the reductions arrive in: parity with the oracle
+// (parcel-ascending order) is to the tolerance DESIGN.md §3.9 derives, not
+// bitwise; per-parcel values (weights, interpolants) use the oracle's exact
+// expression order and differ only through pow() (CUDA's vs libm's ulps).
+#include <climits>
+
+#include "common.cuh"
+
+namespace mfx {
+
+namespace {
+
+constexpr int kPicThreads = 256;
+constexpr double kPi = 3.14159265358979323846;
+
+struct PicGeo {
+    int n[3];
+    double h[3], L[3];
+    double V, Vs, eps_min;
+    int bc_zlo;
+    double w_in;
+    long long N;
+};
+
+__device__ __forceinline__ void pic_axis(double x, double h, int n, bool face, int nd[2], double w[2])
+{
+    const double xi = face ? x / h - 1.0 : x / h - 0.5;
+    const double fl = floor(xi);
+    const double f = xi - fl;
+    int i0 = (int)fl, i1 = i0 + 1;
+    const int lo = face ? -1 : 0;
+    i0 = i0 < lo ? lo : (i0 > n - 1 ? n - 1 : i0);
+    i1 = i1 < lo ? lo : (i1 > n - 1 ? n - 1 : i1);
+    nd[0] = i0; nd[1] = i1;
+    w[0] = 1.0 - f; w[1] = f;
+}
+
+__device__ __forceinline__ long long pic_lin(const PicGeo &G, int i, int j, int k)
+{
+    return (long long)i + (long long)G.n[0] * ((long long)j + (long long)G.n[1] * k);
+}
+
+__device__ __forceinline__ bool parcel_ok(const PicGeo &G, double x, double y, double z, double om)
+{
+    return x >= 0.0 && x <= G.L[0] && y >= 0.0 && y <= G.L[1] && z >= 0.0 && z <= G.L[2] && om >= 0.0;
+}
+
+// trilinear value of field f on the lattice whose face axis is FA (-1: cell centres)
+template <int FA>
+__device__ __forceinline__ double pic_interp(const PicGeo &G, const double *__restrict__ f, const double X[3])
+{
+    int nd[3][2];
+    double w[3][2];
+#pragma unroll
+    for (int a = 0; a < 3; a++) pic_axis(X[a], G.h[a], G.n[a], a == FA, nd[a], w[a]);
+    double v8[8];
+#pragma unroll
+    for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+        for (int jj = 0; jj < 2; jj++)
+#pragma unroll
+            for (int ii = 0; ii < 2; ii++) {
+                int q[3] = {nd[0][ii], nd[1][jj], nd[2][kk]};
+                double v;
+                if (FA >= 0 && q[FA] == -1) {
+                    v = (FA == 2 && G.bc_zlo == MFX_BC_INLET) ? G.w_in : 0.0;
+                } else {
+                    v = __ldg(f + pic_lin(G, q[0], q[1], q[2]));
+                }
+                v8[(kk * 2 + jj) * 2 + ii] = v;
+            }
+    double val = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+        for (int jj = 0; jj < 2; jj++)
+#pragma unroll
+            for (int ii = 0; ii < 2; ii++) {
+                const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+                val = val + W * v8[(kk * 2 + jj) * 2 + ii];
+            }
+    return val;
+}
+
+struct PicEpsArgs {
+    PicGeo G;
+    const double *x, *y, *z, *om;
+    long long m;
+    double *acc;
+    WsHeader *hdr;
+};
+
+__global__ void __launch_bounds__(kPicThreads) k_pic_eps(PicEpsArgs a)
+{
+    const PicGeo &G = a.G;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
+        const double om = __ldg(a.om + p);
+        if (!parcel_ok(G, X[0], X[1], X[2], om)) {
+            atomicMin(&a.hdr->bad_parcel, (unsigned long long)p);
+            continue;
+        }
+        const double vol = om * G.Vs;
+        int nd[3][2];
+        double w[3][2];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) pic_axis(X[ax], G.h[ax], G.n[ax], false, nd[ax], w[ax]);
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++)
+#pragma unroll
+                for (int ii = 0; ii < 2; ii++) {
+                    const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+                    atomicAdd(a.acc + pic_lin(G, nd[0][ii], nd[1][jj], nd[2][kk]), W * vol);
+                }
+    }
+}
+
+__global__ void __launch_bounds__(kPicThreads) k_pic_eps_final(double *eps, long long N, double V, double eps_min)
+{
+    const long long n2 = N / 2;
+    double2 *e2 = reinterpret_cast<double2 *>(eps);
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n2;
+         q += (long long)gridDim.x * blockDim.x) {
+        double2 a = e2[q];
+        double e0 = 1.0 - a.x / V, e1 = 1.0 - a.y / V;
+        a.x = e0 < eps_min ? eps_min : e0;
+        a.y = e1 < eps_min ? eps_min : e1;
+        e2[q] = a;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (N & 1)) {
+        const double e = 1.0 - eps[N - 1] / V;
+        eps[N - 1] = e < eps_min ? eps_min : e;
+    }
+}
+
+struct PicDragArgs {
+    PicGeo G;
+    double rho, mu, dp;
+    const double *x, *y, *z, *up, *vp, *wp, *om;
+    long long m;
+    const double *eps, *u, *v, *w;
+    double *beta, *sb[3], *Kout;
+    WsHeader *hdr;
+};
+
+// DESIGN.md §3.9 (SPEC.md:285-289 closure, written without the eps_s that cancels)
+__device__ __forceinline__ double drag_coef(double rho, double mu, double dp, double Vs, double eg, double slip,
+                                            double om)
+{
+    double Re = ((rho * dp) * slip) / mu;
+    Re = Re < 1e-12 ? 1e-12 : Re;
+    const double A = pow(eg, 4.14);
+    const double B = eg <= 0.85 ? 0.8 * pow(eg, 1.28) : pow(eg, 2.65);
+    const double q = 0.06 * Re;
+    const double Vr = 0.5 * ((A - q) + sqrt((q * q + (0.12 * Re) * (2.0 * B - A)) + A * A));
+    double Cd = 0.63 + 4.8 / sqrt(Re / Vr);
+    Cd = Cd * Cd;
+    return (om * Vs) * ((((0.75 * Cd) * eg) * rho) * slip) / ((Vr * Vr) * dp);
+}
+
+__global__ void __launch_bounds__(kPicThreads) k_pic_drag(PicDragArgs a)
+{
+    const PicGeo &G = a.G;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
+        const double om = __ldg(a.om + p);
+        const double up[3] = {__ldg(a.up + p), __ldg(a.vp + p), __ldg(a.wp + p)};
+        if (!parcel_ok(G, X[0], X[1], X[2], om)) {
+            atomicMin(&a.hdr->bad_parcel, (unsigned long long)p);
+            continue;
+        }
+        const double eg = pic_interp<-1>(G, a.eps, X);
+        const double ug0 = pic_interp<0>(G, a.u, X);
+        const double ug1 = pic_interp<1>(G, a.v, X);
+        const double ug2 = pic_interp<2>(G, a.w, X);
+        const double sx = ug0 - up[0], sy = ug1 - up[1], sz = ug2 - up[2];
+        const double slip = sqrt((sx * sx + sy * sy) + sz * sz);
+        const double K = drag_coef(a.rho, a.mu, a.dp, G.Vs, eg, slip, om);
+        if (a.Kout) a.Kout[p] = K;
+        const double KV = K / G.V;
+        double KuV[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) KuV[c] = (K * up[c]) / G.V;
+        int nd[3][2];
+        double w[3][2];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) pic_axis(X[ax], G.h[ax], G.n[ax], false, nd[ax], w[ax]);
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++)
+#pragma unroll
+                for (int ii = 0; ii < 2; ii++) {
+                    const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+                    const long long n = pic_lin(G, nd[0][ii], nd[1][jj], nd[2][kk]);
+                    atomicAdd(a.beta + n, W * KV);
+#pragma unroll
+                    for (int c = 0; c < 3; c++) atomicAdd(a.sb[c] + n, W * KuV[c]);
+                }
+    }
+}
+
+bool pic_geo(const mfx_grid *g, const mfx_pic_params *pp, PicGeo &G)
+{
+    if (!g || !pp) { set_error("NULL grid / pic params"); return false; }
+    if (g->nx < 2 || g->ny < 2 || g->nz < 2) { set_error("grid extents must be >= 2"); return false; }
+    if (!(g->dx > 0 && g->dy > 0 && g->dz > 0)) { set_error("spacing must be positive"); return false; }
+    if (!(pp->d_p > 0.0)) { set_error("d_p must be positive"); return false; }
+    G.n[0] = g->nx; G.n[1] = g->ny; G.n[2] = g->nz;
+    G.h[0] = g->dx; G.h[1] = g->dy; G.h[2] = g->dz;
+    G.L[0] = g->nx * g->dx; G.L[1] = g->ny * g->dy; G.L[2] = g->nz * g->dz;
+    G.V = (g->dx * g->dy) * g->dz;
+    G.Vs = (((kPi / 6.0) * pp->d_p) * pp->d_p) * pp->d_p;
+    G.eps_min = pp->eps_min;
+    G.bc_zlo = g->bc_zlo;
+    G.w_in = g->w_in;
+    G.N = (long long)g->nx * g->ny * g->nz;
+    return true;
+}
+
+int pic_grid(long long m)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long need = (m + kPicThreads - 1) / kPicThreads;
+    const long long cap = (long long)sms * 8;
+    return (int)(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
+}  // namespace
+
+mfx_status pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *pc, double *eps,
+                           void *ws, size_t wsb, cudaStream_t s)
+{
+    PicGeo G;
+    if (!pic_geo(grid, pp, G)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(pc && eps, "NULL parcels / eps");
+    MFX_ARG_CHECK(pc->n >= 0, "negative parcel count");
+    MFX_ARG_CHECK(pc->n == 0 || (pc->x && pc->y && pc->z && pc->omega), "NULL parcel array");
+    MFX_ARG_CHECK(ws && wsb >= ws_header_bytes(), "bad workspace");
+    MFX_CUDA_TRY(cudaMemsetAsync(eps, 0, sizeof(double) * G.N, s));
+    if (pc->n > 0) {
+        PicEpsArgs a;
+        a.G = G;
+        a.x = pc->x; a.y = pc->y; a.z = pc->z; a.om = pc->omega;
+        a.m = pc->n;
+        a.acc = eps;
+        a.hdr = (WsHeader *)ws;
+        count_launch(10, s, true);
+        k_pic_eps<<<pic_grid(pc->n), kPicThreads, 0, s>>>(a);
+        count_launch(10, s, false);
+        MFX_CUDA_TRY(cudaGetLastError());
+    }
+    k_pic_eps_final<<<reduce_grid(G.N / 2 + 1), kPicThreads, 0, s>>>(eps, G.N, G.V, G.eps_min);
+    launch_count_add(1);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp, const mfx_parcels *pc,
+                    const double *eps, const double *u, const double *v, const double *w, double *beta,
+                    double *sbu, double *sbv, double *sbw, double *Kout, void *ws, size_t wsb, cudaStream_t s)
+{
+    PicGeo G;
+    if (!pic_geo(grid, pp, G)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(pr && pc, "NULL params / parcels");
+    MFX_ARG_CHECK(pr->mu > 0.0, "mu must be positive");
+    MFX_ARG_CHECK(eps && u && v && w && beta && sbu && sbv && sbw, "NULL field");
+    MFX_ARG_CHECK(pc->n >= 0, "negative parcel count");
+    MFX_ARG_CHECK(pc->n == 0 || (pc->x && pc->y && pc->z && pc->u && pc->v && pc->w && pc->omega),
+                  "NULL parcel array");
+    MFX_ARG_CHECK(ws && wsb >= ws_header_bytes(), "bad workspace");
+    double *outs[4] = {beta, sbu, sbv, sbw};
+    for (int q = 0; q < 4; q++) MFX_CUDA_TRY(cudaMemsetAsync(outs[q], 0, sizeof(double) * G.N, s));
+    if (pc->n == 0) return MFX_OK;
+    PicDragArgs a;
+    a.G = G;
+    a.rho = pr->rho; a.mu = pr->mu; a.dp = pp->d_p;
+    a.x = pc->x; a.y = pc->y; a.z = pc->z; a.up = pc->u; a.vp = pc->v; a.wp = pc->w; a.om = pc->omega;
+    a.m = pc->n;
+    a.eps = eps; a.u = u; a.v = v; a.w = w;
+    a.beta = beta; a.sb[0] = sbu; a.sb[1] = sbv; a.sb[2] = sbw; a.Kout = Kout;
+    a.hdr = (WsHeader *)ws;
+    count_launch(11, s, true);
+    k_pic_drag<<<pic_grid(pc->n), kPicThreads, 0, s>>>(a);
+    count_launch(11, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+}  // namespace mfx

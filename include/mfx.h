@@ -207,12 +207,14 @@ mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *ou
  * GATHER (momentum owners -> p' owner(s): u*, d per component, plus a
  * 16-double residual record), phase 1 = BCAST (p' owner -> all: u, v, w, p,
  * residual record; scalar owners -> all: phi), phase 2 = PSLAB (multi-GPU p':
- * every rank's slab of p' -> P0; k0/k1 give the plane range).  Ops are
- * returned in the order they are issued inside one NCCL group. */
+ * every rank's slab of p' -> P0; k0/k1 give the plane range), phase 3 = PIC
+ * (the PIC device, rank 0 = "GPU 1" of P:95, broadcasts the refreshed drag
+ * fields beta, sbeta_u, sbeta_v, sbeta_w).  Ops are returned in the order they
+ * are issued inside one NCCL group. */
 enum { MFX_OP_SEND = 0, MFX_OP_RECV = 1, MFX_OP_BCAST = 2 };
 enum { MFX_BUF_U = 0, MFX_BUF_V, MFX_BUF_W, MFX_BUF_DX, MFX_BUF_DY, MFX_BUF_DZ,
        MFX_BUF_P, MFX_BUF_PHI0, MFX_BUF_PHI1, MFX_BUF_PHI2, MFX_BUF_PHI3,
-       MFX_BUF_META, MFX_BUF_PP, MFX_NBUF };
+       MFX_BUF_META, MFX_BUF_PP, MFX_BUF_BETA, MFX_BUF_SBU, MFX_BUF_SBV, MFX_BUF_SBW, MFX_NBUF };
 /* buf MFX_BUF_META moves nslots 16-double residual records starting at slot;
  * other buffers move planes [k0, k1) (k1 = 0: the whole field of N doubles).
  * peer = root for BCAST. */
@@ -269,14 +271,28 @@ void mfx_dist_slab(int nz, int rank, int nranks, int *k0, int *k1);
  * Synchronises `stream` once at the end (residual record to host). */
 mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void *stream);
 
+/* Particle -> fluid coupling inside the SIMPLE loop (NEXT-2).
+ * mode MFX_PIC_IMPLICIT: the drag fields of mfx_state (beta, sbeta_*) are
+ * recomputed by mfx_pic_drag from the current snapshot (eps, u, v, w) at the
+ * head of every mfx_simple_iter; MFX_PIC_EXPLICIT: only at the next
+ * mfx_simple_iter (call again at the start of each time step: "calculated
+ * before the first SIMPLE iteration and not updated during subsequent SIMPLE
+ * iterations"); MFX_PIC_OFF: never.  The PIC device is rank 0 ("PICdev
+ * is always on GPU 1"): only rank 0 needs `parcels` (device arrays, kept by
+ * pointer until the next call; other ranks pass NULL) and, for nranks > 1, it
+ * broadcasts the four drag fields (exchange phase 3) before the momentum
+ * assembly. */
+enum { MFX_PIC_OFF = 0, MFX_PIC_EXPLICIT = 1, MFX_PIC_IMPLICIT = 2 };
+mfx_status mfx_ctx_set_pic(mfx_ctx *ctx, const mfx_parcels *parcels, const mfx_pic_params *pic, int mode);
+
 /* Device pointers to the context's internal buffers from the last
  * mfx_simple_iter (NULL where this rank does not hold them): which =
  * 0..2 u*, v*, w* (momentum predictors), 3..5 d_x, d_y, d_z, 6 p' solution. */
 double *mfx_ctx_buffer(mfx_ctx *ctx, int which);
 
 /* Per-phase device times of the last mfx_simple_iter on this rank (ms):
- * [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction,
- * [4] BCAST, [5] total. */
+ * [0] momentum+scalars (including a PIC drag refresh and its broadcast),
+ * [1] GATHER, [2] p' assemble+solve, [3] correction, [4] BCAST, [5] total. */
 mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
 
 /* ---------------------------------------------------------------- instrumentation */

@@ -25,7 +25,9 @@ EQ_U, EQ_V, EQ_W, EQ_PP, EQ_SCALAR = 0, 1, 2, 3, 4
 BC_WALL, BC_INLET, BC_OUTLET, BC_DIRICHLET_TEST = 0, 1, 2, 3
 OK, NOT_CONVERGED, ERR_ARG, ERR_NONFINITE, ERR_ZERO_DIAG, ERR_BREAKDOWN, ERR_CUDA, ERR_NCCL = 0, 1, -1, -2, -3, -4, -5, -6
 OP_SEND, OP_RECV, OP_BCAST = 0, 1, 2
-BUF_NAMES = ("u", "v", "w", "dx", "dy", "dz", "p", "phi0", "phi1", "phi2", "phi3", "meta", "pp")
+BUF_NAMES = ("u", "v", "w", "dx", "dy", "dz", "p", "phi0", "phi1", "phi2", "phi3", "meta", "pp",
+             "beta", "sbeta_u", "sbeta_v", "sbeta_w")
+PIC_OFF, PIC_EXPLICIT, PIC_IMPLICIT = 0, 1, 2
 NBUF = len(BUF_NAMES)
 
 
@@ -125,6 +127,7 @@ _sigs = {
     "mfx_simple_iter": (C.c_int, [_V, C.POINTER(State), C.POINTER(Resid), _V]),
     "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
     "mfx_ctx_buffer": (C.c_void_p, [_V, C.c_int]),
+    "mfx_ctx_set_pic": (C.c_int, [_V, C.POINTER(Parcels), C.POINTER(PicParams), C.c_int]),
     "mfx_dist_solve": (C.c_int, [_V, C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
                                  C.POINTER(SolveInfo), _V]),
     "mfx_dist_slab": (None, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -385,6 +388,16 @@ class SimpleContext:
         _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))   # NONFINITE/ZERO_DIAG raise
         return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
                     status=list(r.status), converged=bool(r.converged))
+
+    def set_pic(self, parcels: dict | None, pic=None, mode: int = PIC_IMPLICIT):
+        """Particle -> fluid coupling in the SIMPLE loop: PIC_IMPLICIT
+        refreshes the state's drag fields at the head of every step, PIC_EXPLICIT
+        at the next step only.  Rank 0 (the PIC device) passes the parcels (device
+        tensors, kept alive here); other ranks pass None."""
+        self._pic_keep = parcels
+        cp = C.byref(c_parcels(parcels)) if parcels is not None else None
+        pp = C.byref(PicParams(pic.d_p, pic.eps_min)) if pic is not None else None
+        _check(_lib.mfx_ctx_set_pic(self.ptr, cp, pp, mode), "mfx_ctx_set_pic")
 
     def buffer(self, which: str):
         """Copy of an internal buffer of the last step: 'u*','v*','w*','dx','dy','dz','pp'."""

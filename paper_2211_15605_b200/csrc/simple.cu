@@ -97,7 +97,7 @@ mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer 
 {
     MFX_ARG_CHECK(a && n_ops && (ops || max_ops == 0), "NULL argument");
     MFX_ARG_CHECK(phase != 2 || a->n_p == 1 || nz >= a->n_p, "PSLAB plan needs nz >= number of p' ranks");
-    MFX_ARG_CHECK(phase >= 0 && phase <= 2, "phase must be 0 (GATHER), 1 (BCAST) or 2 (PSLAB)");
+    MFX_ARG_CHECK(phase >= 0 && phase <= 3, "phase must be 0 (GATHER), 1 (BCAST), 2 (PSLAB) or 3 (PIC)");
     std::vector<mfx_xfer> v;
     const int P = a->owner[3];
     const bool multi_p = a->n_p > 1;   // every rank is a p' rank
@@ -128,6 +128,9 @@ mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer 
             v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_PHI0 + s, 0, 0, 0, 0});
             v.push_back({MFX_OP_BCAST, a->owner[4 + s], MFX_BUF_META, 4 + s, 1, 0, 0});
         }
+    } else if (phase == 3) {
+        // PIC: the PIC device (rank 0) broadcasts the refreshed drag fields
+        for (int b = MFX_BUF_BETA; b <= MFX_BUF_SBW; b++) v.push_back({MFX_OP_BCAST, 0, b, 0, 0, 0, 0});
     } else if (multi_p) {
         // PSLAB: the slabs of the domain-decomposed p' solution -> P0 (= rank 0)
         for (int q = 0; q < a->n_p; q++) {
@@ -281,6 +284,11 @@ struct mfx_ctx {
     size_t dist_bytes;
     cudaEvent_t ev[6];
     double phase_ms[6];
+    // particle -> fluid coupling: parcels live on the PIC device (rank 0)
+    int pic_mode, pic_pending;
+    mfx_parcels pic_pc;
+    mfx_pic_params pic_pp;
+    void *pic_ws;
 };
 
 namespace mfx {
@@ -563,6 +571,19 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     mfx_status rc;
     MFX_CUDA_TRY(cudaMemsetAsync(c->meta, 0, 8 * 16 * sizeof(double), s));
     MFX_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    // head of the SIMPLE iteration: particle -> fluid drag refresh
+    if (c->pic_mode == MFX_PIC_IMPLICIT || (c->pic_mode == MFX_PIC_EXPLICIT && c->pic_pending)) {
+        if (r == 0) {
+            rc = pic_drag(&c->grid, &pr, &c->pic_pp, &c->pic_pc, st->eps, st->u, st->v, st->w, st->beta,
+                          st->sbeta_u, st->sbeta_v, st->sbeta_w, nullptr, c->pic_ws, ws_header_bytes(), s);
+            if (rc != MFX_OK) return rc;
+        }
+        double *D[MFX_NBUF] = {0};
+        D[MFX_BUF_BETA] = st->beta; D[MFX_BUF_SBU] = st->sbeta_u;
+        D[MFX_BUF_SBV] = st->sbeta_v; D[MFX_BUF_SBW] = st->sbeta_w;
+        if ((rc = exchange_state(c, 3, D, s)) != MFX_OK) return rc;
+        c->pic_pending = 0;
+    }
     // momentum predictors (snapshot) on their owners
     for (int q = 0; q < 3; q++) {
         if (a.owner[q] != r) continue;
@@ -683,6 +704,17 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
             worst = bad[0] != ~0ull ? MFX_ERR_NONFINITE : MFX_ERR_ZERO_DIAG;
         }
     }
+    if (c->pic_ws) {
+        unsigned long long badp;
+        const WsHeader *h = (const WsHeader *)c->pic_ws;
+        MFX_CUDA_TRY(cudaMemcpy(&badp, &h->bad_parcel, 8, cudaMemcpyDeviceToHost));
+        if (badp != ~0ull) {
+            const unsigned long long none = ~0ull;
+            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_parcel, &none, 8, cudaMemcpyHostToDevice));
+            set_error("PIC drag refresh: parcel %llu outside the domain (or negative / NaN weight)", badp);
+            worst = MFX_ERR_ARG;
+        }
+    }
     double mx = out->R_u;
     if (out->R_v > mx) mx = out->R_v;
     if (out->R_w > mx) mx = out->R_w;
@@ -753,6 +785,29 @@ mfx_status mfx_dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mf
 }
 
 void mfx_dist_slab(int nz, int rank, int nranks, int *k0, int *k1) { mfx::dist_slab(nz, rank, nranks, k0, k1); }
+
+mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic_params *pic, int mode)
+{
+    MFX_ARG_CHECK(c, "NULL ctx");
+    MFX_ARG_CHECK(mode >= MFX_PIC_OFF && mode <= MFX_PIC_IMPLICIT, "bad PIC mode %d", mode);
+    if (mode != MFX_PIC_OFF && c->rank == 0) {
+        MFX_ARG_CHECK(parcels && pic, "the PIC device (rank 0) needs parcels and pic params");
+        MFX_ARG_CHECK(parcels->n >= 0, "negative parcel count");
+        MFX_ARG_CHECK(pic->d_p > 0.0, "d_p must be positive");
+        c->pic_pc = *parcels;
+        c->pic_pp = *pic;
+        if (!c->pic_ws) {
+            mfx_status st = mfx::ctx_alloc(c, &c->pic_ws, mfx::ws_header_bytes());
+            if (st != MFX_OK) return st;
+            MFX_CUDA_TRY(cudaMemset(c->pic_ws, 0, mfx::ws_header_bytes()));
+            MFX_CUDA_TRY(cudaMemset(&((mfx::WsHeader *)c->pic_ws)->bad_nonfinite, 0xff, 16));
+            MFX_CUDA_TRY(cudaMemset(&((mfx::WsHeader *)c->pic_ws)->bad_parcel, 0xff, 8));
+        }
+    }
+    c->pic_mode = mode;
+    c->pic_pending = mode == MFX_PIC_EXPLICIT;
+    return MFX_OK;
+}
 
 double *mfx_ctx_buffer(mfx_ctx *c, int which)
 {

@@ -5,5 +5,4 @@ timeout 900 python -m pytest tests/test_gpu_pic.py -x -q > gpurun_out/pytest_pic
 timeout 600 python -c "
 import json, torch, bench, paper_2211_15605_b200 as mfx
 print(json.dumps(bench.measure_pic(mfx, torch)))
-print(json.dumps(bench.measure_momentum_c2(mfx, torch)))
 " > gpurun_out/pic_time.json 2>&1; cat gpurun_out/pic_time.json

@@ -144,3 +144,35 @@ def test_no_unresolved_library_symbols():
     bad = [l for l in out.splitlines() if l.strip() and not re.search(r"@(GLIBC|GLIBCXX|CXXABI|GCC)", l)
            and "__gmon_start__" not in l and "_ITM_" not in l and "__cxa_finalize" not in l]
     assert not bad, bad
+
+
+@pytest.mark.parametrize("text,n", [("234[1]", 4), ("111[1]", 1), ("234[1]5678", 8)])
+def test_exchange_plan_pic_phase(mfx, text, n):
+    """Phase 3 (PIC): the PIC device (rank 0) broadcasts the four
+    drag fields; identical op list on every rank (collective order)."""
+    plans = [mfx.exchange_plan(text, n, r, 3) for r in range(n)]
+    assert all(p == plans[0] for p in plans)
+    assert [o["buf"] for o in plans[0]] == ["beta", "sbeta_u", "sbeta_v", "sbeta_w"]
+    assert all(o["op"] == mfx.OP_BCAST and o["peer"] == 0 for o in plans[0])
+
+
+def test_exchange_plan_bad_phase(mfx):
+    with pytest.raises(mfx.MfxError):
+        mfx.exchange_plan("234[1]", 4, 0, 4)
+
+
+def test_pic_entry_points_reject_bad_args(mfx):
+    """Argument errors return MFX_ERR_ARG before any launch (no GPU needed)."""
+    import ctypes as C
+    import synth
+    g = synth.make_grid(16, 16, 32)
+    cg = mfx.c_grid(g)
+    pp = mfx.PicParams(0.0, 0.35)                     # d_p <= 0
+    pc = mfx.Parcels(None, None, None, None, None, None, None, 0)
+    assert mfx.lib().mfx_pic_deposit_eps(C.byref(cg), C.byref(pp), C.byref(pc), None, None, 0, None) == mfx.ERR_ARG
+    assert "d_p" in mfx.last_error()
+    pp = mfx.PicParams(200e-6, 0.35)
+    pc = mfx.Parcels(None, None, None, None, None, None, None, 5)   # n > 0 with NULL arrays
+    assert mfx.lib().mfx_pic_deposit_eps(C.byref(cg), C.byref(pp), C.byref(pc), C.c_void_p(8), C.c_void_p(8),
+                                         1 << 20, None) == mfx.ERR_ARG
+    assert mfx.lib().mfx_ctx_set_pic(None, None, None, 2) == mfx.ERR_ARG

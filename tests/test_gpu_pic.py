@@ -117,6 +117,7 @@ def test_pic_parity(mfx, orc, shape, m, sort):
 def test_pic_bookkeeping(mfx, orc):
     """SPEC.md:306 on the GPU outputs: sum beta V = sum K (GPU's own K)."""
     g, st, pic, pc = case(16, 16, 32, 20000, 5)
+    pic = synth.PicParams(eps_min=-1.0)      # no floor: partition of unity holds cell by cell
     eps_d, eps_o, out_d, out_o, K = run_both(mfx, orc, g, st, pic, pc)
     V = g.dx * g.dy * g.dz
     assert math.fsum(host(out_d["beta"]) * V) == pytest.approx(math.fsum(host(K)), rel=1e-12)
@@ -155,3 +156,102 @@ def test_pic_fullsize_c2(mfx, orc):
     times: every cell compared."""
     g, st, pic, pc = case(128, 128, 512, synth.PAPER_PARCELS, 15607, sort=False, edges=False)
     check(*run_both(mfx, orc, g, st, pic, pc))
+
+
+# ---------------------------------------------------------------- coupling inside the SIMPLE loop (P:97)
+def coupled_case():
+    g = synth.make_grid(16, 12, 20)
+    # tight linear tolerances: both sides converge to the discrete solution, so
+    # the 1e-16-level differences of the deposits cannot be amplified by the
+    # Krylov iteration's path (DESIGN.md §3.9)
+    pr = synth.Params(lin_tol_mom=1e-13, lin_maxit_mom=400, lin_tol_pp=1e-13, lin_maxit_pp=6000)
+    st = synth.make_state(g, 4321, pr)
+    pic = synth.PicParams()
+    pc = synth.make_parcels(g, 4322, 6000, st["eps"], pic)
+    return g, pr, st, pic, pc
+
+
+def oracle_coupled(orc, g, pr, st, pic, pc, outer, implicit):
+    s = {k: v.copy() for k, v in st.items()}
+    for it in range(outer):
+        if implicit or it == 0:
+            d = orc.pic_drag(g, pr, pic, pc, s["eps"], s["u"], s["v"], s["w"])
+            for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w"):
+                s[k] = d[k]
+        s, R, iters, status, rc = orc.simple_iter(g, pr, s)
+        s = {k: np.asarray(v).copy() for k, v in s.items()}
+    return s
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+def test_simple_with_pic_coupling_vs_oracle(mfx, orc, mode):
+    g, pr, st, pic, pc = coupled_case()
+    sd = {k: dev(v) for k, v in st.items()}
+    dpc = {k: dev(v) for k, v in pc.items()}
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    ctx.set_pic(dpc, pic, mfx.PIC_IMPLICIT if mode == "implicit" else mfx.PIC_EXPLICIT)
+    betas = []
+    for _ in range(3):
+        ctx.step(sd)
+        betas.append(host(sd["beta"]).copy())
+    ctx.close()
+    ref = oracle_coupled(orc, g, pr, st, pic, pc, 3, mode == "implicit")
+    # drag fields of the last refresh: within the deposit bound, scaled by beta
+    # (|beta u_s| <= beta |u_p|max with |u_p| well below 1 m/s here)
+    for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w"):
+        assert np.all(np.abs(host(sd[k]) - ref[k]) <= TOL_SUM * ref["beta"]), k
+    for k in ("u", "v", "w", "p"):
+        assert rel_l2(host(sd[k]), ref[k]) <= 1e-9, (k, rel_l2(host(sd[k]), ref[k]))
+    if mode == "explicit":     # refreshed once, then frozen (P:97)
+        assert np.array_equal(betas[0], betas[1]) and np.array_equal(betas[1], betas[2])
+    else:                      # refreshed from the new velocities every iteration
+        assert not np.array_equal(betas[0], betas[1])
+
+
+def test_pic_coupling_multirank_consistent(mfx, orc):
+    """"234[1]" over 4 thread-ranks with implicit coupling: only rank 0 (the PIC
+    device) holds the parcels; its drag fields are broadcast (phase 3),
+    so every rank ends with the same bits, and close to the oracle."""
+    import threading
+    g, pr, st, pic, pc = coupled_case()
+    n = 4
+    group = mfx.LocalGroup(n)
+    res, errs = {}, []
+    bar = threading.Barrier(n)
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sd = {k: dev(v) for k, v in st.items()}
+                dpc = {k: dev(v) for k, v in pc.items()} if rank == 0 else None
+                ctx = mfx.SimpleContext("234[1]", g, pr, rank=rank, nranks=n, group=group)
+                ctx.set_pic(dpc, pic if rank == 0 else None, mfx.PIC_IMPLICIT)
+                bar.wait()
+                for _ in range(2):
+                    ctx.step(sd, stream=stream)
+                stream.synchronize()
+                res[rank] = {k: host(v) for k, v in sd.items()}
+                ctx.close()
+        except Exception as e:  # pragma: no cover
+            errs.append((rank, repr(e)))
+            bar.abort()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    group.close()
+    assert not errs, errs
+    for r in range(1, n):
+        for k in ("u", "v", "w", "p", "beta", "sbeta_w"):
+            assert np.array_equal(res[r][k], res[0][k]), (r, k)
+    ref = oracle_coupled(orc, g, pr, st, pic, pc, 2, True)
+    for k in ("u", "v", "w", "p"):
+        assert rel_l2(res[0][k], ref[k]) <= 1e-9, k

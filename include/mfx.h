@@ -310,7 +310,9 @@ mfx_status mfx_prof_read(int counts[16], double ms[16]);
  * 1 = TMA z-marching kernels, 2 = single-cluster persistent kernel,
  * 3 = v1 grid-stride reference kernels.  "graphs": 1/0 enables CUDA-graph
  * replay of the iteration loop.  "pdl": 1/0 enables programmatic dependent
- * launch between the BiCGSTAB kernels.  Returns MFX_ERR_ARG for an unknown key. */
+ * launch between the BiCGSTAB kernels.  "asm_tma": 1/0 selects the TMA
+ * z-marching momentum assembly (default) or the grid-stride kernel (both give
+ * identical bits).  Returns MFX_ERR_ARG for an unknown key. */
 mfx_status mfx_set_option(const char *key, int value);
 int mfx_get_option(const char *key);
 

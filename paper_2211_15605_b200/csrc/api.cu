@@ -104,6 +104,17 @@ static int env_default(const char *name, int dflt)
 static std::atomic<int> g_opt_path{-1};
 static std::atomic<int> g_opt_graphs{-1};
 static std::atomic<int> g_opt_pdl{-1};
+static std::atomic<int> g_opt_asm{-1};
+int opt_asm_tma()
+{
+    int v = g_opt_asm.load();
+    if (v < 0) {
+        const char *e = getenv("MFX_KERNELS");
+        v = (e && e[0] == 'v' && e[1] == '1') ? 0 : env_default("MFX_ASM_TMA", 1);
+        g_opt_asm.store(v);
+    }
+    return v;
+}
 int opt_pdl()
 {
     int v = g_opt_pdl.load();
@@ -318,6 +329,10 @@ API mfx_status mfx_set_option(const char *key, int value)
         g_opt_pdl.store(value ? 1 : 0);
         return MFX_OK;
     }
+    if (!strcmp(key, "asm_tma")) {
+        g_opt_asm.store(value ? 1 : 0);
+        return MFX_OK;
+    }
     set_error("unknown option '%s'", key);
     return MFX_ERR_ARG;
 }
@@ -328,5 +343,6 @@ API int mfx_get_option(const char *key)
     if (!strcmp(key, "solver_path")) return opt_solver_path();
     if (!strcmp(key, "graphs")) return opt_graphs();
     if (!strcmp(key, "pdl")) return opt_pdl();
+    if (!strcmp(key, "asm_tma")) return opt_asm_tma();
     return -1;
 }

@@ -248,6 +248,9 @@ bool prof_enabled();
 int opt_solver_path();   // 0 auto, 1 TMA, 2 cluster, 3 v1
 int opt_graphs();
 int opt_pdl();
+int opt_asm_tma();
+mfx_status assemble_mom_tma(int kind, const Geo &G, const mfx_params *pr, const mfx_state *st, mfx_eqsys *out,
+                            double *resid2, WsHeader *hdr, dd *part, cudaStream_t s);
 bool cluster_fits(const Geo &G, bool sym);
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s);

@@ -67,7 +67,15 @@ GRIDS = {
     "rag2": (34, 19, 23),
     "thin": (2, 2, 2),
     "tall": (6, 5, 41),
+    "tiles": (70, 21, 45),     # several 32x8 assembly tiles with ragged x/y tails
 }
+
+
+@pytest.fixture(params=["tma", "gridstride"])
+def asm_path(request, mfx):
+    mfx.set_option("asm_tma", 1 if request.param == "tma" else 0)
+    yield request.param
+    mfx.set_option("asm_tma", 1)
 
 
 def case(name, seed=0, n_scalars=1, bc_zhi=BC_OUTLET):
@@ -85,7 +93,7 @@ def case(name, seed=0, n_scalars=1, bc_zhi=BC_OUTLET):
 # ---------------------------------------------------------------- a-1/a-2/a-3 assembly
 @pytest.mark.parametrize("name", list(GRIDS))
 @pytest.mark.parametrize("comp", [0, 1, 2])
-def test_assemble_momentum_bitwise(mfx, orc, name, comp):
+def test_assemble_momentum_bitwise(mfx, orc, name, comp, asm_path):
     g, pr, st = case(name)
     ref, r2, rc = orc.assemble_mom(g, pr, comp, st)
     ws = mfx.Workspace(g)
@@ -96,9 +104,9 @@ def test_assemble_momentum_bitwise(mfx, orc, name, comp):
     assert np.array_equal(host(res2), r2)
 
 
-@pytest.mark.parametrize("name", ["c1", "rag2", "thin"])
+@pytest.mark.parametrize("name", ["c1", "rag2", "thin", "tiles"])
 @pytest.mark.parametrize("bc_zhi", [BC_OUTLET, BC_WALL])
-def test_assemble_momentum_bc_variants(mfx, orc, name, bc_zhi):
+def test_assemble_momentum_bc_variants(mfx, orc, name, bc_zhi, asm_path):
     g, pr, st = case(name, bc_zhi=bc_zhi)
     for comp in range(3):
         ref, r2, _ = orc.assemble_mom(g, pr, comp, st)

@@ -306,9 +306,11 @@ void mfx_prof_enable(int on);
 void mfx_prof_reset(void);
 mfx_status mfx_prof_read(int counts[16], double ms[16]);
 /* Runtime options (process-wide).  "solver_path": 0 = auto (cluster kernel
- * when the system fits one cluster's shared memory, else TMA z-marching),
- * 1 = TMA z-marching kernels, 2 = single-cluster persistent kernel,
- * 3 = v1 grid-stride reference kernels.  "graphs": 1/0 enables CUDA-graph
+ * when the system fits one cluster's shared memory, else the grid-synchronous
+ * kernel when the solver's working set fits in L2 (<= 96 MB, e.g.
+ * configuration 3), else TMA z-marching), 1 = TMA z-marching kernels,
+ * 2 = single-cluster persistent kernel, 3 = v1 grid-stride reference kernels,
+ * 4 = grid-synchronous persistent kernel (one cooperative launch per solve).  "graphs": 1/0 enables CUDA-graph
  * replay of the iteration loop.  "pdl": 1/0 enables programmatic dependent
  * launch between the BiCGSTAB kernels.  "asm_tma": 1/0 selects the TMA
  * z-marching momentum assembly (default) or the grid-stride kernel (both give

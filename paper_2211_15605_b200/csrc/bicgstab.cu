@@ -176,6 +176,109 @@ __global__ void k_zero_if(const WsHeader *h, double *x, long long N)
 }
 
 // ------------------------------------------------------------------ K1
+// The phase bodies and scalar tails are shared by the per-phase kernels
+// (k1/k2/k3) and the grid-synchronous persistent solver (k_bicg_grid).  LD
+// selects the load path: __ldg for data that is constant during a kernel,
+// L1-cached weak loads (coherent after the grid barrier's fence) for vectors another CTA wrote earlier in
+// the same persistent kernel.
+template <bool CG>
+__device__ __forceinline__ double ldv(const double *p)
+{
+    // CG: weak (L1-cached) load, coherent in k_bicg_grid because every grid
+    // barrier ends with a gpu-scope fence in each CTA (MEMBAR + CCTL.IVALL:
+    // the SM's L1 is invalidated) before anything another CTA wrote is read.
+    if (CG) {
+        double v;
+        asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+        return v;
+    }
+    return __ldg(p);
+}
+
+struct K1Pro {
+    double rho, rhn, beta, omega;
+    bool rst, newly, exit;
+};
+
+// K1 prologue: restart / breakdown decision (Q4).  exit: the
+// solve ended in a second breakdown (block 0 thread 0 has written the status).
+template <class SC>
+__device__ __forceinline__ K1Pro k1_prologue(SC &S)
+{
+    K1Pro o;
+    double rho = S.rho, rhn = S.rhn, rho_prev = S.rho_prev, alpha = S.alpha, omega = S.omega;
+    const double rn = S.rn, rr = S.rr;
+    const int restarted = S.restarted;
+    bool rst = S.restart_mode != 0;
+    o.newly = false;
+    o.exit = false;
+    if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
+    if (fabs(rho) <= (1e-14 * rhn) * rn) {
+        if (restarted) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) { S.status = MFX_ERR_BREAKDOWN; S.done = 1; }
+            o.exit = true;
+            return o;
+        }
+        rst = true;
+        o.newly = true;
+        rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
+    }
+    o.rho = rho; o.rhn = rhn; o.omega = omega; o.rst = rst;
+    o.beta = (rho / rho_prev) * (alpha / omega);
+    return o;
+}
+
+template <bool SYM, bool CG>
+__device__ __forceinline__ void k1_body(const Geo &G, const Coef &c, const double *r, double *rh, const double *p_old,
+                                        const double *v_old, double *p_new, double *v_new, const K1Pro &P, Acc &sg,
+                                        long long n0, long long n1, long long step)
+{
+    const double beta = P.beta, omega = P.omega;
+    const bool rst = P.rst;
+    for (long long n = n0; n < n1; n += step) {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        auto pv = [&](long long m) {
+            if (rst) return fma(beta, fma(-omega, 0.0, 0.0), ldv<CG>(r + m));
+            return fma(beta, fma(-omega, ldv<CG>(v_old + m), ldv<CG>(p_old + m)), ldv<CG>(r + m));
+        };
+        const double v = stencil<SYM>(G, c, n, i, j, k, pv);
+        p_new[n] = pv(n);
+        v_new[n] = v;
+        double rhv;
+        if (rst) {
+            rhv = ldv<CG>(r + n);
+            rh[n] = rhv;
+        } else {
+            rhv = CG ? ldv<true>(rh + n) : rh[n];
+        }
+        sg.prod(rhv, v);
+    }
+}
+
+template <class SC>
+__device__ __forceinline__ void k1_tail(SC &S, const K1Pro &P, dd sigma_dd)
+{
+    if (P.rst) {
+        S.rho = P.rho; S.rhn = P.rhn; S.rho_prev = 1.0; S.alpha = 1.0; S.omega = 1.0;
+    }
+    if (P.newly) { S.restarted = 1; S.restarts += 1; }
+    S.restart_mode = 0;
+    S.skip = 0;
+    const double sigma = dd_round(sigma_dd);
+    S.sigma = sigma;
+    if (sigma == 0.0) {
+        if (S.restarted) {
+            S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
+        } else {
+            S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
+            if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+        }
+    } else {
+        S.alpha = P.rho / sigma;
+    }
+}
+
 template <bool SYM>
 __global__ void __launch_bounds__(kThreads) k1(Geo G, Coef c, const double *__restrict__ r, double *rh,
                                               const double *__restrict__ p_old, const double *__restrict__ v_old,
@@ -183,83 +286,27 @@ __global__ void __launch_bounds__(kThreads) k1(Geo G, Coef c, const double *__re
 {
     SolverScalars &S = h->sc;
     if (S.done) return;
-    double rho = S.rho, rhn = S.rhn, rho_prev = S.rho_prev, alpha = S.alpha, omega = S.omega;
-    const double rn = S.rn, rr = S.rr;
-    const int restarted = S.restarted;
-    bool rst = S.restart_mode != 0;
-    bool newly = false;
-    if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
-    if (fabs(rho) <= (1e-14 * rhn) * rn) {
-        if (restarted) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) { S.status = MFX_ERR_BREAKDOWN; S.done = 1; }
-            return;
-        }
-        rst = true;
-        newly = true;
-        rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
-    }
-    const double beta = (rho / rho_prev) * (alpha / omega);
+    const K1Pro P = k1_prologue(S);
+    if (P.exit) return;
     Acc sg;
     sg.zero();
-    GRID_STRIDE(n)
-    {
-        int i, j, k;
-        decode(G, n, i, j, k);
-        auto pv = [&](long long m) {
-            if (rst) return fma(beta, fma(-omega, 0.0, 0.0), __ldg(r + m));
-            return fma(beta, fma(-omega, __ldg(v_old + m), __ldg(p_old + m)), __ldg(r + m));
-        };
-        const double v = stencil<SYM>(G, c, n, i, j, k, pv);
-        p_new[n] = pv(n);
-        v_new[n] = v;
-        double rhv;
-        if (rst) {
-            rhv = __ldg(r + n);
-            rh[n] = rhv;
-        } else {
-            rhv = rh[n];
-        }
-        sg.prod(rhv, v);
-    }
+    k1_body<SYM, false>(G, c, r, rh, p_old, v_old, p_new, v_new, P, sg,
+                        (long long)blockIdx.x * blockDim.x + threadIdx.x, G.N, (long long)gridDim.x * blockDim.x);
     __shared__ dd sh[(kThreads / 32) * 1];
     dd vv[1] = {sg.get()}, out[1];
-    if (grid_reduce_dd<1>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
-        if (rst) {
-            S.rho = rho; S.rhn = rhn; S.rho_prev = 1.0; S.alpha = 1.0; S.omega = 1.0;
-        }
-        if (newly) { S.restarted = 1; S.restarts += 1; }
-        S.restart_mode = 0;
-        S.skip = 0;
-        const double sigma = dd_round(out[0]);
-        S.sigma = sigma;
-        if (sigma == 0.0) {
-            if (S.restarted) {
-                S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
-            } else {
-                S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-                if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-            }
-        } else {
-            S.alpha = rho / sigma;
-        }
-    }
+    if (grid_reduce_dd<1>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k1_tail(S, P, out[0]);
 }
 
 // ------------------------------------------------------------------ K2
-template <bool SYM>
-__global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__restrict__ r,
-                                              const double *__restrict__ v, double *t, WsHeader *h, dd *part)
+template <bool SYM, bool CG>
+__device__ __forceinline__ void k2_body(const Geo &G, const Coef &c, const double *r, const double *v, double *t,
+                                        double alpha, Acc &ts, Acc &tt, Acc &ss, long long n0, long long n1,
+                                        long long step)
 {
-    SolverScalars &S = h->sc;
-    if (S.done || S.skip) return;
-    const double alpha = S.alpha;
-    Acc ts, tt, ss;
-    ts.zero(); tt.zero(); ss.zero();
-    GRID_STRIDE(n)
-    {
+    for (long long n = n0; n < n1; n += step) {
         int i, j, k;
         decode(G, n, i, j, k);
-        auto sv = [&](long long m) { return fma(-alpha, __ldg(v + m), __ldg(r + m)); };
+        auto sv = [&](long long m) { return fma(-alpha, ldv<CG>(v + m), ldv<CG>(r + m)); };
         const double tv = stencil<SYM>(G, c, n, i, j, k, sv);
         const double s = sv(n);
         t[n] = tv;
@@ -267,73 +314,100 @@ __global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__re
         tt.prod(tv, tv);
         ss.prod(s, s);
     }
-    __shared__ dd sh[(kThreads / 32) * 3];
-    dd vv[3] = {ts.get(), tt.get(), ss.get()}, out[3];
-    if (grid_reduce_dd<3>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
-        const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
-        S.ts = tsv; S.tt = ttv; S.ss = ssv;
-        if (sqrt(ssv) <= S.tol * S.bn) {
-            S.half = 1;
-        } else {
-            const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
-            if (ttv == 0.0 || om == 0.0) {
-                if (S.restarted) {
-                    S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
-                } else {
-                    S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-                    if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-                }
+}
+
+template <class SC>
+__device__ __forceinline__ void k2_tail(SC &S, const dd (&out)[3])
+{
+    const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
+    S.ts = tsv; S.tt = ttv; S.ss = ssv;
+    if (sqrt(ssv) <= S.tol * S.bn) {
+        S.half = 1;
+    } else {
+        const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
+        if (ttv == 0.0 || om == 0.0) {
+            if (S.restarted) {
+                S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
             } else {
-                S.omega = om;
+                S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
+                if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
             }
+        } else {
+            S.omega = om;
         }
     }
 }
 
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__restrict__ r,
+                                              const double *__restrict__ v, double *t, WsHeader *h, dd *part)
+{
+    SolverScalars &S = h->sc;
+    if (S.done || S.skip) return;
+    Acc ts, tt, ss;
+    ts.zero(); tt.zero(); ss.zero();
+    k2_body<SYM, false>(G, c, r, v, t, S.alpha, ts, tt, ss, (long long)blockIdx.x * blockDim.x + threadIdx.x, G.N,
+                        (long long)gridDim.x * blockDim.x);
+    __shared__ dd sh[(kThreads / 32) * 3];
+    dd vv[3] = {ts.get(), tt.get(), ss.get()}, out[3];
+    if (grid_reduce_dd<3>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k2_tail(S, out);
+}
+
 // ------------------------------------------------------------------ K3
+template <bool CG>
+__device__ __forceinline__ void k3_body(double *x, double *r, const double *rh, const double *p, const double *v,
+                                        const double *t, double alpha, double omega, bool half, Acc &rhr, Acc &rr,
+                                        long long n0, long long n1, long long step)
+{
+    for (long long n = n0; n < n1; n += step) {
+        const double s = fma(-alpha, ldv<CG>(v + n), CG ? ldv<true>(r + n) : r[n]);
+        double xn, rn;
+        if (half) {
+            xn = fma(alpha, ldv<CG>(p + n), CG ? ldv<true>(x + n) : x[n]);
+            rn = s;
+        } else {
+            xn = fma(omega, s, fma(alpha, ldv<CG>(p + n), CG ? ldv<true>(x + n) : x[n]));
+            rn = fma(-omega, ldv<CG>(t + n), s);
+        }
+        x[n] = xn;
+        r[n] = rn;
+        rhr.prod(ldv<CG>(rh + n), rn);
+        rr.prod(rn, rn);
+    }
+}
+
+template <class SC>
+__device__ __forceinline__ void k3_tail(SC &S, bool half, const dd (&out)[2])
+{
+    S.it += 1;
+    if (half) {
+        S.rn = sqrt(S.ss);
+        S.status = MFX_OK;
+        S.done = 1;
+    } else {
+        S.rho_prev = S.rho;
+        S.rho = dd_round(out[0]);
+        S.rr = dd_round(out[1]);
+        S.rn = sqrt(S.rr);
+        if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
+        else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k3(Geo G, double *x, double *r, const double *__restrict__ rh,
                                               const double *__restrict__ p, const double *__restrict__ v,
                                               const double *__restrict__ t, WsHeader *h, dd *part)
 {
     SolverScalars &S = h->sc;
     if (S.done || S.skip) return;
-    const double alpha = S.alpha, omega = S.omega;
     const bool half = S.half != 0;
     Acc rhr, rr;
     rhr.zero(); rr.zero();
-    GRID_STRIDE(n)
-    {
-        const double s = fma(-alpha, __ldg(v + n), r[n]);
-        double xn, rn;
-        if (half) {
-            xn = fma(alpha, __ldg(p + n), x[n]);
-            rn = s;
-        } else {
-            xn = fma(omega, s, fma(alpha, __ldg(p + n), x[n]));
-            rn = fma(-omega, __ldg(t + n), s);
-        }
-        x[n] = xn;
-        r[n] = rn;
-        rhr.prod(__ldg(rh + n), rn);
-        rr.prod(rn, rn);
-    }
+    k3_body<false>(x, r, rh, p, v, t, S.alpha, S.omega, half, rhr, rr,
+                   (long long)blockIdx.x * blockDim.x + threadIdx.x, G.N, (long long)gridDim.x * blockDim.x);
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
-        S.it += 1;
-        if (half) {
-            S.rn = sqrt(S.ss);
-            S.status = MFX_OK;
-            S.done = 1;
-        } else {
-            S.rho_prev = S.rho;
-            S.rho = dd_round(out[0]);
-            S.rr = dd_round(out[1]);
-            S.rn = sqrt(S.rr);
-            if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
-            else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-        }
-    }
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k3_tail(S, half, out);
 }
 
 // K3, streaming form used with the TMA path: x fastest and nx even, so every
@@ -412,21 +486,189 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
-        S.it += 1;
-        if (half) {
-            S.rn = sqrt(S.ss);
-            S.status = MFX_OK;
-            S.done = 1;
-        } else {
-            S.rho_prev = S.rho;
-            S.rho = dd_round(out[0]);
-            S.rr = dd_round(out[1]);
-            S.rn = sqrt(S.rr);
-            if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
-            else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k3_tail(S, half, out);
+}
+
+// ------------------------------------------------------------------ grid-synchronous persistent solver
+// For systems whose working set fits in L2 (configuration 3: 1M cells, 88 MB
+// for p') the three launches per iteration cost more than the data movement.
+// k_bicg_grid runs the whole iteration loop in ONE cooperative launch: the
+// K1/K2/K3 bodies above with coherent (L2) loads, and in place of the kernel
+// boundaries a grid barrier that also performs the reduction: every CTA posts
+// its double-double partials, the last to arrive folds them in block order,
+// runs the phase's scalar tail (the same code as the per-phase kernels) and
+// releases the others.  Same expressions, same correctly rounded dots: the
+// iterates equal the other paths' bitwise.
+__device__ __forceinline__ SolverScalars sc_load(const SolverScalars *S)
+{
+    static_assert(sizeof(SolverScalars) % 8 == 0, "8-byte words");
+    SolverScalars L;
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(S);
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(&L);
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(SolverScalars) / 8); q++) dst[q] = __ldcg(src + q);
+    return L;
+}
+__device__ __forceinline__ void sc_store(SolverScalars *S, const SolverScalars &L)
+{
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&L);
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(S);
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(SolverScalars) / 8); q++) __stcg(dst + q, src[q]);
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int K, class Tail>
+__device__ __forceinline__ void grid_sync_reduce(dd (&v)[K], dd *part, unsigned *ticket, unsigned *gen, dd *sh,
+                                                 Tail tail)
+{
+    block_reduce_dd<K>(v, sh);
+    __shared__ bool s_last;
+    __shared__ unsigned s_gen;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) part[(size_t)blockIdx.x * K + q] = v[q];
+        s_gen = ld_acquire(gen);
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        dd acc[K];
+#pragma unroll
+        for (int q = 0; q < K; q++) acc[q] = dd{0.0, 0.0};
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                dd x;
+                x.hi = __ldcg(&part[(size_t)b * K + q].hi);
+                x.lo = __ldcg(&part[(size_t)b * K + q].lo);
+                acc[q] = dd_add(acc[q], x);
+            }
+        }
+        block_reduce_dd<K>(acc, sh);
+        if (threadIdx.x == 0) {
+            tail(acc);
+            *ticket = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        }
+    } else if (threadIdx.x == 0) {
+        while (ld_acquire(gen) == s_gen) __nanosleep(32);
+    }
+    if (threadIdx.x == 0) __threadfence();   // L1 invalidate: see ldv<true>
+    __syncthreads();
+}
+
+struct GridVecs {
+    double *r, *rh, *p[2], *v[2], *t;
+};
+
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k_bicg_grid(Geo G, Coef c, double *x, GridVecs W, WsHeader *h, dd *part)
+{
+    unsigned *ticket = &h->ticket[2], *gen = &h->ticket[3];
+    SolverScalars *Sg = &h->sc;
+    const long long n0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    __shared__ dd sh[(kThreads / 32) * 3];
+    int parity = 0;
+    for (;;) {
+        SolverScalars L = sc_load(Sg);
+        if (L.done) break;
+        // ---- K1
+        const K1Pro P = k1_prologue(L);
+        if (P.exit) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) sc_store(Sg, L);
+            break;
+        }
+        double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
+        double *v_old = W.v[parity], *v_new = W.v[parity ^ 1];
+        {
+            Acc sg;
+            sg.zero();
+            k1_body<SYM, true>(G, c, W.r, W.rh, p_old, v_old, p_new, v_new, P, sg, n0, G.N, step);
+            dd vv[1] = {sg.get()};
+            grid_sync_reduce<1>(vv, part, ticket, gen, sh, [&](dd (&o)[1]) {
+                SolverScalars T = sc_load(Sg);
+                k1_tail(T, P, o[0]);
+                sc_store(Sg, T);
+            });
+        }
+        parity ^= 1;
+        L = sc_load(Sg);
+        if (L.done || L.skip) continue;
+        // ---- K2
+        {
+            Acc ts, tt, ss;
+            ts.zero(); tt.zero(); ss.zero();
+            k2_body<SYM, true>(G, c, W.r, v_new, W.t, L.alpha, ts, tt, ss, n0, G.N, step);
+            dd vv[3] = {ts.get(), tt.get(), ss.get()};
+            grid_sync_reduce<3>(vv, part, ticket, gen, sh, [&](dd (&o)[3]) {
+                SolverScalars T = sc_load(Sg);
+                k2_tail(T, o);
+                sc_store(Sg, T);
+            });
+        }
+        L = sc_load(Sg);
+        if (L.done || L.skip) continue;
+        // ---- K3
+        {
+            const bool half = L.half != 0;
+            Acc rhr, rr;
+            rhr.zero(); rr.zero();
+            k3_body<true>(x, W.r, W.rh, p_new, v_new, W.t, L.alpha, L.omega, half, rhr, rr, n0, G.N, step);
+            dd vv[2] = {rhr.get(), rr.get()};
+            grid_sync_reduce<2>(vv, part, ticket, gen, sh, [&](dd (&o)[2]) {
+                SolverScalars T = sc_load(Sg);
+                k3_tail(T, half, o);
+                sc_store(Sg, T);
+            });
         }
     }
+}
+
+template <bool SYM>
+int grid_solver_blocks(long long N)
+{
+    static int g = 0;
+    if (!g) {
+        int occ = 0, dev = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bicg_grid<SYM>, kThreads, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // fewer, fuller CTAs: every barrier is one atomic arrival per CTA
+        const char *e = getenv("MFX_GRID_CTAS_PER_SM");
+        const int want = e ? atoi(e) : 0;   // measured: more CTAs are faster (occupancy limit best)
+        if (want > 0 && want < occ) occ = want;
+        g = sms * (occ > 0 ? occ : 1);
+        if (g > kMaxBlocks) g = kMaxBlocks;
+    }
+    const long long need = (N + kThreads - 1) / kThreads;
+    return (int)(need < g ? need : g);
+}
+
+template <bool SYM>
+mfx_status launch_grid_solver(const Geo &G, const Coef &c, double *x, const WsView &W, cudaStream_t s)
+{
+    GridVecs V;
+    V.r = W.r; V.rh = W.rh; V.p[0] = W.p[0]; V.p[1] = W.p[1]; V.v[0] = W.v[0]; V.v[1] = W.v[1]; V.t = W.t;
+    Geo Gc = G;
+    Coef cc = c;
+    WsHeader *h = W.hdr;
+    dd *part = W.part;
+    void *args[] = {&Gc, &cc, &x, &V, &h, &part};
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[2], 0, 2 * sizeof(unsigned), s));
+    MFX_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_bicg_grid<SYM>, dim3(grid_solver_blocks<SYM>(G.N)),
+                                             dim3(kThreads), args, 0, s));
+    return MFX_OK;
 }
 
 int k3v_grid()
@@ -583,6 +825,21 @@ bool grid_valid(const mfx_grid *g, bool scalar);
 // reference for tests and profiling); default is the TMA z-marching path.
 static bool use_tma() { return opt_solver_path() != 3; }
 
+// grid-synchronous solver (path 4) in auto mode: the solver's working set
+// (coefficients + b + 8 vectors) fits comfortably in the 126 MB L2 and the
+// system is too large for the single-cluster kernel.  MFX_GRID_SOLVER_MB
+// overrides the byte budget (0 disables the auto choice).
+static bool grid_solver_fits(const Geo &G, bool sym)
+{
+    static long long budget = -1;
+    if (budget < 0) {
+        const char *e = getenv("MFX_GRID_SOLVER_MB");
+        budget = (e ? atoll(e) : 0) << 20;   // off by default: measured slower than TMA at c3 (94 vs 61 us)
+    }
+    const long long bytes = (long long)(sym ? 3 + 1 + 8 : 7 + 1 + 8) * 8 * G.N;
+    return budget > 0 && bytes <= budget && !cluster_fits(G, sym);
+}
+
 mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, cudaStream_t s)
 {
     if (!grid_valid(grid, kind == MFX_EQ_SCALAR)) return MFX_ERR_ARG;
@@ -638,8 +895,9 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
         info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
         return (mfx_status)S.status;
     }
+    const bool grid_path = path == 4 || (path == 0 && grid_solver_fits(G, sym));
     count_launch(0, s, true);
-    if (use_tma()) {
+    if (use_tma() && !grid_path) {
         const double *h0[3] = {x, nullptr, nullptr};
         mfx_status st = stencil_launch(1, sym, G, h0, A, A->b, W.r, nullptr, nullptr, W.hdr, W.part, tol, maxit, s,
                                        sweep_dir(true));
@@ -653,6 +911,21 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
     count_launch(15, s, false);
     MFX_CUDA_TRY(cudaGetLastError());
+    if (grid_path) {
+        count_launch(sym ? 6 : 1, s, true);
+        mfx_status st = sym ? launch_grid_solver<true>(G, c, x, W, s) : launch_grid_solver<false>(G, c, x, W, s);
+        count_launch(sym ? 6 : 1, s, false);
+        if (st != MFX_OK) return st;
+        if (!info) return MFX_OK;
+        MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+        MFX_CUDA_TRY(cudaStreamSynchronize(s));
+        const SolverScalars &S = *g_host.pinned;
+        info->iters = S.it;
+        info->status = S.status;
+        info->restarts = S.restarts;
+        info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
+        return (mfx_status)S.status;
+    }
     int launched = 0, chunk = 4;
     while (launched < maxit) {
         int cnt = maxit - launched < chunk ? maxit - launched : chunk;

@@ -248,6 +248,14 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
         double czq1[CPT], czq0[CPT];                 // cz at planes q-1 (aT of output) and q-2 (aB)
 #pragma unroll
         for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
+        // SYM: what step 2 of plane q-1 needs from that plane's stage -- c_x at
+        // x-1..x+CPT, c_y at y-1 and y, the extra field (b | r^ or r) -- is
+        // copied to registers at the end of iteration q-1, so the stage is
+        // released one plane earlier (prefetch depth S-1 instead of S-2).
+        double kxw[CPT + 1], kys[CPT], kyn[CPT], kex[CPT];
+#pragma unroll
+        for (int m = 0; m < CPT; m++) { kxw[m] = 0.0; kys[m] = 0.0; kyn[m] = 0.0; kex[m] = 0.0; }
+        kxw[CPT] = 0.0;
         const int cx0 = (tid % RW) * CPT, cy = tid / RW;
         const int ci = cy * TX + cx0;                // cell-box index of the first owned cell
         const int hc = (cy + 1) * C::HX + (cx0 + 2); // halo-box index of the first owned cell
@@ -329,15 +337,10 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                 }
                 if (CPT == 2) {
                     if (SYM) {
-                        const double *xw = (const double *)(so + C::OFF_XW);
-                        const double *ys = (const double *)(so + C::OFF_YS);
-                        const double2 e2 = *(const double2 *)&xw[cy * C::HX + cx0 + 2];
-                        aW[0] = xw[cy * C::HX + cx0 + 1]; aE[0] = e2.x;
-                        aW[CPT - 1] = e2.x; aE[CPT - 1] = e2.y;
-                        const double2 s2 = *(const double2 *)&ys[cy * TX + cx0];
-                        const double2 n2 = *(const double2 *)&ys[(cy + 1) * TX + cx0];
-                        aS[0] = s2.x; aS[CPT - 1] = s2.y;
-                        aN[0] = n2.x; aN[CPT - 1] = n2.y;
+                        aW[0] = kxw[0]; aE[0] = kxw[1];
+                        aW[CPT - 1] = kxw[1]; aE[CPT - 1] = kxw[CPT];
+                        aS[0] = kys[0]; aS[CPT - 1] = kys[CPT - 1];
+                        aN[0] = kyn[0]; aN[CPT - 1] = kyn[CPT - 1];
                         aB[0] = czq0[0]; aB[CPT - 1] = czq0[CPT - 1];
                         aT[0] = czq1[0]; aT[CPT - 1] = czq1[CPT - 1];
                     } else {
@@ -354,12 +357,10 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 #pragma unroll
                 for (int m = 0; m < CPT; m++) {
                     if (SYM) {
-                        const double *xw = (const double *)(so + C::OFF_XW);
-                        const double *ys = (const double *)(so + C::OFF_YS);
-                        aW[m] = xw[cy * C::HX + cx0 + m + 1];
-                        aE[m] = xw[cy * C::HX + cx0 + m + 2];
-                        aS[m] = ys[cy * TX + cx0 + m];
-                        aN[m] = ys[(cy + 1) * TX + cx0 + m];
+                        aW[m] = kxw[m];
+                        aE[m] = kxw[m + 1];
+                        aS[m] = kys[m];
+                        aN[m] = kyn[m];
                         aB[m] = czq0[m];
                         aT[m] = czq1[m];
                     } else {
@@ -398,8 +399,9 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         double rv[CPT];
 #pragma unroll
                         for (int m = 0; m < CPT; m++) {
-                            rv[m] = bb[m] - y[m];
-                            acc[0][m].prod(bb[m], bb[m]);
+                            const double bm = SYM ? kex[m] : bb[m];
+                            rv[m] = bm - y[m];
+                            acc[0][m].prod(bm, bm);
                             acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
                         }
                         store_cells<CPT>(a.out0 + n, rv);
@@ -409,8 +411,9 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         double rhv[CPT];
 #pragma unroll
                         for (int m = 0; m < CPT; m++)
-                            rhv[m] = rst ? ((const double *)(so + C::OFF_HALO))[hc + m]     // r at the cell
-                                         : ((const double *)(so + C::OFF_EXTRA))[ci + m];
+                            rhv[m] = SYM ? kex[m]
+                                         : (rst ? ((const double *)(so + C::OFF_HALO))[hc + m]     // r at the cell
+                                                : ((const double *)(so + C::OFF_EXTRA))[ci + m]);
                         if (rst) store_cells<CPT>(a.out2 + n, rhv);
 #pragma unroll
                         for (int m = 0; m < CPT; m++) acc[0][m].prod(rhv[m], y[m]);
@@ -425,9 +428,31 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                     }
                 }
             }
-            // stage of plane q-1 is no longer read: release it to the producer
-            __syncwarp();
-            if (q >= 1 && lane == 0) mbar_arrive(&empty[(q + S - 1) % S]);
+            if (SYM) {
+                // plane q's step-2 inputs -> registers, then its stage goes back
+                // to the producer (nothing of stage q is read after this point)
+                if (!virt) {
+                    const double *xw = (const double *)(st + C::OFF_XW);
+                    const double *ys = (const double *)(st + C::OFF_YS);
+#pragma unroll
+                    for (int m = 0; m <= CPT; m++) kxw[m] = xw[cy * C::HX + cx0 + m + 1];
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) {
+                        kys[m] = ys[cy * TX + cx0 + m];
+                        kyn[m] = ys[(cy + 1) * TX + cx0 + m];
+                        if (MODE == SM_SETUP) kex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                        if (MODE == SM_K1)
+                            kex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
+                                         : ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            } else {
+                // stage of plane q-1 is no longer read: release it to the producer
+                __syncwarp();
+                if (q >= 1 && lane == 0) mbar_arrive(&empty[(q + S - 1) % S]);
+            }
 #pragma unroll
             for (int m = 0; m < CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
             cons.advance(a.nz);

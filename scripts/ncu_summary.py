@@ -21,8 +21,8 @@ def classify(name):
     if m:
         mode, sym = int(m.group(1)), int(m.group(2))
         return {0: "spmv", 1: "setup", 2: "K1", 3: "K2"}[mode] + ("_pp" if sym else "_mom")
-    for k in ("k3v", "k_assemble_mom", "k_assemble_pp", "k_assemble_scalar", "k_correct", "k_zero_if",
-              "k_meta", "k_bicg_cluster"):
+    for k in ("k3v", "k_asm_mom_tma", "k_assemble_mom", "k_assemble_pp", "k_assemble_scalar", "k_correct",
+              "k_zero_if", "k_meta", "k_bicg_cluster", "k_pic_eps_final", "k_pic_eps", "k_pic_drag"):
         if k in name:
             return {"k3v": "K3"}.get(k, k)
     return "other:" + name.split("(")[0][-40:]

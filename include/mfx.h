@@ -186,6 +186,32 @@ mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mf
                         const double *w, double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w,
                         double *K, void *ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------- dump / restart (NEXT-4) */
+/* MPXD state dumps (PAPER.md:119 restarts, PAPER.md:121
+ * Eq. 6 comparisons; layout in DESIGN.md §13): a packed little-endian header
+ * {"MPXD", version 1, nx, ny, nz, n_parcels, time, dt, n_fields}, a table of
+ * named fields (8-byte name, kind 0 = cell field of N, 1 = parcel array),
+ * then the binary64 arrays.  Dumped fields: eps, eps_old, u, v, w, u_old,
+ * v_old, w_old, p, beta, sbu, sbv, sbw, phi<s>/phio<s> for s < n_scalars, and
+ * px..pomega when parcels (may be NULL) are given.  Device buffers are copied
+ * on `stream` (synchronises it); the file is written / read with stdio.
+ * Errors (unwritable path, bad magic/version, grid mismatch, truncated file,
+ * missing field, too small parcel capacity) return MFX_ERR_ARG with the
+ * reason in mfx_last_error().  Load of a dump is bitwise: a run continued
+ * from a reloaded state equals the uninterrupted run. */
+mfx_status mfx_state_dump(const char *path, const mfx_grid *grid, const mfx_state *state, int n_scalars,
+                          const mfx_parcels *parcels, double time, double dt, void *stream);
+/* Header query without a GPU (host only): grid extents, parcel count, number
+ * of scalar fields, time and dt.  Any output pointer may be NULL. */
+mfx_status mfx_dump_info(const char *path, int dims[3], long long *n_parcels, int *n_scalars, double *time,
+                         double *dt);
+/* Loads the state fields into `state` (device buffers of N) and, if
+ * parcel_out (7 device arrays x, y, z, u, v, w, omega of parcel_capacity) is
+ * given, the parcels; n_parcels / time / dt outputs may be NULL. */
+mfx_status mfx_state_load(const char *path, const mfx_grid *grid, mfx_state *state, int n_scalars,
+                          double *const parcel_out[7], long long parcel_capacity, long long *n_parcels,
+                          double *time, double *dt, void *stream);
+
 /* ---------------------------------------------------------------- equation decomposition */
 /* Assignment string: three 1-based GPU ids for U, V, W,
  * a bracketed P list, then optional scalar owners, e.g. "111[1]", "234[1]",

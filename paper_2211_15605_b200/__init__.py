@@ -108,6 +108,13 @@ _sigs = {
                                       C.c_size_t, _V]),
     "mfx_pic_drag": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(PicParams), C.POINTER(Parcels)] +
                      [_V] * 9 + [_V, C.c_size_t, _V]),
+    "mfx_state_dump": (C.c_int, [C.c_char_p, C.POINTER(Grid), C.POINTER(State), C.c_int, C.POINTER(Parcels),
+                                 C.c_double, C.c_double, _V]),
+    "mfx_dump_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_int),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mfx_state_load": (C.c_int, [C.c_char_p, C.POINTER(Grid), C.POINTER(State), C.c_int, C.POINTER(_V),
+                                 C.c_longlong, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), _V]),
     "mfx_spmv": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, _V, _V]),
     "mfx_bicgstab_solve": (C.c_int, [C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
                                      _V, C.c_size_t, C.POINTER(SolveInfo), _V]),
@@ -303,6 +310,40 @@ def pic_drag(grid, params, pic, parcels: dict, eps, u, v, w, ws: Workspace, out=
                              _ptr(K, m) if K is not None else None, C.c_void_p(ws.ptr), ws.nbytes,
                              _stream(stream)), "mfx_pic_drag")
     return out
+
+
+def state_dump(path: str, grid, state: dict, n_scalars: int = 0, parcels: dict | None = None, time: float = 0.0,
+               dt: float = 0.0, stream=None):
+    """NEXT-4: MPXD dump of a device state (and parcels) -- mfx_state_dump."""
+    n = grid.nx * grid.ny * grid.nz
+    cp = C.byref(c_parcels(parcels)) if parcels is not None else None
+    _check(_lib.mfx_state_dump(os.fsencode(path), C.byref(c_grid(grid)), C.byref(c_state(state, n)), n_scalars, cp,
+                               time, dt, _stream(stream)), "mfx_state_dump")
+
+
+def dump_info(path: str) -> dict:
+    """Header of an MPXD dump (host only, no GPU needed)."""
+    dims = (C.c_int * 3)()
+    np_, ns = C.c_longlong(), C.c_int()
+    t, dt = C.c_double(), C.c_double()
+    _check(_lib.mfx_dump_info(os.fsencode(path), dims, C.byref(np_), C.byref(ns), C.byref(t), C.byref(dt)),
+           "mfx_dump_info")
+    return dict(dims=tuple(dims), n_parcels=np_.value, n_scalars=ns.value, time=t.value, dt=dt.value)
+
+
+def state_load(path: str, grid, state: dict, n_scalars: int = 0, parcels: dict | None = None, stream=None) -> dict:
+    """Loads an MPXD dump into existing device tensors (state, optional parcels
+    dict with capacity >= the dump's count).  Returns dump_info-like fields."""
+    n = grid.nx * grid.ny * grid.nz
+    pout, cap = None, 0
+    if parcels is not None:
+        cap = parcels["x"].numel()
+        pout = (C.c_void_p * 7)(*[_ptr(parcels[k], cap) for k in PARCEL_KEYS])
+    np_ = C.c_longlong()
+    t, dt = C.c_double(), C.c_double()
+    _check(_lib.mfx_state_load(os.fsencode(path), C.byref(c_grid(grid)), C.byref(c_state(state, n)), n_scalars,
+                               pout, cap, C.byref(np_), C.byref(t), C.byref(dt), _stream(stream)), "mfx_state_load")
+    return dict(n_parcels=np_.value, time=t.value, dt=dt.value)
 
 
 def correct(grid, params, star, pp, p, out=None, stream=None):

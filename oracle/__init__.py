@@ -72,7 +72,7 @@ _DP = C.POINTER(C.c_double)
 class OgState(C.Structure):
     _fields_ = [(n, _DP) for n in ("eps", "eps_old", "u", "v", "w", "u_old", "v_old", "w_old",
                                    "p", "beta", "sbeta_u", "sbeta_v", "sbeta_w")] + \
-               [("phi", _DP * 4), ("phi_old", _DP * 4)]
+               [("phi", _DP * 4), ("phi_old", _DP * 4), ("blocked", C.c_void_p)]
 
 
 class OgEqsys(C.Structure):
@@ -154,16 +154,20 @@ class _State:
     """Keeps numpy arrays alive while the C struct points at them."""
 
     def __init__(self, st: dict, n: int):
-        self.arrays = {k: _f64(v).copy() for k, v in st.items()}
+        self.arrays = {k: (_f64(v).copy() if k != "blocked" else v) for k, v in st.items()}
         for k in ("eps", "eps_old", "u", "v", "w", "u_old", "v_old", "w_old", "p", "beta",
                   "sbeta_u", "sbeta_v", "sbeta_w"):
             self.arrays.setdefault(k, np.zeros(n))
         phis = [self.arrays.setdefault(f"phi{s}", np.zeros(n)) for s in range(4)]
         phios = [self.arrays.setdefault(f"phi_old{s}", np.zeros(n)) for s in range(4)]
         a = self.arrays
+        blocked = st.get("blocked")
+        self.blocked = None if blocked is None else np.ascontiguousarray(blocked, dtype=np.uint8)
+        a.pop("blocked", None)
         self.c = OgState(*[_p(a[k]) for k in ("eps", "eps_old", "u", "v", "w", "u_old", "v_old",
                                               "w_old", "p", "beta", "sbeta_u", "sbeta_v", "sbeta_w")],
-                         (_DP * 4)(*[_p(x) for x in phis]), (_DP * 4)(*[_p(x) for x in phios]))
+                         (_DP * 4)(*[_p(x) for x in phis]), (_DP * 4)(*[_p(x) for x in phios]),
+                         None if self.blocked is None else self.blocked.ctypes.data)
 
 
 SYS_KEYS = ("aP", "aE", "aW", "aN", "aS", "aT", "aB", "b", "d")

@@ -116,6 +116,18 @@ static int inside(const og_grid *g, const int q[3])
 static long at(const og_grid *g, const int q[3]) { return idx(g, q[0], q[1], q[2]); }
 static double maxp(double f) { return f > 0.0 ? f : 0.0; }
 static long ncell(const og_grid *g) { return (long)g->nx * g->ny * g->nz; }
+/* §3.10: Q is a BLOCKED cell (inside the domain and flagged) */
+static int blk(const og_grid *g, const og_state *st, const int Q[3])
+{
+    return st->blocked && inside(g, Q) && st->blocked[at(g, Q)] != 0;
+}
+/* the face between X and X + e_a touches a BLOCKED cell: an internal wall */
+static int wall_face(const og_grid *g, const og_state *st, int a, const int X[3])
+{
+    int Y[3] = {X[0], X[1], X[2]};
+    Y[a] += 1;
+    return blk(g, st, X) || blk(g, st, Y);
+}
 
 static int grid_ok(const og_grid *g)
 {
@@ -178,9 +190,10 @@ void or_spmv(const og_grid *g, const og_eqsys *A, const double *x, double *y)
 
 enum { ROW_INTERIOR = 0, ROW_IDENTITY = 1, ROW_OUTLET = 2 };
 
-static int mom_row_type(const og_grid *g, int c, const int P[3])
+static int mom_row_type(const og_grid *g, const og_state *st, int c, const int P[3])
 {
-    if (P[c] < ext(g, c) - 1) return ROW_INTERIOR;
+    if (blk(g, st, P)) return ROW_IDENTITY;                     /* §3.10 */
+    if (P[c] < ext(g, c) - 1) return wall_face(g, st, c, P) ? ROW_IDENTITY : ROW_INTERIOR;
     if (c == 2 && g->bc_zhi == OG_OUTLET) return ROW_OUTLET;
     return ROW_IDENTITY;
 }
@@ -194,7 +207,7 @@ static const double *comp_field(const og_state *st, int a)
 static double vel_c(const og_grid *g, const og_state *st, int c, const int Q[3])
 {
     if (Q[c] == -1) return (c == 2 && g->bc_zlo == OG_INLET) ? g->w_in : 0.0;
-    if (Q[c] == ext(g, c) - 1 && mom_row_type(g, c, Q) == ROW_IDENTITY) return 0.0;
+    if (mom_row_type(g, st, c, Q) == ROW_IDENTITY) return 0.0;   /* domain or internal wall face */
     return comp_field(st, c)[at(g, Q)];
 }
 
@@ -229,7 +242,7 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
             for (int i = 0; i < g->nx; i++) {
                 const int P[3] = {i, j, k};
                 const long n = at(g, P);
-                const int type = mom_row_type(g, c, P);
+                const int type = mom_row_type(g, st, c, P);
                 if (type == ROW_IDENTITY) {
                     out->aP[n] = 1.0;
                     out->aW[n] = out->aE[n] = out->aS[n] = out->aN[n] = out->aB[n] = out->aT[n] = 0.0;
@@ -256,8 +269,8 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                         double Dm = Dc[c] * st->eps[n];
                         a_side[2 * c] = Dm + maxp(Fm);
                         inP[2 * c] = 1;
-                        if (P[c] >= 1) kept[2 * c] = 1;
-                        else phi_b[2 * c] = vel_c(g, st, c, Qm); /* B1 */
+                        if (P[c] >= 1 && !blk(g, st, Qm)) kept[2 * c] = 1;
+                        else phi_b[2 * c] = vel_c(g, st, c, Qm); /* B1 (domain or internal wall face: 0) */
                         /* plus side: face at the centre of E */
                         if (type == ROW_OUTLET) {
                             a_side[2 * c + 1] = 0.0; /* B3 */
@@ -267,7 +280,7 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                             double Dp = Dc[c] * st->eps[nE];
                             a_side[2 * c + 1] = Dp + maxp(-Fp);
                             inP[2 * c + 1] = 1;
-                            if (mom_row_type(g, c, E) == ROW_IDENTITY) phi_b[2 * c + 1] = 0.0; /* B1 */
+                            if (mom_row_type(g, st, c, E) == ROW_IDENTITY) phi_b[2 * c + 1] = 0.0; /* B1 */
                             else kept[2 * c + 1] = 1;
                         }
                         continue;
@@ -276,7 +289,7 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                         const int side = 2 * t + (s > 0);
                         int Pt[3] = {i, j, k}; Pt[t] += s;
                         int Et[3] = {E[0], E[1], E[2]}; Et[t] += s;
-                        if (inside(g, Pt)) {
+                        if (inside(g, Pt) && !blk(g, st, Pt) && !blk(g, st, Et)) {
                             const int *Q = s > 0 ? P : Pt;
                             const int *R = s > 0 ? E : Et;
                             double F = 0.5 * (mflux_t(g, pr, st, t, Q) + mflux_t(g, pr, st, t, R));
@@ -287,8 +300,8 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                             inP[side] = 1;
                             kept[side] = 1;
                         } else {
-                            int bc = OG_WALL;
-                            if (t == 2) bc = s < 0 ? g->bc_zlo : g->bc_zhi;
+                            int bc = OG_WALL;                    /* domain wall or internal wall (§3.10) */
+                            if (t == 2 && !inside(g, Pt)) bc = s < 0 ? g->bc_zlo : g->bc_zhi;
                             if (bc == OG_OUTLET) { a_side[side] = 0.0; continue; } /* B3 */
                             double F = 0.0;
                             if (bc == OG_INLET)
@@ -367,9 +380,11 @@ static double face_eps(const og_grid *g, const og_state *st, int a, const int X[
 static double plus_face(const og_grid *g, const og_params *pr, const og_state *st, int a,
                         const int X[3], const double *q)
 {
-    if (X[a] <= ext(g, a) - 2)
+    if (X[a] <= ext(g, a) - 2) {
+        if (wall_face(g, st, a, X)) return 0.0;                   /* internal wall (§3.10) */
         return ((pr->rho * face_eps(g, st, a, X)) * area(g, a)) * q[at(g, X)];
-    if (a == 2 && g->bc_zhi == OG_OUTLET)
+    }
+    if (a == 2 && g->bc_zhi == OG_OUTLET && !blk(g, st, X))
         return ((pr->rho * st->eps[at(g, X)]) * area(g, 2)) * q[at(g, X)];
     return 0.0;
 }
@@ -401,18 +416,19 @@ int or_assemble_pp(const og_grid *g, const og_params *pr, const og_state *st,
                         mm[a] = plus_face(g, pr, st, a, Q, vel[a]);
                     } else {
                         cm[a] = 0.0;
-                        mm[a] = (a == 2 && g->bc_zlo == OG_INLET)
+                        mm[a] = (a == 2 && g->bc_zlo == OG_INLET && !blk(g, st, P))
                                     ? ((pr->rho * st->eps[n]) * area(g, 2)) * g->w_in : 0.0;
                     }
                 }
                 double aP = ((((cm[0] + cpl[0]) + cm[1]) + cpl[1]) + cm[2]) + cpl[2];
                 double b = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) -
                            rVdt * (st->eps[n] - st->eps_old[n]);
+                if (blk(g, st, P)) b = 0.0;                               /* empty row: p' stays 0 */
                 out->aP[n] = aP;
                 for (int a = 0; a < 3; a++) cf[a][n] = cpl[a];
                 out->b[n] = b;
                 if (!isfinite(aP) || !isfinite(b)) status = OG_ERR_NONFINITE;
-                else if (aP == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+                else if (aP == 0.0 && !blk(g, st, P) && status == OG_OK) status = OG_ERR_ZERO_DIAG;
             }
     if (cont) *cont = or_sumabs(ncell(g), out->b);
     return status;
@@ -448,7 +464,11 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                     int sm = 2 * a, sp = 2 * a + 1;
                     a_side[sm] = a_side[sp] = 0.0; phib[sm] = phib[sp] = 0.0;
                     kept[sm] = kept[sp] = 0; inP[sm] = inP[sp] = 0;
-                    if (P[a] >= 1) {
+                    int Qm_[3] = {i, j, k}; Qm_[a] -= 1;
+                    int Qp_[3] = {i, j, k}; Qp_[a] += 1;
+                    if (P[a] >= 1 && blk(g, st, Qm_)) {
+                        /* internal zero-flux wall (§3.10): a = 0 */
+                    } else if (P[a] >= 1) {
                         int Q[3] = {i, j, k}; Q[a] -= 1;
                         double e = 0.5 * (st->eps[at(g, Q)] + st->eps[n]);
                         double F = ((pr->rho * e) * area(g, a)) * vel[a][at(g, Q)];
@@ -461,7 +481,9 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                         phib[sm] = g->phi_in;
                     }
                     /* plus side */
-                    if (P[a] <= ext(g, a) - 2) {
+                    if (P[a] <= ext(g, a) - 2 && blk(g, st, Qp_)) {
+                        /* internal zero-flux wall (§3.10) */
+                    } else if (P[a] <= ext(g, a) - 2) {
                         double e = 0.5 * (st->eps[n] + st->eps[at(g, (int[3]){i + (a == 0), j + (a == 1), k + (a == 2)})]);
                         double F = ((pr->rho * e) * area(g, a)) * vel[a][n];
                         a_side[sp] = Dc[a] * e + maxp(-F);
@@ -472,6 +494,16 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                         inP[sp] = 1;
                         phib[sp] = g->phi_out;
                     }
+                }
+                if (blk(g, st, P)) {
+                    /* BLOCKED cell: identity row phi = 0 (no scalar inside an obstacle), no residual */
+                    out->aP[n] = 1.0;
+                    out->aW[n] = out->aE[n] = out->aS[n] = out->aN[n] = out->aB[n] = out->aT[n] = 0.0;
+                    out->b[n] = 0.0;
+                    if (out->d) out->d[n] = 0.0;
+                    rnum[n] = 0.0;
+                    rden[n] = 0.0;
+                    continue;
                 }
                 double sum = ((((a_side[0] + a_side[1]) + a_side[2]) + a_side[3]) + a_side[4]) + a_side[5];
                 double bcb = 0.0;

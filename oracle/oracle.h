@@ -37,6 +37,7 @@ typedef struct {
     double *eps, *eps_old, *u, *v, *w, *u_old, *v_old, *w_old, *p;
     double *beta, *sbeta_u, *sbeta_v, *sbeta_w;
     double *phi[4], *phi_old[4];
+    const unsigned char *blocked;   /* NULL or N flags: 1 = BLOCKED cell (internal obstacle, §3.10) */
 } og_state;
 
 /* Momentum / scalar systems use all 7 coefficient arrays; the p' system is

@@ -229,3 +229,59 @@ def make_parcels(grid: Grid, seed: int, n_parcels: int, eps=None, pic: PicParams
     vel = rng.normal(0.0, 0.05, (3, n_parcels))
     out = dict(x=x, y=y, z=z, u=vel[0], v=vel[1], w=vel[2], omega=omega)
     return {k: np.ascontiguousarray(out[k], dtype=np.float64) for k in PARCEL_KEYS}
+
+
+def bfs_blocked(grid: Grid, step_x: int, step_z: int):
+    """BLOCKED flags of a backward-facing step (Fig. 8): the
+    block fills x < step_x cells, all y, z < step_z cells.  uint8, N."""
+    blocked = np.zeros((grid.nz, grid.ny, grid.nx), dtype=np.uint8)
+    blocked[:step_z, :, :step_x] = 1
+    return blocked.ravel()
+
+
+def zero_wall_faces(grid: Grid, state: dict, blocked):
+    """Staggered velocities (and their old-time values) on faces that touch a
+    BLOCKED cell are wall faces: set them to 0 (input hygiene, no method
+    arithmetic)."""
+    nx, ny, nz = grid.nx, grid.ny, grid.nz
+    bl = np.asarray(blocked).reshape(nz, ny, nx).astype(bool)
+    for key, ax in (("u", 2), ("v", 1), ("w", 0)):
+        wall = bl.copy()
+        src = [slice(None)] * 3
+        dst = [slice(None)] * 3
+        src[ax] = slice(1, None)
+        dst[ax] = slice(0, bl.shape[ax] - 1)
+        wall[tuple(dst)] |= bl[tuple(src)]
+        for k in (key, key + "_old"):
+            if k in state:
+                a = state[k].reshape(nz, ny, nx)
+                a[wall] = 0.0
+    return state
+
+
+def make_bfs_state(grid: Grid, step_x: int, step_z: int, seed: int, params: Params | None = None):
+    """Single-phase backward-facing-step snapshot (rho = 1,
+    mu = 1.8e-5, inlet along +z): eps = 1, no drag, w = w_in plus small noise
+    in the fluid, u, v small noise, hydrostatic gauge pressure; wall faces 0."""
+    params = params or Params()
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = grid.nx, grid.ny, grid.nz
+    sh = (nz, ny, nx)
+    blocked = bfs_blocked(grid, step_x, step_z)
+    u = rng.normal(0.0, 0.01 * max(grid.w_in, 1e-3), sh)
+    v = rng.normal(0.0, 0.01 * max(grid.w_in, 1e-3), sh)
+    w = grid.w_in + rng.normal(0.0, 0.01 * max(grid.w_in, 1e-3), sh)
+    u[:, :, nx - 1] = 0.0
+    v[:, ny - 1, :] = 0.0
+    if grid.bc_zhi == BC_WALL:
+        w[nz - 1] = 0.0
+    zc = (np.arange(nz) + 0.5) * grid.dz
+    lz = nz * grid.dz
+    p = np.broadcast_to((params.rho * 9.81 * (lz - zc))[:, None, None], sh).copy()
+    st = dict(eps=np.ones(sh), eps_old=np.ones(sh), u=u, v=v, w=w, u_old=u.copy(), v_old=v.copy(),
+              w_old=w.copy(), p=p, beta=np.zeros(sh), sbeta_u=np.zeros(sh), sbeta_v=np.zeros(sh),
+              sbeta_w=np.zeros(sh))
+    st = {k: np.ascontiguousarray(a, dtype=np.float64).ravel() for k, a in st.items()}
+    zero_wall_faces(grid, st, blocked)
+    st["blocked"] = blocked
+    return st

@@ -233,6 +233,7 @@ def measure_other_configs(mfx, torch):
         ctx.close()
         del sd
         torch.cuda.empty_cache()
+    out["bfs_10M"] = measure_bfs(mfx, torch)
     out["c5_one_gpu"] = measure_scalars_one_gpu(mfx, torch)
     out["pic_coupling"] = measure_pic(mfx, torch)
     return out
@@ -285,6 +286,41 @@ def _ev_ms(torch, fn, reps):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     return statistics.median(ts), r
+
+
+def measure_bfs(mfx, torch):
+    """NEXT-3 geometry: the paper's single-phase backward-facing step
+    (Fig. 8) at its 10,001,880-cell size (PAPER.md:165,
+    126 x 63 x 1260, BLOCKED cells for the step), SIMPLE outer iterations
+    '111[1]' (4 equations on one GPU)."""
+    import synth
+    g, pr, st = synth.bfs_case()
+    sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    ctx.step(sd)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps, its = 3, 0
+    e0.record()
+    for _ in range(steps):
+        o = ctx.step(sd)
+        its += sum(o["iters"][:4])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ph = ctx.phase_times()
+    ctx.close()
+    pp_it = max(o["iters"][3], 1)
+    res = {"workload": f"BFS single phase, {g.nx}x{g.ny}x{g.nz} = {g.n} cells (block: {g.nx // 2}x{g.ny}x{g.nz // 10}), "
+                       "SIMPLE 111[1]",
+           "simple_iters_per_s": steps / (ms / 1e3), "ms_per_simple_iter": ms / steps,
+           "bicgstab_iters_per_s": its / (ms / 1e3), "iters_last": o["iters"][:4],
+           "pp_us_per_iter": 1e3 * ph["pp"] / pp_it,
+           "pp_alg_GBps": PP_ITER_BPC * g.n / (1e-3 * ph["pp"] / pp_it) / 1e9,
+           "phase_ms_last": ph}
+    del sd
+    torch.cuda.empty_cache()
+    return res
 
 
 def measure_momentum_c2(mfx, torch):

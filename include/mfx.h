@@ -79,6 +79,9 @@ typedef struct {
     double *beta;                         /* implicit drag coefficient per cell (Q11) */
     double *sbeta_u, *sbeta_v, *sbeta_w;  /* explicit drag source beta*u_s per cell */
     double *phi[4], *phi_old[4];          /* optional scalars (NULL if unused) */
+    const unsigned char *blocked;         /* NULL, or N flags, 1 = BLOCKED cell (internal obstacle,
+                                             NEXT-3): faces touching it are walls;
+                                             velocities on those faces and scalars inside must be 0 */
 } mfx_state;
 
 /* Equation system (device pointers, N each).  Momentum/scalar: all seven

@@ -59,7 +59,8 @@ SYS_KEYS = ("aP", "aE", "aW", "aN", "aS", "aT", "aB", "b", "d")
 
 
 class State(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in STATE_KEYS] + [("phi", C.c_void_p * 4), ("phi_old", C.c_void_p * 4)]
+    _fields_ = [(k, C.c_void_p) for k in STATE_KEYS] + [("phi", C.c_void_p * 4), ("phi_old", C.c_void_p * 4),
+                                                        ("blocked", C.c_void_p)]
 
 
 class Eqsys(C.Structure):
@@ -204,6 +205,12 @@ def c_state(state: dict, n: int) -> State:
     for s in range(4):
         st.phi[s] = _ptr(state.get(f"phi{s}"), n)
         st.phi_old[s] = _ptr(state.get(f"phi_old{s}"), n)
+    b = state.get("blocked")
+    if b is not None:
+        import torch
+        if not (b.is_cuda and b.dtype == torch.uint8 and b.is_contiguous() and b.numel() == n):
+            raise ValueError("blocked must be a contiguous uint8 CUDA tensor of N flags")
+        st.blocked = b.data_ptr()
     return st
 
 

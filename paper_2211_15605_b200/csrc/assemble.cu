@@ -52,6 +52,7 @@ struct MomArgs {
     double rho, urf, gc, rVdt;
     double Dc[3];
     const double *eps, *eps0, *vel0, *vel1, *vel2, *uold, *p, *beta, *S;
+    const unsigned char *blocked;   // NULL or N flags
     double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d;
     double *resid2;
     WsHeader *hdr;
@@ -60,10 +61,29 @@ struct MomArgs {
 
 enum { kInterior = 0, kIdentity = 1, kOutlet = 2 };
 
-template <int C>
-__device__ __forceinline__ int row_type(const Geo &G, const int q[3])
+// §3.10: cell (i, j, k) is BLOCKED (outside the domain: not blocked)
+__device__ __forceinline__ bool blk_at(const Geo &G, const unsigned char *bl, int i, int j, int k)
 {
-    if (q[C] < extent(G, C) - 1) return kInterior;
+    if (!bl || i < 0 || j < 0 || k < 0 || i >= G.nx || j >= G.ny || k >= G.nz) return false;
+    return __ldg(bl + ((long long)i + (long long)G.nx * ((long long)j + (long long)G.ny * k))) != 0;
+}
+__device__ __forceinline__ bool blk_q(const Geo &G, const unsigned char *bl, const int q[3])
+{
+    return blk_at(G, bl, q[0], q[1], q[2]);
+}
+
+template <int C>
+__device__ __forceinline__ int row_type(const Geo &G, const int q[3], const unsigned char *bl = nullptr)
+{
+    if (bl && blk_q(G, bl, q)) return kIdentity;                         // §3.10
+    if (q[C] < extent(G, C) - 1) {
+        if (bl) {
+            int e[3] = {q[0], q[1], q[2]};
+            e[C] += 1;
+            if (blk_q(G, bl, e)) return kIdentity;                       // internal wall face
+        }
+        return kInterior;
+    }
     if (C == 2 && G.bc_zhi == MFX_BC_OUTLET) return kOutlet;
     return kIdentity;
 }
@@ -131,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_assemble_mom(MomArgs a)
          n += (long long)gridDim.x * blockDim.x) {
         int P[3];
         decode32(G, n, P);
-        const int type = row_type<C>(G, P);
+        const int type = row_type<C>(G, P, a.blocked);
         if (type == kIdentity) {
             a.aP[n] = 1.0;
             a.aE[n] = 0.0; a.aW[n] = 0.0; a.aN[n] = 0.0; a.aS[n] = 0.0; a.aT[n] = 0.0; a.aB[n] = 0.0;
@@ -188,18 +208,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_assemble_mom(MomArgs a)
         {
             // main axis
             double vm;
+            const bool m_wall = P[C] >= 1 && blk_q(G, a.blocked, Pm);       // internal wall face (§3.10)
             if (P[C] == 0) vm = (C == 2 && G.bc_zlo == MFX_BC_INLET) ? G.w_in : 0.0;
-            else vm = umM;
+            else vm = m_wall ? 0.0 : umM;
             const double Fm = ((a.rho * epsP) * G.A[C]) * (0.5 * (vm + umP));
             const double Dm = a.Dc[C] * epsP;
             as[2 * C] = Dm + maxp(Fm);
             inP[2 * C] = true;
-            if (P[C] >= 1) kept[2 * C] = true;
+            if (P[C] >= 1 && !m_wall) kept[2 * C] = true;
             else phib[2 * C] = vm;                                            // B1
             if (type == kOutlet) {
                 as[2 * C + 1] = 0.0;                                          // B3
             } else {
-                const bool e_ident = row_type<C>(G, E) == kIdentity;
+                const bool e_ident = row_type<C>(G, E, a.blocked) == kIdentity;
                 const double vE_ = e_ident ? 0.0 : umE;
                 const double Fp = ((a.rho * epsE) * G.A[C]) * (0.5 * (umP + vE_));
                 const double Dp = a.Dc[C] * epsE;
@@ -217,7 +238,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_assemble_mom(MomArgs a)
                 const int s = sg ? 1 : -1;
                 const int side = 2 * t + sg;
                 const int pt = P[t] + s;
-                if (pt >= 0 && pt < extent(G, t)) {
+                bool nb_wall = false;                                          // §3.10
+                if (a.blocked && pt >= 0 && pt < extent(G, t)) {
+                    int Pt[3] = {P[0], P[1], P[2]}, Et[3] = {E[0], E[1], E[2]};
+                    Pt[t] += s;
+                    Et[t] += s;
+                    nb_wall = blk_q(G, a.blocked, Pt) || blk_q(G, a.blocked, Et);
+                }
+                if (pt >= 0 && pt < extent(G, t) && !nb_wall) {
                     // +t face mass fluxes of Q and R: eps at X and X + e_t
                     const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
                     const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
@@ -230,8 +258,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_assemble_mom(MomArgs a)
                     inP[side] = true;
                     kept[side] = true;
                 } else {
-                    int bc = MFX_BC_WALL;
-                    if (t == 2) bc = s < 0 ? G.bc_zlo : G.bc_zhi;
+                    int bc = MFX_BC_WALL;                                      // domain or internal wall
+                    if (t == 2 && !nb_wall) bc = s < 0 ? G.bc_zlo : G.bc_zhi;
                     if (bc == MFX_BC_OUTLET) continue;                        // B3
                     double F = 0.0;
                     if (bc == MFX_BC_INLET)
@@ -291,6 +319,7 @@ struct PPArgs {
     Geo G;
     double rho, rVdt;
     const double *eps, *eps0, *us[3], *dv[3];
+    const unsigned char *blocked;
     double *aP, *cx, *cy, *cz, *b;
     double *resid2;
     WsHeader *hdr;
@@ -323,15 +352,24 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
             uM[ax] = __ldg(a.us[ax] + im);
         }
         double cm[3], cpl[3], mm[3], mp[3];
+        const bool bP = blk_q(G, a.blocked, P);
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
             const int ext = extent(G, ax);
+            int Qp[3] = {P[0], P[1], P[2]}, Qm[3] = {P[0], P[1], P[2]};
+            Qp[ax] += 1;
+            Qm[ax] -= 1;
+            const bool wall_p = bP || blk_q(G, a.blocked, Qp);             // §3.10 internal walls
+            const bool wall_m = bP || blk_q(G, a.blocked, Qm);
             // +a face of P
-            if (P[ax] <= ext - 2) {
+            if (P[ax] <= ext - 2 && wall_p) {
+                cpl[ax] = 0.0;
+                mp[ax] = 0.0;
+            } else if (P[ax] <= ext - 2) {
                 const double ef = 0.5 * (epsP + eP[ax]);
                 cpl[ax] = ((a.rho * ef) * G.A[ax]) * dP[ax];
                 mp[ax] = ((a.rho * ef) * G.A[ax]) * uP[ax];
-            } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET) {
+            } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET && !bP) {
                 cpl[ax] = ((a.rho * epsP) * G.A[2]) * dP[ax];
                 mp[ax] = ((a.rho * epsP) * G.A[2]) * uP[ax];
             } else {
@@ -339,24 +377,29 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
                 mp[ax] = 0.0;
             }
             // -a face of P = +a face of P - e_a (interior by construction)
-            if (P[ax] >= 1) {
+            if (P[ax] >= 1 && wall_m) {
+                cm[ax] = 0.0;
+                mm[ax] = 0.0;
+            } else if (P[ax] >= 1) {
                 const double ef = 0.5 * (eM[ax] + epsP);
                 cm[ax] = ((a.rho * ef) * G.A[ax]) * dM[ax];
                 mm[ax] = ((a.rho * ef) * G.A[ax]) * uM[ax];
             } else {
                 cm[ax] = 0.0;
-                mm[ax] = (ax == 2 && G.bc_zlo == MFX_BC_INLET) ? ((a.rho * epsP) * G.A[2]) * G.w_in : 0.0;
+                mm[ax] = (ax == 2 && G.bc_zlo == MFX_BC_INLET && !bP) ? ((a.rho * epsP) * G.A[2]) * G.w_in : 0.0;
             }
         }
         const double aP = ((((cm[0] + cpl[0]) + cm[1]) + cpl[1]) + cm[2]) + cpl[2];
-        const double bb = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) - a.rVdt * (epsP - eps0P);
+        double bb = (((mm[0] - mp[0]) + (mm[1] - mp[1])) + (mm[2] - mp[2])) - a.rVdt * (epsP - eps0P);
+        if (bP) bb = 0.0;                                                   // empty row: p' stays 0
         a.aP[n] = aP;
         a.cx[n] = cpl[0];
         a.cy[n] = cpl[1];
         a.cz[n] = cpl[2];
         a.b[n] = bb;
         const bool nonfin = !isfinite(aP) || !isfinite(bb);
-        if (nonfin || aP == 0.0) latch(a.hdr, nonfin, aP == 0.0, n);
+        const bool zd = aP == 0.0 && !bP;
+        if (nonfin || zd) latch(a.hdr, nonfin, zd, n);
         cont.add(fabs(bb));
     }
     __shared__ dd sh[(kThreads / 32) * 1];
@@ -373,6 +416,7 @@ struct ScalArgs {
     double rho, urf, rVdt;
     double Dc[3];
     const double *eps, *eps0, *vel[3], *phim, *phi0;
+    const unsigned char *blocked;
     double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d;
     double *resid2;
     WsHeader *hdr;
@@ -389,6 +433,14 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
          n += (long long)gridDim.x * blockDim.x) {
         int P[3];
         decode(G, n, P);
+        if (blk_q(G, a.blocked, P)) {
+            // BLOCKED cell (§3.10): identity row phi = 0, no residual
+            a.aP[n] = 1.0;
+            a.aE[n] = 0.0; a.aW[n] = 0.0; a.aN[n] = 0.0; a.aS[n] = 0.0; a.aT[n] = 0.0; a.aB[n] = 0.0;
+            a.b[n] = 0.0;
+            if (a.d) a.d[n] = 0.0;
+            continue;
+        }
         const double epsP = __ldg(a.eps + n);
         double as[6], phib[6];
         bool kept[6], inP[6];
@@ -397,7 +449,12 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
             const int sm = 2 * ax, sp = 2 * ax + 1;
             as[sm] = 0.0; as[sp] = 0.0; phib[sm] = 0.0; phib[sp] = 0.0;
             kept[sm] = false; kept[sp] = false; inP[sm] = false; inP[sp] = false;
-            if (P[ax] >= 1) {
+            int Qm_[3] = {P[0], P[1], P[2]}, Qp_[3] = {P[0], P[1], P[2]};
+            Qm_[ax] -= 1;
+            Qp_[ax] += 1;
+            if (P[ax] >= 1 && blk_q(G, a.blocked, Qm_)) {
+                // internal zero-flux wall (§3.10)
+            } else if (P[ax] >= 1) {
                 int Q[3] = {P[0], P[1], P[2]};
                 Q[ax] -= 1;
                 const long long nQ = lin(G, Q);
@@ -411,7 +468,9 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
                 inP[sm] = true;
                 phib[sm] = G.phi_in;
             }
-            if (P[ax] <= extent(G, ax) - 2) {
+            if (P[ax] <= extent(G, ax) - 2 && blk_q(G, a.blocked, Qp_)) {
+                // internal zero-flux wall (§3.10)
+            } else if (P[ax] <= extent(G, ax) - 2) {
                 int Q[3] = {P[0], P[1], P[2]};
                 Q[ax] += 1;
                 const double e = 0.5 * (epsP + __ldg(a.eps + lin(G, Q)));
@@ -549,11 +608,12 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.uold = kind == 0 ? st->u_old : (kind == 1 ? st->v_old : st->w_old);
         a.S = kind == 0 ? st->sbeta_u : (kind == 1 ? st->sbeta_v : st->sbeta_w);
         a.p = st->p; a.beta = st->beta;
+        a.blocked = st->blocked;
         a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
         count_launch(4, s, true);
-        if (opt_asm_tma()) {
+        if (opt_asm_tma() && !st->blocked) {   // BLOCKED cells: grid-stride kernel (§3.10)
             const mfx_status rc = assemble_mom_tma(kind, G, pr, st, out, resid2, W.hdr, W.part, s);
             count_launch(4, s, false);
             return rc;
@@ -583,6 +643,7 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.rho = pr->rho;
         a.rVdt = rVdt;
         a.eps = st->eps; a.eps0 = st->eps_old;
+        a.blocked = st->blocked;
         for (int t = 0; t < 3; t++) { a.us[t] = star[t]; a.dv[t] = star[3 + t]; }
         a.aP = out->aP; a.cx = out->aE; a.cy = out->aN; a.cz = out->aT; a.b = out->b;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
@@ -604,6 +665,7 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.eps = st->eps; a.eps0 = st->eps_old;
         a.vel[0] = st->u; a.vel[1] = st->v; a.vel[2] = st->w;
         a.phim = st->phi[sid]; a.phi0 = st->phi_old[sid];
+        a.blocked = st->blocked;
         a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;

@@ -285,3 +285,19 @@ def make_bfs_state(grid: Grid, step_x: int, step_z: int, seed: int, params: Para
     zero_wall_faces(grid, st, blocked)
     st["blocked"] = blocked
     return st
+
+
+# PAPER.md:155, Fig. 8: BFS domain 9.8 x 4.9 x 98 cm, block 4.9 x 4.9 x 9.8 cm,
+# inlet 1 m/s along +z; the 10,001,880-cell grid = 126 x 63 x 1260.
+BFS_CELLS = (126, 63, 1260)
+
+
+def bfs_case(nx: int = 126, ny: int = 63, nz: int = 1260, seed: int = 15605 + 10):
+    """(grid, params, state) of the paper's backward-facing-step workload at
+    nx x ny x nz cells (cubic cells, Delta = 9.8 cm / nx), the block occupying
+    half of x and the first tenth of z."""
+    h = 0.098 / nx
+    grid = Grid(nx, ny, nz, h, h, h, bc_zlo=BC_INLET, bc_zhi=BC_OUTLET, w_in=1.0)
+    params = Params()
+    state = make_bfs_state(grid, nx // 2, nz // 10, seed, params)
+    return grid, params, state

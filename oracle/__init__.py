@@ -84,6 +84,12 @@ class OgSolveInfo(C.Structure):
                 ("rel_resid", C.c_double)]
 
 
+class OgTimeCtrl(C.Structure):
+    _fields_ = [("dt", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("grow", C.c_double),
+                ("shrink", C.c_double), ("grow_threshold", C.c_int), ("max_outer", C.c_int),
+                ("time", C.c_double), ("steps", C.c_int), ("rejected", C.c_int)]
+
+
 class OgParcels(C.Structure):
     _fields_ = [(k, _DP) for k in ("x", "y", "z", "u", "v", "w", "omega")] + [("n", C.c_long)]
 
@@ -123,6 +129,9 @@ def lib():
                                        C.c_double]
         L.or_pic_drag.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.POINTER(OgPicParams),
                                   C.POINTER(OgParcels)] + [_DP] * 10
+        L.or_adapt_dt.argtypes = [C.POINTER(OgTimeCtrl), C.c_int, C.c_int]
+        L.or_time_step.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.c_int, C.POINTER(OgState),
+                                   C.POINTER(OgTimeCtrl), C.POINTER(C.c_int), _DP]
         _lib = L
     return _lib
 
@@ -314,6 +323,29 @@ def pic_drag(grid, params, pic, parcels: dict, eps_g, u, v, w, diag: bool = Fals
     if diag:
         out["diag"] = dg
     return out
+
+
+def time_ctrl(dt=1e-3, dt_min=1e-5, dt_max=5e-4, grow=1.1, shrink=0.5, grow_threshold=3, max_outer=10):
+    return OgTimeCtrl(dt, dt_min, dt_max, grow, shrink, grow_threshold, max_outer, 0.0, 0, 0)
+
+
+def adapt_dt(tc: OgTimeCtrl, outer_iters: int, converged: bool) -> bool:
+    """§3.11 controller; updates tc in place, True if accepted."""
+    return bool(lib().or_adapt_dt(C.byref(tc), outer_iters, int(converged)))
+
+
+def time_step(grid, params, state: dict, tc: OgTimeCtrl, n_scalars: int = 0):
+    """One accepted time step (§3.11): returns (new_state, outer_iters, resid[4], rc); tc updated."""
+    S = _State(state, grid.n)
+    resid = np.zeros(4)
+    its = C.c_int()
+    cg, cp = c_grid(grid), c_params(params)
+    rc = lib().or_time_step(C.byref(cg), C.byref(cp), n_scalars, C.byref(S.c), C.byref(tc), C.byref(its),
+                            _p(resid))
+    out = dict(S.arrays)
+    if S.blocked is not None:
+        out["blocked"] = S.blocked
+    return out, its.value, resid, rc
 
 
 # ---------------------------------------------------------------- helpers for pins

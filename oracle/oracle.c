@@ -921,3 +921,80 @@ int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, 
     }
     return OG_OK;
 }
+
+/* ------------------------------------------------------------------ §3.11 */
+/* Time loop (NEXT-3; "initial time step was set to 1 ms and
+ * varied depending on the convergence of SIMPLE iterations with the given
+ * tolerance and maximum number of iterations"; PAPER.md:165 gradual growth
+ * to the maximum 5e-4 s; SPEC.md:388-396 adapt_dt).  Plain definition:
+ *   converged within grow_threshold outer iterations -> dt = min(dt*grow, dt_max)
+ *   converged later                                  -> dt unchanged
+ *   not converged in max_outer, dt > dt_min          -> reject: restore the
+ *        step's initial state, dt = max(dt*shrink, dt_min), retry
+ *   not converged at dt_min                          -> accept (flagged)
+ * On acceptance: time += dt_used, u_old, v_old, w_old <- u, v, w,
+ * eps_old <- eps, phi_old <- phi. */
+int or_adapt_dt(og_time_ctrl *tc, int outer_iters, int converged)
+{
+    if (converged) {
+        if (outer_iters <= tc->grow_threshold) {
+            double d = tc->dt * tc->grow;
+            tc->dt = d < tc->dt_max ? d : tc->dt_max;
+        }
+        return 1;
+    }
+    if (tc->dt > tc->dt_min) {
+        double d = tc->dt * tc->shrink;
+        tc->dt = d > tc->dt_min ? d : tc->dt_min;
+        return 0;
+    }
+    return 1; /* accepted at dt_min although not converged */
+}
+
+int or_time_step(const og_grid *g, const og_params *pr0, int n_scalars, og_state *st, og_time_ctrl *tc,
+                 int *outer_used, double resid[4])
+{
+    const long N = ncell(g);
+    const size_t vb = sizeof(double) * (size_t)N;
+    double *save[8];
+    double *fld[8] = {st->u, st->v, st->w, st->p, NULL, NULL, NULL, NULL};
+    for (int s = 0; s < n_scalars; s++) fld[4 + s] = st->phi[s];
+    for (int q = 0; q < 8; q++) {
+        save[q] = NULL;
+        if (fld[q]) { save[q] = malloc(vb); memcpy(save[q], fld[q], vb); }
+    }
+    og_params pr = *pr0;
+    int rc = OG_OK, accepted = 0, its = 0, conv = 0;
+    double dt_used = tc->dt;
+    while (!accepted) {
+        pr.dt = tc->dt;
+        dt_used = tc->dt;
+        conv = 0;
+        its = 0;
+        for (int it = 1; it <= tc->max_outer; it++) {
+            int iters[8], status[8];
+            rc = or_simple_iter(g, &pr, n_scalars, st, resid, iters, status);
+            its = it;
+            if (rc < 0 && rc != OG_ERR_BREAKDOWN) goto out;
+            double mx = resid[0];
+            for (int q = 1; q < 4; q++) mx = resid[q] > mx ? resid[q] : mx;
+            if (mx < pr.tol) { conv = 1; break; }
+        }
+        accepted = or_adapt_dt(tc, its, conv);
+        if (!accepted) {
+            tc->rejected += 1;
+            for (int q = 0; q < 8; q++)
+                if (fld[q]) memcpy(fld[q], save[q], vb);
+        }
+    }
+    tc->time += dt_used;
+    tc->steps += 1;
+    memcpy(st->u_old, st->u, vb); memcpy(st->v_old, st->v, vb); memcpy(st->w_old, st->w, vb);
+    memcpy(st->eps_old, st->eps, vb);
+    for (int s = 0; s < n_scalars; s++) memcpy(st->phi_old[s], st->phi[s], vb);
+    rc = conv ? OG_OK : OG_NOT_CONVERGED;
+out:
+    if (outer_used) *outer_used = its;
+    for (int q = 0; q < 8; q++) free(save[q]);
+    return rc;
+}

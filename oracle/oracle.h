@@ -95,6 +95,20 @@ int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, 
                 const double *eps_g, const double *u, const double *v, const double *w,
                 double *beta, double *sbu, double *sbv, double *sbw, double *diag, double *sabs);
 
+/* §3.11 time loop: adaptive dt controller */
+typedef struct {
+    double dt, dt_min, dt_max, grow, shrink;
+    int grow_threshold, max_outer;
+    double time;
+    int steps, rejected;
+} og_time_ctrl;
+/* returns 1 if the step is accepted; updates tc->dt */
+int or_adapt_dt(og_time_ctrl *tc, int outer_iters, int converged);
+/* one accepted time step (retries included); returns OG_OK (converged),
+ * OG_NOT_CONVERGED (accepted at dt_min) or an error */
+int or_time_step(const og_grid *g, const og_params *pr, int n_scalars, og_state *st, og_time_ctrl *tc,
+                 int *outer_used, double resid[4]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,6 @@
 // residual sums reduce in a fixed order (correctly rounded).
 // Assembly runs once per outer iteration; the BiCGSTAB kernels dominate.
 #include <climits>
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -137,8 +136,8 @@ __device__ __forceinline__ void decode32(const Geo &G, long long n, int q[3])
 // Momentum row.  Every neighbour value the row can need is
 // loaded first, unconditionally, from clamped indices (34 independent loads in
 // flight per thread); the boundary rules then only select among them.
-template <int C, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_assemble_mom(MomArgs a)
+template <int C>
+__global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
 {
     const Geo &G = a.G;
     constexpr int T1 = C == 0 ? 1 : 0, T2 = C == 2 ? 1 : 2;   // transverse axes
@@ -618,20 +617,9 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
             count_launch(4, s, false);
             return rc;
         }
-        static const int minb = [] { const char *e = getenv("MFX_ASM_MINB"); return e ? atoi(e) : 2; }();
-        if (minb == 3) {
-            if (kind == 0) k_assemble_mom<0, 3><<<nb, kThreads, 0, s>>>(a);
-            else if (kind == 1) k_assemble_mom<1, 3><<<nb, kThreads, 0, s>>>(a);
-            else k_assemble_mom<2, 3><<<nb, kThreads, 0, s>>>(a);
-        } else if (minb == 4) {
-            if (kind == 0) k_assemble_mom<0, 4><<<nb, kThreads, 0, s>>>(a);
-            else if (kind == 1) k_assemble_mom<1, 4><<<nb, kThreads, 0, s>>>(a);
-            else k_assemble_mom<2, 4><<<nb, kThreads, 0, s>>>(a);
-        } else {
-            if (kind == 0) k_assemble_mom<0, 2><<<nb, kThreads, 0, s>>>(a);
-            else if (kind == 1) k_assemble_mom<1, 2><<<nb, kThreads, 0, s>>>(a);
-            else k_assemble_mom<2, 2><<<nb, kThreads, 0, s>>>(a);
-        }
+        if (kind == 0) k_assemble_mom<0><<<nb, kThreads, 0, s>>>(a);
+        else if (kind == 1) k_assemble_mom<1><<<nb, kThreads, 0, s>>>(a);
+        else k_assemble_mom<2><<<nb, kThreads, 0, s>>>(a);
         count_launch(4, s, false);
     } else if (kind == MFX_EQ_PP) {
         MFX_ARG_CHECK(star && star[0] && star[1] && star[2] && star[3] && star[4] && star[5], "p' needs star[6]");

@@ -314,6 +314,29 @@ mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void 
 enum { MFX_PIC_OFF = 0, MFX_PIC_EXPLICIT = 1, MFX_PIC_IMPLICIT = 2 };
 mfx_status mfx_ctx_set_pic(mfx_ctx *ctx, const mfx_parcels *parcels, const mfx_pic_params *pic, int mode);
 
+/* Time loop (NEXT-3; "initial time step was set
+ * to 1 ms and varied depending on the convergence of SIMPLE iterations",
+ * PAPER.md:165).  mfx_adapt_dt (host, pure): converged within
+ * grow_threshold outer iterations -> dt = min(dt*grow, dt_max); converged
+ * later -> unchanged; not converged and dt > dt_min -> returns *accept = 0
+ * with dt = max(dt*shrink, dt_min); not converged at dt_min -> accepted.
+ * mfx_time_step: one accepted time step on this rank's context: params.dt is
+ * set to tc->dt, up to max_outer mfx_simple_iter calls until the residual
+ * record converges, a rejected attempt restores u, v, w, p, phi to the step's
+ * start (device copies) and retries; on acceptance time += dt_used, steps++,
+ * and u_old, v_old, w_old, eps_old, phi_old <- u, v, w, eps, phi.  Every rank
+ * takes identical decisions (the residual record is exchanged).  Returns
+ * MFX_OK (converged) or MFX_NOT_CONVERGED (accepted at dt_min). */
+typedef struct {
+    double dt, dt_min, dt_max, grow, shrink;
+    int grow_threshold, max_outer;
+    double time;            /* in/out: simulated time */
+    int steps, rejected;    /* in/out: accepted steps, rejected attempts */
+} mfx_time_ctrl;
+mfx_status mfx_adapt_dt(mfx_time_ctrl *tc, int outer_iters, int converged, int *accept);
+mfx_status mfx_time_step(mfx_ctx *ctx, mfx_state *state, mfx_time_ctrl *tc, mfx_resid *last, int *outer_iters,
+                         void *stream);
+
 /* Device pointers to the context's internal buffers from the last
  * mfx_simple_iter (NULL where this rank does not hold them): which =
  * 0..2 u*, v*, w* (momentum predictors), 3..5 d_x, d_y, d_z, 6 p' solution. */

@@ -96,6 +96,17 @@ class PicParams(C.Structure):
 
 PARCEL_KEYS = ("x", "y", "z", "u", "v", "w", "omega")
 
+
+class TimeCtrl(C.Structure):
+    """mfx_time_ctrl (include/mfx.h): adaptive dt controller state."""
+    _fields_ = [("dt", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double), ("grow", C.c_double),
+                ("shrink", C.c_double), ("grow_threshold", C.c_int), ("max_outer", C.c_int),
+                ("time", C.c_double), ("steps", C.c_int), ("rejected", C.c_int)]
+
+
+def time_ctrl(dt=1e-3, dt_min=1e-5, dt_max=5e-4, grow=1.1, shrink=0.5, grow_threshold=3, max_outer=10) -> TimeCtrl:
+    return TimeCtrl(dt, dt_min, dt_max, grow, shrink, grow_threshold, max_outer, 0.0, 0, 0)
+
 _V = C.c_void_p
 _sigs = {
     "mfx_last_error": (C.c_char_p, []),
@@ -136,6 +147,8 @@ _sigs = {
     "mfx_ctx_phase_times": (C.c_int, [_V, C.POINTER(C.c_double)]),
     "mfx_ctx_buffer": (C.c_void_p, [_V, C.c_int]),
     "mfx_ctx_set_pic": (C.c_int, [_V, C.POINTER(Parcels), C.POINTER(PicParams), C.c_int]),
+    "mfx_adapt_dt": (C.c_int, [C.POINTER(TimeCtrl), C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "mfx_time_step": (C.c_int, [_V, C.POINTER(State), C.POINTER(TimeCtrl), C.POINTER(Resid), C.POINTER(C.c_int), _V]),
     "mfx_dist_solve": (C.c_int, [_V, C.c_int, C.POINTER(Grid), C.POINTER(Eqsys), _V, C.c_double, C.c_int,
                                  C.POINTER(SolveInfo), _V]),
     "mfx_dist_slab": (None, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -353,6 +366,13 @@ def state_load(path: str, grid, state: dict, n_scalars: int = 0, parcels: dict |
     return dict(n_parcels=np_.value, time=t.value, dt=dt.value)
 
 
+def adapt_dt(tc: TimeCtrl, outer_iters: int, converged: bool) -> bool:
+    """Host-side adaptive dt rule (mfx_adapt_dt); returns True if accepted."""
+    acc = C.c_int()
+    _check(_lib.mfx_adapt_dt(C.byref(tc), outer_iters, int(converged), C.byref(acc)), "mfx_adapt_dt")
+    return bool(acc.value)
+
+
 def correct(grid, params, star, pp, p, out=None, stream=None):
     """a-7. star = (u*, v*, w*, d_x, d_y, d_z). Returns (u, v, w, p_new)."""
     import torch
@@ -436,6 +456,17 @@ class SimpleContext:
         _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))   # NONFINITE/ZERO_DIAG raise
         return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
                     status=list(r.status), converged=bool(r.converged))
+
+    def time_step(self, state: dict, tc: TimeCtrl, stream=None) -> dict:
+        """One accepted time step with adaptive dt (mfx_time_step, DESIGN.md §3.11);
+        tc is updated in place."""
+        n = self.grid.nx * self.grid.ny * self.grid.nz
+        cs = c_state(state, n)
+        r = Resid()
+        its = C.c_int()
+        st = _lib.mfx_time_step(self.ptr, C.byref(cs), C.byref(tc), C.byref(r), C.byref(its), _stream(stream))
+        _check(st, "mfx_time_step", ok=(OK, NOT_CONVERGED))
+        return dict(status=st, outer_iters=its.value, R=[r.R_u, r.R_v, r.R_w, r.R_cont], converged=bool(r.converged))
 
     def set_pic(self, parcels: dict | None, pic=None, mode: int = PIC_IMPLICIT):
         """Particle -> fluid coupling in the SIMPLE loop: PIC_IMPLICIT

@@ -284,6 +284,7 @@ struct mfx_ctx {
     size_t dist_bytes;
     cudaEvent_t ev[6];
     double phase_ms[6];
+    double *ts_save[8];       // time loop: state at the start of the step (allocated on first use)
     // particle -> fluid coupling: parcels live on the PIC device (rank 0)
     int pic_mode, pic_pending;
     mfx_parcels pic_pc;
@@ -785,6 +786,86 @@ mfx_status mfx_dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mf
 }
 
 void mfx_dist_slab(int nz, int rank, int nranks, int *k0, int *k1) { mfx::dist_slab(nz, rank, nranks, k0, k1); }
+
+mfx_status mfx_adapt_dt(mfx_time_ctrl *tc, int outer_iters, int converged, int *accept)
+{
+    MFX_ARG_CHECK(tc && accept, "NULL argument");
+    MFX_ARG_CHECK(tc->dt > 0.0 && tc->dt_min > 0.0 && tc->dt_max >= tc->dt_min, "bad dt bounds");
+    if (converged) {
+        if (outer_iters <= tc->grow_threshold) {
+            const double d = tc->dt * tc->grow;
+            tc->dt = d < tc->dt_max ? d : tc->dt_max;
+        }
+        *accept = 1;
+        return MFX_OK;
+    }
+    if (tc->dt > tc->dt_min) {
+        const double d = tc->dt * tc->shrink;
+        tc->dt = d > tc->dt_min ? d : tc->dt_min;
+        *accept = 0;
+        return MFX_OK;
+    }
+    *accept = 1;   // accepted at dt_min although not converged
+    return MFX_OK;
+}
+
+mfx_status mfx_time_step(mfx_ctx *c, mfx_state *st, mfx_time_ctrl *tc, mfx_resid *last, int *outer_iters,
+                         void *stream)
+{
+    MFX_ARG_CHECK(c && st && tc, "NULL argument");
+    MFX_ARG_CHECK(tc->max_outer >= 1, "max_outer must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t vb = sizeof(double) * (size_t)c->N;
+    const int ns = c->asg.n_scalars;
+    double *fld[8] = {st->u, st->v, st->w, st->p, nullptr, nullptr, nullptr, nullptr};
+    for (int q = 0; q < ns; q++) fld[4 + q] = st->phi[q];
+    for (int q = 0; q < 4 + ns; q++) {
+        MFX_ARG_CHECK(fld[q], "state field %d is NULL", q);
+        if (!c->ts_save[q]) {
+            mfx_status rc = mfx::ctx_alloc(c, (void **)&c->ts_save[q], vb);
+            if (rc != MFX_OK) return rc;
+        }
+        MFX_CUDA_TRY(cudaMemcpyAsync(c->ts_save[q], fld[q], vb, cudaMemcpyDeviceToDevice, s));
+    }
+    const double dt0 = c->params.dt;
+    mfx_resid R;
+    memset(&R, 0, sizeof(R));
+    int accepted = 0, its = 0, conv = 0;
+    double dt_used = tc->dt;
+    mfx_status rc = MFX_OK;
+    while (!accepted) {
+        c->params.dt = tc->dt;
+        dt_used = tc->dt;
+        conv = 0;
+        its = 0;
+        for (int it = 1; it <= tc->max_outer; it++) {
+            rc = mfx::simple_iter(c, st, &R, s);
+            its = it;
+            if (rc < 0 && rc != MFX_ERR_BREAKDOWN) { c->params.dt = dt0; return rc; }
+            if (R.converged) { conv = 1; break; }
+        }
+        rc = mfx_adapt_dt(tc, its, conv, &accepted);
+        if (rc != MFX_OK) { c->params.dt = dt0; return rc; }
+        if (!accepted) {
+            tc->rejected += 1;
+            for (int q = 0; q < 4 + ns; q++)
+                MFX_CUDA_TRY(cudaMemcpyAsync(fld[q], c->ts_save[q], vb, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    c->params.dt = dt0;
+    tc->time += dt_used;
+    tc->steps += 1;
+    MFX_CUDA_TRY(cudaMemcpyAsync(st->u_old, st->u, vb, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(st->v_old, st->v, vb, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(st->w_old, st->w, vb, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(st->eps_old, st->eps, vb, cudaMemcpyDeviceToDevice, s));
+    for (int q = 0; q < ns; q++)
+        MFX_CUDA_TRY(cudaMemcpyAsync(st->phi_old[q], st->phi[q], vb, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    if (last) *last = R;
+    if (outer_iters) *outer_iters = its;
+    return conv ? MFX_OK : MFX_NOT_CONVERGED;
+}
 
 mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic_params *pic, int mode)
 {

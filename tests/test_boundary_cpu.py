@@ -176,3 +176,27 @@ def test_pic_entry_points_reject_bad_args(mfx):
     assert mfx.lib().mfx_pic_deposit_eps(C.byref(cg), C.byref(pp), C.byref(pc), C.c_void_p(8), C.c_void_p(8),
                                          1 << 20, None) == mfx.ERR_ARG
     assert mfx.lib().mfx_ctx_set_pic(None, None, None, 2) == mfx.ERR_ARG
+
+
+def test_adapt_dt_matches_spec_examples(mfx):
+    """mfx_adapt_dt is host logic: SPEC.md:393-395 examples without a GPU."""
+    tc = mfx.time_ctrl(dt=4.8e-4, dt_max=5e-4, grow=1.1, grow_threshold=3)
+    assert mfx.adapt_dt(tc, 2, True) and tc.dt == 5e-4
+    tc = mfx.time_ctrl(dt=1e-3, shrink=0.5)
+    assert not mfx.adapt_dt(tc, 10, False) and tc.dt == 5e-4
+    tc = mfx.time_ctrl(dt=3e-4, grow_threshold=3)
+    assert mfx.adapt_dt(tc, 4, True) and tc.dt == 3e-4
+    tc = mfx.time_ctrl(dt=1e-5, dt_min=1e-5)
+    assert mfx.adapt_dt(tc, 10, False) and tc.dt == 1e-5
+
+
+def test_adapt_dt_same_decisions_as_oracle(mfx, orc):
+    rng = __import__("numpy").random.default_rng(4)
+    for _ in range(200):
+        args = dict(dt=float(rng.uniform(1e-5, 2e-3)), dt_min=1e-5, dt_max=float(rng.uniform(1e-4, 1e-3)),
+                    grow=float(rng.uniform(1.0, 1.5)), shrink=float(rng.uniform(0.2, 0.9)),
+                    grow_threshold=int(rng.integers(1, 5)), max_outer=10)
+        a, b = mfx.time_ctrl(**args), orc.time_ctrl(**args)
+        its, conv = int(rng.integers(1, 11)), bool(rng.integers(0, 2))
+        assert mfx.adapt_dt(a, its, conv) == orc.adapt_dt(b, its, conv)
+        assert a.dt == b.dt

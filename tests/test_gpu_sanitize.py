@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("path", ["1", "2", "4", "pic", "bfs"])
 def test_sanitizer_clean(tool, path):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
@@ -22,7 +22,7 @@ def test_sanitizer_clean(tool, path):
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not found")
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
-                        os.path.join(ROOT, "scripts", "sanitize_case.py"), str(path)],
+                        os.path.join(ROOT, "scripts", "sanitize_case.py"), path],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert ("0 errors" in r.stdout) or ("0 hazards" in r.stdout)

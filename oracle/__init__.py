@@ -63,7 +63,8 @@ class OgParams(C.Structure):
                 ("g", C.c_double * 3), ("dt", C.c_double), ("urf_mom", C.c_double),
                 ("urf_p", C.c_double), ("urf_phi", C.c_double), ("tol", C.c_double),
                 ("lin_tol_mom", C.c_double), ("lin_tol_pp", C.c_double), ("lin_tol_phi", C.c_double),
-                ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int)]
+                ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int),
+                ("face_eps_upwind", C.c_int)]
 
 
 _DP = C.POINTER(C.c_double)
@@ -156,7 +157,8 @@ def c_grid(grid) -> OgGrid:
 def c_params(pr) -> OgParams:
     return OgParams(pr.rho, pr.mu, (C.c_double * 4)(*pr.gamma_phi), (C.c_double * 3)(*pr.g), pr.dt,
                     pr.urf_mom, pr.urf_p, pr.urf_phi, pr.tol, pr.lin_tol_mom, pr.lin_tol_pp,
-                    pr.lin_tol_phi, pr.lin_maxit_mom, pr.lin_maxit_pp, pr.lin_maxit_phi)
+                    pr.lin_tol_phi, pr.lin_maxit_mom, pr.lin_maxit_pp, pr.lin_maxit_phi,
+                    int(getattr(pr, "face_eps_upwind", 0)))
 
 
 class _State:

@@ -212,11 +212,21 @@ static double vel_c(const og_grid *g, const og_state *st, int c, const int Q[3])
 }
 
 /* mass flux through the +t face of cell X, the face being interior */
+/* §3.12: eps on the +a face of X for a convective mass flux: the central
+ * average (reading Q9), or with face_eps_upwind the upwind cell's value by
+ * the sign of the snapshot velocity on that face (>= 0: X). */
+static double conv_face_eps(const og_grid *g, const og_params *pr, const og_state *st, int a, const int X[3])
+{
+    int Y[3] = {X[0], X[1], X[2]};
+    Y[a] += 1;
+    if (pr->face_eps_upwind)
+        return comp_field(st, a)[at(g, X)] >= 0.0 ? st->eps[at(g, X)] : st->eps[at(g, Y)];
+    return 0.5 * (st->eps[at(g, X)] + st->eps[at(g, Y)]);
+}
+
 static double mflux_t(const og_grid *g, const og_params *pr, const og_state *st, int t, const int X[3])
 {
-    int Xt[3] = {X[0], X[1], X[2]};
-    Xt[t] += 1;
-    double ef = 0.5 * (st->eps[at(g, X)] + st->eps[at(g, Xt)]);
+    double ef = conv_face_eps(g, pr, st, t, X);
     return ((pr->rho * ef) * area(g, t)) * comp_field(st, t)[at(g, X)];
 }
 
@@ -370,11 +380,6 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
  * outlet face stays in a_P with ghost p' = 0 (Q13).  b = mass imbalance of
  * the starred field minus the transient term (Eq. 1 discretised). */
 
-static double face_eps(const og_grid *g, const og_state *st, int a, const int X[3])
-{
-    int Y[3] = {X[0], X[1], X[2]}; Y[a] += 1;
-    return 0.5 * (st->eps[at(g, X)] + st->eps[at(g, Y)]);
-}
 
 /* coefficient-like quantity rho eps_f A_f q on the +a face of X */
 static double plus_face(const og_grid *g, const og_params *pr, const og_state *st, int a,
@@ -382,7 +387,7 @@ static double plus_face(const og_grid *g, const og_params *pr, const og_state *s
 {
     if (X[a] <= ext(g, a) - 2) {
         if (wall_face(g, st, a, X)) return 0.0;                   /* internal wall (§3.10) */
-        return ((pr->rho * face_eps(g, st, a, X)) * area(g, a)) * q[at(g, X)];
+        return ((pr->rho * conv_face_eps(g, pr, st, a, X)) * area(g, a)) * q[at(g, X)];
     }
     if (a == 2 && g->bc_zhi == OG_OUTLET && !blk(g, st, X))
         return ((pr->rho * st->eps[at(g, X)]) * area(g, 2)) * q[at(g, X)];
@@ -471,7 +476,7 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                     } else if (P[a] >= 1) {
                         int Q[3] = {i, j, k}; Q[a] -= 1;
                         double e = 0.5 * (st->eps[at(g, Q)] + st->eps[n]);
-                        double F = ((pr->rho * e) * area(g, a)) * vel[a][at(g, Q)];
+                        double F = ((pr->rho * conv_face_eps(g, pr, st, a, Q)) * area(g, a)) * vel[a][at(g, Q)];
                         a_side[sm] = Dc[a] * e + maxp(F);
                         kept[sm] = inP[sm] = 1;
                     } else if (a == 2 && g->bc_zlo == OG_INLET) {
@@ -485,7 +490,7 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                         /* internal zero-flux wall (§3.10) */
                     } else if (P[a] <= ext(g, a) - 2) {
                         double e = 0.5 * (st->eps[n] + st->eps[at(g, (int[3]){i + (a == 0), j + (a == 1), k + (a == 2)})]);
-                        double F = ((pr->rho * e) * area(g, a)) * vel[a][n];
+                        double F = ((pr->rho * conv_face_eps(g, pr, st, a, P)) * area(g, a)) * vel[a][n];
                         a_side[sp] = Dc[a] * e + maxp(-F);
                         kept[sp] = inP[sp] = 1;
                     } else if (a == 2 && g->bc_zhi == OG_DIRICHLET_TEST) {

@@ -31,6 +31,7 @@ typedef struct {
     double rho, mu, gamma_phi[4], g[3], dt, urf_mom, urf_p, urf_phi;
     double tol, lin_tol_mom, lin_tol_pp, lin_tol_phi;
     int lin_maxit_mom, lin_maxit_pp, lin_maxit_phi;
+    int face_eps_upwind;        /* §3.12: 1 = convective face eps upwinded by the snapshot velocity */
 } og_params;
 
 typedef struct {

@@ -75,6 +75,7 @@ class Params:
     lin_maxit_mom: int = 20
     lin_maxit_pp: int = 500
     lin_maxit_phi: int = 20
+    face_eps_upwind: int = 0      # DESIGN.md §3.12 (0: central face eps, reading Q9)
 
 
 def syamlal_obrien_beta(eps, slip, d_p=200e-6, rho_g=1.0, mu_g=1.8e-5):

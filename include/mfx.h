@@ -67,6 +67,8 @@ typedef struct {
     double tol;                 /* SIMPLE residual tolerance */
     double lin_tol_mom, lin_tol_pp, lin_tol_phi;
     int lin_maxit_mom, lin_maxit_pp, lin_maxit_phi;
+    int face_eps_upwind;        /* 0: central face eps in convective fluxes (reading Q9); 1: upwind cell
+                                   by the sign of the snapshot velocity (MFiX-style) */
 } mfx_params;
 
 /* Snapshot state (device pointers, N each).  Read-only to assembly; u, v, w,

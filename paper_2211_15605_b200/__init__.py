@@ -49,7 +49,8 @@ class Params(C.Structure):
                 ("g", C.c_double * 3), ("dt", C.c_double), ("urf_mom", C.c_double),
                 ("urf_p", C.c_double), ("urf_phi", C.c_double), ("tol", C.c_double),
                 ("lin_tol_mom", C.c_double), ("lin_tol_pp", C.c_double), ("lin_tol_phi", C.c_double),
-                ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int)]
+                ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int),
+                ("face_eps_upwind", C.c_int)]
 
 
 _DP = C.POINTER(C.c_double)
@@ -193,7 +194,7 @@ def c_grid(g) -> Grid:
 def c_params(p) -> Params:
     return Params(p.rho, p.mu, (C.c_double * 4)(*p.gamma_phi), (C.c_double * 3)(*p.g), p.dt, p.urf_mom,
                   p.urf_p, p.urf_phi, p.tol, p.lin_tol_mom, p.lin_tol_pp, p.lin_tol_phi,
-                  p.lin_maxit_mom, p.lin_maxit_pp, p.lin_maxit_phi)
+                  p.lin_maxit_mom, p.lin_maxit_pp, p.lin_maxit_phi, int(getattr(p, "face_eps_upwind", 0)))
 
 
 def _ptr(t, n=None):

@@ -48,6 +48,7 @@ __device__ __forceinline__ void latch(WsHeader *h, bool nonfinite, bool zerodiag
 // ------------------------------------------------------------------ momentum
 struct MomArgs {
     Geo G;
+    int upwind;                       // face_eps_upwind
     double rho, urf, gc, rVdt;
     double Dc[3];
     const double *eps, *eps0, *vel0, *vel1, *vel2, *uold, *p, *beta, *S;
@@ -248,8 +249,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
                     // +t face mass fluxes of Q and R: eps at X and X + e_t
                     const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
                     const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
-                    const double mQ = ((a.rho * (0.5 * (eQ0 + eQ1))) * G.A[t]) * vP[ti][sg];
-                    const double mR = ((a.rho * (0.5 * (eR0 + eR1))) * G.A[t]) * vE[ti][sg];
+                    const double efQ = a.upwind ? (vP[ti][sg] >= 0.0 ? eQ0 : eQ1) : 0.5 * (eQ0 + eQ1);
+                    const double efR = a.upwind ? (vE[ti][sg] >= 0.0 ? eR0 : eR1) : 0.5 * (eR0 + eR1);
+                    const double mQ = ((a.rho * efQ) * G.A[t]) * vP[ti][sg];
+                    const double mR = ((a.rho * efR) * G.A[t]) * vE[ti][sg];
                     const double F = 0.5 * (mQ + mR);
                     const double e4 = 0.25 * (((epsP + epsE) + epsPt[ti][sg]) + epsEt[ti][sg]);
                     const double D = a.Dc[t] * e4;
@@ -316,8 +319,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
 // ------------------------------------------------------------------ p'
 struct PPArgs {
     Geo G;
+    int upwind;
     double rho, rVdt;
     const double *eps, *eps0, *us[3], *dv[3];
+    const double *um[3];              // snapshot velocities (upwind direction, §3.12)
     const unsigned char *blocked;
     double *aP, *cx, *cy, *cz, *b;
     double *resid2;
@@ -365,7 +370,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
                 cpl[ax] = 0.0;
                 mp[ax] = 0.0;
             } else if (P[ax] <= ext - 2) {
-                const double ef = 0.5 * (epsP + eP[ax]);
+                const double ef = a.upwind ? (__ldg(a.um[ax] + n) >= 0.0 ? epsP : eP[ax]) : 0.5 * (epsP + eP[ax]);
                 cpl[ax] = ((a.rho * ef) * G.A[ax]) * dP[ax];
                 mp[ax] = ((a.rho * ef) * G.A[ax]) * uP[ax];
             } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET && !bP) {
@@ -380,7 +385,8 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
                 cm[ax] = 0.0;
                 mm[ax] = 0.0;
             } else if (P[ax] >= 1) {
-                const double ef = 0.5 * (eM[ax] + epsP);
+                const double ef = a.upwind ? (__ldg(a.um[ax] + lin_cl(G, Qm[0], Qm[1], Qm[2])) >= 0.0 ? eM[ax] : epsP)
+                                           : 0.5 * (eM[ax] + epsP);
                 cm[ax] = ((a.rho * ef) * G.A[ax]) * dM[ax];
                 mm[ax] = ((a.rho * ef) * G.A[ax]) * uM[ax];
             } else {
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
 // ------------------------------------------------------------------ scalar
 struct ScalArgs {
     Geo G;
+    int upwind;
     double rho, urf, rVdt;
     double Dc[3];
     const double *eps, *eps0, *vel[3], *phim, *phi0;
@@ -457,8 +464,11 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
                 int Q[3] = {P[0], P[1], P[2]};
                 Q[ax] -= 1;
                 const long long nQ = lin(G, Q);
-                const double e = 0.5 * (__ldg(a.eps + nQ) + epsP);
-                const double F = ((a.rho * e) * G.A[ax]) * __ldg(a.vel[ax] + nQ);
+                const double eQ = __ldg(a.eps + nQ);
+                const double e = 0.5 * (eQ + epsP);
+                const double vQ = __ldg(a.vel[ax] + nQ);
+                const double eu = a.upwind ? (vQ >= 0.0 ? eQ : epsP) : e;
+                const double F = ((a.rho * eu) * G.A[ax]) * vQ;
                 as[sm] = a.Dc[ax] * e + maxp(F);
                 kept[sm] = true; inP[sm] = true;
             } else if (ax == 2 && G.bc_zlo == MFX_BC_INLET) {
@@ -472,8 +482,11 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
             } else if (P[ax] <= extent(G, ax) - 2) {
                 int Q[3] = {P[0], P[1], P[2]};
                 Q[ax] += 1;
-                const double e = 0.5 * (epsP + __ldg(a.eps + lin(G, Q)));
-                const double F = ((a.rho * e) * G.A[ax]) * __ldg(a.vel[ax] + n);
+                const double eE = __ldg(a.eps + lin(G, Q));
+                const double e = 0.5 * (epsP + eE);
+                const double vP = __ldg(a.vel[ax] + n);
+                const double eu = a.upwind ? (vP >= 0.0 ? epsP : eE) : e;
+                const double F = ((a.rho * eu) * G.A[ax]) * vP;
                 as[sp] = a.Dc[ax] * e + maxp(-F);
                 kept[sp] = true; inP[sp] = true;
             } else if (ax == 2 && G.bc_zhi == MFX_BC_DIRICHLET_TEST) {
@@ -597,6 +610,7 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
                       "NULL eqsys array");
         MomArgs a;
         a.G = G;
+        a.upwind = pr->face_eps_upwind;
         a.rho = pr->rho;
         a.urf = pr->urf_mom;
         a.gc = pr->g[kind];
@@ -628,6 +642,9 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
                       "p' eqsys: aP,aE,aN,aT,b required and aW,aS,aB must be NULL");
         PPArgs a;
         a.G = G;
+        a.upwind = pr->face_eps_upwind;
+        MFX_ARG_CHECK(!a.upwind || (st->u && st->v && st->w), "upwind p' assembly needs the snapshot u, v, w");
+        a.um[0] = st->u; a.um[1] = st->v; a.um[2] = st->w;
         a.rho = pr->rho;
         a.rVdt = rVdt;
         a.eps = st->eps; a.eps0 = st->eps_old;
@@ -646,6 +663,7 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
                       "NULL eqsys array");
         ScalArgs a;
         a.G = G;
+        a.upwind = pr->face_eps_upwind;
         a.rho = pr->rho;
         a.urf = pr->urf_phi;
         a.rVdt = rVdt;

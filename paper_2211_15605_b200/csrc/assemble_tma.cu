@@ -24,6 +24,7 @@ namespace mfx {
 
 struct AsmMomArgs {
     int nx, ny, nz;
+    int upwind;                        // face_eps_upwind
     int tiles_x, tiles_y, Lz;
     long long units;
     int bc_zlo, bc_zhi;
@@ -249,8 +250,10 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                                 if (pt >= 0 && pt < ext[t]) {
                                     const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
                                     const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
-                                    const double mQ = ((a.rho * (0.5 * (eQ0 + eQ1))) * a.A[t]) * vP[ti][sg];
-                                    const double mR = ((a.rho * (0.5 * (eR0 + eR1))) * a.A[t]) * vE[ti][sg];
+                                    const double efQ = a.upwind ? (vP[ti][sg] >= 0.0 ? eQ0 : eQ1) : 0.5 * (eQ0 + eQ1);
+                                    const double efR = a.upwind ? (vE[ti][sg] >= 0.0 ? eR0 : eR1) : 0.5 * (eR0 + eR1);
+                                    const double mQ = ((a.rho * efQ) * a.A[t]) * vP[ti][sg];
+                                    const double mR = ((a.rho * efR) * a.A[t]) * vE[ti][sg];
                                     const double Fl = 0.5 * (mQ + mR);
                                     const double e4 = 0.25 * (((epsP + epsE) + epsPt[ti][sg]) + epsEt[ti][sg]);
                                     const double D = a.Dc[t] * e4;
@@ -387,6 +390,7 @@ mfx_status assemble_mom_tma(int kind, const Geo &G, const mfx_params *pr, const 
     AsmMomArgs a;
     memset(&a, 0, sizeof(a));
     a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
+    a.upwind = pr->face_eps_upwind;
     a.tiles_x = (G.nx + ATX - 1) / ATX;
     a.tiles_y = (G.ny + ATY - 1) / ATY;
     a.bc_zlo = G.bc_zlo; a.bc_zhi = G.bc_zhi;

@@ -330,9 +330,13 @@ struct PPArgs {
     dd *part;
 };
 
+// UP: upwinded convective face eps (§3.12); BL: BLOCKED cells (§3.10).  The
+// default <false, false> instantiation is the plain row of §3.4.
+template <bool UP, bool BL>
 __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
 {
-    // DESIGN.md §3.4; all 20 neighbour values loaded up front from clamped indices
+    // DESIGN.md §3.4; every neighbour value (and flag / snapshot velocity the
+    // variant needs) loaded up front from clamped indices
     const Geo &G = a.G;
     Acc cont;
     cont.zero();
@@ -341,7 +345,9 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
         int P[3];
         decode32(G, n, P);
         const double epsP = __ldg(a.eps + n), eps0P = __ldg(a.eps0 + n);
-        double eM[3], eP[3], dP[3], dM[3], uP[3], uM[3];
+        double eM[3], eP[3], dP[3], dM[3], uP[3], uM[3], vmP[3], vmM[3];
+        bool blP[3], blM[3];
+        const bool bP = BL ? __ldg(a.blocked + n) != 0 : false;
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
             int Qm[3] = {P[0], P[1], P[2]}, Qp[3] = {P[0], P[1], P[2]};
@@ -354,23 +360,23 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
             dM[ax] = __ldg(a.dv[ax] + im);
             uP[ax] = __ldg(a.us[ax] + n);
             uM[ax] = __ldg(a.us[ax] + im);
+            vmP[ax] = UP ? __ldg(a.um[ax] + n) : 0.0;
+            vmM[ax] = UP ? __ldg(a.um[ax] + im) : 0.0;
+            blP[ax] = BL ? (P[ax] < extent(G, ax) - 1 && __ldg(a.blocked + ip) != 0) : false;
+            blM[ax] = BL ? (P[ax] >= 1 && __ldg(a.blocked + im) != 0) : false;
         }
         double cm[3], cpl[3], mm[3], mp[3];
-        const bool bP = blk_q(G, a.blocked, P);
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
             const int ext = extent(G, ax);
-            int Qp[3] = {P[0], P[1], P[2]}, Qm[3] = {P[0], P[1], P[2]};
-            Qp[ax] += 1;
-            Qm[ax] -= 1;
-            const bool wall_p = bP || blk_q(G, a.blocked, Qp);             // §3.10 internal walls
-            const bool wall_m = bP || blk_q(G, a.blocked, Qm);
+            const bool wall_p = bP || blP[ax];                               // §3.10 internal walls
+            const bool wall_m = bP || blM[ax];
             // +a face of P
             if (P[ax] <= ext - 2 && wall_p) {
                 cpl[ax] = 0.0;
                 mp[ax] = 0.0;
             } else if (P[ax] <= ext - 2) {
-                const double ef = a.upwind ? (__ldg(a.um[ax] + n) >= 0.0 ? epsP : eP[ax]) : 0.5 * (epsP + eP[ax]);
+                const double ef = UP ? (vmP[ax] >= 0.0 ? epsP : eP[ax]) : 0.5 * (epsP + eP[ax]);
                 cpl[ax] = ((a.rho * ef) * G.A[ax]) * dP[ax];
                 mp[ax] = ((a.rho * ef) * G.A[ax]) * uP[ax];
             } else if (ax == 2 && G.bc_zhi == MFX_BC_OUTLET && !bP) {
@@ -385,8 +391,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble_pp(PPArgs a)
                 cm[ax] = 0.0;
                 mm[ax] = 0.0;
             } else if (P[ax] >= 1) {
-                const double ef = a.upwind ? (__ldg(a.um[ax] + lin_cl(G, Qm[0], Qm[1], Qm[2])) >= 0.0 ? eM[ax] : epsP)
-                                           : 0.5 * (eM[ax] + epsP);
+                const double ef = UP ? (vmM[ax] >= 0.0 ? eM[ax] : epsP) : 0.5 * (eM[ax] + epsP);
                 cm[ax] = ((a.rho * ef) * G.A[ax]) * dM[ax];
                 mm[ax] = ((a.rho * ef) * G.A[ax]) * uM[ax];
             } else {
@@ -653,7 +658,10 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.aP = out->aP; a.cx = out->aE; a.cy = out->aN; a.cz = out->aT; a.b = out->b;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
         count_launch(8, s, true);
-        k_assemble_pp<<<nb, kThreads, 0, s>>>(a);
+        if (a.upwind && a.blocked) k_assemble_pp<true, true><<<nb, kThreads, 0, s>>>(a);
+        else if (a.upwind) k_assemble_pp<true, false><<<nb, kThreads, 0, s>>>(a);
+        else if (a.blocked) k_assemble_pp<false, true><<<nb, kThreads, 0, s>>>(a);
+        else k_assemble_pp<false, false><<<nb, kThreads, 0, s>>>(a);
         count_launch(8, s, false);
     } else {
         MFX_ARG_CHECK(sid >= 0 && sid < 4, "scalar id %d", sid);

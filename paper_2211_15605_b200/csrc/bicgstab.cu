@@ -17,6 +17,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "bicg_state.cuh"
 
 namespace mfx {
 
@@ -131,41 +132,8 @@ __global__ void __launch_bounds__(kThreads) k_setup(Geo G, Coef c, const double 
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd v[2] = {bb.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(v, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
-        SolverScalars &s = h->sc;
-        const double bn = sqrt(dd_round(out[0]));
-        const double rrv = dd_round(out[1]);
-        s.tol = tol;
-        s.maxit = maxit;
-        s.bn = bn;
-        s.rr = rrv;
-        s.rn = sqrt(rrv);
-        s.it = 0;
-        s.status = MFX_NOT_CONVERGED;
-        s.done = 0;
-        s.restarted = 0;
-        s.restarts = 0;
-        s.restart_mode = 1;   // r^ = r, p = v = 0, rho = <r^,r> = rr (DESIGN.md §3.6 init)
-        s.skip = 0;
-        s.half = 0;
-        s.zero_x = 0;
-        s.rho = rrv;
-        s.rhn = s.rn;
-        s.rho_prev = 1.0;
-        s.alpha = 1.0;
-        s.omega = 1.0;
-        if (bn == 0.0) {
-            s.zero_x = 1;
-            s.done = 1;
-            s.status = MFX_OK;
-            s.rn = 0.0;
-        } else if (s.rn <= tol * bn) {
-            s.done = 1;
-            s.status = MFX_OK;
-        } else if (maxit <= 0) {
-            s.done = 1;
-        }
-    }
+    if (grid_reduce_dd<2>(v, part, &h->ticket[1], sh, out) && threadIdx.x == 0)
+        bicg_setup(h->sc, dd_round(out[0]), dd_round(out[1]), tol, maxit);
 }
 
 __global__ void k_zero_if(const WsHeader *h, double *x, long long N)
@@ -193,39 +161,6 @@ __device__ __forceinline__ double ldv(const double *p)
         return v;
     }
     return __ldg(p);
-}
-
-struct K1Pro {
-    double rho, rhn, beta, omega;
-    bool rst, newly, exit;
-};
-
-// K1 prologue: restart / breakdown decision (Q4).  exit: the
-// solve ended in a second breakdown (block 0 thread 0 has written the status).
-template <class SC>
-__device__ __forceinline__ K1Pro k1_prologue(SC &S)
-{
-    K1Pro o;
-    double rho = S.rho, rhn = S.rhn, rho_prev = S.rho_prev, alpha = S.alpha, omega = S.omega;
-    const double rn = S.rn, rr = S.rr;
-    const int restarted = S.restarted;
-    bool rst = S.restart_mode != 0;
-    o.newly = false;
-    o.exit = false;
-    if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
-    if (fabs(rho) <= (1e-14 * rhn) * rn) {
-        if (restarted) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) { S.status = MFX_ERR_BREAKDOWN; S.done = 1; }
-            o.exit = true;
-            return o;
-        }
-        rst = true;
-        o.newly = true;
-        rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
-    }
-    o.rho = rho; o.rhn = rhn; o.omega = omega; o.rst = rst;
-    o.beta = (rho / rho_prev) * (alpha / omega);
-    return o;
 }
 
 template <bool SYM, bool CG>
@@ -256,29 +191,6 @@ __device__ __forceinline__ void k1_body(const Geo &G, const Coef &c, const doubl
     }
 }
 
-template <class SC>
-__device__ __forceinline__ void k1_tail(SC &S, const K1Pro &P, dd sigma_dd)
-{
-    if (P.rst) {
-        S.rho = P.rho; S.rhn = P.rhn; S.rho_prev = 1.0; S.alpha = 1.0; S.omega = 1.0;
-    }
-    if (P.newly) { S.restarted = 1; S.restarts += 1; }
-    S.restart_mode = 0;
-    S.skip = 0;
-    const double sigma = dd_round(sigma_dd);
-    S.sigma = sigma;
-    if (sigma == 0.0) {
-        if (S.restarted) {
-            S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
-        } else {
-            S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-            if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-        }
-    } else {
-        S.alpha = P.rho / sigma;
-    }
-}
-
 template <bool SYM>
 __global__ void __launch_bounds__(kThreads) k1(Geo G, Coef c, const double *__restrict__ r, double *rh,
                                               const double *__restrict__ p_old, const double *__restrict__ v_old,
@@ -286,15 +198,18 @@ __global__ void __launch_bounds__(kThreads) k1(Geo G, Coef c, const double *__re
 {
     SolverScalars &S = h->sc;
     if (S.done) return;
-    const K1Pro P = k1_prologue(S);
-    if (P.exit) return;
+    const K1Pro P = bicg_k1_prologue(S);
+    if (P.breakdown) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) bicg_breakdown(S);
+        return;
+    }
     Acc sg;
     sg.zero();
     k1_body<SYM, false>(G, c, r, rh, p_old, v_old, p_new, v_new, P, sg,
                         (long long)blockIdx.x * blockDim.x + threadIdx.x, G.N, (long long)gridDim.x * blockDim.x);
     __shared__ dd sh[(kThreads / 32) * 1];
     dd vv[1] = {sg.get()}, out[1];
-    if (grid_reduce_dd<1>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k1_tail(S, P, out[0]);
+    if (grid_reduce_dd<1>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) bicg_k1_tail(S, P, dd_round(out[0]));
 }
 
 // ------------------------------------------------------------------ K2
@@ -316,28 +231,6 @@ __device__ __forceinline__ void k2_body(const Geo &G, const Coef &c, const doubl
     }
 }
 
-template <class SC>
-__device__ __forceinline__ void k2_tail(SC &S, const dd (&out)[3])
-{
-    const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
-    S.ts = tsv; S.tt = ttv; S.ss = ssv;
-    if (sqrt(ssv) <= S.tol * S.bn) {
-        S.half = 1;
-    } else {
-        const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
-        if (ttv == 0.0 || om == 0.0) {
-            if (S.restarted) {
-                S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1;
-            } else {
-                S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-                if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-            }
-        } else {
-            S.omega = om;
-        }
-    }
-}
-
 template <bool SYM>
 __global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__restrict__ r,
                                               const double *__restrict__ v, double *t, WsHeader *h, dd *part)
@@ -350,7 +243,8 @@ __global__ void __launch_bounds__(kThreads) k2(Geo G, Coef c, const double *__re
                         (long long)gridDim.x * blockDim.x);
     __shared__ dd sh[(kThreads / 32) * 3];
     dd vv[3] = {ts.get(), tt.get(), ss.get()}, out[3];
-    if (grid_reduce_dd<3>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k2_tail(S, out);
+    if (grid_reduce_dd<3>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0)
+        bicg_k2_tail(S, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
 }
 
 // ------------------------------------------------------------------ K3
@@ -376,24 +270,6 @@ __device__ __forceinline__ void k3_body(double *x, double *r, const double *rh, 
     }
 }
 
-template <class SC>
-__device__ __forceinline__ void k3_tail(SC &S, bool half, const dd (&out)[2])
-{
-    S.it += 1;
-    if (half) {
-        S.rn = sqrt(S.ss);
-        S.status = MFX_OK;
-        S.done = 1;
-    } else {
-        S.rho_prev = S.rho;
-        S.rho = dd_round(out[0]);
-        S.rr = dd_round(out[1]);
-        S.rn = sqrt(S.rr);
-        if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
-        else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-    }
-}
-
 __global__ void __launch_bounds__(kThreads) k3(Geo G, double *x, double *r, const double *__restrict__ rh,
                                               const double *__restrict__ p, const double *__restrict__ v,
                                               const double *__restrict__ t, WsHeader *h, dd *part)
@@ -407,7 +283,8 @@ __global__ void __launch_bounds__(kThreads) k3(Geo G, double *x, double *r, cons
                    (long long)blockIdx.x * blockDim.x + threadIdx.x, G.N, (long long)gridDim.x * blockDim.x);
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k3_tail(S, half, out);
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0)
+        bicg_k3_tail(S, half, dd_round(out[0]), dd_round(out[1]));
 }
 
 // K3, streaming form used with the TMA path: x fastest and nx even, so every
@@ -486,7 +363,8 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) k3_tail(S, half, out);
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0)
+        bicg_k3_tail(S, half, dd_round(out[0]), dd_round(out[1]));
 }
 
 // ------------------------------------------------------------------ grid-synchronous persistent solver
@@ -584,9 +462,12 @@ __global__ void __launch_bounds__(kThreads) k_bicg_grid(Geo G, Coef c, double *x
         SolverScalars L = sc_load(Sg);
         if (L.done) break;
         // ---- K1
-        const K1Pro P = k1_prologue(L);
-        if (P.exit) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) sc_store(Sg, L);
+        const K1Pro P = bicg_k1_prologue(L);
+        if (P.breakdown) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                bicg_breakdown(L);
+                sc_store(Sg, L);
+            }
             break;
         }
         double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
@@ -598,7 +479,7 @@ __global__ void __launch_bounds__(kThreads) k_bicg_grid(Geo G, Coef c, double *x
             dd vv[1] = {sg.get()};
             grid_sync_reduce<1>(vv, part, ticket, gen, sh, [&](dd (&o)[1]) {
                 SolverScalars T = sc_load(Sg);
-                k1_tail(T, P, o[0]);
+                bicg_k1_tail(T, P, dd_round(o[0]));
                 sc_store(Sg, T);
             });
         }
@@ -613,7 +494,7 @@ __global__ void __launch_bounds__(kThreads) k_bicg_grid(Geo G, Coef c, double *x
             dd vv[3] = {ts.get(), tt.get(), ss.get()};
             grid_sync_reduce<3>(vv, part, ticket, gen, sh, [&](dd (&o)[3]) {
                 SolverScalars T = sc_load(Sg);
-                k2_tail(T, o);
+                bicg_k2_tail(T, dd_round(o[0]), dd_round(o[1]), dd_round(o[2]));
                 sc_store(Sg, T);
             });
         }
@@ -628,7 +509,7 @@ __global__ void __launch_bounds__(kThreads) k_bicg_grid(Geo G, Coef c, double *x
             dd vv[2] = {rhr.get(), rr.get()};
             grid_sync_reduce<2>(vv, part, ticket, gen, sh, [&](dd (&o)[2]) {
                 SolverScalars T = sc_load(Sg);
-                k3_tail(T, half, o);
+                bicg_k3_tail(T, half, dd_round(o[0]), dd_round(o[1]));
                 sc_store(Sg, T);
             });
         }

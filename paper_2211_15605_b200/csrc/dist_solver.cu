@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "bicg_state.cuh"
 
 namespace mfx {
 
@@ -120,16 +121,7 @@ __global__ void __launch_bounds__(kT) dk_setup(DSlab D, DCoef c, const double *c
 __global__ void dk_fold_setup(WsHeader *h, const dd *all, int R, double tol, int maxit)
 {
     if (threadIdx.x != 0) return;
-    SolverScalars &s = h->sc;
-    const double bn = sqrt(fold_ranks(all, R, 2, 0));
-    const double rrv = fold_ranks(all, R, 2, 1);
-    s.tol = tol; s.maxit = maxit; s.bn = bn; s.rr = rrv; s.rn = sqrt(rrv);
-    s.it = 0; s.status = MFX_NOT_CONVERGED; s.done = 0; s.restarted = 0; s.restarts = 0;
-    s.restart_mode = 1; s.skip = 0; s.half = 0; s.zero_x = 0;
-    s.rho = rrv; s.rhn = s.rn; s.rho_prev = 1.0; s.alpha = 1.0; s.omega = 1.0;
-    if (bn == 0.0) { s.zero_x = 1; s.done = 1; s.status = MFX_OK; s.rn = 0.0; }
-    else if (s.rn <= tol * bn) { s.done = 1; s.status = MFX_OK; }
-    else if (maxit <= 0) { s.done = 1; }
+    bicg_setup(h->sc, fold_ranks(all, R, 2, 0), fold_ranks(all, R, 2, 1), tol, maxit);
 }
 
 __global__ void dk_zero_if(DSlab D, const WsHeader *h, double *x)
@@ -138,41 +130,14 @@ __global__ void dk_zero_if(DSlab D, const WsHeader *h, double *x)
     SLAB_LOOP(n) x[n] = 0.0;
 }
 
-// K1 prologue decision, shared by dk_p and dk_fold_sigma
-struct K1Decision {
-    double rho, rhn, beta, omega;
-    bool rst, newly, breakdown;
-};
-__device__ __forceinline__ K1Decision k1_decide(const SolverScalars &S)
-{
-    K1Decision d;
-    d.rho = S.rho; d.rhn = S.rhn;
-    double rho_prev = S.rho_prev, alpha = S.alpha;
-    d.omega = S.omega;
-    const double rn = S.rn, rr = S.rr;
-    d.rst = S.restart_mode != 0;
-    d.newly = false;
-    d.breakdown = false;
-    if (d.rst) { d.rho = rr; d.rhn = rn; rho_prev = 1.0; alpha = 1.0; d.omega = 1.0; }
-    if (fabs(d.rho) <= (1e-14 * d.rhn) * rn) {
-        if (S.restarted) { d.breakdown = true; }
-        else {
-            d.rst = true; d.newly = true;
-            d.rho = rr; d.rhn = rn; rho_prev = 1.0; alpha = 1.0; d.omega = 1.0;
-        }
-    }
-    d.beta = (d.rho / rho_prev) * (alpha / d.omega);
-    return d;
-}
-
 __global__ void __launch_bounds__(kT) dk_p(DSlab D, const double *r, double *rh, double *p, const double *v,
                                            WsHeader *h)
 {
     SolverScalars &S = h->sc;
     if (S.done) return;
-    const K1Decision d = k1_decide(S);
+    const K1Pro d = bicg_k1_prologue(S);
     if (d.breakdown) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) { S.status = MFX_ERR_BREAKDOWN; S.done = 1; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) bicg_breakdown(S);
         return;
     }
     SLAB_LOOP(n) {
@@ -206,22 +171,8 @@ __global__ void dk_fold_sigma(WsHeader *h, const dd *all, int R)
     if (threadIdx.x != 0) return;
     SolverScalars &S = h->sc;
     if (S.done) return;
-    const K1Decision d = k1_decide(S);
-    if (d.rst) { S.rho = d.rho; S.rhn = d.rhn; S.rho_prev = 1.0; S.alpha = 1.0; S.omega = 1.0; }
-    if (d.newly) { S.restarted = 1; S.restarts += 1; }
-    S.restart_mode = 0;
-    S.skip = 0;
-    const double sigma = fold_ranks(all, R, 1, 0);
-    S.sigma = sigma;
-    if (sigma == 0.0) {
-        if (S.restarted) { S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1; }
-        else {
-            S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-            if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-        }
-    } else {
-        S.alpha = d.rho / sigma;
-    }
+    const K1Pro d = bicg_k1_prologue(S);
+    bicg_k1_tail(S, d, fold_ranks(all, R, 1, 0));
 }
 
 __global__ void __launch_bounds__(kT) dk_s(DSlab D, const double *r, const double *v, double *s, const WsHeader *h)
@@ -257,22 +208,7 @@ __global__ void dk_fold_t(WsHeader *h, const dd *all, int R)
     if (threadIdx.x != 0) return;
     SolverScalars &S = h->sc;
     if (S.done || S.skip) return;
-    const double tsv = fold_ranks(all, R, 3, 0), ttv = fold_ranks(all, R, 3, 1), ssv = fold_ranks(all, R, 3, 2);
-    S.ts = tsv; S.tt = ttv; S.ss = ssv;
-    if (sqrt(ssv) <= S.tol * S.bn) {
-        S.half = 1;
-    } else {
-        const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
-        if (ttv == 0.0 || om == 0.0) {
-            if (S.restarted) { S.status = MFX_ERR_BREAKDOWN; S.it += 1; S.done = 1; }
-            else {
-                S.restarted = 1; S.restarts += 1; S.restart_mode = 1; S.skip = 1; S.it += 1;
-                if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
-            }
-        } else {
-            S.omega = om;
-        }
-    }
+    bicg_k2_tail(S, fold_ranks(all, R, 3, 0), fold_ranks(all, R, 3, 1), fold_ranks(all, R, 3, 2));
 }
 
 __global__ void __launch_bounds__(kT) dk_k3(DSlab D, double *x, double *r, const double *rh, const double *p,
@@ -307,19 +243,8 @@ __global__ void dk_fold_r(WsHeader *h, const dd *all, int R)
     if (threadIdx.x != 0) return;
     SolverScalars &S = h->sc;
     if (S.done || S.skip) return;
-    S.it += 1;
-    if (S.half) {
-        S.rn = sqrt(S.ss);
-        S.status = MFX_OK;
-        S.done = 1;
-        return;
-    }
-    S.rho_prev = S.rho;
-    S.rho = fold_ranks(all, R, 2, 0);
-    S.rr = fold_ranks(all, R, 2, 1);
-    S.rn = sqrt(S.rr);
-    if (S.rn <= S.tol * S.bn) { S.status = MFX_OK; S.done = 1; }
-    else if (S.it >= S.maxit) { S.status = MFX_NOT_CONVERGED; S.done = 1; }
+    const bool half = S.half != 0;
+    bicg_k3_tail(S, half, half ? 0.0 : fold_ranks(all, R, 2, 0), half ? 0.0 : fold_ranks(all, R, 2, 1));
 }
 
 int dgrid(long long n)

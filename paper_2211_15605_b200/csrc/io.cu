@@ -107,7 +107,7 @@ mfx_status state_dump(const char *path, const mfx_grid *grid, const mfx_state *s
     for (auto &fr : fields) {
         TableEntry e;
         memset(&e, 0, sizeof(e));
-        strncpy(e.name, fr.name, sizeof(e.name));
+        memcpy(e.name, fr.name, strnlen(fr.name, sizeof(e.name)));   // NUL padded by the memset
         e.kind = (uint8_t)fr.kind;
         ok = ok && fwrite(&e, sizeof(e), 1, F.f) == 1;
     }

@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "tma.cuh"
+#include "bicg_state.cuh"
 
 namespace mfx {
 
@@ -190,28 +191,23 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     pdl_wait();
 
     // ---- scalar prologue (uniform across the grid)
-    double beta = 0.0, omega = 0.0, alpha = 0.0, rho = 0.0, rhn = 0.0;
-    bool rst = false, newly = false;
+    double beta = 0.0, omega = 0.0, alpha = 0.0;
+    bool rst = false;
+    K1Pro P1;
+    P1.rst = false;
     if (MODE == SM_K1 || MODE == SM_K2) {
         SolverScalars &Sc = a.h->sc;
         if (Sc.done) return;
         if (MODE == SM_K2 && Sc.skip) return;
         if (MODE == SM_K1) {
-            rho = Sc.rho; rhn = Sc.rhn;
-            double rho_prev = Sc.rho_prev;
-            alpha = Sc.alpha; omega = Sc.omega;
-            const double rn = Sc.rn, rr = Sc.rr;
-            rst = Sc.restart_mode != 0;
-            if (rst) { rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0; }
-            if (fabs(rho) <= (1e-14 * rhn) * rn) {
-                if (Sc.restarted) {
-                    if (blockIdx.x == 0 && tid == 0) { Sc.status = MFX_ERR_BREAKDOWN; Sc.done = 1; }
-                    return;
-                }
-                rst = true; newly = true;
-                rho = rr; rhn = rn; rho_prev = 1.0; alpha = 1.0; omega = 1.0;
+            P1 = bicg_k1_prologue(Sc);           // DESIGN.md §3.6 restart / breakdown decision
+            if (P1.breakdown) {
+                if (blockIdx.x == 0 && tid == 0) bicg_breakdown(Sc);
+                return;
             }
-            beta = (rho / rho_prev) * (alpha / omega);
+            rst = P1.rst;
+            beta = P1.beta;
+            omega = P1.omega;
         } else {
             alpha = Sc.alpha;
         }
@@ -470,50 +466,9 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     }
     if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
     SolverScalars &Sc = a.h->sc;
-    if (MODE == SM_SETUP) {
-        const double bn = sqrt(dd_round(out[0]));
-        const double rrv = dd_round(out[1]);
-        Sc.tol = a.tol; Sc.maxit = a.maxit; Sc.bn = bn; Sc.rr = rrv; Sc.rn = sqrt(rrv);
-        Sc.it = 0; Sc.status = MFX_NOT_CONVERGED; Sc.done = 0; Sc.restarted = 0; Sc.restarts = 0;
-        Sc.restart_mode = 1; Sc.skip = 0; Sc.half = 0; Sc.zero_x = 0;
-        Sc.rho = rrv; Sc.rhn = Sc.rn; Sc.rho_prev = 1.0; Sc.alpha = 1.0; Sc.omega = 1.0;
-        if (bn == 0.0) { Sc.zero_x = 1; Sc.done = 1; Sc.status = MFX_OK; Sc.rn = 0.0; }
-        else if (Sc.rn <= a.tol * bn) { Sc.done = 1; Sc.status = MFX_OK; }
-        else if (a.maxit <= 0) { Sc.done = 1; }
-    } else if (MODE == SM_K1) {
-        if (rst) { Sc.rho = rho; Sc.rhn = rhn; Sc.rho_prev = 1.0; Sc.alpha = 1.0; Sc.omega = 1.0; }
-        if (newly) { Sc.restarted = 1; Sc.restarts += 1; }
-        Sc.restart_mode = 0;
-        Sc.skip = 0;
-        const double sigma = dd_round(out[0]);
-        Sc.sigma = sigma;
-        if (sigma == 0.0) {
-            if (Sc.restarted) { Sc.status = MFX_ERR_BREAKDOWN; Sc.it += 1; Sc.done = 1; }
-            else {
-                Sc.restarted = 1; Sc.restarts += 1; Sc.restart_mode = 1; Sc.skip = 1; Sc.it += 1;
-                if (Sc.it >= Sc.maxit) { Sc.status = MFX_NOT_CONVERGED; Sc.done = 1; }
-            }
-        } else {
-            Sc.alpha = rho / sigma;
-        }
-    } else if (MODE == SM_K2) {
-        const double tsv = dd_round(out[0]), ttv = dd_round(out[1]), ssv = dd_round(out[2]);
-        Sc.ts = tsv; Sc.tt = ttv; Sc.ss = ssv;
-        if (sqrt(ssv) <= Sc.tol * Sc.bn) {
-            Sc.half = 1;
-        } else {
-            const double om = ttv == 0.0 ? 0.0 : tsv / ttv;
-            if (ttv == 0.0 || om == 0.0) {
-                if (Sc.restarted) { Sc.status = MFX_ERR_BREAKDOWN; Sc.it += 1; Sc.done = 1; }
-                else {
-                    Sc.restarted = 1; Sc.restarts += 1; Sc.restart_mode = 1; Sc.skip = 1; Sc.it += 1;
-                    if (Sc.it >= Sc.maxit) { Sc.status = MFX_NOT_CONVERGED; Sc.done = 1; }
-                }
-            } else {
-                Sc.omega = om;
-            }
-        }
-    }
+    if (MODE == SM_SETUP) bicg_setup(Sc, dd_round(out[0]), dd_round(out[1]), a.tol, a.maxit);
+    else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
+    else if (MODE == SM_K2) bicg_k2_tail(Sc, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
 }
 
 // ------------------------------------------------------------------ host side

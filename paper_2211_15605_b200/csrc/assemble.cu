@@ -8,6 +8,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "mom_row.cuh"
 
 namespace mfx {
 
@@ -48,6 +49,7 @@ __device__ __forceinline__ void latch(WsHeader *h, bool nonfinite, bool zerodiag
 // ------------------------------------------------------------------ momentum
 struct MomArgs {
     Geo G;
+    MomRowPar R;                      // row constants (mom_row.cuh)
     int upwind;                       // face_eps_upwind
     double rho, urf, gc, rVdt;
     double Dc[3];
@@ -58,8 +60,6 @@ struct MomArgs {
     WsHeader *hdr;
     dd *part;
 };
-
-enum { kInterior = 0, kIdentity = 1, kOutlet = 2 };
 
 // §3.10: cell (i, j, k) is BLOCKED (outside the domain: not blocked)
 __device__ __forceinline__ bool blk_at(const Geo &G, const unsigned char *bl, int i, int j, int k)
@@ -162,9 +162,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
         int E[3] = {P[0], P[1], P[2]};
         if (type == kInterior) E[C] += 1;
         const long long nE = lin(G, E);
-        // ---- gather
-        const double epsP = __ldg(a.eps + n), epsE = __ldg(a.eps + nE);
-        double epsPt[2][2], epsEt[2][2], vP[2][2], vE[2][2];   // [transverse t][side: 0 = -, 1 = +]
+        // ---- gather (every value the row can need, from clamped indices)
+        MomRowIn in;
+        in.P[0] = P[0]; in.P[1] = P[1]; in.P[2] = P[2];
+        in.type = type;
+        in.epsP = __ldg(a.eps + n);
+        in.epsE = __ldg(a.eps + nE);
 #pragma unroll
         for (int ti = 0; ti < 2; ti++) {
             const int t = ti == 0 ? T1 : T2;
@@ -175,138 +178,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
                 Pt[t] += s;
                 Et[t] += s;
                 const long long iP = lin_cl(G, Pt[0], Pt[1], Pt[2]), iE = lin_cl(G, Et[0], Et[1], Et[2]);
-                epsPt[ti][sg] = __ldg(a.eps + iP);
-                epsEt[ti][sg] = __ldg(a.eps + iE);
+                in.epsPt[ti][sg] = __ldg(a.eps + iP);
+                in.epsEt[ti][sg] = __ldg(a.eps + iE);
                 // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
-                vP[ti][sg] = __ldg(vt[ti] + (s > 0 ? n : iP));
-                vE[ti][sg] = __ldg(vt[ti] + (s > 0 ? nE : iE));
+                in.vP[ti][sg] = __ldg(vt[ti] + (s > 0 ? n : iP));
+                in.vE[ti][sg] = __ldg(vt[ti] + (s > 0 ? nE : iE));
+                const int pt = P[t] + s;
+                in.nb_wall[ti][sg] = a.blocked && pt >= 0 && pt < extent(G, t) &&
+                                     (blk_q(G, a.blocked, Pt) || blk_q(G, a.blocked, Et));   // §3.10
             }
         }
         int Pm[3] = {P[0], P[1], P[2]};
         Pm[C] -= 1;
-        const double umP = __ldg(um + n);
-        const double umE = __ldg(um + nE);
-        const double umM = __ldg(um + lin_cl(G, Pm[0], Pm[1], Pm[2]));
-        double unb[6];                                            // residual neighbours W,E,S,N,B,T
+        in.umP = __ldg(um + n);
+        in.umE = __ldg(um + nE);
+        in.umM = __ldg(um + lin_cl(G, Pm[0], Pm[1], Pm[2]));
 #pragma unroll
         for (int s6 = 0; s6 < 6; s6++) {
             int Q[3] = {P[0], P[1], P[2]};
             Q[s6 / 2] += (s6 & 1) ? 1 : -1;
-            unb[s6] = in_dom(G, Q) ? __ldg(um + lin_cl(G, Q[0], Q[1], Q[2])) : 0.0;
+            in.unb[s6] = in_dom(G, Q) ? __ldg(um + lin_cl(G, Q[0], Q[1], Q[2])) : 0.0;
         }
-        const double e0P = __ldg(a.eps0 + n), e0E = __ldg(a.eps0 + nE);
-        const double bP = __ldg(a.beta + n), bE = __ldg(a.beta + nE);
-        const double SP = __ldg(a.S + n), SE = __ldg(a.S + nE);
-        const double pP = __ldg(a.p + n), pEv = __ldg(a.p + nE);
-        const double uoP = __ldg(a.uold + n);
+        in.e0P = __ldg(a.eps0 + n); in.e0E = __ldg(a.eps0 + nE);
+        in.bP = __ldg(a.beta + n); in.bE = __ldg(a.beta + nE);
+        in.SP = __ldg(a.S + n); in.SE = __ldg(a.S + nE);
+        in.pP = __ldg(a.p + n); in.pEv = __ldg(a.p + nE);
+        in.uoP = __ldg(a.uold + n);
+        in.m_wall = P[C] >= 1 && blk_q(G, a.blocked, Pm);                    // internal wall face (§3.10)
+        in.e_ident = type != kOutlet && row_type<C>(G, E, a.blocked) == kIdentity;
 
-        // ---- row (same expressions as DESIGN.md §3.3)
-        double as[6], phib[6];
-        bool kept[6], inP[6];
-#pragma unroll
-        for (int s6 = 0; s6 < 6; s6++) { as[s6] = 0.0; phib[s6] = 0.0; kept[s6] = false; inP[s6] = false; }
-        {
-            // main axis
-            double vm;
-            const bool m_wall = P[C] >= 1 && blk_q(G, a.blocked, Pm);       // internal wall face (§3.10)
-            if (P[C] == 0) vm = (C == 2 && G.bc_zlo == MFX_BC_INLET) ? G.w_in : 0.0;
-            else vm = m_wall ? 0.0 : umM;
-            const double Fm = ((a.rho * epsP) * G.A[C]) * (0.5 * (vm + umP));
-            const double Dm = a.Dc[C] * epsP;
-            as[2 * C] = Dm + maxp(Fm);
-            inP[2 * C] = true;
-            if (P[C] >= 1 && !m_wall) kept[2 * C] = true;
-            else phib[2 * C] = vm;                                            // B1
-            if (type == kOutlet) {
-                as[2 * C + 1] = 0.0;                                          // B3
-            } else {
-                const bool e_ident = row_type<C>(G, E, a.blocked) == kIdentity;
-                const double vE_ = e_ident ? 0.0 : umE;
-                const double Fp = ((a.rho * epsE) * G.A[C]) * (0.5 * (umP + vE_));
-                const double Dp = a.Dc[C] * epsE;
-                as[2 * C + 1] = Dp + maxp(-Fp);
-                inP[2 * C + 1] = true;
-                if (e_ident) phib[2 * C + 1] = 0.0;                           // B1
-                else kept[2 * C + 1] = true;
-            }
-        }
-#pragma unroll
-        for (int ti = 0; ti < 2; ti++) {
-            const int t = ti == 0 ? T1 : T2;
-#pragma unroll
-            for (int sg = 0; sg < 2; sg++) {
-                const int s = sg ? 1 : -1;
-                const int side = 2 * t + sg;
-                const int pt = P[t] + s;
-                bool nb_wall = false;                                          // §3.10
-                if (a.blocked && pt >= 0 && pt < extent(G, t)) {
-                    int Pt[3] = {P[0], P[1], P[2]}, Et[3] = {E[0], E[1], E[2]};
-                    Pt[t] += s;
-                    Et[t] += s;
-                    nb_wall = blk_q(G, a.blocked, Pt) || blk_q(G, a.blocked, Et);
-                }
-                if (pt >= 0 && pt < extent(G, t) && !nb_wall) {
-                    // +t face mass fluxes of Q and R: eps at X and X + e_t
-                    const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
-                    const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
-                    const double efQ = a.upwind ? (vP[ti][sg] >= 0.0 ? eQ0 : eQ1) : 0.5 * (eQ0 + eQ1);
-                    const double efR = a.upwind ? (vE[ti][sg] >= 0.0 ? eR0 : eR1) : 0.5 * (eR0 + eR1);
-                    const double mQ = ((a.rho * efQ) * G.A[t]) * vP[ti][sg];
-                    const double mR = ((a.rho * efR) * G.A[t]) * vE[ti][sg];
-                    const double F = 0.5 * (mQ + mR);
-                    const double e4 = 0.25 * (((epsP + epsE) + epsPt[ti][sg]) + epsEt[ti][sg]);
-                    const double D = a.Dc[t] * e4;
-                    as[side] = D + maxp(s > 0 ? -F : F);
-                    inP[side] = true;
-                    kept[side] = true;
-                } else {
-                    int bc = MFX_BC_WALL;                                      // domain or internal wall
-                    if (t == 2 && !nb_wall) bc = s < 0 ? G.bc_zlo : G.bc_zhi;
-                    if (bc == MFX_BC_OUTLET) continue;                        // B3
-                    double F = 0.0;
-                    if (bc == MFX_BC_INLET)
-                        F = 0.5 * (((a.rho * epsP) * G.A[2]) * G.w_in + ((a.rho * epsE) * G.A[2]) * G.w_in);
-                    const double e2 = 0.5 * (epsP + epsE);
-                    const double D = a.Dc[t] * e2;
-                    as[side] = 2.0 * D + maxp(s > 0 ? -F : F);                // B2, phi_b = 0
-                    inP[side] = true;
-                    phib[side] = 0.0;
-                }
-            }
-        }
-        const double sum = ((((as[0] + as[1]) + as[2]) + as[3]) + as[4]) + as[5];
-        double bcb = 0.0;
-#pragma unroll
-        for (int s6 = 0; s6 < 6; s6++)
-            if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
-        const double ef = 0.5 * (epsP + epsE);
-        const double e0f = 0.5 * (e0P + e0E);
-        const double bf = 0.5 * (bP + bE);
-        const double Sf = 0.5 * (SP + SE);
-        const double pE = type == kOutlet ? 0.0 : pEv;
-        const double a0 = a.rVdt * e0f;
-        const double aP = (sum + a0) + bf * G.V;
-        const double bb = ((((a0 * uoP) + (ef * G.A[C]) * (pP - pE)) + ((a.rho * ef) * a.gc) * G.V) + Sf * G.V) + bcb;
-        const double aPr = aP / a.urf;
-        const double bR = bb + (aPr - aP) * umP;
-        const double dd_ = (ef * G.A[C]) / aPr;
-        double st6[6];
-#pragma unroll
-        for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? as[s6] : 0.0;
-        a.aW[n] = st6[0]; a.aE[n] = st6[1];
-        a.aS[n] = st6[2]; a.aN[n] = st6[3];
-        a.aB[n] = st6[4]; a.aT[n] = st6[5];
-        a.aP[n] = aPr;
-        a.b[n] = bR;
-        a.d[n] = dd_;
-        const bool nonfin = !isfinite(aPr) || !isfinite(bR) || !isfinite(dd_);
-        if (nonfin || aPr == 0.0) latch(a.hdr, nonfin, aPr == 0.0, n);
-
-        double res = bb - aP * umP;
-#pragma unroll
-        for (int s6 = 0; s6 < 6; s6++) res = res + st6[s6] * unb[s6];
-        num.add(fabs(res));
-        den.add(fabs(aP * umP));
+        // ---- row (mom_row.cuh)
+        MomRowOut o;
+        mom_row<C>(a.R, in, o);
+        a.aW[n] = o.st6[0]; a.aE[n] = o.st6[1];
+        a.aS[n] = o.st6[2]; a.aN[n] = o.st6[3];
+        a.aB[n] = o.st6[4]; a.aT[n] = o.st6[5];
+        a.aP[n] = o.aPr;
+        a.b[n] = o.bR;
+        a.d[n] = o.d;
+        const bool nonfin = !isfinite(o.aPr) || !isfinite(o.bR) || !isfinite(o.d);
+        if (nonfin || o.aPr == 0.0) latch(a.hdr, nonfin, o.aPr == 0.0, n);
+        num.add(o.res);
+        den.add(o.den);
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd v[2] = {num.get(), den.get()}, out[2];
@@ -621,6 +534,11 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.gc = pr->g[kind];
         a.rVdt = rVdt;
         for (int t = 0; t < 3; t++) a.Dc[t] = (pr->mu * G.A[t]) / G.h[t];
+        a.R.ext[0] = G.nx; a.R.ext[1] = G.ny; a.R.ext[2] = G.nz;
+        a.R.bc_zlo = G.bc_zlo; a.R.bc_zhi = G.bc_zhi; a.R.upwind = pr->face_eps_upwind;
+        a.R.w_in = G.w_in; a.R.V = G.V;
+        a.R.rho = pr->rho; a.R.urf = pr->urf_mom; a.R.gc = pr->g[kind]; a.R.rVdt = rVdt;
+        for (int t = 0; t < 3; t++) { a.R.A[t] = G.A[t]; a.R.Dc[t] = a.Dc[t]; }
         a.eps = st->eps; a.eps0 = st->eps_old;
         a.vel0 = st->u; a.vel1 = st->v; a.vel2 = st->w;
         a.uold = kind == 0 ? st->u_old : (kind == 1 ? st->v_old : st->w_old);

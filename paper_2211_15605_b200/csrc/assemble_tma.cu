@@ -19,10 +19,12 @@
 
 #include "common.cuh"
 #include "tma.cuh"
+#include "mom_row.cuh"
 
 namespace mfx {
 
 struct AsmMomArgs {
+    MomRowPar R;                       // row constants (mom_row.cuh)
     int nx, ny, nz;
     int upwind;                        // face_eps_upwind
     int tiles_x, tiles_y, Lz;
@@ -52,8 +54,6 @@ constexpr int ABOX_B = (ABOX * 8 + 127) & ~127;
 constexpr int ASTAGE_B = 4 * ABOX_B;
 constexpr int ASTAGE_TX = 4 * ABOX * 8;
 constexpr int AS = 6;                            // stages: planes k-1, k, k+1 resident + 3 ahead
-
-__device__ __forceinline__ double maxp_t(double f) { return f > 0.0 ? f : 0.0; }
 
 struct ACursor {
     int u, units, G, ntiles, Lz, tiles_x;
@@ -178,8 +178,11 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                     } else {
                         int e[3] = {0, 0, 0};
                         e[C] = oE;                                   // E = P + e (E = P on the outlet row)
-                        const double epsP = F(0, 0, 0, 0), epsE = F(0, e[0], e[1], e[2]);
-                        double epsPt[2][2], epsEt[2][2], vP[2][2], vE[2][2];
+                        MomRowIn in;
+                        in.P[0] = P[0]; in.P[1] = P[1]; in.P[2] = P[2];
+                        in.type = type;
+                        in.epsP = F(0, 0, 0, 0);
+                        in.epsE = F(0, e[0], e[1], e[2]);
 #pragma unroll
                         for (int ti = 0; ti < 2; ti++) {
                             const int t = ti == 0 ? T1 : T2;
@@ -188,128 +191,47 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                                 const int s = sg ? 1 : -1;
                                 int o[3] = {0, 0, 0};
                                 o[t] = s;
-                                epsPt[ti][sg] = F(0, o[0], o[1], o[2]);
-                                epsEt[ti][sg] = F(0, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
+                                in.epsPt[ti][sg] = F(0, o[0], o[1], o[2]);
+                                in.epsEt[ti][sg] = F(0, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
                                 // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
-                                vP[ti][sg] = s > 0 ? F(1 + t, 0, 0, 0) : F(1 + t, o[0], o[1], o[2]);
-                                vE[ti][sg] = s > 0 ? F(1 + t, e[0], e[1], e[2])
-                                                   : F(1 + t, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
+                                in.vP[ti][sg] = s > 0 ? F(1 + t, 0, 0, 0) : F(1 + t, o[0], o[1], o[2]);
+                                in.vE[ti][sg] = s > 0 ? F(1 + t, e[0], e[1], e[2])
+                                                      : F(1 + t, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
+                                in.nb_wall[ti][sg] = false;          // no BLOCKED cells on this path
                             }
                         }
                         int m_[3] = {0, 0, 0};
                         m_[C] = -1;
-                        const double umP = F(1 + C, 0, 0, 0);
-                        const double umE = F(1 + C, e[0], e[1], e[2]);
-                        const double umM = F(1 + C, m_[0], m_[1], m_[2]);
-                        double unb[6];
+                        in.umP = F(1 + C, 0, 0, 0);
+                        in.umE = F(1 + C, e[0], e[1], e[2]);
+                        in.umM = F(1 + C, m_[0], m_[1], m_[2]);
 #pragma unroll
                         for (int s6 = 0; s6 < 6; s6++) {
                             int o[3] = {0, 0, 0};
                             o[s6 / 2] = (s6 & 1) ? 1 : -1;
                             const int qa = P[s6 / 2] + o[s6 / 2];
-                            unb[s6] = (qa >= 0 && qa < ext[s6 / 2]) ? F(1 + C, o[0], o[1], o[2]) : 0.0;
+                            in.unb[s6] = (qa >= 0 && qa < ext[s6 / 2]) ? F(1 + C, o[0], o[1], o[2]) : 0.0;
                         }
-
-                        // ---- row (the expressions of k_assemble_mom)
-                        double as[6], phib[6];
-                        bool kept[6], inP[6];
-#pragma unroll
-                        for (int s6 = 0; s6 < 6; s6++) { as[s6] = 0.0; phib[s6] = 0.0; kept[s6] = false; inP[s6] = false; }
-                        {
-                            double vm;
-                            if (P[C] == 0) vm = (C == 2 && a.bc_zlo == MFX_BC_INLET) ? a.w_in : 0.0;
-                            else vm = umM;
-                            const double Fm = ((a.rho * epsP) * a.A[C]) * (0.5 * (vm + umP));
-                            const double Dm = a.Dc[C] * epsP;
-                            as[2 * C] = Dm + maxp_t(Fm);
-                            inP[2 * C] = true;
-                            if (P[C] >= 1) kept[2 * C] = true;
-                            else phib[2 * C] = vm;                                            // B1
-                            if (type == 2) {
-                                as[2 * C + 1] = 0.0;                                          // B3
-                            } else {
-                                // E is an identity row iff it is the last face along C and that face is a wall
-                                const bool e_ident = (P[C] + 1 >= ext[C] - 1) && !(C == 2 && a.bc_zhi == MFX_BC_OUTLET);
-                                const double vE_ = e_ident ? 0.0 : umE;
-                                const double Fp = ((a.rho * epsE) * a.A[C]) * (0.5 * (umP + vE_));
-                                const double Dp = a.Dc[C] * epsE;
-                                as[2 * C + 1] = Dp + maxp_t(-Fp);
-                                inP[2 * C + 1] = true;
-                                if (e_ident) phib[2 * C + 1] = 0.0;                           // B1
-                                else kept[2 * C + 1] = true;
-                            }
-                        }
-#pragma unroll
-                        for (int ti = 0; ti < 2; ti++) {
-                            const int t = ti == 0 ? T1 : T2;
-#pragma unroll
-                            for (int sg = 0; sg < 2; sg++) {
-                                const int s = sg ? 1 : -1;
-                                const int side = 2 * t + sg;
-                                const int pt = P[t] + s;
-                                if (pt >= 0 && pt < ext[t]) {
-                                    const double eQ0 = s > 0 ? epsP : epsPt[ti][0], eQ1 = s > 0 ? epsPt[ti][1] : epsP;
-                                    const double eR0 = s > 0 ? epsE : epsEt[ti][0], eR1 = s > 0 ? epsEt[ti][1] : epsE;
-                                    const double efQ = a.upwind ? (vP[ti][sg] >= 0.0 ? eQ0 : eQ1) : 0.5 * (eQ0 + eQ1);
-                                    const double efR = a.upwind ? (vE[ti][sg] >= 0.0 ? eR0 : eR1) : 0.5 * (eR0 + eR1);
-                                    const double mQ = ((a.rho * efQ) * a.A[t]) * vP[ti][sg];
-                                    const double mR = ((a.rho * efR) * a.A[t]) * vE[ti][sg];
-                                    const double Fl = 0.5 * (mQ + mR);
-                                    const double e4 = 0.25 * (((epsP + epsE) + epsPt[ti][sg]) + epsEt[ti][sg]);
-                                    const double D = a.Dc[t] * e4;
-                                    as[side] = D + maxp_t(s > 0 ? -Fl : Fl);
-                                    inP[side] = true;
-                                    kept[side] = true;
-                                } else {
-                                    int bc = MFX_BC_WALL;
-                                    if (t == 2) bc = s < 0 ? a.bc_zlo : a.bc_zhi;
-                                    if (bc == MFX_BC_OUTLET) continue;                        // B3
-                                    double Fl = 0.0;
-                                    if (bc == MFX_BC_INLET)
-                                        Fl = 0.5 * (((a.rho * epsP) * a.A[2]) * a.w_in + ((a.rho * epsE) * a.A[2]) * a.w_in);
-                                    const double e2 = 0.5 * (epsP + epsE);
-                                    const double D = a.Dc[t] * e2;
-                                    as[side] = 2.0 * D + maxp_t(s > 0 ? -Fl : Fl);            // B2, phi_b = 0
-                                    inP[side] = true;
-                                    phib[side] = 0.0;
-                                }
-                            }
-                        }
-                        const double sum = ((((as[0] + as[1]) + as[2]) + as[3]) + as[4]) + as[5];
-                        double bcb = 0.0;
-#pragma unroll
-                        for (int s6 = 0; s6 < 6; s6++)
-                            if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
-                        const double ef = 0.5 * (epsP + epsE);
-                        const double e0f = 0.5 * (e0P + e0E);
-                        const double bf = 0.5 * (bP + bE);
-                        const double Sf = 0.5 * (SP + SE);
-                        const double pE = type == 2 ? 0.0 : pEv;
-                        const double a0 = a.rVdt * e0f;
-                        const double aPv = (sum + a0) + bf * a.V;
-                        const double bb = ((((a0 * uoP) + (ef * a.A[C]) * (pP - pE)) + ((a.rho * ef) * a.gc) * a.V) + Sf * a.V) + bcb;
-                        const double aPr = aPv / a.urf;
-                        const double bR = bb + (aPr - aPv) * umP;
-                        const double dd_ = (ef * a.A[C]) / aPr;
-                        double st6[6];
-#pragma unroll
-                        for (int s6 = 0; s6 < 6; s6++) st6[s6] = kept[s6] ? as[s6] : 0.0;
-                        a.aW[n] = st6[0]; a.aE[n] = st6[1];
-                        a.aS[n] = st6[2]; a.aN[n] = st6[3];
-                        a.aB[n] = st6[4]; a.aT[n] = st6[5];
-                        a.aP[n] = aPr;
-                        a.b[n] = bR;
-                        a.d[n] = dd_;
-                        const bool nonfin = !isfinite(aPr) || !isfinite(bR) || !isfinite(dd_);
-                        if (nonfin || aPr == 0.0) {
+                        in.e0P = e0P; in.e0E = e0E; in.bP = bP; in.bE = bE; in.SP = SP; in.SE = SE;
+                        in.pP = pP; in.pEv = pEv; in.uoP = uoP;
+                        in.m_wall = false;
+                        // E is an identity row iff it is the last face along C and that face is a wall
+                        in.e_ident = type != 2 && (P[C] + 1 >= ext[C] - 1) && !(C == 2 && a.bc_zhi == MFX_BC_OUTLET);
+                        MomRowOut ro;
+                        mom_row<C>(a.R, in, ro);
+                        a.aW[n] = ro.st6[0]; a.aE[n] = ro.st6[1];
+                        a.aS[n] = ro.st6[2]; a.aN[n] = ro.st6[3];
+                        a.aB[n] = ro.st6[4]; a.aT[n] = ro.st6[5];
+                        a.aP[n] = ro.aPr;
+                        a.b[n] = ro.bR;
+                        a.d[n] = ro.d;
+                        const bool nonfin = !isfinite(ro.aPr) || !isfinite(ro.bR) || !isfinite(ro.d);
+                        if (nonfin || ro.aPr == 0.0) {
                             if (nonfin) atomicMin(&a.hdr->bad_nonfinite, (unsigned long long)n);
                             else atomicMin(&a.hdr->bad_zerodiag, (unsigned long long)n);
                         }
-                        double res = bb - aPv * umP;
-#pragma unroll
-                        for (int s6 = 0; s6 < 6; s6++) res = res + st6[s6] * unb[s6];
-                        num.add(fabs(res));
-                        den.add(fabs(aPv * umP));
+                        num.add(ro.res);
+                        den.add(ro.den);
                     }
                 }
                 // plane k-1 is no longer needed by this CTA
@@ -391,6 +313,11 @@ mfx_status assemble_mom_tma(int kind, const Geo &G, const mfx_params *pr, const 
     memset(&a, 0, sizeof(a));
     a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
     a.upwind = pr->face_eps_upwind;
+    a.R.ext[0] = G.nx; a.R.ext[1] = G.ny; a.R.ext[2] = G.nz;
+    a.R.bc_zlo = G.bc_zlo; a.R.bc_zhi = G.bc_zhi; a.R.upwind = pr->face_eps_upwind;
+    a.R.w_in = G.w_in; a.R.V = G.V;
+    a.R.rho = pr->rho; a.R.urf = pr->urf_mom; a.R.gc = pr->g[kind]; a.R.rVdt = (pr->rho * G.V) / pr->dt;
+    for (int t = 0; t < 3; t++) { a.R.A[t] = G.A[t]; a.R.Dc[t] = (pr->mu * G.A[t]) / G.h[t]; }
     a.tiles_x = (G.nx + ATX - 1) / ATX;
     a.tiles_y = (G.ny + ATY - 1) / ATY;
     a.bc_zlo = G.bc_zlo; a.bc_zhi = G.bc_zhi;

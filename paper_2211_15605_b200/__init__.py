@@ -298,7 +298,8 @@ def c_parcels(parcels: dict) -> Parcels:
     n = parcels["x"].numel()
     for k in PARCEL_KEYS:
         t = parcels[k]
-        assert t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous() and t.numel() == n, k
+        if not (t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous() and t.numel() == n):
+            raise ValueError(f"parcel array {k!r} must be a contiguous float64 tensor of {n} elements")
     return Parcels(*[_ptr(parcels[k], n) for k in PARCEL_KEYS], n)
 
 

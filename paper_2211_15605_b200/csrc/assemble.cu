@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
         MomRowIn in;
         in.P[0] = P[0]; in.P[1] = P[1]; in.P[2] = P[2];
         in.type = type;
-        in.epsP = __ldg(a.eps + n);
-        in.epsE = __ldg(a.eps + nE);
+        in.epsP_ = __ldg(a.eps + n);
+        in.epsE_ = __ldg(a.eps + nE);
 #pragma unroll
         for (int ti = 0; ti < 2; ti++) {
             const int t = ti == 0 ? T1 : T2;
@@ -178,26 +178,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_assemble_mom(MomArgs a)
                 Pt[t] += s;
                 Et[t] += s;
                 const long long iP = lin_cl(G, Pt[0], Pt[1], Pt[2]), iE = lin_cl(G, Et[0], Et[1], Et[2]);
-                in.epsPt[ti][sg] = __ldg(a.eps + iP);
-                in.epsEt[ti][sg] = __ldg(a.eps + iE);
+                in.epsPt_[ti][sg] = __ldg(a.eps + iP);
+                in.epsEt_[ti][sg] = __ldg(a.eps + iE);
                 // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
-                in.vP[ti][sg] = __ldg(vt[ti] + (s > 0 ? n : iP));
-                in.vE[ti][sg] = __ldg(vt[ti] + (s > 0 ? nE : iE));
+                in.vP_[ti][sg] = __ldg(vt[ti] + (s > 0 ? n : iP));
+                in.vE_[ti][sg] = __ldg(vt[ti] + (s > 0 ? nE : iE));
                 const int pt = P[t] + s;
-                in.nb_wall[ti][sg] = a.blocked && pt >= 0 && pt < extent(G, t) &&
+                in.nb_wall_[ti][sg] = a.blocked && pt >= 0 && pt < extent(G, t) &&
                                      (blk_q(G, a.blocked, Pt) || blk_q(G, a.blocked, Et));   // §3.10
             }
         }
         int Pm[3] = {P[0], P[1], P[2]};
         Pm[C] -= 1;
-        in.umP = __ldg(um + n);
-        in.umE = __ldg(um + nE);
-        in.umM = __ldg(um + lin_cl(G, Pm[0], Pm[1], Pm[2]));
+        in.umP_ = __ldg(um + n);
+        in.umE_ = __ldg(um + nE);
+        in.umM_ = __ldg(um + lin_cl(G, Pm[0], Pm[1], Pm[2]));
 #pragma unroll
         for (int s6 = 0; s6 < 6; s6++) {
             int Q[3] = {P[0], P[1], P[2]};
             Q[s6 / 2] += (s6 & 1) ? 1 : -1;
-            in.unb[s6] = in_dom(G, Q) ? __ldg(um + lin_cl(G, Q[0], Q[1], Q[2])) : 0.0;
+            in.unb_[s6] = in_dom(G, Q) ? __ldg(um + lin_cl(G, Q[0], Q[1], Q[2])) : 0.0;
         }
         in.e0P = __ldg(a.eps0 + n); in.e0E = __ldg(a.eps0 + nE);
         in.bP = __ldg(a.beta + n); in.bE = __ldg(a.beta + nE);

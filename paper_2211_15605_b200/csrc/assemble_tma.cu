@@ -85,6 +85,66 @@ struct ACursor {
     }
 };
 
+// mom_row inputs read from the staged planes where the row uses them (the
+// 3x3x3 neighbourhood of eps, u, v, w) plus the pointwise values in registers
+template <int C>
+struct SmemRowIn {
+    static constexpr int T1 = C == 0 ? 1 : 0, T2 = C == 2 ? 1 : 2;
+    int P[3];
+    int type;
+    bool m_wall, e_ident;
+    double e0P, e0E, bP, bE, SP, SE, pP, pEv, uoP;
+    const double *pl[3];   // planes k-1, k, k+1
+    int hc, e[3], ext[3];
+    __device__ double F(int f, int dx, int dy, int dz) const
+    {
+        return pl[dz + 1][f * (ABOX_B / 8) + hc + dy * AHX + dx];
+    }
+    __device__ double at(int f, const int o[3]) const { return F(f, o[0], o[1], o[2]); }
+    __device__ void off(int ti, int sg, int o[3]) const
+    {
+        o[0] = o[1] = o[2] = 0;
+        o[ti == 0 ? T1 : T2] = sg ? 1 : -1;
+    }
+    __device__ double epsP() const { return F(0, 0, 0, 0); }
+    __device__ double epsE() const { return F(0, e[0], e[1], e[2]); }
+    __device__ double epsPt(int ti, int sg) const { int o[3]; off(ti, sg, o); return at(0, o); }
+    __device__ double epsEt(int ti, int sg) const
+    {
+        int o[3]; off(ti, sg, o);
+        return F(0, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
+    }
+    // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
+    __device__ double vP(int ti, int sg) const
+    {
+        const int t = ti == 0 ? T1 : T2;
+        int o[3]; off(ti, sg, o);
+        return sg ? F(1 + t, 0, 0, 0) : at(1 + t, o);
+    }
+    __device__ double vE(int ti, int sg) const
+    {
+        const int t = ti == 0 ? T1 : T2;
+        int o[3]; off(ti, sg, o);
+        return sg ? F(1 + t, e[0], e[1], e[2]) : F(1 + t, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
+    }
+    __device__ double umP() const { return F(1 + C, 0, 0, 0); }
+    __device__ double umE() const { return F(1 + C, e[0], e[1], e[2]); }
+    __device__ double umM() const
+    {
+        int o[3] = {0, 0, 0};
+        o[C] = -1;
+        return at(1 + C, o);
+    }
+    __device__ double unb(int s6) const
+    {
+        int o[3] = {0, 0, 0};
+        o[s6 / 2] = (s6 & 1) ? 1 : -1;
+        const int qa = P[s6 / 2] + o[s6 / 2];
+        return (qa >= 0 && qa < ext[s6 / 2]) ? at(1 + C, o) : 0.0;
+    }
+    __device__ bool nb_wall(int, int) const { return false; }   // no BLOCKED cells on this path
+};
+
 template <int C>
 __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_constant__ AsmMomMaps M, AsmMomArgs a)
 {
@@ -165,10 +225,6 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                 const double *pl[3] = {(const double *)(smem + (size_t)((qk - 1) % AS) * ASTAGE_B),
                                        (const double *)(smem + (size_t)(qk % AS) * ASTAGE_B),
                                        (const double *)(smem + (size_t)((qk + 1) % AS) * ASTAGE_B)};
-                // F(f, dx, dy, dz): field f (0 eps, 1 u, 2 v, 3 w) at P + (dx, dy, dz)
-                auto F = [&](int f, int dx, int dy, int dz) -> double {
-                    return pl[dz + 1][f * (ABOX_B / 8) + hc + dy * AHX + dx];
-                };
                 if (mine) {
                     if (type == 1) {
                         a.aP[n] = 1.0;
@@ -176,42 +232,14 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                         a.b[n] = 0.0;
                         a.d[n] = 0.0;
                     } else {
-                        int e[3] = {0, 0, 0};
-                        e[C] = oE;                                   // E = P + e (E = P on the outlet row)
-                        MomRowIn in;
+                        SmemRowIn<C> in;
                         in.P[0] = P[0]; in.P[1] = P[1]; in.P[2] = P[2];
                         in.type = type;
-                        in.epsP = F(0, 0, 0, 0);
-                        in.epsE = F(0, e[0], e[1], e[2]);
-#pragma unroll
-                        for (int ti = 0; ti < 2; ti++) {
-                            const int t = ti == 0 ? T1 : T2;
-#pragma unroll
-                            for (int sg = 0; sg < 2; sg++) {
-                                const int s = sg ? 1 : -1;
-                                int o[3] = {0, 0, 0};
-                                o[t] = s;
-                                in.epsPt[ti][sg] = F(0, o[0], o[1], o[2]);
-                                in.epsEt[ti][sg] = F(0, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
-                                // velocity on the +t face of Q (s>0: Q = P, R = E; s<0: Q = P-e_t, R = E-e_t)
-                                in.vP[ti][sg] = s > 0 ? F(1 + t, 0, 0, 0) : F(1 + t, o[0], o[1], o[2]);
-                                in.vE[ti][sg] = s > 0 ? F(1 + t, e[0], e[1], e[2])
-                                                      : F(1 + t, e[0] + o[0], e[1] + o[1], e[2] + o[2]);
-                                in.nb_wall[ti][sg] = false;          // no BLOCKED cells on this path
-                            }
-                        }
-                        int m_[3] = {0, 0, 0};
-                        m_[C] = -1;
-                        in.umP = F(1 + C, 0, 0, 0);
-                        in.umE = F(1 + C, e[0], e[1], e[2]);
-                        in.umM = F(1 + C, m_[0], m_[1], m_[2]);
-#pragma unroll
-                        for (int s6 = 0; s6 < 6; s6++) {
-                            int o[3] = {0, 0, 0};
-                            o[s6 / 2] = (s6 & 1) ? 1 : -1;
-                            const int qa = P[s6 / 2] + o[s6 / 2];
-                            in.unb[s6] = (qa >= 0 && qa < ext[s6 / 2]) ? F(1 + C, o[0], o[1], o[2]) : 0.0;
-                        }
+                        in.e[0] = in.e[1] = in.e[2] = 0;
+                        in.e[C] = oE;                                // E = P + e (E = P on the outlet row)
+                        in.ext[0] = ext[0]; in.ext[1] = ext[1]; in.ext[2] = ext[2];
+                        in.pl[0] = pl[0]; in.pl[1] = pl[1]; in.pl[2] = pl[2];
+                        in.hc = hc;
                         in.e0P = e0P; in.e0E = e0E; in.bP = bP; in.bE = bE; in.SP = SP; in.SE = SE;
                         in.pP = pP; in.pEv = pEv; in.uoP = uoP;
                         in.m_wall = false;

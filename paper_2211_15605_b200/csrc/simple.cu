@@ -899,10 +899,12 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
                 if (st != MFX_OK) return st;
                 c->pic_scratch_bytes = need;
             }
+            // the parcels may have been written on any stream of this device
+            MFX_CUDA_TRY(cudaDeviceSynchronize());
             mfx_status st = mfx::pic_sort(&c->grid, pic, parcels, c->pic_sorted, c->pic_scratch,
                                           c->pic_scratch_bytes, nullptr);
             if (st != MFX_OK) return st;
-            MFX_CUDA_TRY(cudaStreamSynchronize(nullptr));
+            MFX_CUDA_TRY(cudaDeviceSynchronize());
             mfx_parcels sp;
             sp.x = c->pic_sorted[0]; sp.y = c->pic_sorted[1]; sp.z = c->pic_sorted[2];
             sp.u = c->pic_sorted[3]; sp.v = c->pic_sorted[4]; sp.w = c->pic_sorted[5];

@@ -200,3 +200,33 @@ def test_adapt_dt_same_decisions_as_oracle(mfx, orc):
         its, conv = int(rng.integers(1, 11)), bool(rng.integers(0, 2))
         assert mfx.adapt_dt(a, its, conv) == orc.adapt_dt(b, its, conv)
         assert a.dt == b.dt
+
+
+def test_time_and_sort_entry_points_reject_bad_args(mfx):
+    """Argument errors of the time-loop and parcel-sort entry points return
+    MFX_ERR_ARG before any device work (no GPU needed)."""
+    import ctypes as C
+    import synth
+    tc = mfx.time_ctrl(dt=-1.0)
+    acc = C.c_int()
+    assert mfx.lib().mfx_adapt_dt(C.byref(tc), 1, 1, C.byref(acc)) == mfx.ERR_ARG
+    assert mfx.lib().mfx_time_step(None, None, None, None, None, None) == mfx.ERR_ARG
+    g = synth.make_grid(16, 16, 32)
+    cg = mfx.c_grid(g)
+    assert mfx.lib().mfx_pic_sort_scratch_bytes(C.byref(cg), 1000) > 4 * 2 * g.n
+    pp = mfx.PicParams(200e-6, 0.35)
+    pc = mfx.Parcels(C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8),
+                     C.c_void_p(8), 10)
+    outs = (C.c_void_p * 7)(*([8] * 7))                       # aliases the input
+    assert mfx.lib().mfx_pic_sort(C.byref(cg), C.byref(pp), C.byref(pc), outs, None, 0, None) == mfx.ERR_ARG
+    assert "in place" in mfx.last_error()
+
+
+def test_state_load_rejects_missing_file(mfx, tmp_path):
+    import ctypes as C
+    import synth
+    g = synth.make_grid(8, 6, 10)
+    st = mfx.State()
+    rc = mfx.lib().mfx_state_load(str(tmp_path / "nope.mpxd").encode(), C.byref(mfx.c_grid(g)), C.byref(st), 0,
+                                  None, 0, None, None, None, None)
+    assert rc == mfx.ERR_ARG and "cannot open" in mfx.last_error()

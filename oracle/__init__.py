@@ -125,6 +125,8 @@ def lib():
         L.or_simple_iter.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.c_int,
                                      C.POINTER(OgState), _DP, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_pic_deposit_eps.argtypes = [C.POINTER(OgGrid), C.POINTER(OgPicParams), C.POINTER(OgParcels), _DP]
+        L.or_pow.restype = C.c_double
+        L.or_pow.argtypes = [C.c_double, C.c_double]
         L.or_pic_drag_coef.restype = C.c_double
         L.or_pic_drag_coef.argtypes = [C.POINTER(OgParams), C.POINTER(OgPicParams), C.c_double, C.c_double,
                                        C.c_double]
@@ -299,6 +301,11 @@ def pic_deposit_eps(grid, pic, parcels: dict):
     cg, cpp = c_grid(grid), OgPicParams(pic.d_p, pic.eps_min)
     rc = lib().or_pic_deposit_eps(C.byref(cg), C.byref(cpp), C.byref(P.c), _p(eps))
     return eps, rc
+
+
+def pow_(x: float, y: float) -> float:
+    """§3.9 written pow algorithm (x > 0)."""
+    return lib().or_pow(x, y)
 
 
 def pic_drag_coef(params, pic, eg: float, slip: float, omega: float = 1.0) -> float:

@@ -91,6 +91,7 @@ typedef struct { const double *x, *y, *z, *u, *v, *w, *omega; long n; } og_parce
 typedef struct { double d_p, eps_min; } og_pic_params;
 
 int or_pic_deposit_eps(const og_grid *g, const og_pic_params *pp, const og_parcels *pc, double *eps_g);
+double or_pow(double x, double y);
 double or_pic_drag_coef(const og_params *pr, const og_pic_params *pp, double eg, double slip, double omega);
 int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, const og_parcels *pc,
                 const double *eps_g, const double *u, const double *v, const double *w,

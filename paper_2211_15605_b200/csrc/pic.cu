@@ -163,14 +163,51 @@ struct PicDragArgs {
     WsHeader *hdr;
 };
 
+// x^y for x > 0 by the written algorithm of DESIGN.md §3.9 (the closure's
+// powers have one bit pattern on every side; CUDA's pow and libm's differ in
+// the last bit): ln(x) = e ln2 + 2 atanh((m-1)/(m+1)), m in [sqrt(1/2),
+// sqrt(2)), series to t^21; exp(z) = 2^k exp(r), Taylor to r^13 (Horner).
+__device__ __forceinline__ double dev_ln(double x)
+{
+    int e;
+    double m = frexp(x, &e);
+    if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
+    const double t = (m - 1.0) / (m + 1.0);
+    const double t2 = t * t;
+    double q = 1.0 / 21.0;
+    q = q * t2 + 1.0 / 19.0;
+    q = q * t2 + 1.0 / 17.0;
+    q = q * t2 + 1.0 / 15.0;
+    q = q * t2 + 1.0 / 13.0;
+    q = q * t2 + 1.0 / 11.0;
+    q = q * t2 + 1.0 / 9.0;
+    q = q * t2 + 1.0 / 7.0;
+    q = q * t2 + 1.0 / 5.0;
+    q = q * t2 + 1.0 / 3.0;
+    q = q * t2 + 1.0;
+    const double lm = 2.0 * (t * q);
+    const double de = (double)e;
+    return de * 6.93147180369123816490e-01 + (de * 1.90821492927058770002e-10 + lm);
+}
+__device__ __forceinline__ double dev_exp(double z)
+{
+    const double k = floor(z * 1.44269504088896338700e+00 + 0.5);
+    const double r = (z - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
+    double q = 1.0;
+#pragma unroll
+    for (int n = 13; n >= 1; n--) q = 1.0 + (r / (double)n) * q;
+    return ldexp(q, (int)k);
+}
+__device__ __forceinline__ double dev_pow(double x, double y) { return x == 1.0 ? 1.0 : dev_exp(y * dev_ln(x)); }
+
 // DESIGN.md §3.9 (SPEC.md:285-289 closure, written without the eps_s that cancels)
 __device__ __forceinline__ double drag_coef(double rho, double mu, double dp, double Vs, double eg, double slip,
                                             double om)
 {
     double Re = ((rho * dp) * slip) / mu;
     Re = Re < 1e-12 ? 1e-12 : Re;
-    const double A = pow(eg, 4.14);
-    const double B = eg <= 0.85 ? 0.8 * pow(eg, 1.28) : pow(eg, 2.65);
+    const double A = dev_pow(eg, 4.14);
+    const double B = eg <= 0.85 ? 0.8 * dev_pow(eg, 1.28) : dev_pow(eg, 2.65);
     const double q = 0.06 * Re;
     const double Vr = 0.5 * ((A - q) + sqrt((q * q + (0.12 * Re) * (2.0 * B - A)) + A * A));
     double Cd = 0.63 + 4.8 / sqrt(Re / Vr);

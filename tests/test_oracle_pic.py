@@ -210,3 +210,14 @@ def test_momentum_bookkeeping(orc):
         rhs = math.fsum(K * pc[key])
         assert abs(lhs - rhs) <= 1e-13 * math.fsum(np.abs(K * pc[key]))
     assert np.all(out["beta"] >= 0.0)
+
+
+def test_written_pow_accuracy(orc):
+    """The closure's powers use one written algorithm; it is
+    within a few ulp of the correctly rounded power and exact at x = 1."""
+    rng = np.random.default_rng(12)
+    xs = np.concatenate([rng.uniform(0.3, 1.0, 5000), [0.35, 0.5, 0.85, 0.999999999, 1.0 - 2**-52]])
+    for y in (4.14, 1.28, 2.65):
+        for x in xs:
+            assert abs(orc.pow_(x, y) - x ** y) <= 8 * 2.2e-16 * x ** y
+        assert orc.pow_(1.0, y) == 1.0

@@ -272,7 +272,14 @@ def measure_pic(mfx, torch):
             scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
             t_sort, _ = _ev_ms(torch, lambda: mfx.pic_sort(g, pic, d, out=srt, scratch=scratch), 7)
             t_drag_sorted, _ = _ev_ms(torch, lambda: mfx.pic_drag(g, pr, pic, srt, eps, u, v, w, ws, out=outs), 7)
-            res["gpu_sort"] = {"sort_us": 1e3 * t_sort, "drag_deposit_after_sort_us": 1e3 * t_drag_sorted}
+            vals = torch.empty(4 * m, dtype=torch.float64, device="cuda")
+            t_gather, _ = _ev_ms(torch, lambda: mfx.pic_drag_binned(g, pr, pic, srt, eps, u, v, w, ws, out=outs,
+                                                                    vals=vals), 7)
+            t_eps_gather, _ = _ev_ms(torch, lambda: mfx.pic_deposit_eps_binned(g, pic, srt, ws, eps=eps, vals=vals), 7)
+            res["gpu_sort"] = {"sort_us": 1e3 * t_sort, "drag_deposit_after_sort_us": 1e3 * t_drag_sorted,
+                               "drag_binned_gather_us": 1e3 * t_gather, "eps_binned_gather_us": 1e3 * t_eps_gather,
+                               "note": "binned gathers: deterministic, bitwise the parcel-ordered definition"}
+            del vals
             del srt, scratch
         res[name] = {"eps_deposit_us": 1e3 * t_eps, "drag_deposit_us": 1e3 * t_drag,
                      "parcels_per_s_drag": m / (t_drag * 1e-3),

@@ -191,16 +191,37 @@ mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mf
                         const double *w, double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w,
                         double *K, void *ws, size_t ws_bytes, void *stream);
 
-/* Cell-ordered copy of the parcels (counting sort by the containing cell,
- * clamped into the grid): out = 7 device arrays x, y, z, u, v, w, omega of n
- * (must not alias the input).  The deposits above are 2.5x faster on
- * cell-ordered parcels; parcels move once per time step, so one sort serves
- * every SIMPLE iteration of an implicit coupling.  scratch: device
- * buffer of at least mfx_pic_sort_scratch_bytes(grid, n) bytes.  The order of
- * parcels inside one cell is not specified. */
+/* Binned copy of the parcels: a deterministic counting sort by BASE cell (the
+ * clamped lower corner floor(x/h - 0.5) of the parcel's trilinear stencil),
+ * ascending original index inside a bin, so the binned order is unique.
+ * out = 7 device arrays x, y, z, u, v, w, omega of n (must not alias the
+ * input); orig (device, n, may be NULL) = original index of each binned
+ * parcel; bin_start (device, N + 1, may be NULL) = first binned position of
+ * each base cell (bin_start[N] = n).  scratch: device buffer of at least
+ * mfx_pic_sort_scratch_bytes(grid, n) bytes.  Parcels move once per time step,
+ * so one binning serves every SIMPLE iteration of an implicit coupling. */
 size_t mfx_pic_sort_scratch_bytes(const mfx_grid *grid, long long n_parcels);
 mfx_status mfx_pic_sort(const mfx_grid *grid, const mfx_pic_params *pic, const mfx_parcels *parcels,
-                        double *const out[7], void *scratch, size_t scratch_bytes, void *stream);
+                        double *const out[7], unsigned int *orig, unsigned int *bin_start, void *scratch,
+                        size_t scratch_bytes, void *stream);
+
+/* The two deposits on binned parcels, as gathers: every node sums, in
+ * ascending ORIGINAL parcel index, the contributions of the parcels whose
+ * stencil contains it -- the exact sequence of additions of the parcel-ordered
+ * definition, so the fields are bitwise those of the
+ * definition and do not depend on scheduling (no atomics).  vals: device
+ * scratch of n (eps) or 4 n (drag) doubles.  K (may be NULL) is per binned
+ * parcel.  Invalid parcels contribute nothing and are latched in ws by their
+ * original index. */
+mfx_status mfx_pic_deposit_eps_binned(const mfx_grid *grid, const mfx_pic_params *pic,
+                                      const mfx_parcels *binned, const unsigned int *orig,
+                                      const unsigned int *bin_start, double *eps_g, double *vals, void *ws,
+                                      size_t ws_bytes, void *stream);
+mfx_status mfx_pic_drag_binned(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,
+                               const mfx_parcels *binned, const unsigned int *orig, const unsigned int *bin_start,
+                               const double *eps_g, const double *u, const double *v, const double *w,
+                               double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w, double *K,
+                               double *vals, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------- dump / restart (NEXT-4) */
 /* MPXD state dumps (PAPER.md:119 restarts, PAPER.md:121

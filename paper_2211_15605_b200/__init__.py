@@ -120,8 +120,12 @@ _sigs = {
     "mfx_pic_deposit_eps": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), _V, _V,
                                       C.c_size_t, _V]),
     "mfx_pic_sort_scratch_bytes": (C.c_size_t, [C.POINTER(Grid), C.c_longlong]),
-    "mfx_pic_sort": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), C.POINTER(_V), _V,
-                               C.c_size_t, _V]),
+    "mfx_pic_sort": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), C.POINTER(_V), _V, _V,
+                               _V, C.c_size_t, _V]),
+    "mfx_pic_deposit_eps_binned": (C.c_int, [C.POINTER(Grid), C.POINTER(PicParams), C.POINTER(Parcels), _V, _V,
+                                             _V, _V, _V, C.c_size_t, _V]),
+    "mfx_pic_drag_binned": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(PicParams), C.POINTER(Parcels),
+                                      _V, _V] + [_V] * 10 + [_V, C.c_size_t, _V]),
     "mfx_pic_drag": (C.c_int, [C.POINTER(Grid), C.POINTER(Params), C.POINTER(PicParams), C.POINTER(Parcels)] +
                      [_V] * 9 + [_V, C.c_size_t, _V]),
     "mfx_state_dump": (C.c_int, [C.c_char_p, C.POINTER(Grid), C.POINTER(State), C.c_int, C.POINTER(Parcels),
@@ -319,17 +323,59 @@ def pic_deposit_eps(grid, pic, parcels: dict, ws: Workspace, eps=None, stream=No
 
 
 def pic_sort(grid, pic, parcels: dict, out: dict | None = None, scratch=None, stream=None) -> dict:
-    """Cell-ordered copy of the parcels (mfx_pic_sort).  Returns the sorted dict."""
+    """Binned copy of the parcels (mfx_pic_sort, deterministic): returns a dict with
+    the seven sorted arrays plus 'orig' (int32 view of the original indices) and
+    'bin_start' (N + 1)."""
     import torch
     m = parcels["x"].numel()
+    n = grid.nx * grid.ny * grid.nz
     dev = parcels["x"].device
     out = out if out is not None else {k: torch.empty(m, dtype=torch.float64, device=dev) for k in PARCEL_KEYS}
+    out.setdefault("orig", torch.empty(m, dtype=torch.int32, device=dev))
+    out.setdefault("bin_start", torch.empty(n + 1, dtype=torch.int32, device=dev))
     nb = int(_lib.mfx_pic_sort_scratch_bytes(C.byref(c_grid(grid)), m))
     scratch = scratch if scratch is not None else torch.empty(nb, dtype=torch.uint8, device=dev)
     arr = (C.c_void_p * 7)(*[_ptr(out[k], m) for k in PARCEL_KEYS])
     _check(_lib.mfx_pic_sort(C.byref(c_grid(grid)), C.byref(PicParams(pic.d_p, pic.eps_min)),
-                             C.byref(c_parcels(parcels)), arr, C.c_void_p(scratch.data_ptr()), scratch.numel(),
+                             C.byref(c_parcels(parcels)), arr, C.c_void_p(out["orig"].data_ptr()),
+                             C.c_void_p(out["bin_start"].data_ptr()), C.c_void_p(scratch.data_ptr()), scratch.numel(),
                              _stream(stream)), "mfx_pic_sort")
+    return out
+
+
+def pic_deposit_eps_binned(grid, pic, binned: dict, ws: Workspace, eps=None, vals=None, stream=None):
+    """Deterministic gather eps deposit on binned parcels (bitwise the definition)."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    m = binned["x"].numel()
+    dev = binned["x"].device
+    eps = eps if eps is not None else torch.empty(n, dtype=torch.float64, device=dev)
+    vals = vals if vals is not None else torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    _check(_lib.mfx_pic_deposit_eps_binned(C.byref(c_grid(grid)), C.byref(PicParams(pic.d_p, pic.eps_min)),
+                                           C.byref(c_parcels(binned)), C.c_void_p(binned["orig"].data_ptr()),
+                                           C.c_void_p(binned["bin_start"].data_ptr()), _ptr(eps, n),
+                                           C.c_void_p(vals.data_ptr()), C.c_void_p(ws.ptr), ws.nbytes,
+                                           _stream(stream)), "mfx_pic_deposit_eps_binned")
+    return eps
+
+
+def pic_drag_binned(grid, params, pic, binned: dict, eps, u, v, w, ws: Workspace, out=None, K=None, vals=None,
+                    stream=None):
+    """Deterministic gather drag deposit on binned parcels (bitwise the definition)."""
+    import torch
+    n = grid.nx * grid.ny * grid.nz
+    m = binned["x"].numel()
+    dev = eps.device
+    out = out if out is not None else {k: torch.empty(n, dtype=torch.float64, device=dev)
+                                       for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")}
+    vals = vals if vals is not None else torch.empty(max(4 * m, 1), dtype=torch.float64, device=dev)
+    _check(_lib.mfx_pic_drag_binned(C.byref(c_grid(grid)), C.byref(c_params(params)),
+                                    C.byref(PicParams(pic.d_p, pic.eps_min)), C.byref(c_parcels(binned)),
+                                    C.c_void_p(binned["orig"].data_ptr()), C.c_void_p(binned["bin_start"].data_ptr()),
+                                    _ptr(eps, n), _ptr(u, n), _ptr(v, n), _ptr(w, n),
+                                    *[_ptr(out[k], n) for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")],
+                                    _ptr(K, m) if K is not None else None, C.c_void_p(vals.data_ptr()),
+                                    C.c_void_p(ws.ptr), ws.nbytes, _stream(stream)), "mfx_pic_drag_binned")
     return out
 
 

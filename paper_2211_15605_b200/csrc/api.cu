@@ -237,9 +237,31 @@ API size_t mfx_pic_sort_scratch_bytes(const mfx_grid *grid, long long n_parcels)
 }
 
 API mfx_status mfx_pic_sort(const mfx_grid *grid, const mfx_pic_params *pic, const mfx_parcels *parcels,
-                            double *const out[7], void *scratch, size_t scratch_bytes, void *stream)
+                            double *const out[7], unsigned int *orig, unsigned int *bin_start, void *scratch,
+                            size_t scratch_bytes, void *stream)
 {
-    return pic_sort(grid, pic, parcels, out, scratch, scratch_bytes, (cudaStream_t)stream);
+    return pic_sort(grid, pic, parcels, out, orig, bin_start, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_pic_deposit_eps_binned(const mfx_grid *grid, const mfx_pic_params *pic,
+                                          const mfx_parcels *binned, const unsigned int *orig,
+                                          const unsigned int *bin_start, double *eps_g, double *vals, void *ws,
+                                          size_t ws_bytes, void *stream)
+{
+    double *outs[4] = {eps_g, nullptr, nullptr, nullptr};
+    return pic_deposit_binned(0, grid, nullptr, pic, binned, orig, bin_start, nullptr, nullptr, nullptr, nullptr,
+                              outs, nullptr, vals, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+API mfx_status mfx_pic_drag_binned(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,
+                                   const mfx_parcels *binned, const unsigned int *orig, const unsigned int *bin_start,
+                                   const double *eps_g, const double *u, const double *v, const double *w,
+                                   double *beta, double *sbeta_u, double *sbeta_v, double *sbeta_w, double *K,
+                                   double *vals, void *ws, size_t ws_bytes, void *stream)
+{
+    double *outs[4] = {beta, sbeta_u, sbeta_v, sbeta_w};
+    return pic_deposit_binned(1, grid, params, pic, binned, orig, bin_start, eps_g, u, v, w, outs, K, vals, ws,
+                              ws_bytes, (cudaStream_t)stream);
 }
 
 API mfx_status mfx_pic_drag(const mfx_grid *grid, const mfx_params *params, const mfx_pic_params *pic,

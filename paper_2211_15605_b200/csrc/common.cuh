@@ -257,7 +257,13 @@ mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, 
 long long launch_count_get();
 size_t pic_sort_scratch_bytes(long long N, long long m);
 mfx_status pic_sort(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *in, double *const out[7],
-                    void *scratch, size_t scratch_bytes, cudaStream_t s);
+                    unsigned int *orig_out, unsigned int *start_out, void *scratch, size_t scratch_bytes,
+                    cudaStream_t s);
+mfx_status pic_deposit_binned(int drag, const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp,
+                              const mfx_parcels *pc, const unsigned int *orig, const unsigned int *start,
+                              const double *eps_in, const double *u, const double *v, const double *w,
+                              double *const outs[4], double *Kout, double *vals, void *ws, size_t wsb,
+                              cudaStream_t s);
 mfx_status pic_deposit_eps(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *pc, double *eps,
                            void *ws, size_t wsb, cudaStream_t s);
 mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp, const mfx_parcels *pc,

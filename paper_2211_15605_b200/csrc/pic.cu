@@ -20,6 +20,7 @@
 // bitwise; per-parcel values (weights, interpolants) use the oracle's exact
 // expression order and differ only through pow() (CUDA's vs libm's ulps).
 #include <climits>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -286,19 +287,21 @@ int pic_grid(long long m)
     return (int)(need < 1 ? 1 : (need < cap ? need : cap));
 }
 
-// ------------------------------------------------------------------ parcel sort
-// Counting sort of the parcels by the cell that contains them (PAPER.md:97:
-// the coupling runs every SIMPLE iteration under implicit coupling, parcels
-// move once per time step): cell-ordered parcels make neighbouring threads
-// gather the same nodes and reduce into the same L2 lines (measured 2.5x
-// faster drag deposit).  Order inside a cell follows the atomic slot order.
-__device__ __forceinline__ unsigned int parcel_cell(const PicGeo &G, double x, double y, double z)
+// ------------------------------------------------------------------ parcel binning
+// Deterministic counting sort of the parcels by their BASE cell, i.e. the
+// clamped lower corner (floor(x/h - 0.5) per axis) of their trilinear stencil
+// (parcels move once per time step, the coupling runs every SIMPLE
+// iteration).  Inside a bin the parcels keep ascending original index, so the
+// binned order is unique.  Steps: bin + count (atomics), exclusive scan,
+// scatter of the original indices (atomic slots), per-bin insertion sort of
+// the indices, gather of the seven parcel arrays.
+__device__ __forceinline__ unsigned int parcel_bin(const PicGeo &G, double x, double y, double z)
 {
     int q[3];
     const double X[3] = {x, y, z};
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        int i = (int)floor(X[a] / G.h[a]);
+        int i = (int)floor(X[a] / G.h[a] - 0.5);
         q[a] = i < 0 ? 0 : (i > G.n[a] - 1 ? G.n[a] - 1 : i);
     }
     return (unsigned int)((long long)q[0] + (long long)G.n[0] * ((long long)q[1] + (long long)G.n[1] * q[2]));
@@ -306,16 +309,16 @@ __device__ __forceinline__ unsigned int parcel_cell(const PicGeo &G, double x, d
 
 __global__ void __launch_bounds__(kPicThreads) k_pic_count(PicGeo G, const double *x, const double *y,
                                                            const double *z, long long m, unsigned int *cnt,
-                                                           unsigned int *cell_of)
+                                                           unsigned int *bin_of)
 {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (long long)gridDim.x * blockDim.x) {
-        const unsigned int c = parcel_cell(G, __ldg(x + p), __ldg(y + p), __ldg(z + p));
-        cell_of[p] = c;
+        const unsigned int c = parcel_bin(G, __ldg(x + p), __ldg(y + p), __ldg(z + p));
+        bin_of[p] = c;
         atomicAdd(cnt + c, 1u);
     }
 }
 
-// exclusive scan, 2 levels of 2048-element tiles (N <= 2048 * 2048 * 2048)
+// exclusive scan, levels of 2048-element tiles
 constexpr int kScanT = 1024, kScanTile = 2 * kScanT;
 
 __device__ __forceinline__ unsigned int block_exclusive_scan(unsigned int v, unsigned int *sh, unsigned int &total)
@@ -380,21 +383,198 @@ mfx_status exclusive_scan(unsigned int *a, long long n, unsigned int *scratch, c
     return MFX_OK;
 }
 
-struct SortArgs {
+__global__ void __launch_bounds__(kPicThreads) k_pic_slot(long long m, const unsigned int *bin_of,
+                                                          const unsigned int *start, unsigned int *fill,
+                                                          unsigned int *orig)
+{
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (long long)gridDim.x * blockDim.x) {
+        const unsigned int c = bin_of[p];
+        orig[start[c] + atomicAdd(fill + c, 1u)] = (unsigned int)p;
+    }
+}
+
+// one thread per bin: ascending original index inside the bin (insertion sort)
+__global__ void __launch_bounds__(kPicThreads) k_pic_binsort(long long nbins, const unsigned int *start,
+                                                             const unsigned int *cnt, unsigned int *orig)
+{
+    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += (long long)gridDim.x * blockDim.x) {
+        const unsigned int lo = start[b], len = cnt[b];
+        for (unsigned int i = 1; i < len; i++) {
+            const unsigned int v = orig[lo + i];
+            unsigned int j = i;
+            while (j > 0 && orig[lo + j - 1] > v) { orig[lo + j] = orig[lo + j - 1]; j--; }
+            orig[lo + j] = v;
+        }
+    }
+}
+
+struct GatherArgs {
     const double *in[7];
     double *out[7];
     long long m;
-    const unsigned int *cell_of, *start;
-    unsigned int *fill;
+    const unsigned int *orig;
 };
 
-__global__ void __launch_bounds__(kPicThreads) k_pic_scatter(SortArgs a)
+__global__ void __launch_bounds__(kPicThreads) k_pic_gather_parcels(GatherArgs a)
 {
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
-        const unsigned int c = a.cell_of[p];
-        const unsigned int pos = a.start[c] + atomicAdd(a.fill + c, 1u);
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < a.m; q += (long long)gridDim.x * blockDim.x) {
+        const unsigned int p = a.orig[q];
 #pragma unroll
-        for (int f = 0; f < 7; f++) a.out[f][pos] = __ldg(a.in[f] + p);
+        for (int f = 0; f < 7; f++) a.out[f][q] = __ldg(a.in[f] + p);
+    }
+}
+
+__global__ void k_pic_bin_end(unsigned int *start, long long nbins, unsigned int m)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) start[nbins] = m;
+}
+
+// ------------------------------------------------------------------ gather deposits on binned parcels
+// Node c receives, in ascending original parcel index, W * value from every
+// parcel whose stencil contains c -- exactly the sequence of additions the
+// parcel-ordered definition makes to that node, so the sums
+// are bitwise those of the oracle.  Contributors sit in the bins c - {0,1}^3;
+// the (<= 8) bin lists are merged by original index.
+template <int NV>
+struct NodeGather {
+    const PicGeo *G;
+    const double *x, *y, *z;
+    const double *val[NV];
+    const unsigned int *orig, *start;
+    __device__ void run(long long c, double (&acc)[NV]) const
+    {
+        const int ci = (int)(c % G->n[0]);
+        const int cj = (int)((c / G->n[0]) % G->n[1]);
+        const int ck = (int)(c / ((long long)G->n[0] * G->n[1]));
+        unsigned int cur[8], end[8];
+        int nb = 0;
+#pragma unroll
+        for (int dk = 1; dk >= 0; dk--)
+#pragma unroll
+            for (int dj = 1; dj >= 0; dj--)
+#pragma unroll
+                for (int di = 1; di >= 0; di--) {
+                    const int bi = ci - di, bj = cj - dj, bk = ck - dk;
+                    cur[nb] = 0u; end[nb] = 0u;
+                    if (bi >= 0 && bj >= 0 && bk >= 0) {
+                        const long long b = (long long)bi + (long long)G->n[0] * ((long long)bj + (long long)G->n[1] * bk);
+                        cur[nb] = __ldg(start + b);
+                        end[nb] = __ldg(start + b + 1);
+                    }
+                    nb++;
+                }
+#pragma unroll
+        for (int v = 0; v < NV; v++) acc[v] = 0.0;
+        for (;;) {
+            int best = -1;
+            unsigned int bo = 0xffffffffu;
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (cur[q] < end[q]) {
+                    const unsigned int o = __ldg(orig + cur[q]);
+                    if (o < bo) { bo = o; best = q; }
+                }
+            if (best < 0) break;
+            const unsigned int pos = cur[best]++;
+            const double X[3] = {__ldg(x + pos), __ldg(y + pos), __ldg(z + pos)};
+            int nd[3][2];
+            double w[3][2];
+#pragma unroll
+            for (int ax = 0; ax < 3; ax++) pic_axis(X[ax], G->h[ax], G->n[ax], false, nd[ax], w[ax]);
+            double vv[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) vv[v] = __ldg(val[v] + pos);
+#pragma unroll
+            for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+                for (int jj = 0; jj < 2; jj++)
+#pragma unroll
+                    for (int ii = 0; ii < 2; ii++)
+                        if (nd[0][ii] == ci && nd[1][jj] == cj && nd[2][kk] == ck) {
+                            const double W = (w[0][ii] * w[1][jj]) * w[2][kk];
+#pragma unroll
+                            for (int v = 0; v < NV; v++) acc[v] += W * vv[v];
+                        }
+        }
+    }
+};
+
+struct PicValsArgs {
+    PicGeo G;
+    double rho, mu, dp;
+    const double *x, *y, *z, *up, *vp, *wp, *om;
+    long long m;
+    const double *eps, *u, *v, *w;
+    double *vals;           // [4][m]: K/V, (K u)/V, (K v)/V, (K w)/V   or [1][m]: omega Vs (eps mode)
+    double *Kout;
+    const unsigned int *orig;
+    WsHeader *hdr;
+    int drag;
+};
+
+// per-parcel values in binned order (invalid parcels contribute 0 and are latched by original index)
+__global__ void __launch_bounds__(kPicThreads) k_pic_vals(PicValsArgs a)
+{
+    const PicGeo &G = a.G;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
+        const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
+        const double om = __ldg(a.om + p);
+        if (!parcel_ok(G, X[0], X[1], X[2], om)) {
+            atomicMin(&a.hdr->bad_parcel, (unsigned long long)a.orig[p]);
+            for (int v = 0; v < (a.drag ? 4 : 1); v++) a.vals[v * a.m + p] = 0.0;
+            if (a.Kout) a.Kout[p] = 0.0;
+            continue;
+        }
+        if (!a.drag) {
+            a.vals[p] = om * G.Vs;
+            continue;
+        }
+        const double up[3] = {__ldg(a.up + p), __ldg(a.vp + p), __ldg(a.wp + p)};
+        const double eg = pic_interp<-1>(G, a.eps, X);
+        const double ug0 = pic_interp<0>(G, a.u, X);
+        const double ug1 = pic_interp<1>(G, a.v, X);
+        const double ug2 = pic_interp<2>(G, a.w, X);
+        const double sx = ug0 - up[0], sy = ug1 - up[1], sz = ug2 - up[2];
+        const double slip = sqrt((sx * sx + sy * sy) + sz * sz);
+        const double K = drag_coef(a.rho, a.mu, a.dp, G.Vs, eg, slip, om);
+        if (a.Kout) a.Kout[p] = K;
+        a.vals[p] = K / G.V;
+#pragma unroll
+        for (int c = 0; c < 3; c++) a.vals[(c + 1) * a.m + p] = (K * up[c]) / G.V;
+    }
+}
+
+struct NodeArgs1 {
+    PicGeo G;
+    NodeGather<1> ng;
+    double *eps;
+};
+__global__ void __launch_bounds__(kPicThreads) k_node_eps(NodeArgs1 a)
+{
+    NodeGather<1> ng = a.ng;
+    ng.G = &a.G;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < a.G.N; c += (long long)gridDim.x * blockDim.x) {
+        double acc[1];
+        ng.run(c, acc);
+        const double e = 1.0 - acc[0] / a.G.V;
+        a.eps[c] = e < a.G.eps_min ? a.G.eps_min : e;
+    }
+}
+
+struct NodeArgs4 {
+    PicGeo G;
+    NodeGather<4> ng;
+    double *out[4];
+};
+__global__ void __launch_bounds__(kPicThreads) k_node_drag(NodeArgs4 a)
+{
+    NodeGather<4> ng = a.ng;
+    ng.G = &a.G;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < a.G.N; c += (long long)gridDim.x * blockDim.x) {
+        double acc[4];
+        ng.run(c, acc);
+#pragma unroll
+        for (int v = 0; v < 4; v++) a.out[v][c] = acc[v];
     }
 }
 
@@ -461,41 +641,109 @@ mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_pa
 
 size_t pic_sort_scratch_bytes(long long N, long long m)
 {
-    const long long tiles = (N + kScanTile - 1) / kScanTile;
+    const long long tiles = (N + 1 + kScanTile - 1) / kScanTile;
     const long long scan = ((tiles + 255) & ~255LL) + ((tiles / kScanTile + 1 + 255) & ~255LL) + 256;
-    return sizeof(unsigned int) * (size_t)(2 * ((N + 63) & ~63LL) + ((m + 63) & ~63LL) + scan);
+    return sizeof(unsigned int) * (size_t)(2 * ((N + 64) & ~63LL) + ((m + 63) & ~63LL) + ((m + 63) & ~63LL) + scan);
 }
 
+// scratch layout: cnt[N+1] (becomes bin starts), fill[N+1], bin_of[m], orig[m], scan scratch
 mfx_status pic_sort(const mfx_grid *grid, const mfx_pic_params *pp, const mfx_parcels *in, double *const out[7],
-                    void *scratch, size_t scratch_bytes, cudaStream_t s)
+                    unsigned int *orig_out, unsigned int *start_out, void *scratch, size_t scratch_bytes,
+                    cudaStream_t s)
 {
     PicGeo G;
     if (!pic_geo(grid, pp, G)) return MFX_ERR_ARG;
     MFX_ARG_CHECK(in && out, "NULL parcels / out");
     MFX_ARG_CHECK(in->n >= 0, "negative parcel count");
     const long long m = in->n;
-    if (m == 0) return MFX_OK;
     const double *src[7] = {in->x, in->y, in->z, in->u, in->v, in->w, in->omega};
     for (int f = 0; f < 7; f++) {
-        MFX_ARG_CHECK(src[f] && out[f], "NULL parcel array %d", f);
-        MFX_ARG_CHECK(src[f] != out[f], "parcel sort cannot run in place (array %d)", f);
+        MFX_ARG_CHECK(m == 0 || (src[f] && out[f]), "NULL parcel array %d", f);
+        MFX_ARG_CHECK(m == 0 || src[f] != out[f], "parcel sort cannot run in place (array %d)", f);
     }
-    MFX_ARG_CHECK(G.N < (1LL << 32) && m < (1LL << 32), "grid / parcel count too large for 32-bit bins");
+    MFX_ARG_CHECK(G.N < (1LL << 32) - 1 && m < (1LL << 32), "grid / parcel count too large for 32-bit bins");
     MFX_ARG_CHECK(scratch && scratch_bytes >= pic_sort_scratch_bytes(G.N, m), "scratch of %zu bytes, need %zu",
                   scratch_bytes, pic_sort_scratch_bytes(G.N, m));
+    const long long NB = (G.N + 64) & ~63LL;
     unsigned int *cnt = (unsigned int *)scratch;
-    unsigned int *fill = cnt + ((G.N + 63) & ~63LL);
-    unsigned int *cell_of = fill + ((G.N + 63) & ~63LL);
-    unsigned int *scan_scratch = cell_of + ((m + 63) & ~63LL);
-    MFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned int) * 2 * ((G.N + 63) & ~63LL), s));
-    k_pic_count<<<pic_grid(m), kPicThreads, 0, s>>>(G, in->x, in->y, in->z, m, cnt, cell_of);
-    launch_count_add(1);
+    unsigned int *fill = cnt + NB;
+    unsigned int *bin_of = fill + NB;
+    unsigned int *orig = bin_of + ((m + 63) & ~63LL);
+    unsigned int *scan_scratch = orig + ((m + 63) & ~63LL);
+    MFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned int) * 2 * NB, s));
+    if (m > 0) {
+        k_pic_count<<<pic_grid(m), kPicThreads, 0, s>>>(G, in->x, in->y, in->z, m, cnt, bin_of);
+        launch_count_add(1);
+    }
     mfx_status st = exclusive_scan(cnt, G.N, scan_scratch, s);
     if (st != MFX_OK) return st;
-    SortArgs a;
-    for (int f = 0; f < 7; f++) { a.in[f] = src[f]; a.out[f] = out[f]; }
-    a.m = m; a.cell_of = cell_of; a.start = cnt; a.fill = fill;
-    k_pic_scatter<<<pic_grid(m), kPicThreads, 0, s>>>(a);
+    k_pic_bin_end<<<1, 1, 0, s>>>(cnt, G.N, (unsigned int)m);
+    if (m > 0) {
+        k_pic_slot<<<pic_grid(m), kPicThreads, 0, s>>>(m, bin_of, cnt, fill, orig);
+        // per-bin sort: fill[] now holds the counts again (every slot taken)
+        k_pic_binsort<<<reduce_grid(G.N), kPicThreads, 0, s>>>(G.N, cnt, fill, orig);
+        GatherArgs ga;
+        for (int f = 0; f < 7; f++) { ga.in[f] = src[f]; ga.out[f] = out[f]; }
+        ga.m = m;
+        ga.orig = orig;
+        k_pic_gather_parcels<<<pic_grid(m), kPicThreads, 0, s>>>(ga);
+        launch_count_add(4);
+        if (orig_out) MFX_CUDA_TRY(cudaMemcpyAsync(orig_out, orig, sizeof(unsigned int) * m, cudaMemcpyDeviceToDevice, s));
+    }
+    if (start_out)
+        MFX_CUDA_TRY(cudaMemcpyAsync(start_out, cnt, sizeof(unsigned int) * (G.N + 1), cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+// deposits on binned parcels (bitwise the parcel-ordered definition)
+mfx_status pic_deposit_binned(int drag, const mfx_grid *grid, const mfx_params *pr, const mfx_pic_params *pp,
+                              const mfx_parcels *pc, const unsigned int *orig, const unsigned int *start,
+                              const double *eps_in, const double *u, const double *v, const double *w,
+                              double *const outs[4], double *Kout, double *vals, void *ws, size_t wsb,
+                              cudaStream_t s)
+{
+    PicGeo G;
+    if (!pic_geo(grid, pp, G)) return MFX_ERR_ARG;
+    MFX_ARG_CHECK(pc && pc->n >= 0 && start && outs && outs[0], "NULL argument");
+    MFX_ARG_CHECK(pc->n == 0 || (pc->x && pc->y && pc->z && pc->omega && orig && vals), "NULL parcel array / orig / vals");
+    MFX_ARG_CHECK(ws && wsb >= ws_header_bytes(), "bad workspace");
+    if (drag) {
+        MFX_ARG_CHECK(pr && pr->mu > 0.0, "params / mu");
+        MFX_ARG_CHECK(eps_in && u && v && w && outs[1] && outs[2] && outs[3], "NULL field");
+        MFX_ARG_CHECK(pc->n == 0 || (pc->u && pc->v && pc->w), "NULL parcel velocity");
+    }
+    const long long m = pc->n;
+    if (m > 0) {
+        PicValsArgs a;
+        memset(&a, 0, sizeof(a));
+        a.G = G;
+        if (drag) { a.rho = pr->rho; a.mu = pr->mu; a.dp = pp->d_p; }
+        a.x = pc->x; a.y = pc->y; a.z = pc->z; a.up = pc->u; a.vp = pc->v; a.wp = pc->w; a.om = pc->omega;
+        a.m = m;
+        a.eps = eps_in; a.u = u; a.v = v; a.w = w;
+        a.vals = vals; a.Kout = Kout; a.orig = orig; a.hdr = (WsHeader *)ws; a.drag = drag;
+        count_launch(drag ? 11 : 10, s, true);
+        k_pic_vals<<<pic_grid(m), kPicThreads, 0, s>>>(a);
+        count_launch(drag ? 11 : 10, s, false);
+    }
+    const int nb = reduce_grid(G.N);
+    if (drag) {
+        NodeArgs4 na;
+        na.G = G;
+        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
+        for (int q = 0; q < 4; q++) { na.ng.val[q] = vals + (size_t)q * (size_t)m; na.out[q] = outs[q]; }
+        na.ng.orig = orig; na.ng.start = start;
+        k_node_drag<<<nb, kPicThreads, 0, s>>>(na);
+    } else {
+        NodeArgs1 na;
+        na.G = G;
+        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
+        na.ng.val[0] = vals;
+        na.ng.orig = orig; na.ng.start = start;
+        na.eps = outs[0];
+        k_node_eps<<<nb, kPicThreads, 0, s>>>(na);
+    }
     launch_count_add(1);
     MFX_CUDA_TRY(cudaGetLastError());
     return MFX_OK;

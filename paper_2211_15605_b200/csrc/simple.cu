@@ -290,7 +290,10 @@ struct mfx_ctx {
     mfx_parcels pic_pc;            // the caller's parcels, or the context's cell-sorted copy
     mfx_pic_params pic_pp;
     void *pic_ws;
-    double *pic_sorted[7];         // cell-ordered copy (mfx_pic_sort), capacity pic_cap
+    double *pic_sorted[7];         // binned copy (mfx_pic_sort), capacity pic_cap
+    unsigned int *pic_orig;        // original index per binned parcel
+    unsigned int *pic_start;       // bin starts (N + 1)
+    double *pic_vals;              // 4 x pic_cap per-parcel deposit values
     long long pic_cap;
     void *pic_scratch;
     size_t pic_scratch_bytes;
@@ -580,8 +583,10 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     // head of the SIMPLE iteration: particle -> fluid drag refresh
     if (c->pic_mode == MFX_PIC_IMPLICIT || (c->pic_mode == MFX_PIC_EXPLICIT && c->pic_pending)) {
         if (r == 0) {
-            rc = pic_drag(&c->grid, &pr, &c->pic_pp, &c->pic_pc, st->eps, st->u, st->v, st->w, st->beta,
-                          st->sbeta_u, st->sbeta_v, st->sbeta_w, nullptr, c->pic_ws, ws_header_bytes(), s);
+            // deterministic gather deposit on the binned parcels (bitwise the parcel-ordered definition)
+            double *outs[4] = {st->beta, st->sbeta_u, st->sbeta_v, st->sbeta_w};
+            rc = pic_deposit_binned(1, &c->grid, &pr, &c->pic_pp, &c->pic_pc, c->pic_orig, c->pic_start, st->eps,
+                                    st->u, st->v, st->w, outs, nullptr, c->pic_vals, c->pic_ws, ws_header_bytes(), s);
             if (rc != MFX_OK) return rc;
         }
         double *D[MFX_NBUF] = {0};
@@ -882,16 +887,24 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
         MFX_ARG_CHECK(pic->d_p > 0.0, "d_p must be positive");
         c->pic_pc = *parcels;
         c->pic_pp = *pic;
-        // keep a cell-ordered copy: the deposits are 2.5x faster on it and the
-        // parcels do not move between SIMPLE iterations of a time step
-        if (parcels->n > 0) {
+        // keep a binned copy (deterministic order): the refresh is a gather over
+        // it, and the parcels do not move between SIMPLE iterations of a time step
+        {
             const long long n = parcels->n;
             if (n > c->pic_cap) {
                 for (int f = 0; f < 7; f++) {
                     mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_sorted[f], sizeof(double) * (size_t)n);
                     if (st != MFX_OK) return st;
                 }
+                mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_orig, sizeof(unsigned int) * (size_t)n);
+                if (st != MFX_OK) return st;
+                st = mfx::ctx_alloc(c, (void **)&c->pic_vals, 4 * sizeof(double) * (size_t)n);
+                if (st != MFX_OK) return st;
                 c->pic_cap = n;
+            }
+            if (!c->pic_start) {
+                mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_start, sizeof(unsigned int) * (size_t)(c->N + 1));
+                if (st != MFX_OK) return st;
             }
             const size_t need = mfx::pic_sort_scratch_bytes(c->N, n);
             if (need > c->pic_scratch_bytes) {
@@ -901,8 +914,8 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
             }
             // the parcels may have been written on any stream of this device
             MFX_CUDA_TRY(cudaDeviceSynchronize());
-            mfx_status st = mfx::pic_sort(&c->grid, pic, parcels, c->pic_sorted, c->pic_scratch,
-                                          c->pic_scratch_bytes, nullptr);
+            mfx_status st = mfx::pic_sort(&c->grid, pic, parcels, c->pic_sorted, c->pic_orig, c->pic_start,
+                                          c->pic_scratch, c->pic_scratch_bytes, nullptr);
             if (st != MFX_OK) return st;
             MFX_CUDA_TRY(cudaDeviceSynchronize());
             mfx_parcels sp;

@@ -218,7 +218,8 @@ def test_time_and_sort_entry_points_reject_bad_args(mfx):
     pc = mfx.Parcels(C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8), C.c_void_p(8),
                      C.c_void_p(8), 10)
     outs = (C.c_void_p * 7)(*([8] * 7))                       # aliases the input
-    assert mfx.lib().mfx_pic_sort(C.byref(cg), C.byref(pp), C.byref(pc), outs, None, 0, None) == mfx.ERR_ARG
+    assert mfx.lib().mfx_pic_sort(C.byref(cg), C.byref(pp), C.byref(pc), outs, None, None, None, 0,
+                                  None) == mfx.ERR_ARG
     assert "in place" in mfx.last_error()
 
 

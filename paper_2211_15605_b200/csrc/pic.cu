@@ -438,8 +438,7 @@ __global__ void k_pic_bin_end(unsigned int *start, long long nbins, unsigned int
 template <int NV>
 struct NodeGather {
     const PicGeo *G;
-    const double *stencil;   // vals row 4: weights (6 rows) then node pairs (3 rows of int2)
-    long long m;
+    const double *x, *y, *z;
     const double *val[NV];
     const unsigned int *orig, *start;
     __device__ void run(long long c, double (&acc)[NV]) const
@@ -477,15 +476,11 @@ struct NodeGather {
                 }
             if (best < 0) break;
             const unsigned int pos = cur[best]++;
+            const double X[3] = {__ldg(x + pos), __ldg(y + pos), __ldg(z + pos)};
             int nd[3][2];
             double w[3][2];
 #pragma unroll
-            for (int ax = 0; ax < 3; ax++) {
-                const int2 n2 = __ldg(reinterpret_cast<const int2 *>(stencil + (size_t)(6 + ax) * m) + pos);
-                nd[ax][0] = n2.x; nd[ax][1] = n2.y;
-                w[ax][0] = __ldg(stencil + (size_t)(2 * ax) * m + pos);
-                w[ax][1] = __ldg(stencil + (size_t)(2 * ax + 1) * m + pos);
-            }
+            for (int ax = 0; ax < 3; ax++) pic_axis(X[ax], G->h[ax], G->n[ax], false, nd[ax], w[ax]);
             double vv[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) vv[v] = __ldg(val[v] + pos);
@@ -524,31 +519,9 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_vals(PicValsArgs a)
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
         const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
         const double om = __ldg(a.om + p);
-        // the stencil (nodes, weights) of the parcel for the node gathers: rows 4..9
-        // hold w[ax][0], w[ax][1]; rows 10..12 the node pair of each axis as two int32
-        const bool ok = parcel_ok(G, X[0], X[1], X[2], om);
-        {
-            int nd[3][2];
-            double w[3][2];
-#pragma unroll
-            for (int ax = 0; ax < 3; ax++) {
-                if (ok) {
-                    pic_axis(X[ax], G.h[ax], G.n[ax], false, nd[ax], w[ax]);
-                } else {                                  // never matches a node, contributes nothing
-                    nd[ax][0] = nd[ax][1] = -1;
-                    w[ax][0] = w[ax][1] = 0.0;
-                }
-            }
-#pragma unroll
-            for (int ax = 0; ax < 3; ax++) {
-                a.vals[(4 + 2 * ax) * a.m + p] = w[ax][0];
-                a.vals[(5 + 2 * ax) * a.m + p] = w[ax][1];
-                reinterpret_cast<int2 *>(a.vals + (size_t)(10 + ax) * a.m)[p] = make_int2(nd[ax][0], nd[ax][1]);
-            }
-        }
-        if (!ok) {
+        if (!parcel_ok(G, X[0], X[1], X[2], om)) {
             atomicMin(&a.hdr->bad_parcel, (unsigned long long)a.orig[p]);
-            for (int v = 0; v < 4; v++) a.vals[v * a.m + p] = 0.0;
+            for (int v = 0; v < (a.drag ? 4 : 1); v++) a.vals[v * a.m + p] = 0.0;
             if (a.Kout) a.Kout[p] = 0.0;
             continue;
         }
@@ -758,16 +731,14 @@ mfx_status pic_deposit_binned(int drag, const mfx_grid *grid, const mfx_params *
     if (drag) {
         NodeArgs4 na;
         na.G = G;
-        na.ng.stencil = vals + 4 * (size_t)m;
-        na.ng.m = m;
+        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
         for (int q = 0; q < 4; q++) { na.ng.val[q] = vals + (size_t)q * (size_t)m; na.out[q] = outs[q]; }
         na.ng.orig = orig; na.ng.start = start;
         k_node_drag<<<nb, kPicThreads, 0, s>>>(na);
     } else {
         NodeArgs1 na;
         na.G = G;
-        na.ng.stencil = vals + 4 * (size_t)m;
-        na.ng.m = m;
+        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
         na.ng.val[0] = vals;
         na.ng.orig = orig; na.ng.start = start;
         na.eps = outs[0];

@@ -477,9 +477,9 @@ struct NodeGather {
             if (best < 0) break;
             const unsigned int pos = cur[best]++;
             const double X[3] = {__ldg(x + pos), __ldg(y + pos), __ldg(z + pos)};
-            // invalid parcels (latched by the value pass) contribute nothing, NaN positions included
-            if (!(X[0] >= 0.0 && X[0] <= G->L[0] && X[1] >= 0.0 && X[1] <= G->L[1] && X[2] >= 0.0 && X[2] <= G->L[2]))
-                continue;
+            // invalid parcels carry value 0 (latched by the value pass); a NaN position
+            // would still turn W * 0 into NaN, so those are skipped here
+            if (X[0] != X[0] || X[1] != X[1] || X[2] != X[2]) continue;
             int nd[3][2];
             double w[3][2];
 #pragma unroll

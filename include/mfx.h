@@ -16,13 +16,15 @@
  *  - All calls are stream-ordered on `stream` (a cudaStream_t passed as
  *    void*; NULL = legacy default stream) and never allocate device memory,
  *    except mfx_ctx_create.  Nothing throws; every call returns mfx_status.
- *  - Argument errors (NULL pointer, bad sizes, odd nx, unsupported boundary
+ *  - Argument errors (NULL pointer, bad sizes, unsupported boundary
  *    combination, workspace too small) return MFX_ERR_ARG before any launch;
  *    mfx_last_error() (thread-local) describes the first error.
  *  - Device-side problems (non-finite coefficient, zero diagonal) are latched
  *    in the workspace and reported by mfx_ws_check() (synchronises `stream`)
  *    with the first offending linear cell index in mfx_last_error().
- *  - Requirements: nx even (TMA/row-stride 16-byte rule), nx, ny, nz >= 2,
+ *  - Requirements: nx, ny, nz >= 2 (an odd nx is accepted; its rows are not
+ *    16-byte aligned, so the TMA kernels give way to the grid-stride ones,
+ *    which produce the same bits), device arrays 16-byte aligned,
  *    x/y sides are no-slip walls, z- INLET or WALL, z+ OUTLET or WALL
  *    (DIRICHLET_TEST: scalar equations only).
  */

@@ -505,7 +505,6 @@ bool grid_ok(const mfx_grid *g, bool scalar)
 {
     if (!g) { set_error("grid is NULL"); return false; }
     if (g->nx < 2 || g->ny < 2 || g->nz < 2) { set_error("grid extents must be >= 2 (got %d %d %d)", g->nx, g->ny, g->nz); return false; }
-    if (g->nx % 2) { set_error("nx must be even (16-byte row stride), got %d", g->nx); return false; }
     if (!(g->dx > 0 && g->dy > 0 && g->dz > 0)) { set_error("spacing must be positive"); return false; }
     if (g->bc_zlo != MFX_BC_WALL && g->bc_zlo != MFX_BC_INLET) { set_error("bc_zlo must be WALL or INLET"); return false; }
     const bool hi_ok = g->bc_zhi == MFX_BC_WALL || g->bc_zhi == MFX_BC_OUTLET ||
@@ -560,7 +559,8 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
         count_launch(4, s, true);
-        if (opt_asm_tma() && !st->blocked) {   // BLOCKED cells: grid-stride kernel (§3.10)
+        // BLOCKED cells (§3.10) and odd nx (rows not 16-byte aligned for TMA): grid-stride kernel
+        if (opt_asm_tma() && !st->blocked && grid->nx % 2 == 0) {
             const mfx_status rc = assemble_mom_tma(kind, G, pr, st, out, resid2, W.hdr, W.part, s);
             count_launch(4, s, false);
             return rc;

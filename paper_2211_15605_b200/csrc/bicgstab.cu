@@ -704,7 +704,20 @@ bool grid_valid(const mfx_grid *g, bool scalar);
 
 // MFX_KERNELS=v1 selects the simple grid-stride kernels (kept as an A/B
 // reference for tests and profiling); default is the TMA z-marching path.
-static bool use_tma() { return opt_solver_path() != 3; }
+// Odd nx: rows are not 16-byte aligned, so TMA boxes and the paired K3 do not
+// apply; the grid-stride kernels (same expressions, same bits) take over.
+static bool use_tma(const Geo &G) { return opt_solver_path() != 3 && G.nx % 2 == 0; }
+
+// TMA tensor maps and the 16-byte pair accesses need 16-byte aligned arrays
+// (torch allocations are; an offset view may not be): refused up front.
+static bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+static bool sys_aligned(const mfx_eqsys *A, const double *x, const double *y)
+{
+    const double *q[11] = {A->aP, A->aE, A->aW, A->aN, A->aS, A->aT, A->aB, A->b, x, y, nullptr};
+    for (int i = 0; i < 10; i++)
+        if (q[i] && !al16(q[i])) return false;
+    return true;
+}
 
 // grid-synchronous solver (path 4) in auto mode: the solver's working set
 // (coefficients + b + 8 vectors) fits comfortably in the 126 MB L2 and the
@@ -727,9 +740,10 @@ mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double
     MFX_ARG_CHECK(sys_ok(kind, A), "bad eqsys for kind %d", kind);
     MFX_ARG_CHECK(x && y, "NULL x/y");
     const Geo G = make_geo(*grid);
+    MFX_ARG_CHECK(!use_tma(G) || sys_aligned(A, x, y), "device arrays must be 16-byte aligned");
     const int nb = reduce_grid(G.N);
     count_launch(0, s, true);
-    if (use_tma()) {
+    if (use_tma(G)) {
         const double *halo[3] = {x, nullptr, nullptr};
         mfx_status st = stencil_launch(0, kind == MFX_EQ_PP, G, halo, A, nullptr, y, nullptr, nullptr, nullptr,
                                        nullptr, 0.0, 0, s);
@@ -751,6 +765,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     MFX_ARG_CHECK(x, "NULL x");
     MFX_ARG_CHECK(tol >= 0.0 && maxit >= 0, "bad tol/maxit");
     const Geo G = make_geo(*grid);
+    MFX_ARG_CHECK(!use_tma(G) || sys_aligned(A, x, nullptr), "device arrays must be 16-byte aligned");
     WsView W;
     if (!ws_view(ws, wsb, G.N, true, W)) return MFX_ERR_ARG;
     const bool sym = kind == MFX_EQ_PP;
@@ -778,7 +793,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     }
     const bool grid_path = path == 4 || (path == 0 && grid_solver_fits(G, sym));
     count_launch(0, s, true);
-    if (use_tma() && !grid_path) {
+    if (use_tma(G) && !grid_path) {
         const double *h0[3] = {x, nullptr, nullptr};
         mfx_status st = stencil_launch(1, sym, G, h0, A, A->b, W.r, nullptr, nullptr, W.hdr, W.part, tol, maxit, s,
                                        sweep_dir(true));
@@ -810,7 +825,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     int launched = 0, chunk = 4;
     while (launched < maxit) {
         int cnt = maxit - launched < chunk ? maxit - launched : chunk;
-        if (use_tma() && use_graphs() && cnt >= GC && (launched & 1) == 0) {
+        if (use_tma(G) && use_graphs() && cnt >= GC && (launched & 1) == 0) {
             cudaGraphExec_t ex;
             mfx_status st = sym ? get_graph<true>(G, A, W, x, nb, ex) : get_graph<false>(G, A, W, x, nb, ex);
             if (st != MFX_OK) return st;
@@ -820,7 +835,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
             }
         }
         for (int q = 0; q < cnt; q++, launched++) {
-            if (use_tma()) {
+            if (use_tma(G)) {
                 mfx_status st = sym ? launch_iteration_tma<true>(G, A, W, x, launched & 1, nb, s)
                                     : launch_iteration_tma<false>(G, A, W, x, launched & 1, nb, s);
                 if (st != MFX_OK) return st;

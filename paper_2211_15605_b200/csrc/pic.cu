@@ -138,6 +138,13 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_eps(PicEpsArgs a)
 
 __global__ void __launch_bounds__(kPicThreads) k_pic_eps_final(double *eps, long long N, double V, double eps_min)
 {
+    if ((uintptr_t)eps & 15) {   // offset view: plain 8-byte accesses
+        for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (long long)gridDim.x * blockDim.x) {
+            const double e = 1.0 - eps[q] / V;
+            eps[q] = e < eps_min ? eps_min : e;
+        }
+        return;
+    }
     const long long n2 = N / 2;
     double2 *e2 = reinterpret_cast<double2 *>(eps);
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n2;

@@ -60,7 +60,8 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-# grids: named configs plus ragged shapes (nx even; ny, nz odd / not tile multiples)
+# grids: named configs plus ragged shapes (ny, nz odd / not tile multiples;
+# "odd": odd nx, rows not 16-byte aligned -> grid-stride kernels, same bits)
 GRIDS = {
     "c1": (16, 16, 32),
     "rag1": (10, 7, 9),
@@ -68,6 +69,7 @@ GRIDS = {
     "thin": (2, 2, 2),
     "tall": (6, 5, 41),
     "tiles": (70, 21, 45),     # several 32x8 assembly tiles with ragged x/y tails
+    "odd": (9, 7, 13),
 }
 
 
@@ -298,7 +300,7 @@ def test_correct_bitwise(mfx, orc, name):
 
 
 # ---------------------------------------------------------------- a-9 SIMPLE
-@pytest.mark.parametrize("name,n_scalars", [("c1", 0), ("rag2", 1), ("tall", 2)])
+@pytest.mark.parametrize("name,n_scalars", [("c1", 0), ("rag2", 1), ("tall", 2), ("odd", 1)])
 def test_simple_iter_111_parity(mfx, orc, name, n_scalars, solver_path):
     g, pr, st = case(name, n_scalars=n_scalars)
     need_path(solver_path, g, False)
@@ -323,12 +325,12 @@ def test_simple_iter_111_parity(mfx, orc, name, n_scalars, solver_path):
 
 # ---------------------------------------------------------------- errors
 def test_argument_errors(mfx):
-    g = Grid(5, 4, 4, 1.0, 1.0, 1.0)        # odd nx
+    g = Grid(1, 4, 4, 1.0, 1.0, 1.0)        # extent < 2
     with pytest.raises(mfx.MfxError) as e:
         mfx.Workspace(synth.make_grid(4, 4, 4))  # fine
-        mfx.spmv(0, g, {k: torch.zeros(80, dtype=torch.float64, device="cuda") for k in mfx.SYS_KEYS},
-                 torch.zeros(80, dtype=torch.float64, device="cuda"))
-    assert e.value.status == mfx.ERR_ARG and "even" in str(e.value)
+        mfx.spmv(0, g, {k: torch.zeros(16, dtype=torch.float64, device="cuda") for k in mfx.SYS_KEYS},
+                 torch.zeros(16, dtype=torch.float64, device="cuda"))
+    assert e.value.status == mfx.ERR_ARG and ">= 2" in str(e.value)
 
 
 def test_nonfinite_latched(mfx):

@@ -470,11 +470,6 @@ struct NodeGather {
                     }
                     nb++;
                 }
-        // head[q]: original index at the front of list q (~0u once exhausted;
-        // original indices are < 2^32 - 1), refilled only for the list consumed
-        unsigned int head[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) head[q] = cur[q] < end[q] ? __ldg(orig + cur[q]) : 0xffffffffu;
 #pragma unroll
         for (int v = 0; v < NV; v++) acc[v] = 0.0;
         for (;;) {
@@ -482,15 +477,12 @@ struct NodeGather {
             unsigned int bo = 0xffffffffu;
 #pragma unroll
             for (int q = 0; q < 8; q++)
-                if (head[q] < bo) { bo = head[q]; best = q; }
-            if (best < 0) break;
-            unsigned int pos = 0;
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                if (q == best) {
-                    pos = cur[q]++;
-                    head[q] = cur[q] < end[q] ? __ldg(orig + cur[q]) : 0xffffffffu;
+                if (cur[q] < end[q]) {
+                    const unsigned int o = __ldg(orig + cur[q]);
+                    if (o < bo) { bo = o; best = q; }
                 }
+            if (best < 0) break;
+            const unsigned int pos = cur[best]++;
             const double X[3] = {__ldg(x + pos), __ldg(y + pos), __ldg(z + pos)};
             // invalid parcels carry value 0 (latched by the value pass); a NaN position
             // would still turn W * 0 into NaN, so those are skipped here

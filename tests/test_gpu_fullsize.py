@@ -1,4 +1,5 @@
-"""Full-size parity at BASELINE.json configuration 2 (128x128x512, 8.4M cells),
+"""Full-size parity at BASELINE.json configuration 2 (128x128x512, 8.4M cells;
+configuration 4, 256x256x512, in the last test),
 in the launch configuration bench.py uses.  The oracle computes the whole
 assembly and two BiCGSTAB iterations at this size (~20 s of CPU); the SIMPLE
 iteration is checked through properties that hold at any size (continuity
@@ -122,3 +123,32 @@ def test_c2_simple_iteration_in_bench_configuration(mfx, orc, c2):
     # the p' solve either met its tolerance or ran to maxit (last iterate returned)
     assert out["iters"][3] == pr.lin_maxit_pp or out["status"][3] == 0
     ctx.close()
+
+
+def test_c4_largest_grid_pp_and_momentum(mfx, orc):
+    """BASELINE.json configuration 4 (256x256x512, 33.5M cells, the largest
+    single-GPU size): p' and w-momentum assembly, the 7-point apply and one
+    p' BiCGSTAB iteration equal the oracle's bitwise (~1 min of oracle CPU)."""
+    g, pr, st = synth.config_case(4)
+    rng = np.random.default_rng(4)
+    dv = [rng.uniform(1e-4, 1e-3, g.n) for _ in range(3)]
+    ref, cont, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+    ws = mfx.Workspace(g)
+    sd = {k: dev(v) for k, v in st.items()}
+    out, res2 = mfx.assemble_eq(mfx.EQ_PP, g, pr, sd, ws, star=[sd["u"], sd["v"], sd["w"]] + [dev(a) for a in dv])
+    for k in ("aP", "aE", "aN", "aT", "b"):
+        assert np.array_equal(host(out[k]), ref[k]), k
+    assert host(res2)[0] == cont
+    x = rng.normal(size=g.n)
+    assert np.array_equal(host(mfx.spmv(mfx.EQ_PP, g, out, dev(x))), orc.spmv(g, ref, x))
+    oref = orc.bicgstab(g, ref, np.zeros(g.n), 1e-6, 1)
+    xg = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+    info = mfx.bicgstab_solve(mfx.EQ_PP, g, out, xg, 1e-6, 1, ws)
+    assert info["iters"] == oref["iters"] == 1
+    assert np.array_equal(host(xg), oref["x"])
+    del out, xg
+    mref, mr2, _ = orc.assemble_mom(g, pr, 2, st)
+    mout, mres2 = mfx.assemble_eq(mfx.EQ_W, g, pr, sd, ws)
+    for k in ("aP", "aE", "aW", "aN", "aS", "aT", "aB", "b", "d"):
+        assert np.array_equal(host(mout[k]), mref[k]), k
+    assert np.array_equal(host(mres2), mr2)

@@ -4,7 +4,8 @@
                 single-cluster solver / grid-synchronous solver, correction);
   pic:          eps + drag deposits and one SIMPLE iteration with implicit
                 particle coupling (PIC kernels, exchange phase 3 path);
-  bfs:          one SIMPLE iteration with BLOCKED cells (step geometry)."""
+  bfs:          one SIMPLE iteration with BLOCKED cells (step geometry);
+  odd:          one SIMPLE iteration on an odd-nx grid (grid-stride kernels)."""
 import os
 import sys
 
@@ -25,8 +26,8 @@ elif mode == "pic":
     st = synth.make_state(g, 99, pr)
     asg = "111[1]"
 else:
-    mfx.set_option("solver_path", int(mode))
-    g = synth.make_grid(34, 11, 13)
+    mfx.set_option("solver_path", 1 if mode == "odd" else int(mode))
+    g = synth.make_grid(33 if mode == "odd" else 34, 11, 13)
     st = synth.make_state(g, 99, pr, n_scalars=1)
     asg = "111[1]1"
 sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}

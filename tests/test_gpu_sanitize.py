@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-@pytest.mark.parametrize("path", ["1", "2", "4", "pic", "bfs"])
+@pytest.mark.parametrize("path", ["1", "2", "4", "pic", "bfs", "odd"])
 def test_sanitizer_clean(tool, path):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():

@@ -15,11 +15,13 @@ Parity status per function:
   or_fsum / or_dot / or_sumabs ... pinned (math.fsum, fractions.Fraction)
   or_spmv ........................ pinned (dense matrix brute force)
   or_bicgstab .................... pinned (dense LU, k-eigenvalue count, SPEC examples)
-  or_assemble_pp ................. pinned (symmetry, Laplacian closed form)
-  or_assemble_scalar ............. pinned (geometric recurrence, pure convection)
-  or_assemble_mom ................ partially pinned (quiescent, hydrostatic, inertia-only,
-                                   dominance); the general 3-D row with every term
-                                   active is "parity unpinned" beyond these cases.
+  or_assemble_pp ................. pinned (symmetry, Laplacian closed form, S:367-369,
+                                   consistency with Eq. 1 under mesh refinement)
+  or_assemble_scalar ............. pinned (geometric recurrence, pure convection,
+                                   consistency under mesh refinement)
+  or_assemble_mom ................ pinned (quiescent, hydrostatic, inertia-only, dominance;
+                                   the general 3-D row with every term active by
+                                   consistency with Eq. 2 under mesh refinement)
   or_correct ..................... pinned (continuity identity b(u_corr) = b(u*) - A p')
   or_pic_deposit_eps / or_pic_drag  pinned (partition of unity, node coincidence, symmetry,
                                    trilinear exactness on linear fields, Dalla Valle

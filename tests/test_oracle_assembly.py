@@ -3,8 +3,8 @@
 
 Each test fixes the oracle to something other than itself: closed forms,
 exact identities of the discretisation, or the worked examples of
-SPEC.md:358-387.  The general momentum row with every term active is only
-pinned through these special cases ("parity unpinned" beyond them).
+SPEC.md:358-387.  The general rows with every term active are pinned by
+consistency with the PDEs under mesh refinement (test_oracle_consistency.py).
 """
 import json
 import os

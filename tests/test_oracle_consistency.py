@@ -143,9 +143,9 @@ def mom_terms(c, X):
     }
 
 
-def _mom_errors(orc, n, c, drop=None):
+def _mom_errors(orc, n, c, drop=None, upwind=0):
     g, h, cc, st, ijk = make_case(n)
-    p = Params(rho=PR["rho"], mu=PR["mu"], g=PR["g"], dt=PR["dt"], urf_mom=PR["urf_mom"])
+    p = Params(rho=PR["rho"], mu=PR["mu"], g=PR["g"], dt=PR["dt"], urf_mom=PR["urf_mom"], face_eps_upwind=upwind)
     sys, _, rc = orc.assemble_mom(g, p, c, st)
     assert rc == 0
     V = g.dx * g.dy * g.dz
@@ -168,6 +168,16 @@ def test_momentum_row_consistent_with_eq2(orc, c):
         assert np.max(np.abs(v)) > 0.05 * scale, k
     # first-order convergence (upwind convection; measured ratio 0.30-0.35 for
     # 4x refinement, 0.25 asymptotically), small at the fine grid
+    assert e64 < 0.45 * e16, (e16, e64)
+    assert e64 < 0.05 * scale, (e64, scale)
+
+
+@pytest.mark.parametrize("c", [0, 1, 2])
+def test_momentum_row_with_upwinded_face_eps_consistent(orc, c):
+    """the upwinded (eps rho)_f convective mass fluxes keep the
+    row a consistent (first-order) discretisation of Eq. 2."""
+    e16, scale, _ = _mom_errors(orc, 16, c, upwind=1)
+    e64, _, _ = _mom_errors(orc, 64, c, upwind=1)
     assert e64 < 0.45 * e16, (e16, e64)
     assert e64 < 0.05 * scale, (e64, scale)
 

@@ -458,20 +458,21 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
         }
     }
 
-    if (C::NDOT == 0) return;
-    __shared__ dd sh[(C::NW + 1) * ND];
-    dd v[ND], out[ND];
+    if constexpr (C::NDOT > 0) {
+        __shared__ dd sh[(C::NW + 1) * ND];
+        dd v[ND], out[ND];
 #pragma unroll
-    for (int d = 0; d < ND; d++) {
-        v[d] = acc[d][0].get();
+        for (int d = 0; d < ND; d++) {
+            v[d] = acc[d][0].get();
 #pragma unroll
-        for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+            for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+        }
+        if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+        SolverScalars &Sc = a.h->sc;
+        if (MODE == SM_SETUP) bicg_setup(Sc, dd_round(out[0]), dd_round(out[1]), a.tol, a.maxit);
+        else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
+        else if (MODE == SM_K2) bicg_k2_tail(Sc, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
     }
-    if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
-    SolverScalars &Sc = a.h->sc;
-    if (MODE == SM_SETUP) bicg_setup(Sc, dd_round(out[0]), dd_round(out[1]), a.tol, a.maxit);
-    else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
-    else if (MODE == SM_K2) bicg_k2_tail(Sc, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
 }
 
 // ------------------------------------------------------------------ host side

@@ -271,32 +271,51 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             const uint8_t *st = stages + (size_t)s * C::STAGE_B;
             double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
-            // step 1: value on the halo'd plane, two x-adjacent cells per item
-            for (int pi = tid; pi < C::HX * C::HY / 2; pi += C::NT) {
-                double2 val = make_double2(0.0, 0.0);
+            // step 1: value on the halo'd plane, PPI pairs of x-adjacent cells per
+            // item.  PPI = 2 when one pair per thread would need a second, mostly
+            // idle pass over the plane (K2 at 64x8 tiles, 2 cells per thread: 340
+            // pairs for 256 threads); all loads of an item are issued first.
+            constexpr int NPAIR = C::HX * C::HY / 2;
+            constexpr int PPI = (NPAIR > C::NT && NPAIR % 2 == 0) ? 2 : 1;
+            for (int it = tid; it < NPAIR / PPI; it += C::NT) {
+                double2 val[PPI];
                 if (!virt) {
                     const double2 *h0 = (const double2 *)(st + C::OFF_HALO);
-                    if (MODE == SM_SPMV || MODE == SM_SETUP) {
-                        val = h0[pi];
-                    } else if (MODE == SM_K1) {
-                        const double2 rv = h0[pi];
-                        const double2 pv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
-                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + 2 * C::HALO_B))[pi];
-                        if (rst) {
-                            val.x = fma(beta, fma(-omega, 0.0, 0.0), rv.x);
-                            val.y = fma(beta, fma(-omega, 0.0, 0.0), rv.y);
-                        } else {
-                            val.x = fma(beta, fma(-omega, vv.x, pv.x), rv.x);
-                            val.y = fma(beta, fma(-omega, vv.y, pv.y), rv.y);
+                    double2 rv[PPI], pv[PPI], vv[PPI];
+#pragma unroll
+                    for (int u = 0; u < PPI; u++) {
+                        const int pi = it * PPI + u;
+                        rv[u] = h0[pi];
+                        if (MODE == SM_K1) {
+                            pv[u] = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
+                            vv[u] = ((const double2 *)(st + C::OFF_HALO + 2 * C::HALO_B))[pi];
+                        } else if (MODE == SM_K2) {
+                            vv[u] = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
                         }
-                    } else {
-                        const double2 rv = h0[pi];
-                        const double2 vv = ((const double2 *)(st + C::OFF_HALO + C::HALO_B))[pi];
-                        val.x = fma(-alpha, vv.x, rv.x);
-                        val.y = fma(-alpha, vv.y, rv.y);
                     }
+#pragma unroll
+                    for (int u = 0; u < PPI; u++) {
+                        if (MODE == SM_SPMV || MODE == SM_SETUP) {
+                            val[u] = rv[u];
+                        } else if (MODE == SM_K1) {
+                            if (rst) {
+                                val[u].x = fma(beta, fma(-omega, 0.0, 0.0), rv[u].x);
+                                val[u].y = fma(beta, fma(-omega, 0.0, 0.0), rv[u].y);
+                            } else {
+                                val[u].x = fma(beta, fma(-omega, vv[u].x, pv[u].x), rv[u].x);
+                                val[u].y = fma(beta, fma(-omega, vv[u].y, pv[u].y), rv[u].y);
+                            }
+                        } else {
+                            val[u].x = fma(-alpha, vv[u].x, rv[u].x);
+                            val[u].y = fma(-alpha, vv[u].y, rv[u].y);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < PPI; u++) val[u] = make_double2(0.0, 0.0);
                 }
-                ((double2 *)P)[pi] = val;
+#pragma unroll
+                for (int u = 0; u < PPI; u++) ((double2 *)P)[it * PPI + u] = val[u];
             }
             double czcur[CPT];
             if (CPT == 2 && SYM && !virt) {

@@ -632,7 +632,9 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
     // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
     static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8 pairs, 3: 32x16 pairs, 4: 32x8, 5: 64x8
     int t = tile;
-    if (!t) t = G.nx <= 32 ? (SYM ? 3 : 4) : ((MODE == SM_K1 || !SYM) ? 1 : 2);
+    // measured at c2 (profiles/r01s7_tile_sweep.log): p' K1 is fastest at 64x4,
+    // everything else (p' K2, the 7-coefficient kernels) at 64x8 pairs
+    if (!t) t = G.nx <= 32 ? (SYM ? 3 : 4) : ((MODE == SM_K1 && SYM) ? 1 : 2);
     if (t == 2) return run_tile<MODE, SYM, 64, 8, 2>(G, halo, coef, extra, a, s);
     if (t == 3) return run_tile<MODE, SYM, 32, 16, 2>(G, halo, coef, extra, a, s);
     if (t == 4) return run_tile<MODE, SYM, 32, 8, 1>(G, halo, coef, extra, a, s);

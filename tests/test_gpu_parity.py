@@ -333,6 +333,28 @@ def test_argument_errors(mfx):
     assert e.value.status == mfx.ERR_ARG and ">= 2" in str(e.value)
 
 
+def test_misaligned_arrays_refused_on_tma_path(mfx, orc):
+    """TMA tensor maps need 16-byte aligned arrays: an 8-byte aligned view is
+    refused before any launch (even nx); with odd nx the grid-stride kernels
+    accept it and give the oracle's bits."""
+    g, pr, st = case("rag2")
+    ref, _, _ = orc.assemble_mom(g, pr, 0, st)
+    sysd = {k: torch.from_numpy(ref[k]).cuda() for k in mfx.SYS_KEYS}
+    x = np.random.default_rng(5).normal(size=g.n)
+    buf = torch.zeros(g.n + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(x).cuda()
+    with pytest.raises(mfx.MfxError) as e:
+        mfx.spmv(0, g, sysd, buf[1:])
+    assert e.value.status == mfx.ERR_ARG and "aligned" in str(e.value)
+    go, pro, sto = case("odd")
+    refo, _, _ = orc.assemble_mom(go, pro, 0, sto)
+    sysd = {k: torch.from_numpy(refo[k]).cuda() for k in mfx.SYS_KEYS}
+    xo = np.random.default_rng(6).normal(size=go.n)
+    bufo = torch.zeros(go.n + 1, dtype=torch.float64, device="cuda")
+    bufo[1:] = torch.from_numpy(xo).cuda()
+    assert np.array_equal(host(mfx.spmv(0, go, sysd, bufo[1:])), orc.spmv(go, refo, xo))
+
+
 def test_nonfinite_latched(mfx):
     g, pr, st = case("rag1")
     st = dict(st)

@@ -329,3 +329,19 @@ def test_pic_sort_empty_and_large(mfx):
     srt = mfx.pic_sort(g, pic, {k: dev(v) for k, v in pc.items()})
     bc = base_cell(g, host(srt["x"]), host(srt["y"]), host(srt["z"]))
     assert np.all(np.diff(bc) >= 0) and np.array_equal(np.sort(host(srt["omega"])), np.sort(pc["omega"]))
+
+
+def test_pic_eps_into_offset_view(mfx, orc):
+    """An eps output that is an 8-byte (not 16-byte) aligned view takes the
+    plain-access finalize path: same values as the oracle."""
+    g, st, pic, pc = case(22, 14, 37, 20000, 41)
+    ws = mfx.Workspace(g)
+    buf = torch.zeros(g.n + 1, dtype=torch.float64, device="cuda")
+    view = buf[1:]
+    assert view.data_ptr() % 16 == 8
+    mfx.pic_deposit_eps(g, pic, {k: dev(v) for k, v in pc.items()}, ws, eps=view)
+    ws.check()
+    eps_o, rc = orc.pic_deposit_eps(g, pic, pc)
+    assert rc == 0
+    assert np.all(np.abs(host(view) - eps_o) <= TOL_SUM)
+    assert host(buf)[0] == 0.0

@@ -272,7 +272,7 @@ def measure_pic(mfx, torch):
             scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
             t_sort, _ = _ev_ms(torch, lambda: mfx.pic_sort(g, pic, d, out=srt, scratch=scratch), 7)
             t_drag_sorted, _ = _ev_ms(torch, lambda: mfx.pic_drag(g, pr, pic, srt, eps, u, v, w, ws, out=outs), 7)
-            vals = torch.empty(4 * m, dtype=torch.float64, device="cuda")
+            vals = torch.empty(7 * m, dtype=torch.float64, device="cuda")
             t_gather, _ = _ev_ms(torch, lambda: mfx.pic_drag_binned(g, pr, pic, srt, eps, u, v, w, ws, out=outs,
                                                                     vals=vals), 7)
             t_eps_gather, _ = _ev_ms(torch, lambda: mfx.pic_deposit_eps_binned(g, pic, srt, ws, eps=eps, vals=vals), 7)

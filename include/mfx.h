@@ -212,7 +212,9 @@ mfx_status mfx_pic_sort(const mfx_grid *grid, const mfx_pic_params *pic, const m
  * stencil contains it -- the exact sequence of additions of the parcel-ordered
  * definition, so the fields are bitwise those of the
  * definition and do not depend on scheduling (no atomics).  vals: device
- * scratch of n (eps) or 4 n (drag) doubles.  K (may be NULL) is per binned
+ * scratch of 4 n (eps) or 7 n (drag) doubles, n = parcel count: the
+ * per-parcel deposit values, then each parcel's lattice coordinates (computed
+ * once, read by the up to 8 nodes that gather the parcel).  K (may be NULL) is per binned
  * parcel.  Invalid parcels contribute nothing and are latched in ws by their
  * original index. */
 mfx_status mfx_pic_deposit_eps_binned(const mfx_grid *grid, const mfx_pic_params *pic,

@@ -350,7 +350,7 @@ def pic_deposit_eps_binned(grid, pic, binned: dict, ws: Workspace, eps=None, val
     m = binned["x"].numel()
     dev = binned["x"].device
     eps = eps if eps is not None else torch.empty(n, dtype=torch.float64, device=dev)
-    vals = vals if vals is not None else torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    vals = vals if vals is not None else torch.empty(max(4 * m, 1), dtype=torch.float64, device=dev)
     _check(_lib.mfx_pic_deposit_eps_binned(C.byref(c_grid(grid)), C.byref(PicParams(pic.d_p, pic.eps_min)),
                                            C.byref(c_parcels(binned)), C.c_void_p(binned["orig"].data_ptr()),
                                            C.c_void_p(binned["bin_start"].data_ptr()), _ptr(eps, n),
@@ -368,7 +368,7 @@ def pic_drag_binned(grid, params, pic, binned: dict, eps, u, v, w, ws: Workspace
     dev = eps.device
     out = out if out is not None else {k: torch.empty(n, dtype=torch.float64, device=dev)
                                        for k in ("beta", "sbeta_u", "sbeta_v", "sbeta_w")}
-    vals = vals if vals is not None else torch.empty(max(4 * m, 1), dtype=torch.float64, device=dev)
+    vals = vals if vals is not None else torch.empty(max(7 * m, 1), dtype=torch.float64, device=dev)
     _check(_lib.mfx_pic_drag_binned(C.byref(c_grid(grid)), C.byref(c_params(params)),
                                     C.byref(PicParams(pic.d_p, pic.eps_min)), C.byref(c_parcels(binned)),
                                     C.c_void_p(binned["orig"].data_ptr()), C.c_void_p(binned["bin_start"].data_ptr()),

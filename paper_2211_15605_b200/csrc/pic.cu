@@ -40,9 +40,10 @@ struct PicGeo {
     long long N;
 };
 
-__device__ __forceinline__ void pic_axis(double x, double h, int n, bool face, int nd[2], double w[2])
+// stencil along one axis from the lattice coordinate xi (= x/h - 0.5 for cell
+// centres, x/h - 1 for the face lattice)
+__device__ __forceinline__ void pic_axis_xi(double xi, int n, bool face, int nd[2], double w[2])
 {
-    const double xi = face ? x / h - 1.0 : x / h - 0.5;
     const double fl = floor(xi);
     const double f = xi - fl;
     int i0 = (int)fl, i1 = i0 + 1;
@@ -51,6 +52,13 @@ __device__ __forceinline__ void pic_axis(double x, double h, int n, bool face, i
     i1 = i1 < lo ? lo : (i1 > n - 1 ? n - 1 : i1);
     nd[0] = i0; nd[1] = i1;
     w[0] = 1.0 - f; w[1] = f;
+}
+
+__device__ __forceinline__ double pic_xi(double x, double h, bool face) { return face ? x / h - 1.0 : x / h - 0.5; }
+
+__device__ __forceinline__ void pic_axis(double x, double h, int n, bool face, int nd[2], double w[2])
+{
+    pic_axis_xi(pic_xi(x, h, face), n, face, nd, w);
 }
 
 __device__ __forceinline__ long long pic_lin(const PicGeo &G, int i, int j, int k)
@@ -445,7 +453,7 @@ __global__ void k_pic_bin_end(unsigned int *start, long long nbins, unsigned int
 template <int NV>
 struct NodeGather {
     const PicGeo *G;
-    const double *x, *y, *z;
+    const double *xi[3];     // cell-centre lattice coordinates per binned parcel (k_pic_vals)
     const double *val[NV];
     const unsigned int *orig, *start;
     __device__ void run(long long c, double (&acc)[NV]) const
@@ -483,14 +491,14 @@ struct NodeGather {
                 }
             if (best < 0) break;
             const unsigned int pos = cur[best]++;
-            const double X[3] = {__ldg(x + pos), __ldg(y + pos), __ldg(z + pos)};
+            const double X[3] = {__ldg(xi[0] + pos), __ldg(xi[1] + pos), __ldg(xi[2] + pos)};
             // invalid parcels carry value 0 (latched by the value pass); a NaN position
             // would still turn W * 0 into NaN, so those are skipped here
             if (X[0] != X[0] || X[1] != X[1] || X[2] != X[2]) continue;
             int nd[3][2];
             double w[3][2];
 #pragma unroll
-            for (int ax = 0; ax < 3; ax++) pic_axis(X[ax], G->h[ax], G->n[ax], false, nd[ax], w[ax]);
+            for (int ax = 0; ax < 3; ax++) pic_axis_xi(X[ax], G->n[ax], false, nd[ax], w[ax]);
             double vv[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) vv[v] = __ldg(val[v] + pos);
@@ -516,6 +524,7 @@ struct PicValsArgs {
     long long m;
     const double *eps, *u, *v, *w;
     double *vals;           // [4][m]: K/V, (K u)/V, (K v)/V, (K w)/V   or [1][m]: omega Vs (eps mode)
+    double *xi;             // [3][m]: cell-centre lattice coordinates x/h - 0.5 (the gathers' stencils)
     double *Kout;
     const unsigned int *orig;
     WsHeader *hdr;
@@ -529,6 +538,8 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_vals(PicValsArgs a)
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
         const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
         const double om = __ldg(a.om + p);
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) a.xi[ax * a.m + p] = pic_xi(X[ax], G.h[ax], false);
         if (!parcel_ok(G, X[0], X[1], X[2], om)) {
             atomicMin(&a.hdr->bad_parcel, (unsigned long long)a.orig[p]);
             for (int v = 0; v < (a.drag ? 4 : 1); v++) a.vals[v * a.m + p] = 0.0;
@@ -733,6 +744,7 @@ mfx_status pic_deposit_binned(int drag, const mfx_grid *grid, const mfx_params *
         a.m = m;
         a.eps = eps_in; a.u = u; a.v = v; a.w = w;
         a.vals = vals; a.Kout = Kout; a.orig = orig; a.hdr = (WsHeader *)ws; a.drag = drag;
+        a.xi = vals + (size_t)(drag ? 4 : 1) * (size_t)m;
         count_launch(drag ? 11 : 10, s, true);
         k_pic_vals<<<pic_grid(m), kPicThreads, 0, s>>>(a);
         count_launch(drag ? 11 : 10, s, false);
@@ -741,14 +753,14 @@ mfx_status pic_deposit_binned(int drag, const mfx_grid *grid, const mfx_params *
     if (drag) {
         NodeArgs4 na;
         na.G = G;
-        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
+        for (int ax = 0; ax < 3; ax++) na.ng.xi[ax] = vals + (size_t)(4 + ax) * (size_t)m;
         for (int q = 0; q < 4; q++) { na.ng.val[q] = vals + (size_t)q * (size_t)m; na.out[q] = outs[q]; }
         na.ng.orig = orig; na.ng.start = start;
         k_node_drag<<<nb, kPicThreads, 0, s>>>(na);
     } else {
         NodeArgs1 na;
         na.G = G;
-        na.ng.x = pc->x; na.ng.y = pc->y; na.ng.z = pc->z;
+        for (int ax = 0; ax < 3; ax++) na.ng.xi[ax] = vals + (size_t)(1 + ax) * (size_t)m;
         na.ng.val[0] = vals;
         na.ng.orig = orig; na.ng.start = start;
         na.eps = outs[0];

@@ -293,7 +293,7 @@ struct mfx_ctx {
     double *pic_sorted[7];         // binned copy (mfx_pic_sort), capacity pic_cap
     unsigned int *pic_orig;        // original index per binned parcel
     unsigned int *pic_start;       // bin starts (N + 1)
-    double *pic_vals;              // 4 x pic_cap per-parcel deposit values
+    double *pic_vals;              // 7 x pic_cap: per-parcel deposit values + lattice coordinates
     long long pic_cap;
     void *pic_scratch;
     size_t pic_scratch_bytes;
@@ -898,7 +898,7 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
                 }
                 mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_orig, sizeof(unsigned int) * (size_t)n);
                 if (st != MFX_OK) return st;
-                st = mfx::ctx_alloc(c, (void **)&c->pic_vals, 4 * sizeof(double) * (size_t)n);
+                st = mfx::ctx_alloc(c, (void **)&c->pic_vals, 7 * sizeof(double) * (size_t)n);
                 if (st != MFX_OK) return st;
                 c->pic_cap = n;
             }

@@ -71,14 +71,16 @@ __device__ __forceinline__ bool parcel_ok(const PicGeo &G, double x, double y, d
     return x >= 0.0 && x <= G.L[0] && y >= 0.0 && y <= G.L[1] && z >= 0.0 && z <= G.L[2] && om >= 0.0;
 }
 
-// trilinear value of field f on the lattice whose face axis is FA (-1: cell centres)
+// trilinear value of field f on the lattice whose face axis is FA (-1: cell
+// centres), from Q[a] = x_a / h_a (one IEEE quotient per axis shared by the
+// four lattices: x/h - 0.5 and x/h - 1 are exactly pic_xi's expressions)
 template <int FA>
-__device__ __forceinline__ double pic_interp(const PicGeo &G, const double *__restrict__ f, const double X[3])
+__device__ __forceinline__ double pic_interp(const PicGeo &G, const double *__restrict__ f, const double Q[3])
 {
     int nd[3][2];
     double w[3][2];
 #pragma unroll
-    for (int a = 0; a < 3; a++) pic_axis(X[a], G.h[a], G.n[a], a == FA, nd[a], w[a]);
+    for (int a = 0; a < 3; a++) pic_axis_xi(a == FA ? Q[a] - 1.0 : Q[a] - 0.5, G.n[a], a == FA, nd[a], w[a]);
     double v8[8];
 #pragma unroll
     for (int kk = 0; kk < 2; kk++)
@@ -243,10 +245,11 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_drag(PicDragArgs a)
             atomicMin(&a.hdr->bad_parcel, (unsigned long long)p);
             continue;
         }
-        const double eg = pic_interp<-1>(G, a.eps, X);
-        const double ug0 = pic_interp<0>(G, a.u, X);
-        const double ug1 = pic_interp<1>(G, a.v, X);
-        const double ug2 = pic_interp<2>(G, a.w, X);
+        const double Q[3] = {X[0] / G.h[0], X[1] / G.h[1], X[2] / G.h[2]};
+        const double eg = pic_interp<-1>(G, a.eps, Q);
+        const double ug0 = pic_interp<0>(G, a.u, Q);
+        const double ug1 = pic_interp<1>(G, a.v, Q);
+        const double ug2 = pic_interp<2>(G, a.w, Q);
         const double sx = ug0 - up[0], sy = ug1 - up[1], sz = ug2 - up[2];
         const double slip = sqrt((sx * sx + sy * sy) + sz * sz);
         const double K = drag_coef(a.rho, a.mu, a.dp, G.Vs, eg, slip, om);
@@ -538,8 +541,9 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_vals(PicValsArgs a)
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < a.m; p += (long long)gridDim.x * blockDim.x) {
         const double X[3] = {__ldg(a.x + p), __ldg(a.y + p), __ldg(a.z + p)};
         const double om = __ldg(a.om + p);
+        const double Q[3] = {X[0] / G.h[0], X[1] / G.h[1], X[2] / G.h[2]};
 #pragma unroll
-        for (int ax = 0; ax < 3; ax++) a.xi[ax * a.m + p] = pic_xi(X[ax], G.h[ax], false);
+        for (int ax = 0; ax < 3; ax++) a.xi[ax * a.m + p] = Q[ax] - 0.5;     // = pic_xi(X, h, false)
         if (!parcel_ok(G, X[0], X[1], X[2], om)) {
             atomicMin(&a.hdr->bad_parcel, (unsigned long long)a.orig[p]);
             for (int v = 0; v < (a.drag ? 4 : 1); v++) a.vals[v * a.m + p] = 0.0;
@@ -551,10 +555,10 @@ __global__ void __launch_bounds__(kPicThreads) k_pic_vals(PicValsArgs a)
             continue;
         }
         const double up[3] = {__ldg(a.up + p), __ldg(a.vp + p), __ldg(a.wp + p)};
-        const double eg = pic_interp<-1>(G, a.eps, X);
-        const double ug0 = pic_interp<0>(G, a.u, X);
-        const double ug1 = pic_interp<1>(G, a.v, X);
-        const double ug2 = pic_interp<2>(G, a.w, X);
+        const double eg = pic_interp<-1>(G, a.eps, Q);
+        const double ug0 = pic_interp<0>(G, a.u, Q);
+        const double ug1 = pic_interp<1>(G, a.v, Q);
+        const double ug2 = pic_interp<2>(G, a.w, Q);
         const double sx = ug0 - up[0], sy = ug1 - up[1], sz = ug2 - up[2];
         const double slip = sqrt((sx * sx + sy * sy) + sz * sz);
         const double K = drag_coef(a.rho, a.mu, a.dp, G.Vs, eg, slip, om);

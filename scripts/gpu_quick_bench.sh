@@ -1,3 +1,4 @@
+# Quick check after a kernel change: solver/SIMPLE parity subset, p' and w iteration timings, short bench.
 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q -k "bicgstab or simple or spmv or c2 or c4" 2>&1 | tail -2
 for i in 1 2 3; do timeout 300 python scripts/prof_solve.py --kind pp --iters 200 2>&1 | tail -2; done
 timeout 300 python scripts/prof_solve.py --kind w --iters 20 2>&1 | tail -2

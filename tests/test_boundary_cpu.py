@@ -231,3 +231,21 @@ def test_state_load_rejects_missing_file(mfx, tmp_path):
     rc = mfx.lib().mfx_state_load(str(tmp_path / "nope.mpxd").encode(), C.byref(mfx.c_grid(g)), C.byref(st), 0,
                                   None, 0, None, None, None, None)
     assert rc == mfx.ERR_ARG and "cannot open" in mfx.last_error()
+
+
+def test_grid_validation_before_any_launch(mfx):
+    """Grid checks run before any launch (no GPU needed): an extent below 2 is
+    refused with its own message; an odd nx passes grid validation (it runs the
+    grid-stride kernels on a GPU) and the call stops at the next check, the
+    NULL system arrays."""
+    import synth
+    eq = mfx.Eqsys()
+    for nx, ok in ((1, False), (9, True), (10, True)):
+        cg = mfx.c_grid(synth.make_grid(nx, 6, 8))
+        st = mfx.lib().mfx_spmv(0, C.byref(cg), C.byref(eq), None, None, None)
+        assert st == mfx.ERR_ARG
+        msg = mfx.last_error()
+        if ok:
+            assert ">= 2" not in msg and "even" not in msg, msg
+        else:
+            assert ">= 2" in msg, msg

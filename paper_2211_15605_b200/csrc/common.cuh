@@ -105,13 +105,8 @@ struct Acc {
     {
         double ph = a * b;
         double pl = fma(a, b, -ph);
-        // error-free sum of s and ph: Fast2Sum on the operands ordered by
-        // magnitude gives the same (t, e) as TwoSum (both exact) in 3 adds
-        // instead of 6; the ordering is a compare and two selects
-        const bool sw = fabs(s) < fabs(ph);
-        const double hi = sw ? ph : s, lo = sw ? s : ph;
         double t, e;
-        fast_two_sum(hi, lo, t, e);
+        two_sum(s, ph, t, e);
         s = t;
         c = c + (e + pl);
     }

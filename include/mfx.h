@@ -103,6 +103,9 @@ typedef struct {
     int status;                /* mfx_status */
     int restarts;              /* breakdown restarts taken (0 or 1) */
     double rel_resid;          /* recursive ||r|| / ||b|| at exit */
+    double true_rel_resid;     /* ||b - A x|| / ||b|| of the returned iterate, from one extra correctly
+                                  rounded apply at exit (reading Q2; 0 when b = 0); with info == NULL
+                                  it is not computed */
 } mfx_solve_info;
 
 typedef struct {
@@ -111,6 +114,8 @@ typedef struct {
     int iters[8];                   /* u, v, w, pp, phi0..3 */
     int status[8];
     int converged;                  /* max(R_u,R_v,R_w,R_cont) < tol */
+    double rel_resid[8];            /* per equation: recursive ||r||/||b|| at solver exit */
+    double true_rel_resid[8];       /* per equation: ||b - A x||/||b|| of the returned iterate */
 } mfx_resid;
 
 const char *mfx_last_error(void);
@@ -412,6 +417,16 @@ int mfx_get_option(const char *key);
 
 /* Number of libmfx kernel launches issued since process start. */
 long long mfx_launch_count(void);
+
+/* CUDA-graph cache of the BiCGSTAB iteration loop.  A graph is
+ * keyed on every array pointer it bakes in plus nx, ny, nz, the p' flag, the
+ * PDL option and the device, so a replay always matches the launches it
+ * replaces.  mfx_ctx_destroy evicts the graphs of its workspaces; callers that
+ * free their own workspaces may call mfx_graph_cache_clear (releases every
+ * cached graph; stream-ordered, in-flight replays complete).  The cache holds
+ * at most 64 graphs (least recently used out first). */
+void mfx_graph_cache_clear(void);
+size_t mfx_graph_cache_size(void);
 
 #ifdef __cplusplus
 }

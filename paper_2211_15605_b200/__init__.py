@@ -69,13 +69,14 @@ class Eqsys(C.Structure):
 
 
 class SolveInfo(C.Structure):
-    _fields_ = [("iters", C.c_int), ("status", C.c_int), ("restarts", C.c_int), ("rel_resid", C.c_double)]
+    _fields_ = [("iters", C.c_int), ("status", C.c_int), ("restarts", C.c_int), ("rel_resid", C.c_double),
+                ("true_rel_resid", C.c_double)]
 
 
 class Resid(C.Structure):
     _fields_ = [("R_u", C.c_double), ("R_v", C.c_double), ("R_w", C.c_double), ("R_cont", C.c_double),
                 ("R_phi", C.c_double * 4), ("iters", C.c_int * 8), ("status", C.c_int * 8),
-                ("converged", C.c_int)]
+                ("converged", C.c_int), ("rel_resid", C.c_double * 8), ("true_rel_resid", C.c_double * 8)]
 
 
 class Assignment(C.Structure):
@@ -164,6 +165,8 @@ _sigs = {
     "mfx_prof_reset": (None, []),
     "mfx_prof_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "mfx_launch_count": (C.c_longlong, []),
+    "mfx_graph_cache_clear": (None, []),
+    "mfx_graph_cache_size": (C.c_size_t, []),
     "mfx_set_option": (C.c_int, [C.c_char_p, C.c_int]),
     "mfx_get_option": (C.c_int, [C.c_char_p]),
 }
@@ -298,7 +301,8 @@ def bicgstab_solve(kind, grid, sysd: dict, x, tol: float, maxit: int, ws: Worksp
     _check(st, "mfx_bicgstab_solve", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
     if not sync:
         return None
-    return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid)
+    return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid,
+                true_rel_resid=info.true_rel_resid)
 
 
 def c_parcels(parcels: dict) -> Parcels:
@@ -521,7 +525,8 @@ class SimpleContext:
         st = _lib.mfx_simple_iter(self.ptr, C.byref(cs), C.byref(r), _stream(stream))
         _check(st, "mfx_simple_iter", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))   # NONFINITE/ZERO_DIAG raise
         return dict(R=[r.R_u, r.R_v, r.R_w, r.R_cont], R_phi=list(r.R_phi), iters=list(r.iters),
-                    status=list(r.status), converged=bool(r.converged))
+                    status=list(r.status), converged=bool(r.converged), rel_resid=list(r.rel_resid),
+                    true_rel_resid=list(r.true_rel_resid))
 
     def time_step(self, state: dict, tc: TimeCtrl, stream=None) -> dict:
         """One accepted time step with adaptive dt (mfx_time_step, DESIGN.md §3.11);
@@ -561,7 +566,8 @@ class SimpleContext:
         st = _lib.mfx_dist_solve(self.ptr, kind, C.byref(self._g), C.byref(c_sys(sysd_slab, n)), _ptr(x_slab, n),
                                  tol, maxit, C.byref(info), _stream(stream))
         _check(st, "mfx_dist_solve", ok=(OK, NOT_CONVERGED, ERR_BREAKDOWN))
-        return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid)
+        return dict(iters=info.iters, status=info.status, restarts=info.restarts, rel_resid=info.rel_resid,
+                true_rel_resid=info.true_rel_resid)
 
     def phase_times(self):
         ms = (C.c_double * 6)()
@@ -623,6 +629,15 @@ def set_option(key: str, value: int):
 
 def get_option(key: str) -> int:
     return int(_lib.mfx_get_option(key.encode()))
+
+
+def graph_cache_clear():
+    """Release every cached BiCGSTAB CUDA graph (mfx_graph_cache_clear)."""
+    _lib.mfx_graph_cache_clear()
+
+
+def graph_cache_size() -> int:
+    return int(_lib.mfx_graph_cache_size())
 
 
 def launch_count() -> int:

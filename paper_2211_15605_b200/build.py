@@ -43,11 +43,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
         so_t = os.path.getmtime(SO)
         if all(os.path.getmtime(p) <= so_t for p in deps()):
             return SO
+    # one object per translation unit, compiled in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+    odir = os.path.join(HERE, "build")
+    os.makedirs(odir, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f not in ("-shared",)]
+
+    def compile_one(src):
+        obj = os.path.join(odir, os.path.basename(src) + f".{os.getpid()}.o")
+        cmd = [NVCC, *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+        return obj
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, srcs))
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *sources(), "-ldl"]
+    cmd = [NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
+           "-o", tmp, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, SO)
     return SO
 

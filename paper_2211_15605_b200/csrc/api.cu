@@ -347,6 +347,13 @@ API mfx_status mfx_prof_read(int counts[16], double ms[16])
 
 API long long mfx_launch_count(void) { return g_launches.load(); }
 
+namespace mfx {
+void graph_cache_evict(const void *ws);
+size_t graph_cache_size();
+}
+API void mfx_graph_cache_clear(void) { graph_cache_evict(nullptr); }
+API size_t mfx_graph_cache_size(void) { return graph_cache_size(); }
+
 API mfx_status mfx_set_option(const char *key, int value)
 {
     MFX_ARG_CHECK(key, "NULL key");

@@ -136,6 +136,35 @@ __global__ void __launch_bounds__(kThreads) k_setup(Geo G, Coef c, const double 
         bicg_setup(h->sc, dd_round(out[0]), dd_round(out[1]), tol, maxit);
 }
 
+// true residual at exit (reading Q2: "true residual reported at exit only"):
+// r = b - A x with the canonical operator, <b,b> and <r,r> correctly rounded,
+// h->true_rel = sqrt(<r,r>) / sqrt(<b,b>) (0 when b = 0).  One extra apply per
+// solve; it reads nothing the solver writes afterwards.
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads) k_true_resid(Geo G, Coef c, const double *__restrict__ b,
+                                                        const double *__restrict__ x, WsHeader *h, dd *part)
+{
+    Acc bb, rr;
+    bb.zero();
+    rr.zero();
+    GRID_STRIDE(n)
+    {
+        int i, j, k;
+        decode(G, n, i, j, k);
+        const double y = stencil<SYM>(G, c, n, i, j, k, [&](long long m) { return __ldg(x + m); });
+        const double bv = __ldg(b + n);
+        const double rv = bv - y;
+        bb.prod(bv, bv);
+        rr.prod(rv, rv);
+    }
+    __shared__ dd sh[(kThreads / 32) * 2];
+    dd v[2] = {bb.get(), rr.get()}, out[2];
+    if (grid_reduce_dd<2>(v, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        const double bn = sqrt(dd_round(out[0]));
+        h->true_rel = bn == 0.0 ? 0.0 : sqrt(dd_round(out[1])) / bn;
+    }
+}
+
 __global__ void k_zero_if(const WsHeader *h, double *x, long long N)
 {
     if (!h->sc.zero_x) return;
@@ -636,24 +665,37 @@ void launch_iteration(const Geo &G, const Coef &c, const WsView &W, double *x, i
 }
 
 // ------------------------------------------------------------------ CUDA graphs
-// GC BiCGSTAB iterations (3*GC kernels) captured once per (system, x,
-// workspace) and replayed: removes per-kernel launch latency from the loop.
+// GC BiCGSTAB iterations (3*GC kernels) captured once and replayed: removes
+// per-kernel launch latency from the loop.  A captured graph bakes in every
+// array pointer, the TMA tensor maps (dims, strides), the tile / stage /
+// z-chunk choice (functions of the grid shape), the grid sizes and the PDL
+// attribute, so the key holds all of them: the pointers, nx, ny, nz, the
+// symmetric flag and the launch options.  Equal keys therefore describe the
+// same launches, whatever the allocator did in between.  Entries are evicted
+// when a context that owns the workspace is destroyed (graph_cache_evict) or
+// by mfx_graph_cache_clear(), and the cache is bounded (oldest out first).
 constexpr int GC = 16;
+constexpr size_t kMaxGraphs = 64;
 struct GraphKey {
     const void *p[10];
-    long long N;
-    int sym;
+    int nx, ny, nz, sym, pdl, dev;
     bool operator<(const GraphKey &o) const
     {
-        if (N != o.N) return N < o.N;
-        if (sym != o.sym) return sym < o.sym;
+        const int a[6] = {nx, ny, nz, sym, pdl, dev}, b[6] = {o.nx, o.ny, o.nz, o.sym, o.pdl, o.dev};
+        for (int q = 0; q < 6; q++)
+            if (a[q] != b[q]) return a[q] < b[q];
         for (int q = 0; q < 10; q++)
             if (p[q] != o.p[q]) return p[q] < o.p[q];
         return false;
     }
 };
+struct GraphEntry {
+    cudaGraphExec_t ex;
+    unsigned long long stamp;
+};
 std::mutex g_graph_mu;
-std::map<GraphKey, cudaGraphExec_t> g_graphs;
+std::map<GraphKey, GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
 
 bool use_graphs() { return opt_graphs() == 1 && !prof_enabled(); }
 
@@ -663,12 +705,19 @@ mfx_status get_graph(const Geo &G, const mfx_eqsys *A, const WsView &W, double *
     GraphKey k;
     const void *ptrs[10] = {A->aP, A->aE, A->aW, A->aN, A->aS, A->aT, A->aB, A->b, x, W.hdr};
     for (int q = 0; q < 10; q++) k.p[q] = ptrs[q];
-    k.N = G.N;
+    k.nx = G.nx; k.ny = G.ny; k.nz = G.nz;
     k.sym = SYM;
+    k.pdl = opt_pdl();
+    k.dev = 0;
+    cudaGetDevice(&k.dev);
     {
         std::lock_guard<std::mutex> lk(g_graph_mu);
         auto it = g_graphs.find(k);
-        if (it != g_graphs.end()) { out = it->second; return MFX_OK; }
+        if (it != g_graphs.end()) {
+            it->second.stamp = ++g_graph_clock;
+            out = it->second.ex;
+            return MFX_OK;
+        }
     }
     cudaStream_t cs;
     MFX_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -687,7 +736,14 @@ mfx_status get_graph(const Geo &G, const mfx_eqsys *A, const WsView &W, double *
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) { set_error("graph instantiate: %s", cudaGetErrorString(e)); return MFX_ERR_CUDA; }
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    g_graphs[k] = ex;
+    if (g_graphs.size() >= kMaxGraphs) {
+        auto old = g_graphs.begin();
+        for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+            if (it->second.stamp < old->second.stamp) old = it;
+        cudaGraphExecDestroy(old->second.ex);   // stream-ordered: a pending launch completes first
+        g_graphs.erase(old);
+    }
+    g_graphs[k] = GraphEntry{ex, ++g_graph_clock};
     out = ex;
     return MFX_OK;
 }
@@ -700,7 +756,44 @@ thread_local HostScratch g_host;
 
 }  // namespace
 
+// drop every cached graph that refers to workspace `ws` (NULL: all of them)
+void graph_cache_evict(const void *ws)
+{
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+        if (!ws || it->first.p[9] == ws) {
+            cudaGraphExecDestroy(it->second.ex);
+            it = g_graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+size_t graph_cache_size()
+{
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    return g_graphs.size();
+}
+
 bool grid_valid(const mfx_grid *g, bool scalar);
+
+mfx_status true_resid_launch(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, WsHeader *h, dd *part,
+                             cudaStream_t s)
+{
+    const Coef c = coef_of(A);
+    const int nb = reduce_grid(G.N);
+    if (sym) k_true_resid<true><<<nb, kThreads, 0, s>>>(G, c, A->b, x, h, part);
+    else k_true_resid<false><<<nb, kThreads, 0, s>>>(G, c, A->b, x, h, part);
+    count_launch(0, s, false);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
+}
+
+// exit record for a host-synchronous solve: the true residual of the returned
+// iterate, then one device->host copy of the solver state
+static mfx_status finish_info(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, const WsView &W,
+                              mfx_solve_info *info, cudaStream_t s);
 
 // MFX_KERNELS=v1 selects the simple grid-stride kernels (kept as an A/B
 // reference for tests and profiling); default is the TMA z-marching path.
@@ -757,6 +850,30 @@ mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double
     return MFX_OK;
 }
 
+struct HostExit {
+    SolverScalars sc;
+    double true_rel;
+};
+static thread_local HostExit *g_exit = nullptr;
+
+static mfx_status finish_info(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, const WsView &W,
+                              mfx_solve_info *info, cudaStream_t s)
+{
+    if (!g_exit) MFX_CUDA_TRY(cudaMallocHost(&g_exit, sizeof(HostExit)));
+    mfx_status st = true_resid_launch(sym, G, A, x, W.hdr, W.part, s);
+    if (st != MFX_OK) return st;
+    MFX_CUDA_TRY(cudaMemcpyAsync(&g_exit->sc, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(&g_exit->true_rel, &W.hdr->true_rel, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    const SolverScalars &S = g_exit->sc;
+    info->iters = S.it;
+    info->status = S.status;
+    info->restarts = S.restarts;
+    info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
+    info->true_rel_resid = g_exit->true_rel;
+    return (mfx_status)S.status;
+}
+
 mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol, int maxit,
                           void *ws, size_t wsb, mfx_solve_info *info, cudaStream_t s)
 {
@@ -782,14 +899,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
         count_launch(0, s, false);
         if (st != MFX_OK) return st;
         if (!info) return MFX_OK;
-        MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
-        MFX_CUDA_TRY(cudaStreamSynchronize(s));
-        const SolverScalars &S = *g_host.pinned;
-        info->iters = S.it;
-        info->status = S.status;
-        info->restarts = S.restarts;
-        info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
-        return (mfx_status)S.status;
+        return finish_info(sym, G, A, x, W, info, s);
     }
     const bool grid_path = path == 4 || (path == 0 && grid_solver_fits(G, sym));
     count_launch(0, s, true);
@@ -813,14 +923,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
         count_launch(sym ? 6 : 1, s, false);
         if (st != MFX_OK) return st;
         if (!info) return MFX_OK;
-        MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
-        MFX_CUDA_TRY(cudaStreamSynchronize(s));
-        const SolverScalars &S = *g_host.pinned;
-        info->iters = S.it;
-        info->status = S.status;
-        info->restarts = S.restarts;
-        info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
-        return (mfx_status)S.status;
+        return finish_info(sym, G, A, x, W, info, s);
     }
     int launched = 0, chunk = 4;
     while (launched < maxit) {
@@ -853,14 +956,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
         chunk = chunk * 2 > 64 ? 64 : chunk * 2;
     }
     if (!info) return MFX_OK;
-    MFX_CUDA_TRY(cudaMemcpyAsync(g_host.pinned, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
-    MFX_CUDA_TRY(cudaStreamSynchronize(s));
-    const SolverScalars &S = *g_host.pinned;
-    info->iters = S.it;
-    info->status = S.status;
-    info->restarts = S.restarts;
-    info->rel_resid = S.bn == 0.0 ? 0.0 : S.rn / S.bn;
-    return (mfx_status)S.status;
+    return finish_info(sym, G, A, x, W, info, s);
 }
 
 }  // namespace mfx

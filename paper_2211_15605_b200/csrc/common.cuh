@@ -226,7 +226,8 @@ struct WsHeader {
     unsigned int ticket[4];
     double resid[4];
     unsigned long long bad_parcel;      // first parcel outside the domain (ULLONG_MAX = none)
-    double pad[5];
+    double true_rel;                    // ||b - A x|| / ||b|| of the last solve's exit iterate (0 if b = 0)
+    double pad[4];
 };
 
 constexpr int kMaxBlocks = 2048;
@@ -272,5 +273,7 @@ mfx_status pic_drag(const mfx_grid *grid, const mfx_params *pr, const mfx_pic_pa
 void launch_count_set(long long v);
 void launch_count_add(long long v);
 int reduce_grid(long long N);
+mfx_status true_resid_launch(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, WsHeader *h, dd *part,
+                             cudaStream_t s);
 
 }  // namespace mfx

@@ -361,6 +361,7 @@ mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eq
         info->status = pin->status;
         info->restarts = pin->restarts;
         info->rel_resid = pin->bn == 0.0 ? 0.0 : pin->rn / pin->bn;
+        info->true_rel_resid = -1.0;   // not computed per slab (mfx_simple_iter computes it on P0)
     }
     return (mfx_status)pin->status;
 }

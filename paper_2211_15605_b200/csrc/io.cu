@@ -184,6 +184,34 @@ mfx_status state_load(const char *path, const mfx_grid *grid, mfx_state *st, int
     }
     std::vector<FieldRef> want = state_fields(st, n_scalars);
     const long long N = (long long)grid->nx * grid->ny * grid->nz;
+    // validate everything before the first device copy, so a bad file leaves
+    // the caller's state untouched: the payload length must equal what the
+    // header and table imply, and every wanted field exist
+    {
+        const long pos = ftell(F.f);
+        unsigned long long payload = 0;
+        for (auto &e : tab) payload += 8ull * (unsigned long long)(e.kind ? h.n_parcels : N);
+        if (pos < 0 || fseek(F.f, 0, SEEK_END) != 0) { set_error("%s: cannot seek", path); return MFX_ERR_ARG; }
+        const long end = ftell(F.f);
+        if (end < 0 || (unsigned long long)(end - pos) != payload) {
+            set_error("%s: payload is %ld bytes, header and table imply %llu", path, end - pos, payload);
+            return MFX_ERR_ARG;
+        }
+        if (fseek(F.f, pos, SEEK_SET) != 0) { set_error("%s: cannot seek", path); return MFX_ERR_ARG; }
+        for (auto &fr : want) {
+            bool present = false;
+            for (auto &e : tab) {
+                char name[9];
+                memcpy(name, e.name, 8);
+                name[8] = 0;
+                if (e.kind == 0 && !strcmp(fr.name, name)) present = true;
+            }
+            if (!present) {
+                set_error("%s: requested state field %s is missing", path, fr.name);
+                return MFX_ERR_ARG;
+            }
+        }
+    }
     std::vector<double> buf;
     int found = 0;
     for (auto &e : tab) {

@@ -23,6 +23,7 @@
 
 namespace mfx {
 
+void graph_cache_evict(const void *ws);
 bool grid_valid(const mfx_grid *g, bool scalar);
 mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params *pr, const mfx_state *st,
                        const double *const star[6], mfx_eqsys *out, double *resid2, void *ws, size_t wsb,
@@ -131,6 +132,7 @@ mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer 
     } else if (phase == 3) {
         // PIC: the PIC device (rank 0) broadcasts the refreshed drag fields
         for (int b = MFX_BUF_BETA; b <= MFX_BUF_SBW; b++) v.push_back({MFX_OP_BCAST, 0, b, 0, 0, 0, 0});
+        v.push_back({MFX_OP_BCAST, 0, MFX_BUF_META, 8, 1, 0, 0});   // the PIC record (error latch)
     } else if (multi_p) {
         // PSLAB: the slabs of the domain-decomposed p' solution -> P0 (= rank 0)
         for (int q = 0; q < a->n_p; q++) {
@@ -189,8 +191,29 @@ Nccl g_nccl;
     } while (0)
 
 size_t round256(size_t b) { return (b + 255) & ~(size_t)255; }
+constexpr size_t kMetaBytes = 9 * 16 * sizeof(double);
 
-__global__ void k_meta_vals(const double *resid2, double *slot, int iters, int status, int restarts, double rel)
+// Residual record of one equation (16 doubles, exchanged with the state so
+// every rank sees the same record): [0] residual numerator, [1] denominator,
+// [2] iterations, [3] solve status, [4] restarts, [5] recursive rel. residual,
+// [6] present, [7] true rel. residual at exit, [8] device error (0, or
+// MFX_ERR_NONFINITE / MFX_ERR_ZERO_DIAG / MFX_ERR_ARG for a bad parcel),
+// [9] first offending cell (or parcel) index.  The error latch of the
+// equation's workspace is read here on the device and cleared, so the status
+// every rank returns derives from the exchanged record (identical decisions).
+__device__ void meta_error(WsHeader *h, double *slot)
+{
+    const unsigned long long nf = h->bad_nonfinite, zd = h->bad_zerodiag;
+    slot[8] = 0.0;
+    slot[9] = 0.0;
+    if (nf != ~0ull) { slot[8] = (double)MFX_ERR_NONFINITE; slot[9] = (double)nf; }
+    else if (zd != ~0ull) { slot[8] = (double)MFX_ERR_ZERO_DIAG; slot[9] = (double)zd; }
+    h->bad_nonfinite = ~0ull;
+    h->bad_zerodiag = ~0ull;
+}
+
+__global__ void k_meta_vals(const double *resid2, double *slot, int iters, int status, int restarts, double rel,
+                            WsHeader *h)
 {
     if (threadIdx.x != 0) return;
     slot[0] = resid2[0];
@@ -200,9 +223,11 @@ __global__ void k_meta_vals(const double *resid2, double *slot, int iters, int s
     slot[4] = (double)restarts;
     slot[5] = rel;
     slot[6] = 1.0;
+    slot[7] = h->true_rel;
+    meta_error(h, slot);
 }
 
-__global__ void k_meta(const WsHeader *h, const double *resid2, double *slot, int solved)
+__global__ void k_meta(WsHeader *h, const double *resid2, double *slot, int solved)
 {
     if (threadIdx.x != 0) return;
     const SolverScalars &S = h->sc;
@@ -213,6 +238,20 @@ __global__ void k_meta(const WsHeader *h, const double *resid2, double *slot, in
     slot[4] = solved ? (double)S.restarts : 0.0;
     slot[5] = solved && S.bn != 0.0 ? S.rn / S.bn : 0.0;
     slot[6] = 1.0;   // present
+    slot[7] = solved ? h->true_rel : 0.0;
+    meta_error(h, slot);
+}
+
+// PIC record (meta slot 8, broadcast with the drag fields): a parcel latched
+// outside the domain by the refresh on the PIC device
+__global__ void k_meta_pic(WsHeader *h, double *slot)
+{
+    if (threadIdx.x != 0) return;
+    const unsigned long long bp = h->bad_parcel;
+    slot[6] = 1.0;
+    slot[8] = bp != ~0ull ? (double)MFX_ERR_ARG : 0.0;
+    slot[9] = bp != ~0ull ? (double)bp : 0.0;
+    h->bad_parcel = ~0ull;
 }
 }  // namespace
 
@@ -276,8 +315,8 @@ struct mfx_ctx {
     double *star[3], *dv[3]; // u*, v*, w*, d_x, d_y, d_z (owned or received)
     double *pp;              // p' solution
     double *phinew[4];
-    double *meta;            // device [8][16]
-    double *meta_host;       // pinned [8][16]
+    double *meta;            // device [9][16]: 8 equation records + the PIC record
+    double *meta_host;       // pinned [9][16]
     ncclComm_t comm;
     mfx_local_group *group;  // non-NULL: in-process transport instead of NCCL
     void *dist_scratch;      // distributed-solver workspace (allocated on first use)
@@ -321,6 +360,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     MFX_ARG_CHECK(nranks == 1 || uid || group, "uid (NCCL) or a local group required for nranks > 1");
     MFX_ARG_CHECK(!group || group->nranks == nranks, "local group has %d ranks, expected %d",
                   group ? group->nranks : 0, nranks);
+    MFX_ARG_CHECK(a.n_p == 1 || grid->nz >= nranks, "multi-GPU p' needs nz >= ranks");
     mfx_ctx *c = new mfx_ctx();
     c->rank = rank; c->nranks = nranks; c->asg = a; c->grid = *grid; c->params = *params;
     c->N = (long long)grid->nx * grid->ny * grid->nz;
@@ -334,7 +374,6 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     for (int q = 0; q < 8; q++) { memset(&c->sys[q], 0, sizeof(mfx_eqsys)); c->ws[q] = nullptr; }
     const int P = a.owner[3];
     const bool multi_p = a.n_p > 1;                 // every rank solves a slab of p'
-    MFX_ARG_CHECK(!multi_p || grid->nz >= nranks, "multi-GPU p' needs nz >= ranks");
     auto holds = [&](int q) { return a.owner[q] == rank || (q == 3 && multi_p); };
     for (int q = 0; q < 8; q++) {
         if (!holds(q)) continue;
@@ -385,12 +424,12 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     }
     {
         void *blk;
-        if ((st = ctx_alloc(c, &blk, 256 + 8 * 16 * sizeof(double))) != MFX_OK) return fail(st);
+        if ((st = ctx_alloc(c, &blk, 256 + kMetaBytes)) != MFX_OK) return fail(st);
         c->resid2 = (double *)blk;
         c->meta = (double *)((char *)blk + 256);
-        if (cudaMemset(blk, 0, 256 + 8 * 16 * sizeof(double)) != cudaSuccess) return fail(MFX_ERR_CUDA);
+        if (cudaMemset(blk, 0, 256 + kMetaBytes) != cudaSuccess) return fail(MFX_ERR_CUDA);
     }
-    if (cudaMallocHost(&c->meta_host, 8 * 16 * sizeof(double)) != cudaSuccess) {
+    if (cudaMallocHost(&c->meta_host, kMetaBytes) != cudaSuccess) {
         c->meta_host = nullptr;
         return fail(MFX_ERR_CUDA);
     }
@@ -578,7 +617,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     const int r = c->rank, P = a.owner[3];
     const size_t vbytes = sizeof(double) * (size_t)c->N;
     mfx_status rc;
-    MFX_CUDA_TRY(cudaMemsetAsync(c->meta, 0, 8 * 16 * sizeof(double), s));
+    MFX_CUDA_TRY(cudaMemsetAsync(c->meta, 0, kMetaBytes, s));
     MFX_CUDA_TRY(cudaEventRecord(c->ev[0], s));
     // head of the SIMPLE iteration: particle -> fluid drag refresh
     if (c->pic_mode == MFX_PIC_IMPLICIT || (c->pic_mode == MFX_PIC_EXPLICIT && c->pic_pending)) {
@@ -588,6 +627,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
             rc = pic_deposit_binned(1, &c->grid, &pr, &c->pic_pp, &c->pic_pc, c->pic_orig, c->pic_start, st->eps,
                                     st->u, st->v, st->w, outs, nullptr, c->pic_vals, c->pic_ws, ws_header_bytes(), s);
             if (rc != MFX_OK) return rc;
+            k_meta_pic<<<1, 32, 0, s>>>((WsHeader *)c->pic_ws, c->meta + 16 * 8);
         }
         double *D[MFX_NBUF] = {0};
         D[MFX_BUF_BETA] = st->beta; D[MFX_BUF_SBU] = st->sbeta_u;
@@ -606,7 +646,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         rc = bicgstab_solve(q, &c->grid, &c->sys[q], c->star[q], pr.lin_tol_mom, pr.lin_maxit_mom, c->ws[q],
                             c->ws_bytes, &info, s);
         if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
-        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
+        k_meta<<<1, 32, 0, s>>>((WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
     }
     // scalars (same snapshot, Q22)
     for (int sc = 0; sc < a.n_scalars; sc++) {
@@ -619,7 +659,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         rc = bicgstab_solve(MFX_EQ_SCALAR, &c->grid, &c->sys[q], c->phinew[sc], pr.lin_tol_phi, pr.lin_maxit_phi,
                             c->ws[q], c->ws_bytes, &info, s);
         if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
-        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
+        k_meta<<<1, 32, 0, s>>>((WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
     }
     MFX_CUDA_TRY(cudaEventRecord(c->ev[1], s));
     double *F[MFX_NBUF] = {0};
@@ -646,11 +686,18 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         mfx_solve_info info;
         rc = dist_solve(c, MFX_EQ_PP, &c->grid, &sl, c->pp + off, pr.lin_tol_pp, pr.lin_maxit_pp, &info, s);
         if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
-        k_meta_vals<<<1, 32, 0, s>>>(c->resid2 + 6, c->meta + 48, info.iters, info.status, info.restarts,
-                                     info.rel_resid);
         double *Fp[MFX_NBUF] = {0};
         Fp[MFX_BUF_PP] = c->pp;
         if ((rc = exchange_state(c, 2, Fp, s)) != MFX_OK) return rc;
+        // P0 holds the whole p' now: its true residual over the full system
+        WsView W3;
+        ws_view(c->ws[3], c->ws_bytes, c->N, false, W3);
+        if (r == P) {
+            const Geo G = make_geo(c->grid);
+            if ((rc = true_resid_launch(true, G, &c->sys[3], c->pp, W3.hdr, W3.part, s)) != MFX_OK) return rc;
+        }
+        k_meta_vals<<<1, 32, 0, s>>>(c->resid2 + 6, c->meta + 48, info.iters, info.status, info.restarts,
+                                     info.rel_resid, W3.hdr);
         MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
         if (r == P && (rc = correct(&c->grid, &pr, star6, c->pp, st->p, st->u, st->v, st->w, st->p, s)) != MFX_OK)
             return rc;
@@ -663,7 +710,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         rc = bicgstab_solve(MFX_EQ_PP, &c->grid, &c->sys[3], c->pp, pr.lin_tol_pp, pr.lin_maxit_pp, c->ws[3],
                             c->ws_bytes, &info, s);
         if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
-        k_meta<<<1, 32, 0, s>>>((const WsHeader *)c->ws[3], c->resid2 + 6, c->meta + 48, 1);
+        k_meta<<<1, 32, 0, s>>>((WsHeader *)c->ws[3], c->resid2 + 6, c->meta + 48, 1);
         MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
         if ((rc = correct(&c->grid, &pr, star6, c->pp, st->p, st->u, st->v, st->w, st->p, s)) != MFX_OK) return rc;
     } else {
@@ -679,7 +726,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     B[MFX_BUF_META] = c->meta;
     if ((rc = exchange_state(c, 1, B, s)) != MFX_OK) return rc;
     MFX_CUDA_TRY(cudaEventRecord(c->ev[5], s));
-    MFX_CUDA_TRY(cudaMemcpyAsync(c->meta_host, c->meta, 8 * 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(c->meta_host, c->meta, kMetaBytes, cudaMemcpyDeviceToHost, s));
     MFX_CUDA_TRY(cudaStreamSynchronize(s));
     float ms;
     // [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction, [4] BCAST, [5] total
@@ -698,33 +745,22 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     for (int q = 0; q < 8; q++) {
         out->iters[q] = (int)m[16 * q + 2];
         out->status[q] = (int)m[16 * q + 3];
+        out->rel_resid[q] = m[16 * q + 5];
+        out->true_rel_resid[q] = m[16 * q + 7];
         if (out->status[q] < 0) worst = out->status[q];
     }
-    // non-finite / zero-diagonal rows latched by any assembly of this rank
-    for (int q = 0; q < 8; q++) {
-        if (!c->ws[q]) continue;
-        unsigned long long bad[2];
-        const WsHeader *h = (const WsHeader *)c->ws[q];
-        MFX_CUDA_TRY(cudaMemcpy(bad, &h->bad_nonfinite, 16, cudaMemcpyDeviceToHost));
-        if (bad[0] != ~0ull || bad[1] != ~0ull) {
-            const unsigned long long none = ~0ull;
-            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_nonfinite, &none, 8, cudaMemcpyHostToDevice));
-            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_zerodiag, &none, 8, cudaMemcpyHostToDevice));
-            set_error("equation %d: %s at cell %llu", q, bad[0] != ~0ull ? "non-finite coefficient" : "zero diagonal",
-                      bad[0] != ~0ull ? bad[0] : bad[1]);
-            worst = bad[0] != ~0ull ? MFX_ERR_NONFINITE : MFX_ERR_ZERO_DIAG;
-        }
-    }
-    if (c->pic_ws) {
-        unsigned long long badp;
-        const WsHeader *h = (const WsHeader *)c->pic_ws;
-        MFX_CUDA_TRY(cudaMemcpy(&badp, &h->bad_parcel, 8, cudaMemcpyDeviceToHost));
-        if (badp != ~0ull) {
-            const unsigned long long none = ~0ull;
-            MFX_CUDA_TRY(cudaMemcpy((void *)&h->bad_parcel, &none, 8, cudaMemcpyHostToDevice));
-            set_error("PIC drag refresh: parcel %llu outside the domain (or negative / NaN weight)", badp);
-            worst = MFX_ERR_ARG;
-        }
+    // device errors latched by any equation's assembly or by the PIC refresh
+    // (SPEC.md:356, 365), taken from the exchanged records: every rank returns
+    // the same status (a rank-local latch let ranks diverge)
+    for (int q = 0; q < 9; q++) {
+        const double e = m[16 * q + 8];
+        if (e == 0.0) continue;
+        const unsigned long long at = (unsigned long long)m[16 * q + 9];
+        if (q == 8) set_error("PIC drag refresh: parcel %llu outside the domain (or negative / NaN weight)", at);
+        else set_error("equation %d: %s at cell %llu", q, e == (double)MFX_ERR_NONFINITE ? "non-finite coefficient"
+                                                                                      : "zero diagonal", at);
+        worst = (int)e;
+        break;
     }
     double mx = out->R_u;
     if (out->R_v > mx) mx = out->R_v;
@@ -774,6 +810,8 @@ mfx_status mfx_ctx_create_local(const char *assignment, int rank, int nranks, mf
 void mfx_ctx_destroy(mfx_ctx *c)
 {
     if (!c) return;
+    for (int q = 0; q < 8; q++)
+        if (c->ws[q]) mfx::graph_cache_evict(c->ws[q]);   // graphs captured on this context's workspaces
     if (c->comm && mfx::g_nccl.CommDestroy) mfx::g_nccl.CommDestroy(c->comm);
     for (void *p : c->allocs) cudaFree(p);
     if (c->dist_scratch) cudaFree(c->dist_scratch);
@@ -801,6 +839,9 @@ mfx_status mfx_adapt_dt(mfx_time_ctrl *tc, int outer_iters, int converged, int *
 {
     MFX_ARG_CHECK(tc && accept, "NULL argument");
     MFX_ARG_CHECK(tc->dt > 0.0 && tc->dt_min > 0.0 && tc->dt_max >= tc->dt_min, "bad dt bounds");
+    // a shrink factor >= 1 (or NaN) would never reach dt_min: mfx_time_step would retry forever
+    MFX_ARG_CHECK(tc->shrink > 0.0 && tc->shrink < 1.0, "shrink must lie in (0, 1), got %g", tc->shrink);
+    MFX_ARG_CHECK(tc->grow >= 1.0 && tc->dt_max < 1e300, "grow must be >= 1 and dt_max finite");
     if (converged) {
         if (outer_iters <= tc->grow_threshold) {
             const double d = tc->dt * tc->grow;
@@ -892,6 +933,18 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
         {
             const long long n = parcels->n;
             if (n > c->pic_cap) {
+                // release the smaller buffers first (they stay in c->allocs until then)
+                auto release = [&](void *p) {
+                    if (!p) return;
+                    for (auto it = c->allocs.begin(); it != c->allocs.end(); ++it)
+                        if (*it == p) { c->allocs.erase(it); break; }
+                    cudaFree(p);
+                };
+                MFX_CUDA_TRY(cudaDeviceSynchronize());
+                for (int f = 0; f < 7; f++) { release(c->pic_sorted[f]); c->pic_sorted[f] = nullptr; }
+                release(c->pic_orig); c->pic_orig = nullptr;
+                release(c->pic_vals); c->pic_vals = nullptr;
+                c->pic_cap = 0;
                 for (int f = 0; f < 7; f++) {
                     mfx_status st = mfx::ctx_alloc(c, (void **)&c->pic_sorted[f], sizeof(double) * (size_t)n);
                     if (st != MFX_OK) return st;
@@ -908,6 +961,13 @@ mfx_status mfx_ctx_set_pic(mfx_ctx *c, const mfx_parcels *parcels, const mfx_pic
             }
             const size_t need = mfx::pic_sort_scratch_bytes(c->N, n);
             if (need > c->pic_scratch_bytes) {
+                if (c->pic_scratch) {
+                    for (auto it = c->allocs.begin(); it != c->allocs.end(); ++it)
+                        if (*it == c->pic_scratch) { c->allocs.erase(it); break; }
+                    cudaFree(c->pic_scratch);
+                    c->pic_scratch = nullptr;
+                    c->pic_scratch_bytes = 0;
+                }
                 mfx_status st = mfx::ctx_alloc(c, &c->pic_scratch, need);
                 if (st != MFX_OK) return st;
                 c->pic_scratch_bytes = need;

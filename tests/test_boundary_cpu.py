@@ -152,7 +152,8 @@ def test_exchange_plan_pic_phase(mfx, text, n):
     drag fields; identical op list on every rank (collective order)."""
     plans = [mfx.exchange_plan(text, n, r, 3) for r in range(n)]
     assert all(p == plans[0] for p in plans)
-    assert [o["buf"] for o in plans[0]] == ["beta", "sbeta_u", "sbeta_v", "sbeta_w"]
+    assert [o["buf"] for o in plans[0]] == ["beta", "sbeta_u", "sbeta_v", "sbeta_w", "meta"]
+    assert plans[0][-1]["slot"] == 8 and plans[0][-1]["nslots"] == 1    # the PIC error record
     assert all(o["op"] == mfx.OP_BCAST and o["peer"] == 0 for o in plans[0])
 
 
@@ -207,6 +208,11 @@ def test_time_and_sort_entry_points_reject_bad_args(mfx):
     MFX_ERR_ARG before any device work (no GPU needed)."""
     import ctypes as C
     import synth
+    for bad in (dict(shrink=1.0), dict(shrink=0.0), dict(shrink=float("nan")), dict(grow=0.9),
+                dict(dt_max=float("inf"))):
+        tc = mfx.time_ctrl(**bad)
+        acc = C.c_int()
+        assert mfx.lib().mfx_adapt_dt(C.byref(tc), 1, 0, C.byref(acc)) == mfx.ERR_ARG, bad
     tc = mfx.time_ctrl(dt=-1.0)
     acc = C.c_int()
     assert mfx.lib().mfx_adapt_dt(C.byref(tc), 1, 1, C.byref(acc)) == mfx.ERR_ARG

@@ -65,12 +65,16 @@ def test_load_rejects_mismatch(mfx, tmp_path):
     sd2 = dev(synth.make_state(g2, 1, pr, n_scalars=1))
     with pytest.raises(mfx.MfxError, match="does not match"):
         mfx.state_load(str(p), g2, sd2, n_scalars=1)
-    with pytest.raises(mfx.MfxError, match="state fields present"):
+    with pytest.raises(mfx.MfxError, match="missing"):
         mfx.state_load(str(p), g, dev(case(2)[2]), n_scalars=2)     # dump holds one scalar
     raw = p.read_bytes()
-    p.write_bytes(raw[: len(raw) // 2])
-    with pytest.raises(mfx.MfxError, match="truncated"):
-        mfx.state_load(str(p), g, dev(st), n_scalars=1)
+    # a rejected file leaves the caller's buffers untouched (validated before any copy)
+    for bad in (raw[: len(raw) // 2], raw + b"\0" * 8):
+        p.write_bytes(bad)
+        nan = {k: torch.full_like(v, float("nan")) for k, v in dev(st).items()}
+        with pytest.raises(mfx.MfxError, match="payload"):
+            mfx.state_load(str(p), g, nan, n_scalars=1)
+        assert all(bool(torch.isnan(v).all()) for v in nan.values())
 
 
 def test_restart_transparency(mfx, tmp_path):

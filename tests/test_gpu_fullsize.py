@@ -152,3 +152,38 @@ def test_c4_largest_grid_pp_and_momentum(mfx, orc):
     for k in ("aP", "aE", "aW", "aN", "aS", "aT", "aB", "b", "d"):
         assert np.array_equal(host(mout[k]), mref[k]), k
     assert np.array_equal(host(mres2), mr2)
+
+
+def _long_horizon(mfx, orc, cid):
+    """One whole SIMPLE outer iteration '111[1]' in bench.py's launch
+    configuration (SimpleContext, CUDA graphs, TMA kernels, 500 p' iterations
+    -- the cap, NOT_CONVERGED) against or_simple_iter on the same seeded
+    state: every field bitwise, every iteration count and status equal, the
+    four residuals equal (the whole-run verification of P:119-125, on the
+    chaotic p' recurrence where a single differing bit would grow)."""
+    import os
+    g, pr, st = synth.config_case(cid)
+    pr = synth.Params()
+    orc.set_mode(len(os.sched_getaffinity(0)), False)
+    ref_state, R, iters, status, rc = orc.simple_iter(g, pr, {k: v.copy() for k, v in st.items()})
+    assert mfx.get_option("graphs") == 1
+    ctx = mfx.SimpleContext("111[1]", g, pr)
+    sd = {k: dev(v) for k, v in st.items()}
+    out = ctx.step(sd)
+    ctx.close()
+    assert iters[3] == pr.lin_maxit_pp                # the capped, chaotic regime
+    assert out["iters"][:4] == iters[:4] and out["status"][:4] == status[:4]
+    assert out["R"] == list(R)
+    for k in ("u", "v", "w", "p"):
+        assert np.array_equal(host(sd[k]), ref_state[k]), k
+    # the capped p' solve: recursive vs true residual of the returned iterate
+    assert 0.0 < out["true_rel_resid"][3] < 1.0 and 0.0 < out["rel_resid"][3] < 1.0
+    return out
+
+
+def test_c3_long_horizon_simple_iteration_bitwise(mfx, orc):
+    _long_horizon(mfx, orc, 3)
+
+
+def test_c2_long_horizon_simple_iteration_bitwise(mfx, orc):
+    _long_horizon(mfx, orc, 2)

@@ -420,3 +420,56 @@ def test_simple_iter_reports_nonfinite(mfx):
         ctx.step(state_dev(st))
     assert e.value.status == mfx.ERR_NONFINITE and "cell" in str(e.value)
     ctx.close()
+
+
+# ---------------------------------------------------------------- graph cache and exit residual
+def _pp_system(orc, g, seed):
+    pr = Params()
+    st = synth.make_state(g, seed, pr)
+    dv = [np.random.default_rng(seed + a).uniform(1e-4, 1e-3, g.n) for a in range(3)]
+    sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+    return sysd
+
+
+def test_graph_cache_same_n_different_shape(mfx, orc):
+    """Two p' systems with equal N and different shapes solved back to back in
+    the SAME device buffers, with enough iterations that the 16-iteration CUDA
+    graphs engage: each must equal the oracle bitwise (the cached graph bakes
+    in tensor maps and tiles, so it must be keyed on the shape)."""
+    shapes = [(64, 32, 40), (32, 64, 40), (64, 32, 40)]
+    n = 64 * 32 * 40
+    bufs = {k: torch.empty(n, dtype=torch.float64, device="cuda") for k in ("aP", "aE", "aN", "aT", "b")}
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = mfx.Workspace(synth.make_grid(*shapes[0]))
+    mfx.set_option("graphs", 1)
+    for q, shp in enumerate(shapes):
+        g = synth.make_grid(*shp)
+        sysd = _pp_system(orc, g, 300 + q)
+        for k in bufs:
+            bufs[k].copy_(torch.from_numpy(sysd[k]))
+        x.zero_()
+        ref = orc.bicgstab(g, sysd, np.zeros(n), 1e-12, 48)
+        info = mfx.bicgstab_solve(mfx.EQ_PP, g, bufs, x, 1e-12, 48, ws)
+        assert ref["iters"] == 48 and info["iters"] == 48, (shp, ref["iters"], info["iters"])
+        assert np.array_equal(host(x), ref["x"]), shp
+    assert mfx.graph_cache_size() >= 2
+    mfx.graph_cache_clear()
+    assert mfx.graph_cache_size() == 0
+
+
+def test_true_rel_resid_matches_oracle(mfx, orc):
+    """mfx_solve_info.true_rel_resid = ||b - A x|| / ||b|| of the returned
+    iterate (reading Q2), computed once at exit with the canonical operator and
+    correctly rounded dots: bitwise the oracle's composition of the same
+    definitions; for a capped solve it differs from the recursive residual."""
+    g = synth.make_grid(34, 19, 23)
+    sysd = _pp_system(orc, g, 77)
+    for tol, maxit in ((1e-8, 3000), (0.0, 40)):
+        ref = orc.bicgstab(g, sysd, np.zeros(g.n), tol, maxit)
+        x = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+        info = mfx.bicgstab_solve(mfx.EQ_PP, g, {k: dev(v) for k, v in sysd.items()}, x, tol, maxit,
+                                  mfx.Workspace(g))
+        r = sysd["b"] - orc.spmv(g, sysd, ref["x"])
+        want = np.sqrt(orc.dot(r, r)) / np.sqrt(orc.dot(sysd["b"], sysd["b"]))
+        assert info["true_rel_resid"] == want, (info, want)
+        assert info["true_rel_resid"] > 0.0

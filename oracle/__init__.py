@@ -40,7 +40,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
@@ -48,7 +48,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lquadmath", "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -127,6 +127,10 @@ def lib():
         L.or_simple_iter.argtypes = [C.POINTER(OgGrid), C.POINTER(OgParams), C.c_int,
                                      C.POINTER(OgState), _DP, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_pic_deposit_eps.argtypes = [C.POINTER(OgGrid), C.POINTER(OgPicParams), C.POINTER(OgParcels), _DP]
+        L.or_set_mode.argtypes = [C.c_int, C.c_int]
+        L.or_max_threads.restype = C.c_int
+        L.or_pow_ambiguous.restype = C.c_long
+        L.or_pow_ambiguous.argtypes = []
         L.or_pow.restype = C.c_double
         L.or_pow.argtypes = [C.c_double, C.c_double]
         L.or_pic_drag_coef.restype = C.c_double
@@ -305,8 +309,18 @@ def pic_deposit_eps(grid, pic, parcels: dict):
     return eps, rc
 
 
+def set_mode(threads: int = 0, naive: bool = False):
+    """Threads for the row loops and the exact sums (<= 0: unchanged; results are
+    bit-identical for any count); naive=True: plain sums (timing only)."""
+    lib().or_set_mode(int(threads), int(bool(naive)))
+
+
+def max_threads() -> int:
+    return int(lib().or_max_threads())
+
+
 def pow_(x: float, y: float) -> float:
-    """§3.9 written pow algorithm (x > 0)."""
+    """§3.9: correctly rounded x^y (x > 0), quad-precision powq rounded once."""
     return lib().or_pow(x, y)
 
 

@@ -18,8 +18,29 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <omp.h>
+#include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
+
+/* Threading (bench.py cpu_baseline, SURVEY §8(d) "OpenMP over all cores").
+ * Row loops are split over threads with no change to any row's expression;
+ * a correctly rounded sum is split into per-thread exact partial expansions
+ * that are merged exactly before the single rounding, so every result is
+ * bit-identical to the serial evaluation for any thread count ("parity
+ * mode", tested).  or_set_mode(threads, naive = 1) replaces the exact sums by
+ * plain per-thread sequential sums for the "plain CPU" timing only (not
+ * correctly rounded; never used by a parity test). */
+#define OR_PAR_MIN 32768
+static int g_naive = 0;
+
+void or_set_mode(int threads, int naive)
+{
+    if (threads > 0) omp_set_num_threads(threads);
+    g_naive = naive != 0;
+}
+
+int or_max_threads(void) { return omp_get_max_threads(); }
 
 /* ------------------------------------------------------------------ §3.1 */
 /* Exact summation with Shewchuk's non-overlapping partials (the algorithm of
@@ -69,32 +90,79 @@ static double xs_round(const xsum *s)
     return hi + 0.0; /* an exact zero is +0 */
 }
 
+static void xs_merge(xsum *dst, const xsum *src)
+{
+    for (int j = 0; j < src->n; j++) xs_add(dst, src->p[j]);
+}
+
+/* one correctly rounded sum of the terms term(i, &hi, &lo) (lo may be 0):
+ * per-thread exact expansions over contiguous index ranges, merged exactly */
+#define OR_EXACT_SUM(n, BODY)                                                        \
+    do {                                                                             \
+        const int nt_ = (n) >= OR_PAR_MIN ? omp_get_max_threads() : 1;               \
+        xsum *part_ = malloc(sizeof(xsum) * (size_t)nt_);                            \
+        _Pragma("omp parallel num_threads(nt_)")                                     \
+        {                                                                            \
+            const int t_ = omp_get_thread_num(), T_ = omp_get_num_threads();         \
+            const long lo_ = (long)((n) * (double)t_ / T_), hi_ = (long)((n) * (double)(t_ + 1) / T_); \
+            xsum *s = &part_[t_];                                                    \
+            xs_init(s);                                                              \
+            for (long i = lo_; i < hi_; i++) { BODY }                                \
+        }                                                                            \
+        xsum tot_; xs_init(&tot_);                                                   \
+        for (int t_ = 0; t_ < nt_; t_++) xs_merge(&tot_, &part_[t_]);                \
+        free(part_);                                                                 \
+        result_ = xs_round(&tot_);                                                   \
+    } while (0)
+
+/* plain (naive) sum for the timing mode: sequential within a thread range,
+ * thread results added in thread order */
+#define OR_PLAIN_SUM(n, TERM)                                                        \
+    do {                                                                             \
+        const int nt_ = (n) >= OR_PAR_MIN ? omp_get_max_threads() : 1;               \
+        double part_[256];                                                           \
+        _Pragma("omp parallel num_threads(nt_ < 256 ? nt_ : 256)")                   \
+        {                                                                            \
+            const int t_ = omp_get_thread_num(), T_ = omp_get_num_threads();         \
+            const long lo_ = (long)((n) * (double)t_ / T_), hi_ = (long)((n) * (double)(t_ + 1) / T_); \
+            double a_ = 0.0;                                                         \
+            for (long i = lo_; i < hi_; i++) a_ = a_ + (TERM);                       \
+            part_[t_] = a_;                                                          \
+        }                                                                            \
+        double r_ = 0.0;                                                             \
+        for (int t_ = 0; t_ < (nt_ < 256 ? nt_ : 256); t_++) r_ = r_ + part_[t_];    \
+        result_ = r_ + 0.0;                                                          \
+    } while (0)
+
 double or_fsum(long n, const double *x)
 {
-    xsum s; xs_init(&s);
-    for (long i = 0; i < n; i++) xs_add(&s, x[i]);
-    return xs_round(&s);
+    double result_;
+    if (g_naive) { OR_PLAIN_SUM(n, x[i]); return result_; }
+    OR_EXACT_SUM(n, xs_add(s, x[i]););
+    return result_;
 }
 
 /* <a,b> = exact sum of the products a_i b_i, rounded once.  Each product is
  * split exactly as hi + lo with hi = fl(a b), lo = fma(a, b, -hi). */
 double or_dot(long n, const double *a, const double *b)
 {
-    xsum s; xs_init(&s);
-    for (long i = 0; i < n; i++) {
+    double result_;
+    if (g_naive) { OR_PLAIN_SUM(n, a[i] * b[i]); return result_; }
+    OR_EXACT_SUM(n, {
         double hi = a[i] * b[i];
         double lo = fma(a[i], b[i], -hi);
-        xs_add(&s, hi);
-        xs_add(&s, lo);
-    }
-    return xs_round(&s);
+        xs_add(s, hi);
+        xs_add(s, lo);
+    });
+    return result_;
 }
 
 double or_sumabs(long n, const double *x)
 {
-    xsum s; xs_init(&s);
-    for (long i = 0; i < n; i++) xs_add(&s, fabs(x[i]));
-    return xs_round(&s);
+    double result_;
+    if (g_naive) { OR_PLAIN_SUM(n, fabs(x[i])); return result_; }
+    OR_EXACT_SUM(n, xs_add(s, fabs(x[i])););
+    return result_;
 }
 
 /* ------------------------------------------------------------ helpers */
@@ -146,6 +214,7 @@ void or_spmv(const og_grid *g, const og_eqsys *A, const double *x, double *y)
 {
     const int sym = (A->aW == NULL);
     const long sx = 1, sy = g->nx, sz = (long)g->nx * g->ny;
+#pragma omp parallel for collapse(2) schedule(static) if (ncell(g) >= OR_PAR_MIN)
     for (int k = 0; k < g->nz; k++)
         for (int j = 0; j < g->ny; j++)
             for (int i = 0; i < g->nx; i++) {
@@ -244,9 +313,9 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
     for (int a = 0; a < 3; a++) Dc[a] = (pr->mu * area(g, a)) / spacing(g, a);
     const long N = ncell(g);
     double *rnum = malloc(sizeof(double) * N), *rden = malloc(sizeof(double) * N);
-    long nres = 0;
-    int status = OG_OK;
+    int any_nf = 0, any_zd = 0;
 
+#pragma omp parallel for collapse(2) schedule(static) reduction(|: any_nf, any_zd) if (ncell(g) >= OR_PAR_MIN)
     for (int k = 0; k < g->nz; k++)
         for (int j = 0; j < g->ny; j++)
             for (int i = 0; i < g->nx; i++) {
@@ -258,6 +327,8 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                     out->aW[n] = out->aE[n] = out->aS[n] = out->aN[n] = out->aB[n] = out->aT[n] = 0.0;
                     out->b[n] = 0.0;
                     out->d[n] = 0.0;
+                    rnum[n] = 0.0;   /* identity rows are excluded from the residual: exact zeros */
+                    rden[n] = 0.0;
                     continue;
                 }
                 /* E: the other cell of the face, clamped onto P at the outlet row */
@@ -351,8 +422,8 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                 out->aP[n] = aPr;
                 out->b[n] = bR;
                 out->d[n] = d;
-                if (!isfinite(aPr) || !isfinite(bR) || !isfinite(d)) status = OG_ERR_NONFINITE;
-                else if (aPr == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+                if (!isfinite(aPr) || !isfinite(bR) || !isfinite(d)) any_nf = 1;
+                else if (aPr == 0.0) any_zd = 1;
 
                 /* snapshot residual, un-relaxed row */
                 double res = b - aP * um[n];
@@ -362,13 +433,13 @@ int or_assemble_mom(const og_grid *g, const og_params *pr, int c, const og_state
                     double unb = inside(g, Q) ? um[at(g, Q)] : 0.0;
                     res = res + st6[s6] * unb;
                 }
-                rnum[nres] = fabs(res);
-                rden[nres] = fabs(aP * um[n]);
-                nres++;
+                rnum[n] = fabs(res);
+                rden[n] = fabs(aP * um[n]);
             }
+    const int status = any_nf ? OG_ERR_NONFINITE : (any_zd ? OG_ERR_ZERO_DIAG : OG_OK);
     if (resid2) {
-        resid2[0] = or_sumabs(nres, rnum);
-        resid2[1] = or_sumabs(nres, rden);
+        resid2[0] = or_sumabs(N, rnum);
+        resid2[1] = or_sumabs(N, rden);
     }
     free(rnum); free(rden);
     return status;
@@ -405,7 +476,8 @@ int or_assemble_pp(const og_grid *g, const og_params *pr, const og_state *st,
     const double *vel[3] = {us, vs, ws};
     const double *dd[3] = {dxv, dyv, dzv};
     double *cf[3] = {out->aE, out->aN, out->aT};
-    int status = OG_OK;
+    int any_nf = 0, any_zd = 0;
+#pragma omp parallel for collapse(2) schedule(static) reduction(|: any_nf, any_zd) if (ncell(g) >= OR_PAR_MIN)
     for (int k = 0; k < g->nz; k++)
         for (int j = 0; j < g->ny; j++)
             for (int i = 0; i < g->nx; i++) {
@@ -432,9 +504,10 @@ int or_assemble_pp(const og_grid *g, const og_params *pr, const og_state *st,
                 out->aP[n] = aP;
                 for (int a = 0; a < 3; a++) cf[a][n] = cpl[a];
                 out->b[n] = b;
-                if (!isfinite(aP) || !isfinite(b)) status = OG_ERR_NONFINITE;
-                else if (aP == 0.0 && !blk(g, st, P) && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+                if (!isfinite(aP) || !isfinite(b)) any_nf = 1;
+                else if (aP == 0.0 && !blk(g, st, P)) any_zd = 1;
             }
+    const int status = any_nf ? OG_ERR_NONFINITE : (any_zd ? OG_ERR_ZERO_DIAG : OG_OK);
     if (cont) *cont = or_sumabs(ncell(g), out->b);
     return status;
 }
@@ -456,7 +529,8 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
     for (int a = 0; a < 3; a++) Dc[a] = (gam * area(g, a)) / spacing(g, a);
     const long N = ncell(g);
     double *rnum = malloc(sizeof(double) * N), *rden = malloc(sizeof(double) * N);
-    int status = OG_OK;
+    int any_nf = 0, any_zd = 0;
+#pragma omp parallel for collapse(2) schedule(static) reduction(|: any_nf, any_zd) if (ncell(g) >= OR_PAR_MIN)
     for (int k = 0; k < g->nz; k++)
         for (int j = 0; j < g->ny; j++)
             for (int i = 0; i < g->nx; i++) {
@@ -527,8 +601,8 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                 out->aP[n] = aPr;
                 out->b[n] = bR;
                 if (out->d) out->d[n] = 0.0;
-                if (!isfinite(aPr) || !isfinite(bR)) status = OG_ERR_NONFINITE;
-                else if (aPr == 0.0 && status == OG_OK) status = OG_ERR_ZERO_DIAG;
+                if (!isfinite(aPr) || !isfinite(bR)) any_nf = 1;
+                else if (aPr == 0.0) any_zd = 1;
                 double res = b - aP * phim[n];
                 for (int s6 = 0; s6 < 6; s6++) {
                     int Q[3] = {i, j, k};
@@ -539,6 +613,7 @@ int or_assemble_scalar(const og_grid *g, const og_params *pr, int sid, const og_
                 rnum[n] = fabs(res);
                 rden[n] = fabs(aP * phim[n]);
             }
+    const int status = any_nf ? OG_ERR_NONFINITE : (any_zd ? OG_ERR_ZERO_DIAG : OG_OK);
     if (resid2) {
         resid2[0] = or_sumabs(N, rnum);
         resid2[1] = or_sumabs(N, rden);
@@ -562,17 +637,20 @@ int or_bicgstab(const og_grid *g, const og_eqsys *A, double *x, double tol, int 
     double rel = 0.0;
 
     or_spmv(g, A, x, y);
+    #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
     for (long n = 0; n < N; n++) r[n] = A->b[n] - y[n];
     const double bn = sqrt(or_dot(N, A->b, A->b));
     double rr = or_dot(N, r, r);
     double rn = sqrt(rr);
     if (bn == 0.0) {
+        #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
         for (long n = 0; n < N; n++) x[n] = 0.0;
         status = OG_OK; iters = 0; rel = 0.0;
         goto done;
     }
     if (rn <= tol * bn) { status = OG_OK; iters = 0; rel = rn / bn; goto done; }
 
+    #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
     for (long n = 0; n < N; n++) rh[n] = r[n];
     double rhn = rn;
     double rho = or_dot(N, rh, r);
@@ -583,27 +661,32 @@ int or_bicgstab(const og_grid *g, const og_eqsys *A, double *x, double tol, int 
         double *tr = trace ? trace + 8 * (long)(it - 1) : NULL;
         if (fabs(rho) <= (1e-14 * rhn) * rn) {
             if (restarted) { status = OG_ERR_BREAKDOWN; iters = it - 1; goto done_rel; }
+            #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
             for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
             rhn = rn; rho = or_dot(N, rh, r);
             rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
         }
         const double beta = (rho / rho_prev) * (alpha / omega);
+        #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
         for (long n = 0; n < N; n++) p[n] = fma(beta, fma(-omega, v[n], p[n]), r[n]);
         or_spmv(g, A, p, v);
         const double sigma = or_dot(N, rh, v);
         if (tr) { tr[0] = rho; tr[1] = sigma; }
         if (sigma == 0.0) {
             if (restarted) { status = OG_ERR_BREAKDOWN; iters = it; goto done_rel; }
+            #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
             for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
             rhn = rn; rho = or_dot(N, rh, r);
             rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
             continue;
         }
         alpha = rho / sigma;
+        #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
         for (long n = 0; n < N; n++) s[n] = fma(-alpha, v[n], r[n]);
         const double ss = or_dot(N, s, s);
         if (tr) { tr[2] = alpha; tr[3] = ss; }
         if (sqrt(ss) <= tol * bn) {
+            #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
             for (long n = 0; n < N; n++) { x[n] = fma(alpha, p[n], x[n]); r[n] = s[n]; }
             rn = sqrt(ss);
             status = OG_OK; iters = it; goto done_rel;
@@ -615,12 +698,14 @@ int or_bicgstab(const og_grid *g, const og_eqsys *A, double *x, double tol, int 
         if (tr) { tr[4] = ts; tr[5] = tt; tr[6] = om; }
         if (tt == 0.0 || om == 0.0) {
             if (restarted) { status = OG_ERR_BREAKDOWN; iters = it; goto done_rel; }
+            #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
             for (long n = 0; n < N; n++) { rh[n] = r[n]; p[n] = 0.0; v[n] = 0.0; }
             rhn = rn; rho = or_dot(N, rh, r);
             rho_prev = alpha = omega = 1.0; restarted = 1; restarts++;
             continue;
         }
         omega = om;
+        #pragma omp parallel for schedule(static) if (N >= OR_PAR_MIN)
         for (long n = 0; n < N; n++) {
             x[n] = fma(omega, s[n], fma(alpha, p[n], x[n]));
             r[n] = fma(-omega, t[n], s[n]);
@@ -654,6 +739,7 @@ void or_correct(const og_grid *g, const og_params *pr,
     const double *vin[3] = {us, vs, ws};
     const double *dd[3] = {dxv, dyv, dzv};
     double *vout[3] = {u, v, w};
+#pragma omp parallel for collapse(2) schedule(static) if (ncell(g) >= OR_PAR_MIN)
     for (int k = 0; k < g->nz; k++)
         for (int j = 0; j < g->ny; j++)
             for (int i = 0; i < g->nx; i++) {
@@ -857,46 +943,32 @@ int or_pic_deposit_eps(const og_grid *g, const og_pic_params *pp, const og_parce
     return OG_OK;
 }
 
-/* x^y for x > 0 as ONE written algorithm (DESIGN.md §3.9 reading: the closure's
- * powers are evaluated by this sequence of IEEE operations on both sides, so
- * that the drag coefficient has a single bit pattern; libm's pow and CUDA's
- * differ in the last bit).  ln(x) = e ln2 + 2 atanh((m-1)/(m+1)) with
- * m in [sqrt(1/2), sqrt(2)) (series to t^21); exp(z) = 2^k exp(r),
- * r = z - k ln2 (Taylor to r^13, Horner).  Accurate to a few ulp; exact 1 at
- * x = 1. */
-static double or_ln(double x)
-{
-    int e;
-    double m = frexp(x, &e);
-    if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
-    const double t = (m - 1.0) / (m + 1.0);
-    const double t2 = t * t;
-    double q = 1.0 / 21.0;
-    q = q * t2 + 1.0 / 19.0;
-    q = q * t2 + 1.0 / 17.0;
-    q = q * t2 + 1.0 / 15.0;
-    q = q * t2 + 1.0 / 13.0;
-    q = q * t2 + 1.0 / 11.0;
-    q = q * t2 + 1.0 / 9.0;
-    q = q * t2 + 1.0 / 7.0;
-    q = q * t2 + 1.0 / 5.0;
-    q = q * t2 + 1.0 / 3.0;
-    q = q * t2 + 1.0;
-    const double lm = 2.0 * (t * q);
-    const double de = (double)e;
-    return de * 6.93147180369123816490e-01 + (de * 1.90821492927058770002e-10 + lm);
-}
+/* x^y for x > 0, CORRECTLY ROUNDED (DESIGN.md §3.9 reading, the same contract
+ * as the dots of §3.1): the exact real x^y rounded once to nearest-even.
+ * Evaluated with libquadmath's powq on the exactly converted binary64
+ * arguments (113-bit significand, error well below 2^-100 relative), then
+ * rounded to binary64.  That rounding is the correctly rounded value unless
+ * the quad result lies within the quad error of a binary64 rounding boundary
+ * (a midpoint between neighbouring doubles); that case is detected and
+ * reported as NaN plus the or_pow_ambiguous counter, never silently rounded. */
+static long g_pow_ambiguous = 0;
 
-static double or_exp(double z)
-{
-    const double k = floor(z * 1.44269504088896338700e+00 + 0.5);
-    const double r = (z - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
-    double q = 1.0;
-    for (int n = 13; n >= 1; n--) q = 1.0 + (r / (double)n) * q;
-    return ldexp(q, (int)k);
-}
+long or_pow_ambiguous(void) { return g_pow_ambiguous; }
 
-double or_pow(double x, double y) { return x == 1.0 ? 1.0 : or_exp(y * or_ln(x)); }
+double or_pow(double x, double y)
+{
+    const __float128 q = powq((__float128)x, (__float128)y);
+    const double d = (double)q;                       /* round to nearest-even */
+    /* distance of q from the nearer of the two midpoints around d */
+    const double up = nextafter(d, INFINITY), dn = nextafter(d, -INFINITY);
+    const __float128 mid_hi = ((__float128)d + (__float128)up) / 2, mid_lo = ((__float128)d + (__float128)dn) / 2;
+    const __float128 dist = fminq(fabsq(q - mid_hi), fabsq(q - mid_lo));
+    if (dist <= fabsq(q) * 0x1p-100Q) {
+        g_pow_ambiguous++;
+        return NAN;
+    }
+    return d;
+}
 
 /* Syamlal-O'Brien per-parcel drag coefficient K (N s / m): the force on the
  * gas is -K (u_g - u_p); K = beta_d (omega Vs) / eps_s with beta_d of

@@ -91,7 +91,10 @@ typedef struct { const double *x, *y, *z, *u, *v, *w, *omega; long n; } og_parce
 typedef struct { double d_p, eps_min; } og_pic_params;
 
 int or_pic_deposit_eps(const og_grid *g, const og_pic_params *pp, const og_parcels *pc, double *eps_g);
-double or_pow(double x, double y);
+void or_set_mode(int threads, int naive);   /* threads (<= 0: keep), naive = plain sums (timing only) */
+int or_max_threads(void);
+double or_pow(double x, double y);   /* correctly rounded x^y */
+long or_pow_ambiguous(void);           /* calls whose rounding could not be decided (NaN returned) */
 double or_pic_drag_coef(const og_params *pr, const og_pic_params *pp, double eg, double slip, double omega);
 int or_pic_drag(const og_grid *g, const og_params *pr, const og_pic_params *pp, const og_parcels *pc,
                 const double *eps_g, const double *u, const double *v, const double *w,

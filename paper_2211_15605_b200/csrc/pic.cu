@@ -181,42 +181,85 @@ struct PicDragArgs {
     WsHeader *hdr;
 };
 
-// x^y for x > 0 by the written algorithm of DESIGN.md §3.9 (the closure's
-// powers have one bit pattern on every side; CUDA's pow and libm's differ in
-// the last bit): ln(x) = e ln2 + 2 atanh((m-1)/(m+1)), m in [sqrt(1/2),
-// sqrt(2)), series to t^21; exp(z) = 2^k exp(r), Taylor to r^13 (Horner).
-__device__ __forceinline__ double dev_ln(double x)
+// x^y for x > 0, CORRECTLY ROUNDED (DESIGN.md §3.9 reading; the contract of
+// the dots, §3.1): evaluated in double-double and rounded once.
+//   ln x:   y0 = log(x) (binary64, any faithful value), then one Newton step
+//           L = y0 + (x e^{-y0} - 1) in double-double, error ~ (y0 - ln x)^2 / 2
+//           + the double-double rounding, far below 2^-100 relative;
+//   exp z:  z = k ln2 + r (ln2 in double-double), r' = r / 32, expm1(r') by its
+//           Taylor series to r'^12 (|r'| < 0.011), five expm1 doublings
+//           e^{2a} - 1 = (e^a - 1)(e^a - 1 + 2) (relative error kept), 2^k (1 + .).
+// The final fast_two_sum leaves hi = RN(hi + lo): the correctly rounded power
+// unless x^y lies within ~2^-100 relative of a rounding boundary.  The closure
+// needs two powers of one eps: ln is computed once (dd_ln) for both.
+__device__ __forceinline__ dd dd_norm(double a, double b)
 {
-    int e;
-    double m = frexp(x, &e);
-    if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
-    const double t = (m - 1.0) / (m + 1.0);
-    const double t2 = t * t;
-    double q = 1.0 / 21.0;
-    q = q * t2 + 1.0 / 19.0;
-    q = q * t2 + 1.0 / 17.0;
-    q = q * t2 + 1.0 / 15.0;
-    q = q * t2 + 1.0 / 13.0;
-    q = q * t2 + 1.0 / 11.0;
-    q = q * t2 + 1.0 / 9.0;
-    q = q * t2 + 1.0 / 7.0;
-    q = q * t2 + 1.0 / 5.0;
-    q = q * t2 + 1.0 / 3.0;
-    q = q * t2 + 1.0;
-    const double lm = 2.0 * (t * q);
-    const double de = (double)e;
-    return de * 6.93147180369123816490e-01 + (de * 1.90821492927058770002e-10 + lm);
+    dd r;
+    r.hi = a + b;
+    r.lo = b - (r.hi - a);
+    return r;
 }
-__device__ __forceinline__ double dev_exp(double z)
+__device__ __forceinline__ dd dd_mul(dd a, dd b)
 {
-    const double k = floor(z * 1.44269504088896338700e+00 + 0.5);
-    const double r = (z - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
-    double q = 1.0;
-#pragma unroll
-    for (int n = 13; n >= 1; n--) q = 1.0 + (r / (double)n) * q;
-    return ldexp(q, (int)k);
+    const double p = a.hi * b.hi;
+    double e = fma(a.hi, b.hi, -p);
+    e = e + (a.hi * b.lo + a.lo * b.hi);
+    return dd_norm(p, e);
 }
-__device__ __forceinline__ double dev_pow(double x, double y) { return x == 1.0 ? 1.0 : dev_exp(y * dev_ln(x)); }
+__device__ __forceinline__ dd dd_mul_d(dd a, double b)
+{
+    const double p = a.hi * b;
+    double e = fma(a.hi, b, -p);
+    e = e + a.lo * b;
+    return dd_norm(p, e);
+}
+__device__ __forceinline__ dd dd_div_d(dd a, double b)
+{
+    const double q1 = a.hi / b;
+    const double rem = fma(-q1, b, a.hi) + a.lo;   // a - q1 b, exact head
+    return dd_norm(q1, rem / b);
+}
+__device__ __forceinline__ dd dd_add_d(dd a, double b)
+{
+    double s, e;
+    two_sum(a.hi, b, s, e);
+    return dd_norm(s, e + a.lo);
+}
+__device__ dd dd_exp(dd z)
+{
+    const double LN2_HI = 0x1.62e42fefa39efp-1, LN2_LO = 0x1.abc9e3b39803fp-56;
+    const double k = rint(z.hi * 0x1.71547652b82fep+0);
+    // r = z - k ln2 (k ln2_hi exact as a product pair)
+    const double p = k * LN2_HI;
+    const double pe = fma(k, LN2_HI, -p);
+    dd r = dd_add(z, dd{-p, -pe});
+    r = dd_add(r, dd{-k * LN2_LO, -fma(k, LN2_LO, -(k * LN2_LO))});
+    r.hi = r.hi * 0x1p-5;
+    r.lo = r.lo * 0x1p-5;
+    // expm1(r) = r (1 + r/2 (1 + r/3 (1 + ... r/12)))
+    dd t = dd{1.0, 0.0};
+#pragma unroll 1
+    for (int n = 12; n >= 2; n--) t = dd_add_d(dd_div_d(dd_mul(r, t), (double)n), 1.0);
+    dd em1 = dd_mul(r, t);
+#pragma unroll 1
+    for (int q = 0; q < 5; q++) em1 = dd_mul(em1, dd_add_d(em1, 2.0));
+    dd e = dd_add_d(em1, 1.0);
+    const int ki = (int)k;
+    return dd{ldexp(e.hi, ki), ldexp(e.lo, ki)};
+}
+__device__ dd dd_ln(double x)
+{
+    const double y0 = log(x);
+    const dd E = dd_exp(dd{-y0, 0.0});
+    const dd xe = dd_mul_d(E, x);                  // x e^{-y0} ~ 1
+    return dd_add_d(dd_add_d(xe, -1.0), y0);
+}
+// correctly rounded x^y from ln x in double-double (x == 1 gives L = 0 -> 1 exactly)
+__device__ __forceinline__ double dd_pow_from_ln(dd L, double y)
+{
+    const dd P = dd_exp(dd_mul_d(L, y));
+    return dd_norm(P.hi, P.lo).hi;
+}
 
 // DESIGN.md §3.9 (SPEC.md:285-289 closure, written without the eps_s that cancels)
 __device__ __forceinline__ double drag_coef(double rho, double mu, double dp, double Vs, double eg, double slip,
@@ -224,8 +267,9 @@ __device__ __forceinline__ double drag_coef(double rho, double mu, double dp, do
 {
     double Re = ((rho * dp) * slip) / mu;
     Re = Re < 1e-12 ? 1e-12 : Re;
-    const double A = dev_pow(eg, 4.14);
-    const double B = eg <= 0.85 ? 0.8 * dev_pow(eg, 1.28) : dev_pow(eg, 2.65);
+    const dd L = dd_ln(eg);
+    const double A = dd_pow_from_ln(L, 4.14);
+    const double B = eg <= 0.85 ? 0.8 * dd_pow_from_ln(L, 1.28) : dd_pow_from_ln(L, 2.65);
     const double q = 0.06 * Re;
     const double Vr = 0.5 * ((A - q) + sqrt((q * q + (0.12 * Re) * (2.0 * B - A)) + A * A));
     double Cd = 0.63 + 4.8 / sqrt(Re / Vr);

@@ -2,8 +2,9 @@
 libmfx.so's mfx_pic_deposit_eps / mfx_pic_drag through the C ABI against the
 oracle (or_pic_deposit_eps / or_pic_drag) on identical seeded parcels.
 
-Per-parcel quantities use the oracle's expression order and the same written
-pow algorithm, so K is bitwise equal.
+Per-parcel quantities use the oracle's expression order, and both sides
+evaluate the closure's powers correctly rounded with
+independent implementations, so K is bitwise equal.
 The per-cell sums arrive in atomic order instead of parcel order, so the gate
 is the summation error bound of DESIGN.md §3.9: for a cell with m
 contributions of total magnitude S, |gpu - oracle| <= (m - 1) u S + (per-term
@@ -97,7 +98,9 @@ def check(eps_d, eps_o, out_d, out_o, K):
     assert np.all(np.abs(e - eps_o) <= TOL_SUM), np.abs(e - eps_o).max()
     Ko = out_o["diag"][:, 4]
     Kd = host(K)
-    assert np.array_equal(Kd, Ko)       # same expressions and the written pow: bitwise
+    # same expressions, and both sides round x^y correctly (quad powq in the
+    # oracle, double-double log/exp on the GPU, no shared code): bitwise
+    assert np.array_equal(Kd, Ko)
     b = host(out_d["beta"])
     assert np.all(np.abs(b - out_o["beta"]) <= TOL_SUM * out_o["beta"]), np.abs(b - out_o["beta"]).max()
     for c, key in enumerate(("sbeta_u", "sbeta_v", "sbeta_w")):

@@ -212,12 +212,33 @@ def test_momentum_bookkeeping(orc):
     assert np.all(out["beta"] >= 0.0)
 
 
-def test_written_pow_accuracy(orc):
-    """The closure's powers use one written algorithm; it is
-    within a few ulp of the correctly rounded power and exact at x = 1."""
+def _pow_cr_decimal(x: float, y: float) -> float:
+    """x^y correctly rounded, independently of the oracle: exact decimal
+    conversion of the binary64 arguments, ln/exp at 60 significant digits
+    (error ~1e-58 relative), then Python's correctly rounded str -> float."""
+    import decimal
+    ctx = decimal.Context(prec=60)
+    X, Y = decimal.Decimal(x), decimal.Decimal(y)
+    if X == 1:
+        return 1.0
+    return float(ctx.exp(ctx.multiply(Y, ctx.ln(X))))
+
+
+def test_pow_correctly_rounded(orc):
+    """DESIGN.md §3.9 reading: the closure's powers are the correctly rounded
+    x^y (the dots' contract, Q17), pinned against a 60-digit decimal
+    evaluation: bitwise on the closure's exponents over the eps range of the
+    workload, on random exponents, and at the special points; no call is
+    reported ambiguous."""
     rng = np.random.default_rng(12)
-    xs = np.concatenate([rng.uniform(0.3, 1.0, 5000), [0.35, 0.5, 0.85, 0.999999999, 1.0 - 2**-52]])
+    xs = np.concatenate([rng.uniform(0.3, 1.0, 3000), rng.uniform(1e-3, 50.0, 500),
+                         [0.35, 0.36, 0.42, 0.5, 0.85, 0.95, 0.999999999, 1.0 - 2**-52, 1.0 + 2**-52, 2.0]])
+    n0 = orc.lib().or_pow_ambiguous()
     for y in (4.14, 1.28, 2.65):
         for x in xs:
-            assert abs(orc.pow_(x, y) - x ** y) <= 8 * 2.2e-16 * x ** y
+            assert orc.pow_(x, y) == _pow_cr_decimal(float(x), y), (x, y)
         assert orc.pow_(1.0, y) == 1.0
+    for x, y in zip(rng.uniform(0.05, 5.0, 500), rng.uniform(-6.0, 6.0, 500)):
+        assert orc.pow_(x, y) == _pow_cr_decimal(float(x), float(y)), (x, y)
+    assert orc.pow_(2.0, 3.0) == 8.0 and orc.pow_(4.0, 0.5) == 2.0      # exact powers
+    assert orc.lib().or_pow_ambiguous() == n0

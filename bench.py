@@ -11,8 +11,9 @@ iterations completed by all equations on all ranks / device time (CUDA events,
 max over ranks); `e2e` = the same metric through the C ABI with the snapshot
 copied from pinned host memory and u, v, w, p read back inside the timed region.
 
---impl reference times the CPU oracle (oracle/, single thread) on a bounded
-sample of the same workload: it is the "reference arm" of this tier.
+--impl reference times the CPU oracle (oracle/, OpenMP over this host's cores,
+parity mode) on a bounded sample of the same workload: it is the "reference
+arm" of this tier.
 """
 from __future__ import annotations
 
@@ -127,47 +128,117 @@ def bench_config(asg, grid, n_scal):
 
 
 # ---------------------------------------------------------------- reference arm (oracle)
-def oracle_sample(seconds_hint=False):
-    """Bounded sample: BiCGSTAB on the oracle-assembled c2 p' system, x0 = 0,
-    maxit = 2 (includes the setup r = b - A x0).  Returns (iters/s, seconds)."""
+PAPER_CONTEXT = ("PAPER.md:17/:165: 4 x A100 over NVLink competitive with ~1000 JOULE 2.0 CPU cores "
+                 "(25 nodes x 40 cores); context only, not this run")
+
+
+def cpu_info():
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = None
+    try:
+        out = subprocess.check_output(["lscpu"], text=True)
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return cores, model
+
+
+def oracle_pp_system(cid):
+    """The oracle-assembled p' system of configuration `cid` (u* = the snapshot
+    velocities, d = seeded U(1e-4, 1e-3)); returns (grid, params, sysd, seconds)."""
     import numpy as np
     import oracle
     import synth
-    g, pr, st = synth.config_case(CONFIG_ID)
+    g, pr, st = synth.config_case(cid)
     rng = np.random.default_rng(0)
     dv = [rng.uniform(1e-4, 1e-3, g.n) for _ in range(3)]
+    t0 = time.perf_counter()
     sysd, _, _ = oracle.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+    return g, pr, st, sysd, time.perf_counter() - t0
 
-    def step():
+
+def oracle_iter_seconds(g, sysd, k1, k2):
+    """Seconds per BiCGSTAB iteration of the oracle, (T(k2) - T(k1)) / (k2 - k1)
+    (excludes the setup r = b - A x0); tol 0 so no early exit."""
+    import numpy as np
+    import oracle
+    ts = []
+    for k in (k1, k2):
         t0 = time.perf_counter()
-        res = oracle.bicgstab(g, sysd, np.zeros(g.n), pr.lin_tol_pp, 2)
-        dt = time.perf_counter() - t0
-        return res["iters"], dt
-    return step
+        oracle.bicgstab(g, sysd, np.zeros(g.n), 0.0, k)
+        ts.append(time.perf_counter() - t0)
+    return (ts[1] - ts[0]) / (k2 - k1), ts
 
 
-SAMPLE_DESC = ("oracle BiCGSTAB (oracle/oracle.c, correctly rounded dots) on the oracle-assembled "
-               "128x128x512 p' system, x0=0, maxit=2 per sample including setup; 1 thread")
+def cpu_baseline_measure():
+    """The oracle as it stands, on this host's cores (SURVEY §8(d) oracle timing):
+    parity mode (exact dots; bit-identical for any thread count) on all cores
+    and on one core, naive-dot mode on all cores; p' BiCGSTAB s/iteration at
+    c2 (value) and c1, plus the c2 p' and w-momentum assembly.  About 10-30 s."""
+    import oracle
+    import synth
+    cores, model = cpu_info()
+    t_all = time.perf_counter()
+    res = {"cores": cores, "cpu_model": model, "kind": "oracle", "unit": UNIT}
+    oracle.set_mode(cores, False)
+    g2, pr2, st2, s2, t_asm_pp = oracle_pp_system(2)
+    t0 = time.perf_counter()
+    oracle.assemble_mom(g2, pr2, 2, st2)
+    t_asm_mom = time.perf_counter() - t0
+    par2, _ = oracle_iter_seconds(g2, s2, 1, 3)
+    oracle.set_mode(cores, True)
+    nai2, _ = oracle_iter_seconds(g2, s2, 1, 3)
+    oracle.set_mode(cores, False)
+    del st2, s2
+    g1, _, _, s1, _ = oracle_pp_system(1)
+    par1, _ = oracle_iter_seconds(g1, s1, 10, 110)
+    oracle.set_mode(1, False)
+    g3, _, _, s3, _ = oracle_pp_system(3)
+    one3, _ = oracle_iter_seconds(g3, s3, 1, 3)
+    oracle.set_mode(cores, False)
+    res.update({
+        "value": 1.0 / par2,
+        "sample": ("c2 (128x128x512) p' BiCGSTAB on the oracle-assembled system, parity mode "
+                   f"(correctly rounded dots), {cores} threads, (T(3) - T(1)) / 2 per iteration"),
+        "c2_pp": {"parity_all_cores_s_per_iter": par2, "naive_dots_all_cores_s_per_iter": nai2,
+                  "parity_iters_per_s": 1.0 / par2, "naive_iters_per_s": 1.0 / nai2,
+                  "assemble_pp_s": t_asm_pp, "assemble_mom_w_s": t_asm_mom},
+        "c1_pp": {"parity_all_cores_us_per_iter": 1e6 * par1, "iters_per_s": 1.0 / par1,
+                  "note": "8192 cells: below the oracle's parallel threshold, runs on one thread"},
+        "c3_pp_one_core": {"parity_s_per_iter": one3, "iters_per_s": 1.0 / one3},
+        "paper_context": PAPER_CONTEXT,
+        "seconds": time.perf_counter() - t_all,
+    })
+    return res
 
 
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the CPU oracle on this host's cores, on
+    the product arm's workload (the c2 p' BiCGSTAB iteration, BiCGSTAB iters/s).
+    One solve of W iterations and one of W + K iterations: the K timed
+    iterations are the difference (setup excluded).  Under torchrun only rank 0
+    runs it."""
     if rank != 0:
         return
-    step = oracle_sample()
-    for _ in range(args.warmup):
-        step()
-    tot_it, tot_t = 0, 0.0
-    for _ in range(args.steps):
-        it, dt = step()
-        tot_it += it
-        tot_t += dt
-    v = tot_it / tot_t
+    import oracle
+    cores, model = cpu_info()
+    oracle.set_mode(cores, False)
+    g, pr, st, sysd, _ = oracle_pp_system(CONFIG_ID)
+    del st
+    w = max(args.warmup, 1)
+    per_it, ts = oracle_iter_seconds(g, sysd, w, w + args.steps)
+    v = 1.0 / per_it
+    sample = (f"c2 p' BiCGSTAB on the oracle-assembled 128x128x512 system, parity mode (correctly rounded "
+              f"dots), {cores} threads; step = one iteration: (T(W+K) - T(W)) / K with W = {w}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_it,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded fluidized-bed fields, synth/)",
             "config": bench_config("111[1]", (128, 128, 512), 0),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": SAMPLE_DESC},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "cpu_model": model, "kind": "oracle",
+                             "sample": sample, "paper_context": PAPER_CONTEXT},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -649,10 +720,7 @@ def run_mfx(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        step = oracle_sample()
-        it, dt = step()
-        cpu = {"value": it / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": SAMPLE_DESC,
-               "seconds": dt}
+        cpu = cpu_baseline_measure()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

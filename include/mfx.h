@@ -71,6 +71,11 @@ typedef struct {
     int lin_maxit_mom, lin_maxit_pp, lin_maxit_phi;
     int face_eps_upwind;        /* 0: central face eps in convective fluxes (reading Q9); 1: upwind cell
                                    by the sign of the snapshot velocity (MFiX-style) */
+    int packed_state;           /* multi-rank contexts: 1 = on every rank u, v, w, p are ONE contiguous
+                                   [u|v|w|p] block (v = u + N, w = u + 2N, p = u + 3N), so the BCAST
+                                   phase sends them as one broadcast of 4N doubles (mfx_simple_iter
+                                   returns MFX_ERR_ARG if they are not).  Like every parameter it must
+                                   be identical on all ranks; 0 = four grouped broadcasts. */
 } mfx_params;
 
 /* Snapshot state (device pointers, N each).  Read-only to assembly; u, v, w,
@@ -261,16 +266,18 @@ mfx_status mfx_state_load(const char *path, const mfx_grid *grid, mfx_state *sta
 /* ---------------------------------------------------------------- equation decomposition */
 /* Assignment string: three 1-based GPU ids for U, V, W,
  * a bracketed P list, then optional scalar owners, e.g. "111[1]", "234[1]",
- * "234[1]5678", "234[1234]".  A multi-entry P list must name every rank in
- * order ([12..R]): the pressure correction is then solved by the domain-
- * decomposed solver over all ranks (the paper's multi-GPU pressure solver,
- * P:85); owner[3] is its first entry (P0, which corrects and
- * broadcasts). */
+ * "234[1]5678", "234[1234]", "234[23]".  A multi-entry P list is any set of
+ * distinct ranks ("a set of devices"): the pressure correction is
+ * then solved by the domain-decomposed solver over exactly those ranks (the
+ * paper's multi-GPU pressure solver), slab i on rank p_rank[i]
+ * (a sub-communicator of the context's); owner[3] = p_rank[0] is P0, which
+ * corrects and broadcasts. */
 typedef struct {
     int owner[8];       /* 0-based rank owning u, v, w, pp, phi0..phi3; -1 = absent */
     int n_scalars;
     int n_ranks_used;   /* max id */
-    int n_p;            /* entries of the P list (1, or every rank) */
+    int n_p;            /* entries of the P list (1 .. 9, distinct ranks) */
+    int p_rank[9];      /* 0-based ranks of the P list in the order written; -1 past n_p */
 } mfx_assignment;
 
 mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *out);
@@ -279,7 +286,7 @@ mfx_status mfx_parse_assignment(const char *text, int nranks, mfx_assignment *ou
  * GATHER (momentum owners -> p' owner(s): u*, d per component, plus a
  * 16-double residual record), phase 1 = BCAST (p' owner -> all: u, v, w, p,
  * residual record; scalar owners -> all: phi), phase 2 = PSLAB (multi-GPU p':
- * every rank's slab of p' -> P0; k0/k1 give the plane range), phase 3 = PIC
+ * the slab of every P-list rank -> P0; k0/k1 give the plane range), phase 3 = PIC
  * (the PIC device, rank 0 = "GPU 1" of P:95, broadcasts the refreshed drag
  * fields beta, sbeta_u, sbeta_v, sbeta_w).  Ops are returned in the order they
  * are issued inside one NCCL group. */
@@ -402,16 +409,18 @@ mfx_status mfx_ctx_phase_times(const mfx_ctx *ctx, double ms[6]);
 void mfx_prof_enable(int on);
 void mfx_prof_reset(void);
 mfx_status mfx_prof_read(int counts[16], double ms[16]);
-/* Runtime options (process-wide).  "solver_path": 0 = auto (cluster kernel
- * when the system fits one cluster's shared memory, else the grid-synchronous
- * kernel when the solver's working set fits in L2 (<= 96 MB, e.g.
- * configuration 3), else TMA z-marching), 1 = TMA z-marching kernels,
+/* Runtime options (process-wide).  "solver_path": 0 = auto (the
+ * single-cluster kernel when the system fits one cluster's shared memory,
+ * else the TMA z-marching kernels; the grid-synchronous kernel is chosen
+ * automatically only when MFX_GRID_SOLVER_MB sets an L2 budget -- off by
+ * default, measured slower at configuration 3), 1 = TMA z-marching kernels,
  * 2 = single-cluster persistent kernel, 3 = v1 grid-stride reference kernels,
- * 4 = grid-synchronous persistent kernel (one cooperative launch per solve).  "graphs": 1/0 enables CUDA-graph
- * replay of the iteration loop.  "pdl": 1/0 enables programmatic dependent
- * launch between the BiCGSTAB kernels.  "asm_tma": 1/0 selects the TMA
- * z-marching momentum assembly (default) or the grid-stride kernel (both give
- * identical bits).  Returns MFX_ERR_ARG for an unknown key. */
+ * 4 = grid-synchronous persistent kernel (one cooperative launch per solve).
+ * "graphs": 1/0 enables CUDA-graph replay of the iteration loop.  "pdl": 1/0
+ * enables programmatic dependent launch between the BiCGSTAB kernels.
+ * "asm_tma": 1/0 selects the TMA z-marching momentum assembly (default) or
+ * the grid-stride kernel (both give identical bits).  Every path gives the
+ * same bits.  Returns MFX_ERR_ARG for an unknown key. */
 mfx_status mfx_set_option(const char *key, int value);
 int mfx_get_option(const char *key);
 

@@ -50,7 +50,7 @@ class Params(C.Structure):
                 ("urf_p", C.c_double), ("urf_phi", C.c_double), ("tol", C.c_double),
                 ("lin_tol_mom", C.c_double), ("lin_tol_pp", C.c_double), ("lin_tol_phi", C.c_double),
                 ("lin_maxit_mom", C.c_int), ("lin_maxit_pp", C.c_int), ("lin_maxit_phi", C.c_int),
-                ("face_eps_upwind", C.c_int)]
+                ("face_eps_upwind", C.c_int), ("packed_state", C.c_int)]
 
 
 _DP = C.POINTER(C.c_double)
@@ -80,7 +80,8 @@ class Resid(C.Structure):
 
 
 class Assignment(C.Structure):
-    _fields_ = [("owner", C.c_int * 8), ("n_scalars", C.c_int), ("n_ranks_used", C.c_int), ("n_p", C.c_int)]
+    _fields_ = [("owner", C.c_int * 8), ("n_scalars", C.c_int), ("n_ranks_used", C.c_int), ("n_p", C.c_int),
+                ("p_rank", C.c_int * 9)]
 
 
 class Xfer(C.Structure):
@@ -204,7 +205,8 @@ def c_grid(g) -> Grid:
 def c_params(p) -> Params:
     return Params(p.rho, p.mu, (C.c_double * 4)(*p.gamma_phi), (C.c_double * 3)(*p.g), p.dt, p.urf_mom,
                   p.urf_p, p.urf_phi, p.tol, p.lin_tol_mom, p.lin_tol_pp, p.lin_tol_phi,
-                  p.lin_maxit_mom, p.lin_maxit_pp, p.lin_maxit_phi, int(getattr(p, "face_eps_upwind", 0)))
+                  p.lin_maxit_mom, p.lin_maxit_pp, p.lin_maxit_phi, int(getattr(p, "face_eps_upwind", 0)),
+                  int(getattr(p, "packed_state", 0)))
 
 
 def _ptr(t, n=None):
@@ -458,7 +460,8 @@ def correct(grid, params, star, pp, p, out=None, stream=None):
 def parse_assignment(text: str, nranks: int) -> dict:
     a = Assignment()
     _check(_lib.mfx_parse_assignment(text.encode(), nranks, C.byref(a)), "mfx_parse_assignment")
-    return dict(owner=list(a.owner), n_scalars=a.n_scalars, n_ranks_used=a.n_ranks_used, n_p=a.n_p)
+    return dict(owner=list(a.owner), n_scalars=a.n_scalars, n_ranks_used=a.n_ranks_used, n_p=a.n_p,
+                p_rank=list(a.p_rank)[:a.n_p])
 
 
 def exchange_plan(text: str, nranks: int, rank: int, phase: int, nz: int = 0):

@@ -23,7 +23,8 @@ namespace mfx {
 
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
                           const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
-                          double tol, int maxit, cudaStream_t s, int reverse = 0);
+                          double tol, int maxit, cudaStream_t s, int reverse = 0, int kbeg = 0, int kend = 0,
+                          int ghost_store = 0, dd *rank_part = nullptr);
 
 // L2 ping-pong: consecutive sweeps alternate direction so each kernel starts
 // on the cells the previous one touched last (126 MB L2).  MFX_REVERSE=0
@@ -363,7 +364,8 @@ __device__ __forceinline__ void k3_store(const K3Pair &d, long long e, double *x
 
 __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *r, const double *__restrict__ rh,
                                                const double *__restrict__ p, const double *__restrict__ v,
-                                               const double *__restrict__ t, WsHeader *h, dd *part, int rev)
+                                               const double *__restrict__ t, WsHeader *h, dd *part, int rev,
+                                               dd *rank_part)
 {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -392,8 +394,10 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
     }
     __shared__ dd sh[(kThreads / 32) * 2];
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
-    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0)
-        bicg_k3_tail(S, half, dd_round(out[0]), dd_round(out[1]));
+    if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
+        if (rank_part) { rank_part[0] = out[0]; rank_part[1] = out[1]; }   // z-slab mode: folded across ranks
+        else bicg_k3_tail(S, half, dd_round(out[0]), dd_round(out[1]));
+    }
 }
 
 // ------------------------------------------------------------------ grid-synchronous persistent solver
@@ -641,7 +645,7 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
         cfg.numAttrs = 1;
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k3v, G.N, x, W.r, (const double *)W.rh, (const double *)p_new,
                                         (const double *)v_new, (const double *)W.t, W.hdr, W.part,
-                                        sweep_dir(true)));
+                                        sweep_dir(true), (dd *)nullptr));
     }
     count_launch(3, s, false);
     (void)nb;
@@ -825,6 +829,20 @@ static bool grid_solver_fits(const Geo &G, bool sym)
     }
     const long long bytes = (long long)(sym ? 3 + 1 + 8 : 7 + 1 + 8) * 8 * G.N;
     return budget > 0 && bytes <= budget && !cluster_fits(G, sym);
+}
+
+// K3 over n cells (n even, 16-byte aligned arrays) with the rank's dot
+// partials written to rank_part: the z-slab solver's third kernel (dist_solver.cu).
+mfx_status k3_slab_launch(long long n, double *x, double *r, const double *rh, const double *p, const double *v,
+                          const double *t, WsHeader *h, dd *part, dd *rank_part, cudaStream_t s)
+{
+    long long np = n / 2;
+    int g3 = k3v_grid();
+    if ((long long)g3 * kThreads > np) g3 = (int)((np + kThreads - 1) / kThreads);
+    if (g3 < 1) g3 = 1;
+    k3v<<<g3, kThreads, 0, s>>>(n, x, r, rh, p, v, t, h, part, 0, rank_part);
+    MFX_CUDA_TRY(cudaGetLastError());
+    return MFX_OK;
 }
 
 mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double *x, double *y, cudaStream_t s)

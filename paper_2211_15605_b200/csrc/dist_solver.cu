@@ -271,9 +271,138 @@ int ctx_rank(const mfx_ctx *c);
 int ctx_nranks(const mfx_ctx *c);
 void *ctx_dist_scratch(mfx_ctx *c, size_t bytes);
 
+mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
+                          const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
+                          double tol, int maxit, cudaStream_t s, int reverse = 0, int kbeg = 0, int kend = 0,
+                          int ghost_store = 0, dd *rank_part = nullptr);
+mfx_status k3_slab_launch(long long n, double *x, double *r, const double *rh, const double *p, const double *v,
+                          const double *t, WsHeader *h, dd *part, dd *rank_part, cudaStream_t s);
+
+// p' (symmetric, even nx) slab solve on the fused TMA row-warp kernels of the
+// single-GPU path (stencil_tma.cu, slab mode).  Every vector lives in an
+// EXTENDED slab of npl + 2 planes: local plane 0 = global k0 - 1 and plane
+// npl + 1 = global k1 hold the neighbours' ghost copies (zero beyond the
+// domain ends, which is the boundary rule of §3.2).  K1 recomputes p on the
+// ghost planes from the ghost r, p_old, v_old (and stores it, so p_old's
+// ghosts stay current without an exchange); K2 recomputes s there from the
+// ghost r, v.  So per iteration only v (after K1) and r (after K3) cross to
+// the neighbours, next to the three all-gathers of dot partials:
+//   K1 | allgather <r^,v>, halo(v) | fold: alpha
+//   K2 | allgather <t,s>,<t,t>,<s,s> | fold: omega
+//   K3 | allgather <r^,r>,<r,r>, halo(r) | fold: rho, stop test
+static mfx_status dist_solve_tma(mfx_ctx *ctx, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol,
+                                 int maxit, mfx_solve_info *info, cudaStream_t s)
+{
+    const int R = ctx_nranks(ctx), rank = ctx_rank(ctx);
+    int k0, k1;
+    dist_slab(grid->nz, rank, R, &k0, &k1);
+    const int npl = k1 - k0, ne = npl + 2;
+    const long long plane = (long long)grid->nx * grid->ny;
+    DSlab D;
+    D.nx = grid->nx; D.ny = grid->ny; D.nz = grid->nz; D.k0 = k0; D.npl = npl;
+    D.plane = plane;
+    D.nloc = plane * npl;
+    auto r256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t hdr = r256(sizeof(WsHeader)), partb = r256(sizeof(dd) * kMaxBlocks * kMaxDots);
+    const size_t rpb = r256(sizeof(dd) * 4), apb = r256(sizeof(dd) * 4 * 64);
+    const size_t eb = r256(sizeof(double) * (size_t)(plane * ne));
+    constexpr int NV = 12;   // r rh p0 p1 v0 v1 t | x b | cx cy cz
+    const size_t total = hdr + partb + rpb + apb + NV * eb;
+    char *w = (char *)ctx_dist_scratch(ctx, total);
+    if (!w) return MFX_ERR_CUDA;
+    WsHeader *h = (WsHeader *)w;
+    dd *part = (dd *)(w + hdr);
+    dd *rank_part = (dd *)(w + hdr + partb);
+    dd *all = (dd *)(w + hdr + partb + rpb);
+    char *vb = w + hdr + partb + rpb + apb;
+    auto E = [&](int q) { return (double *)(vb + (size_t)q * eb); };
+    double *r = E(0), *rh = E(1), *P[2] = {E(2), E(3)}, *V[2] = {E(4), E(5)}, *t = E(6);
+    double *xe = E(7), *be = E(8), *cxe = E(9), *cye = E(10), *cze = E(11);
+    const size_t slab_b = sizeof(double) * (size_t)D.nloc;
+    MFX_CUDA_TRY(cudaMemsetAsync(w, 0, hdr, s));
+    MFX_CUDA_TRY(cudaMemsetAsync(vb, 0, NV * eb, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(xe + plane, x, slab_b, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(be + plane, A->b, slab_b, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(cxe + plane, A->aE, slab_b, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(cye + plane, A->aN, slab_b, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(cze + plane, A->aT, slab_b, cudaMemcpyDeviceToDevice, s));
+    mfx_grid ge = *grid;
+    ge.nz = ne;
+    const Geo G = make_geo(ge);
+    mfx_eqsys Ae;
+    memset(&Ae, 0, sizeof(Ae));
+    Ae.aE = cxe; Ae.aN = cye; Ae.aT = cze; Ae.b = be;
+    mfx_status st;
+#define XCHG(vecp) do { if ((st = ctx_halo_exchange(ctx, (vecp) + plane, npl, plane, (vecp), (vecp) + (size_t)(npl + 1) * plane, s)) != MFX_OK) return st; } while (0)
+#define GATHER(K) do { if ((st = ctx_allgather_dd(ctx, rank_part, K, all, s)) != MFX_OK) return st; } while (0)
+#define TRY(expr) do { if ((st = (expr)) != MFX_OK) return st; } while (0)
+    XCHG(cze);   // c_z of plane k0 - 1: the B coefficient of the first own plane
+    XCHG(xe);
+    {
+        const double *h0[3] = {xe, nullptr, nullptr};
+        TRY(stencil_launch(1, true, G, h0, &Ae, be, r, nullptr, nullptr, h, part, tol, maxit, s, 0, 1, npl + 1, 0,
+                           rank_part));
+    }
+    GATHER(2);
+    dk_fold_setup<<<1, 32, 0, s>>>(h, all, R, tol, maxit);
+    dk_zero_if<<<dgrid(D.nloc), kT, 0, s>>>(D, h, xe + plane);
+    MFX_CUDA_TRY(cudaGetLastError());
+    XCHG(r);
+    launch_count_add(3);
+    static thread_local SolverScalars *pin = nullptr;
+    if (!pin) MFX_CUDA_TRY(cudaMallocHost(&pin, sizeof(SolverScalars)));
+    int launched = 0, chunk = 4;
+    while (launched < maxit) {
+        const int cnt = maxit - launched < chunk ? maxit - launched : chunk;
+        for (int q = 0; q < cnt; q++, launched++) {
+            const int par = launched & 1;
+            double *p_old = P[par], *p_new = P[par ^ 1], *v_old = V[par], *v_new = V[par ^ 1];
+            const double *h1[3] = {r, p_old, v_old};
+            TRY(stencil_launch(2, true, G, h1, &Ae, rh, p_new, v_new, rh, h, part, 0.0, 0, s, 0, 1, npl + 1, 1,
+                               rank_part));
+            GATHER(1);
+            XCHG(v_new);
+            dk_fold_sigma<<<1, 32, 0, s>>>(h, all, R);
+            const double *h2[3] = {r, v_new, nullptr};
+            TRY(stencil_launch(3, true, G, h2, &Ae, nullptr, t, nullptr, nullptr, h, part, 0.0, 0, s, 0, 1, npl + 1,
+                               0, rank_part));
+            GATHER(3);
+            dk_fold_t<<<1, 32, 0, s>>>(h, all, R);
+            TRY(k3_slab_launch(D.nloc, xe + plane, r + plane, rh + plane, p_new + plane, v_new + plane, t + plane, h,
+                               part, rank_part, s));
+            GATHER(2);
+            XCHG(r);
+            dk_fold_r<<<1, 32, 0, s>>>(h, all, R);
+            launch_count_add(6);
+        }
+        MFX_CUDA_TRY(cudaGetLastError());
+        MFX_CUDA_TRY(cudaMemcpyAsync(pin, &h->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+        MFX_CUDA_TRY(cudaStreamSynchronize(s));
+        if (pin->done) break;
+        chunk = chunk * 2 > 64 ? 64 : chunk * 2;
+    }
+#undef XCHG
+#undef GATHER
+#undef TRY
+    MFX_CUDA_TRY(cudaMemcpyAsync(x, xe + plane, slab_b, cudaMemcpyDeviceToDevice, s));
+    MFX_CUDA_TRY(cudaMemcpyAsync(pin, &h->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
+    MFX_CUDA_TRY(cudaStreamSynchronize(s));
+    if (info) {
+        info->iters = pin->it;
+        info->status = pin->status;
+        info->restarts = pin->restarts;
+        info->rel_resid = pin->bn == 0.0 ? 0.0 : pin->rn / pin->bn;
+        info->true_rel_resid = -1.0;
+    }
+    return (mfx_status)pin->status;
+}
+
 mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eqsys *A, double *x, double tol,
                       int maxit, mfx_solve_info *info, cudaStream_t s)
 {
+    if (kind == MFX_EQ_PP && grid->nx % 2 == 0 && opt_solver_path() != 3 && A->aE && A->aN && A->aT && A->b &&
+        !A->aW && !A->aS && !A->aB && grid->nz >= ctx_nranks(ctx) && !((uintptr_t)x & 15))
+        return dist_solve_tma(ctx, grid, A, x, tol, maxit, info, s);
     MFX_ARG_CHECK(ctx && grid && A && x, "NULL argument");
     const bool sym = kind == MFX_EQ_PP;
     MFX_ARG_CHECK(A->aE && A->aN && A->aT && A->b && (sym ? (!A->aW && !A->aS && !A->aB)

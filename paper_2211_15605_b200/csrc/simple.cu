@@ -58,17 +58,19 @@ mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
     MFX_ARG_CHECK(*c == '[', "assignment '%s': expected '['", text);
     c++;
     int np = 0;
-    bool in_order = true;
+    for (int q = 0; q < 9; q++) a.p_rank[q] = -1;
     while (*c && *c != ']') {
+        MFX_ARG_CHECK(np < 9, "assignment '%s': P list longer than 9", text);
         MFX_ARG_CHECK(digit(id), "assignment '%s': bad P list", text);
+        for (int q = 0; q < np; q++)
+            MFX_ARG_CHECK(a.p_rank[q] != id - 1, "assignment '%s': device %d twice in the P list", text, id);
         if (np == 0) a.owner[3] = id - 1;
-        if (id != np + 1) in_order = false;
-        np++;
+        a.p_rank[np++] = id - 1;
     }
     MFX_ARG_CHECK(*c == ']' && np >= 1, "assignment '%s': expected non-empty [P] list", text);
-    MFX_ARG_CHECK(np == 1 || (in_order && np == nranks),
-                  "assignment '%s': a multi-GPU pressure list must name every rank in order ([12..%d])", text,
-                  nranks);
+    for (int q = 0; q < np; q++)
+        MFX_ARG_CHECK(a.p_rank[q] < nranks, "assignment '%s': device id %d exceeds %d ranks (S:448)", text,
+                      a.p_rank[q] + 1, nranks);
     a.n_p = np;
     c++;
     while (*c) {
@@ -82,6 +84,8 @@ mfx_status parse_assignment(const char *text, int nranks, mfx_assignment *out)
                       a.owner[q] + 1, nranks);
         if (a.owner[q] + 1 > a.n_ranks_used) a.n_ranks_used = a.owner[q] + 1;
     }
+    for (int q = 0; q < a.n_p; q++)
+        if (a.p_rank[q] + 1 > a.n_ranks_used) a.n_ranks_used = a.p_rank[q] + 1;
     *out = a;
     return MFX_OK;
 }
@@ -101,12 +105,12 @@ mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer 
     MFX_ARG_CHECK(phase >= 0 && phase <= 3, "phase must be 0 (GATHER), 1 (BCAST), 2 (PSLAB) or 3 (PIC)");
     std::vector<mfx_xfer> v;
     const int P = a->owner[3];
-    const bool multi_p = a->n_p > 1;   // every rank is a p' rank
+    const bool multi_p = a->n_p > 1;   // the P-list ranks solve p' together
     if (phase == 0) {
         for (int c = 0; c < 3; c++) {
             const int o = a->owner[c];
             for (int dst = 0; dst < (multi_p ? a->n_p : 1); dst++) {
-                const int pr = multi_p ? dst : P;
+                const int pr = multi_p ? a->p_rank[dst] : P;
                 if (pr == o) continue;
                 if (rank == o) {
                     v.push_back({MFX_OP_SEND, pr, MFX_BUF_U + c, 0, 0, 0, 0});
@@ -134,11 +138,11 @@ mfx_status exchange_plan(const mfx_assignment *a, int rank, int phase, mfx_xfer 
         for (int b = MFX_BUF_BETA; b <= MFX_BUF_SBW; b++) v.push_back({MFX_OP_BCAST, 0, b, 0, 0, 0, 0});
         v.push_back({MFX_OP_BCAST, 0, MFX_BUF_META, 8, 1, 0, 0});   // the PIC record (error latch)
     } else if (multi_p) {
-        // PSLAB: the slabs of the domain-decomposed p' solution -> P0 (= rank 0)
-        for (int q = 0; q < a->n_p; q++) {
-            if (q == P) continue;
+        // PSLAB: slab i of the domain-decomposed p' solution (on p_rank[i]) -> P0 = p_rank[0]
+        for (int i = 1; i < a->n_p; i++) {
+            const int q = a->p_rank[i];
             int k0, k1;
-            dist_slab(nz, q, a->n_p, &k0, &k1);
+            dist_slab(nz, i, a->n_p, &k0, &k1);
             if (rank == q) v.push_back({MFX_OP_SEND, P, MFX_BUF_PP, 0, 0, k0, k1});
             else if (rank == P) v.push_back({MFX_OP_RECV, q, MFX_BUF_PP, 0, 0, k0, k1});
         }
@@ -164,6 +168,7 @@ struct Nccl {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;
     bool load()
     {
         if (h) return true;
@@ -174,7 +179,7 @@ struct Nccl {
         if (!h) { set_error("cannot dlopen libnccl.so.2: %s", dlerror()); return false; }
 #define SYM(name) name = (decltype(name))dlsym(h, "nccl" #name); if (!name) { set_error("nccl%s missing", #name); return false; }
         SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(GroupStart) SYM(GroupEnd) SYM(Send) SYM(Recv)
-        SYM(Broadcast) SYM(AllGather) SYM(GetErrorString)
+        SYM(Broadcast) SYM(AllGather) SYM(GetErrorString) SYM(CommSplit)
 #undef SYM
         return true;
     }
@@ -286,6 +291,9 @@ struct mfx_local_group {
     long long dlen[64];       // ... and its length (planes or values)
     cudaEvent_t ready[64];
     cudaEvent_t done[64];
+    // sub-groups for a multi-GPU p' solve over a subset of the ranks (the P
+    // list, in its order), created once by the first rank that asks
+    std::vector<std::pair<std::vector<int>, mfx_local_group *>> subs;
     void barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
@@ -319,10 +327,18 @@ struct mfx_ctx {
     double *meta_host;       // pinned [9][16]
     ncclComm_t comm;
     mfx_local_group *group;  // non-NULL: in-process transport instead of NCCL
+    int prank;               // index of this rank in the P list (-1: not a p' rank)
+    ncclComm_t pcomm;        // the P-list ranks (multi-GPU p'); == comm when the list is every rank in order
+    mfx_local_group *pgroup; // ... in-process transport
+    int dist_sub;            // 1 while the distributed solver runs over the P list
     void *dist_scratch;      // distributed-solver workspace (allocated on first use)
     size_t dist_bytes;
     cudaEvent_t ev[6];
     double phase_ms[6];
+    // GATHER / BCAST run on a dedicated communication stream, ordered against
+    // the compute stream by events (fork/join); xt[] time them on that stream
+    cudaStream_t cs;
+    cudaEvent_t xfork, xjoin, xt[4];
     double *ts_save[8];       // time loop: state at the start of the step (allocated on first use)
     // particle -> fluid coupling: parcels live on the PIC device (rank 0)
     int pic_mode, pic_pending;
@@ -360,8 +376,11 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     MFX_ARG_CHECK(nranks == 1 || uid || group, "uid (NCCL) or a local group required for nranks > 1");
     MFX_ARG_CHECK(!group || group->nranks == nranks, "local group has %d ranks, expected %d",
                   group ? group->nranks : 0, nranks);
-    MFX_ARG_CHECK(a.n_p == 1 || grid->nz >= nranks, "multi-GPU p' needs nz >= ranks");
+    MFX_ARG_CHECK(a.n_p == 1 || grid->nz >= a.n_p, "multi-GPU p' needs nz >= number of p' ranks");
     mfx_ctx *c = new mfx_ctx();
+    c->prank = -1;
+    for (int q = 0; q < a.n_p; q++)
+        if (a.p_rank[q] == rank) c->prank = q;
     c->rank = rank; c->nranks = nranks; c->asg = a; c->grid = *grid; c->params = *params;
     c->N = (long long)grid->nx * grid->ny * grid->nz;
     c->comm = nullptr;
@@ -373,7 +392,7 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
     auto fail = [&](mfx_status s) { mfx_ctx_destroy(c); return s; };
     for (int q = 0; q < 8; q++) { memset(&c->sys[q], 0, sizeof(mfx_eqsys)); c->ws[q] = nullptr; }
     const int P = a.owner[3];
-    const bool multi_p = a.n_p > 1;                 // every rank solves a slab of p'
+    const bool multi_p = a.n_p > 1 && c->prank >= 0;   // this rank solves a slab of p'
     auto holds = [&](int q) { return a.owner[q] == rank || (q == 3 && multi_p); };
     for (int q = 0; q < 8; q++) {
         if (!holds(q)) continue;
@@ -437,6 +456,12 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
         if (cudaEventCreate(&c->ev[q]) != cudaSuccess) return fail(MFX_ERR_CUDA);
         c->phase_ms[q] = 0.0;
     }
+    if (cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->xfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->xjoin, cudaEventDisableTiming) != cudaSuccess)
+        return fail(MFX_ERR_CUDA);
+    for (int q = 0; q < 4; q++)
+        if (cudaEventCreate(&c->xt[q]) != cudaSuccess) return fail(MFX_ERR_CUDA);
     if (nranks > 1 && !group) {
         if (!g_nccl.load()) return fail(MFX_ERR_NCCL);
         ncclUniqueId id;
@@ -446,6 +471,34 @@ mfx_status ctx_create(const char *assignment, int rank, int nranks, const unsign
             set_error("ncclCommInitRank: %s", g_nccl.GetErrorString(r));
             c->comm = nullptr;
             return fail(MFX_ERR_NCCL);
+        }
+    }
+    // the P-list communicator of a multi-GPU p' solve (slab i on p_rank[i])
+    if (a.n_p > 1) {
+        bool every_in_order = a.n_p == nranks;
+        for (int q = 0; q < a.n_p; q++) every_in_order = every_in_order && a.p_rank[q] == q;
+        if (group) {
+            std::vector<int> key(a.p_rank, a.p_rank + a.n_p);
+            std::unique_lock<std::mutex> lk(group->mu);
+            for (auto &e : group->subs)
+                if (e.first == key) c->pgroup = e.second;
+            if (!c->pgroup) {
+                mfx_local_group *sg = nullptr;
+                if (mfx_local_group_create(a.n_p, &sg) != MFX_OK) { lk.unlock(); return fail(MFX_ERR_CUDA); }
+                group->subs.push_back({key, sg});
+                c->pgroup = sg;
+            }
+        } else if (nranks > 1) {
+            if (every_in_order) c->pcomm = c->comm;
+            else {
+                ncclResult_t r = g_nccl.CommSplit(c->comm, c->prank >= 0 ? 0 : -1 /* NCCL_SPLIT_NOCOLOR */,
+                                                  c->prank >= 0 ? c->prank : 0, &c->pcomm, nullptr);
+                if (r != ncclSuccess) {
+                    set_error("ncclCommSplit: %s", g_nccl.GetErrorString(r));
+                    c->pcomm = nullptr;
+                    return fail(MFX_ERR_NCCL);
+                }
+            }
         }
     }
     *out = c;
@@ -462,11 +515,29 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     if (st != MFX_OK) return st;
     const long long plane = (long long)c->grid.nx * c->grid.ny;
     // element offset and count of op o in its buffer
-    auto span = [&](const mfx_xfer &o, size_t &off, size_t &count) {
-        if (o.buf == MFX_BUF_META) { off = 16 * (size_t)o.slot; count = 16 * (size_t)o.nslots; }
+    size_t packed_count[64] = {0};   // > 0: op q carries the whole [u|v|w|p] block
+    auto span = [&](int q, size_t &off, size_t &count) {
+        const mfx_xfer &o = ops[q];
+        if (packed_count[q]) { off = 0; count = packed_count[q]; }
+        else if (o.buf == MFX_BUF_META) { off = 16 * (size_t)o.slot; count = 16 * (size_t)o.nslots; }
         else if (o.k1 > o.k0) { off = (size_t)(o.k0 * plane); count = (size_t)((o.k1 - o.k0) * plane); }
         else { off = 0; count = (size_t)c->N; }
     };
+    // packed BCAST (mfx_params.packed_state, identical on every rank): the four
+    // broadcasts of u, v, w, p from the p' owner become one of 4N doubles
+    bool skip[64] = {false};
+    if (phase == 1 && c->params.packed_state) {
+        auto contiguous = [&](double *const *f) {
+            return f[MFX_BUF_U] && f[MFX_BUF_V] == f[MFX_BUF_U] + c->N && f[MFX_BUF_W] == f[MFX_BUF_U] + 2 * c->N &&
+                   f[MFX_BUF_P] == f[MFX_BUF_U] + 3 * c->N;
+        };
+        MFX_ARG_CHECK(contiguous(fields), "packed_state: u, v, w, p are not one [u|v|w|p] block on rank %d", c->rank);
+        for (int q = 0; q < n; q++) {
+            if (ops[q].op != MFX_OP_BCAST || ops[q].buf < MFX_BUF_U || ops[q].buf > MFX_BUF_P) continue;
+            if (ops[q].buf == MFX_BUF_U) packed_count[q] = 4 * (size_t)c->N;
+            else skip[q] = true;
+        }
+    }
     if (c->group) {
         mfx_local_group &g = *c->group;
         for (int b = 0; b < MFX_NBUF; b++) g.fields[c->rank][b] = fields[b];
@@ -474,11 +545,14 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
         g.barrier();
         for (int q = 0; q < n; q++) {
             const mfx_xfer &o = ops[q];
-            if (o.op == MFX_OP_SEND || (o.op == MFX_OP_BCAST && o.peer == c->rank)) continue;
+            if (skip[q] || o.op == MFX_OP_SEND || (o.op == MFX_OP_BCAST && o.peer == c->rank)) continue;
             double *dst = fields[o.buf];
             const double *src = g.fields[o.peer][o.buf];
             size_t off, count;
-            span(o, off, count);
+            span(q, off, count);
+            MFX_ARG_CHECK(!packed_count[q] || (g.fields[o.peer][MFX_BUF_V] == src + c->N &&
+                                               g.fields[o.peer][MFX_BUF_P] == src + 3 * c->N),
+                          "packed_state: the root's [u|v|w|p] block is not contiguous");
             if (dst) dst += off;
             if (src) src += off;
             if (!dst || !src) {
@@ -498,9 +572,10 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     MFX_NCCL_TRY(g_nccl.GroupStart());
     for (int q = 0; q < n; q++) {
         const mfx_xfer &o = ops[q];
+        if (skip[q]) continue;
         double *buf = fields[o.buf];
         size_t off, count;
-        span(o, off, count);
+        span(q, off, count);
         if (buf) buf += off;
         if (!buf) {
             g_nccl.GroupEnd();
@@ -516,8 +591,12 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
 }
 
 // ------------------------------------------------------------------ distributed-solver transport
-int ctx_rank(const mfx_ctx *c) { return c->rank; }
-int ctx_nranks(const mfx_ctx *c) { return c->nranks; }
+// the distributed solver's group: every rank of the context (mfx_dist_solve),
+// or the P list while mfx_simple_iter runs a multi-GPU p' solve (dist_sub)
+int ctx_rank(const mfx_ctx *c) { return c->dist_sub ? c->prank : c->rank; }
+int ctx_nranks(const mfx_ctx *c) { return c->dist_sub ? c->asg.n_p : c->nranks; }
+static ncclComm_t ctx_comm(const mfx_ctx *c) { return c->dist_sub ? c->pcomm : c->comm; }
+static mfx_local_group *ctx_group(const mfx_ctx *c) { return c->dist_sub ? c->pgroup : c->group; }
 
 void *ctx_dist_scratch(mfx_ctx *c, size_t bytes)
 {
@@ -538,17 +617,18 @@ void *ctx_dist_scratch(mfx_ctx *c, size_t bytes)
 template <class Pull>
 static mfx_status local_phase(mfx_ctx *c, const void *ptr, long long len, cudaStream_t s, Pull pull)
 {
-    mfx_local_group &g = *c->group;
-    g.dptr[c->rank] = ptr;
-    g.dlen[c->rank] = len;
-    MFX_CUDA_TRY(cudaEventRecord(g.ready[c->rank], s));
+    mfx_local_group &g = *ctx_group(c);
+    const int me = ctx_rank(c);
+    g.dptr[me] = ptr;
+    g.dlen[me] = len;
+    MFX_CUDA_TRY(cudaEventRecord(g.ready[me], s));
     g.barrier();
     mfx_status st = pull(g);
     if (st != MFX_OK) return st;
-    MFX_CUDA_TRY(cudaEventRecord(g.done[c->rank], s));
+    MFX_CUDA_TRY(cudaEventRecord(g.done[me], s));
     g.barrier();
     for (int q = 0; q < g.nranks; q++)
-        if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.done[q], 0));
+        if (q != me) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.done[q], 0));
     g.barrier();
     return MFX_OK;
 }
@@ -557,9 +637,10 @@ static mfx_status local_phase(mfx_ctx *c, const void *ptr, long long len, cudaSt
 mfx_status ctx_halo_exchange(mfx_ctx *c, const double *slab, int npl, long long plane, double *hb, double *ha,
                              cudaStream_t s)
 {
-    const int r = c->rank, R = c->nranks;
+    const int r = ctx_rank(c), R = ctx_nranks(c);
     if (R == 1) return MFX_OK;
     const size_t pb = sizeof(double) * (size_t)plane;
+    ncclComm_t comm = ctx_comm(c);
     if (c->group) {
         return local_phase(c, slab, npl, s, [&](mfx_local_group &g) -> mfx_status {
             if (r > 0) {
@@ -576,12 +657,12 @@ mfx_status ctx_halo_exchange(mfx_ctx *c, const double *slab, int npl, long long 
     }
     MFX_NCCL_TRY(g_nccl.GroupStart());
     if (r > 0) {
-        MFX_NCCL_TRY(g_nccl.Send(slab, (size_t)plane, ncclDouble, r - 1, c->comm, s));
-        MFX_NCCL_TRY(g_nccl.Recv(hb, (size_t)plane, ncclDouble, r - 1, c->comm, s));
+        MFX_NCCL_TRY(g_nccl.Send(slab, (size_t)plane, ncclDouble, r - 1, comm, s));
+        MFX_NCCL_TRY(g_nccl.Recv(hb, (size_t)plane, ncclDouble, r - 1, comm, s));
     }
     if (r < R - 1) {
-        MFX_NCCL_TRY(g_nccl.Send(slab + (size_t)(npl - 1) * plane, (size_t)plane, ncclDouble, r + 1, c->comm, s));
-        MFX_NCCL_TRY(g_nccl.Recv(ha, (size_t)plane, ncclDouble, r + 1, c->comm, s));
+        MFX_NCCL_TRY(g_nccl.Send(slab + (size_t)(npl - 1) * plane, (size_t)plane, ncclDouble, r + 1, comm, s));
+        MFX_NCCL_TRY(g_nccl.Recv(ha, (size_t)plane, ncclDouble, r + 1, comm, s));
     }
     MFX_NCCL_TRY(g_nccl.GroupEnd());
     return MFX_OK;
@@ -590,7 +671,7 @@ mfx_status ctx_halo_exchange(mfx_ctx *c, const double *slab, int npl, long long 
 // all[q*K .. q*K+K) <- rank q's K double-double partials, for every rank q
 mfx_status ctx_allgather_dd(mfx_ctx *c, const dd *mine, int K, dd *all, cudaStream_t s)
 {
-    const int R = c->nranks;
+    const int R = ctx_nranks(c);
     const size_t kb = sizeof(dd) * (size_t)K;
     if (R == 1) {
         MFX_CUDA_TRY(cudaMemcpyAsync(all, mine, kb, cudaMemcpyDeviceToDevice, s));
@@ -599,13 +680,39 @@ mfx_status ctx_allgather_dd(mfx_ctx *c, const dd *mine, int K, dd *all, cudaStre
     if (c->group) {
         return local_phase(c, mine, K, s, [&](mfx_local_group &g) -> mfx_status {
             for (int q = 0; q < R; q++) {
-                if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[q], 0));
+                if (q != ctx_rank(c)) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[q], 0));
                 MFX_CUDA_TRY(cudaMemcpyAsync(all + (size_t)q * K, g.dptr[q], kb, cudaMemcpyDefault, s));
             }
             return MFX_OK;
         });
     }
-    MFX_NCCL_TRY(g_nccl.AllGather(mine, all, 2 * (size_t)K, ncclDouble, c->comm, s));
+    MFX_NCCL_TRY(g_nccl.AllGather(mine, all, 2 * (size_t)K, ncclDouble, ctx_comm(c), s));
+    return MFX_OK;
+}
+
+// exchange phase on the communication stream: fork from s, time it with
+// (t0, t1) on cs, and join back into s at the caller's chosen point
+static mfx_status exchange_fork(mfx_ctx *c, int phase, double *const fields[MFX_NBUF], cudaStream_t s,
+                                cudaEvent_t t0, cudaEvent_t t1)
+{
+    if (c->nranks == 1) {
+        MFX_CUDA_TRY(cudaEventRecord(t0, s));
+        MFX_CUDA_TRY(cudaEventRecord(t1, s));
+        return MFX_OK;
+    }
+    MFX_CUDA_TRY(cudaEventRecord(c->xfork, s));
+    MFX_CUDA_TRY(cudaStreamWaitEvent(c->cs, c->xfork, 0));
+    MFX_CUDA_TRY(cudaEventRecord(t0, c->cs));
+    mfx_status rc = exchange_state(c, phase, fields, c->cs);
+    if (rc != MFX_OK) return rc;
+    MFX_CUDA_TRY(cudaEventRecord(t1, c->cs));
+    return MFX_OK;
+}
+static mfx_status exchange_join(mfx_ctx *c, cudaStream_t s)
+{
+    if (c->nranks == 1) return MFX_OK;
+    MFX_CUDA_TRY(cudaEventRecord(c->xjoin, c->cs));
+    MFX_CUDA_TRY(cudaStreamWaitEvent(s, c->xjoin, 0));
     return MFX_OK;
 }
 
@@ -632,7 +739,8 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         double *D[MFX_NBUF] = {0};
         D[MFX_BUF_BETA] = st->beta; D[MFX_BUF_SBU] = st->sbeta_u;
         D[MFX_BUF_SBV] = st->sbeta_v; D[MFX_BUF_SBW] = st->sbeta_w;
-        if ((rc = exchange_state(c, 3, D, s)) != MFX_OK) return rc;
+        if ((rc = exchange_fork(c, 3, D, s, c->xt[0], c->xt[1])) != MFX_OK) return rc;
+        if ((rc = exchange_join(c, s)) != MFX_OK) return rc;
         c->pic_pending = 0;
     }
     // momentum predictors (snapshot) on their owners
@@ -648,6 +756,13 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
         k_meta<<<1, 32, 0, s>>>((WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
     }
+    // GATHER (u*, d -> the p' owner) on the communication stream, overlapping
+    // the scalar equations below (they read only the snapshot)
+    double *F[MFX_NBUF] = {0};
+    F[MFX_BUF_U] = c->star[0]; F[MFX_BUF_V] = c->star[1]; F[MFX_BUF_W] = c->star[2];
+    F[MFX_BUF_DX] = c->dv[0]; F[MFX_BUF_DY] = c->dv[1]; F[MFX_BUF_DZ] = c->dv[2];
+    F[MFX_BUF_META] = c->meta;
+    if ((rc = exchange_fork(c, 0, F, s, c->xt[0], c->xt[1])) != MFX_OK) return rc;
     // scalars (same snapshot, Q22)
     for (int sc = 0; sc < a.n_scalars; sc++) {
         const int q = 4 + sc;
@@ -662,42 +777,46 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         k_meta<<<1, 32, 0, s>>>((WsHeader *)c->ws[q], c->resid2 + 2 * q, c->meta + 16 * q, 1);
     }
     MFX_CUDA_TRY(cudaEventRecord(c->ev[1], s));
-    double *F[MFX_NBUF] = {0};
-    F[MFX_BUF_U] = c->star[0]; F[MFX_BUF_V] = c->star[1]; F[MFX_BUF_W] = c->star[2];
-    F[MFX_BUF_DX] = c->dv[0]; F[MFX_BUF_DY] = c->dv[1]; F[MFX_BUF_DZ] = c->dv[2];
-    F[MFX_BUF_META] = c->meta;
-    if ((rc = exchange_state(c, 0, F, s)) != MFX_OK) return rc;
+    if ((rc = exchange_join(c, s)) != MFX_OK) return rc;
     MFX_CUDA_TRY(cudaEventRecord(c->ev[2], s));
     if (a.n_p > 1) {
-        // multi-GPU pressure correction: every rank assembles p'
-        // (cheap, from the gathered u*, d), solves its z-slab with the
-        // domain-decomposed BiCGSTAB, and the slabs are gathered to P0.
+        // multi-GPU pressure correction: every rank of the P list
+        // assembles p' (cheap, from the gathered u*, d), solves its z-slab with
+        // the domain-decomposed BiCGSTAB over the P list, and the slabs are
+        // gathered to P0 = p_rank[0]
         const double *star6[6] = {c->star[0], c->star[1], c->star[2], c->dv[0], c->dv[1], c->dv[2]};
-        if ((rc = assemble_eq(MFX_EQ_PP, 0, &c->grid, &pr, st, star6, &c->sys[3], c->resid2 + 6, c->ws[3],
-                              c->ws_bytes, s)) != MFX_OK) return rc;
-        MFX_CUDA_TRY(cudaMemsetAsync(c->pp, 0, vbytes, s));
-        int k0, k1;
-        dist_slab(c->grid.nz, r, c->nranks, &k0, &k1);
-        const size_t off = (size_t)k0 * c->grid.nx * c->grid.ny;
-        mfx_eqsys sl;
-        memset(&sl, 0, sizeof(sl));
-        sl.aP = c->sys[3].aP + off; sl.aE = c->sys[3].aE + off; sl.aN = c->sys[3].aN + off;
-        sl.aT = c->sys[3].aT + off; sl.b = c->sys[3].b + off;
-        mfx_solve_info info;
-        rc = dist_solve(c, MFX_EQ_PP, &c->grid, &sl, c->pp + off, pr.lin_tol_pp, pr.lin_maxit_pp, &info, s);
-        if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
-        double *Fp[MFX_NBUF] = {0};
-        Fp[MFX_BUF_PP] = c->pp;
-        if ((rc = exchange_state(c, 2, Fp, s)) != MFX_OK) return rc;
-        // P0 holds the whole p' now: its true residual over the full system
-        WsView W3;
-        ws_view(c->ws[3], c->ws_bytes, c->N, false, W3);
-        if (r == P) {
-            const Geo G = make_geo(c->grid);
-            if ((rc = true_resid_launch(true, G, &c->sys[3], c->pp, W3.hdr, W3.part, s)) != MFX_OK) return rc;
+        if (c->prank >= 0) {
+            if ((rc = assemble_eq(MFX_EQ_PP, 0, &c->grid, &pr, st, star6, &c->sys[3], c->resid2 + 6, c->ws[3],
+                                  c->ws_bytes, s)) != MFX_OK) return rc;
+            MFX_CUDA_TRY(cudaMemsetAsync(c->pp, 0, vbytes, s));
+            int k0, k1;
+            dist_slab(c->grid.nz, c->prank, a.n_p, &k0, &k1);
+            const size_t off = (size_t)k0 * c->grid.nx * c->grid.ny;
+            mfx_eqsys sl;
+            memset(&sl, 0, sizeof(sl));
+            sl.aP = c->sys[3].aP + off; sl.aE = c->sys[3].aE + off; sl.aN = c->sys[3].aN + off;
+            sl.aT = c->sys[3].aT + off; sl.b = c->sys[3].b + off;
+            mfx_solve_info info;
+            c->dist_sub = 1;
+            rc = dist_solve(c, MFX_EQ_PP, &c->grid, &sl, c->pp + off, pr.lin_tol_pp, pr.lin_maxit_pp, &info, s);
+            c->dist_sub = 0;
+            if (rc < 0 && rc != MFX_ERR_BREAKDOWN) return rc;
+            // P0 holds the whole p' after PSLAB: its true residual over the full system
+            WsView W3;
+            ws_view(c->ws[3], c->ws_bytes, c->N, false, W3);
+            double *Fp[MFX_NBUF] = {0};
+            Fp[MFX_BUF_PP] = c->pp;
+            if ((rc = exchange_state(c, 2, Fp, s)) != MFX_OK) return rc;
+            if (r == P) {
+                const Geo G = make_geo(c->grid);
+                if ((rc = true_resid_launch(true, G, &c->sys[3], c->pp, W3.hdr, W3.part, s)) != MFX_OK) return rc;
+            }
+            k_meta_vals<<<1, 32, 0, s>>>(c->resid2 + 6, c->meta + 48, info.iters, info.status, info.restarts,
+                                         info.rel_resid, W3.hdr);
+        } else {
+            double *Fp[MFX_NBUF] = {0};
+            if ((rc = exchange_state(c, 2, Fp, s)) != MFX_OK) return rc;   // no ops; keeps the phase collective
         }
-        k_meta_vals<<<1, 32, 0, s>>>(c->resid2 + 6, c->meta + 48, info.iters, info.status, info.restarts,
-                                     info.rel_resid, W3.hdr);
         MFX_CUDA_TRY(cudaEventRecord(c->ev[3], s));
         if (r == P && (rc = correct(&c->grid, &pr, star6, c->pp, st->p, st->u, st->v, st->w, st->p, s)) != MFX_OK)
             return rc;
@@ -724,17 +843,19 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
     B[MFX_BUF_U] = st->u; B[MFX_BUF_V] = st->v; B[MFX_BUF_W] = st->w; B[MFX_BUF_P] = st->p;
     for (int sc = 0; sc < a.n_scalars; sc++) B[MFX_BUF_PHI0 + sc] = st->phi[sc];
     B[MFX_BUF_META] = c->meta;
-    if ((rc = exchange_state(c, 1, B, s)) != MFX_OK) return rc;
+    if ((rc = exchange_fork(c, 1, B, s, c->xt[2], c->xt[3])) != MFX_OK) return rc;
+    if ((rc = exchange_join(c, s)) != MFX_OK) return rc;
     MFX_CUDA_TRY(cudaEventRecord(c->ev[5], s));
     MFX_CUDA_TRY(cudaMemcpyAsync(c->meta_host, c->meta, kMetaBytes, cudaMemcpyDeviceToHost, s));
     MFX_CUDA_TRY(cudaStreamSynchronize(s));
     float ms;
-    // [0] momentum+scalars, [1] GATHER, [2] p' assemble+solve, [3] correction, [4] BCAST, [5] total
+    // [0] momentum+scalars, [1] GATHER (comm stream, overlaps the scalars), [2] p' assemble+solve,
+    // [3] correction, [4] BCAST (comm stream), [5] total
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); c->phase_ms[0] = ms;
-    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); c->phase_ms[1] = ms;
+    cudaEventElapsedTime(&ms, c->xt[0], c->xt[1]); c->phase_ms[1] = ms;
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); c->phase_ms[2] = ms;
     cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); c->phase_ms[3] = ms;
-    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]); c->phase_ms[4] = ms;
+    cudaEventElapsedTime(&ms, c->xt[2], c->xt[3]); c->phase_ms[4] = ms;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]); c->phase_ms[5] = ms;
     const double *m = c->meta_host;
     auto R = [&](int q) { const double den = m[16 * q + 1]; return m[16 * q] / (den > 1e-30 ? den : 1e-30); };
@@ -793,6 +914,7 @@ mfx_status mfx_local_group_create(int nranks, mfx_local_group **out)
 void mfx_local_group_destroy(mfx_local_group *g)
 {
     if (!g) return;
+    for (auto &e : g->subs) mfx_local_group_destroy(e.second);
     for (int q = 0; q < g->nranks; q++) {
         cudaEventDestroy(g->ready[q]);
         cudaEventDestroy(g->done[q]);
@@ -812,12 +934,18 @@ void mfx_ctx_destroy(mfx_ctx *c)
     if (!c) return;
     for (int q = 0; q < 8; q++)
         if (c->ws[q]) mfx::graph_cache_evict(c->ws[q]);   // graphs captured on this context's workspaces
+    if (c->pcomm && c->pcomm != c->comm && mfx::g_nccl.CommDestroy) mfx::g_nccl.CommDestroy(c->pcomm);
     if (c->comm && mfx::g_nccl.CommDestroy) mfx::g_nccl.CommDestroy(c->comm);
     for (void *p : c->allocs) cudaFree(p);
     if (c->dist_scratch) cudaFree(c->dist_scratch);
     if (c->meta_host) cudaFreeHost(c->meta_host);
     for (int q = 0; q < 6; q++)
         if (c->ev[q]) cudaEventDestroy(c->ev[q]);
+    for (int q = 0; q < 4; q++)
+        if (c->xt[q]) cudaEventDestroy(c->xt[q]);
+    if (c->xfork) cudaEventDestroy(c->xfork);
+    if (c->xjoin) cudaEventDestroy(c->xjoin);
+    if (c->cs) cudaStreamDestroy(c->cs);
     delete c;
 }
 

@@ -52,6 +52,13 @@ struct StencilArgs {
     dd *part;
     double tol;
     int maxit;
+    // z-slab mode (dist_solver.cu): outputs planes [kbeg, kend) of an extended
+    // slab whose planes kbeg-1 and kend hold the neighbours' ghost copies; the
+    // rank's dot partials go to rank_part (folded across ranks by the caller)
+    // instead of the scalar tail; K1 with ghost_store also writes p on the two
+    // ghost planes (the next iteration's p_old there, bitwise the neighbour's).
+    int kbeg, kend, ghost_store;
+    dd *rank_part;
 };
 
 namespace {
@@ -105,7 +112,7 @@ __host__ __device__ constexpr size_t smem_bytes(int S)
 // (virtual, i.e. zero, outside [0, nz)) and outputs planes k0 .. k1-1.
 struct Cursor {
     int u, units;
-    int G, ntiles, Lz, tiles_x, TX, TY, rev;
+    int G, ntiles, Lz, tiles_x, TX, TY, rev, kbeg, kend;
     int x0, y0, k, k0, k1;
     bool valid;
     __device__ void start(int nz)
@@ -117,15 +124,16 @@ struct Cursor {
         const int ty = tile / tiles_x;
         x0 = (tile - ty * tiles_x) * TX;
         y0 = ty * TY;
-        k0 = chunk * Lz;
-        k1 = k0 + Lz < nz ? k0 + Lz : nz;
+        k0 = kbeg + chunk * Lz;
+        k1 = k0 + Lz < kend ? k0 + Lz : kend;
         k = k0 - 1;
         valid = true;
     }
-    __device__ void init(int u0, int nunits, int g, int nt, int lz, int tx, int tX, int tY, int nz, int rv)
+    __device__ void init(int u0, const StencilArgs &a, int nt, int tX, int tY)
     {
-        u = u0; units = nunits; G = g; ntiles = nt; Lz = lz; tiles_x = tx; TX = tX; TY = tY; rev = rv;
-        start(nz);
+        u = u0; units = (int)a.units; G = gridDim.x; ntiles = nt; Lz = a.Lz; tiles_x = a.tiles_x; TX = tX; TY = tY;
+        rev = a.reverse; kbeg = a.kbeg; kend = a.kend;
+        start(a.nz);
     }
     __device__ void advance(int nz)
     {
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 #pragma unroll
             for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
             Cursor prod;
-            prod.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
+            prod.init(blockIdx.x, a, ntiles, TX, TY);
             for (int q = 0; prod.valid; q++) {
                 if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
                 issue<MODE, SYM, TX, TY, CPT_, S>(M, prod, a.nz, stages, full, q);
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
         constexpr int CPT = C::CPT;
         constexpr int RW = TX / CPT;                 // threads per tile row
         Cursor cons;
-        cons.init(blockIdx.x, (int)a.units, gridDim.x, ntiles, a.Lz, a.tiles_x, TX, TY, a.nz, a.reverse);
+        cons.init(blockIdx.x, a, ntiles, TX, TY);
         double czq1[CPT], czq0[CPT];                 // cz at planes q-1 (aT of output) and q-2 (aB)
 #pragma unroll
         for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
@@ -487,6 +495,291 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
         }
         if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+        if (a.rank_part) {
+#pragma unroll
+            for (int d = 0; d < ND; d++) a.rank_part[d] = out[d];
+            return;
+        }
+        SolverScalars &Sc = a.h->sc;
+        if (MODE == SM_SETUP) bicg_setup(Sc, dd_round(out[0]), dd_round(out[1]), a.tol, a.maxit);
+        else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
+        else if (MODE == SM_K2) bicg_k2_tail(Sc, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
+    }
+}
+
+// ------------------------------------------------------------------ row-warp kernels
+// Symmetric (p') systems, DESIGN.md §7 "row-warp": the tile is (32 CPT) x 8
+// cells and consumer warp w owns tile row w (lane l: cells 2l, 2l+1 for
+// CPT = 2).  Everything step 2 needs from the halo'd plane -- the value
+// (x | p | s) on rows y-1, y, y+1 and the two x-edge cells -- the warp
+// computes itself from the staged halo arrays; W/E neighbours inside the row
+// travel by shuffles and z neighbours stay in registers (planes q-2, q-1, q).
+// Warps therefore never wait on each other (no P ring, no per-plane named
+// barrier) and a warp hands its stage back as soon as its loads are in
+// registers.  The expressions and their order are those of k_stencil, so the
+// bits are the same (tested against the oracle on every p' path).
+template <int MODE, int CPT, int S>
+__global__ void __launch_bounds__(8 * 32 + 32) k_stencil_rw(const __grid_constant__ TmaMaps M, StencilArgs a)
+{
+    constexpr int TX = 32 * CPT, TY = 8;
+    using C = Cfg<MODE, true, TX, TY, CPT>;
+    static_assert(C::NW == TY, "one consumer warp per tile row");
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *stages = smem;
+    uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B);
+    uint64_t *empty = full + S;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+
+    pdl_trigger();
+    const int ntiles = a.tiles_x * a.tiles_y;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+
+    double beta = 0.0, omega = 0.0, alpha = 0.0;
+    bool rst = false;
+    K1Pro P1;
+    P1.rst = false;
+    if (MODE == SM_K1 || MODE == SM_K2) {
+        SolverScalars &Sc = a.h->sc;
+        if (Sc.done) return;
+        if (MODE == SM_K2 && Sc.skip) return;
+        if (MODE == SM_K1) {
+            P1 = bicg_k1_prologue(Sc);
+            if (P1.breakdown) {
+                if (blockIdx.x == 0 && tid == 0) bicg_breakdown(Sc);
+                return;
+            }
+            rst = P1.rst;
+            beta = P1.beta;
+            omega = P1.omega;
+        } else {
+            alpha = Sc.alpha;
+        }
+    }
+
+    constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
+    Acc acc[ND][CPT];
+#pragma unroll
+    for (int d = 0; d < ND; d++)
+#pragma unroll
+        for (int m = 0; m < CPT; m++) acc[d][m].zero();
+
+    if (warp == C::NW) {
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
+            Cursor prod;
+            prod.init(blockIdx.x, a, ntiles, TX, TY);
+            for (int q = 0; prod.valid; q++) {
+                if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
+                issue<MODE, true, TX, TY, CPT, S>(M, prod, a.nz, stages, full, q);
+                prod.advance(a.nz);
+            }
+        }
+    } else {
+        Cursor cons;
+        cons.init(blockIdx.x, a, ntiles, TX, TY);
+        const int cx0 = lane * CPT;
+        const int hc = (warp + 1) * C::HX + cx0 + 2;                    // halo-box index of the first owned cell
+        const int he = lane == 31 ? (warp + 1) * C::HX + TX + 2          // right edge cell x0 + TX
+                                  : (warp + 1) * C::HX + 1;              // left edge cell x0 - 1 (used by lane 0)
+        const int ci = warp * TX + cx0;
+        // register pipeline: values of planes q-2 (B), q-1 (centre row + S/N rows + edge), q (T)
+        double vB[CPT], vC[CPT], vS[CPT], vN[CPT], vE = 0.0;
+        double kxw[CPT + 1], kys[CPT], kyn[CPT], kex[CPT], czp[CPT], czpp[CPT];
+#pragma unroll
+        for (int m = 0; m < CPT; m++) {
+            vB[m] = vC[m] = vS[m] = vN[m] = 0.0;
+            kys[m] = kyn[m] = kex[m] = czp[m] = czpp[m] = 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m <= CPT; m++) kxw[m] = 0.0;
+
+        // value of the step-1 field at halo index i (CPT consecutive cells from i)
+        auto value = [&](const uint8_t *st, int i, double (&out)[CPT]) {
+            const double *h0 = (const double *)(st + C::OFF_HALO);
+            const double *h1 = (const double *)(st + C::OFF_HALO + C::HALO_B);
+            const double *h2 = (const double *)(st + C::OFF_HALO + 2 * C::HALO_B);
+            double rv[CPT], pv[CPT], vv[CPT];
+            if (CPT == 2) {
+                const double2 r2 = *(const double2 *)(h0 + i);
+                rv[0] = r2.x; rv[CPT - 1] = r2.y;
+                if (MODE == SM_K1) {
+                    const double2 p2 = *(const double2 *)(h1 + i), v2 = *(const double2 *)(h2 + i);
+                    pv[0] = p2.x; pv[CPT - 1] = p2.y; vv[0] = v2.x; vv[CPT - 1] = v2.y;
+                } else if (MODE == SM_K2) {
+                    const double2 v2 = *(const double2 *)(h1 + i);
+                    vv[0] = v2.x; vv[CPT - 1] = v2.y;
+                }
+            } else {
+                rv[0] = h0[i];
+                if (MODE == SM_K1) { pv[0] = h1[i]; vv[0] = h2[i]; }
+                else if (MODE == SM_K2) vv[0] = h1[i];
+            }
+#pragma unroll
+            for (int m = 0; m < CPT; m++) {
+                if (MODE == SM_SPMV || MODE == SM_SETUP) out[m] = rv[m];
+                else if (MODE == SM_K1) out[m] = rst ? fma(beta, fma(-omega, 0.0, 0.0), rv[m])
+                                                     : fma(beta, fma(-omega, vv[m], pv[m]), rv[m]);
+                else out[m] = fma(-alpha, vv[m], rv[m]);
+            }
+        };
+        auto value1 = [&](const uint8_t *st, int i) -> double {
+            const double r = ((const double *)(st + C::OFF_HALO))[i];
+            if (MODE == SM_K1) {
+                const double p = ((const double *)(st + C::OFF_HALO + C::HALO_B))[i];
+                const double v = ((const double *)(st + C::OFF_HALO + 2 * C::HALO_B))[i];
+                return rst ? fma(beta, fma(-omega, 0.0, 0.0), r) : fma(beta, fma(-omega, v, p), r);
+            }
+            if (MODE == SM_K2) return fma(-alpha, ((const double *)(st + C::OFF_HALO + C::HALO_B))[i], r);
+            return r;
+        };
+
+        for (int q = 0; cons.valid; q++) {
+            const int s = q % S;
+            const bool virt = cons.is_virtual(a.nz);
+            const bool produce = cons.produces();
+            const int kout = cons.k - 1;
+            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+            const uint8_t *st = stages + (size_t)s * C::STAGE_B;
+            // ---- centre row of plane q (T of the output plane, B of the next)
+            double tC[CPT];
+            if (!virt) value(st, hc, tC);
+            else
+#pragma unroll
+                for (int m = 0; m < CPT; m++) tC[m] = 0.0;
+            if (MODE == SM_K1 && a.ghost_store && !virt && (cons.k == a.kbeg - 1 || cons.k == a.kend)) {
+                const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
+                if (gx < a.nx && gy < a.ny)
+                    store_cells<CPT>(a.out0 + (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * cons.k),
+                                     tC);
+            }
+            // ---- step 2: output plane q-1
+            if (produce) {
+                double xc[CPT], xW[CPT], xE[CPT], xS[CPT], xN[CPT], xB[CPT], xT[CPT];
+                const double left = __shfl_up_sync(0xffffffffu, vC[CPT - 1], 1);
+                const double right = __shfl_down_sync(0xffffffffu, vC[0], 1);
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    xc[m] = vC[m];
+                    xW[m] = m > 0 ? vC[m - 1] : (lane == 0 ? vE : left);
+                    xE[m] = m < CPT - 1 ? vC[m + 1] : (lane == 31 ? vE : right);
+                    xS[m] = vS[m]; xN[m] = vN[m]; xB[m] = vB[m]; xT[m] = tC[m];
+                }
+                double y[CPT];
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    const double aW = kxw[m], aE = kxw[m + 1], aS = kys[m], aN = kyn[m], aB = czpp[m], aT = czp[m];
+                    const double aP = ((((aW + aE) + aS) + aN) + aB) + aT;
+                    double t = aP * xc[m];
+                    t = fma(-aW, xW[m], t);
+                    t = fma(-aE, xE[m], t);
+                    t = fma(-aS, xS[m], t);
+                    t = fma(-aN, xN[m], t);
+                    t = fma(-aB, xB[m], t);
+                    t = fma(-aT, xT[m], t);
+                    y[m] = t;
+                }
+                const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
+                if (gx < a.nx && gy < a.ny) {
+                    const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
+                    if (MODE == SM_SPMV) {
+                        store_cells<CPT>(a.out0 + n, y);
+                    } else if (MODE == SM_SETUP) {
+                        double rv[CPT];
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            rv[m] = kex[m] - y[m];
+                            acc[0][m].prod(kex[m], kex[m]);
+                            acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
+                        }
+                        store_cells<CPT>(a.out0 + n, rv);
+                    } else if (MODE == SM_K1) {
+                        store_cells<CPT>(a.out0 + n, xc);
+                        store_cells<CPT>(a.out1 + n, y);
+                        if (rst) store_cells<CPT>(a.out2 + n, kex);
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) acc[0][m].prod(kex[m], y[m]);
+                    } else {
+                        store_cells<CPT>(a.out0 + n, y);
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            acc[0][m].prod(y[m], xc[m]);
+                            acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
+                            acc[ND > 2 ? 2 : 0][m].prod(xc[m], xc[m]);
+                        }
+                    }
+                }
+            }
+            // ---- the rest of plane q -> registers, then the stage goes back to the producer
+            double tS[CPT], tN[CPT], tE = 0.0;
+            double nkxw[CPT + 1], nkys[CPT], nkyn[CPT], nkex[CPT], ncz[CPT];
+            if (!virt) {
+                value(st, hc - C::HX, tS);
+                value(st, hc + C::HX, tN);
+                tE = value1(st, he);
+                const double *xw = (const double *)(st + C::OFF_XW);
+                const double *ys = (const double *)(st + C::OFF_YS);
+                const double *cz = (const double *)(st + C::OFF_CELL);
+#pragma unroll
+                for (int m = 0; m <= CPT; m++) nkxw[m] = xw[warp * C::HX + cx0 + m + 1];
+#pragma unroll
+                for (int m = 0; m < CPT; m++) {
+                    nkys[m] = ys[warp * TX + cx0 + m];
+                    nkyn[m] = ys[(warp + 1) * TX + cx0 + m];
+                    ncz[m] = cz[ci + m];
+                    if (MODE == SM_SETUP) nkex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                    else if (MODE == SM_K1)
+                        nkex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
+                                      : ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                    else nkex[m] = 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < CPT; m++) tS[m] = tN[m] = nkys[m] = nkyn[m] = nkex[m] = ncz[m] = 0.0;
+#pragma unroll
+                for (int m = 0; m <= CPT; m++) nkxw[m] = 0.0;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+
+            // ---- rotate the register pipeline
+#pragma unroll
+            for (int m = 0; m < CPT; m++) {
+                vB[m] = vC[m]; vC[m] = tC[m]; vS[m] = tS[m]; vN[m] = tN[m];
+                czpp[m] = czp[m]; czp[m] = ncz[m];
+                kys[m] = nkys[m]; kyn[m] = nkyn[m]; kex[m] = nkex[m];
+            }
+#pragma unroll
+            for (int m = 0; m <= CPT; m++) kxw[m] = nkxw[m];
+            vE = tE;
+            cons.advance(a.nz);
+        }
+    }
+
+    if constexpr (C::NDOT > 0) {
+        __shared__ dd sh[(C::NW + 1) * ND];
+        dd v[ND], out[ND];
+#pragma unroll
+        for (int d = 0; d < ND; d++) {
+            v[d] = acc[d][0].get();
+#pragma unroll
+            for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+        }
+        if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+        if (a.rank_part) {
+#pragma unroll
+            for (int d = 0; d < ND; d++) a.rank_part[d] = out[d];
+            return;
+        }
         SolverScalars &Sc = a.h->sc;
         if (MODE == SM_SETUP) bicg_setup(Sc, dd_round(out[0]), dd_round(out[1]), a.tol, a.maxit);
         else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
@@ -550,17 +843,20 @@ int choose_lz(long long ntiles, int nz, int grid)
     return best;
 }
 
-template <int MODE, bool SYM, int TX, int TY, int CPT_, int S>
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S, bool RW = false>
 struct Launcher {
     using C = Cfg<MODE, SYM, TX, TY, CPT_>;
+    static constexpr void (*kern)(const TmaMaps, StencilArgs) =
+        RW ? k_stencil_rw<MODE, CPT_, S> : k_stencil<MODE, SYM, TX, TY, CPT_, S>;
+    static constexpr size_t smem() { return RW ? (size_t)S * C::STAGE_B + 16 * (size_t)S : smem_bytes<C>(S); }
     static int grid_size()
     {
         static int g = 0;
         if (g) return g;
-        const size_t sm = smem_bytes<C>(S);
-        cudaFuncSetAttribute(k_stencil<MODE, SYM, TX, TY, CPT_, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const size_t sm = smem();
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<MODE, SYM, TX, TY, CPT_, S>, C::NT + 32, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT + 32, sm);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -589,20 +885,22 @@ struct Launcher {
         a.tiles_y = (G.ny + TY - 1) / TY;
         int grid = grid_size();
         const long long ntiles = (long long)a.tiles_x * a.tiles_y;
-        a.Lz = choose_lz(ntiles, G.nz, grid);
-        a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
+        if (a.kend <= a.kbeg) { a.kbeg = 0; a.kend = G.nz; }
+        const int nout = a.kend - a.kbeg;
+        a.Lz = choose_lz(ntiles, nout, grid);
+        a.units = ntiles * ((nout + a.Lz - 1) / a.Lz);
         if (grid > a.units) grid = (int)a.units;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(C::NT + 32);
-        cfg.dynamicSmemBytes = smem_bytes<C>(S);
+        cfg.dynamicSmemBytes = smem();
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = opt_pdl() ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil<MODE, SYM, TX, TY, CPT_, S>, M, a));
+        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, M, a));
         return MFX_OK;
     }
 };
@@ -625,11 +923,35 @@ mfx_status run_tile(const Geo &G, const double *const halo[3], const double *con
     return Launcher<MODE, SYM, TX, TY, CPT_, 4>::run(G, halo, coef, extra, a, s);
 }
 
+// row-warp kernels (SYM only): MFX_RW = bit mask over modes (1 << MODE) that use
+// them; MFX_RW_STAGES overrides their ring depth.
+template <int MODE>
+mfx_status run_rw(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
+                  const StencilArgs &a, cudaStream_t s)
+{
+    static const int st = env_int("MFX_RW_STAGES", 0);
+    const int S = st ? st : 4;
+    if (G.nx <= 32) {
+        if (S == 3) return Launcher<MODE, true, 32, 8, 1, 3, true>::run(G, halo, coef, extra, a, s);
+        return Launcher<MODE, true, 32, 8, 1, 4, true>::run(G, halo, coef, extra, a, s);
+    }
+    if (S == 3) return Launcher<MODE, true, 64, 8, 2, 3, true>::run(G, halo, coef, extra, a, s);
+    if (S == 6) return Launcher<MODE, true, 64, 8, 2, 6, true>::run(G, halo, coef, extra, a, s);
+    return Launcher<MODE, true, 64, 8, 2, 4, true>::run(G, halo, coef, extra, a, s);
+}
+
+int rw_mask()
+{
+    static const int m = env_int("MFX_RW", 0);
+    return m;
+}
+
 template <int MODE, bool SYM>
 mfx_status run_mode(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
                     const StencilArgs &a, cudaStream_t s)
 {
     // tiles: 64x4 (one cell per thread) or 64x8 / 32x16 (x-adjacent pairs)
+    if (SYM && ((rw_mask() >> MODE & 1) || a.rank_part)) return run_rw<MODE>(G, halo, coef, extra, a, s);
     static const int tile = env_int("MFX_TILE", 0);   // 1: 64x4, 2: 64x8 pairs, 3: 32x16 pairs, 4: 32x8, 5: 64x8
     int t = tile;
     // measured at c2 (profiles/r01s7_tile_sweep.log): p' K1 is fastest at 64x4,
@@ -647,7 +969,8 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
 // coefficient order for the maps: SYM -> {cz, -, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],
                           const mfx_eqsys *A, const double *extra, double *o0, double *o1, double *o2,
-                          WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s, int reverse)
+                          WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s, int reverse, int kbeg,
+                          int kend, int ghost_store, dd *rank_part)
 {
     const double *coef[7];
     if (sym) {
@@ -661,6 +984,8 @@ mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const 
     memset(&a, 0, sizeof(a));
     a.out0 = o0; a.out1 = o1; a.out2 = o2; a.h = h; a.part = part; a.tol = tol; a.maxit = maxit;
     a.reverse = reverse;
+    a.kbeg = kbeg; a.kend = kend; a.ghost_store = ghost_store; a.rank_part = rank_part;
+    MFX_ARG_CHECK(!rank_part || sym, "slab mode: symmetric systems only");
     switch (mode * 2 + (sym ? 1 : 0)) {
     case SM_SPMV * 2 + 0: return run_mode<SM_SPMV, false>(G, halo, coef, extra, a, s);
     case SM_SPMV * 2 + 1: return run_mode<SM_SPMV, true>(G, halo, coef, extra, a, s);

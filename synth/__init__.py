@@ -76,6 +76,7 @@ class Params:
     lin_maxit_pp: int = 500
     lin_maxit_phi: int = 20
     face_eps_upwind: int = 0      # DESIGN.md §3.12 (0: central face eps, reading Q9)
+    packed_state: int = 0         # multi-rank exchange layout only: u, v, w, p in one [u|v|w|p] block
 
 
 def syamlal_obrien_beta(eps, slip, d_p=200e-6, rho_g=1.0, mu_g=1.8e-5):

@@ -57,6 +57,8 @@ def test_version(mfx):
     ("111[1]1111", 1, [0, 0, 0, 0, 0, 0, 0, 0]),
     ("234[1234]", 4, [1, 2, 3, 0, -1, -1, -1, -1]),       # Fig. 2b: multi-GPU pressure
     ("222[12]1", 2, [1, 1, 1, 0, 0, -1, -1, -1]),
+    ("234[23]", 4, [1, 2, 3, 1, -1, -1, -1, -1]),         # a subset of the devices solves p'
+    ("123[31]", 3, [0, 1, 2, 2, -1, -1, -1, -1]),         # ... in any order: P0 is its first entry
 ])
 def test_parse_assignment(mfx, text, n, owner):
     a = mfx.parse_assignment(text, n)
@@ -70,8 +72,8 @@ def test_parse_assignment(mfx, text, n, owner):
     ("111", 1),
     ("111[]", 1),
     ("111[1]x", 1),
-    ("234[124]", 4),       # a multi-GPU pressure list must name every rank ...
-    ("234[2134]", 4),      # ... in order
+    ("234[122]", 4),       # a device twice in the pressure list
+    ("234[125]", 4),       # pressure-list device out of range
     ("111[1]11111", 1),    # > 4 scalars
 ])
 def test_parse_assignment_errors(mfx, text, n):
@@ -86,12 +88,14 @@ def _plan_all(mfx, text, n, nz=16):
 
 
 @pytest.mark.parametrize("text,n", [("234[1]", 4), ("222[1]", 2), ("234[1]5678", 8), ("211[2]3", 3),
-                                    ("111[1]", 1), ("111[1]", 3), ("234[1234]", 4), ("222[12]1", 2)])
+                                    ("111[1]", 1), ("111[1]", 3), ("234[1234]", 4), ("222[12]1", 2),
+                                    ("234[23]", 4), ("234[413]", 4), ("235[35]1", 5)])
 def test_exchange_plan_consistency(mfx, text, n):
     plans = _plan_all(mfx, text, n)
     a = mfx.parse_assignment(text, n)
     P = a["owner"][3]
-    prs = list(range(n)) if a["n_p"] > 1 else [P]
+    prs = a["p_rank"] if a["n_p"] > 1 else [P]
+    assert prs[0] == P
     # GATHER: every send has exactly one matching recv on the peer, same buffer
     sends = [(r, o["peer"], o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_SEND]
     recvs = [(o["peer"], r, o["buf"], o["slot"]) for r, (g, _) in plans.items() for o in g if o["op"] == mfx.OP_RECV]
@@ -106,7 +110,14 @@ def test_exchange_plan_consistency(mfx, text, n):
     if a["n_p"] > 1:
         slabs = sorted((o["k0"], o["k1"]) for r in range(n) for o in mfx.exchange_plan(text, n, r, 2, 16)
                        if o["op"] == mfx.OP_RECV)
-        own = mfx.dist_slab(16, P, n)
+        sends = {r: [o for o in mfx.exchange_plan(text, n, r, 2, 16) if o["op"] == mfx.OP_SEND] for r in range(n)}
+        for r in range(n):   # slab i travels from p_rank[i]; ranks outside the list have no PSLAB ops
+            if r in prs[1:]:
+                i = prs.index(r)
+                assert [(o["k0"], o["k1"]) for o in sends[r]] == [mfx.dist_slab(16, i, a["n_p"])]
+            else:
+                assert not sends[r]
+        own = mfx.dist_slab(16, 0, a["n_p"])
         cover = sorted(slabs + [own])
         assert cover[0][0] == 0 and cover[-1][1] == 16
         assert all(cover[i][1] == cover[i + 1][0] for i in range(len(cover) - 1))

@@ -102,10 +102,11 @@ def decomposed_iter(rank, world, assignment, g, pr, st):
         dv = [bufs["dx"], bufs["dy"], bufs["dz"]]
         s, cont, rc = oracle.assemble_pp(g, pr, st, star, dv)
         res = oracle.bicgstab(g, s, np.zeros(n), pr.lin_tol_pp, pr.lin_maxit_pp)
-        k0, k1 = mfx.dist_slab(g.nz, rank, world)
         plane = g.nx * g.ny
         ppf = {"pp": np.zeros(n)}
-        ppf["pp"][k0 * plane:k1 * plane] = res["x"][k0 * plane:k1 * plane]
+        if rank in a["p_rank"]:   # slab i of the P list
+            k0, k1 = mfx.dist_slab(g.nz, a["p_rank"].index(rank), a["n_p"])
+            ppf["pp"][k0 * plane:k1 * plane] = res["x"][k0 * plane:k1 * plane]
         run(2, ppf)
         meta[3, :4] = (cont, 0.0, res["iters"], res["status"])
         if rank == P:
@@ -139,7 +140,7 @@ def worker(rank, world, port, assignment, n_scalars, q):
 
 
 @pytest.mark.parametrize("assignment,n_scalars", [("222[1]", 0), ("121[2]", 0), ("211[1]2", 1), ("112[2]12", 2),
-                                                   ("212[12]", 0), ("122[12]2", 1)])
+                                                   ("212[12]", 0), ("122[12]2", 1), ("122[21]", 0)])
 def test_two_rank_decomposition_bitwise(orc, mfx_built, assignment, n_scalars):
     world = 2
     ctx = mp.get_context("spawn")

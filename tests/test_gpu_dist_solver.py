@@ -104,3 +104,32 @@ def test_dist_pp_tall_many_ranks_not_converged(mfx, orc):
     x, info = dist_run(mfx, g, pr, mfx.EQ_PP, sysd, np.zeros(g.n), 1e-14, 37, 6)
     assert ref["status"] == 1 and info["status"] == 1 and info["iters"] == 37
     assert np.array_equal(x, ref["x"])
+
+
+@pytest.mark.parametrize("R", [1, 3])
+def test_dist_pp_tma_ragged_tiles_equals_oracle(mfx, orc, R):
+    """p' on the TMA row-warp slab kernels (nx > 64, ragged x and y tiles, uneven
+    slabs): every iterate path -- ghost-plane recompute of p and s, the v and r
+    halos, the rank-ordered dd fold -- must reproduce the oracle bitwise."""
+    g = synth.make_grid(70, 36, 50)
+    pr = synth.Params()
+    st = synth.make_state(g, 47, pr)
+    sysd = pp_system(orc, g, pr, st, seed=5)
+    ref = orc.bicgstab(g, sysd, np.zeros(g.n), 1e-9, 120)
+    x, info = dist_run(mfx, g, pr, mfx.EQ_PP, sysd, np.zeros(g.n), 1e-9, 120, R)
+    assert info["iters"] == ref["iters"] and info["status"] == ref["status"]
+    assert np.array_equal(x, ref["x"])
+
+
+def test_dist_pp_tma_nonzero_guess_uneven_slabs(mfx, orc):
+    """A nonzero initial guess and a tolerance that needs many iterations on 4
+    uneven slabs (nz = 23): bitwise against the oracle, status included."""
+    g = synth.make_grid(16, 14, 23)
+    pr = synth.Params()
+    st = synth.make_state(g, 53, pr)
+    sysd = pp_system(orc, g, pr, st, seed=9)
+    x0 = np.random.default_rng(2).normal(0.0, 1e-3, g.n)
+    ref = orc.bicgstab(g, sysd, x0, 1e-12, 400)
+    x, info = dist_run(mfx, g, pr, mfx.EQ_PP, sysd, x0, 1e-12, 400, 4)
+    assert info["iters"] == ref["iters"] and info["status"] == ref["status"]
+    assert np.array_equal(x, ref["x"])

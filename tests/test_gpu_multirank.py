@@ -73,6 +73,8 @@ def run_ranks(mfx, assignment, nranks, g, pr, st, outer=2):
     ("234[1234]", 4, 0),          # Fig. 2b: multi-GPU pressure solve
     ("212[12]1", 2, 1),
     ("234[12345678]5678", 8, 4),  # p' over all 8 ranks + 4 scalars
+    ("234[23]", 4, 0),            # p' over a subset of the devices ("a set of devices")
+    ("123[32]1", 3, 1),           # ... listed out of order: P0 = rank 2, slab 1 on rank 1
 ])
 def test_multirank_equals_single_rank(mfx, orc, assignment, nranks, n_scalars):
     g, pr, st = make_case(n_scalars)
@@ -92,3 +94,77 @@ def test_multirank_equals_single_rank(mfx, orc, assignment, nranks, n_scalars):
         s, R, iters, status, rc = orc.simple_iter(g, pr, s, n_scalars=n_scalars)
     for k in keys:
         assert np.array_equal(ref_state[k], s[k]), k
+
+
+def packed_state_dict(st, n):
+    """u, v, w, p as views of one [u|v|w|p] device block (mfx_params.packed_state)."""
+    sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+    blk = torch.cat([sd["u"], sd["v"], sd["w"], sd["p"]])
+    for i, k in enumerate(("u", "v", "w", "p")):
+        sd[k] = blk[i * n:(i + 1) * n]
+    return sd, blk
+
+
+@pytest.mark.parametrize("assignment,nranks", [("234[1]", 4), ("222[1]", 2), ("234[1234]", 4), ("234[42]", 4)])
+def test_packed_bcast_equals_grouped(mfx, orc, assignment, nranks):
+    """BCAST of one [u|v|w|p] block (packed_state = 1) gives the same bits as the
+    four grouped broadcasts; a non-contiguous state is refused."""
+    g, pr, st = make_case(0)
+    ref = run_ranks(mfx, assignment, nranks, g, pr, st)
+    prp = synth.Params(lin_maxit_pp=1500, packed_state=1)
+    group = mfx.LocalGroup(nranks)
+    results, errors = {}, []
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sd, blk = packed_state_dict(st, g.n)
+                ctx = mfx.SimpleContext(assignment, g, prp, rank=rank, nranks=nranks, group=group)
+                outs = [ctx.step(sd, stream=stream) for _ in range(2)]
+                stream.synchronize()
+                results[rank] = ({k: v.cpu().numpy() for k, v in sd.items()}, outs)
+                ctx.close()
+        except Exception as e:  # pragma: no cover
+            errors.append((rank, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    group.close()
+    assert not errors, errors
+    for rank in range(nranks):
+        for k in ("u", "v", "w", "p"):
+            assert np.array_equal(results[rank][0][k], ref[rank][0][k]), (rank, k)
+        assert [o["iters"] for o in results[rank][1]] == [o["iters"] for o in ref[rank][1]]
+
+
+def test_packed_state_requires_contiguous_block(mfx):
+    g, pr, st = make_case(0)
+    prp = synth.Params(lin_maxit_pp=1500, packed_state=1)
+    group = mfx.LocalGroup(2)
+    errors = []
+
+    def worker(rank):
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}   # separate allocations
+            ctx = mfx.SimpleContext("222[1]", g, prp, rank=rank, nranks=2, group=group)
+            try:
+                ctx.step(sd, stream=stream)
+            except Exception as e:
+                errors.append((rank, str(e)))
+            finally:
+                ctx.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    group.close()
+    assert len(errors) == 2 and all("packed_state" in e for _, e in errors), errors

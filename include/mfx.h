@@ -415,7 +415,9 @@ mfx_status mfx_prof_read(int counts[16], double ms[16]);
  * automatically only when MFX_GRID_SOLVER_MB sets an L2 budget -- off by
  * default, measured slower at configuration 3), 1 = TMA z-marching kernels,
  * 2 = single-cluster persistent kernel, 3 = v1 grid-stride reference kernels,
- * 4 = grid-synchronous persistent kernel (one cooperative launch per solve).
+ * 4 = grid-synchronous persistent kernel (one cooperative launch per solve),
+ * 5 = persistent row-warp TMA solver (p' only, even nx: the whole iteration
+ * loop in one cooperative launch; other systems take path 1).
  * "graphs": 1/0 enables CUDA-graph replay of the iteration loop.  "pdl": 1/0
  * enables programmatic dependent launch between the BiCGSTAB kernels.
  * "asm_tma": 1/0 selects the TMA z-marching momentum assembly (default) or

@@ -622,7 +622,7 @@ def prof_read():
     return {PROF_IDS[i]: dict(launches=counts[i], ms=ms[i]) for i in range(len(PROF_IDS))}
 
 
-PATH_AUTO, PATH_TMA, PATH_CLUSTER, PATH_V1, PATH_GRID = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_TMA, PATH_CLUSTER, PATH_V1, PATH_GRID, PATH_PERSIST = 0, 1, 2, 3, 4, 5
 
 
 def set_option(key: str, value: int):

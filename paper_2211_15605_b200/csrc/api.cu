@@ -358,7 +358,7 @@ API mfx_status mfx_set_option(const char *key, int value)
 {
     MFX_ARG_CHECK(key, "NULL key");
     if (!strcmp(key, "solver_path")) {
-        MFX_ARG_CHECK(value >= 0 && value <= 4, "solver_path must be 0..4");
+        MFX_ARG_CHECK(value >= 0 && value <= 5, "solver_path must be 0..5");
         g_opt_path.store(value);
         return MFX_OK;
     }

@@ -21,6 +21,8 @@
 
 namespace mfx {
 
+mfx_status persist_solve_launch(const Geo &G, const mfx_eqsys *A, double *x, const WsView &W, int maxit,
+                                cudaStream_t s);
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
                           const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
                           double tol, int maxit, cudaStream_t s, int reverse = 0, int kbeg = 0, int kend = 0,
@@ -831,6 +833,19 @@ static bool grid_solver_fits(const Geo &G, bool sym)
     return budget > 0 && bytes <= budget && !cluster_fits(G, sym);
 }
 
+// persistent row-warp solver (path 5) in auto mode: MFX_PERSIST_MB sets the
+// largest p' working set (3 coefficients + b + 8 vectors) it is chosen for;
+// 0 (default until measured) never.
+static bool persist_fits(const Geo &G)
+{
+    static long long budget = -1;
+    if (budget < 0) {
+        const char *e = getenv("MFX_PERSIST_MB");
+        budget = (e ? atoll(e) : 0) << 20;
+    }
+    return budget > 0 && (long long)(3 + 1 + 8) * 8 * G.N <= budget && !cluster_fits(G, true);
+}
+
 // K3 over n cells (n even, 16-byte aligned arrays) with the rank's dot
 // partials written to rank_part: the z-slab solver's third kernel (dist_solver.cu).
 mfx_status k3_slab_launch(long long n, double *x, double *r, const double *rh, const double *p, const double *v,
@@ -920,6 +935,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
         return finish_info(sym, G, A, x, W, info, s);
     }
     const bool grid_path = path == 4 || (path == 0 && grid_solver_fits(G, sym));
+    const bool persist_path = sym && use_tma(G) && (path == 5 || (path == 0 && persist_fits(G)));
     count_launch(0, s, true);
     if (use_tma(G) && !grid_path) {
         const double *h0[3] = {x, nullptr, nullptr};
@@ -935,6 +951,14 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     k_zero_if<<<nb, kThreads, 0, s>>>(W.hdr, x, G.N);
     count_launch(15, s, false);
     MFX_CUDA_TRY(cudaGetLastError());
+    if (persist_path) {
+        count_launch(6, s, true);
+        mfx_status st = persist_solve_launch(G, A, x, W, maxit, s);
+        count_launch(6, s, false);
+        if (st != MFX_OK) return st;
+        if (!info) return MFX_OK;
+        return finish_info(sym, G, A, x, W, info, s);
+    }
     if (grid_path) {
         count_launch(sym ? 6 : 1, s, true);
         mfx_status st = sym ? launch_grid_solver<true>(G, c, x, W, s) : launch_grid_solver<false>(G, c, x, W, s);

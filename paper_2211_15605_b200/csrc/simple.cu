@@ -526,12 +526,17 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
     // packed BCAST (mfx_params.packed_state, identical on every rank): the four
     // broadcasts of u, v, w, p from the p' owner become one of 4N doubles
     bool skip[64] = {false};
+    mfx_status local_err = MFX_OK;
     if (phase == 1 && c->params.packed_state) {
         auto contiguous = [&](double *const *f) {
             return f[MFX_BUF_U] && f[MFX_BUF_V] == f[MFX_BUF_U] + c->N && f[MFX_BUF_W] == f[MFX_BUF_U] + 2 * c->N &&
                    f[MFX_BUF_P] == f[MFX_BUF_U] + 3 * c->N;
         };
-        MFX_ARG_CHECK(contiguous(fields), "packed_state: u, v, w, p are not one [u|v|w|p] block on rank %d", c->rank);
+        if (!contiguous(fields)) {
+            set_error("packed_state: u, v, w, p are not one [u|v|w|p] block on rank %d", c->rank);
+            if (!c->group) return MFX_ERR_ARG;
+            local_err = MFX_ERR_ARG;   // in-process transport: keep the barriers, fail after them
+        }
         for (int q = 0; q < n; q++) {
             if (ops[q].op != MFX_OP_BCAST || ops[q].buf < MFX_BUF_U || ops[q].buf > MFX_BUF_P) continue;
             if (ops[q].buf == MFX_BUF_U) packed_count[q] = 4 * (size_t)c->N;
@@ -543,21 +548,27 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
         for (int b = 0; b < MFX_NBUF; b++) g.fields[c->rank][b] = fields[b];
         MFX_CUDA_TRY(cudaEventRecord(g.ready[c->rank], s));
         g.barrier();
-        for (int q = 0; q < n; q++) {
+        // a rank-local argument error must not strand the other ranks in the
+        // barriers below: it is reported after them
+        for (int q = 0; q < n && local_err == MFX_OK; q++) {
             const mfx_xfer &o = ops[q];
             if (skip[q] || o.op == MFX_OP_SEND || (o.op == MFX_OP_BCAST && o.peer == c->rank)) continue;
             double *dst = fields[o.buf];
             const double *src = g.fields[o.peer][o.buf];
             size_t off, count;
             span(q, off, count);
-            MFX_ARG_CHECK(!packed_count[q] || (g.fields[o.peer][MFX_BUF_V] == src + c->N &&
-                                               g.fields[o.peer][MFX_BUF_P] == src + 3 * c->N),
-                          "packed_state: the root's [u|v|w|p] block is not contiguous");
+            if (packed_count[q] && !(g.fields[o.peer][MFX_BUF_V] == src + c->N &&
+                                     g.fields[o.peer][MFX_BUF_P] == src + 3 * c->N)) {
+                set_error("packed_state: the root's [u|v|w|p] block is not contiguous");
+                local_err = MFX_ERR_ARG;
+                break;
+            }
             if (dst) dst += off;
             if (src) src += off;
             if (!dst || !src) {
                 set_error("local exchange: buffer %d missing (rank %d <- %d)", o.buf, c->rank, o.peer);
-                return MFX_ERR_ARG;
+                local_err = MFX_ERR_ARG;
+                break;
             }
             MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.ready[o.peer], 0));
             MFX_CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDefault, s));
@@ -567,7 +578,7 @@ mfx_status exchange_state(mfx_ctx *c, int phase, double *const fields[MFX_NBUF],
         for (int q = 0; q < g.nranks; q++)
             if (q != c->rank) MFX_CUDA_TRY(cudaStreamWaitEvent(s, g.done[q], 0));
         g.barrier();   // every rank has enqueued its waits before any event is re-recorded
-        return MFX_OK;
+        return local_err;
     }
     MFX_NCCL_TRY(g_nccl.GroupStart());
     for (int q = 0; q < n; q++) {
@@ -739,6 +750,7 @@ mfx_status simple_iter(mfx_ctx *c, mfx_state *st, mfx_resid *out, cudaStream_t s
         double *D[MFX_NBUF] = {0};
         D[MFX_BUF_BETA] = st->beta; D[MFX_BUF_SBU] = st->sbeta_u;
         D[MFX_BUF_SBV] = st->sbeta_v; D[MFX_BUF_SBW] = st->sbeta_w;
+        D[MFX_BUF_META] = c->meta;   // slot 8: the PIC record (error latch of the refresh)
         if ((rc = exchange_fork(c, 3, D, s, c->xt[0], c->xt[1])) != MFX_OK) return rc;
         if ((rc = exchange_join(c, s)) != MFX_OK) return rc;
         c->pic_pending = 0;

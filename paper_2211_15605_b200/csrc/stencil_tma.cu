@@ -144,18 +144,19 @@ struct Cursor {
     __device__ bool produces() const { return k >= k0 + 1; }
 };
 
-template <int MODE, bool SYM, int TX, int TY, int CPT_, int S>
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S, int STRIDE = Cfg<MODE, SYM, TX, TY, CPT_>::STAGE_B>
 __device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, uint8_t *stages, uint64_t *full,
                                       int q)
 {
     using C = Cfg<MODE, SYM, TX, TY, CPT_>;
+    static_assert(STRIDE >= C::STAGE_B, "stage slot too small");
     const int s = q % S;
     uint64_t *bar = &full[s];
     if (c.is_virtual(nz)) {
         mbar_arrive(bar);
         return;
     }
-    uint8_t *st = stages + (size_t)s * C::STAGE_B;
+    uint8_t *st = stages + (size_t)s * STRIDE;
     const int x0 = c.x0, y0 = c.y0, k = c.k;
     mbar_arrive_expect_tx(bar, C::STAGE_TX);
 #pragma unroll
@@ -518,8 +519,215 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 // barrier) and a warp hands its stage back as soon as its loads are in
 // registers.  The expressions and their order are those of k_stencil, so the
 // bits are the same (tested against the oracle on every p' path).
+// TMA producer of a row-warp pass (lane 0 of the producer warp)
+template <int MODE, int CPT, int S, int STRIDE>
+__device__ __forceinline__ void rw_produce(const TmaMaps &M, const StencilArgs &a, uint8_t *stages, uint64_t *full,
+                                           uint64_t *empty, int &q)
+{
+    constexpr int TX = 32 * CPT, TY = 8;
+    Cursor prod;
+    prod.init(blockIdx.x, a, a.tiles_x * a.tiles_y, TX, TY);
+    for (; prod.valid; q++) {
+        if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
+        issue<MODE, true, TX, TY, CPT, S, STRIDE>(M, prod, a.nz, stages, full, q);
+        prod.advance(a.nz);
+    }
+}
+
+// consumer warps of a row-warp pass (MODE) over this CTA's units; q is the
+// ring position shared with rw_produce, carried across passes of a persistent
+// kernel; stage slots are STRIDE bytes apart.  acc[d][m]: dot d, owned cell m.
+template <int MODE, int CPT, int S, int STRIDE>
+__device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, double beta, double omega, bool rst,
+                                           Acc (&acc)[3][CPT], const uint8_t *stages, uint64_t *full,
+                                           uint64_t *empty, int &q)
+{
+    constexpr int TX = 32 * CPT, TY = 8;
+    using C = Cfg<MODE, true, TX, TY, CPT>;
+    constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Cursor cons;
+    cons.init(blockIdx.x, a, a.tiles_x * a.tiles_y, TX, TY);
+    const int cx0 = lane * CPT;
+    const int hc = (warp + 1) * C::HX + cx0 + 2;                    // halo-box index of the first owned cell
+    const int he = lane == 31 ? (warp + 1) * C::HX + TX + 2          // right edge cell x0 + TX
+                              : (warp + 1) * C::HX + 1;              // left edge cell x0 - 1 (used by lane 0)
+    const int ci = warp * TX + cx0;
+    // register pipeline: values of planes q-2 (B), q-1 (centre row + S/N rows + edge), q (T)
+    double vB[CPT], vC[CPT], vS[CPT], vN[CPT], vE = 0.0;
+    double kxw[CPT + 1], kys[CPT], kyn[CPT], kex[CPT], czp[CPT], czpp[CPT];
+#pragma unroll
+    for (int m = 0; m < CPT; m++) {
+        vB[m] = vC[m] = vS[m] = vN[m] = 0.0;
+        kys[m] = kyn[m] = kex[m] = czp[m] = czpp[m] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m <= CPT; m++) kxw[m] = 0.0;
+
+    // value of the step-1 field at halo index i (CPT consecutive cells from i)
+    auto value = [&](const uint8_t *st, int i, double (&out)[CPT]) {
+        const double *h0 = (const double *)(st + C::OFF_HALO);
+        const double *h1 = (const double *)(st + C::OFF_HALO + C::HALO_B);
+        const double *h2 = (const double *)(st + C::OFF_HALO + 2 * C::HALO_B);
+        double rv[CPT], pv[CPT], vv[CPT];
+        if (CPT == 2) {
+            const double2 r2 = *(const double2 *)(h0 + i);
+            rv[0] = r2.x; rv[CPT - 1] = r2.y;
+            if (MODE == SM_K1) {
+                const double2 p2 = *(const double2 *)(h1 + i), v2 = *(const double2 *)(h2 + i);
+                pv[0] = p2.x; pv[CPT - 1] = p2.y; vv[0] = v2.x; vv[CPT - 1] = v2.y;
+            } else if (MODE == SM_K2) {
+                const double2 v2 = *(const double2 *)(h1 + i);
+                vv[0] = v2.x; vv[CPT - 1] = v2.y;
+            }
+        } else {
+            rv[0] = h0[i];
+            if (MODE == SM_K1) { pv[0] = h1[i]; vv[0] = h2[i]; }
+            else if (MODE == SM_K2) vv[0] = h1[i];
+        }
+#pragma unroll
+        for (int m = 0; m < CPT; m++) {
+            if (MODE == SM_SPMV || MODE == SM_SETUP) out[m] = rv[m];
+            else if (MODE == SM_K1) out[m] = rst ? fma(beta, fma(-omega, 0.0, 0.0), rv[m])
+                                                 : fma(beta, fma(-omega, vv[m], pv[m]), rv[m]);
+            else out[m] = fma(-alpha, vv[m], rv[m]);
+        }
+    };
+    auto value1 = [&](const uint8_t *st, int i) -> double {
+        const double r = ((const double *)(st + C::OFF_HALO))[i];
+        if (MODE == SM_K1) {
+            const double p = ((const double *)(st + C::OFF_HALO + C::HALO_B))[i];
+            const double v = ((const double *)(st + C::OFF_HALO + 2 * C::HALO_B))[i];
+            return rst ? fma(beta, fma(-omega, 0.0, 0.0), r) : fma(beta, fma(-omega, v, p), r);
+        }
+        if (MODE == SM_K2) return fma(-alpha, ((const double *)(st + C::OFF_HALO + C::HALO_B))[i], r);
+        return r;
+    };
+
+    for (; cons.valid; q++) {
+        const int s = q % S;
+        const bool virt = cons.is_virtual(a.nz);
+        const bool produce = cons.produces();
+        const int kout = cons.k - 1;
+        mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+        const uint8_t *st = stages + (size_t)s * STRIDE;
+        // ---- centre row of plane q (T of the output plane, B of the next)
+        double tC[CPT];
+        if (!virt) value(st, hc, tC);
+        else
+#pragma unroll
+            for (int m = 0; m < CPT; m++) tC[m] = 0.0;
+        if (MODE == SM_K1 && a.ghost_store && !virt && (cons.k == a.kbeg - 1 || cons.k == a.kend)) {
+            const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
+            if (gx < a.nx && gy < a.ny)
+                store_cells<CPT>(a.out0 + (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * cons.k),
+                                 tC);
+        }
+        // ---- step 2: output plane q-1
+        if (produce) {
+            double xc[CPT], xW[CPT], xE[CPT], xS[CPT], xN[CPT], xB[CPT], xT[CPT];
+            const double left = __shfl_up_sync(0xffffffffu, vC[CPT - 1], 1);
+            const double right = __shfl_down_sync(0xffffffffu, vC[0], 1);
+#pragma unroll
+            for (int m = 0; m < CPT; m++) {
+                xc[m] = vC[m];
+                xW[m] = m > 0 ? vC[m - 1] : (lane == 0 ? vE : left);
+                xE[m] = m < CPT - 1 ? vC[m + 1] : (lane == 31 ? vE : right);
+                xS[m] = vS[m]; xN[m] = vN[m]; xB[m] = vB[m]; xT[m] = tC[m];
+            }
+            double y[CPT];
+#pragma unroll
+            for (int m = 0; m < CPT; m++) {
+                const double aW = kxw[m], aE = kxw[m + 1], aS = kys[m], aN = kyn[m], aB = czpp[m], aT = czp[m];
+                const double aP = ((((aW + aE) + aS) + aN) + aB) + aT;
+                double t = aP * xc[m];
+                t = fma(-aW, xW[m], t);
+                t = fma(-aE, xE[m], t);
+                t = fma(-aS, xS[m], t);
+                t = fma(-aN, xN[m], t);
+                t = fma(-aB, xB[m], t);
+                t = fma(-aT, xT[m], t);
+                y[m] = t;
+            }
+            const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
+            if (gx < a.nx && gy < a.ny) {
+                const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
+                if (MODE == SM_SPMV) {
+                    store_cells<CPT>(a.out0 + n, y);
+                } else if (MODE == SM_SETUP) {
+                    double rv[CPT];
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) {
+                        rv[m] = kex[m] - y[m];
+                        acc[0][m].prod(kex[m], kex[m]);
+                        acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
+                    }
+                    store_cells<CPT>(a.out0 + n, rv);
+                } else if (MODE == SM_K1) {
+                    store_cells<CPT>(a.out0 + n, xc);
+                    store_cells<CPT>(a.out1 + n, y);
+                    if (rst) store_cells<CPT>(a.out2 + n, kex);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) acc[0][m].prod(kex[m], y[m]);
+                } else {
+                    store_cells<CPT>(a.out0 + n, y);
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) {
+                        acc[0][m].prod(y[m], xc[m]);
+                        acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
+                        acc[ND > 2 ? 2 : 0][m].prod(xc[m], xc[m]);
+                    }
+                }
+            }
+        }
+        // ---- the rest of plane q -> registers, then the stage goes back to the producer
+        double tS[CPT], tN[CPT], tE = 0.0;
+        double nkxw[CPT + 1], nkys[CPT], nkyn[CPT], nkex[CPT], ncz[CPT];
+        if (!virt) {
+            value(st, hc - C::HX, tS);
+            value(st, hc + C::HX, tN);
+            tE = value1(st, he);
+            const double *xw = (const double *)(st + C::OFF_XW);
+            const double *ys = (const double *)(st + C::OFF_YS);
+            const double *cz = (const double *)(st + C::OFF_CELL);
+#pragma unroll
+            for (int m = 0; m <= CPT; m++) nkxw[m] = xw[warp * C::HX + cx0 + m + 1];
+#pragma unroll
+            for (int m = 0; m < CPT; m++) {
+                nkys[m] = ys[warp * TX + cx0 + m];
+                nkyn[m] = ys[(warp + 1) * TX + cx0 + m];
+                ncz[m] = cz[ci + m];
+                if (MODE == SM_SETUP) nkex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                else if (MODE == SM_K1)
+                    nkex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
+                                  : ((const double *)(st + C::OFF_EXTRA))[ci + m];
+                else nkex[m] = 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < CPT; m++) tS[m] = tN[m] = nkys[m] = nkyn[m] = nkex[m] = ncz[m] = 0.0;
+#pragma unroll
+            for (int m = 0; m <= CPT; m++) nkxw[m] = 0.0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+
+        // ---- rotate the register pipeline
+#pragma unroll
+        for (int m = 0; m < CPT; m++) {
+            vB[m] = vC[m]; vC[m] = tC[m]; vS[m] = tS[m]; vN[m] = tN[m];
+            czpp[m] = czp[m]; czp[m] = ncz[m];
+            kys[m] = nkys[m]; kyn[m] = nkyn[m]; kex[m] = nkex[m];
+        }
+#pragma unroll
+        for (int m = 0; m <= CPT; m++) kxw[m] = nkxw[m];
+        vE = tE;
+        cons.advance(a.nz);
+    }
+}
+
 template <int MODE, int CPT, int S>
-__global__ void __launch_bounds__(8 * 32 + 32) k_stencil_rw(const __grid_constant__ TmaMaps M, StencilArgs a)
+__global__ void __launch_bounds__(8 * 32 + 32, 2) k_stencil_rw(const __grid_constant__ TmaMaps M, StencilArgs a)
 {
     constexpr int TX = 32 * CPT, TY = 8;
     using C = Cfg<MODE, true, TX, TY, CPT>;
@@ -532,7 +740,6 @@ __global__ void __launch_bounds__(8 * 32 + 32) k_stencil_rw(const __grid_constan
     const int warp = tid >> 5, lane = tid & 31;
 
     pdl_trigger();
-    const int ntiles = a.tiles_x * a.tiles_y;
     if (tid == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
@@ -566,203 +773,21 @@ __global__ void __launch_bounds__(8 * 32 + 32) k_stencil_rw(const __grid_constan
     }
 
     constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
-    Acc acc[ND][CPT];
+    Acc acc[3][CPT];
 #pragma unroll
-    for (int d = 0; d < ND; d++)
+    for (int d = 0; d < 3; d++)
 #pragma unroll
         for (int m = 0; m < CPT; m++) acc[d][m].zero();
 
+    int q = 0;
     if (warp == C::NW) {
         if (lane == 0) {
 #pragma unroll
-            for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
-            Cursor prod;
-            prod.init(blockIdx.x, a, ntiles, TX, TY);
-            for (int q = 0; prod.valid; q++) {
-                if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
-                issue<MODE, true, TX, TY, CPT, S>(M, prod, a.nz, stages, full, q);
-                prod.advance(a.nz);
-            }
+            for (int h = 0; h < C::NH; h++) prefetch_map(&M.halo[h]);
+            rw_produce<MODE, CPT, S, C::STAGE_B>(M, a, stages, full, empty, q);
         }
     } else {
-        Cursor cons;
-        cons.init(blockIdx.x, a, ntiles, TX, TY);
-        const int cx0 = lane * CPT;
-        const int hc = (warp + 1) * C::HX + cx0 + 2;                    // halo-box index of the first owned cell
-        const int he = lane == 31 ? (warp + 1) * C::HX + TX + 2          // right edge cell x0 + TX
-                                  : (warp + 1) * C::HX + 1;              // left edge cell x0 - 1 (used by lane 0)
-        const int ci = warp * TX + cx0;
-        // register pipeline: values of planes q-2 (B), q-1 (centre row + S/N rows + edge), q (T)
-        double vB[CPT], vC[CPT], vS[CPT], vN[CPT], vE = 0.0;
-        double kxw[CPT + 1], kys[CPT], kyn[CPT], kex[CPT], czp[CPT], czpp[CPT];
-#pragma unroll
-        for (int m = 0; m < CPT; m++) {
-            vB[m] = vC[m] = vS[m] = vN[m] = 0.0;
-            kys[m] = kyn[m] = kex[m] = czp[m] = czpp[m] = 0.0;
-        }
-#pragma unroll
-        for (int m = 0; m <= CPT; m++) kxw[m] = 0.0;
-
-        // value of the step-1 field at halo index i (CPT consecutive cells from i)
-        auto value = [&](const uint8_t *st, int i, double (&out)[CPT]) {
-            const double *h0 = (const double *)(st + C::OFF_HALO);
-            const double *h1 = (const double *)(st + C::OFF_HALO + C::HALO_B);
-            const double *h2 = (const double *)(st + C::OFF_HALO + 2 * C::HALO_B);
-            double rv[CPT], pv[CPT], vv[CPT];
-            if (CPT == 2) {
-                const double2 r2 = *(const double2 *)(h0 + i);
-                rv[0] = r2.x; rv[CPT - 1] = r2.y;
-                if (MODE == SM_K1) {
-                    const double2 p2 = *(const double2 *)(h1 + i), v2 = *(const double2 *)(h2 + i);
-                    pv[0] = p2.x; pv[CPT - 1] = p2.y; vv[0] = v2.x; vv[CPT - 1] = v2.y;
-                } else if (MODE == SM_K2) {
-                    const double2 v2 = *(const double2 *)(h1 + i);
-                    vv[0] = v2.x; vv[CPT - 1] = v2.y;
-                }
-            } else {
-                rv[0] = h0[i];
-                if (MODE == SM_K1) { pv[0] = h1[i]; vv[0] = h2[i]; }
-                else if (MODE == SM_K2) vv[0] = h1[i];
-            }
-#pragma unroll
-            for (int m = 0; m < CPT; m++) {
-                if (MODE == SM_SPMV || MODE == SM_SETUP) out[m] = rv[m];
-                else if (MODE == SM_K1) out[m] = rst ? fma(beta, fma(-omega, 0.0, 0.0), rv[m])
-                                                     : fma(beta, fma(-omega, vv[m], pv[m]), rv[m]);
-                else out[m] = fma(-alpha, vv[m], rv[m]);
-            }
-        };
-        auto value1 = [&](const uint8_t *st, int i) -> double {
-            const double r = ((const double *)(st + C::OFF_HALO))[i];
-            if (MODE == SM_K1) {
-                const double p = ((const double *)(st + C::OFF_HALO + C::HALO_B))[i];
-                const double v = ((const double *)(st + C::OFF_HALO + 2 * C::HALO_B))[i];
-                return rst ? fma(beta, fma(-omega, 0.0, 0.0), r) : fma(beta, fma(-omega, v, p), r);
-            }
-            if (MODE == SM_K2) return fma(-alpha, ((const double *)(st + C::OFF_HALO + C::HALO_B))[i], r);
-            return r;
-        };
-
-        for (int q = 0; cons.valid; q++) {
-            const int s = q % S;
-            const bool virt = cons.is_virtual(a.nz);
-            const bool produce = cons.produces();
-            const int kout = cons.k - 1;
-            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
-            const uint8_t *st = stages + (size_t)s * C::STAGE_B;
-            // ---- centre row of plane q (T of the output plane, B of the next)
-            double tC[CPT];
-            if (!virt) value(st, hc, tC);
-            else
-#pragma unroll
-                for (int m = 0; m < CPT; m++) tC[m] = 0.0;
-            if (MODE == SM_K1 && a.ghost_store && !virt && (cons.k == a.kbeg - 1 || cons.k == a.kend)) {
-                const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
-                if (gx < a.nx && gy < a.ny)
-                    store_cells<CPT>(a.out0 + (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * cons.k),
-                                     tC);
-            }
-            // ---- step 2: output plane q-1
-            if (produce) {
-                double xc[CPT], xW[CPT], xE[CPT], xS[CPT], xN[CPT], xB[CPT], xT[CPT];
-                const double left = __shfl_up_sync(0xffffffffu, vC[CPT - 1], 1);
-                const double right = __shfl_down_sync(0xffffffffu, vC[0], 1);
-#pragma unroll
-                for (int m = 0; m < CPT; m++) {
-                    xc[m] = vC[m];
-                    xW[m] = m > 0 ? vC[m - 1] : (lane == 0 ? vE : left);
-                    xE[m] = m < CPT - 1 ? vC[m + 1] : (lane == 31 ? vE : right);
-                    xS[m] = vS[m]; xN[m] = vN[m]; xB[m] = vB[m]; xT[m] = tC[m];
-                }
-                double y[CPT];
-#pragma unroll
-                for (int m = 0; m < CPT; m++) {
-                    const double aW = kxw[m], aE = kxw[m + 1], aS = kys[m], aN = kyn[m], aB = czpp[m], aT = czp[m];
-                    const double aP = ((((aW + aE) + aS) + aN) + aB) + aT;
-                    double t = aP * xc[m];
-                    t = fma(-aW, xW[m], t);
-                    t = fma(-aE, xE[m], t);
-                    t = fma(-aS, xS[m], t);
-                    t = fma(-aN, xN[m], t);
-                    t = fma(-aB, xB[m], t);
-                    t = fma(-aT, xT[m], t);
-                    y[m] = t;
-                }
-                const int gx = cons.x0 + cx0, gy = cons.y0 + warp;
-                if (gx < a.nx && gy < a.ny) {
-                    const long long n = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * kout);
-                    if (MODE == SM_SPMV) {
-                        store_cells<CPT>(a.out0 + n, y);
-                    } else if (MODE == SM_SETUP) {
-                        double rv[CPT];
-#pragma unroll
-                        for (int m = 0; m < CPT; m++) {
-                            rv[m] = kex[m] - y[m];
-                            acc[0][m].prod(kex[m], kex[m]);
-                            acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
-                        }
-                        store_cells<CPT>(a.out0 + n, rv);
-                    } else if (MODE == SM_K1) {
-                        store_cells<CPT>(a.out0 + n, xc);
-                        store_cells<CPT>(a.out1 + n, y);
-                        if (rst) store_cells<CPT>(a.out2 + n, kex);
-#pragma unroll
-                        for (int m = 0; m < CPT; m++) acc[0][m].prod(kex[m], y[m]);
-                    } else {
-                        store_cells<CPT>(a.out0 + n, y);
-#pragma unroll
-                        for (int m = 0; m < CPT; m++) {
-                            acc[0][m].prod(y[m], xc[m]);
-                            acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
-                            acc[ND > 2 ? 2 : 0][m].prod(xc[m], xc[m]);
-                        }
-                    }
-                }
-            }
-            // ---- the rest of plane q -> registers, then the stage goes back to the producer
-            double tS[CPT], tN[CPT], tE = 0.0;
-            double nkxw[CPT + 1], nkys[CPT], nkyn[CPT], nkex[CPT], ncz[CPT];
-            if (!virt) {
-                value(st, hc - C::HX, tS);
-                value(st, hc + C::HX, tN);
-                tE = value1(st, he);
-                const double *xw = (const double *)(st + C::OFF_XW);
-                const double *ys = (const double *)(st + C::OFF_YS);
-                const double *cz = (const double *)(st + C::OFF_CELL);
-#pragma unroll
-                for (int m = 0; m <= CPT; m++) nkxw[m] = xw[warp * C::HX + cx0 + m + 1];
-#pragma unroll
-                for (int m = 0; m < CPT; m++) {
-                    nkys[m] = ys[warp * TX + cx0 + m];
-                    nkyn[m] = ys[(warp + 1) * TX + cx0 + m];
-                    ncz[m] = cz[ci + m];
-                    if (MODE == SM_SETUP) nkex[m] = ((const double *)(st + C::OFF_EXTRA))[ci + m];
-                    else if (MODE == SM_K1)
-                        nkex[m] = rst ? ((const double *)(st + C::OFF_HALO))[hc + m]
-                                      : ((const double *)(st + C::OFF_EXTRA))[ci + m];
-                    else nkex[m] = 0.0;
-                }
-            } else {
-#pragma unroll
-                for (int m = 0; m < CPT; m++) tS[m] = tN[m] = nkys[m] = nkyn[m] = nkex[m] = ncz[m] = 0.0;
-#pragma unroll
-                for (int m = 0; m <= CPT; m++) nkxw[m] = 0.0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-
-            // ---- rotate the register pipeline
-#pragma unroll
-            for (int m = 0; m < CPT; m++) {
-                vB[m] = vC[m]; vC[m] = tC[m]; vS[m] = tS[m]; vN[m] = tN[m];
-                czpp[m] = czp[m]; czp[m] = ncz[m];
-                kys[m] = nkys[m]; kyn[m] = nkyn[m]; kex[m] = nkex[m];
-            }
-#pragma unroll
-            for (int m = 0; m <= CPT; m++) kxw[m] = nkxw[m];
-            vE = tE;
-            cons.advance(a.nz);
-        }
+        rw_consume<MODE, CPT, S, C::STAGE_B>(a, alpha, beta, omega, rst, acc, stages, full, empty, q);
     }
 
     if constexpr (C::NDOT > 0) {
@@ -785,6 +810,219 @@ __global__ void __launch_bounds__(8 * 32 + 32) k_stencil_rw(const __grid_constan
         else if (MODE == SM_K1) bicg_k1_tail(Sc, P1, dd_round(out[0]));
         else if (MODE == SM_K2) bicg_k2_tail(Sc, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
     }
+}
+
+// ------------------------------------------------------------------ persistent row-warp solver
+// The whole BiCGSTAB loop for a symmetric (p') system in ONE cooperative
+// launch (solver path 5; DESIGN.md §7 "persistent"): per iteration the
+// row-warp K1 and K2 passes (TMA ring carried across passes) and a K3 pass
+// over the CTA's own cells, separated by grid all-reduces.  Every CTA posts its
+// double-double partials, one arrival counter orders the phase, and then every
+// CTA folds all partials in the same fixed order and runs the scalar step of
+// §3.6 itself (identical bits in every CTA), so a phase boundary costs one
+// atomic arrival and one wait instead of a kernel drain, a launch and a
+// pipeline refill.  Same expressions, correctly rounded dots: the iterates
+// equal the other paths' bitwise.
+struct PersistArgs {
+    TmaMaps M1[2], M2[2];          // K1 / K2 maps for iteration parity 0 / 1 (ping-pong p, v)
+    StencilArgs a1[2], a2[2];
+    double *x, *r, *rh, *p[2], *v[2], *t;
+    WsHeader *h;
+    dd *part;                      // 2 x gridDim.x x 3 (double-buffered by phase parity)
+    unsigned *arrive;              // monotone arrival counter, zero at launch
+    int maxit;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// all-reduce of K double-doubles over the grid; out valid in thread 0
+template <int K, int CPT>
+__device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *part, unsigned *arrive, unsigned &phase,
+                                               dd *sh, dd (&out)[K])
+{
+    dd v[K];
+#pragma unroll
+    for (int d = 0; d < K; d++) {
+        v[d] = acc[d][0].get();
+#pragma unroll
+        for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // this thread's generic stores vs later TMA reads
+    block_reduce_dd<K>(v, sh);                                  // (syncs the CTA: every store precedes the arrival)
+    dd *pb = part + (size_t)(phase & 1) * gridDim.x * 3;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d = 0; d < K; d++) pb[(size_t)blockIdx.x * 3 + d] = v[d];
+        __threadfence();
+        atomicAdd(arrive, 1u);
+        const unsigned target = (phase + 1) * gridDim.x;
+        if (ld_acquire_u32(arrive) < target) {
+            unsigned long long t0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (ld_acquire_u32(arrive) < target) {
+                unsigned long long t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                if (t1 - t0 > 20000000000ull) __trap();   // 20 s: a CTA is missing (never expected)
+            }
+        }
+    }
+    phase++;
+    __syncthreads();
+    dd f[K];
+#pragma unroll
+    for (int d = 0; d < K; d++) f[d] = dd{0.0, 0.0};
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < K; d++) {
+            dd x;
+            x.hi = __ldcg(&pb[(size_t)b * 3 + d].hi);
+            x.lo = __ldcg(&pb[(size_t)b * 3 + d].lo);
+            f[d] = dd_add(f[d], x);
+        }
+    }
+    block_reduce_dd<K>(f, sh);
+#pragma unroll
+    for (int d = 0; d < K; d++) out[d] = f[d];
+}
+
+template <int CPT, int S>
+__global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constant__ PersistArgs P)
+{
+    constexpr int TX = 32 * CPT, TY = 8;
+    using C1 = Cfg<SM_K1, true, TX, TY, CPT>;
+    using C2 = Cfg<SM_K2, true, TX, TY, CPT>;
+    constexpr int STRIDE = C1::STAGE_B > C2::STAGE_B ? C1::STAGE_B : C2::STAGE_B;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *stages = smem;
+    uint64_t *full = (uint64_t *)(smem + (size_t)S * STRIDE);
+    uint64_t *empty = full + S;
+    __shared__ SolverScalars Ls;
+    __shared__ dd sh[(C1::NW + 1) * 3];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C1::NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        Ls = P.h->sc;
+    }
+    __syncthreads();
+    const bool producer = warp == C1::NW;
+    int q = 0;
+    unsigned phase = 0;
+    const long long units = P.a1[0].units;
+    const int ntiles = P.a1[0].tiles_x * P.a1[0].tiles_y;
+    Acc acc[3][CPT];
+    for (int it = 0; it <= P.maxit; it++) {
+        if (Ls.done) break;
+        const K1Pro P1 = bicg_k1_prologue(Ls);
+        if (P1.breakdown) {
+            __syncthreads();
+            if (tid == 0) bicg_breakdown(Ls);
+            break;
+        }
+        const int par = it & 1;
+        dd out[3];
+        // ---- K1: p = r + beta (p - omega v) on the halo'd planes, v = A p, <r^, v>
+#pragma unroll
+        for (int d = 0; d < 3; d++)
+#pragma unroll
+            for (int m = 0; m < CPT; m++) acc[d][m].zero();
+        if (producer) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                rw_produce<SM_K1, CPT, S, STRIDE>(P.M1[par], P.a1[par], stages, full, empty, q);
+            }
+        } else {
+            rw_consume<SM_K1, CPT, S, STRIDE>(P.a1[par], 0.0, P1.beta, P1.omega, P1.rst, acc, stages, full, empty, q);
+        }
+        grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out);
+        if (tid == 0) bicg_k1_tail(Ls, P1, dd_round(out[0]));
+        __syncthreads();
+        if (Ls.done || Ls.skip) continue;
+        // ---- K2: s = r - alpha v, t = A s, <t,s>, <t,t>, <s,s>
+        const double alpha = Ls.alpha;
+#pragma unroll
+        for (int d = 0; d < 3; d++)
+#pragma unroll
+            for (int m = 0; m < CPT; m++) acc[d][m].zero();
+        if (producer) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                rw_produce<SM_K2, CPT, S, STRIDE>(P.M2[par], P.a2[par], stages, full, empty, q);
+            }
+        } else {
+            rw_consume<SM_K2, CPT, S, STRIDE>(P.a2[par], alpha, 0.0, 0.0, false, acc, stages, full, empty, q);
+        }
+        grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out);
+        if (tid == 0) bicg_k2_tail(Ls, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
+        __syncthreads();
+        if (Ls.done || Ls.skip) continue;
+        // ---- K3 over this CTA's own cells (the units of K1/K2, so every value it
+        // reads was written by this CTA): x, r update, <r^, r>, <r, r>
+        const bool half = Ls.half != 0;
+        const double al = Ls.alpha, om = Ls.omega;
+#pragma unroll
+        for (int d = 0; d < 3; d++)
+#pragma unroll
+            for (int m = 0; m < CPT; m++) acc[d][m].zero();
+        if (!producer) {
+            const StencilArgs &a = P.a1[par];
+            const double *pn = P.p[par ^ 1], *vn = P.v[par ^ 1];
+            for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+                const int chunk = (int)(u / ntiles), tile = (int)(u - (long long)chunk * ntiles);
+                const int ty = tile / a.tiles_x;
+                const int gx = (tile - ty * a.tiles_x) * TX + lane * CPT, gy = ty * TY + warp;
+                if (gx >= a.nx || gy >= a.ny) continue;
+                const int k0 = a.kbeg + chunk * a.Lz, k1 = k0 + a.Lz < a.kend ? k0 + a.Lz : a.kend;
+                for (int k = k0; k < k1; k++) {
+                    const long long e = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * k);
+                    double xv[CPT], rv[CPT], rhv[CPT], pv[CPT], vv[CPT], tv[CPT];
+                    if (CPT == 2) {
+                        auto ld2 = [&](const double *b, double (&o)[CPT]) {
+                            const double2 w = __ldcg((const double2 *)(b + e));
+                            o[0] = w.x; o[CPT - 1] = w.y;
+                        };
+                        ld2(P.x, xv); ld2(P.r, rv); ld2(P.rh, rhv); ld2(pn, pv); ld2(vn, vv);
+                        if (!half) ld2(P.t, tv);
+                        else tv[0] = tv[CPT - 1] = 0.0;
+                    } else {
+                        xv[0] = __ldcg(P.x + e); rv[0] = __ldcg(P.r + e); rhv[0] = __ldcg(P.rh + e);
+                        pv[0] = __ldcg(pn + e); vv[0] = __ldcg(vn + e); tv[0] = half ? 0.0 : __ldcg(P.t + e);
+                    }
+#pragma unroll
+                    for (int m = 0; m < CPT; m++) {
+                        const double sv = fma(-al, vv[m], rv[m]);
+                        double xo, ro;
+                        if (half) {
+                            xo = fma(al, pv[m], xv[m]);
+                            ro = sv;
+                        } else {
+                            xo = fma(om, sv, fma(al, pv[m], xv[m]));
+                            ro = fma(-om, tv[m], sv);
+                        }
+                        xv[m] = xo;
+                        rv[m] = ro;
+                        acc[0][m].prod(rhv[m], ro);
+                        acc[1][m].prod(ro, ro);
+                    }
+                    store_cells<CPT>(P.x + e, xv);
+                    store_cells<CPT>(P.r + e, rv);
+                }
+            }
+        }
+        grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out);
+        if (tid == 0) bicg_k3_tail(Ls, half, dd_round(out[0]), dd_round(out[1]));
+        __syncthreads();
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) P.h->sc = Ls;
 }
 
 // ------------------------------------------------------------------ host side
@@ -964,7 +1202,94 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
     return run_tile<MODE, SYM, 64, 4, 1>(G, halo, coef, extra, a, s);
 }
 
+template <int CPT, int S>
+struct PersistLauncher {
+    static constexpr int TX = 32 * CPT, TY = 8;
+    using C1 = Cfg<SM_K1, true, TX, TY, CPT>;
+    using C2 = Cfg<SM_K2, true, TX, TY, CPT>;
+    static constexpr int STRIDE = C1::STAGE_B > C2::STAGE_B ? C1::STAGE_B : C2::STAGE_B;
+    static constexpr size_t smem() { return (size_t)S * STRIDE + 16 * (size_t)S; }
+    static int grid_size()
+    {
+        static int g = 0;
+        if (g) return g;
+        cudaFuncSetAttribute(k_bicg_rw<CPT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        int occ = 0, dev = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bicg_rw<CPT, S>, C1::NT + 32, smem());
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g = sms * (occ > 0 ? occ : 1);
+        if (g > kMaxBlocks / 2) g = kMaxBlocks / 2;
+        return g;
+    }
+    static mfx_status run(const Geo &G, const mfx_eqsys *A, double *x, const WsView &W, int maxit, cudaStream_t s)
+    {
+        PersistArgs P;
+        memset(&P, 0, sizeof(P));
+        StencilArgs a;
+        memset(&a, 0, sizeof(a));
+        a.nx = G.nx; a.ny = G.ny; a.nz = G.nz;
+        a.tiles_x = (G.nx + TX - 1) / TX;
+        a.tiles_y = (G.ny + TY - 1) / TY;
+        int grid = grid_size();
+        const long long ntiles = (long long)a.tiles_x * a.tiles_y;
+        a.kbeg = 0; a.kend = G.nz;
+        a.Lz = choose_lz(ntiles, G.nz, grid);
+        a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
+        if (grid > a.units) grid = (int)a.units;
+        a.h = W.hdr; a.part = W.part;
+        for (int par = 0; par < 2; par++) {
+            const double *h1[3] = {W.r, W.p[par], W.v[par]};
+            const double *h2[2] = {W.r, W.v[par ^ 1]};
+            for (int q = 0; q < 3; q++)
+                if (!make_map(&P.M1[par].halo[q], h1[q], G.nx, G.ny, G.nz, C1::HX, C1::HY)) return MFX_ERR_CUDA;
+            for (int q = 0; q < 2; q++)
+                if (!make_map(&P.M2[par].halo[q], h2[q], G.nx, G.ny, G.nz, C2::HX, C2::HY)) return MFX_ERR_CUDA;
+            TmaMaps *Ms[2] = {&P.M1[par], &P.M2[par]};
+            for (TmaMaps *M : Ms) {
+                if (!make_map(&M->coef[0], A->aT, G.nx, G.ny, G.nz, TX, TY) ||
+                    !make_map(&M->coef[2], A->aE, G.nx, G.ny, G.nz, C1::HX, TY) ||
+                    !make_map(&M->coef[3], A->aN, G.nx, G.ny, G.nz, TX, TY + 1))
+                    return MFX_ERR_CUDA;
+            }
+            if (!make_map(&P.M1[par].extra, W.rh, G.nx, G.ny, G.nz, TX, TY)) return MFX_ERR_CUDA;
+            P.a1[par] = a;
+            P.a1[par].out0 = W.p[par ^ 1]; P.a1[par].out1 = W.v[par ^ 1]; P.a1[par].out2 = W.rh;
+            P.a2[par] = a;
+            P.a2[par].out0 = W.t;
+        }
+        P.x = x; P.r = W.r; P.rh = W.rh; P.t = W.t;
+        P.p[0] = W.p[0]; P.p[1] = W.p[1]; P.v[0] = W.v[0]; P.v[1] = W.v[1];
+        P.h = W.hdr; P.part = W.part; P.arrive = &W.hdr->ticket[2]; P.maxit = maxit;
+        MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[2], 0, sizeof(unsigned), s));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C1::NT + 32);
+        cfg.dynamicSmemBytes = smem();
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
+        return MFX_OK;
+    }
+};
+
 }  // namespace
+
+// solver path 5: the whole p' BiCGSTAB loop in one cooperative launch (after
+// the setup kernel); symmetric systems, even nx, 16-byte aligned arrays.
+mfx_status persist_solve_launch(const Geo &G, const mfx_eqsys *A, double *x, const WsView &W, int maxit,
+                                cudaStream_t s)
+{
+    if (!get_encode()) return MFX_ERR_CUDA;
+    if (G.nx <= 32) return PersistLauncher<1, 3>::run(G, A, x, W, maxit, s);
+    return PersistLauncher<2, 3>::run(G, A, x, W, maxit, s);
+}
+
+
 
 // coefficient order for the maps: SYM -> {cz, -, cx, cy}; else {aP, aW, aE, aS, aN, aB, aT}
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],

@@ -17,6 +17,11 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 
 def classify(name):
+    m = re.search(r"k_stencil_rw<(\d)", name)
+    if m:
+        return {0: "spmv", 1: "setup", 2: "K1", 3: "K2"}[int(m.group(1))] + "_pp"
+    if "k_bicg_rw" in name:
+        return "persist_pp"
     m = re.search(r"k_stencil<(\d), (\d)", name)
     if m:
         mode, sym = int(m.group(1)), int(m.group(2))

@@ -108,7 +108,7 @@ def test_bfs_multirank_equals_single(mfx, orc):
             errs.append((rank, repr(e)))
             bar.abort()
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(n)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(n)]
     for t in th:
         t.start()
     for t in th:

@@ -49,7 +49,7 @@ def dist_run(mfx, g, pr, kind, sysd, x0, tol, maxit, R):
         except Exception as e:  # pragma: no cover
             errors.append((rank, repr(e)))
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(R)]
     for t in th:
         t.start()
     for t in th:

@@ -54,7 +54,7 @@ def run_ranks(mfx, assignment, nranks, g, pr, st, outer=2):
             errors.append((rank, repr(e)))
             barrier.abort()
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(nranks)]
     for t in th:
         t.start()
     for t in th:
@@ -129,7 +129,7 @@ def test_packed_bcast_equals_grouped(mfx, orc, assignment, nranks):
         except Exception as e:  # pragma: no cover
             errors.append((rank, repr(e)))
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(nranks)]
     for t in th:
         t.start()
     for t in th:
@@ -161,7 +161,7 @@ def test_packed_state_requires_contiguous_block(mfx):
             finally:
                 ctx.close()
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(2)]
     for t in th:
         t.start()
     for t in th:

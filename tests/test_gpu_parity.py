@@ -24,9 +24,10 @@ def mfx():
     return m
 
 
-@pytest.fixture(params=["tma", "cluster", "v1", "grid"])
+@pytest.fixture(params=["tma", "cluster", "v1", "grid", "persist"])
 def solver_path(request, mfx):
-    v = {"tma": mfx.PATH_TMA, "cluster": mfx.PATH_CLUSTER, "v1": mfx.PATH_V1, "grid": mfx.PATH_GRID}[request.param]
+    v = {"tma": mfx.PATH_TMA, "cluster": mfx.PATH_CLUSTER, "v1": mfx.PATH_V1, "grid": mfx.PATH_GRID,
+         "persist": mfx.PATH_PERSIST}[request.param]
     mfx.set_option("solver_path", v)
     yield request.param
     mfx.set_option("solver_path", mfx.PATH_AUTO)

@@ -78,7 +78,7 @@ def test_time_step_multirank_identical(mfx, orc):
             errs.append((rank, repr(e)))
             bar.abort()
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(n)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(n)]
     for t in th:
         t.start()
     for t in th:

@@ -269,6 +269,7 @@ mfx_status ctx_halo_exchange(mfx_ctx *c, const double *slab, int npl, long long 
 mfx_status ctx_allgather_dd(mfx_ctx *c, const dd *mine, int K, dd *all, cudaStream_t s);
 int ctx_rank(const mfx_ctx *c);
 int ctx_nranks(const mfx_ctx *c);
+bool ctx_capturable(const mfx_ctx *c);
 void *ctx_dist_scratch(mfx_ctx *c, size_t bytes);
 
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
@@ -351,35 +352,71 @@ static mfx_status dist_solve_tma(mfx_ctx *ctx, const mfx_grid *grid, const mfx_e
     launch_count_add(3);
     static thread_local SolverScalars *pin = nullptr;
     if (!pin) MFX_CUDA_TRY(cudaMallocHost(&pin, sizeof(SolverScalars)));
+    auto iteration = [&](int par, cudaStream_t st_) -> mfx_status {
+        double *p_old = P[par], *p_new = P[par ^ 1], *v_old = V[par], *v_new = V[par ^ 1];
+        const double *h1[3] = {r, p_old, v_old};
+        cudaStream_t s = st_;
+        TRY(stencil_launch(2, true, G, h1, &Ae, rh, p_new, v_new, rh, h, part, 0.0, 0, s, 0, 1, npl + 1, 1,
+                           rank_part));
+        GATHER(1);
+        XCHG(v_new);
+        dk_fold_sigma<<<1, 32, 0, s>>>(h, all, R);
+        const double *h2[3] = {r, v_new, nullptr};
+        TRY(stencil_launch(3, true, G, h2, &Ae, nullptr, t, nullptr, nullptr, h, part, 0.0, 0, s, 0, 1, npl + 1, 0,
+                           rank_part));
+        GATHER(3);
+        dk_fold_t<<<1, 32, 0, s>>>(h, all, R);
+        TRY(k3_slab_launch(D.nloc, xe + plane, r + plane, rh + plane, p_new + plane, v_new + plane, t + plane, h,
+                           part, rank_part, s));
+        GATHER(2);
+        XCHG(r);
+        dk_fold_r<<<1, 32, 0, s>>>(h, all, R);
+        MFX_CUDA_TRY(cudaGetLastError());
+        return MFX_OK;
+    };
+    // NCCL (or a single rank): the iteration sequence is captured once per solve
+    // into a CUDA graph of DG iterations and replayed (the in-process transport
+    // synchronises host threads, so it launches directly)
+    constexpr int DG = 16;
+    cudaGraphExec_t gex = nullptr;
+    if (ctx_capturable(ctx) && maxit >= DG) {
+        cudaStream_t cs;
+        MFX_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        MFX_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        mfx_status cst = MFX_OK;
+        for (int q = 0; q < DG && cst == MFX_OK; q++) cst = iteration(q & 1, cs);
+        cudaGraph_t gr = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cs, &gr);
+        cudaStreamDestroy(cs);
+        if (cst != MFX_OK) { if (gr) cudaGraphDestroy(gr); return cst; }
+        if (e != cudaSuccess) { set_error("dist graph capture: %s", cudaGetErrorString(e)); return MFX_ERR_CUDA; }
+        e = cudaGraphInstantiate(&gex, gr, 0);
+        cudaGraphDestroy(gr);
+        if (e != cudaSuccess) { set_error("dist graph instantiate: %s", cudaGetErrorString(e)); return MFX_ERR_CUDA; }
+    }
     int launched = 0, chunk = 4;
-    while (launched < maxit) {
-        const int cnt = maxit - launched < chunk ? maxit - launched : chunk;
-        for (int q = 0; q < cnt; q++, launched++) {
-            const int par = launched & 1;
-            double *p_old = P[par], *p_new = P[par ^ 1], *v_old = V[par], *v_new = V[par ^ 1];
-            const double *h1[3] = {r, p_old, v_old};
-            TRY(stencil_launch(2, true, G, h1, &Ae, rh, p_new, v_new, rh, h, part, 0.0, 0, s, 0, 1, npl + 1, 1,
-                               rank_part));
-            GATHER(1);
-            XCHG(v_new);
-            dk_fold_sigma<<<1, 32, 0, s>>>(h, all, R);
-            const double *h2[3] = {r, v_new, nullptr};
-            TRY(stencil_launch(3, true, G, h2, &Ae, nullptr, t, nullptr, nullptr, h, part, 0.0, 0, s, 0, 1, npl + 1,
-                               0, rank_part));
-            GATHER(3);
-            dk_fold_t<<<1, 32, 0, s>>>(h, all, R);
-            TRY(k3_slab_launch(D.nloc, xe + plane, r + plane, rh + plane, p_new + plane, v_new + plane, t + plane, h,
-                               part, rank_part, s));
-            GATHER(2);
-            XCHG(r);
-            dk_fold_r<<<1, 32, 0, s>>>(h, all, R);
+    mfx_status lst = MFX_OK;
+    while (launched < maxit && lst == MFX_OK) {
+        int cnt = maxit - launched < chunk ? maxit - launched : chunk;
+        if (gex && (launched & 1) == 0)
+            for (; cnt >= DG; cnt -= DG, launched += DG) {
+                if (cudaGraphLaunch(gex, s) != cudaSuccess) { lst = MFX_ERR_CUDA; break; }
+                launch_count_add(6 * DG);
+            }
+        for (int q = 0; q < cnt && lst == MFX_OK; q++, launched++) {
+            lst = iteration(launched & 1, s);
             launch_count_add(6);
         }
-        MFX_CUDA_TRY(cudaGetLastError());
+        if (lst != MFX_OK) break;
         MFX_CUDA_TRY(cudaMemcpyAsync(pin, &h->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
         MFX_CUDA_TRY(cudaStreamSynchronize(s));
         if (pin->done) break;
         chunk = chunk * 2 > 64 ? 64 : chunk * 2;
+    }
+    if (gex) cudaGraphExecDestroy(gex);
+    if (lst != MFX_OK) {
+        if (lst == MFX_ERR_CUDA) set_error("dist solve: %s", cudaGetErrorString(cudaGetLastError()));
+        return lst;
     }
 #undef XCHG
 #undef GATHER

@@ -608,6 +608,9 @@ int ctx_rank(const mfx_ctx *c) { return c->dist_sub ? c->prank : c->rank; }
 int ctx_nranks(const mfx_ctx *c) { return c->dist_sub ? c->asg.n_p : c->nranks; }
 static ncclComm_t ctx_comm(const mfx_ctx *c) { return c->dist_sub ? c->pcomm : c->comm; }
 static mfx_local_group *ctx_group(const mfx_ctx *c) { return c->dist_sub ? c->pgroup : c->group; }
+// the distributed solver may capture its iterations in a CUDA graph: NCCL (or
+// one rank), not the in-process transport, whose phases synchronise host threads
+bool ctx_capturable(const mfx_ctx *c) { return ctx_nranks(c) == 1 || !ctx_group(c); }
 
 void *ctx_dist_scratch(mfx_ctx *c, size_t bytes)
 {

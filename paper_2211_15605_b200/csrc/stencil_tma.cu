@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -537,7 +538,7 @@ __device__ __forceinline__ void rw_produce(const TmaMaps &M, const StencilArgs &
 // consumer warps of a row-warp pass (MODE) over this CTA's units; q is the
 // ring position shared with rw_produce, carried across passes of a persistent
 // kernel; stage slots are STRIDE bytes apart.  acc[d][m]: dot d, owned cell m.
-template <int MODE, int CPT, int S, int STRIDE>
+template <int MODE, int CPT, int S, int STRIDE, bool ONEACC = false>
 __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, double beta, double omega, bool rst,
                                            Acc (&acc)[3][CPT], const uint8_t *stages, uint64_t *full,
                                            uint64_t *empty, int &q)
@@ -659,8 +660,8 @@ __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, d
 #pragma unroll
                     for (int m = 0; m < CPT; m++) {
                         rv[m] = kex[m] - y[m];
-                        acc[0][m].prod(kex[m], kex[m]);
-                        acc[ND > 1 ? 1 : 0][m].prod(rv[m], rv[m]);
+                        acc[0][ONEACC ? 0 : m].prod(kex[m], kex[m]);
+                        acc[ND > 1 ? 1 : 0][ONEACC ? 0 : m].prod(rv[m], rv[m]);
                     }
                     store_cells<CPT>(a.out0 + n, rv);
                 } else if (MODE == SM_K1) {
@@ -668,14 +669,14 @@ __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, d
                     store_cells<CPT>(a.out1 + n, y);
                     if (rst) store_cells<CPT>(a.out2 + n, kex);
 #pragma unroll
-                    for (int m = 0; m < CPT; m++) acc[0][m].prod(kex[m], y[m]);
+                    for (int m = 0; m < CPT; m++) acc[0][ONEACC ? 0 : m].prod(kex[m], y[m]);
                 } else {
                     store_cells<CPT>(a.out0 + n, y);
 #pragma unroll
                     for (int m = 0; m < CPT; m++) {
-                        acc[0][m].prod(y[m], xc[m]);
-                        acc[ND > 1 ? 1 : 0][m].prod(y[m], y[m]);
-                        acc[ND > 2 ? 2 : 0][m].prod(xc[m], xc[m]);
+                        acc[0][ONEACC ? 0 : m].prod(y[m], xc[m]);
+                        acc[ND > 1 ? 1 : 0][ONEACC ? 0 : m].prod(y[m], y[m]);
+                        acc[ND > 2 ? 2 : 0][ONEACC ? 0 : m].prod(xc[m], xc[m]);
                     }
                 }
             }
@@ -726,8 +727,8 @@ __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, d
     }
 }
 
-template <int MODE, int CPT, int S>
-__global__ void __launch_bounds__(8 * 32 + 32, 2) k_stencil_rw(const __grid_constant__ TmaMaps M, StencilArgs a)
+template <int MODE, int CPT, int S, int MB>
+__global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_constant__ TmaMaps M, StencilArgs a)
 {
     constexpr int TX = 32 * CPT, TY = 8;
     using C = Cfg<MODE, true, TX, TY, CPT>;
@@ -787,7 +788,8 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_stencil_rw(const __grid_cons
             rw_produce<MODE, CPT, S, C::STAGE_B>(M, a, stages, full, empty, q);
         }
     } else {
-        rw_consume<MODE, CPT, S, C::STAGE_B>(a, alpha, beta, omega, rst, acc, stages, full, empty, q);
+        // MB = 3 CTAs per SM: one accumulator per dot (registers)
+        rw_consume<MODE, CPT, S, C::STAGE_B, (MB >= 3)>(a, alpha, beta, omega, rst, acc, stages, full, empty, q);
     }
 
     if constexpr (C::NDOT > 0) {
@@ -831,7 +833,17 @@ struct PersistArgs {
     dd *part;                      // 2 x gridDim.x x 3 (double-buffered by phase parity)
     unsigned *arrive;              // monotone arrival counter, zero at launch
     int maxit;
+    unsigned long long *trace;     // optional (MFX_PERSIST_TRACE): %globaltimer stamps of CTA 0, 8 per iteration
 };
+
+__device__ __forceinline__ void ptrace(const PersistArgs &P, int it, int slot)
+{
+    if (P.trace && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[it * 8 + slot] = t;
+    }
+}
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p)
 {
@@ -929,6 +941,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
         }
         const int par = it & 1;
         dd out[3];
+        ptrace(P, it, 0);
         // ---- K1: p = r + beta (p - omega v) on the halo'd planes, v = A p, <r^, v>
 #pragma unroll
         for (int d = 0; d < 3; d++)
@@ -942,7 +955,9 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
         } else {
             rw_consume<SM_K1, CPT, S, STRIDE>(P.a1[par], 0.0, P1.beta, P1.omega, P1.rst, acc, stages, full, empty, q);
         }
+        ptrace(P, it, 1);
         grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out);
+        ptrace(P, it, 2);
         if (tid == 0) bicg_k1_tail(Ls, P1, dd_round(out[0]));
         __syncthreads();
         if (Ls.done || Ls.skip) continue;
@@ -960,7 +975,9 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
         } else {
             rw_consume<SM_K2, CPT, S, STRIDE>(P.a2[par], alpha, 0.0, 0.0, false, acc, stages, full, empty, q);
         }
+        ptrace(P, it, 3);
         grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out);
+        ptrace(P, it, 4);
         if (tid == 0) bicg_k2_tail(Ls, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
         __syncthreads();
         if (Ls.done || Ls.skip) continue;
@@ -981,43 +998,58 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
                 const int gx = (tile - ty * a.tiles_x) * TX + lane * CPT, gy = ty * TY + warp;
                 if (gx >= a.nx || gy >= a.ny) continue;
                 const int k0 = a.kbeg + chunk * a.Lz, k1 = k0 + a.Lz < a.kend ? k0 + a.Lz : a.kend;
-                for (int k = k0; k < k1; k++) {
-                    const long long e = (long long)gx + (long long)a.nx * ((long long)gy + (long long)a.ny * k);
-                    double xv[CPT], rv[CPT], rhv[CPT], pv[CPT], vv[CPT], tv[CPT];
-                    if (CPT == 2) {
-                        auto ld2 = [&](const double *b, double (&o)[CPT]) {
-                            const double2 w = __ldcg((const double2 *)(b + e));
-                            o[0] = w.x; o[CPT - 1] = w.y;
-                        };
-                        ld2(P.x, xv); ld2(P.r, rv); ld2(P.rh, rhv); ld2(pn, pv); ld2(vn, vv);
-                        if (!half) ld2(P.t, tv);
-                        else tv[0] = tv[CPT - 1] = 0.0;
-                    } else {
-                        xv[0] = __ldcg(P.x + e); rv[0] = __ldcg(P.r + e); rhv[0] = __ldcg(P.rh + e);
-                        pv[0] = __ldcg(pn + e); vv[0] = __ldcg(vn + e); tv[0] = half ? 0.0 : __ldcg(P.t + e);
+                const long long pl = (long long)a.nx * a.ny;
+                const long long e0 = (long long)gx + (long long)a.nx * gy;
+                // KU planes per step, every load of the step issued before any use
+                constexpr int KU = 1;
+                for (int kb = k0; kb < k1; kb += KU) {
+                    double xv[KU][CPT], rv[KU][CPT], rhv[KU][CPT], pv[KU][CPT], vv[KU][CPT], tv[KU][CPT];
+#pragma unroll
+                    for (int j = 0; j < KU; j++) {
+                        if (kb + j >= k1) continue;
+                        const long long e = e0 + pl * (kb + j);
+                        if (CPT == 2) {
+                            auto ld2 = [&](const double *b_, double (&o)[CPT]) {
+                                const double2 w = __ldcg((const double2 *)(b_ + e));
+                                o[0] = w.x; o[CPT - 1] = w.y;
+                            };
+                            ld2(P.x, xv[j]); ld2(P.r, rv[j]); ld2(P.rh, rhv[j]); ld2(pn, pv[j]); ld2(vn, vv[j]);
+                            if (!half) ld2(P.t, tv[j]);
+                            else tv[j][0] = tv[j][CPT - 1] = 0.0;
+                        } else {
+                            xv[j][0] = __ldcg(P.x + e); rv[j][0] = __ldcg(P.r + e); rhv[j][0] = __ldcg(P.rh + e);
+                            pv[j][0] = __ldcg(pn + e); vv[j][0] = __ldcg(vn + e); tv[j][0] = half ? 0.0 : __ldcg(P.t + e);
+                        }
                     }
 #pragma unroll
-                    for (int m = 0; m < CPT; m++) {
-                        const double sv = fma(-al, vv[m], rv[m]);
-                        double xo, ro;
-                        if (half) {
-                            xo = fma(al, pv[m], xv[m]);
-                            ro = sv;
-                        } else {
-                            xo = fma(om, sv, fma(al, pv[m], xv[m]));
-                            ro = fma(-om, tv[m], sv);
+                    for (int j = 0; j < KU; j++) {
+                        if (kb + j >= k1) continue;
+                        const long long e = e0 + pl * (kb + j);
+#pragma unroll
+                        for (int m = 0; m < CPT; m++) {
+                            const double sv = fma(-al, vv[j][m], rv[j][m]);
+                            double xo, ro;
+                            if (half) {
+                                xo = fma(al, pv[j][m], xv[j][m]);
+                                ro = sv;
+                            } else {
+                                xo = fma(om, sv, fma(al, pv[j][m], xv[j][m]));
+                                ro = fma(-om, tv[j][m], sv);
+                            }
+                            xv[j][m] = xo;
+                            rv[j][m] = ro;
+                            acc[0][m].prod(rhv[j][m], ro);
+                            acc[1][m].prod(ro, ro);
                         }
-                        xv[m] = xo;
-                        rv[m] = ro;
-                        acc[0][m].prod(rhv[m], ro);
-                        acc[1][m].prod(ro, ro);
+                        store_cells<CPT>(P.x + e, xv[j]);
+                        store_cells<CPT>(P.r + e, rv[j]);
                     }
-                    store_cells<CPT>(P.x + e, xv);
-                    store_cells<CPT>(P.r + e, rv);
                 }
             }
         }
+        ptrace(P, it, 5);
         grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out);
+        ptrace(P, it, 6);
         if (tid == 0) bicg_k3_tail(Ls, half, dd_round(out[0]), dd_round(out[1]));
         __syncthreads();
     }
@@ -1081,11 +1113,11 @@ int choose_lz(long long ntiles, int nz, int grid)
     return best;
 }
 
-template <int MODE, bool SYM, int TX, int TY, int CPT_, int S, bool RW = false>
+template <int MODE, bool SYM, int TX, int TY, int CPT_, int S, bool RW = false, int MB = 2>
 struct Launcher {
     using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     static constexpr void (*kern)(const TmaMaps, StencilArgs) =
-        RW ? k_stencil_rw<MODE, CPT_, S> : k_stencil<MODE, SYM, TX, TY, CPT_, S>;
+        RW ? k_stencil_rw<MODE, CPT_, S, MB> : k_stencil<MODE, SYM, TX, TY, CPT_, S>;
     static constexpr size_t smem() { return RW ? (size_t)S * C::STAGE_B + 16 * (size_t)S : smem_bytes<C>(S); }
     static int grid_size()
     {
@@ -1168,13 +1200,23 @@ mfx_status run_rw(const Geo &G, const double *const halo[3], const double *const
                   const StencilArgs &a, cudaStream_t s)
 {
     static const int st = env_int("MFX_RW_STAGES", 0);
-    const int S = st ? st : 4;
+    static const int mb = env_int("MFX_RW_MB", 2);
     if (G.nx <= 32) {
-        if (S == 3) return Launcher<MODE, true, 32, 8, 1, 3, true>::run(G, halo, coef, extra, a, s);
+        if ((st ? st : 4) == 3) return Launcher<MODE, true, 32, 8, 1, 3, true>::run(G, halo, coef, extra, a, s);
         return Launcher<MODE, true, 32, 8, 1, 4, true>::run(G, halo, coef, extra, a, s);
     }
+    if (mb == 1) {   // one CTA per SM with a deep ring (prefetch depth S - 1)
+        constexpr bool BIG = Cfg<MODE, true, 64, 8, 2>::STAGE_B > 25000;
+        if (BIG) return Launcher<MODE, true, 64, 8, 2, 6, true, 1>::run(G, halo, coef, extra, a, s);
+        return Launcher<MODE, true, 64, 8, 2, 8, true, 1>::run(G, halo, coef, extra, a, s);
+    }
+    if (mb == 3) {   // three CTAs per SM: stages must fit 227 KB / 3
+        constexpr bool BIG = Cfg<MODE, true, 64, 8, 2>::STAGE_B > 25000;
+        if (BIG || st == 2) return Launcher<MODE, true, 64, 8, 2, 2, true, 3>::run(G, halo, coef, extra, a, s);
+        return Launcher<MODE, true, 64, 8, 2, 3, true, 3>::run(G, halo, coef, extra, a, s);
+    }
+    const int S = st ? st : 4;
     if (S == 3) return Launcher<MODE, true, 64, 8, 2, 3, true>::run(G, halo, coef, extra, a, s);
-    if (S == 6) return Launcher<MODE, true, 64, 8, 2, 6, true>::run(G, halo, coef, extra, a, s);
     return Launcher<MODE, true, 64, 8, 2, 4, true>::run(G, halo, coef, extra, a, s);
 }
 
@@ -1272,7 +1314,30 @@ struct PersistLauncher {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        static const int tr = env_int("MFX_PERSIST_TRACE", 0);
+        if (tr) {
+            MFX_CUDA_TRY(cudaMalloc(&P.trace, 64 * 8 * sizeof(unsigned long long)));
+            MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, 64 * 8 * sizeof(unsigned long long), s));
+        }
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
+        if (tr) {
+            unsigned long long h[64 * 8];
+            MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, s));
+            MFX_CUDA_TRY(cudaStreamSynchronize(s));
+            cudaFree(P.trace);
+            double acc[7] = {0};
+            int n = 0;
+            for (int it = 2; it < 64 && h[it * 8 + 6] && h[(it + 1) * 8]; it++, n++) {
+                const unsigned long long *t = h + it * 8;
+                for (int k = 0; k < 6; k++) acc[k] += 1e-3 * (double)(t[k + 1] - t[k]);
+                acc[6] += 1e-3 * (double)(h[(it + 1) * 8] - t[6]);
+            }
+            if (n)
+                fprintf(stderr, "persist trace (CTA 0, %d iters, us): K1 pass %.2f  allreduce %.2f  K2 pass %.2f  "
+                        "allreduce %.2f  K3 pass %.2f  allreduce %.2f  loop %.2f  grid %d units %lld Lz %d\n",
+                        n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, grid,
+                        a.units, a.Lz);
+        }
         return MFX_OK;
     }
 };

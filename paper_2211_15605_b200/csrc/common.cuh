@@ -135,33 +135,41 @@ __device__ __forceinline__ dd shfl_dd(dd v, int off)
 
 // Block reduction of K double-doubles in a fixed order; result valid in
 // thread 0.  `sh` needs (blockDim/32) * K dd slots.  All threads must call.
+// Two butterfly levels (lanes, then warps), the K chains advancing level by
+// level so they interleave, with Dekker's double-double add: its error
+// ~u^2 (|x| + |y|) per add keeps the total in the O(depth u^2 sum|terms|)
+// class of DESIGN.md §3.1.  (The linear fold of the warp partials by one
+// thread, and the K chains one after another, put ~K (32 + NW) dependent
+// double-double adds on the tail of every dot kernel.)
+template <int K>
+__device__ __forceinline__ void butterfly_dd(dd (&x)[K])
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dd y[K];
+#pragma unroll
+        for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+        for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void block_reduce_dd(dd (&v)[K], dd *sh)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int q = 0; q < K; q++) {
-        dd x = v[q];
-        // fixed butterfly: lane 0 ends with ((0+16)+(8..))... deterministic
-        for (int off = 16; off > 0; off >>= 1) {
-            dd y = shfl_dd(x, off);
-            x = (lane & off) ? dd_add(y, x) : dd_add(x, y);
-        }
-        v[q] = x;
-    }
+    butterfly_dd<K>(v);
     __syncthreads();
     if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < K; q++) sh[wid * K + q] = v[q];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (wid == 0) {
 #pragma unroll
-        for (int q = 0; q < K; q++) {
-            dd x = sh[q];
-            for (int w = 1; w < nw; w++) x = dd_add(x, sh[w * K + q]);
-            v[q] = x;
-        }
+        for (int q = 0; q < K; q++) v[q] = lane < nw ? sh[lane * K + q] : dd{0.0, 0.0};
+        butterfly_dd<K>(v);
     }
     __syncthreads();
 }

@@ -838,10 +838,17 @@ struct PersistArgs {
 
 __device__ __forceinline__ void ptrace(const PersistArgs &P, int it, int slot)
 {
-    if (P.trace && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) {
+    if (P.trace && threadIdx.x == 0 && it < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        P.trace[it * 8 + slot] = t;
+        if (blockIdx.x == 0) P.trace[it * 8 + slot] = t;
+        // every CTA: iteration 5's stamps + SM id (load balance across CTAs)
+        if (it == 5) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            P.trace[512 + blockIdx.x * 8 + slot] = t;
+            P.trace[512 + blockIdx.x * 8 + 7] = sm;
+        }
     }
 }
 
@@ -1315,14 +1322,15 @@ struct PersistLauncher {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         static const int tr = env_int("MFX_PERSIST_TRACE", 0);
+        const size_t trn = 512 + (size_t)grid * 8;
         if (tr) {
-            MFX_CUDA_TRY(cudaMalloc(&P.trace, 64 * 8 * sizeof(unsigned long long)));
-            MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, 64 * 8 * sizeof(unsigned long long), s));
+            MFX_CUDA_TRY(cudaMalloc(&P.trace, trn * sizeof(unsigned long long)));
+            MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, trn * sizeof(unsigned long long), s));
         }
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
         if (tr) {
-            unsigned long long h[64 * 8];
-            MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, s));
+            static unsigned long long h[512 + 8 * 2048];
+            MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, trn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             MFX_CUDA_TRY(cudaStreamSynchronize(s));
             cudaFree(P.trace);
             double acc[7] = {0};
@@ -1337,6 +1345,28 @@ struct PersistLauncher {
                         "allreduce %.2f  K3 pass %.2f  allreduce %.2f  loop %.2f  grid %d units %lld Lz %d\n",
                         n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, grid,
                         a.units, a.Lz);
+            // iteration 5 across CTAs: pass durations and arrival spread per phase
+            {
+                const unsigned long long *c = h + 512;
+                double mn[3] = {1e30, 1e30, 1e30}, mx[3] = {0, 0, 0}, sum[3] = {0, 0, 0};
+                unsigned long long amin[3] = {~0ull, ~0ull, ~0ull}, amax[3] = {0, 0, 0};
+                int slow[3] = {0, 0, 0};
+                const int ps[3][2] = {{0, 1}, {2, 3}, {4, 5}};
+                for (int b = 0; b < grid; b++)
+                    for (int k = 0; k < 3; k++) {
+                        const double d = 1e-3 * (double)(c[b * 8 + ps[k][1]] - c[b * 8 + ps[k][0]]);
+                        if (d < mn[k]) mn[k] = d;
+                        if (d > mx[k]) { mx[k] = d; slow[k] = b; }
+                        sum[k] += d;
+                        const unsigned long long ar = c[b * 8 + ps[k][1]];
+                        if (ar < amin[k]) amin[k] = ar;
+                        if (ar > amax[k]) amax[k] = ar;
+                    }
+                for (int k = 0; k < 3; k++)
+                    fprintf(stderr, "  iter 5 %s pass over %d CTAs: min %.2f mean %.2f max %.2f us (slowest CTA %d on SM %llu); "
+                            "arrival spread %.2f us\n", k == 0 ? "K1" : (k == 1 ? "K2" : "K3"), grid, mn[k],
+                            sum[k] / grid, mx[k], slow[k], c[slow[k] * 8 + 7], 1e-3 * (double)(amax[k] - amin[k]));
+            }
         }
         return MFX_OK;
     }

@@ -15,7 +15,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libmfx.so")
+_SO = os.environ.get("MFX_SO_VARIANT") or os.path.join(_HERE, "libmfx.so")   # variant: A/B builds only
 if not os.path.exists(_SO):
     raise ImportError(f"{_SO} is not built: run `python paper_2211_15605_b200/build.py` "
                       "(there is no CPU fallback)")

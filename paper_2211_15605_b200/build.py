@@ -27,7 +27,7 @@ FLAGS = [
     "-shared", "-cudart", "static",
     "-I" + os.path.join(ROOT, "include"),
     "-I/usr/include",
-]
+] + os.environ.get("MFX_EXTRA_NVCC_FLAGS", "").split()
 
 
 def sources():

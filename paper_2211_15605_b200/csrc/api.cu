@@ -26,7 +26,7 @@ void set_error(const char *fmt, ...)
 // ------------------------------------------------------------------ workspace
 static size_t r256(size_t b) { return (b + 255) & ~(size_t)255; }
 size_t ws_header_bytes() { return r256(sizeof(WsHeader)); }
-static size_t ws_part_bytes() { return r256(sizeof(dd) * kMaxBlocks * kMaxDots); }
+static size_t ws_part_bytes() { return r256(sizeof(dd) * kPartCap); }
 size_t ws_total_bytes(long long N) { return ws_header_bytes() + ws_part_bytes() + 7 * r256(sizeof(double) * N); }
 
 bool ws_view(void *ws, size_t bytes, long long N, bool need_vectors, WsView &W)

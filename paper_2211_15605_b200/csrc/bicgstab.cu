@@ -833,15 +833,17 @@ static bool grid_solver_fits(const Geo &G, bool sym)
     return budget > 0 && bytes <= budget && !cluster_fits(G, sym);
 }
 
-// persistent row-warp solver (path 5) in auto mode: MFX_PERSIST_MB sets the
-// largest p' working set (3 coefficients + b + 8 vectors) it is chosen for;
-// 0 (default until measured) never.
+// persistent row-warp solver (path 5) in auto mode: chosen when the p'
+// working set (3 coefficients + b + 8 vectors) fits 112 MiB, i.e. lives in the
+// 126 MB L2 (configuration 3: 50 vs 57 us per iteration on B200, r02; at
+// configuration 2 the per-launch kernels are faster, 265 vs 284 us).
+// MFX_PERSIST_MB overrides the budget (0: never).
 static bool persist_fits(const Geo &G)
 {
     static long long budget = -1;
     if (budget < 0) {
         const char *e = getenv("MFX_PERSIST_MB");
-        budget = (e ? atoll(e) : 0) << 20;
+        budget = (e ? atoll(e) : 112) << 20;
     }
     return budget > 0 && (long long)(3 + 1 + 8) * 8 * G.N <= budget && !cluster_fits(G, true);
 }

@@ -59,6 +59,11 @@ inline Geo make_geo(const mfx_grid &g)
 // accumulation of exact products, then an accurate double-double tree.
 struct dd { double hi, lo; };
 
+constexpr int kMaxBlocks = 2048;
+constexpr int kMaxDots = 4;
+constexpr int kPartCap = kMaxBlocks * kMaxDots * 8;   // dd slots of the partials buffer (warp partials)
+
+
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e)
 {
     s = a + b;
@@ -134,24 +139,21 @@ __device__ __forceinline__ dd shfl_dd(dd v, int off)
 }
 
 // Block reduction of K double-doubles in a fixed order; result valid in
-// thread 0.  `sh` needs (blockDim/32) * K dd slots.  All threads must call.
-// Two butterfly levels (lanes, then warps), the K chains advancing level by
-// level so they interleave, with Dekker's double-double add: its error
-// ~u^2 (|x| + |y|) per add keeps the total in the O(depth u^2 sum|terms|)
-// class of DESIGN.md §3.1.  (The linear fold of the warp partials by one
-// thread, and the K chains one after another, put ~K (32 + NW) dependent
-// double-double adds on the tail of every dot kernel.)
-template <int K>
-__device__ __forceinline__ void butterfly_dd(dd (&x)[K])
+// thread 0.  `sh` needs (blockDim/32) + K dd slots.  All threads must call.
+// Per value: a lane butterfly, then one warp's butterfly over the warp
+// partials, with Dekker's double-double add (error ~u^2 (|x| + |y|) per add:
+// the O(depth u^2 sum|terms|) class of DESIGN.md §3.1).  The K values are
+// reduced one after another: interleaving the K chains inside the dot
+// kernels' tails measured slower (K = 3: 9.5 vs 6.4 us for the K2 tail on
+// B200, register pressure), and so was the earlier linear fold of the warp
+// partials by one thread.
+__device__ __forceinline__ void butterfly_dd1(dd &x)
 {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        dd y[K];
-#pragma unroll
-        for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
-#pragma unroll
-        for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
+        const dd y = shfl_dd(x, off);
+        x = (lane & off) ? dd_add_fast(y, x) : dd_add_fast(x, y);
     }
 }
 
@@ -159,17 +161,18 @@ template <int K>
 __device__ __forceinline__ void block_reduce_dd(dd (&v)[K], dd *sh)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    butterfly_dd<K>(v);
-    __syncthreads();
-    if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < K; q++) sh[wid * K + q] = v[q];
-    }
-    __syncthreads();
-    if (wid == 0) {
-#pragma unroll
-        for (int q = 0; q < K; q++) v[q] = lane < nw ? sh[lane * K + q] : dd{0.0, 0.0};
-        butterfly_dd<K>(v);
+    for (int q = 0; q < K; q++) {
+        dd x = v[q];
+        butterfly_dd1(x);
+        __syncthreads();   // the previous value's readers of sh are done
+        if (lane == 0) sh[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            x = lane < nw ? sh[lane] : dd{0.0, 0.0};
+            butterfly_dd1(x);
+            v[q] = x;
+        }
     }
     __syncthreads();
 }
@@ -177,7 +180,9 @@ __device__ __forceinline__ void block_reduce_dd(dd (&v)[K], dd *sh)
 // Deterministic grid reduction: each block writes K partials to part[blk*K+q];
 // the last block to finish (ticket) folds them in block order with all its
 // threads (strided sequential fold, then a fixed block tree) and returns true
-// in every thread of that block, with out[q] valid in thread 0.
+// in every thread of that block, with out[q] valid in thread 0.  (Publishing
+// warp partials instead, to keep one block reduction off the tail, measured
+// slower: the last block's fold over 9x more partials costs more.)
 template <int K>
 __device__ __forceinline__ bool grid_reduce_dd(dd (&v)[K], dd *part, unsigned int *ticket, dd *sh,
                                                dd (&out)[K])
@@ -238,12 +243,10 @@ struct WsHeader {
     double pad[4];
 };
 
-constexpr int kMaxBlocks = 2048;
-constexpr int kMaxDots = 4;
 
 struct WsView {
     WsHeader *hdr;
-    dd *part;                 // kMaxBlocks * kMaxDots
+    dd *part;                 // kPartCap
     double *r, *rh, *p[2], *v[2], *t;
 };
 

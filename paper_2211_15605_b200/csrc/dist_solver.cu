@@ -304,7 +304,7 @@ static mfx_status dist_solve_tma(mfx_ctx *ctx, const mfx_grid *grid, const mfx_e
     D.plane = plane;
     D.nloc = plane * npl;
     auto r256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t hdr = r256(sizeof(WsHeader)), partb = r256(sizeof(dd) * kMaxBlocks * kMaxDots);
+    const size_t hdr = r256(sizeof(WsHeader)), partb = r256(sizeof(dd) * kPartCap);
     const size_t rpb = r256(sizeof(dd) * 4), apb = r256(sizeof(dd) * 4 * 64);
     const size_t eb = r256(sizeof(double) * (size_t)(plane * ne));
     constexpr int NV = 12;   // r rh p0 p1 v0 v1 t | x b | cx cy cz
@@ -455,7 +455,7 @@ mfx_status dist_solve(mfx_ctx *ctx, int kind, const mfx_grid *grid, const mfx_eq
     D.nloc = D.plane * D.npl;
     // scratch: header | block partials | rank part | all parts | r rh p v s t | hb ha czb
     auto r256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t hdr = r256(sizeof(WsHeader)), partb = r256(sizeof(dd) * kMaxBlocks * kMaxDots);
+    const size_t hdr = r256(sizeof(WsHeader)), partb = r256(sizeof(dd) * kPartCap);
     const size_t rpb = r256(sizeof(dd) * 4), apb = r256(sizeof(dd) * 4 * 64);
     const size_t vb = r256(sizeof(double) * D.nloc), pb = r256(sizeof(double) * D.plane);
     const size_t total = hdr + partb + rpb + apb + 6 * vb + 3 * pb;

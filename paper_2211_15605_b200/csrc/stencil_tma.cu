@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -60,11 +61,28 @@ struct StencilArgs {
     // ghost planes (the next iteration's p_old there, bitwise the neighbour's).
     int kbeg, kend, ghost_store;
     dd *rank_part;
+    unsigned long long *trace;             // optional (MFX_RW_TRACE): per-CTA %globaltimer stamps
 };
+
+__device__ __forceinline__ void ktrace(const StencilArgs &a, int slot)
+{
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[blockIdx.x * 4 + slot] = t;
+    }
+}
 
 namespace {
 
 constexpr int r128(int b) { return (b + 127) & ~127; }
+
+int env_int(const char *name, int dflt)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 
 template <int CPT>
 __device__ __forceinline__ void store_cells(double *dst, const double (&v)[CPT])
@@ -750,6 +768,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
     }
     __syncthreads();
     pdl_wait();
+    ktrace(a, 0);
 
     double beta = 0.0, omega = 0.0, alpha = 0.0;
     bool rst = false;
@@ -792,6 +811,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
         rw_consume<MODE, CPT, S, C::STAGE_B, (MB >= 3)>(a, alpha, beta, omega, rst, acc, stages, full, empty, q);
     }
 
+    ktrace(a, 1);
     if constexpr (C::NDOT > 0) {
         __shared__ dd sh[(C::NW + 1) * ND];
         dd v[ND], out[ND];
@@ -801,7 +821,9 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
 #pragma unroll
             for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
         }
-        if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+        const bool last = grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out);
+        ktrace(a, last ? 3 : 2);
+        if (!last || tid != 0) return;
         if (a.rank_part) {
 #pragma unroll
             for (int d = 0; d < ND; d++) a.rank_part[d] = out[d];
@@ -841,13 +863,13 @@ __device__ __forceinline__ void ptrace(const PersistArgs &P, int it, int slot)
     if (P.trace && threadIdx.x == 0 && it < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (blockIdx.x == 0) P.trace[it * 8 + slot] = t;
+        if (blockIdx.x == 0) P.trace[it * 16 + slot] = t;
         // every CTA: iteration 5's stamps + SM id (load balance across CTAs)
         if (it == 5) {
             unsigned sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            P.trace[512 + blockIdx.x * 8 + slot] = t;
-            P.trace[512 + blockIdx.x * 8 + 7] = sm;
+            P.trace[1024 + blockIdx.x * 16 + slot] = t;
+            P.trace[1024 + blockIdx.x * 16 + 15] = sm;
         }
     }
 }
@@ -862,7 +884,7 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p)
 // all-reduce of K double-doubles over the grid; out valid in thread 0
 template <int K, int CPT>
 __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *part, unsigned *arrive, unsigned &phase,
-                                               dd *sh, dd (&out)[K])
+                                               dd *sh, dd (&out)[K], const PersistArgs &P, int it, int slot)
 {
     dd v[K];
 #pragma unroll
@@ -871,9 +893,12 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
 #pragma unroll
         for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");   // this thread's generic stores vs later TMA reads
+    // this thread's generic stores vs the next passes' TMA (async-proxy) reads; K2's
+    // output t is read back only by generic loads (K3), so it needs none
+    if (K != 3) asm volatile("fence.proxy.async.global;" ::: "memory");
     block_reduce_dd<K>(v, sh);                                  // (syncs the CTA: every store precedes the arrival)
     dd *pb = part + (size_t)(phase & 1) * gridDim.x * 3;
+    ptrace(P, it, slot);        // every warp of the CTA done with the pass
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int d = 0; d < K; d++) pb[(size_t)blockIdx.x * 3 + d] = v[d];
@@ -884,6 +909,7 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
             unsigned long long t0;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
             while (ld_acquire_u32(arrive) < target) {
+                __nanosleep(40);   // back off: ~300 spinning CTAs on one L2 line delay the arrivals
                 unsigned long long t1;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
                 if (t1 - t0 > 20000000000ull) __trap();   // 20 s: a CTA is missing (never expected)
@@ -891,6 +917,7 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
         }
     }
     phase++;
+    ptrace(P, it, slot + 1);    // released
     __syncthreads();
     dd f[K];
 #pragma unroll
@@ -963,8 +990,8 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
             rw_consume<SM_K1, CPT, S, STRIDE>(P.a1[par], 0.0, P1.beta, P1.omega, P1.rst, acc, stages, full, empty, q);
         }
         ptrace(P, it, 1);
-        grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out);
-        ptrace(P, it, 2);
+        grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out, P, it, 2);
+        ptrace(P, it, 4);
         if (tid == 0) bicg_k1_tail(Ls, P1, dd_round(out[0]));
         __syncthreads();
         if (Ls.done || Ls.skip) continue;
@@ -982,9 +1009,9 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
         } else {
             rw_consume<SM_K2, CPT, S, STRIDE>(P.a2[par], alpha, 0.0, 0.0, false, acc, stages, full, empty, q);
         }
-        ptrace(P, it, 3);
-        grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out);
-        ptrace(P, it, 4);
+        ptrace(P, it, 5);
+        grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out, P, it, 6);
+        ptrace(P, it, 8);
         if (tid == 0) bicg_k2_tail(Ls, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
         __syncthreads();
         if (Ls.done || Ls.skip) continue;
@@ -1054,9 +1081,9 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
                 }
             }
         }
-        ptrace(P, it, 5);
-        grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out);
-        ptrace(P, it, 6);
+        ptrace(P, it, 9);
+        grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out, P, it, 10);
+        ptrace(P, it, 12);
         if (tid == 0) bicg_k3_tail(Ls, half, dd_round(out[0]), dd_round(out[1]));
         __syncthreads();
     }
@@ -1177,17 +1204,40 @@ struct Launcher {
         attr[0].val.programmaticStreamSerializationAllowed = opt_pdl() ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        static const int tr = env_int("MFX_RW_TRACE", 0);
+        static int traced = 0;
+        if (RW && tr && traced < 40) {
+            MFX_CUDA_TRY(cudaMalloc(&a.trace, (size_t)grid * 4 * sizeof(unsigned long long)));
+            MFX_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)grid * 4 * sizeof(unsigned long long), s));
+        }
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, M, a));
+        if (a.trace) {
+            traced++;
+            std::vector<unsigned long long> h((size_t)grid * 4);
+            MFX_CUDA_TRY(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            MFX_CUDA_TRY(cudaStreamSynchronize(s));
+            cudaFree(a.trace);
+            unsigned long long t0 = ~0ull, tend = 0, tlast = 0, tpass_max = 0;
+            double pass_sum = 0, pass_min = 1e30, pass_max = 0;
+            for (int b = 0; b < grid; b++) {
+                const unsigned long long *c = &h[(size_t)b * 4];
+                if (c[0] < t0) t0 = c[0];
+                if (c[1] > tpass_max) tpass_max = c[1];
+                const double d = 1e-3 * (double)(c[1] - c[0]);
+                pass_sum += d; if (d < pass_min) pass_min = d; if (d > pass_max) pass_max = d;
+                if (c[2] > tend) tend = c[2];
+                if (c[3]) tlast = c[3];
+            }
+            if (traced > 3)
+                fprintf(stderr, "rw trace mode %d: first start -> last pass end %.2f us; pass per CTA min %.2f mean %.2f "
+                        "max %.2f us; last pass end -> last CTA folded %.2f us\n", MODE, 1e-3 * (double)(tpass_max - t0),
+                        pass_min, pass_sum / grid, pass_max, tlast ? 1e-3 * (double)(tlast - tpass_max) : -1.0);
+        }
         return MFX_OK;
     }
 };
 
 // MFX_TILE=32x8 / 64x4 and MFX_STAGES=3/4/6 override the defaults (tuning).
-int env_int(const char *name, int dflt)
-{
-    const char *e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
 
 template <int MODE, bool SYM, int TX, int TY, int CPT_>
 mfx_status run_tile(const Geo &G, const double *const halo[3], const double *const coef[7], const double *extra,
@@ -1227,9 +1277,11 @@ mfx_status run_rw(const Geo &G, const double *const halo[3], const double *const
     return Launcher<MODE, true, 64, 8, 2, 4, true>::run(G, halo, coef, extra, a, s);
 }
 
+// default: the row-warp kernel for p' K2 only (B200, r02: K2 82 vs 84-86 us at
+// c2, 23 vs 27 us at c3; the row-warp K1, apply and setup are not faster)
 int rw_mask()
 {
-    static const int m = env_int("MFX_RW", 0);
+    static const int m = env_int("MFX_RW", 1 << SM_K2);
     return m;
 }
 
@@ -1322,51 +1374,49 @@ struct PersistLauncher {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         static const int tr = env_int("MFX_PERSIST_TRACE", 0);
-        const size_t trn = 512 + (size_t)grid * 8;
+        const size_t trn = 1024 + (size_t)grid * 16;
         if (tr) {
             MFX_CUDA_TRY(cudaMalloc(&P.trace, trn * sizeof(unsigned long long)));
             MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, trn * sizeof(unsigned long long), s));
         }
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
         if (tr) {
-            static unsigned long long h[512 + 8 * 2048];
+            static unsigned long long h[1024 + 16 * 2048];
             MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, trn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             MFX_CUDA_TRY(cudaStreamSynchronize(s));
             cudaFree(P.trace);
-            double acc[7] = {0};
+            // slots: 0 K1 start | 1 warp0 K1 end, 2 CTA K1 end, 3 released, 4 folded | 5..8 K2 | 9..12 K3
+            const char *nm[12] = {"K1 warp0", "K1 CTA tail", "K1 barrier", "K1 fold", "K2 warp0", "K2 CTA tail",
+                                  "K2 barrier", "K2 fold", "K3 warp0", "K3 CTA tail", "K3 barrier", "K3 fold"};
+            double acc[12] = {0};
             int n = 0;
-            for (int it = 2; it < 64 && h[it * 8 + 6] && h[(it + 1) * 8]; it++, n++) {
-                const unsigned long long *t = h + it * 8;
-                for (int k = 0; k < 6; k++) acc[k] += 1e-3 * (double)(t[k + 1] - t[k]);
-                acc[6] += 1e-3 * (double)(h[(it + 1) * 8] - t[6]);
+            for (int it = 2; it < 63 && h[it * 16 + 12] && h[(it + 1) * 16]; it++, n++)
+                for (int k = 0; k < 12; k++) acc[k] += 1e-3 * (double)(h[it * 16 + k + 1] - h[it * 16 + k]);
+            if (n) {
+                fprintf(stderr, "persist trace (CTA 0, %d iters, us; grid %d units %lld Lz %d):", n, grid, a.units, a.Lz);
+                for (int k = 0; k < 12; k++) fprintf(stderr, " %s %.2f", nm[k], acc[k] / n);
+                fprintf(stderr, "\n");
             }
-            if (n)
-                fprintf(stderr, "persist trace (CTA 0, %d iters, us): K1 pass %.2f  allreduce %.2f  K2 pass %.2f  "
-                        "allreduce %.2f  K3 pass %.2f  allreduce %.2f  loop %.2f  grid %d units %lld Lz %d\n",
-                        n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, grid,
-                        a.units, a.Lz);
-            // iteration 5 across CTAs: pass durations and arrival spread per phase
-            {
-                const unsigned long long *c = h + 512;
-                double mn[3] = {1e30, 1e30, 1e30}, mx[3] = {0, 0, 0}, sum[3] = {0, 0, 0};
-                unsigned long long amin[3] = {~0ull, ~0ull, ~0ull}, amax[3] = {0, 0, 0};
-                int slow[3] = {0, 0, 0};
-                const int ps[3][2] = {{0, 1}, {2, 3}, {4, 5}};
-                for (int b = 0; b < grid; b++)
-                    for (int k = 0; k < 3; k++) {
-                        const double d = 1e-3 * (double)(c[b * 8 + ps[k][1]] - c[b * 8 + ps[k][0]]);
-                        if (d < mn[k]) mn[k] = d;
-                        if (d > mx[k]) { mx[k] = d; slow[k] = b; }
-                        sum[k] += d;
-                        const unsigned long long ar = c[b * 8 + ps[k][1]];
-                        if (ar < amin[k]) amin[k] = ar;
-                        if (ar > amax[k]) amax[k] = ar;
-                    }
-                for (int k = 0; k < 3; k++)
-                    fprintf(stderr, "  iter 5 %s pass over %d CTAs: min %.2f mean %.2f max %.2f us (slowest CTA %d on SM %llu); "
-                            "arrival spread %.2f us\n", k == 0 ? "K1" : (k == 1 ? "K2" : "K3"), grid, mn[k],
-                            sum[k] / grid, mx[k], slow[k], c[slow[k] * 8 + 7], 1e-3 * (double)(amax[k] - amin[k]));
+            const unsigned long long *c = h + 1024;
+            const int ps[3][3] = {{0, 2, 3}, {4, 6, 7}, {8, 10, 11}};   // pass start, CTA end, released
+            for (int k = 0; k < 3; k++) {
+                double mn = 1e30, mx = 0, sum = 0;
+                unsigned long long amin = ~0ull, amax = 0;
+                int slow = 0;
+                for (int b = 0; b < grid; b++) {
+                    const double d = 1e-3 * (double)(c[b * 16 + ps[k][1]] - c[b * 16 + ps[k][0]]);
+                    if (d < mn) mn = d;
+                    if (d > mx) { mx = d; slow = b; }
+                    sum += d;
+                    const unsigned long long ar = c[b * 16 + ps[k][1]];
+                    if (ar < amin) amin = ar;
+                    if (ar > amax) amax = ar;
+                }
+                fprintf(stderr, "  iter 5 K%d (pass start -> CTA done) over %d CTAs: min %.2f mean %.2f max %.2f us "
+                        "(slowest CTA %d, SM %llu); arrival spread %.2f us\n", k + 1, grid, mn, sum / grid, mx, slow,
+                        c[slow * 16 + 15], 1e-3 * (double)(amax - amin));
             }
+
         }
         return MFX_OK;
     }

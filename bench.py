@@ -505,6 +505,12 @@ def run_mfx(args, rank, world, local_rank):
     keep = list(synth.FIELD_NAMES) + [f"phi{s}" for s in range(n_scal)] + [f"phi_old{s}" for s in range(n_scal)]
     host = {k: torch.from_numpy(st[k]).pin_memory() for k in keep}
     sd = {k: v.cuda(non_blocking=True) for k, v in host.items()}
+    if world > 1:
+        # BCAST as one broadcast of the [u|v|w|p] block (mfx_params.packed_state)
+        blk = torch.cat([sd["u"], sd["v"], sd["w"], sd["p"]])
+        for i, k in enumerate(("u", "v", "w", "p")):
+            sd[k] = blk[i * g.n:(i + 1) * g.n]
+        pr.packed_state = 1
     uid = None
     if world > 1:
         obj = [mfx.nccl_unique_id() if rank == 0 else None]
@@ -543,10 +549,11 @@ def run_mfx(args, rank, world, local_rank):
     clk = clocks.stop()
     t_ms = ev0.elapsed_time(ev1)
     phase = ctx.phase_times()
+    xch = phase["gather"] + phase["bcast"]   # this rank's exchange time in the last step (comm stream)
     if dist is not None:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_ms, xch], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+        t_ms, xch = float(tt[0].item()), float(tt[1].item())
     # iterations: every equation counted once (owners are disjoint; identical records on all ranks)
     it_all = sum(outs[i]["iters"][q] for i in range(len(outs)) for q in range(8)
                  if ctx.assignment["owner"][q] >= 0)
@@ -732,6 +739,10 @@ def run_mfx(args, rank, world, local_rank):
                 "bicgstab_iters_per_step": it_all / args.steps,
                 "iters_last_step": outs[-1]["iters"],
                 "phase_ms_last_step": phase,
+                "exchange": {"gather_plus_bcast_ms_max_over_ranks": xch,
+                             "share_of_step": xch / (t_ms / args.steps),
+                             "packed_bcast": world > 1,
+                             "note": "north star: state exchange < 10% of the step (4 GPUs)"},
                 "kernel_avg_us": {k: (v * 1e3 if v else None) for k, v in kern_ms.items()},
                 "pp_iteration": {"alg_bytes": pp_iter_bytes,
                                  "us": 1e3 * phase["pp"] / max(outs[-1]["iters"][3], 1),

@@ -79,10 +79,20 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
         "launch__occupancy_limit_shared_mem", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
-for rep in sorted(x for x in os.listdir(GO) if x.startswith(f"{tag}_prof") and x.endswith(".ncu-rep")):
-    out = subprocess.run(["ncu", "-i", os.path.join(GO, rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
+def raw_pages():
+    # the box exports `ncu -i rep --page raw --csv` (reps exceed gpurun's copy-back limit); older tags have reps
+    for x in sorted(os.listdir(GO)):
+        if x.startswith(f"{tag}_prof") and x.endswith("_raw.csv"):
+            yield x, open(os.path.join(GO, x)).read()
+        elif x.startswith(f"{tag}_prof") and x.endswith(".ncu-rep"):
+            yield x, subprocess.run(["ncu", "-i", os.path.join(GO, x), "--page", "raw", "--csv"],
+                                    capture_output=True, text=True).stdout
+
+
+for rep, out in raw_pages():
+    lines_ = out.splitlines()
+    k0 = next((i for i, l in enumerate(lines_) if "Kernel Name" in l), 0)
+    rows = list(csv.reader(lines_[k0:]))
     if len(rows) < 3:
         continue
     h, units = rows[0], rows[1]

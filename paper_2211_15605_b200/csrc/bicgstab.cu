@@ -925,6 +925,7 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     const int nb = reduce_grid(G.N);
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
     MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->work[0], 0, sizeof(W.hdr->work), s));
     if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
     const int path = opt_solver_path();
     if (path == 2 || (path == 0 && cluster_fits(G, sym))) {

@@ -240,7 +240,8 @@ struct WsHeader {
     double resid[4];
     unsigned long long bad_parcel;      // first parcel outside the domain (ULLONG_MAX = none)
     double true_rel;                    // ||b - A x|| / ||b|| of the last solve's exit iterate (0 if b = 0)
-    double pad[4];
+    unsigned int work[2];               // dynamic unit counters of the z-marching kernels (reset by their last CTA)
+    double pad[3];
 };
 
 

@@ -62,6 +62,7 @@ struct StencilArgs {
     int kbeg, kend, ghost_store;
     dd *rank_part;
     unsigned long long *trace;             // optional (MFX_RW_TRACE): per-CTA %globaltimer stamps
+    unsigned int *work;                    // dynamic units: grab counter (NULL: static round-robin)
 };
 
 __device__ __forceinline__ void ktrace(const StencilArgs &a, int slot)
@@ -120,7 +121,7 @@ struct Cfg {
 template <class C>
 __host__ __device__ constexpr size_t smem_bytes(int S)
 {
-    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 16 * (size_t)S;
+    return (size_t)S * C::STAGE_B + 4 * (size_t)C::PBUF_B + 24 * (size_t)S;   // + full, empty, meta
 }
 
 // plane-stream cursor.  Units are (z-chunk, tile) pairs in chunk-major order,
@@ -133,7 +134,8 @@ struct Cursor {
     int u, units;
     int G, ntiles, Lz, tiles_x, TX, TY, rev, kbeg, kend;
     int x0, y0, k, k0, k1;
-    bool valid;
+    bool valid, pending;
+    unsigned int *work;   // dynamic units: the producer grabs them, consumers read them from the stage
     __device__ void start(int nz)
     {
         if (u >= units) { valid = false; return; }
@@ -148,29 +150,49 @@ struct Cursor {
         k = k0 - 1;
         valid = true;
     }
-    __device__ void init(int u0, const StencilArgs &a, int nt, int tX, int tY)
+    // producer: dyn -> units come from the counter; consumer: dyn -> from the stage (set_unit)
+    __device__ void init(int u0, const StencilArgs &a, int nt, int tX, int tY, bool producer = true)
     {
-        u = u0; units = (int)a.units; G = gridDim.x; ntiles = nt; Lz = a.Lz; tiles_x = a.tiles_x; TX = tX; TY = tY;
-        rev = a.reverse; kbeg = a.kbeg; kend = a.kend;
+        units = (int)a.units; G = gridDim.x; ntiles = nt; Lz = a.Lz; tiles_x = a.tiles_x; TX = tX; TY = tY;
+        rev = a.reverse; kbeg = a.kbeg; kend = a.kend; work = a.work;
+        pending = false;
+        if (work && !producer) { pending = true; valid = true; return; }
+        u = work ? (int)atomicAdd(work, 1u) : u0;
         start(a.nz);
     }
-    __device__ void advance(int nz)
+    __device__ void set_unit(int uu, int nz) { u = uu; pending = false; start(nz); }
+    __device__ void advance(int nz, bool producer = true)
     {
         k++;
-        if (k > k1) { u += G; start(nz); }
+        if (k > k1) {
+            if (!work) { u += G; start(nz); }
+            else if (producer) { u = (int)atomicAdd(work, 1u); start(nz); }
+            else pending = true;
+        }
     }
     __device__ bool is_virtual(int nz) const { return k < 0 || k >= nz; }
     __device__ bool produces() const { return k >= k0 + 1; }
 };
 
+// dynamic units: every issued stage carries its unit id (meta[s]); after the
+// last unit the producer posts one stage with id -1 and no data
+__device__ __forceinline__ void post_end(uint64_t *full, uint64_t *empty, int *meta, int S, int q)
+{
+    const int s = q % S;
+    if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+    meta[s] = -1;
+    mbar_arrive(&full[s]);
+}
+
 template <int MODE, bool SYM, int TX, int TY, int CPT_, int S, int STRIDE = Cfg<MODE, SYM, TX, TY, CPT_>::STAGE_B>
 __device__ __forceinline__ void issue(const TmaMaps &M, const Cursor &c, int nz, uint8_t *stages, uint64_t *full,
-                                      int q)
+                                      int q, int *meta = nullptr)
 {
     using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     static_assert(STRIDE >= C::STAGE_B, "stage slot too small");
     const int s = q % S;
     uint64_t *bar = &full[s];
+    if (meta) meta[s] = c.u;   // read by the consumers after the full barrier (release by the arrive below)
     if (c.is_virtual(nz)) {
         mbar_arrive(bar);
         return;
@@ -199,6 +221,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     double *pbuf = (double *)(smem + (size_t)S * C::STAGE_B);
     uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B + 4 * C::PBUF_B);
     uint64_t *empty = full + S;
+    int *meta = (int *)(empty + S);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
@@ -255,11 +278,13 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             for (int q = 0; q < C::NH; q++) prefetch_map(&M.halo[q]);
             Cursor prod;
             prod.init(blockIdx.x, a, ntiles, TX, TY);
-            for (int q = 0; prod.valid; q++) {
+            int q = 0;
+            for (; prod.valid; q++) {
                 if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
-                issue<MODE, SYM, TX, TY, CPT_, S>(M, prod, a.nz, stages, full, q);
+                issue<MODE, SYM, TX, TY, CPT_, S>(M, prod, a.nz, stages, full, q, a.work ? meta : nullptr);
                 prod.advance(a.nz);
             }
+            if (a.work) post_end(full, empty, meta, S, q);
         }
     } else {
         // ------------------------------------------------ consumer warps
@@ -268,7 +293,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
         constexpr int CPT = C::CPT;
         constexpr int RW = TX / CPT;                 // threads per tile row
         Cursor cons;
-        cons.init(blockIdx.x, a, ntiles, TX, TY);
+        cons.init(blockIdx.x, a, ntiles, TX, TY, false);
         double czq1[CPT], czq0[CPT];                 // cz at planes q-1 (aT of output) and q-2 (aB)
 #pragma unroll
         for (int m = 0; m < CPT; m++) { czq1[m] = 0.0; czq0[m] = 0.0; }
@@ -291,11 +316,16 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
         const int hc = (cy + 1) * C::HX + (cx0 + 2); // halo-box index of the first owned cell
         for (int q = 0; cons.valid; q++) {
             const int s = q % S;
+            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+            if (cons.pending) {   // dynamic units: the stage names the unit (or the end)
+                const int um = meta[s];
+                if (um < 0) break;
+                cons.set_unit(um, a.nz);
+            }
             const bool virt = cons.is_virtual(a.nz);
             const bool produce = cons.produces();
             const int kout = cons.k - 1;
             const int x0 = cons.x0, y0 = cons.y0;
-            mbar_wait(&full[s], (uint32_t)((q / S) & 1));
             const uint8_t *st = stages + (size_t)s * C::STAGE_B;
             double *P = pbuf + (size_t)(q & 3) * (C::PBUF_B / 8);
 
@@ -501,7 +531,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             if (lane == 0) mbar_arrive(&empty[s]);
 #pragma unroll
             for (int m = 0; m < CPT; m++) { czq0[m] = czq1[m]; czq1[m] = czcur[m]; }
-            cons.advance(a.nz);
+            cons.advance(a.nz, false);
         }
     }
 
@@ -515,6 +545,7 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
             for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
         }
         if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
+        if (a.work) *a.work = 0u;   // every CTA has passed the ticket: all units were taken
         if (a.rank_part) {
 #pragma unroll
             for (int d = 0; d < ND; d++) a.rank_part[d] = out[d];
@@ -541,16 +572,17 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 // TMA producer of a row-warp pass (lane 0 of the producer warp)
 template <int MODE, int CPT, int S, int STRIDE>
 __device__ __forceinline__ void rw_produce(const TmaMaps &M, const StencilArgs &a, uint8_t *stages, uint64_t *full,
-                                           uint64_t *empty, int &q)
+                                           uint64_t *empty, int &q, int *meta = nullptr)
 {
     constexpr int TX = 32 * CPT, TY = 8;
     Cursor prod;
     prod.init(blockIdx.x, a, a.tiles_x * a.tiles_y, TX, TY);
     for (; prod.valid; q++) {
         if (q >= S) mbar_wait(&empty[q % S], (uint32_t)(((q / S) - 1) & 1));
-        issue<MODE, true, TX, TY, CPT, S, STRIDE>(M, prod, a.nz, stages, full, q);
+        issue<MODE, true, TX, TY, CPT, S, STRIDE>(M, prod, a.nz, stages, full, q, a.work ? meta : nullptr);
         prod.advance(a.nz);
     }
+    if (a.work) post_end(full, empty, meta, S, q++);
 }
 
 // consumer warps of a row-warp pass (MODE) over this CTA's units; q is the
@@ -559,14 +591,14 @@ __device__ __forceinline__ void rw_produce(const TmaMaps &M, const StencilArgs &
 template <int MODE, int CPT, int S, int STRIDE, bool ONEACC = false>
 __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, double beta, double omega, bool rst,
                                            Acc (&acc)[3][CPT], const uint8_t *stages, uint64_t *full,
-                                           uint64_t *empty, int &q)
+                                           uint64_t *empty, int &q, const int *meta = nullptr)
 {
     constexpr int TX = 32 * CPT, TY = 8;
     using C = Cfg<MODE, true, TX, TY, CPT>;
     constexpr int ND = C::NDOT > 0 ? C::NDOT : 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Cursor cons;
-    cons.init(blockIdx.x, a, a.tiles_x * a.tiles_y, TX, TY);
+    cons.init(blockIdx.x, a, a.tiles_x * a.tiles_y, TX, TY, false);
     const int cx0 = lane * CPT;
     const int hc = (warp + 1) * C::HX + cx0 + 2;                    // halo-box index of the first owned cell
     const int he = lane == 31 ? (warp + 1) * C::HX + TX + 2          // right edge cell x0 + TX
@@ -625,10 +657,15 @@ __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, d
 
     for (; cons.valid; q++) {
         const int s = q % S;
+        mbar_wait(&full[s], (uint32_t)((q / S) & 1));
+        if (cons.pending) {   // dynamic units: the stage names the unit (or the end)
+            const int um = meta[s];
+            if (um < 0) { q++; break; }
+            cons.set_unit(um, a.nz);
+        }
         const bool virt = cons.is_virtual(a.nz);
         const bool produce = cons.produces();
         const int kout = cons.k - 1;
-        mbar_wait(&full[s], (uint32_t)((q / S) & 1));
         const uint8_t *st = stages + (size_t)s * STRIDE;
         // ---- centre row of plane q (T of the output plane, B of the next)
         double tC[CPT];
@@ -741,7 +778,7 @@ __device__ __forceinline__ void rw_consume(const StencilArgs &a, double alpha, d
 #pragma unroll
         for (int m = 0; m <= CPT; m++) kxw[m] = nkxw[m];
         vE = tE;
-        cons.advance(a.nz);
+        cons.advance(a.nz, false);
     }
 }
 
@@ -755,6 +792,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
     uint8_t *stages = smem;
     uint64_t *full = (uint64_t *)(smem + (size_t)S * C::STAGE_B);
     uint64_t *empty = full + S;
+    int *meta = (int *)(empty + S);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
@@ -804,11 +842,11 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
         if (lane == 0) {
 #pragma unroll
             for (int h = 0; h < C::NH; h++) prefetch_map(&M.halo[h]);
-            rw_produce<MODE, CPT, S, C::STAGE_B>(M, a, stages, full, empty, q);
+            rw_produce<MODE, CPT, S, C::STAGE_B>(M, a, stages, full, empty, q, meta);
         }
     } else {
         // MB = 3 CTAs per SM: one accumulator per dot (registers)
-        rw_consume<MODE, CPT, S, C::STAGE_B, (MB >= 3)>(a, alpha, beta, omega, rst, acc, stages, full, empty, q);
+        rw_consume<MODE, CPT, S, C::STAGE_B, (MB >= 3)>(a, alpha, beta, omega, rst, acc, stages, full, empty, q, meta);
     }
 
     ktrace(a, 1);
@@ -824,6 +862,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
         const bool last = grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out);
         ktrace(a, last ? 3 : 2);
         if (!last || tid != 0) return;
+        if (a.work) *a.work = 0u;   // every CTA has passed the ticket: all units were taken
         if (a.rank_part) {
 #pragma unroll
             for (int d = 0; d < ND; d++) a.rank_part[d] = out[d];
@@ -1152,7 +1191,7 @@ struct Launcher {
     using C = Cfg<MODE, SYM, TX, TY, CPT_>;
     static constexpr void (*kern)(const TmaMaps, StencilArgs) =
         RW ? k_stencil_rw<MODE, CPT_, S, MB> : k_stencil<MODE, SYM, TX, TY, CPT_, S>;
-    static constexpr size_t smem() { return RW ? (size_t)S * C::STAGE_B + 16 * (size_t)S : smem_bytes<C>(S); }
+    static constexpr size_t smem() { return RW ? (size_t)S * C::STAGE_B + 24 * (size_t)S : smem_bytes<C>(S); }
     static int grid_size()
     {
         static int g = 0;
@@ -1190,6 +1229,10 @@ struct Launcher {
         int grid = grid_size();
         const long long ntiles = (long long)a.tiles_x * a.tiles_y;
         if (a.kend <= a.kbeg) { a.kbeg = 0; a.kend = G.nz; }
+        // dynamic units (MFX_DYN=1; off: measured no gain at c2, finer units cost halo planes)
+        // (the dot kernels only: their last CTA resets the counter)
+        static const int dyn = env_int("MFX_DYN", 0);
+        a.work = (dyn && C::NDOT > 0 && a.h) ? &a.h->work[0] : nullptr;
         const int nout = a.kend - a.kbeg;
         a.Lz = choose_lz(ntiles, nout, grid);
         a.units = ntiles * ((nout + a.Lz - 1) / a.Lz);

@@ -314,7 +314,8 @@ static mfx_status dist_solve_tma(mfx_ctx *ctx, const mfx_grid *grid, const mfx_e
     WsHeader *h = (WsHeader *)w;
     dd *part = (dd *)(w + hdr);
     dd *rank_part = (dd *)(w + hdr + partb);
-    dd *all = (dd *)(w + hdr + partb + rpb);
+    // one rank: the fold kernels read the rank's own partials (no gather copy)
+    dd *all = R == 1 ? rank_part : (dd *)(w + hdr + partb + rpb);
     char *vb = w + hdr + partb + rpb + apb;
     auto E = [&](int q) { return (double *)(vb + (size_t)q * eb); };
     double *r = E(0), *rh = E(1), *P[2] = {E(2), E(3)}, *V[2] = {E(4), E(5)}, *t = E(6);
@@ -335,7 +336,7 @@ static mfx_status dist_solve_tma(mfx_ctx *ctx, const mfx_grid *grid, const mfx_e
     Ae.aE = cxe; Ae.aN = cye; Ae.aT = cze; Ae.b = be;
     mfx_status st;
 #define XCHG(vecp) do { if ((st = ctx_halo_exchange(ctx, (vecp) + plane, npl, plane, (vecp), (vecp) + (size_t)(npl + 1) * plane, s)) != MFX_OK) return st; } while (0)
-#define GATHER(K) do { if ((st = ctx_allgather_dd(ctx, rank_part, K, all, s)) != MFX_OK) return st; } while (0)
+#define GATHER(K) do { if (R > 1 && (st = ctx_allgather_dd(ctx, rank_part, K, all, s)) != MFX_OK) return st; } while (0)
 #define TRY(expr) do { if ((st = (expr)) != MFX_OK) return st; } while (0)
     XCHG(cze);   // c_z of plane k0 - 1: the B coefficient of the first own plane
     XCHG(xe);

@@ -65,9 +65,18 @@ struct StencilArgs {
     unsigned int *work;                    // dynamic units: grab counter (NULL: static round-robin)
 };
 
+// per-CTA %globaltimer traces (MFX_RW_TRACE / MFX_PERSIST_TRACE) are compiled
+// only with -DMFX_TRACE (a variant build: MFX_EXTRA_NVCC_FLAGS=-DMFX_TRACE);
+// in the default build they cost registers in the persistent kernel
+#ifdef MFX_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+
 __device__ __forceinline__ void ktrace(const StencilArgs &a, int slot)
 {
-    if (a.trace && threadIdx.x == 0) {
+    if (kTrace && a.trace && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[blockIdx.x * 4 + slot] = t;
@@ -899,7 +908,7 @@ struct PersistArgs {
 
 __device__ __forceinline__ void ptrace(const PersistArgs &P, int it, int slot)
 {
-    if (P.trace && threadIdx.x == 0 && it < 64) {
+    if (kTrace && P.trace && threadIdx.x == 0 && it < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (blockIdx.x == 0) P.trace[it * 16 + slot] = t;
@@ -1249,7 +1258,7 @@ struct Launcher {
         cfg.numAttrs = 1;
         static const int tr = env_int("MFX_RW_TRACE", 0);
         static int traced = 0;
-        if (RW && tr && traced < 40) {
+        if (kTrace && RW && tr && traced < 40) {
             MFX_CUDA_TRY(cudaMalloc(&a.trace, (size_t)grid * 4 * sizeof(unsigned long long)));
             MFX_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)grid * 4 * sizeof(unsigned long long), s));
         }
@@ -1418,12 +1427,12 @@ struct PersistLauncher {
         cfg.numAttrs = 1;
         static const int tr = env_int("MFX_PERSIST_TRACE", 0);
         const size_t trn = 1024 + (size_t)grid * 16;
-        if (tr) {
+        if (kTrace && tr) {
             MFX_CUDA_TRY(cudaMalloc(&P.trace, trn * sizeof(unsigned long long)));
             MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, trn * sizeof(unsigned long long), s));
         }
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
-        if (tr) {
+        if (kTrace && tr) {
             static unsigned long long h[1024 + 16 * 2048];
             MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, trn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             MFX_CUDA_TRY(cudaStreamSynchronize(s));

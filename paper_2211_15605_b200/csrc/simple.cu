@@ -610,7 +610,11 @@ static ncclComm_t ctx_comm(const mfx_ctx *c) { return c->dist_sub ? c->pcomm : c
 static mfx_local_group *ctx_group(const mfx_ctx *c) { return c->dist_sub ? c->pgroup : c->group; }
 // the distributed solver may capture its iterations in a CUDA graph: NCCL (or
 // one rank), not the in-process transport, whose phases synchronise host threads
-bool ctx_capturable(const mfx_ctx *c) { return ctx_nranks(c) == 1 || !ctx_group(c); }
+bool ctx_capturable(const mfx_ctx *c)
+{
+    static const int allowed = [] { const char *e = getenv("MFX_DIST_GRAPH"); return e ? atoi(e) : 1; }();
+    return allowed && (ctx_nranks(c) == 1 || !ctx_group(c));
+}
 
 void *ctx_dist_scratch(mfx_ctx *c, size_t bytes)
 {

@@ -70,6 +70,45 @@ def run(assignment, nranks, n_scalars, packed=False, outer=2):
     return res
 
 
+def run_pic(nranks):
+    """Implicit PIC coupling: the PIC device (rank 0) refreshes the drag fields
+    and broadcasts them (exchange phase 3, with its error record)."""
+    g = synth.make_grid(16, 12, 20)
+    pr = synth.Params(lin_tol_mom=1e-13, lin_maxit_mom=400, lin_tol_pp=1e-13, lin_maxit_pp=6000)
+    st = synth.make_state(g, 4321, pr)
+    pic = synth.PicParams()
+    pc = synth.make_parcels(g, 4322, 6000, st["eps"], pic)
+    asg = "111[1]" if nranks == 1 else "234[1]"
+    uid = mfx.nccl_unique_id() if nranks > 1 else None
+    res, errs = {}, []
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sd = {k: torch.from_numpy(v).cuda() for k, v in st.items()}
+                dpc = {k: torch.from_numpy(v).cuda() for k, v in pc.items()} if rank == 0 else None
+                ctx = mfx.SimpleContext(asg, g, pr, rank=rank, nranks=nranks, uid=uid)
+                ctx.set_pic(dpc, pic if rank == 0 else None, mfx.PIC_IMPLICIT)
+                for _ in range(2):
+                    ctx.step(sd, stream=stream)
+                stream.synchronize()
+                res[rank] = {k: v.cpu().numpy() for k, v in sd.items()}
+                ctx.close()
+        except Exception as e:
+            errs.append((rank, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert len(res) == nranks
+    return res
+
+
 def main():
     cases = [("222[1]", 2, 0, False), ("234[1]", 4, 0, False), ("234[1]", 4, 0, True),
              ("234[1]5678", 8, 4, True), ("234[1234]", 4, 0, False), ("234[23]", 4, 0, True),
@@ -88,6 +127,13 @@ def main():
             for o, r in zip(outs, ref_outs):
                 assert o["iters"] == r["iters"] and o["R"] == r["R"], (asg, rank, o["iters"], r["iters"])
         print(f"loopback NCCL {asg} on {n} ranks{' packed' if packed else ''}: bitwise = 111[1]", flush=True)
+    ref = run_pic(1)[0]
+    multi = run_pic(4)
+    for rank in range(4):
+        for k in ("u", "v", "w", "p", "beta", "sbeta_w"):
+            assert np.array_equal(multi[rank][k], ref[k]), ("pic", rank, k)
+    print("loopback NCCL 234[1] with implicit PIC coupling (phase-3 broadcast) on 4 ranks: bitwise = 111[1]",
+          flush=True)
     print("LOOPBACK OK", flush=True)
 
 

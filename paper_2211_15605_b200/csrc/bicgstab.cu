@@ -26,7 +26,7 @@ mfx_status persist_solve_launch(const Geo &G, const mfx_eqsys *A, double *x, con
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
                           const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
                           double tol, int maxit, cudaStream_t s, int reverse = 0, int kbeg = 0, int kend = 0,
-                          int ghost_store = 0, dd *rank_part = nullptr);
+                          int ghost_store = 0, dd *rank_part = nullptr, int chain = 0);
 
 // L2 ping-pong: consecutive sweeps alternate direction so each kernel starts
 // on the cells the previous one touched last (126 MB L2).  MFX_REVERSE=0
@@ -367,14 +367,32 @@ __device__ __forceinline__ void k3_store(const K3Pair &d, long long e, double *x
 __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *r, const double *__restrict__ rh,
                                                const double *__restrict__ p, const double *__restrict__ v,
                                                const double *__restrict__ t, WsHeader *h, dd *part, int rev,
-                                               dd *rank_part)
+                                               dd *rank_part, int chain)
 {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    SolverScalars &S = h->sc;
-    if (S.done || S.skip) return;
-    const double alpha = S.alpha, omega = S.omega;
-    const bool half = S.half != 0;
+    // chained (path 1): K2's scalar tail runs here in every CTA -- fold K2's
+    // published <t,s>, <t,t>, <s,s> partials onto the state after K1's tail
+    // (sc2); the last CTA writes the state after K3's tail to sc
+    SolverScalars L;
+    if (chain) {
+        __shared__ dd s_fsh[32], s_fbc[3];
+        L = sc_ldcg(&h->sc2);
+        if (!(L.done || L.skip)) {
+            double o[3];
+            fold_published<3>(part + kPartK2, __ldcg(&h->npart[1]), 3, s_fsh, s_fbc, o);
+            bicg_k2_tail(L, o[0], o[1], o[2]);
+        }
+        if (L.done || L.skip) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) h->sc = L;
+            return;
+        }
+    } else {
+        L = h->sc;
+        if (L.done || L.skip) return;
+    }
+    const double alpha = L.alpha, omega = L.omega;
+    const bool half = L.half != 0;
     Acc rhr, rr;
     rhr.zero(); rr.zero();
     const long long npairs = N / 2;
@@ -398,7 +416,8 @@ __global__ void __launch_bounds__(kThreads) k3v(long long N, double *x, double *
     dd vv[2] = {rhr.get(), rr.get()}, out[2];
     if (grid_reduce_dd<2>(vv, part, &h->ticket[1], sh, out) && threadIdx.x == 0) {
         if (rank_part) { rank_part[0] = out[0]; rank_part[1] = out[1]; }   // z-slab mode: folded across ranks
-        else bicg_k3_tail(S, half, dd_round(out[0]), dd_round(out[1]));
+        else if (chain) { bicg_k3_tail(L, half, dd_round(out[0]), dd_round(out[1])); h->sc = L; }
+        else bicg_k3_tail(h->sc, half, dd_round(out[0]), dd_round(out[1]));
     }
 }
 
@@ -621,14 +640,22 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
     double *p_old = W.p[parity], *p_new = W.p[parity ^ 1];
     double *v_old = W.v[parity], *v_new = W.v[parity ^ 1];
     mfx_status st;
+    // chained tails (option MFX_CHAIN=1): K1 and K2 publish their dot partials
+    // and exit; K2 and K3 fold them in their prologues (every CTA), so no
+    // last-CTA fold sits between the kernels (common.cuh).  Off: measured
+    // slower (c2 K2 89 vs 82 us, K3 99 vs 88 us: every CTA re-reading the same
+    // partials costs more than one CTA's serial fold).
+    static const int chain = [] { const char *e = getenv("MFX_CHAIN"); return e ? atoi(e) : 0; }();
     count_launch(SYM ? 6 : 1, s, true);
     const double *h1[3] = {W.r, p_old, v_old};
-    st = stencil_launch(2, SYM, G, h1, A, W.rh, p_new, v_new, W.rh, W.hdr, W.part, 0.0, 0, s, sweep_dir(true));
+    st = stencil_launch(2, SYM, G, h1, A, W.rh, p_new, v_new, W.rh, W.hdr, W.part, 0.0, 0, s, sweep_dir(true), 0, 0,
+                        0, nullptr, chain);
     count_launch(SYM ? 6 : 1, s, false);
     if (st != MFX_OK) return st;
     count_launch(SYM ? 7 : 2, s, true);
     const double *h2[3] = {W.r, v_new, nullptr};
-    st = stencil_launch(3, SYM, G, h2, A, nullptr, W.t, nullptr, nullptr, W.hdr, W.part, 0.0, 0, s, sweep_dir(true));
+    st = stencil_launch(3, SYM, G, h2, A, nullptr, W.t, nullptr, nullptr, W.hdr, W.part, 0.0, 0, s, sweep_dir(true),
+                        0, 0, 0, nullptr, chain);
     count_launch(SYM ? 7 : 2, s, false);
     if (st != MFX_OK) return st;
     count_launch(3, s, true);
@@ -647,7 +674,7 @@ mfx_status launch_iteration_tma(const Geo &G, const mfx_eqsys *A, const WsView &
         cfg.numAttrs = 1;
         MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k3v, G.N, x, W.r, (const double *)W.rh, (const double *)p_new,
                                         (const double *)v_new, (const double *)W.t, W.hdr, W.part,
-                                        sweep_dir(true), (dd *)nullptr));
+                                        sweep_dir(true), (dd *)nullptr, chain));
     }
     count_launch(3, s, false);
     (void)nb;
@@ -857,7 +884,7 @@ mfx_status k3_slab_launch(long long n, double *x, double *r, const double *rh, c
     int g3 = k3v_grid();
     if ((long long)g3 * kThreads > np) g3 = (int)((np + kThreads - 1) / kThreads);
     if (g3 < 1) g3 = 1;
-    k3v<<<g3, kThreads, 0, s>>>(n, x, r, rh, p, v, t, h, part, 0, rank_part);
+    k3v<<<g3, kThreads, 0, s>>>(n, x, r, rh, p, v, t, h, part, 0, rank_part, 0);
     MFX_CUDA_TRY(cudaGetLastError());
     return MFX_OK;
 }

@@ -242,7 +242,66 @@ struct WsHeader {
     double true_rel;                    // ||b - A x|| / ||b|| of the last solve's exit iterate (0 if b = 0)
     unsigned int work[2];               // dynamic unit counters of the z-marching kernels (reset by their last CTA)
     double pad[3];
+    // chained tails (bicgstab.cu, path 1): K1 and K2 publish block partials
+    // without a last-CTA fold; the next kernel's CTAs fold them in their
+    // prologue.  sc2 = the state after K1's tail (written by K2, read by K3);
+    // npart = how many partials K1 / K2 published.
+    SolverScalars sc2;
+    unsigned int npart[2];
 };
+
+// offsets of the chained partials in the workspace's partials buffer
+constexpr int kPartK1 = 0, kPartK2 = 8192;
+
+// every thread gets the same fold of n published partials part[b * stride + q]
+// (thread-strided, then the block tree of block_reduce_dd): the prologue of a
+// chained kernel.  `bc` is K dd of shared memory.
+template <int K>
+__device__ __forceinline__ void fold_published(const dd *part, unsigned n, int stride, dd *sh, dd *bc,
+                                               double (&out)[K])
+{
+    dd f[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) f[q] = dd{0.0, 0.0};
+    for (unsigned b = threadIdx.x; b < n; b += blockDim.x) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            dd x;
+            x.hi = __ldcg(&part[(size_t)b * stride + q].hi);
+            x.lo = __ldcg(&part[(size_t)b * stride + q].lo);
+            f[q] = dd_add(f[q], x);
+        }
+    }
+    block_reduce_dd<K>(f, sh);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < K; q++) bc[q] = f[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < K; q++) out[q] = dd_round(bc[q]);
+}
+
+__device__ __forceinline__ SolverScalars sc_ldcg(const SolverScalars *S)
+{
+    SolverScalars L;
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(S);
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(&L);
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(SolverScalars) / 8); q++) dst[q] = __ldcg(src + q);
+    return L;
+}
+
+// publish this block's K partials (no ticket): the chained kernels' epilogue
+template <int K>
+__device__ __forceinline__ void publish_partials(dd (&v)[K], dd *part, unsigned *npart, dd *sh)
+{
+    block_reduce_dd<K>(v, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) part[(size_t)blockIdx.x * K + q] = v[q];
+        if (blockIdx.x == 0) *npart = gridDim.x;
+    }
+}
 
 
 struct WsView {

@@ -275,7 +275,7 @@ void *ctx_dist_scratch(mfx_ctx *c, size_t bytes);
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3], const mfx_eqsys *A,
                           const double *extra, double *o0, double *o1, double *o2, WsHeader *h, dd *part,
                           double tol, int maxit, cudaStream_t s, int reverse = 0, int kbeg = 0, int kend = 0,
-                          int ghost_store = 0, dd *rank_part = nullptr);
+                          int ghost_store = 0, dd *rank_part = nullptr, int chain = 0);
 mfx_status k3_slab_launch(long long n, double *x, double *r, const double *rh, const double *p, const double *v,
                           const double *t, WsHeader *h, dd *part, dd *rank_part, cudaStream_t s);
 

@@ -63,6 +63,7 @@ struct StencilArgs {
     dd *rank_part;
     unsigned long long *trace;             // optional (MFX_RW_TRACE): per-CTA %globaltimer stamps
     unsigned int *work;                    // dynamic units: grab counter (NULL: static round-robin)
+    int chain;                             // K1/K2: chained tails (common.cuh: publish partials; K2 folds K1's)
 };
 
 // per-CTA %globaltimer traces (MFX_RW_TRACE / MFX_PERSIST_TRACE) are compiled
@@ -255,7 +256,21 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
     bool rst = false;
     K1Pro P1;
     P1.rst = false;
-    if (MODE == SM_K1 || MODE == SM_K2) {
+    if (MODE == SM_K2 && a.chain) {
+        // chained: K1's scalar tail runs here, in every CTA (identical bits):
+        // fold K1's published <r^, v> partials, apply it to the state K1 read
+        __shared__ dd s_fsh[32], s_fbc[3];
+        SolverScalars L = sc_ldcg(&a.h->sc);
+        if (!L.done) {
+            const K1Pro P = bicg_k1_prologue(L);
+            double sg[1];
+            fold_published<1>(a.part + kPartK1, __ldcg(&a.h->npart[0]), 1, s_fsh, s_fbc, sg);
+            bicg_k1_tail(L, P, sg[0]);
+        }
+        if (blockIdx.x == 0 && tid == 0) a.h->sc2 = L;   // read by K3
+        if (L.done || L.skip) return;
+        alpha = L.alpha;
+    } else if (MODE == SM_K1 || MODE == SM_K2) {
         SolverScalars &Sc = a.h->sc;
         if (Sc.done) return;
         if (MODE == SM_K2 && Sc.skip) return;
@@ -553,6 +568,11 @@ __global__ void __launch_bounds__(Cfg<MODE, SYM, TX, TY, CPT_>::NT + 32) k_stenc
 #pragma unroll
             for (int m = 1; m < C::CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
         }
+        if ((MODE == SM_K1 || MODE == SM_K2) && a.chain) {   // the next kernel folds them
+            publish_partials<ND>(v, a.part + (MODE == SM_K1 ? kPartK1 : kPartK2), &a.h->npart[MODE == SM_K1 ? 0 : 1],
+                                 sh);
+            return;
+        }
         if (!grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out) || tid != 0) return;
         if (a.work) *a.work = 0u;   // every CTA has passed the ticket: all units were taken
         if (a.rank_part) {
@@ -821,7 +841,21 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
     bool rst = false;
     K1Pro P1;
     P1.rst = false;
-    if (MODE == SM_K1 || MODE == SM_K2) {
+    if (MODE == SM_K2 && a.chain) {
+        // chained: K1's scalar tail runs here, in every CTA (identical bits):
+        // fold K1's published <r^, v> partials, apply it to the state K1 read
+        __shared__ dd s_fsh[32], s_fbc[3];
+        SolverScalars L = sc_ldcg(&a.h->sc);
+        if (!L.done) {
+            const K1Pro P = bicg_k1_prologue(L);
+            double sg[1];
+            fold_published<1>(a.part + kPartK1, __ldcg(&a.h->npart[0]), 1, s_fsh, s_fbc, sg);
+            bicg_k1_tail(L, P, sg[0]);
+        }
+        if (blockIdx.x == 0 && tid == 0) a.h->sc2 = L;   // read by K3
+        if (L.done || L.skip) return;
+        alpha = L.alpha;
+    } else if (MODE == SM_K1 || MODE == SM_K2) {
         SolverScalars &Sc = a.h->sc;
         if (Sc.done) return;
         if (MODE == SM_K2 && Sc.skip) return;
@@ -867,6 +901,11 @@ __global__ void __launch_bounds__(8 * 32 + 32, MB) k_stencil_rw(const __grid_con
             v[d] = acc[d][0].get();
 #pragma unroll
             for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+        }
+        if ((MODE == SM_K1 || MODE == SM_K2) && a.chain) {   // the next kernel folds them
+            publish_partials<ND>(v, a.part + (MODE == SM_K1 ? kPartK1 : kPartK2), &a.h->npart[MODE == SM_K1 ? 0 : 1],
+                                 sh);
+            return;
         }
         const bool last = grid_reduce_dd<ND>(v, a.part, &a.h->ticket[1], sh, out);
         ktrace(a, last ? 3 : 2);
@@ -1492,7 +1531,7 @@ mfx_status persist_solve_launch(const Geo &G, const mfx_eqsys *A, double *x, con
 mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const halo[3],
                           const mfx_eqsys *A, const double *extra, double *o0, double *o1, double *o2,
                           WsHeader *h, dd *part, double tol, int maxit, cudaStream_t s, int reverse, int kbeg,
-                          int kend, int ghost_store, dd *rank_part)
+                          int kend, int ghost_store, dd *rank_part, int chain)
 {
     const double *coef[7];
     if (sym) {
@@ -1507,6 +1546,7 @@ mfx_status stencil_launch(int mode, bool sym, const Geo &G, const double *const 
     a.out0 = o0; a.out1 = o1; a.out2 = o2; a.h = h; a.part = part; a.tol = tol; a.maxit = maxit;
     a.reverse = reverse;
     a.kbeg = kbeg; a.kend = kend; a.ghost_store = ghost_store; a.rank_part = rank_part;
+    a.chain = chain && !rank_part && (mode == SM_K1 || mode == SM_K2);
     MFX_ARG_CHECK(!rank_part || sym, "slab mode: symmetric systems only");
     switch (mode * 2 + (sym ? 1 : 0)) {
     case SM_SPMV * 2 + 0: return run_mode<SM_SPMV, false>(G, halo, coef, extra, a, s);

@@ -410,8 +410,10 @@ void mfx_prof_enable(int on);
 void mfx_prof_reset(void);
 mfx_status mfx_prof_read(int counts[16], double ms[16]);
 /* Runtime options (process-wide).  "solver_path": 0 = auto (the
- * single-cluster kernel when the system fits one cluster's shared memory,
- * else the TMA z-marching kernels; the grid-synchronous kernel is chosen
+ * single-cluster kernel when the system fits one cluster's shared memory;
+ * else, for a p' system with even nx whose working set is <= 112 MiB (L2-
+ * resident, MFX_PERSIST_MB overrides), the persistent row-warp solver (path
+ * 5); else the TMA z-marching kernels; the grid-synchronous kernel is chosen
  * automatically only when MFX_GRID_SOLVER_MB sets an L2 budget -- off by
  * default, measured slower at configuration 3), 1 = TMA z-marching kernels,
  * 2 = single-cluster persistent kernel, 3 = v1 grid-stride reference kernels,
@@ -421,8 +423,12 @@ mfx_status mfx_prof_read(int counts[16], double ms[16]);
  * "graphs": 1/0 enables CUDA-graph replay of the iteration loop.  "pdl": 1/0
  * enables programmatic dependent launch between the BiCGSTAB kernels.
  * "asm_tma": 1/0 selects the TMA z-marching momentum assembly (default) or
- * the grid-stride kernel (both give identical bits).  Every path gives the
- * same bits.  Returns MFX_ERR_ARG for an unknown key. */
+ * the grid-stride kernel (both give identical bits).  "cluster_size": 16 or 8
+ * CTAs for the single-cluster solver (default 16, the non-portable maximum,
+ * when the device can place such a cluster; MFX_CLUSTER=8 forces 8); the
+ * systems that fit it follow from the size (mfx_get_option reports the one in
+ * use).  Every path gives the same bits.  Returns MFX_ERR_ARG for an unknown
+ * key. */
 mfx_status mfx_set_option(const char *key, int value);
 int mfx_get_option(const char *key);
 

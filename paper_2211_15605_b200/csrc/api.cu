@@ -348,6 +348,8 @@ API mfx_status mfx_prof_read(int counts[16], double ms[16])
 API long long mfx_launch_count(void) { return g_launches.load(); }
 
 namespace mfx {
+int cluster_size();
+void cluster_size_set(int cl);
 void graph_cache_evict(const void *ws);
 size_t graph_cache_size();
 }
@@ -374,6 +376,11 @@ API mfx_status mfx_set_option(const char *key, int value)
         g_opt_asm.store(value ? 1 : 0);
         return MFX_OK;
     }
+    if (!strcmp(key, "cluster_size")) {
+        MFX_ARG_CHECK(value == 8 || value == 16, "cluster_size must be 8 or 16");
+        cluster_size_set(value);
+        return MFX_OK;
+    }
     set_error("unknown option '%s'", key);
     return MFX_ERR_ARG;
 }
@@ -385,5 +392,6 @@ API int mfx_get_option(const char *key)
     if (!strcmp(key, "graphs")) return opt_graphs();
     if (!strcmp(key, "pdl")) return opt_pdl();
     if (!strcmp(key, "asm_tma")) return opt_asm_tma();
+    if (!strcmp(key, "cluster_size")) return cluster_size();
     return -1;
 }

@@ -1,41 +1,42 @@
 // bicg_cluster.cu -- a-6 for small systems (BASELINE.json configuration 1,
 // 16x16x32): the whole unpreconditioned BiCGSTAB solve in
-// ONE launch of one thread-block cluster of 8 CTAs (8 SMs).
+// ONE launch of one thread-block cluster of CL CTAs (16 SMs, the
+// non-portable maximum on B200; 8 where a 16-CTA cluster cannot be placed).
 //
-// The grid is split into 8 z-slabs; CTA `rank` keeps its slab of every
-// coefficient and vector in shared memory for the whole solve, reads the z
-// halo planes of its neighbours through distributed shared memory
-// (map_shared_rank), and replaces the grid-wide reductions of the large-N
-// kernels by cluster barriers: each CTA publishes its double-double partial,
-// barrier.cluster, and every CTA folds the 8 partials in rank order, so all
-// CTAs take identical scalar decisions (correctly rounded dots, §3.1).
-// Five cluster barriers per iteration; no kernel launches inside the loop.
-#include <cooperative_groups.h>
-
+// The grid is split into CL z-slabs; CTA `rank` keeps its slab of every
+// coefficient and vector in shared memory for the whole solve.  Nothing in the
+// iteration loop uses barrier.cluster: every cross-CTA transfer is a PUSH --
+// st.async remote stores into the consumer CTA's shared memory that complete
+// a transaction count on the consumer's own mbarrier -- so a consumer waits
+// exactly for the bytes it needs, and no CTA ever reads remote memory:
+//   * z halos: the thread that updates a cell of a slab's first/last plane
+//     (p in the K1 update, s in the K2 update) also stores it into the
+//     neighbour's halo plane (one mbarrier per halo vector);
+//   * reductions: lane butterfly per warp, one warp folds the CTA's warp
+//     partials, and its first CL lanes store the CTA partial into slot `rank`
+//     of every CTA (double-buffered slots, one mbarrier per buffer); each CTA
+//     then folds the CL partials in rank order, so all CTAs take identical
+//     scalar decisions (correctly rounded dots, §3.1).
+// Reuse of a buffer is safe without a barrier because a CTA can only push into
+// a buffer's next use after every CTA has pushed the intervening transfer,
+// i.e. after every CTA has consumed this one (program order: consume, then
+// push the next).  mbarrier tx counts may run negative when remote bytes land
+// before the local arm (expect_tx), which the PTX semantics allow.
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
-
-namespace cg = cooperative_groups;
+#include "tma.cuh"
 
 namespace mfx {
 
 namespace {
 
-constexpr int CL = 8;     // CTAs per cluster (portable maximum)
-constexpr int CT = 256;   // threads per CTA
-
-// Cluster barrier for shared-memory exchange.  cg::cluster_group::sync()
-// (barrier.cluster.arrive.release) compiles to MEMBAR.ALL.GPU on sm_100a;
-// everything exchanged here lives in shared memory, so a CTA barrier (which
-// drains this CTA's pending shared stores) followed by a relaxed cluster
-// arrive / wait orders the writes before any remote DSMEM read.
-__device__ __forceinline__ void cluster_barrier()
-{
-    __syncthreads();
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-}
+#ifndef MFX_CL_CT
+#define MFX_CL_CT 256
+#endif
+constexpr int CT = MFX_CL_CT;   // threads per CTA (B200, c1: 256 -> 6.4 us per iteration, 512 -> 7.2 us)
+constexpr int NW = CT / 32;
 
 struct ClArgs {
     int nx, ny, nz;
@@ -48,70 +49,77 @@ struct ClArgs {
     long long *trace;      // optional: clock64 stamps of CTA 0 per phase (MFX_CLUSTER_TRACE)
 };
 
-// Cluster-wide correctly rounded reduction of K double-doubles: each warp
-// publishes its butterfly partial; after barrier.cluster the 64 partials
-// (8 CTAs x 8 warps) of each value are gathered in parallel into local
-// shared memory and folded by one warp in a fixed order, so every CTA gets
-// the identical result.  Publication slots alternate between two buffers
-// (the barrier of reduction j+1 orders all remote reads of reduction j
-// before any CTA overwrites its slots in reduction j+2).
+// Cluster-wide correctly rounded reduction of K double-doubles (push model,
+// see the file comment); every thread of every CTA gets the same out[].
+template <int CL>
 struct ClusterRed {
-    dd (*pub)[3][8];       // [2][3][8] this CTA's per-warp partials
-    dd (*tmp)[64];         // [3][64] gathered partials
-    dd *bc;                // [3] folded results
+    dd (*wpart)[NW];       // [3][NW] this CTA's warp partials
+    dd (*red)[3][CL];      // [2][3][CL] pushed CTA partials
+    uint64_t *mb;          // [2] one mbarrier per buffer
+    uint32_t dst;          // lane j < CL: address of red[0][0][rank] in CTA j
+    uint32_t bar0, bar1;   // lane j < CL: CTA j's mbarriers
+    double (*bc)[3];       // [2][3] folded results (double-buffered: no barrier before the next write)
+    uint32_t ph0 = 0, ph1 = 0;   // (scalars, not arrays indexed by buf: no local memory)
+    int buf = 0;
     template <int K>
-    __device__ void run(cg::cluster_group &cl, int &buf, dd (&v)[K], double (&out)[K])
+    __device__ __forceinline__ void run(dd (&v)[K], double (&out)[K])
     {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        dd x[K];
-#pragma unroll
-        for (int q = 0; q < K; q++) x[q] = v[q];
-        // the K butterflies advance level by level (independent chains interleave)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            dd y[K];
-#pragma unroll
-            for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
-#pragma unroll
-            for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
-        }
+        butterfly_lazy<K, 32>(v);
         if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < K; q++) pub[buf][q][wid] = x[q];
-        cluster_barrier();
-        if (threadIdx.x < 64 * K) {
-            const int q = threadIdx.x >> 6, idx = threadIdx.x & 63;
-            tmp[q][idx] = *cl.map_shared_rank(&pub[buf][q][idx & 7], idx >> 3);
-        }
+            for (int q = 0; q < K; q++) wpart[q][wid] = v[q];
         __syncthreads();
         if (wid == 0) {
+            dd y[K];
 #pragma unroll
-            for (int q = 0; q < K; q++) x[q] = dd_add_fast(tmp[q][lane], tmp[q][lane + 32]);
+            for (int q = 0; q < K; q++) y[q] = wpart[q][lane & (NW - 1)];
+            butterfly_lazy<K, NW>(y);
+            // always 3 slots (zeros beyond K): every use of a buffer carries the
+            // same byte count, so its mbarrier is re-armed right after each use
+            if (lane < CL)
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                dd y[K];
+                for (int q = 0; q < 3; q++)
+                    push_f64x2(dst + (uint32_t)((buf * 3 + q) * CL * 16), q < K ? y[q].hi : 0.0, q < K ? y[q].lo : 0.0,
+                               buf ? bar1 : bar0);
+        }
+        if (buf) { mbar_wait_cluster(&mb[1], ph1); ph1 ^= 1u; }
+        else { mbar_wait_cluster(&mb[0], ph0); ph0 ^= 1u; }
+        // arm the buffer's next use now: no CTA can push into it before this
+        // CTA has pushed the next reduction (so the arm precedes every push)
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&mb[buf], (uint32_t)(CL * 3 * 16));
+#ifdef MFX_CL_ALLFOLD
+        dd y[K];
 #pragma unroll
-                for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+        for (int q = 0; q < K; q++) y[q] = red[buf][q][lane & (CL - 1)];
+        butterfly_lazy<K, CL>(y);   // every group of CL lanes folds the same slots in the same order
 #pragma unroll
-                for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
-            }
+        for (int q = 0; q < K; q++) out[q] = dd_round(y[q]);
+#else
+        // one warp folds the CL partials, the others wait at the CTA barrier
+        // (16 warps folding redundantly contend for the fp64 pipe)
+        if (wid == 0) {
+            dd y[K];
+#pragma unroll
+            for (int q = 0; q < K; q++) y[q] = red[buf][q][lane & (CL - 1)];
+            butterfly_lazy<K, CL>(y);
             if (lane == 0)
 #pragma unroll
-                for (int q = 0; q < K; q++) bc[q] = x[q];
+                for (int q = 0; q < K; q++) bc[buf][q] = dd_round(y[q]);
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < K; q++) out[q] = dd_round(bc[q]);
+        for (int q = 0; q < K; q++) out[q] = bc[buf][q];
+#endif
         buf ^= 1;
     }
 };
 
-template <bool SYM>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
+template <bool SYM, int CL>
+__global__ void __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
 {
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = (int)cl.block_rank();
-    const int tid = threadIdx.x;
+    const int rank = (int)cl_rank();
+    const int tid = threadIdx.x, lane = tid & 31;
     constexpr int NA = SYM ? 3 : 7;
     extern __shared__ __align__(16) double smd[];
     const int M = a.M;
@@ -119,11 +127,20 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     double *b = C + NA * M;
     double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
     __shared__ int k0s[CL + 1];
-    __shared__ dd pub[2][3][8];
-    __shared__ dd tmp[3][64];
-    __shared__ dd bc[3];
+    __shared__ __align__(16) dd wpart[3][NW];     // this CTA's warp partials
+    __shared__ __align__(16) dd red[2][3][CL];    // pushed CTA partials, double-buffered
+    __shared__ double bcast[2][3];                // folded results
+    __shared__ __align__(8) uint64_t mb_red[2], mb_halo[2];   // reductions; halo planes of p / s
     const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
     if (tid <= CL) k0s[tid] = (int)((long long)nz * tid / CL);
+    if (tid == 0) {
+        mbar_init(&mb_red[0], 1); mbar_init(&mb_red[1], 1);
+        mbar_init(&mb_halo[0], 1); mbar_init(&mb_halo[1], 1);
+        // first phases armed before any CTA can push (the setup cluster barrier)
+        mbar_arrive_expect_tx(&mb_red[0], (uint32_t)(CL * 3 * 16));
+        mbar_arrive_expect_tx(&mb_red[1], (uint32_t)(CL * 3 * 16));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const int k0 = k0s[rank], k1 = k0s[rank + 1];
     const int npl = k1 - k0, nc = npl * plane;
@@ -138,6 +155,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             if (k0s[q] <= k1 && k1 < k0s[q + 1]) ra = q;
     const int lb = rb >= 0 ? (k0 - 1 - k0s[rb]) * plane : 0;   // offset of plane k0-1 in rb's slab
     const int la = ra >= 0 ? (k1 - k0s[ra]) * plane : 0;       // offset of plane k1 in ra's slab
+    // halo bytes this CTA receives per halo transfer
+    const uint32_t halo_bytes = (uint32_t)(((rb >= 0) + (ra >= 0)) * plane * 8);
 
     for (int i = tid; i < nc; i += CT) {
         if (SYM) {
@@ -156,10 +175,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         b[i] = a.b[g0 + i];
         x[i] = a.x[g0 + i];
     }
-    ClusterRed R{pub, tmp, bc};
-    int buf = 0;   // parity of the publication slots, shared by all reductions
-    double *hb = t + M, *ha = hb + plane;                 // local copies of the z-halo planes
-    double *czb = ha + plane;                             // cz of plane k0-1 (SYM)
+    // halo planes: [vector 0 = p (and x at setup) | 1 = s][below | above]
+    double *hal = t + M;
+    double *czb = hal + 4 * plane;                        // cz of plane k0-1 (SYM)
     int *cf = (int *)(czb + plane);                       // per-cell neighbour flags | in-plane offset << 8
     for (int i = tid; i < nc; i += CT) {
         const int kl = i / plane, o = i - kl * plane;
@@ -176,9 +194,31 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         if (kl < npl - 1) f |= 128;
         cf[i] = f | (o << 8);
     }
+    // remote addresses: the neighbour below receives my first plane into its
+    // "above" halo, the neighbour above my last plane into its "below" halo
+    const uint32_t hal_u = smem_u32(hal);
+    // (halo vector h's planes sit 2 h planes apart, its mbarrier 8 h bytes apart)
+    uint32_t dst_b = 0, dst_a = 0, bar_b = 0, bar_a = 0;
+    if (rb >= 0) {
+        dst_b = mapa_u32(hal_u + (uint32_t)(plane * 8), rb);
+        bar_b = mapa_u32(smem_u32(&mb_halo[0]), rb);
+    }
+    if (ra >= 0) {
+        dst_a = mapa_u32(hal_u, ra);
+        bar_a = mapa_u32(smem_u32(&mb_halo[0]), ra);
+    }
+    uint32_t red_dst = 0, red_bar[2] = {0, 0};   // lane j < CL of the folding warp pushes to CTA j
+    if (lane < CL) {
+        red_dst = mapa_u32(smem_u32(&red[0][0][rank]), lane);
+        red_bar[0] = mapa_u32(smem_u32(&mb_red[0]), lane);
+        red_bar[1] = mapa_u32(smem_u32(&mb_red[1]), lane);
+    }
+    uint32_t ph_halo0 = 0, ph_halo1 = 0;
 
-    // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X read with its z halo
-    auto apply = [&](const double *X, int i) -> double {
+    ClusterRed<CL> R{wpart, red, mb_red, red_dst, red_bar[0], red_bar[1], bcast};
+
+    // y = A X at own cell i (DESIGN.md §3.2 order W,E,S,N,B,T); X's z halo in hb / ha
+    auto apply = [&](const double *X, const double *hb, const double *ha, int i) -> double {
         const int f = cf[i], o = f >> 8;
         const double xc = X[i];
         const double xW = (f & 1) ? X[i - 1] : 0.0;
@@ -213,25 +253,45 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         y = fma(-aT, xT, y);
         return y;
     };
-    auto reduce1 = [&](Acc &a0, double &o0) {
-        dd vv[1] = {a0.get()};
-        double out[1];
-        R.run<1>(cl, buf, vv, out);
-        o0 = out[0];
+    // a slab-boundary value of halo vector h goes to the neighbours' halo planes
+    auto push_halo = [&](int h, int i, double val) {
+        const int kl = i / plane, o = i - kl * plane;
+#ifdef MFX_CL_PULL
+        return;
+#endif
+        const uint32_t ho = (uint32_t)(h * 2 * plane * 8 + o * 8);
+        if (kl == 0 && rb >= 0) push_f64(dst_b + ho, val, bar_b + 8u * h);
+        if (kl == npl - 1 && ra >= 0) push_f64(dst_a + ho, val, bar_a + 8u * h);
     };
-    auto reduce2 = [&](Acc &a0, Acc &a1, double &o0, double &o1) {
-        dd vv[2] = {a0.get(), a1.get()};
-        double out[2];
-        R.run<2>(cl, buf, vv, out);
-        o0 = out[0]; o1 = out[1];
-    };
-    // after a cluster barrier: copy the neighbours' boundary planes of X locally
-    auto fetch_halo = [&](const double *X) {
-        for (int o = tid; o < plane; o += CT) {
-            if (rb >= 0) hb[o] = cl.map_shared_rank(X, rb)[lb + o];
-            if (ra >= 0) ha[o] = cl.map_shared_rank(X, ra)[la + o];
+    // halo mbarriers: armed for their first phase before the setup barrier and
+    // re-armed right after each wait (a neighbour pushes the next phase only
+    // after the following reduction, which waits for this CTA)
+    if (tid == 0 && halo_bytes) {
+        mbar_arrive_expect_tx(&mb_halo[0], halo_bytes);
+        mbar_arrive_expect_tx(&mb_halo[1], halo_bytes);
+    }
+    auto arm_halo = [&](int) {};
+    auto wait_halo = [&](int h) {
+        __syncthreads();   // in-slab neighbours
+#ifdef MFX_CL_PULL
+        {
+            cluster_sync_full();
+            const double *X = h ? s : p;
+            const double *xb = rb >= 0 ? (const double *)__cluster_map_shared_rank((void *)X, rb) : nullptr;
+            const double *xa = ra >= 0 ? (const double *)__cluster_map_shared_rank((void *)X, ra) : nullptr;
+            for (int o = tid; o < plane; o += CT) {
+                if (rb >= 0) hal[2 * h * plane + o] = xb[lb + o];
+                if (ra >= 0) hal[(2 * h + 1) * plane + o] = xa[la + o];
+            }
+            cluster_sync_full();
+            return;
         }
-        __syncthreads();
+#endif
+        if (halo_bytes) {
+            if (h) { mbar_wait_cluster(&mb_halo[1], ph_halo1); ph_halo1 ^= 1u; }
+            else { mbar_wait_cluster(&mb_halo[0], ph_halo0); ph_halo0 ^= 1u; }
+            if (tid == 0) mbar_arrive_expect_tx(&mb_halo[h], halo_bytes);
+        }
     };
 
     const double tol = a.tol;
@@ -243,24 +303,37 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
     int status = MFX_NOT_CONVERGED, iters = 0, restarts = 0;
     double bn, rr, rn;
 
-    // ---- setup: r = b - A x0
-    cluster_barrier();   // x0 and coefficients of every slab loaded
-    if (SYM)
-        for (int o = tid; o < plane; o += CT) czb[o] = rb >= 0 ? cl.map_shared_rank(C + 2 * M, rb)[lb + o] : 0.0;
-    fetch_halo(x);
+    // ---- setup: r = b - A x0 (x0 and cz halos read once over DSMEM after a full barrier)
+    cluster_sync_full();   // x0, coefficients and mbarriers of every CTA initialised
+    {
+        const double *xr_b = rb >= 0 ? (const double *)__cluster_map_shared_rank((void *)x, rb) : nullptr;
+        const double *xr_a = ra >= 0 ? (const double *)__cluster_map_shared_rank((void *)x, ra) : nullptr;
+        const double *cz_b = (SYM && rb >= 0) ? (const double *)__cluster_map_shared_rank((void *)(C + 2 * M), rb)
+                                              : nullptr;
+        for (int o = tid; o < plane; o += CT) {
+            if (rb >= 0) hal[o] = xr_b[lb + o];
+            if (ra >= 0) hal[plane + o] = xr_a[la + o];
+            if (SYM) czb[o] = rb >= 0 ? cz_b[lb + o] : 0.0;
+        }
+    }
+    __syncthreads();   // halo planes and cz below filled before any thread applies A
+    // (no second cluster barrier: a neighbour pushes p into these halo planes only
+    // after the setup reduction, which waits for this CTA's push, issued after its reads)
     {
         Acc bb, ra_;
         bb.zero(); ra_.zero();
         for (int i = tid; i < nc; i += CT) {
-            const double y = apply(x, i);
+            const double y = apply(x, hal, hal + plane, i);
             const double rv = b[i] - y;
             r[i] = rv;
             bb.prod(b[i], b[i]);
             ra_.prod(rv, rv);
         }
-        double bbv;
-        reduce2(bb, ra_, bbv, rr);
-        bn = sqrt(bbv);
+        dd vv[2] = {bb.get(), ra_.get()};
+        double out[2];
+        R.template run<2>(vv, out);
+        bn = sqrt(out[0]);
+        rr = out[1];
         rn = sqrt(rr);
     }
     if (bn == 0.0) {
@@ -270,49 +343,60 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         status = MFX_OK;
     } else {
         for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
-        double rhn = rn, rho = rr, rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+        double rhn = rn, rho = rr, rho_prev = 1.0, alpha = 1.0, omega = 1.0, aw = 1.0;   // aw = alpha / omega
         bool restarted = false;
         int it;
         for (it = 1; it <= maxit; it++) {
             if (fabs(rho) <= (1e-14 * rhn) * rn) {
                 if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it - 1; break; }
                 for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
-                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+                rhn = rn; rho = rr; rho_prev = alpha = omega = aw = 1.0; restarted = true; restarts++;
             }
             stamp();
-            const double beta = (rho / rho_prev) * (alpha / omega);
-            for (int i = tid; i < nc; i += CT) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
+            const double beta = (rho / rho_prev) * aw;
+            arm_halo(0);
+            for (int i = tid; i < nc; i += CT) {
+                const double pv = fma(beta, fma(-omega, v[i], p[i]), r[i]);
+                p[i] = pv;
+                push_halo(0, i, pv);
+            }
             stamp();
-            cluster_barrier();   // p of every slab visible
-            stamp();
-            fetch_halo(p);
+            wait_halo(0);   // p of this slab and of the neighbours' boundary planes
             stamp();
             Acc sg;
             sg.zero();
             for (int i = tid; i < nc; i += CT) {
-                const double vv = apply(p, i);
+                const double vv = apply(p, hal, hal + plane, i);
                 v[i] = vv;
                 sg.prod(rh[i], vv);
             }
             double sigma;
             stamp();
-            reduce1(sg, sigma);
+            {
+                dd vv[1] = {sg.get()};
+                double out[1];
+                R.template run<1>(vv, out);
+                sigma = out[0];
+            }
             stamp();
             if (sigma == 0.0) {
                 if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it; break; }
                 for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
-                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+                rhn = rn; rho = rr; rho_prev = alpha = omega = aw = 1.0; restarted = true; restarts++;
                 continue;
             }
             alpha = rho / sigma;
-            for (int i = tid; i < nc; i += CT) s[i] = fma(-alpha, v[i], r[i]);
-            cluster_barrier();   // s of every slab visible
-            fetch_halo(s);
-            stamp();
+            arm_halo(1);
+            for (int i = tid; i < nc; i += CT) {
+                const double sv = fma(-alpha, v[i], r[i]);
+                s[i] = sv;
+                push_halo(1, i, sv);
+            }
+            wait_halo(1);
             Acc ts, tt, ss;
             ts.zero(); tt.zero(); ss.zero();
             for (int i = tid; i < nc; i += CT) {
-                const double tv = apply(s, i);
+                const double tv = apply(s, hal + 2 * plane, hal + 3 * plane, i);
                 t[i] = tv;
                 ts.prod(tv, s[i]);
                 tt.prod(tv, tv);
@@ -323,9 +407,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             {
                 dd vv[3] = {ts.get(), tt.get(), ss.get()};
                 double out[3];
-                R.run<3>(cl, buf, vv, out);
+                R.template run<3>(vv, out);
                 tsv = out[0]; ttv = out[1]; ssv = out[2];
             }
+            stamp();
             if (sqrt(ssv) <= tol * bn) {
                 for (int i = tid; i < nc; i += CT) { x[i] = fma(alpha, p[i], x[i]); r[i] = s[i]; }
                 rn = sqrt(ssv);
@@ -336,10 +421,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             if (ttv == 0.0 || om == 0.0) {
                 if (restarted) { status = MFX_ERR_BREAKDOWN; iters = it; break; }
                 for (int i = tid; i < nc; i += CT) { rh[i] = r[i]; p[i] = 0.0; v[i] = 0.0; }
-                rhn = rn; rho = rr; rho_prev = alpha = omega = 1.0; restarted = true; restarts++;
+                rhn = rn; rho = rr; rho_prev = alpha = omega = aw = 1.0; restarted = true; restarts++;
                 continue;
             }
             omega = om;
+            aw = alpha / omega;   // beta's second quotient, off the critical path after the next reduction
             Acc rhr, rra;
             rhr.zero(); rra.zero();
             for (int i = tid; i < nc; i += CT) {
@@ -352,8 +438,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
             }
             rho_prev = rho;
             stamp();
-            reduce2(rhr, rra, rho, rr);
-            stamp();
+            {
+                dd vv[2] = {rhr.get(), rra.get()};
+                double out[2];
+                R.template run<2>(vv, out);
+                rho = out[0]; rr = out[1];
+            }
             rn = sqrt(rr);
             if (rn <= tol * bn) { status = MFX_OK; iters = it; break; }
         }
@@ -365,10 +455,55 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) k_bicg_cluster(
         S.it = iters; S.status = status; S.restarts = restarts; S.rn = rn; S.bn = bn; S.done = 1;
         S.tol = tol; S.maxit = maxit;
     }
-    cluster_barrier();   // keep every CTA's shared memory alive until all remote reads are done
+    // every push into this CTA's shared memory has completed (each was waited
+    // for); keep it alive until every CTA is done as well
+    cluster_sync_full();
+}
+
+// cluster size: 16 where the device can place a 16-CTA cluster of this
+// kernel, else 8 (portable); MFX_CLUSTER=8 forces the portable size
+int g_cl = 0;
+
+template <bool SYM, int CL>
+bool cluster_can_launch(size_t smem)
+{
+    auto kfn = k_bicg_cluster<SYM, CL>;
+    if (CL > 8 && cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL); cfg.blockDim = dim3(CT); cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return n >= 1;
 }
 
 }  // namespace
+
+int cluster_size()
+{
+    if (g_cl == 0) {
+        const char *e = getenv("MFX_CLUSTER");
+        int want = e ? atoi(e) : 16;
+        if (want != 8) want = cluster_can_launch<true, 16>(200 * 1024) && cluster_can_launch<false, 16>(200 * 1024)
+                              ? 16 : 8;
+        g_cl = want;
+    }
+    return g_cl;
+}
+void cluster_size_set(int cl) { g_cl = cl; }
 
 long long *&cluster_trace_ptr()
 {
@@ -376,15 +511,32 @@ long long *&cluster_trace_ptr()
     return p;
 }
 
-// dynamic smem: (NA + 8) arrays of M cells + 3 planes (two halo copies, cz below)
+// dynamic smem: (NA + 8) arrays of M cells + 5 planes (four halo planes, cz below) + M flags
 size_t cluster_smem(const Geo &G, bool sym)
 {
     const long long plane = (long long)G.nx * G.ny;
+    const int CL = cluster_size();
     const long long M = plane * ((G.nz + CL - 1) / CL);
-    return (size_t)(((sym ? 11 : 15) * M + 3 * plane) * sizeof(double) + M * sizeof(int));
+    return (size_t)(((sym ? 11 : 15) * M + 5 * plane) * sizeof(double) + M * sizeof(int));
 }
 
 bool cluster_fits(const Geo &G, bool sym) { return cluster_smem(G, sym) <= 200 * 1024; }
+
+template <bool SYM, int CL>
+static mfx_status cluster_launch(const ClArgs &a, size_t smem, cudaStream_t s)
+{
+    auto kfn = k_bicg_cluster<SYM, CL>;
+    if (CL > 8) MFX_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    MFX_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL); cfg.blockDim = dim3(CT); cfg.dynamicSmemBytes = smem; cfg.stream = s;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kfn, a));
+    return MFX_OK;
+}
 
 mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, double tol, int maxit,
                          WsHeader *h, cudaStream_t s)
@@ -401,25 +553,24 @@ mfx_status cluster_solve(bool sym, const Geo &G, const mfx_eqsys *A, double *x, 
         a.trace = tr;
         cluster_trace_ptr() = tr;
     }
+    const int CL = cluster_size();
     a.M = G.nx * G.ny * ((G.nz + CL - 1) / CL);
     const size_t smem = cluster_smem(G, sym);
-    if (sym) {
-        MFX_CUDA_TRY(cudaFuncSetAttribute(k_bicg_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_bicg_cluster<true><<<CL, CT, smem, s>>>(a);
-    } else {
-        MFX_CUDA_TRY(cudaFuncSetAttribute(k_bicg_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_bicg_cluster<false><<<CL, CT, smem, s>>>(a);
-    }
+    mfx_status st;
+    if (CL == 16) st = sym ? cluster_launch<true, 16>(a, smem, s) : cluster_launch<false, 16>(a, smem, s);
+    else st = sym ? cluster_launch<true, 8>(a, smem, s) : cluster_launch<false, 8>(a, smem, s);
+    if (st != MFX_OK) return st;
     MFX_CUDA_TRY(cudaGetLastError());
     if (a.trace) {   // debug: per-phase cycle deltas of CTA 0 for the first iterations
-        long long h[512];
-        cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+        long long hh[512];
+        cudaMemcpyAsync(hh, a.trace, sizeof(hh), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        fprintf(stderr, "cluster trace (cycles): p-update bar halo apply1 red1 s+bar+halo+apply2 red3 k3 red2\n");
-        for (int it = 0; it < 8 && h[it * 10 + 9] != 0; it++) {
+        fprintf(stderr, "cluster trace (CL %d, cycles): p-update halo-wait apply1 red1 s+halo+apply2 red3 k3 red2\n",
+                CL);
+        for (int it = 0; it < 8 && hh[it * 8 + 7] != 0; it++) {
             fprintf(stderr, "  it %d:", it + 1);
-            for (int q = 1; q < 10; q++) fprintf(stderr, " %lld", h[it * 10 + q] - h[it * 10 + q - 1]);
-            if (h[(it + 1) * 10] != 0) fprintf(stderr, " | total %lld", h[(it + 1) * 10] - h[it * 10]);
+            for (int q = 1; q < 8; q++) fprintf(stderr, " %lld", hh[it * 8 + q] - hh[it * 8 + q - 1]);
+            if (hh[(it + 1) * 8] != 0) fprintf(stderr, " | total %lld", hh[(it + 1) * 8] - hh[it * 8]);
             fprintf(stderr, "\n");
         }
     }

@@ -102,6 +102,20 @@ __device__ __forceinline__ dd dd_add_fast(dd x, dd y)
     return r;
 }
 
+// Lazy double-double add for reduction trees: TwoSum of the heads, the tails
+// and the TwoSum error added plainly, no renormalisation.  The heads' chain is
+// one add per tree level (the tails follow off the critical path), so a level
+// costs a shuffle and two dependent adds instead of the ~9-add chain of
+// dd_add_fast.  The error stays in the same O(depth u^2 sum|partials|) class:
+// every head error is captured exactly, the tails (each <= u |head|) are
+// summed with relative error u.
+__device__ __forceinline__ dd dd_add_lazy(dd x, dd y)
+{
+    double s, e;
+    two_sum(x.hi, y.hi, s, e);
+    return dd{s, (x.lo + y.lo) + e};
+}
+
 // Per-thread accumulator: s + c with s the running TwoSum head.
 struct Acc {
     double s, c;
@@ -154,6 +168,37 @@ __device__ __forceinline__ void butterfly_dd1(dd &x)
     for (int off = 16; off > 0; off >>= 1) {
         const dd y = shfl_dd(x, off);
         x = (lane & off) ? dd_add_fast(y, x) : dd_add_fast(x, y);
+    }
+}
+
+// butterfly over the lanes of a warp with Dekker's double-double add, the K
+// chains interleaved level by level; every lane ends with the same bits
+template <int K, int W>
+__device__ __forceinline__ void butterfly_k(dd (&x)[K])
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        dd y[K];
+#pragma unroll
+        for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+        for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_fast(y[q], x[q]) : dd_add_fast(x[q], y[q]);
+    }
+}
+
+// the same butterfly with lazy adds (every lane ends with the same bits)
+template <int K, int W>
+__device__ __forceinline__ void butterfly_lazy(dd (&x)[K])
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        dd y[K];
+#pragma unroll
+        for (int q = 0; q < K; q++) y[q] = shfl_dd(x[q], off);
+#pragma unroll
+        for (int q = 0; q < K; q++) x[q] = (lane & off) ? dd_add_lazy(y[q], x[q]) : dd_add_lazy(x[q], y[q]);
     }
 }
 

@@ -1023,7 +1023,128 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
     for (int d = 0; d < K; d++) out[d] = f[d];
 }
 
-template <int CPT, int S>
+// Cluster-hierarchical all-reduce (CLP > 1 CTAs per cluster; DESIGN.md §7
+// "persistent"): per value a lane butterfly, warp 0 folds the CTA's warp
+// partials and pushes the CTA partial into the cluster leader's shared memory
+// (st.async + the leader's mbarrier); the leader folds its CLP partials,
+// publishes one partial per cluster and is the only CTA to arrive on the
+// global counter and spin; after the release it folds the NC cluster
+// partials in cluster order and pushes the result into every member's shared
+// memory (st.async + the member's mbarrier).  Every CTA gets the same bits.
+// Buffer reuse needs no barrier: a member pushes reduction j+1 only after it
+// received result j, which the leader sends after consuming partials j; a
+// leader publishes j+2 into the global double buffer only after release j+1,
+// i.e. after every leader has read the partials of j.
+struct ClRed {
+    dd (*wsh)[16];          // [3][16] warp partials (slots >= NW stay zero)
+    dd (*lred)[3][16];      // [2][3][CLP] leader: pushed CTA partials
+    dd (*res)[3];           // [2][3] result (pushed by the leader; written locally in the leader)
+    uint64_t *mb;           // [4]: leader receive [0..1], member receive [2..3]
+    uint32_t dst_l;         // warp 0 lane 0: address of lred[0][0][rank] in the leader
+    uint32_t bar_l;         // ... and of the leader's mb[0]
+    uint32_t dst_m, bar_m;  // leader lane j < CLP: res[0][0] and mb[2] of member j
+    uint32_t ph = 0;        // per-buffer phase bits: bit b = leader receive b, bit 2+b = member receive b
+};
+
+template <int K, int CPT, int CLP>
+__device__ __forceinline__ void cluster_allreduce(const Acc (&acc)[3][CPT], dd *cpart, unsigned *arrive,
+                                                  unsigned &phase, ClRed &R, dd (&out)[K], const PersistArgs &P,
+                                                  int it, int slot)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rank = (int)cl_rank();
+    const int b = (int)(phase & 1);
+    if (tid == 0) {
+        if (rank == 0) mbar_arrive_expect_tx(&R.mb[b], (uint32_t)(CLP * K * 16));
+        else mbar_arrive_expect_tx(&R.mb[2 + b], (uint32_t)(K * 16));
+    }
+    dd v[K];
+#pragma unroll
+    for (int d = 0; d < K; d++) {
+        v[d] = acc[d][0].get();
+#pragma unroll
+        for (int m = 1; m < CPT; m++) v[d] = dd_add(v[d], acc[d][m].get());
+    }
+    if (K != 3) asm volatile("fence.proxy.async.global;" ::: "memory");
+    butterfly_k<K, 32>(v);
+    if (lane == 0)
+#pragma unroll
+        for (int d = 0; d < K; d++) R.wsh[d][warp] = v[d];
+    __syncthreads();   // every store of the pass precedes the CTA's partial
+    ptrace(P, it, slot);
+    if (warp == 0) {
+        dd y[K];
+#pragma unroll
+        for (int d = 0; d < K; d++) y[d] = R.wsh[d][lane & 15];
+        butterfly_k<K, 16>(y);
+        if (lane == 0) {
+            __threadfence();   // this CTA's global stores before the leader's publication
+#pragma unroll
+            for (int d = 0; d < K; d++) push_f64x2(R.dst_l + (uint32_t)((b * 3 + d) * 16 * 16), y[d].hi, y[d].lo, R.bar_l + 8u * b);
+        }
+    }
+    if (rank == 0) {
+        if (warp == 0) {
+            mbar_wait_cluster(&R.mb[b], (R.ph >> b) & 1u);
+            dd y[K];
+#pragma unroll
+            for (int d = 0; d < K; d++) y[d] = R.lred[b][d][lane & (CLP - 1)];
+            butterfly_k<K, CLP>(y);
+            const int nc = gridDim.x / CLP, me = blockIdx.x / CLP;
+            dd *pb = cpart + (size_t)b * nc * 3;
+            if (lane == 0) {
+#pragma unroll
+                for (int d = 0; d < K; d++) pb[(size_t)me * 3 + d] = y[d];
+                __threadfence();
+                atomicAdd(arrive, 1u);
+                const unsigned target = (phase + 1) * (unsigned)nc;
+                if (ld_acquire_u32(arrive) < target) {
+                    unsigned long long t0;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                    while (ld_acquire_u32(arrive) < target) {
+                        __nanosleep(20);
+                        unsigned long long t1;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                        if (t1 - t0 > 20000000000ull) __trap();   // 20 s: a cluster is missing (never expected)
+                    }
+                }
+            }
+            __syncwarp();
+            ptrace(P, it, slot + 1);
+            dd f[K];
+#pragma unroll
+            for (int d = 0; d < K; d++) f[d] = dd{0.0, 0.0};
+            for (int c = lane; c < nc; c += 32) {
+#pragma unroll
+                for (int d = 0; d < K; d++) {
+                    dd x;
+                    x.hi = __ldcg(&pb[(size_t)c * 3 + d].hi);
+                    x.lo = __ldcg(&pb[(size_t)c * 3 + d].lo);
+                    f[d] = dd_add(f[d], x);
+                }
+            }
+            butterfly_k<K, 32>(f);
+            if (lane == 0)
+#pragma unroll
+                for (int d = 0; d < K; d++) R.res[b][d] = f[d];
+            if (lane >= 1 && lane < CLP)
+#pragma unroll
+                for (int d = 0; d < K; d++)
+                    push_f64x2(R.dst_m + (uint32_t)((b * 3 + d) * 16), f[d].hi, f[d].lo, R.bar_m + 8u * b);
+        }
+        R.ph ^= 1u << b;
+        __syncthreads();
+    } else {
+        mbar_wait_cluster(&R.mb[2 + b], (R.ph >> (2 + b)) & 1u);
+        R.ph ^= 1u << (2 + b);
+        ptrace(P, it, slot + 1);
+    }
+    phase++;
+#pragma unroll
+    for (int d = 0; d < K; d++) out[d] = R.res[b][d];
+}
+
+template <int CPT, int S, int CLP>
 __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constant__ PersistArgs P)
 {
     constexpr int TX = 32 * CPT, TY = 8;
@@ -1037,6 +1158,26 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
     __shared__ SolverScalars Ls;
     __shared__ dd sh[(C1::NW + 1) * 3];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // cluster all-reduce state (CLP > 1)
+    constexpr int CLS = CLP > 1 ? CLP : 1;
+    __shared__ __align__(16) dd c_wsh[3][16];
+    __shared__ __align__(16) dd c_lred[2][3][16];
+    __shared__ __align__(16) dd c_res[2][3];
+    __shared__ __align__(8) uint64_t c_mb[4];
+    ClRed R;
+    if constexpr (CLP > 1) {
+        static_assert(CLP <= 16 && (CLP & (CLP - 1)) == 0, "cluster size: a power of two <= 16");
+        static_assert(C1::NW + 1 <= 16, "warp partial slots");
+        if (tid < 3 * 16) c_wsh[tid / 16][tid % 16] = dd{0.0, 0.0};
+        if (tid == 0)
+            for (int q = 0; q < 4; q++) mbar_init(&c_mb[q], 1);
+        const uint32_t rank = cl_rank();
+        R.wsh = c_wsh; R.lred = c_lred; R.res = c_res; R.mb = c_mb;
+        R.dst_l = mapa_u32(smem_u32(&c_lred[0][0][rank]), 0);
+        R.bar_l = mapa_u32(smem_u32(&c_mb[0]), 0);
+        R.dst_m = mapa_u32(smem_u32(&c_res[0][0]), (uint32_t)(lane % CLS));
+        R.bar_m = mapa_u32(smem_u32(&c_mb[2]), (uint32_t)(lane % CLS));
+    }
     if (tid == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
@@ -1046,6 +1187,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
         Ls = P.h->sc;
     }
     __syncthreads();
+    if constexpr (CLP > 1) cluster_sync_full();   // every member's mbarriers initialised before any push
     const bool producer = warp == C1::NW;
     int q = 0;
     unsigned phase = 0;
@@ -1077,7 +1219,8 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
             rw_consume<SM_K1, CPT, S, STRIDE>(P.a1[par], 0.0, P1.beta, P1.omega, P1.rst, acc, stages, full, empty, q);
         }
         ptrace(P, it, 1);
-        grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out, P, it, 2);
+        if constexpr (CLP > 1) cluster_allreduce<1, CPT, CLS>(acc, P.part, P.arrive, phase, R, (dd(&)[1])out, P, it, 2);
+        else grid_allreduce<1, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[1])out, P, it, 2);
         ptrace(P, it, 4);
         if (tid == 0) bicg_k1_tail(Ls, P1, dd_round(out[0]));
         __syncthreads();
@@ -1097,7 +1240,8 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
             rw_consume<SM_K2, CPT, S, STRIDE>(P.a2[par], alpha, 0.0, 0.0, false, acc, stages, full, empty, q);
         }
         ptrace(P, it, 5);
-        grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out, P, it, 6);
+        if constexpr (CLP > 1) cluster_allreduce<3, CPT, CLS>(acc, P.part, P.arrive, phase, R, out, P, it, 6);
+        else grid_allreduce<3, CPT>(acc, P.part, P.arrive, phase, sh, out, P, it, 6);
         ptrace(P, it, 8);
         if (tid == 0) bicg_k2_tail(Ls, dd_round(out[0]), dd_round(out[1]), dd_round(out[2]));
         __syncthreads();
@@ -1169,13 +1313,15 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
             }
         }
         ptrace(P, it, 9);
-        grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out, P, it, 10);
+        if constexpr (CLP > 1) cluster_allreduce<2, CPT, CLS>(acc, P.part, P.arrive, phase, R, (dd(&)[2])out, P, it, 10);
+        else grid_allreduce<2, CPT>(acc, P.part, P.arrive, phase, sh, (dd(&)[2])out, P, it, 10);
         ptrace(P, it, 12);
         if (tid == 0) bicg_k3_tail(Ls, half, dd_round(out[0]), dd_round(out[1]));
         __syncthreads();
     }
     __syncthreads();
     if (blockIdx.x == 0 && tid == 0) P.h->sc = Ls;
+    if constexpr (CLP > 1) cluster_sync_full();   // no CTA exits while a push into it may be in flight
 }
 
 // ------------------------------------------------------------------ host side
@@ -1394,20 +1540,38 @@ mfx_status run_mode(const Geo &G, const double *const halo[3], const double *con
     return run_tile<MODE, SYM, 64, 4, 1>(G, halo, coef, extra, a, s);
 }
 
-template <int CPT, int S>
+template <int CPT, int S, int CLP>
 struct PersistLauncher {
     static constexpr int TX = 32 * CPT, TY = 8;
     using C1 = Cfg<SM_K1, true, TX, TY, CPT>;
     using C2 = Cfg<SM_K2, true, TX, TY, CPT>;
     static constexpr int STRIDE = C1::STAGE_B > C2::STAGE_B ? C1::STAGE_B : C2::STAGE_B;
     static constexpr size_t smem() { return (size_t)S * STRIDE + 16 * (size_t)S; }
+    // co-resident grid: SMs x CTAs per SM, or (CLP > 1) the clusters the
+    // device can hold at once x CLP (0: a cluster of CLP cannot be placed)
     static int grid_size()
     {
-        static int g = 0;
-        if (g) return g;
-        cudaFuncSetAttribute(k_bicg_rw<CPT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        static int g = -1;
+        if (g >= 0) return g;
+        auto kfn = k_bicg_rw<CPT, S, CLP>;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        if (CLP > 1) {
+            if (CLP > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CLP; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(CLP); cfg.blockDim = dim3(C1::NT + 32); cfg.dynamicSmemBytes = smem();
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, kfn, &cfg) != cudaSuccess) { cudaGetLastError(); nc = 0; }
+            // the leaders' fold reads one partial per cluster per lane pass; keep it to <= 64 clusters
+            if (nc > 64) nc = 64;
+            g = nc * CLP;
+            return g;
+        }
         int occ = 0, dev = 0, sms = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bicg_rw<CPT, S>, C1::NT + 32, smem());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, C1::NT + 32, smem());
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         g = sms * (occ > 0 ? occ : 1);
@@ -1428,7 +1592,7 @@ struct PersistLauncher {
         a.kbeg = 0; a.kend = G.nz;
         a.Lz = choose_lz(ntiles, G.nz, grid);
         a.units = ntiles * ((G.nz + a.Lz - 1) / a.Lz);
-        if (grid > a.units) grid = (int)a.units;
+        if (grid > a.units) grid = CLP > 1 ? (int)((a.units + CLP - 1) / CLP) * CLP : (int)a.units;
         a.h = W.hdr; a.part = W.part;
         for (int par = 0; par < 2; par++) {
             const double *h1[3] = {W.r, W.p[par], W.v[par]};
@@ -1459,9 +1623,16 @@ struct PersistLauncher {
         cfg.blockDim = dim3(C1::NT + 32);
         cfg.dynamicSmemBytes = smem();
         cfg.stream = s;
+        // co-residency: a cooperative launch for the flat grid; for clusters the
+        // grid never exceeds what cudaOccupancyMaxActiveClusters reports
         cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
+        if (CLP > 1) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = CLP; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+        } else {
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+        }
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         static const int tr = env_int("MFX_PERSIST_TRACE", 0);
@@ -1470,7 +1641,7 @@ struct PersistLauncher {
             MFX_CUDA_TRY(cudaMalloc(&P.trace, trn * sizeof(unsigned long long)));
             MFX_CUDA_TRY(cudaMemsetAsync(P.trace, 0, trn * sizeof(unsigned long long), s));
         }
-        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S>, P));
+        MFX_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_bicg_rw<CPT, S, CLP>, P));
         if (kTrace && tr) {
             static unsigned long long h[1024 + 16 * 2048];
             MFX_CUDA_TRY(cudaMemcpyAsync(h, P.trace, trn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1521,8 +1692,19 @@ mfx_status persist_solve_launch(const Geo &G, const mfx_eqsys *A, double *x, con
                                 cudaStream_t s)
 {
     if (!get_encode()) return MFX_ERR_CUDA;
-    if (G.nx <= 32) return PersistLauncher<1, 3>::run(G, A, x, W, maxit, s);
-    return PersistLauncher<2, 3>::run(G, A, x, W, maxit, s);
+    // MFX_PERSIST_CL: CTAs per cluster of the hierarchical all-reduce (8 or 16;
+    // default 1 = the flat grid all-reduce: B200, c3 51.6 us per iteration vs
+    // 55.2 with clusters of 8 and 60.2 with 16 -- the two DSMEM hops cost more
+    // than the shorter global fold saves)
+    static const int clp = env_int("MFX_PERSIST_CL", 1);
+    if (G.nx <= 32) {
+        if (clp == 16 && PersistLauncher<1, 3, 16>::grid_size() > 0) return PersistLauncher<1, 3, 16>::run(G, A, x, W, maxit, s);
+        if (clp >= 8 && PersistLauncher<1, 3, 8>::grid_size() > 0) return PersistLauncher<1, 3, 8>::run(G, A, x, W, maxit, s);
+        return PersistLauncher<1, 3, 1>::run(G, A, x, W, maxit, s);
+    }
+    if (clp == 16 && PersistLauncher<2, 3, 16>::grid_size() > 0) return PersistLauncher<2, 3, 16>::run(G, A, x, W, maxit, s);
+    if (clp >= 8 && PersistLauncher<2, 3, 8>::grid_size() > 0) return PersistLauncher<2, 3, 8>::run(G, A, x, W, maxit, s);
+    return PersistLauncher<2, 3, 1>::run(G, A, x, W, maxit, s);
 }
 
 

@@ -24,19 +24,28 @@ def mfx():
     return m
 
 
-@pytest.fixture(params=["tma", "cluster", "v1", "grid", "persist"])
+@pytest.fixture(params=["tma", "cluster", "cluster8", "v1", "grid", "persist"])
 def solver_path(request, mfx):
-    v = {"tma": mfx.PATH_TMA, "cluster": mfx.PATH_CLUSTER, "v1": mfx.PATH_V1, "grid": mfx.PATH_GRID,
-         "persist": mfx.PATH_PERSIST}[request.param]
+    """cluster: the single-cluster solver at its default size (16 CTAs where the
+    device places such a cluster); cluster8: the same kernel on 8 CTAs."""
+    v = {"tma": mfx.PATH_TMA, "cluster": mfx.PATH_CLUSTER, "cluster8": mfx.PATH_CLUSTER, "v1": mfx.PATH_V1,
+         "grid": mfx.PATH_GRID, "persist": mfx.PATH_PERSIST}[request.param]
+    cl = mfx.get_option("cluster_size")
+    if request.param == "cluster8":
+        mfx.set_option("cluster_size", 8)
     mfx.set_option("solver_path", v)
-    yield request.param
+    yield "cluster" if request.param == "cluster8" else request.param
     mfx.set_option("solver_path", mfx.PATH_AUTO)
+    mfx.set_option("cluster_size", cl)
 
 
 def cluster_fits(g, sym):
+    # bicg_cluster.cu: (NA + 8) slab arrays + 5 planes (fp64) + slab flags (int32) <= 200 KiB
+    import paper_2211_15605_b200 as m_
+    cl = m_.get_option("cluster_size")
     plane = g.nx * g.ny
-    m = plane * -(-g.nz // 8)
-    return ((12 if sym else 15) * m + 3 * plane) * 8 + 4 * m <= 200 * 1024
+    m = plane * -(-g.nz // cl)
+    return ((11 if sym else 15) * m + 5 * plane) * 8 + 4 * m <= 200 * 1024
 
 
 def need_path(solver_path, g, sym):

@@ -222,17 +222,62 @@ __device__ __forceinline__ void block_reduce_dd(dd (&v)[K], dd *sh)
     __syncthreads();
 }
 
+// Block reduction with lazy trees, the K values interleaved: a lane butterfly
+// per warp, then warp 0 folds the warp partials; the result is valid in warp
+// 0 (every lane of it when blockDim <= 512).  All threads must call.
+// (B200: the K-serial block_reduce_dd costs ~1k cycles per value in the K2 /
+// persistent tails; this is one pass for all K.)
+template <int K>
+__device__ __forceinline__ void block_reduce_lazy(dd (&v)[K])
+{
+    __shared__ dd s_w[3][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    butterfly_lazy<K, 32>(v);
+    __syncthreads();   // readers of the previous call's slots are done
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < K; q++) s_w[q][wid] = v[q];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < K; q++) v[q] = lane < nw ? s_w[q][lane] : dd{0.0, 0.0};
+        if (nw <= 16) butterfly_lazy<K, 16>(v);
+        else butterfly_lazy<K, 32>(v);
+    }
+}
+
+// every thread folds its share of n published partials part[b * stride + q]
+// (thread-strided: one L2 round trip for n <= blockDim), then the block tree;
+// the result is valid in warp 0.  All threads must call.  (A one-warp fold
+// is slower: ~10 L2 round trips per lane at n ~ 300.)
+template <int K>
+__device__ __forceinline__ void block_fold_partials(const dd *part, unsigned n, int stride, dd (&f)[K])
+{
+#pragma unroll
+    for (int q = 0; q < K; q++) f[q] = dd{0.0, 0.0};
+    for (unsigned b = threadIdx.x; b < n; b += blockDim.x) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            dd x;
+            x.hi = __ldcg(&part[(size_t)b * stride + q].hi);
+            x.lo = __ldcg(&part[(size_t)b * stride + q].lo);
+            f[q] = dd_add_lazy(f[q], x);
+        }
+    }
+    block_reduce_lazy<K>(f);
+}
+
 // Deterministic grid reduction: each block writes K partials to part[blk*K+q];
-// the last block to finish (ticket) folds them in block order with all its
-// threads (strided sequential fold, then a fixed block tree) and returns true
-// in every thread of that block, with out[q] valid in thread 0.  (Publishing
-// warp partials instead, to keep one block reduction off the tail, measured
-// slower: the last block's fold over 9x more partials costs more.)
+// the last block to finish (ticket) folds them with all its threads and returns
+// true in every thread of that block, with out[q] valid in thread 0.
+// (Publishing warp partials instead, to keep one block reduction off the
+// tail, measured slower: the last block's fold over 9x more partials costs more.)
 template <int K>
 __device__ __forceinline__ bool grid_reduce_dd(dd (&v)[K], dd *part, unsigned int *ticket, dd *sh,
                                                dd (&out)[K])
 {
-    block_reduce_dd<K>(v, sh);
+    (void)sh;
+    block_reduce_lazy<K>(v);
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -244,22 +289,11 @@ __device__ __forceinline__ bool grid_reduce_dd(dd (&v)[K], dd *part, unsigned in
     __syncthreads();
     if (!s_last) return false;
     __threadfence();
-    dd acc[K];
-#pragma unroll
-    for (int q = 0; q < K; q++) acc[q] = dd{0.0, 0.0};
-    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-#pragma unroll
-        for (int q = 0; q < K; q++) {
-            dd x;
-            x.hi = __ldcg(&part[(size_t)b * K + q].hi);
-            x.lo = __ldcg(&part[(size_t)b * K + q].lo);
-            acc[q] = dd_add(acc[q], x);
-        }
-    }
-    block_reduce_dd<K>(acc, sh);
+    dd f[K];
+    block_fold_partials<K>(part, gridDim.x, K, f);
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < K; q++) out[q] = acc[q];
+        for (int q = 0; q < K; q++) out[q] = f[q];
         *ticket = 0u;   // reset for the next launch (stream-ordered)
     }
     return true;

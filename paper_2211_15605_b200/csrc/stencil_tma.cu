@@ -983,7 +983,8 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
     // this thread's generic stores vs the next passes' TMA (async-proxy) reads; K2's
     // output t is read back only by generic loads (K3), so it needs none
     if (K != 3) asm volatile("fence.proxy.async.global;" ::: "memory");
-    block_reduce_dd<K>(v, sh);                                  // (syncs the CTA: every store precedes the arrival)
+    (void)sh;
+    block_reduce_lazy<K>(v);   // (syncs the CTA: every store precedes the arrival)
     dd *pb = part + (size_t)(phase & 1) * gridDim.x * 3;
     ptrace(P, it, slot);        // every warp of the CTA done with the pass
     if (threadIdx.x == 0) {
@@ -1006,21 +1007,7 @@ __device__ __forceinline__ void grid_allreduce(const Acc (&acc)[3][CPT], dd *par
     phase++;
     ptrace(P, it, slot + 1);    // released
     __syncthreads();
-    dd f[K];
-#pragma unroll
-    for (int d = 0; d < K; d++) f[d] = dd{0.0, 0.0};
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-#pragma unroll
-        for (int d = 0; d < K; d++) {
-            dd x;
-            x.hi = __ldcg(&pb[(size_t)b * 3 + d].hi);
-            x.lo = __ldcg(&pb[(size_t)b * 3 + d].lo);
-            f[d] = dd_add(f[d], x);
-        }
-    }
-    block_reduce_dd<K>(f, sh);
-#pragma unroll
-    for (int d = 0; d < K; d++) out[d] = f[d];
+    block_fold_partials<K>(pb, gridDim.x, 3, out);   // out valid in thread 0
 }
 
 // Cluster-hierarchical all-reduce (CLP > 1 CTAs per cluster; DESIGN.md §7
@@ -1266,7 +1253,10 @@ __global__ void __launch_bounds__(8 * 32 + 32, 2) k_bicg_rw(const __grid_constan
                 const long long pl = (long long)a.nx * a.ny;
                 const long long e0 = (long long)gx + (long long)a.nx * gy;
                 // KU planes per step, every load of the step issued before any use
-                constexpr int KU = 1;
+#ifndef MFX_PK3_KU
+#define MFX_PK3_KU 1
+#endif
+                constexpr int KU = MFX_PK3_KU;
                 for (int kb = k0; kb < k1; kb += KU) {
                     double xv[KU][CPT], rv[KU][CPT], rhv[KU][CPT], pv[KU][CPT], vv[KU][CPT], tv[KU][CPT];
 #pragma unroll

@@ -1,7 +1,6 @@
-# c1 single-cluster solver: parity (default build) + A/B of variant builds (abv/)
+# c1 single-cluster solver: parity (default build) + A/B against abv/libmfx_before.so
 python scripts/dbg_cl.py 2>&1 | tail -10
-for rep in 1 2; do for so in "" abv/libmfx_ct128.so; do for cl in 16 8; do
+for rep in 1 2; do for so in "" abv/libmfx_before.so; do for cl in 16; do
   echo -n "so=${so:-default} MFX_CLUSTER=$cl c1: "; MFX_SO_VARIANT=$so MFX_CLUSTER=$cl timeout 300 python scripts/prof_solve.py --config 1 --kind pp --iters 400 --repeat 3 --path 2 2>&1 | grep timed | tail -1
 done; done; done
 MFX_CLUSTER_TRACE=1 timeout 300 python scripts/prof_solve.py --config 1 --kind pp --iters 50 --repeat 1 --path 2 2>&1 | grep -A4 "cluster trace"
-MFX_SO_VARIANT=abv/libmfx_ct128.so MFX_CLUSTER_TRACE=1 timeout 300 python scripts/prof_solve.py --config 1 --kind pp --iters 50 --repeat 1 --path 2 2>&1 | grep -A4 "cluster trace"

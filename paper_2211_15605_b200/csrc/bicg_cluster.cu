@@ -51,12 +51,22 @@ struct ClArgs {
 
 // Cluster-wide correctly rounded reduction of K double-doubles (push model,
 // see the file comment); every thread of every CTA gets the same out[].
+// Default: warp 0 folds the CTA's warp partials and pushes one CTA partial
+// per value (NS = CL slots).  MFX_CL_WPUSH: every warp pushes its own
+// partial (NS = CL x NW slots), skipping the CTA barrier and fold before the
+// push at the price of a longer final fold.
+#ifdef MFX_CL_WPUSH
+constexpr int kWpush = 1;
+#else
+constexpr int kWpush = 0;
+#endif
 template <int CL>
 struct ClusterRed {
+    static constexpr int NS = kWpush ? CL * NW : CL;
     dd (*wpart)[NW];       // [3][NW] this CTA's warp partials
-    dd (*red)[3][CL];      // [2][3][CL] pushed CTA partials
+    dd (*red)[3][NS];      // [2][3][NS] pushed partials
     uint64_t *mb;          // [2] one mbarrier per buffer
-    uint32_t dst;          // lane j < CL: address of red[0][0][rank] in CTA j
+    uint32_t dst;          // lane j < CL: address of this CTA's (warp's) slot red[0][0][.] in CTA j
     uint32_t bar0, bar1;   // lane j < CL: CTA j's mbarriers
     double (*bc)[3];       // [2][3] folded results (double-buffered: no barrier before the next write)
     uint32_t ph0 = 0, ph1 = 0;   // (scalars, not arrays indexed by buf: no local memory)
@@ -66,43 +76,54 @@ struct ClusterRed {
     {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         butterfly_lazy<K, 32>(v);
-        if (lane == 0)
-#pragma unroll
-            for (int q = 0; q < K; q++) wpart[q][wid] = v[q];
-        __syncthreads();
-        if (wid == 0) {
-            dd y[K];
-#pragma unroll
-            for (int q = 0; q < K; q++) y[q] = wpart[q][lane & (NW - 1)];
-            butterfly_lazy<K, NW>(y);
-            // always 3 slots (zeros beyond K): every use of a buffer carries the
-            // same byte count, so its mbarrier is re-armed right after each use
+        // always 3 slots (zeros beyond K): every use of a buffer carries the
+        // same byte count, so its mbarrier is re-armed right after each use
+        if (kWpush) {
             if (lane < CL)
 #pragma unroll
                 for (int q = 0; q < 3; q++)
-                    push_f64x2(dst + (uint32_t)((buf * 3 + q) * CL * 16), q < K ? y[q].hi : 0.0, q < K ? y[q].lo : 0.0,
+                    push_f64x2(dst + (uint32_t)((buf * 3 + q) * NS * 16), q < K ? v[q].hi : 0.0, q < K ? v[q].lo : 0.0,
                                buf ? bar1 : bar0);
+        } else {
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < K; q++) wpart[q][wid] = v[q];
+            __syncthreads();
+            if (wid == 0) {
+                dd y[K];
+#pragma unroll
+                for (int q = 0; q < K; q++) y[q] = wpart[q][lane & (NW - 1)];
+                butterfly_lazy<K, NW>(y);
+                if (lane < CL)
+#pragma unroll
+                    for (int q = 0; q < 3; q++)
+                        push_f64x2(dst + (uint32_t)((buf * 3 + q) * NS * 16), q < K ? y[q].hi : 0.0,
+                                   q < K ? y[q].lo : 0.0, buf ? bar1 : bar0);
+            }
         }
         if (buf) { mbar_wait_cluster(&mb[1], ph1); ph1 ^= 1u; }
         else { mbar_wait_cluster(&mb[0], ph0); ph0 ^= 1u; }
         // arm the buffer's next use now: no CTA can push into it before this
         // CTA has pushed the next reduction (so the arm precedes every push)
-        if (threadIdx.x == 0) mbar_arrive_expect_tx(&mb[buf], (uint32_t)(CL * 3 * 16));
-#ifdef MFX_CL_ALLFOLD
-        dd y[K];
-#pragma unroll
-        for (int q = 0; q < K; q++) y[q] = red[buf][q][lane & (CL - 1)];
-        butterfly_lazy<K, CL>(y);   // every group of CL lanes folds the same slots in the same order
-#pragma unroll
-        for (int q = 0; q < K; q++) out[q] = dd_round(y[q]);
-#else
-        // one warp folds the CL partials, the others wait at the CTA barrier
-        // (16 warps folding redundantly contend for the fp64 pipe)
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&mb[buf], (uint32_t)(NS * 3 * 16));
+        // one warp folds the pushed partials, the others wait at the CTA
+        // barrier (16 warps folding redundantly contend for the fp64 pipe:
+        // measured slower)
         if (wid == 0) {
             dd y[K];
+            if (NS <= 32) {
 #pragma unroll
-            for (int q = 0; q < K; q++) y[q] = red[buf][q][lane & (CL - 1)];
-            butterfly_lazy<K, CL>(y);
+                for (int q = 0; q < K; q++) y[q] = red[buf][q][lane & (NS - 1)];
+                butterfly_lazy<K, (NS <= 32 ? NS : 32)>(y);
+            } else {
+#pragma unroll
+                for (int q = 0; q < K; q++) {
+                    y[q] = red[buf][q][lane];
+#pragma unroll
+                    for (int j = 32; j < NS; j += 32) y[q] = dd_add_lazy(y[q], red[buf][q][lane + j]);
+                }
+                butterfly_lazy<K, 32>(y);
+            }
             if (lane == 0)
 #pragma unroll
                 for (int q = 0; q < K; q++) bc[buf][q] = dd_round(y[q]);
@@ -110,7 +131,6 @@ struct ClusterRed {
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < K; q++) out[q] = bc[buf][q];
-#endif
         buf ^= 1;
     }
 };
@@ -128,7 +148,7 @@ __global__ void __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
     double *x = b + M, *r = x + M, *rh = r + M, *p = rh + M, *v = p + M, *s = v + M, *t = s + M;
     __shared__ int k0s[CL + 1];
     __shared__ __align__(16) dd wpart[3][NW];     // this CTA's warp partials
-    __shared__ __align__(16) dd red[2][3][CL];    // pushed CTA partials, double-buffered
+    __shared__ __align__(16) dd red[2][3][ClusterRed<CL>::NS];   // pushed partials, double-buffered
     __shared__ double bcast[2][3];                // folded results
     __shared__ __align__(8) uint64_t mb_red[2], mb_halo[2];   // reductions; halo planes of p / s
     const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
@@ -137,8 +157,8 @@ __global__ void __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
         mbar_init(&mb_red[0], 1); mbar_init(&mb_red[1], 1);
         mbar_init(&mb_halo[0], 1); mbar_init(&mb_halo[1], 1);
         // first phases armed before any CTA can push (the setup cluster barrier)
-        mbar_arrive_expect_tx(&mb_red[0], (uint32_t)(CL * 3 * 16));
-        mbar_arrive_expect_tx(&mb_red[1], (uint32_t)(CL * 3 * 16));
+        mbar_arrive_expect_tx(&mb_red[0], (uint32_t)(ClusterRed<CL>::NS * 3 * 16));
+        mbar_arrive_expect_tx(&mb_red[1], (uint32_t)(ClusterRed<CL>::NS * 3 * 16));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -209,7 +229,7 @@ __global__ void __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
     }
     uint32_t red_dst = 0, red_bar[2] = {0, 0};   // lane j < CL of the folding warp pushes to CTA j
     if (lane < CL) {
-        red_dst = mapa_u32(smem_u32(&red[0][0][rank]), lane);
+        red_dst = mapa_u32(smem_u32(&red[0][0][kWpush ? rank * NW + (tid >> 5) : rank]), lane);
         red_bar[0] = mapa_u32(smem_u32(&mb_red[0]), lane);
         red_bar[1] = mapa_u32(smem_u32(&mb_red[1]), lane);
     }

@@ -483,3 +483,33 @@ def test_true_rel_resid_matches_oracle(mfx, orc):
         want = np.sqrt(orc.dot(r, r)) / np.sqrt(orc.dot(sysd["b"], sysd["b"]))
         assert info["true_rel_resid"] == want, (info, want)
         assert info["true_rel_resid"] > 0.0
+
+
+@pytest.mark.parametrize("cl", [16, 8])
+def test_cluster_solver_back_to_back_shapes(mfx, orc, cl):
+    """Single-cluster solver: different systems back to back (shared memory
+    left over from the previous launch holds another system's slabs -- a
+    missing barrier after a shared-memory fill reads those stale values
+    instead of failing loudly), each bitwise vs the oracle; ragged slab splits
+    (nz not a multiple of the cluster size) included."""
+    prev = mfx.get_option("cluster_size")
+    mfx.set_option("cluster_size", cl)
+    mfx.set_option("solver_path", mfx.PATH_CLUSTER)
+    try:
+        for (nx, ny, nz) in ((16, 16, 32), (8, 8, 48), (16, 16, 20), (16, 16, 32), (12, 10, 37)):
+            g = synth.make_grid(nx, ny, nz)
+            pr = Params()
+            st = synth.make_state(g, 77 + nx + nz, pr, n_scalars=0)
+            if not cluster_fits(g, True):
+                continue
+            dv = [np.random.default_rng(3 + a).uniform(1e-4, 1e-3, g.n) for a in range(3)]
+            sysd, _, _ = orc.assemble_pp(g, pr, st, [st["u"], st["v"], st["w"]], dv)
+            for maxit in (1, 2, 7):
+                ref, info, x = solve_both(mfx, orc, g, mfx.EQ_PP, sysd, np.zeros(g.n), 1e-30, maxit)
+                assert info["iters"] == ref["iters"] and np.array_equal(x, ref["x"]), ((nx, ny, nz), maxit)
+            sysm, _, _ = orc.assemble_mom(g, pr, 2, st)
+            ref, info, x = solve_both(mfx, orc, g, 2, sysm, st["w"], 1e-10, 60)
+            assert_solve_parity(ref, info, x)
+    finally:
+        mfx.set_option("solver_path", mfx.PATH_AUTO)
+        mfx.set_option("cluster_size", prev)

@@ -276,7 +276,10 @@ def measure_other_configs(mfx, torch):
     ms = float(np.median(times))
     out["c1"] = {"workload": "p' BiCGSTAB solve 16x16x32, tol 1e-6 (single-cluster solver)",
                  "iters": iters, "ms_per_solve": ms, "us_per_iter": 1e3 * ms / iters,
-                 "bicgstab_iters_per_s": iters / (ms / 1e3)}
+                 "bicgstab_iters_per_s": iters / (ms / 1e3),
+                 "solver": f"single cluster of {mfx.get_option('cluster_size')} CTAs (one launch per solve)",
+                 "memory_regime": "shared-memory resident: the whole system lives in the cluster's shared memory "
+                                  "for the solve (DRAM: one read of the system, one write of x)"}
     out["c2_momentum"] = measure_momentum_c2(mfx, torch)
     for cid, steps in ((3, 5), (4, 3)):
         g, pr, st = synth.config_case(cid)
@@ -300,7 +303,11 @@ def measure_other_configs(mfx, torch):
                           "bicgstab_iters_per_s": its / (ms / 1e3),
                           "pp_us_per_iter": 1e3 * ph["pp"] / pp_it,
                           "pp_alg_GBps": PP_ITER_BPC * g.n / (1e-3 * ph["pp"] / pp_it) / 1e9,
-                          "iters_last": o["iters"][:4]}
+                          "iters_last": o["iters"][:4],
+                          "memory_regime": ("L2-resident reads: p' working set 92 MB < 126 MB L2 (ncu of the "
+                                            "persistent solver: 90% L2 hit rate, profiles/r02q_ncu_summary.md); "
+                                            "latency-bound" if cid == 3 else
+                                            "HBM-streaming: working set >> 126 MB L2")}
         ctx.close()
         del sd
         torch.cuda.empty_cache()

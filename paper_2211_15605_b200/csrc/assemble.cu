@@ -559,8 +559,9 @@ mfx_status assemble_eq(int kind, int sid, const mfx_grid *grid, const mfx_params
         a.aB = out->aB; a.b = out->b; a.d = out->d;
         a.resid2 = resid2; a.hdr = W.hdr; a.part = W.part;
         count_launch(4, s, true);
-        // BLOCKED cells (§3.10) and odd nx (rows not 16-byte aligned for TMA): grid-stride kernel
-        if (opt_asm_tma() && !st->blocked && grid->nx % 2 == 0) {
+        // odd nx (rows not 16-byte aligned for TMA): grid-stride kernel; BLOCKED
+        // cells (§3.10) take either kernel (the same row decisions in both)
+        if (opt_asm_tma() && grid->nx % 2 == 0) {
             const mfx_status rc = assemble_mom_tma(kind, G, pr, st, out, resid2, W.hdr, W.part, s);
             count_launch(4, s, false);
             return rc;

@@ -33,6 +33,7 @@ struct AsmMomArgs {
     double w_in, A[3], V;
     double rho, urf, gc, rVdt, Dc[3];
     const double *eps0, *uold, *p, *beta, *S;
+    const unsigned char *blocked;      // NULL or N flags (BLOCKED cells)
     double *aP, *aE, *aW, *aN, *aS, *aT, *aB, *b, *d;
     double *resid2;
     WsHeader *hdr;
@@ -93,6 +94,7 @@ struct SmemRowIn {
     int P[3];
     int type;
     bool m_wall, e_ident;
+    bool nb_wall_[2][2];   // neighbour row (P + s e_t, E + s e_t) touches a BLOCKED cell (§3.10)
     double e0P, e0E, bP, bE, SP, SE, pP, pEv, uoP;
     const double *pl[3];   // planes k-1, k, k+1
     int hc, e[3], ext[3];
@@ -142,10 +144,20 @@ struct SmemRowIn {
         const int qa = P[s6 / 2] + o[s6 / 2];
         return (qa >= 0 && qa < ext[s6 / 2]) ? at(1 + C, o) : 0.0;
     }
-    __device__ bool nb_wall(int, int) const { return false; }   // no BLOCKED cells on this path
+    __device__ bool nb_wall(int ti, int sg) const { return nb_wall_[ti][sg]; }
 };
 
-template <int C>
+// §3.10: cell q is BLOCKED (outside the domain: not blocked); the flags are
+// one byte per cell, read through the read-only path (L1/L2), not staged
+__device__ __forceinline__ bool blk_tma(const AsmMomArgs &a, int i, int j, int k)
+{
+    if (i < 0 || j < 0 || k < 0 || i >= a.nx || j >= a.ny || k >= a.nz) return false;
+    return __ldg(a.blocked + ((long long)i + (long long)a.nx * ((long long)j + (long long)a.ny * k))) != 0;
+}
+
+// BL: the grid has BLOCKED cells (the row rules of DESIGN.md §3.10, the same
+// decisions as the grid-stride kernel's row_type / m_wall / e_ident / nb_wall)
+template <int C, bool BL>
 __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_constant__ AsmMomMaps M, AsmMomArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -208,6 +220,12 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                 const long long n = (long long)P0 + (long long)a.nx * ((long long)P1 + (long long)a.ny * k);
                 int type = 0;                                        // kInterior / kIdentity / kOutlet
                 if (P[C] >= ext[C] - 1) type = (C == 2 && a.bc_zhi == MFX_BC_OUTLET) ? 2 : 1;
+                if (BL && mine) {
+                    // a blocked P, or an internal wall face (E = P + e_C blocked): identity row
+                    int E[3] = {P[0], P[1], P[2]};
+                    E[C] += 1;
+                    if (blk_tma(a, P[0], P[1], P[2]) || (type == 0 && blk_tma(a, E[0], E[1], E[2]))) type = 1;
+                }
                 // pointwise fields at P and E (global, issued before the stage wait)
                 const int oE = type == 0 ? 1 : 0;
                 const long long nE = n + (type == 0 ? (C == 0 ? 1 : (C == 1 ? (long long)a.nx : sz)) : 0);
@@ -244,6 +262,36 @@ __global__ void __launch_bounds__(ANT + 32, 2) k_asm_mom_tma(const __grid_consta
                         in.m_wall = false;
                         // E is an identity row iff it is the last face along C and that face is a wall
                         in.e_ident = type != 2 && (P[C] + 1 >= ext[C] - 1) && !(C == 2 && a.bc_zhi == MFX_BC_OUTLET);
+                        in.nb_wall_[0][0] = in.nb_wall_[0][1] = in.nb_wall_[1][0] = in.nb_wall_[1][1] = false;
+                        if (BL) {
+                            int E[3] = {P[0], P[1], P[2]};
+                            E[C] += oE;
+                            int Pm[3] = {P[0], P[1], P[2]};
+                            Pm[C] -= 1;
+                            in.m_wall = P[C] >= 1 && blk_tma(a, Pm[0], Pm[1], Pm[2]);
+                            if (type != 2) {
+                                // row_type(E): E itself blocked, or its own +e_C face a wall (§3.10)
+                                int EE[3] = {E[0], E[1], E[2]};
+                                EE[C] += 1;
+                                const bool eb = blk_tma(a, E[0], E[1], E[2]);
+                                in.e_ident = eb || (E[C] < ext[C] - 1 ? blk_tma(a, EE[0], EE[1], EE[2])
+                                                                       : !(C == 2 && a.bc_zhi == MFX_BC_OUTLET));
+                            }
+#pragma unroll
+                            for (int ti = 0; ti < 2; ti++) {
+                                const int t = ti == 0 ? SmemRowIn<C>::T1 : SmemRowIn<C>::T2;
+#pragma unroll
+                                for (int sg = 0; sg < 2; sg++) {
+                                    const int sgn = sg ? 1 : -1;
+                                    int Pt[3] = {P[0], P[1], P[2]}, Et[3] = {E[0], E[1], E[2]};
+                                    Pt[t] += sgn;
+                                    Et[t] += sgn;
+                                    const int pt = P[t] + sgn;
+                                    in.nb_wall_[ti][sg] = pt >= 0 && pt < ext[t] &&
+                                                          (blk_tma(a, Pt[0], Pt[1], Pt[2]) || blk_tma(a, Et[0], Et[1], Et[2]));
+                                }
+                            }
+                        }
                         MomRowOut ro;
                         mom_row<C>(a.R, in, ro);
                         a.aW[n] = ro.st6[0]; a.aE[n] = ro.st6[1];
@@ -297,31 +345,31 @@ int asm_choose_lz(long long ntiles, int nz, int grid)
     return best;
 }
 
-template <int C>
+template <int C, bool BL>
 int asm_grid()
 {
     static int g = 0;
     if (g) return g;
     const size_t sm = (size_t)AS * ASTAGE_B + 16 * AS;
-    cudaFuncSetAttribute(k_asm_mom_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_asm_mom_tma<C, BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int occ = 0, dev = 0, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_asm_mom_tma<C>, ANT + 32, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_asm_mom_tma<C, BL>, ANT + 32, sm);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g = sms * (occ > 0 ? occ : 1);
     return g;
 }
 
-template <int C>
+template <int C, bool BL>
 mfx_status launch_c(const AsmMomMaps &M, AsmMomArgs &a, cudaStream_t s)
 {
-    const int grid = asm_grid<C>();
+    const int grid = asm_grid<C, BL>();
     const long long ntiles = (long long)a.tiles_x * a.tiles_y;
     a.Lz = asm_choose_lz(ntiles, a.nz, grid);
     a.units = ntiles * ((a.nz + a.Lz - 1) / a.Lz);
     const int g = (int)(a.units < grid ? a.units : grid);
     const size_t sm = (size_t)AS * ASTAGE_B + 16 * AS;
-    k_asm_mom_tma<C><<<g, ANT + 32, sm, s>>>(M, a);
+    k_asm_mom_tma<C, BL><<<g, ANT + 32, sm, s>>>(M, a);
     MFX_CUDA_TRY(cudaGetLastError());
     return MFX_OK;
 }
@@ -362,9 +410,15 @@ mfx_status assemble_mom_tma(int kind, const Geo &G, const mfx_params *pr, const 
     a.aP = out->aP; a.aE = out->aE; a.aW = out->aW; a.aN = out->aN; a.aS = out->aS; a.aT = out->aT;
     a.aB = out->aB; a.b = out->b; a.d = out->d;
     a.resid2 = resid2; a.hdr = hdr; a.part = part;
-    if (kind == 0) return launch_c<0>(M, a, s);
-    if (kind == 1) return launch_c<1>(M, a, s);
-    return launch_c<2>(M, a, s);
+    a.blocked = st->blocked;
+    if (a.blocked) {
+        if (kind == 0) return launch_c<0, true>(M, a, s);
+        if (kind == 1) return launch_c<1, true>(M, a, s);
+        return launch_c<2, true>(M, a, s);
+    }
+    if (kind == 0) return launch_c<0, false>(M, a, s);
+    if (kind == 1) return launch_c<1, false>(M, a, s);
+    return launch_c<2, false>(M, a, s);
 }
 
 }  // namespace mfx

@@ -32,8 +32,17 @@ def host(t):
     return t.detach().cpu().numpy()
 
 
+@pytest.fixture(params=["tma", "gridstride"])
+def asm_path(request, mfx):
+    """momentum assembly kernel: TMA z-marching (BLOCKED rules read from the
+    flag bytes) or grid-stride; both must give the oracle's bits"""
+    mfx.set_option("asm_tma", 1 if request.param == "tma" else 0)
+    yield request.param
+    mfx.set_option("asm_tma", 1)
+
+
 @pytest.mark.parametrize("shape", SHAPES)
-def test_bfs_assembly_bitwise(mfx, orc, shape):
+def test_bfs_assembly_bitwise(mfx, orc, shape, asm_path):
     g, pr, st = synth.bfs_case(*shape, seed=11)
     st["phi0"] = np.zeros(g.n)
     st["phi_old0"] = np.where(st["blocked"] == 0, np.random.default_rng(1).uniform(0, 1, g.n), 0.0)

@@ -1,5 +1,4 @@
-# persistent solver: 2 CTAs/SM x 3 stages vs 1 CTA/SM x 6 stages (MFX_PERSIST_S)
-MFX_PERSIST_S=6 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "persist" 2>&1 | tail -1
-for rep in 1 2 3; do for ps in 3 6; do for cfg in 3 2; do
-  echo -n "MFX_PERSIST_S=$ps c$cfg path5: "; MFX_PERSIST_S=$ps timeout 300 python scripts/prof_solve.py --config $cfg --kind pp --iters 200 --repeat 3 --path 5 2>&1 | grep -E "timed" | tail -1
+# K3 grid: CTAs per SM (MFX_K3_CPS; default = occupancy)
+for rep in 1 2; do for cps in 0 2 4; do for cfg in 2 3; do
+  echo -n "MFX_K3_CPS=$cps c$cfg path1: "; MFX_K3_CPS=$cps timeout 300 python scripts/prof_solve.py --config $cfg --kind pp --iters 200 --repeat 3 --path 1 2>&1 | grep -E "timed|kernels" | tail -2 | tr '\n' ' '; echo
 done; done; done

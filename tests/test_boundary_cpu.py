@@ -266,3 +266,17 @@ def test_grid_validation_before_any_launch(mfx):
             assert ">= 2" not in msg and "even" not in msg, msg
         else:
             assert ">= 2" in msg, msg
+
+
+def test_runtime_option_validation(mfx):
+    """mfx_set_option refuses out-of-range values and unknown keys before any
+    device work (include/mfx.h "Runtime options")."""
+    lib = mfx.lib()
+    lib.mfx_set_option.restype = C.c_int
+    lib.mfx_set_option.argtypes = [C.c_char_p, C.c_int]
+    assert lib.mfx_set_option(b"cluster_size", 7) != 0
+    assert lib.mfx_set_option(b"cluster_size", 32) != 0
+    assert lib.mfx_set_option(b"solver_path", 6) != 0
+    assert lib.mfx_set_option(b"no_such_option", 1) != 0
+    assert lib.mfx_get_option(b"no_such_option") == -1
+    assert lib.mfx_set_option(b"solver_path", 0) == 0

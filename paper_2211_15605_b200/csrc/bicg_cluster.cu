@@ -469,11 +469,33 @@ __global__ void __launch_bounds__(CT) k_bicg_cluster(ClArgs a)
         }
         if (it > maxit) { status = MFX_NOT_CONVERGED; iters = maxit; }
     }
+    // true residual of the returned iterate (mfx_solve_info.true_rel_resid,
+    // the k_true_resid definition: sqrt(dot(r, r)) / sqrt(dot(b, b)) with
+    // r = b - A x, correctly rounded dots): x's boundary planes travel like
+    // p's (halo 0 is armed for its next phase), one more reduction; saves the
+    // separate launch per solve
+    double true_rel = 0.0;
+    if (bn != 0.0) {
+        for (int i = tid; i < nc; i += CT) push_halo(0, i, x[i]);
+        wait_halo(0);
+        Acc rt;
+        rt.zero();
+        for (int i = tid; i < nc; i += CT) {
+            const double rv = b[i] - apply(x, hal, hal + plane, i);
+            rt.prod(rv, rv);
+        }
+        dd vv[1] = {rt.get()};
+        double out[1];
+        R.template run<1>(vv, out);
+        true_rel = sqrt(out[0]) / bn;
+    }
     for (int i = tid; i < nc; i += CT) a.x[g0 + i] = x[i];
     if (rank == 0 && tid == 0) {
-        SolverScalars &S = a.h->sc;
+        SolverScalars S = SolverScalars{};   // the whole record (the host path skips its memset)
         S.it = iters; S.status = status; S.restarts = restarts; S.rn = rn; S.bn = bn; S.done = 1;
         S.tol = tol; S.maxit = maxit;
+        a.h->sc = S;
+        a.h->true_rel = true_rel;
     }
     // every push into this CTA's shared memory has completed (each was waited
     // for); keep it alive until every CTA is done as well

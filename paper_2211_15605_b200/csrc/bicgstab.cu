@@ -12,6 +12,7 @@
 //       rho = <r^, r>, rr = <r, r>
 // 17 vector passes + 2 coefficient passes per iteration.
 #include <climits>
+#include <cstddef>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -826,7 +827,7 @@ mfx_status true_resid_launch(bool sym, const Geo &G, const mfx_eqsys *A, const d
 // exit record for a host-synchronous solve: the true residual of the returned
 // iterate, then one device->host copy of the solver state
 static mfx_status finish_info(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, const WsView &W,
-                              mfx_solve_info *info, cudaStream_t s);
+                              mfx_solve_info *info, cudaStream_t s, bool have_true = false);
 
 // MFX_KERNELS=v1 selects the simple grid-stride kernels (kept as an A/B
 // reference for tests and profiling); default is the TMA z-marching path.
@@ -912,20 +913,19 @@ mfx_status spmv(int kind, const mfx_grid *grid, const mfx_eqsys *A, const double
     return MFX_OK;
 }
 
-struct HostExit {
-    SolverScalars sc;
-    double true_rel;
-};
-static thread_local HostExit *g_exit = nullptr;
+static thread_local WsHeader *g_exit = nullptr;   // pinned copy of the workspace header prefix
 
 static mfx_status finish_info(bool sym, const Geo &G, const mfx_eqsys *A, const double *x, const WsView &W,
-                              mfx_solve_info *info, cudaStream_t s)
+                              mfx_solve_info *info, cudaStream_t s, bool have_true)
 {
-    if (!g_exit) MFX_CUDA_TRY(cudaMallocHost(&g_exit, sizeof(HostExit)));
-    mfx_status st = true_resid_launch(sym, G, A, x, W.hdr, W.part, s);
-    if (st != MFX_OK) return st;
-    MFX_CUDA_TRY(cudaMemcpyAsync(&g_exit->sc, &W.hdr->sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, s));
-    MFX_CUDA_TRY(cudaMemcpyAsync(&g_exit->true_rel, &W.hdr->true_rel, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (!g_exit) MFX_CUDA_TRY(cudaMallocHost(&g_exit, sizeof(WsHeader)));
+    if (!have_true) {   // (the single-cluster kernel computes it itself)
+        mfx_status st = true_resid_launch(sym, G, A, x, W.hdr, W.part, s);
+        if (st != MFX_OK) return st;
+    }
+    // one copy of the header prefix: the solver state ... true_rel
+    MFX_CUDA_TRY(cudaMemcpyAsync(g_exit, W.hdr, offsetof(WsHeader, true_rel) + sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
     MFX_CUDA_TRY(cudaStreamSynchronize(s));
     const SolverScalars &S = g_exit->sc;
     info->iters = S.it;
@@ -950,20 +950,22 @@ mfx_status bicgstab_solve(int kind, const mfx_grid *grid, const mfx_eqsys *A, do
     const bool sym = kind == MFX_EQ_PP;
     const Coef c = coef_of(A);
     const int nb = reduce_grid(G.N);
-    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
-    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
-    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->work[0], 0, sizeof(W.hdr->work), s));
     if (!g_host.pinned) MFX_CUDA_TRY(cudaMallocHost(&g_host.pinned, sizeof(SolverScalars)));
     const int path = opt_solver_path();
     if (path == 2 || (path == 0 && cluster_fits(G, sym))) {
+        // one launch per solve: the kernel writes the whole solver record and
+        // the true residual (no memsets, no true-residual launch)
         MFX_ARG_CHECK(cluster_fits(G, sym), "system too large for the single-cluster solver");
         count_launch(0, s, true);
         mfx_status st = cluster_solve(sym, G, A, x, tol, maxit, W.hdr, s);
         count_launch(0, s, false);
         if (st != MFX_OK) return st;
         if (!info) return MFX_OK;
-        return finish_info(sym, G, A, x, W, info, s);
+        return finish_info(sym, G, A, x, W, info, s, true);
     }
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->sc, 0, sizeof(SolverScalars), s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->ticket[0], 0, sizeof(W.hdr->ticket), s));
+    MFX_CUDA_TRY(cudaMemsetAsync(&W.hdr->work[0], 0, sizeof(W.hdr->work), s));
     const bool grid_path = path == 4 || (path == 0 && grid_solver_fits(G, sym));
     const bool persist_path = sym && use_tma(G) && (path == 5 || (path == 0 && persist_fits(G)));
     count_launch(0, s, true);

@@ -8,7 +8,9 @@
 // iteration loop uses barrier.cluster: every cross-CTA transfer is a PUSH --
 // st.async remote stores into the consumer CTA's shared memory that complete
 // a transaction count on the consumer's own mbarrier -- so a consumer waits
-// exactly for the bytes it needs, and no CTA ever reads remote memory:
+// exactly for the bytes it needs, and no CTA reads remote memory inside the
+// loop (the setup reads x0's and cz's halo planes once, after a full cluster
+// barrier):
 //   * z halos: the thread that updates a cell of a slab's first/last plane
 //     (p in the K1 update, s in the K2 update) also stores it into the
 //     neighbour's halo plane (one mbarrier per halo vector);
@@ -20,8 +22,11 @@
 // Reuse of a buffer is safe without a barrier because a CTA can only push into
 // a buffer's next use after every CTA has pushed the intervening transfer,
 // i.e. after every CTA has consumed this one (program order: consume, then
-// push the next).  mbarrier tx counts may run negative when remote bytes land
-// before the local arm (expect_tx), which the PTX semantics allow.
+// push the next).  For the same reason each mbarrier is armed (expect_tx) for
+// its next phase right after the consumer's wait, before any producer can
+// push that phase.  At exit the kernel also computes the true residual of the
+// returned iterate (x's halos pushed like p's, one more reduction) and writes
+// the whole solver record, so a solve is one launch.
 #include <cstdio>
 #include <cstdlib>
 
